@@ -1,0 +1,161 @@
+/*
+ * flexemb.h — C-ABI of the B200-native embedding-lookup path (libflexemb.so).
+ *
+ * Drop-in boundary for the hot path of the reference `embserve` package
+ * (FlexEMR, arXiv 2410.12794; paths below are relative to
+ * /root/reference/pkg/src/embserve). The reference has no FFI: its seams are
+ * Python module APIs. Each entry point below names the reference function
+ * whose semantics it replaces; the Python mirror package
+ * (paper_2410_12794_b200) binds these through ctypes.
+ *
+ * Conventions
+ *  - plain C types only; every device buffer is caller-owned device memory
+ *    (e.g. a torch CUDA tensor's data_ptr()); no allocation on the hot path
+ *    except where a `workspace` is documented;
+ *  - every call is asynchronous on the given stream (a cudaStream_t passed
+ *    as void*; NULL = legacy default stream) unless marked [sync];
+ *  - return codes map 1:1 onto embserve/errors.py:4-41 (see FX_E_*);
+ *    fx_last_error() returns a thread-local message for the last failure;
+ *  - handles are thread-compatible, not thread-safe (one host thread drives
+ *    one handle and stream), like the reference's single-writer cache
+ *    (SPEC.md:306).
+ */
+#ifndef FLEXEMB_H
+#define FLEXEMB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- return codes (errors.py:4-41) ------------------------------------ */
+#define FX_OK 0
+#define FX_E_CONFIG 1             /* ConfigError            errors.py:8   */
+#define FX_E_LOOKUP_VALIDATION 2  /* LookupValidationError  errors.py:13  */
+#define FX_E_ROUTING_VIOLATION 3  /* RoutingViolationError  errors.py:18  */
+#define FX_E_CAPACITY 4           /* CapacityError          errors.py:23  */
+#define FX_E_INVARIANT 5          /* InvariantError         errors.py:40  */
+#define FX_E_EMPTY 6              /* EmbServeError (empty pool/combine)   */
+#define FX_E_CUDA 7               /* EmbServeError (device failure)       */
+
+/* ---- enums -------------------------------------------------------------- */
+#define FX_OP_SUM 0               /* PoolingOp.SUM   pooling.py:25-27 */
+#define FX_OP_MEAN 1              /* PoolingOp.MEAN */
+
+#define FX_IDX_I32 0              /* index element type */
+#define FX_IDX_I64 1
+
+#define FX_OUT_F32 0              /* final pooled f32 (Mean divided once)        */
+#define FX_OUT_F64_PARTIAL 1      /* f64 partial sum (Mean deferred), see counts */
+
+const char *fx_last_error(void);
+int fx_version(void);
+int fx_num_sms(int device);
+
+/* ---- K0: table materialisation (store.py:62-89 table_block/_table_base) --
+ * out[r*ld + c] = f32(((mix64(base_t + (row_start+r)*dim + c) >> 11) * 2^-53)
+ *                 * 2 - 1),  base_t = mix64(table_id ^ mix64(seed)).
+ * Bit-exact with the reference PRF. */
+int fx_table_init(float *out, int64_t ld, uint64_t seed, int64_t table_id,
+                  int32_t dim, int64_t row_start, int64_t n_rows, void *stream);
+uint64_t fx_table_base(uint64_t seed, int64_t table_id); /* host helper */
+
+/* ---- bag segments ---------------------------------------------------------
+ * A batch is CSR bags (offsets[n_bags+1], indices[nnz]) grouped into
+ * segments: contiguous bag ranges that read one shard of one table with one
+ * pooling op. Row r of the shard lives at table + (r - row_begin)*ld. */
+typedef struct fx_segment {
+  const float *table;   /* device shard base                                  */
+  int64_t row_begin;    /* first hosted row (global row id)                   */
+  int64_t row_end;      /* one past the last hosted row                       */
+  int64_t bag_begin;    /* first bag of this segment                          */
+  int64_t bag_end;      /* one past the last bag                              */
+  void *out;            /* output base (float* or double*, see out mode)      */
+  int64_t out_stride;   /* elements between consecutive bags' outputs         */
+  int64_t ld;           /* elements between consecutive shard rows (>= dim)   */
+  int32_t dim;          /* embedding dimension                                */
+  int32_t op;           /* FX_OP_*                                            */
+} fx_segment;
+
+/* ---- K4: fused gather + pool (store.py:184-193 partial_pool,
+ *      pooling.py:60-85 sum_rows_f64/pool_flat, ranker.py:458-465) --------
+ * For every bag: f64 accumulation of its rows in index order (each lane owns
+ * columns, so the per-element summation order is exactly the reference's
+ * sequential order), then
+ *   FX_OUT_F32:         emit f32 (Mean divides the f64 sum by the bag length
+ *                       once, pooling.py:82-84); empty bag -> zeros;
+ *   FX_OUT_F64_PARTIAL: emit the f64 sum; counts[bag] = bag length
+ *                       (PartialResult(sum, count), pooling.py:35-47).
+ * Indices outside [row_begin,row_end) are never dereferenced: the first bad
+ * occurrence's CSR position is atomically min-recorded in err[0] (init it to
+ * INT64_MAX) and err_code (if non-NULL) is set to `bad_code`
+ * (FX_E_LOOKUP_VALIDATION at ingress, FX_E_ROUTING_VIOLATION on a shard).
+ * `segs` is a DEVICE array; all segments must share one dim (host groups by
+ * dim). `counts` may be NULL. */
+int fx_gather_pool(const fx_segment *segs, int32_t n_segs, int32_t dim,
+                   const void *indices, int32_t idx_type, const int64_t *offsets,
+                   int64_t n_bags, int32_t out_mode, int32_t *counts,
+                   int64_t *err, int32_t bad_code, int32_t *err_code, void *stream);
+
+/* ---- raw row gather (store.py:151-182 lookup_rows) ---------------------
+ * out[i*dim + c] = shard[indices[i] - row_begin][c], input order,
+ * duplicates per occurrence; unhosted index -> err/err_code as above. */
+int fx_gather_rows(const float *table, int64_t ld, int64_t row_begin, int64_t row_end,
+                   int32_t dim, const void *indices, int32_t idx_type, int64_t n,
+                   float *out, int64_t *err, int32_t *err_code, void *stream);
+
+/* ---- K5: combine (pooling.py:103-123 combine_partials) ------------------
+ * out[b] = f32( sum_{s=0..n_src-1} partials[s][b] (f64, ascending s)
+ *               + sum_{k} raw rows of bag b in position order (f64) )
+ * Mean divides by (sum_s counts[s][b] + raw count) once.
+ * partials: device array of n_src pointers to [n_bags, dim] f64 (row stride
+ * p_stride); counts: n_src pointers to int32[n_bags] (NULL -> partial absent
+ * for every bag). raw_offsets/raw_rows: optional CSR of f32 raw vectors
+ * (raw_rows row stride = dim), may be NULL. ops: int32[n_bags] or NULL (all
+ * `op`). out row stride = out_stride. Bags with nothing to combine get
+ * zeros and set *err_code = FX_E_EMPTY if err_code != NULL. */
+int fx_combine(const double *const *partials, const int32_t *const *counts, int32_t n_src,
+               int64_t p_stride, const int64_t *raw_offsets, const float *raw_rows,
+               int64_t n_bags, int32_t dim, int32_t op, const int32_t *ops,
+               float *out, int64_t out_stride, int32_t *err_code, void *stream);
+
+/* ---- K1: range routing (routing.py:87-97 resolve_many, 117-148) ---------
+ * For occurrence i of a bag of table t:
+ *   shard = upper_bound(starts[route_off[t]..route_off[t+1]), idx) - 1
+ *   dest[i] = servers[route_off[t] + shard]
+ * bag_table[n_bags] gives the table per bag; num_rows[t] bounds validation
+ * (bad -> err/err_code FX_E_LOOKUP_VALIDATION). dest may be NULL (validate only). */
+int fx_route(const int64_t *route_off, const int64_t *starts, const int32_t *servers,
+             const int64_t *num_rows, const int32_t *bag_table, const void *indices,
+             int32_t idx_type, const int64_t *offsets, int64_t n_bags, int32_t *dest,
+             int64_t *err, int32_t *err_code, void *stream);
+
+/* Stable per-destination bucketing (routing.py:117-148 group_by_server,
+ * GroupItem.positions): given dest[nnz] in CSR (bag, position) order, produce
+ *   perm[nnz]        CSR positions ordered by (dest, bag, position)
+ *   dest_count[n_dest]  occurrences per destination
+ *   bag_count[n_dest*n_bags] occurrences of bag b routed to dest d.
+ * Requires n_dest <= 256. workspace: query with ws == NULL (*ws_bytes set). */
+int fx_bucket(const int32_t *dest, int64_t nnz, const int64_t *offsets, int64_t n_bags,
+              int32_t n_dest, int64_t *perm, int64_t *dest_count, int32_t *bag_count,
+              void *ws, size_t *ws_bytes, void *stream);
+
+/* ---- K2: per-batch dedup (no reference counterpart) ---
+ * keys[i] = bag_table[bag(i)] << 40 | row(i) for every occurrence in CSR
+ * order; ordinal[i] = the occurrence's (lookup, feature, position) ordinal
+ * (sm_start[bag] + position). Produces, deterministically, the unique keys
+ * in FIRST-OCCURRENCE (ordinal) order:
+ *   uniq[n_uniq], mult[n_uniq] (multiplicity), first_ord / last_ord[n_uniq],
+ *   inverse[nnz] (unique id per occurrence), *n_uniq_dev (device int64).
+ * Sorting uniq reproduces np.unique exactly. workspace: query with ws==NULL. */
+int fx_dedup(const int32_t *bag_table, const void *indices, int32_t idx_type,
+             const int64_t *offsets, const int64_t *sm_start, int64_t n_bags, int64_t nnz,
+             uint64_t *uniq, int32_t *mult, int64_t *first_ord, int64_t *last_ord,
+             int32_t *inverse, int64_t *n_uniq_dev, void *ws, size_t *ws_bytes, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FLEXEMB_H */

@@ -1,0 +1,150 @@
+"""ctypes binding of libflexemb.so (include/flexemb.h).
+
+The library is the only compute path: if it is missing this module raises at
+import time (no CPU fallback). Device buffers are torch CUDA tensors passed
+by data_ptr(); every call runs on torch's current CUDA stream.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+from . import errors
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libflexemb.so")
+
+FX_OK = 0
+FX_E_CONFIG = 1
+FX_E_LOOKUP_VALIDATION = 2
+FX_E_ROUTING_VIOLATION = 3
+FX_E_CAPACITY = 4
+FX_E_INVARIANT = 5
+FX_E_EMPTY = 6
+FX_E_CUDA = 7
+
+FX_OP_SUM = 0
+FX_OP_MEAN = 1
+FX_IDX_I32 = 0
+FX_IDX_I64 = 1
+FX_OUT_F32 = 0
+FX_OUT_F64_PARTIAL = 1
+
+INT64_MAX = (1 << 63) - 1
+
+_CODE_TO_EXC = {
+    FX_E_CONFIG: errors.ConfigError,
+    FX_E_LOOKUP_VALIDATION: errors.LookupValidationError,
+    FX_E_ROUTING_VIOLATION: errors.RoutingViolationError,
+    FX_E_CAPACITY: errors.CapacityError,
+    FX_E_INVARIANT: errors.InvariantError,
+    FX_E_EMPTY: errors.EmbServeError,
+    FX_E_CUDA: errors.EmbServeError,
+}
+
+
+class FxSegment(ctypes.Structure):
+    """Mirror of `fx_segment` (include/flexemb.h)."""
+    _fields_ = [
+        ("table", ctypes.c_void_p),
+        ("row_begin", ctypes.c_int64),
+        ("row_end", ctypes.c_int64),
+        ("bag_begin", ctypes.c_int64),
+        ("bag_end", ctypes.c_int64),
+        ("out", ctypes.c_void_p),
+        ("out_stride", ctypes.c_int64),
+        ("ld", ctypes.c_int64),
+        ("dim", ctypes.c_int32),
+        ("op", ctypes.c_int32),
+    ]
+
+
+SEGMENT_BYTES = ctypes.sizeof(FxSegment)
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build it with `python -m paper_2410_12794_b200.build` "
+        "(there is no CPU fallback for the lookup path)")
+
+lib = ctypes.CDLL(LIB_PATH)
+
+_P = ctypes.c_void_p
+_I32 = ctypes.c_int32
+_I64 = ctypes.c_int64
+_U64 = ctypes.c_uint64
+_SZP = ctypes.POINTER(ctypes.c_size_t)
+
+_SIGS = {
+    "fx_last_error": ([], ctypes.c_char_p),
+    "fx_version": ([], ctypes.c_int),
+    "fx_num_sms": ([ctypes.c_int], ctypes.c_int),
+    "fx_table_base": ([_U64, _I64], _U64),
+    "fx_table_init": ([_P, _I64, _U64, _I64, _I32, _I64, _I64, _P], ctypes.c_int),
+    "fx_gather_pool": ([_P, _I32, _I32, _P, _I32, _P, _I64, _I32, _P, _P, _I32, _P, _P], ctypes.c_int),
+    "fx_gather_rows": ([_P, _I64, _I64, _I64, _I32, _P, _I32, _I64, _P, _P, _P, _P], ctypes.c_int),
+    "fx_combine": ([_P, _P, _I32, _I64, _P, _P, _I64, _I32, _I32, _P, _P, _I64, _P, _P], ctypes.c_int),
+    "fx_route": ([_P, _P, _P, _P, _P, _P, _I32, _P, _I64, _P, _P, _P, _P], ctypes.c_int),
+    "fx_bucket": ([_P, _I64, _P, _I64, _I32, _P, _P, _P, _P, _SZP, _P], ctypes.c_int),
+    "fx_dedup": ([_P, _P, _I32, _P, _P, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _SZP, _P], ctypes.c_int),
+}
+
+EXPORTED = []
+for _name, (_args, _res) in _SIGS.items():
+    _fn = getattr(lib, _name, None)
+    if _fn is None:
+        continue
+    _fn.argtypes = _args
+    _fn.restype = _res
+    EXPORTED.append(_name)
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc != FX_OK:
+        msg = lib.fx_last_error().decode(errors="replace")
+        raise _CODE_TO_EXC.get(rc, errors.EmbServeError)(f"{what}: {msg}" if what else msg)
+
+
+def stream_ptr(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def ptr(t) -> int | None:
+    if t is None:
+        return None
+    return int(t.data_ptr())
+
+
+def idx_type_of(t: torch.Tensor) -> int:
+    if t.dtype == torch.int32:
+        return FX_IDX_I32
+    if t.dtype == torch.int64:
+        return FX_IDX_I64
+    raise errors.ConfigError(f"indices must be int32 or int64, got {t.dtype}")
+
+
+def require_cuda(t: torch.Tensor, name: str) -> None:
+    if not t.is_cuda:
+        raise errors.ConfigError(f"{name} must be a CUDA tensor")
+
+
+class Status:
+    """Device-side first-error word: err[0] = min bad CSR position (INT64_MAX
+    when clean), code[0] = FX_E_* of the last violation (0 when clean)."""
+
+    def __init__(self, device):
+        self.err = torch.full((1,), INT64_MAX, dtype=torch.int64, device=device)
+        self.code = torch.zeros((1,), dtype=torch.int32, device=device)
+
+    def reset(self):
+        self.err.fill_(INT64_MAX)
+        self.code.zero_()
+
+    def read(self):
+        """[sync] -> (code, position)."""
+        code = int(self.code.item())
+        pos = int(self.err.item())
+        return code, pos

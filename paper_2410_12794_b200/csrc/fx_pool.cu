@@ -1,0 +1,380 @@
+// K0 table materialisation, K4 fused gather+pool, raw gather, K5 combine.
+//
+// Reference semantics (paths under /root/reference/pkg/src/embserve):
+//   table_block / _table_base / _mix64      store.py:62-89
+//   ServerStore.lookup_rows                 store.py:151-182
+//   ServerStore.partial_pool, sum_rows_f64  store.py:184-193, pooling.py:60-71
+//   pool_flat                               pooling.py:74-85
+//   combine_partials                        pooling.py:103-123
+#include <climits>
+
+#include "fx_common.cuh"
+
+namespace fx {
+
+// ----------------------------------------------------------------- K0
+// One warp per row, lanes stride the columns: coalesced stores, integer
+// SplitMix64 + exact f64 scaling + one RN rounding to f32 (bit-exact).
+__global__ void __launch_bounds__(256) k_table_init(float *__restrict__ out, int64_t ld, uint64_t base,
+                                                    int32_t dim, int64_t row_start, int64_t n_rows) {
+  const int lane = threadIdx.x & 31;
+  int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (gridDim.x * (int64_t)blockDim.x) >> 5;
+  for (int64_t r = w; r < n_rows; r += nw) {
+    const uint64_t ctr0 = static_cast<uint64_t>(row_start + r) * static_cast<uint64_t>(dim) + base;
+    float *dst = out + r * ld;
+    for (int c = lane; c < dim; c += 32) {
+      const uint64_t bits = mix64(ctr0 + static_cast<uint64_t>(c));
+      const double unit = static_cast<double>(bits >> 11) * 0x1p-53;
+      dst[c] = __double2float_rn(unit * 2.0 - 1.0);  // both ops exact; one rounding
+    }
+  }
+}
+
+// ----------------------------------------------------------------- K4
+// Vectorised path: rows are 16-B aligned (dim % 4 == 0, ld % 4 == 0).
+// A group of G lanes owns one bag; lane gl owns columns (k*G + gl)*4 .. +3 for
+// k < NCH, so every output element is accumulated over the bag's rows in
+// index order (the reference's sequential order) in f64. Indices are staged
+// G at a time (one coalesced load), broadcast by shuffle, and U row loads
+// are issued before any accumulation to keep U*16 B per lane in flight.
+template <int G, int NCH, int U, typename IdxT, int MODE>
+__global__ void __launch_bounds__(256) k_gather_pool_v4(
+    const fx_segment *__restrict__ segs, int n_segs, int dim, const IdxT *__restrict__ indices,
+    const int64_t *__restrict__ offsets, int64_t n_bags, int32_t *__restrict__ counts,
+    int64_t *err, int32_t bad_code, int32_t *err_code) {
+  constexpr int GPW = 32 / G;
+  const int lane = threadIdx.x & 31;
+  const int gl = lane % G;
+  const int gw = lane / G;
+  const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (gw * G));
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (gridDim.x * (int64_t)blockDim.x) >> 5;
+
+  for (int64_t bag = warp * GPW + gw; bag < n_bags; bag += nwarps * GPW) {
+    const int s = find_segment(segs, n_segs, bag);
+    const float *__restrict__ tab = segs[s].table;
+    const int64_t rb = segs[s].row_begin, re = segs[s].row_end, ld = segs[s].ld;
+    const int64_t beg = __ldg(&offsets[bag]), end = __ldg(&offsets[bag + 1]);
+
+    double acc[NCH][4];
+#pragma unroll
+    for (int k = 0; k < NCH; ++k) acc[k][0] = acc[k][1] = acc[k][2] = acc[k][3] = 0.0;
+
+    for (int64_t c0 = beg; c0 < end; c0 += G) {
+      const int n = static_cast<int>((end - c0 < G ? end - c0 : (int64_t)G));
+      int64_t my_off = 0;
+      if (gl < n) {
+        const int64_t idx = load_index(indices + c0 + gl);
+        if (idx < rb || idx >= re) {
+          record_bad(err, err_code, c0 + gl, bad_code);
+        } else {
+          my_off = (idx - rb) * ld;
+        }
+      }
+      for (int r = 0; r < n; r += U) {
+        float4 v[U][NCH];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t off = __shfl_sync(gmask, my_off, (r + u) & (G - 1), G);
+          if (r + u < n) {
+#pragma unroll
+            for (int k = 0; k < NCH; ++k) {
+              const int col = (k * G + gl) * 4;
+              if (NCH == 1 || col < dim) v[u][k] = ldg_f4(tab + off + col);
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (r + u < n) {
+#pragma unroll
+            for (int k = 0; k < NCH; ++k) {
+              acc[k][0] += static_cast<double>(v[u][k].x);
+              acc[k][1] += static_cast<double>(v[u][k].y);
+              acc[k][2] += static_cast<double>(v[u][k].z);
+              acc[k][3] += static_cast<double>(v[u][k].w);
+            }
+          }
+        }
+      }
+    }
+
+    const int64_t cnt = end - beg;
+    const int64_t orow = bag - segs[s].bag_begin;
+    if (MODE == FX_OUT_F32) {
+      float *o = static_cast<float *>(segs[s].out) + orow * segs[s].out_stride;
+      const bool mean = segs[s].op == FX_OP_MEAN && cnt > 0;
+      const double dn = static_cast<double>(cnt);
+#pragma unroll
+      for (int k = 0; k < NCH; ++k) {
+        const int col = (k * G + gl) * 4;
+        if (NCH == 1 || col < dim) {
+          float4 q;
+          if (mean) {
+            q = make_float4(__double2float_rn(acc[k][0] / dn), __double2float_rn(acc[k][1] / dn),
+                            __double2float_rn(acc[k][2] / dn), __double2float_rn(acc[k][3] / dn));
+          } else {
+            q = make_float4(__double2float_rn(acc[k][0]), __double2float_rn(acc[k][1]),
+                            __double2float_rn(acc[k][2]), __double2float_rn(acc[k][3]));
+          }
+          *reinterpret_cast<float4 *>(o + col) = q;
+        }
+      }
+    } else {
+      double *o = static_cast<double *>(segs[s].out) + orow * segs[s].out_stride;
+#pragma unroll
+      for (int k = 0; k < NCH; ++k) {
+        const int col = (k * G + gl) * 4;
+        if (NCH == 1 || col < dim) {
+          *reinterpret_cast<double2 *>(o + col) = make_double2(acc[k][0], acc[k][1]);
+          *reinterpret_cast<double2 *>(o + col + 2) = make_double2(acc[k][2], acc[k][3]);
+        }
+      }
+      if (counts && gl == 0) counts[bag] = static_cast<int32_t>(cnt);
+    }
+  }
+}
+
+// Generic path (any dim / alignment): one warp per (bag, 128-column tile),
+// scalar coalesced loads, same per-element sequential f64 order.
+template <typename IdxT, int MODE>
+__global__ void __launch_bounds__(256) k_gather_pool_generic(
+    const fx_segment *__restrict__ segs, int n_segs, int dim, const IdxT *__restrict__ indices,
+    const int64_t *__restrict__ offsets, int64_t n_bags, int32_t *__restrict__ counts,
+    int64_t *err, int32_t bad_code, int32_t *err_code) {
+  constexpr int TILE = 128, U = 4;
+  const int lane = threadIdx.x & 31;
+  const int tiles = (dim + TILE - 1) / TILE;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (gridDim.x * (int64_t)blockDim.x) >> 5;
+  for (int64_t work = warp; work < n_bags * tiles; work += nwarps) {
+    const int64_t bag = work / tiles;
+    const int tile = static_cast<int>(work % tiles);
+    const int s = find_segment(segs, n_segs, bag);
+    const float *__restrict__ tab = segs[s].table;
+    const int64_t rb = segs[s].row_begin, re = segs[s].row_end, ld = segs[s].ld;
+    const int64_t beg = __ldg(&offsets[bag]), end = __ldg(&offsets[bag + 1]);
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int64_t c0 = beg; c0 < end; c0 += 32) {
+      const int n = static_cast<int>((end - c0 < 32 ? end - c0 : (int64_t)32));
+      int64_t my_off = 0;
+      if (lane < n) {
+        const int64_t idx = load_index(indices + c0 + lane);
+        if (idx < rb || idx >= re) {
+          if (tile == 0) record_bad(err, err_code, c0 + lane, bad_code);
+        } else {
+          my_off = (idx - rb) * ld;
+        }
+      }
+      for (int r = 0; r < n; r += U) {
+        float v[U][4];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t off = __shfl_sync(0xffffffffu, my_off, (r + u) & 31);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int col = tile * TILE + k * 32 + lane;
+            v[u][k] = (r + u < n && col < dim) ? __ldg(tab + off + col) : 0.0f;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (r + u < n) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) acc[k] += static_cast<double>(v[u][k]);
+          }
+      }
+    }
+    const int64_t cnt = end - beg;
+    const int64_t orow = bag - segs[s].bag_begin;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int col = tile * TILE + k * 32 + lane;
+      if (col >= dim) continue;
+      if (MODE == FX_OUT_F32) {
+        float *o = static_cast<float *>(segs[s].out) + orow * segs[s].out_stride;
+        const double v = (segs[s].op == FX_OP_MEAN && cnt > 0) ? acc[k] / static_cast<double>(cnt) : acc[k];
+        o[col] = __double2float_rn(v);
+      } else {
+        double *o = static_cast<double *>(segs[s].out) + orow * segs[s].out_stride;
+        o[col] = acc[k];
+      }
+    }
+    if (MODE == FX_OUT_F64_PARTIAL && counts && tile == 0 && lane == 0) counts[bag] = static_cast<int32_t>(cnt);
+  }
+}
+
+template <typename IdxT>
+__global__ void __launch_bounds__(256) k_gather_rows(const float *__restrict__ tab, int64_t ld, int64_t rb,
+                                                     int64_t re, int dim, const IdxT *__restrict__ indices,
+                                                     int64_t n, float *__restrict__ out, int64_t *err,
+                                                     int32_t *err_code) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (gridDim.x * (int64_t)blockDim.x) >> 5;
+  for (int64_t i = warp; i < n; i += nwarps) {
+    const int64_t idx = load_index(indices + i);
+    if (idx < rb || idx >= re) {
+      if (lane == 0) record_bad(err, err_code, i, FX_E_ROUTING_VIOLATION);
+      continue;
+    }
+    const float *src = tab + (idx - rb) * ld;
+    for (int c = lane; c < dim; c += 32) out[i * dim + c] = __ldg(src + c);
+  }
+}
+
+// ----------------------------------------------------------------- K5
+// One warp per bag, lanes over columns (stride 32): fold partial sums in
+// ascending source order, then raw rows in position order, in f64; round once.
+__global__ void __launch_bounds__(256) k_combine(const double *const *__restrict__ partials,
+                                                 const int32_t *const *__restrict__ counts, int n_src,
+                                                 int64_t p_stride, const int64_t *__restrict__ raw_offsets,
+                                                 const float *__restrict__ raw_rows, int64_t n_bags, int dim,
+                                                 int op, const int32_t *__restrict__ ops, float *__restrict__ out,
+                                                 int64_t out_stride, int32_t *err_code) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (gridDim.x * (int64_t)blockDim.x) >> 5;
+  for (int64_t b = warp; b < n_bags; b += nwarps) {
+    int64_t total = 0;
+    int present = 0;
+    for (int s = 0; s < n_src; ++s) {
+      const int32_t c = counts && counts[s] ? counts[s][b] : 1;
+      if (c > 0) { total += c; ++present; }
+    }
+    int64_t r0 = 0, r1 = 0;
+    if (raw_offsets) { r0 = raw_offsets[b]; r1 = raw_offsets[b + 1]; }
+    total += r1 - r0;
+    if (present == 0 && r1 == r0 && err_code && lane == 0) atomicExch(err_code, FX_E_EMPTY);
+    const int bop = ops ? ops[b] : op;
+    for (int c = lane; c < dim; c += 32) {
+      double acc = 0.0;
+      for (int s = 0; s < n_src; ++s) {
+        const int32_t cs = counts && counts[s] ? counts[s][b] : 1;
+        if (cs > 0) acc += partials[s][b * p_stride + c];
+      }
+      for (int64_t r = r0; r < r1; ++r) acc += static_cast<double>(raw_rows[r * dim + c]);
+      if (bop == FX_OP_MEAN && total > 0) acc /= static_cast<double>(total);
+      out[b * out_stride + c] = __double2float_rn(acc);
+    }
+  }
+}
+
+}  // namespace fx
+
+using namespace fx;
+
+template <typename IdxT, int MODE>
+static int launch_pool(const fx_segment *segs, int n_segs, int dim, const void *indices, const int64_t *offsets,
+                       int64_t n_bags, int32_t *counts, int64_t *err, int32_t bad_code, int32_t *err_code,
+                       cudaStream_t st, bool vec4) {
+  const IdxT *ix = static_cast<const IdxT *>(indices);
+  if (vec4 && dim == 128) {
+    k_gather_pool_v4<32, 1, 8, IdxT, MODE><<<grid_for(n_bags * 32, 256), 256, 0, st>>>(
+        segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code);
+  } else if (vec4 && dim == 64) {
+    k_gather_pool_v4<16, 1, 8, IdxT, MODE><<<grid_for(n_bags * 16, 256), 256, 0, st>>>(
+        segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code);
+  } else if (vec4 && dim == 32) {
+    k_gather_pool_v4<8, 1, 8, IdxT, MODE><<<grid_for(n_bags * 8, 256), 256, 0, st>>>(
+        segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code);
+  } else if (vec4 && dim <= 256) {
+    k_gather_pool_v4<32, 2, 4, IdxT, MODE><<<grid_for(n_bags * 32, 256), 256, 0, st>>>(
+        segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code);
+  } else if (vec4 && dim <= 512) {
+    k_gather_pool_v4<32, 4, 2, IdxT, MODE><<<grid_for(n_bags * 32, 256), 256, 0, st>>>(
+        segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code);
+  } else {
+    const int tiles = (dim + 127) / 128;
+    k_gather_pool_generic<IdxT, MODE><<<grid_for(n_bags * tiles * 32, 256), 256, 0, st>>>(
+        segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code);
+  }
+  FX_LAUNCH_CHECK("fx_gather_pool");
+  return FX_OK;
+}
+
+
+extern "C" {
+
+uint64_t fx_table_base(uint64_t seed, int64_t table_id) {
+  return mix64(static_cast<uint64_t>(table_id) ^ mix64(seed));
+}
+
+int fx_table_init(float *out, int64_t ld, uint64_t seed, int64_t table_id, int32_t dim, int64_t row_start,
+                  int64_t n_rows, void *stream) {
+  if (dim < 1 || n_rows < 0 || ld < dim) {
+    set_error("fx_table_init: bad shape");
+    return FX_E_CONFIG;
+  }
+  if (n_rows == 0) return FX_OK;
+  const uint64_t base = fx_table_base(seed, table_id);
+  k_table_init<<<grid_for(n_rows * 32, 256, 16), 256, 0, as_stream(stream)>>>(out, ld, base, dim, row_start,
+                                                                               n_rows);
+  FX_LAUNCH_CHECK("fx_table_init");
+  return FX_OK;
+}
+
+int fx_gather_pool(const fx_segment *segs, int32_t n_segs, int32_t dim, const void *indices, int32_t idx_type,
+                   const int64_t *offsets, int64_t n_bags, int32_t out_mode, int32_t *counts, int64_t *err,
+                   int32_t bad_code, int32_t *err_code, void *stream) {
+  if (n_segs < 1 || dim < 1 || (idx_type != FX_IDX_I32 && idx_type != FX_IDX_I64) ||
+      (out_mode != FX_OUT_F32 && out_mode != FX_OUT_F64_PARTIAL)) {
+    set_error("fx_gather_pool: bad arguments");
+    return FX_E_CONFIG;
+  }
+  if (n_bags == 0) return FX_OK;
+  // The caller guarantees 16-B aligned rows/outputs when it requests the
+  // vector path through dim % 4 == 0 (ld and out_stride are multiples of 4 and
+  // base pointers 16-B aligned, checked host-side by the Python binding).
+  const bool vec4 = (dim % 4) == 0;
+  cudaStream_t st = as_stream(stream);
+  if (idx_type == FX_IDX_I32) {
+    return out_mode == FX_OUT_F32
+               ? launch_pool<int32_t, FX_OUT_F32>(segs, n_segs, dim, indices, offsets, n_bags, counts, err, bad_code,
+                                                  err_code, st, vec4)
+               : launch_pool<int32_t, FX_OUT_F64_PARTIAL>(segs, n_segs, dim, indices, offsets, n_bags, counts, err,
+                                                          bad_code, err_code, st, vec4);
+  }
+  return out_mode == FX_OUT_F32
+             ? launch_pool<int64_t, FX_OUT_F32>(segs, n_segs, dim, indices, offsets, n_bags, counts, err, bad_code,
+                                                err_code, st, vec4)
+             : launch_pool<int64_t, FX_OUT_F64_PARTIAL>(segs, n_segs, dim, indices, offsets, n_bags, counts, err,
+                                                        bad_code, err_code, st, vec4);
+}
+
+int fx_gather_rows(const float *table, int64_t ld, int64_t row_begin, int64_t row_end, int32_t dim,
+                   const void *indices, int32_t idx_type, int64_t n, float *out, int64_t *err, int32_t *err_code,
+                   void *stream) {
+  if (dim < 1 || n < 0) {
+    set_error("fx_gather_rows: bad arguments");
+    return FX_E_CONFIG;
+  }
+  if (n == 0) return FX_OK;
+  cudaStream_t st = as_stream(stream);
+  const int grid = grid_for(n * 32, 256);
+  if (idx_type == FX_IDX_I32)
+    k_gather_rows<int32_t><<<grid, 256, 0, st>>>(table, ld, row_begin, row_end, dim,
+                                                 static_cast<const int32_t *>(indices), n, out, err, err_code);
+  else
+    k_gather_rows<int64_t><<<grid, 256, 0, st>>>(table, ld, row_begin, row_end, dim,
+                                                 static_cast<const int64_t *>(indices), n, out, err, err_code);
+  FX_LAUNCH_CHECK("fx_gather_rows");
+  return FX_OK;
+}
+
+int fx_combine(const double *const *partials, const int32_t *const *counts, int32_t n_src, int64_t p_stride,
+               const int64_t *raw_offsets, const float *raw_rows, int64_t n_bags, int32_t dim, int32_t op,
+               const int32_t *ops, float *out, int64_t out_stride, int32_t *err_code, void *stream) {
+  if (dim < 1 || n_src < 0 || n_bags < 0) {
+    set_error("fx_combine: bad arguments");
+    return FX_E_CONFIG;
+  }
+  if (n_bags == 0) return FX_OK;
+  k_combine<<<grid_for(n_bags * 32, 256), 256, 0, as_stream(stream)>>>(
+      partials, counts, n_src, p_stride, raw_offsets, raw_rows, n_bags, dim, op, ops, out, out_stride, err_code);
+  FX_LAUNCH_CHECK("fx_combine");
+  return FX_OK;
+}
+
+}  // extern "C"

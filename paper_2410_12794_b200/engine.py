@@ -1,0 +1,209 @@
+"""Batched single-GPU lookup engine: the hot path behind Ranker.execute_batch.
+
+A batch is KJT-like CSR: `indices` [nnz] (int32/int64) and `offsets`
+[n_bags+1] (int64) with bags TABLE-MAJOR (bag = f*B + s for feature slot f
+and sample s), so each feature is one contiguous bag segment reading one
+HBM-resident table. One fx_gather_pool (K4) launch pools every bag of the
+batch, validates every index at ingress (bad index -> LookupValidationError,
+ranker.py:184-193) and writes the pooled f32 vectors sample-major into
+out[B, F*D] (out[s, f*D:(f+1)*D] = bag (s, f)).
+"""
+
+from __future__ import annotations
+
+from collections import OrderedDict
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import ConfigError, LookupValidationError
+from .pooling import op_code
+from .store import make_segments
+
+
+@dataclass
+class CsrBatch:
+    """Device (or pinned host) CSR batch, table-major bags."""
+
+    indices: torch.Tensor
+    offsets: torch.Tensor
+    feature_tables: tuple
+    feature_ops: tuple
+    batch_size: int
+
+    @property
+    def n_features(self) -> int:
+        return len(self.feature_tables)
+
+    @property
+    def n_bags(self) -> int:
+        return self.offsets.numel() - 1
+
+    def to(self, device, non_blocking=True) -> "CsrBatch":
+        return CsrBatch(self.indices.to(device, non_blocking=non_blocking),
+                        self.offsets.to(device, non_blocking=non_blocking),
+                        self.feature_tables, self.feature_ops, self.batch_size)
+
+    def pin_memory(self) -> "CsrBatch":
+        return CsrBatch(self.indices.pin_memory(), self.offsets.pin_memory(), self.feature_tables,
+                        self.feature_ops, self.batch_size)
+
+
+class LookupEngine:
+    """Pools CSR batches against the deployment's shards resident on one GPU.
+
+    Every table must be a single shard hosted on this device (table-wise or
+    single-GPU placement); multi-shard tables go through ShardedLookup."""
+
+    def __init__(self, deployment, device=None):
+        self.dep = deployment
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.tables: dict = {}
+        for sid, server in deployment.servers.items():
+            for t in server.hosted_tables():
+                shards = server.shards(t)
+                for sh in shards:
+                    if sh.data is None:
+                        continue
+                    if sh.data.device != self.device:
+                        continue
+                    if sh.start != 0 or sh.end != deployment.meta(t).num_rows:
+                        continue
+                    self.tables[t] = sh.data
+        self.status = _lib.Status(self.device)
+        self._segs: OrderedDict = OrderedDict()
+
+    def dim_of(self, t: int) -> int:
+        return self.dep.meta(t).dim
+
+    def _segments(self, batch: CsrBatch, out: torch.Tensor) -> torch.Tensor:
+        key = (batch.feature_tables, batch.feature_ops, batch.batch_size, out.data_ptr(), out.stride(0))
+        seg = self._segs.get(key)
+        if seg is not None:
+            self._segs.move_to_end(key)
+            return seg
+        B = batch.batch_size
+        segs = []
+        col = 0
+        for f, (t, op) in enumerate(zip(batch.feature_tables, batch.feature_ops)):
+            if t not in self.tables:
+                raise ConfigError(f"table {t} is not resident as one shard on {self.device}")
+            tab = self.tables[t]
+            D = tab.shape[1]
+            segs.append(_lib.FxSegment(tab.data_ptr(), 0, tab.shape[0], f * B, (f + 1) * B,
+                                       out.data_ptr() + col * 4, out.stride(0), tab.stride(0), D, op_code(op)))
+            col += D
+        seg = make_segments(segs, self.device)
+        self._segs[key] = seg
+        if len(self._segs) > 16:
+            self._segs.popitem(last=False)
+        return seg
+
+    def out_dim(self, batch: CsrBatch) -> int:
+        return sum(self.dim_of(t) for t in batch.feature_tables)
+
+    def pool(self, batch: CsrBatch, out: torch.Tensor | None = None, check: bool = True,
+             stream=None) -> torch.Tensor:
+        """Launch K4 for the whole batch; returns out [B, sum(D_f)] f32."""
+        B = batch.batch_size
+        if batch.n_bags != B * batch.n_features:
+            raise ConfigError("offsets must describe batch_size * n_features table-major bags")
+        if out is None:
+            out = torch.empty((B, self.out_dim(batch)), dtype=torch.float32, device=self.device)
+        dims = {self.dim_of(t) for t in batch.feature_tables}
+        if len(dims) != 1:
+            return self._pool_mixed(batch, out, check, stream)
+        D = dims.pop()
+        segs = self._segments(batch, out)
+        _lib.check(_lib.lib.fx_gather_pool(segs.data_ptr(), batch.n_features, D, batch.indices.data_ptr(),
+                                           _lib.idx_type_of(batch.indices), batch.offsets.data_ptr(), batch.n_bags,
+                                           _lib.FX_OUT_F32, None, self.status.err.data_ptr(),
+                                           _lib.FX_E_LOOKUP_VALIDATION, self.status.code.data_ptr(),
+                                           _lib.stream_ptr(stream)), "gather_pool")
+        if check:
+            self.raise_if_bad(batch)
+        return out
+
+    def _pool_mixed(self, batch, out, check, stream):
+        # one launch per distinct dim; segments of other dims are skipped by
+        # giving the kernel only the bags of the matching features
+        segs_all = []
+        B = batch.batch_size
+        col = 0
+        for f, t in enumerate(batch.feature_tables):
+            D = self.dim_of(t)
+            segs_all.append((f, t, D, col))
+            col += D
+        for D in sorted({s[2] for s in segs_all}):
+            for f, t, d, c in segs_all:
+                if d != D:
+                    continue
+                tab = self.tables[t]
+                seg = make_segments([_lib.FxSegment(tab.data_ptr(), 0, tab.shape[0], 0, B, out.data_ptr() + c * 4,
+                                                    out.stride(0), tab.stride(0), D,
+                                                    op_code(batch.feature_ops[f]))], self.device)
+                offs = batch.offsets[f * B:(f + 1) * B + 1]
+                _lib.check(_lib.lib.fx_gather_pool(seg.data_ptr(), 1, D, batch.indices.data_ptr(),
+                                                   _lib.idx_type_of(batch.indices), offs.data_ptr(), B,
+                                                   _lib.FX_OUT_F32, None, self.status.err.data_ptr(),
+                                                   _lib.FX_E_LOOKUP_VALIDATION, self.status.code.data_ptr(),
+                                                   _lib.stream_ptr(stream)), "gather_pool")
+        if check:
+            self.raise_if_bad(batch)
+        return out
+
+    def raise_if_bad(self, batch: CsrBatch, batch_id: int = 0) -> None:
+        """[sync] Raise LookupValidationError for the first bad index in
+        (lookup, feature, position) order, with the reference's message
+        (ranker.py:184-193)."""
+        code, pos = self.status.read()
+        if not code:
+            return
+        self.status.reset()
+        offs = batch.offsets.cpu().numpy()
+        idx = batch.indices.cpu().numpy()
+        B = batch.batch_size
+        best = None
+        for f, t in enumerate(batch.feature_tables):
+            n = self.dep.meta(t).num_rows
+            for s in range(B):
+                b = f * B + s
+                seg = idx[offs[b]:offs[b + 1]]
+                bad = np.nonzero((seg < 0) | (seg >= n))[0]
+                if bad.size:
+                    cand = (s, f, int(seg[bad[0]]), t, n)
+                    if best is None or cand[:2] < best[:2]:
+                        best = cand
+        s, f, index, t, n = best
+        raise LookupValidationError(f"batch {batch_id}, lookup {s}: index {index} out of range [0,{n}) for table {t}")
+
+
+def algorithmic_bytes(batch_nnz: int, n_bags: int, dim: int, idx_bytes: int = 4) -> int:
+    """per bag L*D*4 (rows) + L*idx (indices) + 8 (offset) + D*4 (pooled write)."""
+    return batch_nnz * dim * 4 + batch_nnz * idx_bytes + n_bags * 8 + n_bags * dim * 4
+
+
+class HostLookup:
+    """Reference-facing host API over the engine: host (pinned) CSR in,
+    host pooled [B, sum D] f32 out, synchronous like Ranker.execute_batch
+    (validation errors raise after the call). Copies ride the engine stream."""
+
+    def __init__(self, engine: LookupEngine):
+        self.engine = engine
+        self._out_host = {}
+
+    def lookup(self, batch_host: CsrBatch, out_host: torch.Tensor | None = None) -> torch.Tensor:
+        eng = self.engine
+        dev_batch = batch_host.to(eng.device, non_blocking=True)
+        out = eng.pool(dev_batch, check=False)
+        if out_host is None:
+            key = tuple(out.shape)
+            out_host = self._out_host.get(key)
+            if out_host is None:
+                out_host = self._out_host[key] = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
+        out_host.copy_(out, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        eng.raise_if_bad(dev_batch)
+        return out_host
