@@ -114,9 +114,12 @@ def committed_traffic(config_name):
     return None
 
 
-def build_cfg(cfg_key, rank, n_batches):
+def build_cfg(cfg_key, rank, n_batches, alpha=None):
     from paper_2410_12794_b200.workload import CONFIGS, DlrmBatchGen
-    cfg = CONFIGS[cfg_key]
+    cfg = dict(CONFIGS[cfg_key])
+    if alpha is not None:
+        cfg["alpha"] = alpha
+        cfg["name"] = cfg["name"] + f"-alpha{alpha:g}"
     gen = DlrmBatchGen(cfg["table_rows"], cfg["alpha"], cfg["batch"], cfg["pooling"], seed=1000 * rank)
     return cfg, [gen.next() for _ in range(n_batches)]
 
@@ -185,6 +188,7 @@ def main():
     ap.add_argument("--batches", type=int, default=4, help="distinct batches cycled through")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--alpha", type=float, default=None, help="override Zipf alpha (0 = uniform cold control)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -200,7 +204,7 @@ def main():
     import paper_2410_12794_b200 as P
     from paper_2410_12794_b200.engine import CsrBatch, HostLookup, LookupEngine
 
-    cfg, host_batches = build_cfg(args.config, rank, args.batches)
+    cfg, host_batches = build_cfg(args.config, rank, args.batches, args.alpha)
     dim = cfg["dim"]
     metas = [P.TableMeta(t, n, dim) for t, n in enumerate(cfg["table_rows"])]
     placement = [P.ShardSpec(t, 0, n, rank) for t, n in enumerate(cfg["table_rows"])]
