@@ -114,9 +114,12 @@ def committed_traffic(config_name):
     return None
 
 
-def build_cfg(cfg_key, rank, n_batches, alpha=None):
+def build_cfg(cfg_key, rank, n_batches, alpha=None, table_rows=None):
     from paper_2410_12794_b200.workload import CONFIGS, DlrmBatchGen
     cfg = dict(CONFIGS[cfg_key])
+    if table_rows is not None:
+        cfg["table_rows"] = (table_rows,) * len(cfg["table_rows"])
+        cfg["name"] = cfg["name"] + f"-rows{table_rows}"
     if alpha is not None:
         cfg["alpha"] = alpha
         cfg["name"] = cfg["name"] + f"-alpha{alpha:g}"
@@ -189,6 +192,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--alpha", type=float, default=None, help="override Zipf alpha (0 = uniform cold control)")
+    ap.add_argument("--table-rows", type=int, default=None, help="override every table's row count (cold control)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -204,7 +208,7 @@ def main():
     import paper_2410_12794_b200 as P
     from paper_2410_12794_b200.engine import CsrBatch, HostLookup, LookupEngine
 
-    cfg, host_batches = build_cfg(args.config, rank, args.batches, args.alpha)
+    cfg, host_batches = build_cfg(args.config, rank, args.batches, args.alpha, args.table_rows)
     dim = cfg["dim"]
     metas = [P.TableMeta(t, n, dim) for t, n in enumerate(cfg["table_rows"])]
     placement = [P.ShardSpec(t, 0, n, rank) for t, n in enumerate(cfg["table_rows"])]
@@ -307,11 +311,12 @@ def main():
                        "alpha": cfg["alpha"], "dim": dim, "tables": len(cfg["table_rows"]),
                        "parallelism": "single" if world == 1 else f"replicas{world}",
                        "l2": f"inputs larger than L2: {len(batches)} distinct batches cycled, "
-                             f"{bytes_per[0] / 1e9:.2f} GB algorithmic bytes/batch over 17.3 GB of tables",
+                             f"{bytes_per[0] / 1e9:.2f} GB algorithmic bytes/batch over "
+                             f"{sum(cfg['table_rows']) * dim * 4 / 1e9:.1f} GB of tables",
                        "init_store_s": round(init_s, 2)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": tr, "peak_source": peak_src,
-                         "kernel": "fx::k_gather_pool_v4<32,1,8,int,0>",
+                         "kernel": os.environ.get("FX_POOL_VARIANT_NAME", "fx::k_pool_stream<32,1,8,int,0>"),
                          "bytes_per_launch": tot_bytes / launches, "launch_ms": kernel_ms},
             "gpu_launches": launches,
             "e2e": e2e,

@@ -155,6 +155,62 @@ int fx_dedup(const int32_t *bag_table, const void *indices, int32_t idx_type,
              uint64_t *uniq, int32_t *mult, int64_t *first_ord, int64_t *last_ord,
              int32_t *inverse, int64_t *n_uniq_dev, void *ws, size_t *ws_bytes, void *stream);
 
+
+/* ---- K3/K6: GPU hot-row cache (cache.py:114-352 AdaptiveCache +
+ *      FrequencySketch) ------------------------------------------------------
+ * Keys are u64 (table << 40 | row). The handle owns its device memory
+ * (cudaMalloc at create / reserve; documented exception to "no allocation").
+ * Scalars (fx_cache_scalars order): budget, used, tick, hits, misses, entries,
+ * free_top, sketch_live, sketch_tomb, hash_tomb, pending, n_evlog, n_acc,
+ * n_ev, n_cand, staged. Calls marked [sync] read scalars back to the host. */
+typedef struct fx_cache fx_cache;
+typedef struct fx_table_dir {   /* where rows of `table` in [row_begin,row_end) live */
+  const float *base;
+  int64_t row_begin;
+  int64_t row_end;
+  int64_t ld;
+  int32_t table;
+  int32_t dim;
+} fx_table_dir;
+
+/* admission 0 = "sketch", 1 = "always" (cache.py:164-186) */
+int fx_cache_create(fx_cache **out, int64_t slot_capacity, int32_t max_dim, int32_t admission, double decay,
+                    double prune_below, int64_t budget_bytes, int64_t sketch_capacity, int32_t record_evictions);
+int fx_cache_destroy(fx_cache *c);
+int fx_cache_set_tables(fx_cache *c, const fx_table_dir *dir, int32_t n_dir, const int32_t *table_bytes,
+                        int32_t n_tables);                                     /* host arrays */
+int fx_cache_scalars(fx_cache *c, int64_t *out16, void *stream);               /* [sync] */
+int fx_cache_reserve_sketch(fx_cache *c, int64_t new_keys, void *stream);      /* [sync] */
+int fx_cache_reserve_slots(fx_cache *c, int64_t slots, void *stream);          /* [sync] */
+/* get() per unique key (cache.py:189-202): hit -> last_tick = tick0 +
+ * last_ord + 1, hits += mult; miss -> sketch += mult, misses += mult;
+ * tick += nnz. n_uniq from device (n_uniq_dev) or host. slot_out: slot|-1 */
+int fx_cache_probe(fx_cache *c, const uint64_t *uniq, const int32_t *mult, const int64_t *last_ord,
+                   const int64_t *n_uniq_dev, int64_t n_uniq_host, int64_t nnz, int32_t *slot_out, void *stream);
+/* ordered offers (cache.py:237-268); rows from src_rows[j] or the table dir  [sync] */
+int fx_cache_offer(fx_cache *c, const uint64_t *keys, int64_t n, const int32_t *sizes,
+                   const float *const *src_rows, uint8_t *accepted, void *stream);
+/* resize: new budget; shrink evicts LRU to fit (cache.py:290-309)        [sync] */
+int fx_cache_set_budget(fx_cache *c, int64_t budget, void *stream);
+/* stage_hot_admissions(limit; -1 = None) (cache.py:311-342)                [sync] */
+int fx_cache_stage(fx_cache *c, int64_t limit, int64_t *staged, void *stream);
+/* apply_pending_admissions (cache.py:344-352)                             [sync] */
+int fx_cache_apply_pending(fx_cache *c, int64_t *applied, void *stream);
+/* FrequencySketch.age (cache.py:128-136) */
+int fx_cache_age(fx_cache *c, void *stream);
+int fx_cache_lookup(fx_cache *c, const uint64_t *keys, int64_t n, float *rows_out, int32_t out_ld,
+                    int32_t *slot_out, void *stream);
+int fx_cache_sketch_estimate(fx_cache *c, const uint64_t *keys, int64_t n, double *out, void *stream);
+int fx_cache_sketch_bump(fx_cache *c, const uint64_t *keys, const double *weights, int64_t n, void *stream);
+/* FrequencySketch.hottest order (-count, key), device outputs            [sync] */
+int fx_cache_sketch_ranked(fx_cache *c, uint64_t *keys_out, double *vals_out, int64_t cap, int64_t *n_out,
+                           void *stream);
+/* entries in LRU order (ascending last_tick), device outputs            [sync] */
+int fx_cache_lru(fx_cache *c, uint64_t *keys_out, int64_t *ticks_out, int32_t *hits_out, int64_t cap,
+                 int64_t *n_out, void *stream);
+int fx_cache_eviction_log(fx_cache *c, uint64_t *out, int64_t cap, int64_t *n_out, void *stream); /* [sync] */
+int fx_cache_pending(fx_cache *c, uint64_t *out, int64_t cap, int64_t *n_out, void *stream);      /* [sync] */
+
 #ifdef __cplusplus
 }
 #endif

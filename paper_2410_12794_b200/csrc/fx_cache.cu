@@ -1,0 +1,1027 @@
+// K3 cache probe + K6 admission / eviction / staging / aging: the GPU-resident
+// hot-row cache (mirror of embserve cache.py:114-352 AdaptiveCache +
+// FrequencySketch).
+//
+// Semantics kept bit-exact with the reference under the canonical order
+// (SURVEY §8(c)):
+//  * LRU order == ascending last_tick; every probe advances the tick, a hit's
+//    last_tick = tick0 + (ordinal of its LAST occurrence in the batch) + 1
+//    (cache.py:189-202);
+//  * a miss bumps the exact decayed-frequency sketch by 1.0 per occurrence
+//    (cache.py:194-197), i.e. by the key's miss multiplicity;
+//  * offers are processed strictly in order: sketch admission compares the
+//    candidate against the CURRENT LRU victim, inserts evict LRU until the
+//    byte budget fits and take a fresh tick (cache.py:237-280);
+//  * stage_hot_admissions ranks ALL sketch keys by (-count, key), takes the
+//    top `limit`, skips cached/pending keys and keys that do not fit the spare
+//    room (cache.py:311-342); apply_pending inserts them in order;
+//  * age halves every count and drops counts < prune (cache.py:128-136).
+// The order-dependent steps run as one sequential device thread over
+// precomputed, parallel-gathered inputs (sketch estimates, LRU order); the
+// hash-index and row-copy side effects are applied afterwards in parallel.
+#include <cub/device/device_radix_sort.cuh>
+
+#include <climits>
+#include <vector>
+
+#include "fx_common.cuh"
+
+namespace fx {
+
+constexpr uint64_t kEmpty = ~0ull;
+constexpr uint64_t kTomb = ~0ull - 1;
+constexpr long long kFree = LLONG_MAX;
+constexpr int kRowBitsC = 40;
+constexpr uint64_t kRowMask = (1ull << kRowBitsC) - 1;
+
+struct Scalars {
+  long long budget, used, tick, hits, misses, entries;
+  long long free_top, sketch_live, sketch_tomb, hash_tomb, pending;
+  long long n_evlog, n_acc, n_ev, n_cand, staged;
+};
+
+struct CacheView {
+  Scalars *sc;
+  uint64_t *hkeys;
+  int32_t *hslot;
+  int64_t hcap;
+  uint64_t *skey;
+  long long *stick;
+  int32_t *ssize;
+  int32_t *shits;
+  float *rows;
+  int64_t scap;
+  int32_t row_ld;
+  int32_t *free_stack;
+  uint64_t *kkeys;
+  double *kval;
+  uint8_t *kflag;
+  int64_t kcap;
+  uint64_t *pend;
+  int64_t pend_cap;
+  uint64_t *evlog;
+  int64_t evlog_cap;
+  const fx_table_dir *dir;
+  int32_t n_dir;
+  const int32_t *tbytes;
+  int32_t n_tbytes;
+  int32_t admission;
+  double decay, prune;
+};
+
+// ---------------------------------------------------------------- hashing
+__device__ __forceinline__ int32_t h_find(const CacheView &c, uint64_t key) {
+  const uint64_t m = static_cast<uint64_t>(c.hcap - 1);
+  uint64_t h = hash_key(key) & m;
+  for (int64_t probe = 0; probe < c.hcap; ++probe) {
+    const uint64_t k = c.hkeys[h];
+    if (k == key) return c.hslot[h];
+    if (k == kEmpty) return -1;
+    h = (h + 1) & m;
+  }
+  return -1;
+}
+
+__device__ __forceinline__ void h_insert(const CacheView &c, uint64_t key, int32_t slot) {
+  const uint64_t m = static_cast<uint64_t>(c.hcap - 1);
+  uint64_t h = hash_key(key) & m;
+  while (true) {
+    const unsigned long long prev =
+        atomicCAS(reinterpret_cast<unsigned long long *>(&c.hkeys[h]), (unsigned long long)kEmpty,
+                  (unsigned long long)key);
+    if (prev == kEmpty || prev == key) {
+      c.hslot[h] = slot;
+      return;
+    }
+    h = (h + 1) & m;
+  }
+}
+
+__device__ __forceinline__ bool h_erase(const CacheView &c, uint64_t key) {
+  const uint64_t m = static_cast<uint64_t>(c.hcap - 1);
+  uint64_t h = hash_key(key) & m;
+  for (int64_t probe = 0; probe < c.hcap; ++probe) {
+    const uint64_t k = c.hkeys[h];
+    if (k == key) {
+      c.hkeys[h] = kTomb;
+      return true;
+    }
+    if (k == kEmpty) return false;
+    h = (h + 1) & m;
+  }
+  return false;
+}
+
+__device__ __forceinline__ int64_t k_find(const CacheView &c, uint64_t key) {
+  const uint64_t m = static_cast<uint64_t>(c.kcap - 1);
+  uint64_t h = hash_key(key) & m;
+  for (int64_t probe = 0; probe < c.kcap; ++probe) {
+    const uint64_t k = c.kkeys[h];
+    if (k == key) return static_cast<int64_t>(h);
+    if (k == kEmpty) return -1;
+    h = (h + 1) & m;
+  }
+  return -1;
+}
+
+__device__ __forceinline__ double k_est(const CacheView &c, uint64_t key) {
+  const int64_t i = k_find(c, key);
+  return i >= 0 ? c.kval[i] : 0.0;
+}
+
+// insert-or-add (returns true when the key was new)
+__device__ __forceinline__ bool k_add(const CacheView &c, uint64_t key, double w) {
+  const uint64_t m = static_cast<uint64_t>(c.kcap - 1);
+  uint64_t h = hash_key(key) & m;
+  while (true) {
+    const unsigned long long prev =
+        atomicCAS(reinterpret_cast<unsigned long long *>(&c.kkeys[h]), (unsigned long long)kEmpty,
+                  (unsigned long long)key);
+    if (prev == kEmpty || prev == key) {
+      atomicAdd(&c.kval[h], w);
+      return prev == kEmpty;
+    }
+    h = (h + 1) & m;
+  }
+}
+
+__device__ __forceinline__ int32_t table_bytes_of(const CacheView &c, uint64_t key) {
+  const int64_t t = static_cast<int64_t>(key >> kRowBitsC);
+  return (t >= 0 && t < c.n_tbytes) ? c.tbytes[t] : -1;
+}
+
+__device__ __forceinline__ const float *dir_row(const CacheView &c, uint64_t key, int32_t *dim) {
+  const int32_t t = static_cast<int32_t>(key >> kRowBitsC);
+  const int64_t r = static_cast<int64_t>(key & kRowMask);
+  for (int i = 0; i < c.n_dir; ++i) {
+    const fx_table_dir &d = c.dir[i];
+    if (d.table == t && r >= d.row_begin && r < d.row_end) {
+      *dim = d.dim;
+      return d.base + (r - d.row_begin) * d.ld;
+    }
+  }
+  *dim = 0;
+  return nullptr;
+}
+
+// ---------------------------------------------------------------- init
+__global__ void k_cache_init(CacheView c) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  for (int64_t i = i0; i < c.hcap; i += stride) c.hkeys[i] = kEmpty;
+  for (int64_t i = i0; i < c.kcap; i += stride) {
+    c.kkeys[i] = kEmpty;
+    c.kval[i] = 0.0;
+    c.kflag[i] = 0;
+  }
+  for (int64_t i = i0; i < c.scap; i += stride) {
+    c.stick[i] = kFree;
+    c.skey[i] = kEmpty;
+    c.free_stack[i] = static_cast<int32_t>(c.scap - 1 - i);  // pops give 0, 1, 2, ...
+  }
+}
+
+// ---------------------------------------------------------------- K3 probe
+__global__ void __launch_bounds__(256) k_probe(CacheView c, const uint64_t *__restrict__ uniq,
+                                               const int32_t *__restrict__ mult,
+                                               const int64_t *__restrict__ last_ord, const int64_t *n_ptr,
+                                               int64_t n_host, int32_t *slot_out) {
+  const int64_t n = n_ptr ? *n_ptr : n_host;
+  const long long tick0 = c.sc->tick;
+  long long hits = 0, misses = 0, born = 0;
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t key = uniq[u];
+    const int32_t m = mult[u];
+    const int32_t s = h_find(c, key);
+    if (s >= 0) {
+      c.stick[s] = tick0 + last_ord[u] + 1;
+      c.shits[s] += m;
+      hits += m;
+    } else {
+      born += k_add(c, key, static_cast<double>(m)) ? 1 : 0;
+      misses += m;
+    }
+    if (slot_out) slot_out[u] = s;
+  }
+  // warp-aggregate the counters
+  for (int o = 16; o; o >>= 1) {
+    hits += __shfl_down_sync(0xffffffffu, hits, o);
+    misses += __shfl_down_sync(0xffffffffu, misses, o);
+    born += __shfl_down_sync(0xffffffffu, born, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (hits) atomicAdd(reinterpret_cast<unsigned long long *>(&c.sc->hits), (unsigned long long)hits);
+    if (misses) atomicAdd(reinterpret_cast<unsigned long long *>(&c.sc->misses), (unsigned long long)misses);
+    if (born) atomicAdd(reinterpret_cast<unsigned long long *>(&c.sc->sketch_live), (unsigned long long)born);
+  }
+}
+
+__global__ void k_advance_tick(Scalars *sc, long long nnz) { sc->tick += nnz; }
+
+// ---------------------------------------------------------------- offers
+struct OfferWS {
+  double *est_cand;
+  int32_t *size_cand;
+  uint8_t *present;
+  int32_t *lru_slot;   // sorted occupied slots (ascending tick)
+  double *est_vic;
+  int32_t *acc_slot;
+  int32_t *acc_j;
+  uint64_t *ev_keys;
+  long long *sort_keys_in;
+  long long *sort_keys_out;
+  int32_t *iota;
+};
+
+__global__ void k_offer_prep(CacheView c, const uint64_t *keys, int64_t n, const int32_t *sizes, OfferWS w) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t key = keys[j];
+    w.est_cand[j] = k_est(c, key);
+    w.size_cand[j] = sizes ? sizes[j] : table_bytes_of(c, key);
+    w.present[j] = h_find(c, key) >= 0 ? 1 : 0;
+  }
+}
+
+__global__ void k_lru_keys(CacheView c, OfferWS w) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < c.scap; i += (int64_t)gridDim.x * blockDim.x) {
+    w.sort_keys_in[i] = c.stick[i];
+    w.iota[i] = static_cast<int32_t>(i);
+  }
+}
+
+__global__ void k_vic_prep(CacheView c, OfferWS w, int64_t k) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x)
+    w.est_vic[i] = k_est(c, c.skey[w.lru_slot[i]]);
+}
+
+// mode 0: offer (admission policy); mode 1: apply pending (always admit,
+// skip present keys); n == 0 with used > budget: evict to budget (shrink).
+__global__ void k_offer_seq(CacheView c, const uint64_t *keys, int64_t n, int32_t mode, OfferWS w, int64_t k_vic,
+                            uint8_t *accepted, int32_t record) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  Scalars *sc = c.sc;
+  long long used = sc->used, budget = sc->budget, tick = sc->tick, entries = sc->entries, ftop = sc->free_top;
+  const long long e0 = entries;
+  long long h = 0, n_acc = 0, n_ev = 0, n_log = sc->n_evlog;
+  auto head_slot = [&](long long q) -> int32_t { return q < e0 ? w.lru_slot[q] : w.acc_slot[q - e0]; };
+  auto evict_head = [&]() {
+    const int32_t s = head_slot(h);
+    ++h;
+    used -= c.ssize[s];
+    const uint64_t k = c.skey[s];
+    w.ev_keys[n_ev++] = k;
+    if (record && n_log < c.evlog_cap) c.evlog[n_log] = k;
+    if (record) ++n_log;
+    c.stick[s] = kFree;
+    c.skey[s] = kEmpty;
+    c.free_stack[ftop++] = s;
+    --entries;
+  };
+  while (used > budget && entries > 0) evict_head();  // resize shrink (cache.py:270-274)
+  for (int64_t j = 0; j < n; ++j) {
+    const uint64_t key = keys[j];
+    const int32_t size = w.size_cand[j];
+    if (w.present[j]) {  // already cached: offer -> True; apply -> skip
+      if (accepted) accepted[j] = mode == 0 ? 1 : 0;
+      continue;
+    }
+    if (size < 0 || size > budget) {
+      if (accepted) accepted[j] = 0;
+      continue;
+    }
+    if (mode == 0 && c.admission == 0 && used + size > budget && entries > 0) {
+      const double ve = h < k_vic ? w.est_vic[h] : (h < e0 ? k_est(c, c.skey[w.lru_slot[h]])
+                                                            : w.est_cand[w.acc_j[h - e0]]);
+      if (w.est_cand[j] < ve) {
+        if (accepted) accepted[j] = 0;
+        continue;
+      }
+    }
+    while (used + size > budget) evict_head();
+    ++tick;
+    const int32_t s = c.free_stack[--ftop];
+    c.skey[s] = key;
+    c.stick[s] = tick;
+    c.ssize[s] = size;
+    c.shits[s] = 0;
+    w.acc_slot[n_acc] = s;
+    w.acc_j[n_acc] = static_cast<int32_t>(j);
+    ++n_acc;
+    used += size;
+    ++entries;
+    if (accepted) accepted[j] = 1;
+  }
+  sc->used = used;
+  sc->tick = tick;
+  sc->entries = entries;
+  sc->free_top = ftop;
+  sc->n_acc = n_acc;
+  sc->n_ev = n_ev;
+  sc->n_evlog = n_log;
+}
+
+__global__ void k_hash_erase(CacheView c, OfferWS w) {
+  const long long n = c.sc->n_ev;
+  long long t = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    t += h_erase(c, w.ev_keys[i]) ? 1 : 0;
+  if (t) atomicAdd(reinterpret_cast<unsigned long long *>(&c.sc->hash_tomb), (unsigned long long)t);
+}
+
+// one warp per accepted entry: index it and copy its row into the slot
+__global__ void __launch_bounds__(256) k_install(CacheView c, OfferWS w, const uint64_t *keys,
+                                                 const float *const *src_rows) {
+  const long long n = c.sc->n_acc;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t a = warp; a < n; a += nw) {
+    const int32_t s = w.acc_slot[a];
+    const int32_t j = w.acc_j[a];
+    const uint64_t key = keys[j];
+    if (c.skey[s] != key || c.stick[s] == kFree) continue;  // evicted again later in the same call
+    if (lane == 0) h_insert(c, key, s);
+    int32_t dim = c.ssize[s] / 4;
+    const float *src = src_rows ? src_rows[j] : nullptr;
+    if (!src) src = dir_row(c, key, &dim);
+    float *dst = c.rows + static_cast<int64_t>(s) * c.row_ld;
+    if (src)
+      for (int i = lane; i < dim; i += 32) dst[i] = src[i];
+  }
+}
+
+// ---------------------------------------------------------------- staging
+__global__ void k_sketch_collect(CacheView c, uint64_t *out_keys, long long *out_vbits, int32_t *out_pos,
+                                 long long *count) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < c.kcap; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = c.kkeys[i];
+    if (k == kEmpty || k == kTomb) continue;
+    const long long p = atomicAdd(reinterpret_cast<unsigned long long *>(count), 1ull);
+    out_keys[p] = k;
+    out_vbits[p] = ~__double_as_longlong(c.kval[i]) & LLONG_MAX;  // ascending = descending count
+    out_pos[p] = static_cast<int32_t>(i);
+  }
+}
+
+// ranked keys -> pending (sequential room accounting, cache.py:323-342)
+__global__ void k_stage_seq(CacheView c, const int32_t *ranked_pos, int64_t m, int64_t limit) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  Scalars *sc = c.sc;
+  long long room = sc->budget - sc->used;
+  long long staged = 0, pend = sc->pending;
+  if (room > 0 && sc->sketch_live > 0) {
+    for (int64_t i = 0; i < m; ++i) {
+      const int32_t p = ranked_pos[i];
+      const uint64_t key = c.kkeys[p];
+      if (c.kflag[p] || h_find(c, key) >= 0) continue;
+      const int32_t size = table_bytes_of(c, key);
+      if (size < 0 || size > room) continue;
+      if (pend >= c.pend_cap) break;
+      c.pend[pend++] = key;
+      c.kflag[p] = 1;
+      room -= size;
+      ++staged;
+      if (limit >= 0 && staged >= limit) break;
+    }
+  }
+  sc->pending = pend;
+  sc->staged = staged;
+}
+
+__global__ void k_clear_pending_flags(CacheView c) {
+  const long long n = c.sc->pending;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = k_find(c, c.pend[i]);
+    if (p >= 0) c.kflag[p] = 0;
+  }
+}
+
+__global__ void k_pending_done(Scalars *sc) { sc->pending = 0; }
+
+// ---------------------------------------------------------------- aging
+__global__ void k_age(CacheView c) {
+  long long dead = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < c.kcap; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = c.kkeys[i];
+    if (k == kEmpty || k == kTomb) continue;
+    const double v = c.kval[i] * c.decay;
+    if (v < c.prune) {
+      c.kkeys[i] = kTomb;
+      c.kval[i] = 0.0;
+      c.kflag[i] = 0;
+      ++dead;
+    } else {
+      c.kval[i] = v;
+    }
+  }
+  for (int o = 16; o; o >>= 1) dead += __shfl_down_sync(0xffffffffu, dead, o);
+  if ((threadIdx.x & 31) == 0 && dead) {
+    atomicAdd(reinterpret_cast<unsigned long long *>(&c.sc->sketch_live), (unsigned long long)(-dead));
+    atomicAdd(reinterpret_cast<unsigned long long *>(&c.sc->sketch_tomb), (unsigned long long)dead);
+  }
+}
+
+// ---------------------------------------------------------------- rehash
+__global__ void k_sketch_rehash(CacheView dst, const uint64_t *okeys, const double *oval, const uint8_t *oflag,
+                                int64_t ocap) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ocap; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = okeys[i];
+    if (k == kEmpty || k == kTomb) continue;
+    const uint64_t m = static_cast<uint64_t>(dst.kcap - 1);
+    uint64_t h = hash_key(k) & m;
+    while (atomicCAS(reinterpret_cast<unsigned long long *>(&dst.kkeys[h]), (unsigned long long)kEmpty,
+                     (unsigned long long)k) != kEmpty)
+      h = (h + 1) & m;
+    dst.kval[h] = oval[i];
+    dst.kflag[h] = oflag[i];
+  }
+}
+
+__global__ void k_index_rebuild(CacheView c) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < c.scap; i += (int64_t)gridDim.x * blockDim.x)
+    if (c.stick[i] != kFree) h_insert(c, c.skey[i], static_cast<int32_t>(i));
+}
+
+__global__ void k_fill_u64(uint64_t *p, int64_t n, uint64_t v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+// ---------------------------------------------------------------- queries
+__global__ void k_lookup_rows(CacheView c, const uint64_t *keys, int64_t n, float *out, int32_t out_ld,
+                              int32_t *found) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp; i < n; i += nw) {
+    const int32_t s = h_find(c, keys[i]);
+    if (lane == 0) found[i] = s;
+    if (s < 0) continue;
+    const int32_t dim = c.ssize[s] / 4;
+    for (int k = lane; k < dim && k < out_ld; k += 32) out[i * out_ld + k] = c.rows[(int64_t)s * c.row_ld + k];
+  }
+}
+
+__global__ void k_sketch_lookup(CacheView c, const uint64_t *keys, int64_t n, double *out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = k_est(c, keys[i]);
+}
+
+__global__ void k_sketch_bump(CacheView c, const uint64_t *keys, const double *w, int64_t n) {
+  long long born = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    born += k_add(c, keys[i], w[i]) ? 1 : 0;
+  if (born) atomicAdd(reinterpret_cast<unsigned long long *>(&c.sc->sketch_live), (unsigned long long)born);
+}
+
+__global__ void k_gather_vbits(CacheView c, const int32_t *pos, int64_t n, long long *out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = ~__double_as_longlong(c.kval[pos[i]]) & LLONG_MAX;
+}
+
+__global__ void k_dump_lru(CacheView c, const int32_t *lru_slot, int64_t n, uint64_t *keys, long long *ticks,
+                           int32_t *hits) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t s = lru_slot[i];
+    keys[i] = c.skey[s];
+    if (ticks) ticks[i] = c.stick[s];
+    if (hits) hits[i] = c.shits[s];
+  }
+}
+
+__global__ void k_dump_sketch(CacheView c, const int32_t *pos, int64_t n, uint64_t *keys, double *vals) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    keys[i] = c.kkeys[pos[i]];
+    vals[i] = c.kval[pos[i]];
+  }
+}
+
+static inline size_t al(size_t x) { return (x + 255) & ~size_t(255); }
+
+}  // namespace fx
+
+using namespace fx;
+
+struct fx_cache {
+  CacheView v;
+  int32_t record;
+  std::vector<fx_table_dir> dir_host;
+  std::vector<int32_t> tbytes_host;
+  fx_table_dir *dir_dev = nullptr;
+  int32_t *tbytes_dev = nullptr;
+  void *ws = nullptr;
+  size_t ws_bytes = 0;
+};
+
+namespace {
+
+template <typename T>
+int dmalloc(T **p, size_t n) {
+  *p = nullptr;
+  if (n == 0) n = 1;
+  cudaError_t e = cudaMalloc(reinterpret_cast<void **>(p), n * sizeof(T));
+  return cuda_check(e, "fx_cache: cudaMalloc");
+}
+
+int ensure_ws(fx_cache *c, size_t need) {
+  if (c->ws_bytes >= need) return FX_OK;
+  if (c->ws) cudaFree(c->ws);
+  c->ws = nullptr;
+  c->ws_bytes = 0;
+  int rc = cuda_check(cudaMalloc(&c->ws, need), "fx_cache: workspace");
+  if (rc == FX_OK) c->ws_bytes = need;
+  return rc;
+}
+
+int64_t pow2_at_least(int64_t x) {
+  int64_t p = 1024;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+int read_scalars(fx_cache *c, Scalars *h, cudaStream_t st) {
+  int rc = cuda_check(cudaMemcpyAsync(h, c->v.sc, sizeof(Scalars), cudaMemcpyDeviceToHost, st), "scalars");
+  if (rc) return rc;
+  return cuda_check(cudaStreamSynchronize(st), "scalars sync");
+}
+
+// Layout one offer workspace for n candidates over the cache's slot capacity.
+size_t offer_ws_bytes(fx_cache *c, int64_t n, size_t *cub_bytes) {
+  const int64_t S = c->v.scap;
+  size_t cb = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, cb, (const long long *)nullptr, (long long *)nullptr,
+                                  (const int32_t *)nullptr, (int32_t *)nullptr, static_cast<int>(S));
+  *cub_bytes = cb;
+  const int64_t nn = n > 0 ? n : 1;
+  return al(nn * 8) + al(nn * 4) + al(nn) + al(S * 4) + al(S * 8) + al(S * 4) + al(nn * 4) + al(S * 8 + nn * 8) +
+         al(S * 8) * 2 + al(S * 4) + al(cb);
+}
+
+OfferWS carve_offer_ws(fx_cache *c, int64_t n, void **cub_tmp) {
+  const int64_t S = c->v.scap;
+  const int64_t nn = n > 0 ? n : 1;
+  char *p = static_cast<char *>(c->ws);
+  OfferWS w;
+  w.est_cand = reinterpret_cast<double *>(p); p += al(nn * 8);
+  w.size_cand = reinterpret_cast<int32_t *>(p); p += al(nn * 4);
+  w.present = reinterpret_cast<uint8_t *>(p); p += al(nn);
+  w.lru_slot = reinterpret_cast<int32_t *>(p); p += al(S * 4);
+  w.est_vic = reinterpret_cast<double *>(p); p += al(S * 8);
+  w.acc_slot = reinterpret_cast<int32_t *>(p); p += al(S * 4);
+  w.acc_j = reinterpret_cast<int32_t *>(p); p += al(nn * 4);
+  w.ev_keys = reinterpret_cast<uint64_t *>(p); p += al(S * 8 + nn * 8);
+  w.sort_keys_in = reinterpret_cast<long long *>(p); p += al(S * 8);
+  w.sort_keys_out = reinterpret_cast<long long *>(p); p += al(S * 8);
+  w.iota = reinterpret_cast<int32_t *>(p); p += al(S * 4);
+  *cub_tmp = p;
+  return w;
+}
+
+// Shared offer/apply/shrink pipeline (see k_offer_seq).
+int run_offer(fx_cache *c, const uint64_t *keys, int64_t n, int32_t mode, const int32_t *sizes,
+              const float *const *src_rows, uint8_t *accepted, cudaStream_t st) {
+  size_t cb = 0;
+  const size_t need = offer_ws_bytes(c, n, &cb);
+  int rc = ensure_ws(c, need);
+  if (rc) return rc;
+  void *cub_tmp = nullptr;
+  OfferWS w = carve_offer_ws(c, n, &cub_tmp);
+  Scalars h;
+  rc = read_scalars(c, &h, st);
+  if (rc) return rc;
+  // room check: capacity for the worst case (every candidate inserted)
+  if (h.entries + n > c->v.scap) {
+    // slots can run out only if the byte budget admits more rows than the
+    // reserved slot capacity; the host reserves slots for the budget.
+    long long min_bytes = LLONG_MAX;
+    for (int32_t b : c->tbytes_host)
+      if (b > 0 && b < min_bytes) min_bytes = b;
+    if (min_bytes == LLONG_MAX || h.budget / min_bytes > c->v.scap) {
+      set_error("fx_cache: slot capacity below the budget's row count; call fx_cache_reserve_slots");
+      return FX_E_CAPACITY;
+    }
+  }
+  if (n > 0) k_offer_prep<<<grid_for(n, 256), 256, 0, st>>>(c->v, keys, n, sizes, w);
+  int64_t k_vic = 0;
+  if (h.entries > 0) {
+    const int64_t S = c->v.scap;
+    k_lru_keys<<<grid_for(S, 256), 256, 0, st>>>(c->v, w);
+    cub::DeviceRadixSort::SortPairs(cub_tmp, cb, w.sort_keys_in, w.sort_keys_out, w.iota, w.lru_slot,
+                                    static_cast<int>(S), 0, 64, st);
+    k_vic = h.entries < n ? h.entries : n;
+    if (mode == 0 && c->v.admission == 0 && k_vic > 0)
+      k_vic_prep<<<grid_for(k_vic, 256), 256, 0, st>>>(c->v, w, k_vic);
+    else
+      k_vic = 0;
+  }
+  k_offer_seq<<<1, 32, 0, st>>>(c->v, keys, n, mode, w, k_vic, accepted, c->record);
+  k_hash_erase<<<grid_for(h.entries + n + 1, 256), 256, 0, st>>>(c->v, w);
+  if (n > 0) k_install<<<grid_for(n * 32, 256), 256, 0, st>>>(c->v, w, keys, src_rows);
+  FX_LAUNCH_CHECK("fx_cache offer");
+  // keep the index below half tombstones
+  rc = read_scalars(c, &h, st);
+  if (rc) return rc;
+  if ((h.hash_tomb + h.entries) * 2 > c->v.hcap) {
+    k_fill_u64<<<grid_for(c->v.hcap, 256), 256, 0, st>>>(c->v.hkeys, c->v.hcap, kEmpty);
+    k_index_rebuild<<<grid_for(c->v.scap, 256), 256, 0, st>>>(c->v);
+    cudaMemsetAsync(&c->v.sc->hash_tomb, 0, sizeof(long long), st);
+    FX_LAUNCH_CHECK("fx_cache index rebuild");
+  }
+  return FX_OK;
+}
+
+int upload_dir(fx_cache *c) {
+  if (c->dir_dev) cudaFree(c->dir_dev);
+  if (c->tbytes_dev) cudaFree(c->tbytes_dev);
+  c->dir_dev = nullptr;
+  c->tbytes_dev = nullptr;
+  int rc = dmalloc(&c->dir_dev, c->dir_host.size());
+  if (rc) return rc;
+  rc = dmalloc(&c->tbytes_dev, c->tbytes_host.size());
+  if (rc) return rc;
+  if (!c->dir_host.empty())
+    cudaMemcpy(c->dir_dev, c->dir_host.data(), c->dir_host.size() * sizeof(fx_table_dir), cudaMemcpyHostToDevice);
+  if (!c->tbytes_host.empty())
+    cudaMemcpy(c->tbytes_dev, c->tbytes_host.data(), c->tbytes_host.size() * 4, cudaMemcpyHostToDevice);
+  c->v.dir = c->dir_dev;
+  c->v.n_dir = static_cast<int32_t>(c->dir_host.size());
+  c->v.tbytes = c->tbytes_dev;
+  c->v.n_tbytes = static_cast<int32_t>(c->tbytes_host.size());
+  return cuda_check(cudaGetLastError(), "fx_cache: upload dir");
+}
+
+}  // namespace
+
+extern "C" {
+
+int fx_cache_create(fx_cache **out, int64_t slot_capacity, int32_t max_dim, int32_t admission, double decay,
+                    double prune_below, int64_t budget_bytes, int64_t sketch_capacity, int32_t record_evictions) {
+  if (!out || slot_capacity < 0 || max_dim < 1 || (admission != 0 && admission != 1) || budget_bytes < 0) {
+    set_error("fx_cache_create: bad arguments");
+    return FX_E_CONFIG;
+  }
+  fx_cache *c = new fx_cache();
+  CacheView &v = c->v;
+  v.scap = slot_capacity > 0 ? slot_capacity : 1;
+  v.row_ld = (max_dim + 3) & ~3;
+  v.hcap = pow2_at_least(4 * v.scap);
+  v.kcap = pow2_at_least(sketch_capacity > 0 ? 2 * sketch_capacity : 4096);
+  v.pend_cap = v.scap + 1024;
+  v.evlog_cap = record_evictions ? 1 << 20 : 0;
+  v.admission = admission;
+  v.decay = decay;
+  v.prune = prune_below;
+  c->record = record_evictions;
+  int rc = FX_OK;
+  rc = rc ? rc : dmalloc(&v.sc, 1);
+  rc = rc ? rc : dmalloc(&v.hkeys, v.hcap);
+  rc = rc ? rc : dmalloc(&v.hslot, v.hcap);
+  rc = rc ? rc : dmalloc(&v.skey, v.scap);
+  rc = rc ? rc : dmalloc(&v.stick, v.scap);
+  rc = rc ? rc : dmalloc(&v.ssize, v.scap);
+  rc = rc ? rc : dmalloc(&v.shits, v.scap);
+  rc = rc ? rc : dmalloc(&v.rows, static_cast<size_t>(v.scap) * v.row_ld);
+  rc = rc ? rc : dmalloc(&v.free_stack, v.scap);
+  rc = rc ? rc : dmalloc(&v.kkeys, v.kcap);
+  rc = rc ? rc : dmalloc(&v.kval, v.kcap);
+  rc = rc ? rc : dmalloc(&v.kflag, v.kcap);
+  rc = rc ? rc : dmalloc(&v.pend, v.pend_cap);
+  rc = rc ? rc : dmalloc(&v.evlog, v.evlog_cap);
+  if (rc) {
+    delete c;
+    return rc;
+  }
+  Scalars h{};
+  h.budget = budget_bytes;
+  h.free_top = v.scap;
+  cudaMemcpy(v.sc, &h, sizeof(h), cudaMemcpyHostToDevice);
+  cudaMemset(v.ssize, 0, v.scap * 4);
+  cudaMemset(v.shits, 0, v.scap * 4);
+  upload_dir(c);
+  k_cache_init<<<grid_for(v.hcap > v.kcap ? v.hcap : v.kcap, 256), 256>>>(v);
+  rc = cuda_check(cudaDeviceSynchronize(), "fx_cache_create");
+  if (rc) {
+    delete c;
+    return rc;
+  }
+  *out = c;
+  return FX_OK;
+}
+
+int fx_cache_destroy(fx_cache *c) {
+  if (!c) return FX_OK;
+  CacheView &v = c->v;
+  void *ps[] = {v.sc, v.hkeys, v.hslot, v.skey, v.stick, v.ssize, v.shits, v.rows, v.free_stack, v.kkeys,
+                v.kval, v.kflag, v.pend, v.evlog, c->dir_dev, c->tbytes_dev, c->ws};
+  for (void *p : ps)
+    if (p) cudaFree(p);
+  delete c;
+  return FX_OK;
+}
+
+int fx_cache_set_tables(fx_cache *c, const fx_table_dir *dir, int32_t n_dir, const int32_t *table_bytes,
+                        int32_t n_tables) {
+  c->dir_host.assign(dir, dir + n_dir);
+  c->tbytes_host.assign(table_bytes, table_bytes + n_tables);
+  int max_dim = 0;
+  for (auto &d : c->dir_host) max_dim = d.dim > max_dim ? d.dim : max_dim;
+  for (int32_t b : c->tbytes_host) max_dim = b / 4 > max_dim ? b / 4 : max_dim;
+  if (max_dim > c->v.row_ld) {
+    set_error("fx_cache_set_tables: table dim exceeds the cache row width");
+    return FX_E_CONFIG;
+  }
+  return upload_dir(c);
+}
+
+int fx_cache_scalars(fx_cache *c, int64_t *out, void *stream) {
+  Scalars h;
+  int rc = read_scalars(c, &h, as_stream(stream));
+  if (rc) return rc;
+  const long long *p = reinterpret_cast<const long long *>(&h);
+  for (size_t i = 0; i < sizeof(Scalars) / 8; ++i) out[i] = p[i];
+  return FX_OK;
+}
+
+int fx_cache_set_budget(fx_cache *c, int64_t budget, void *stream) {
+  cudaStream_t st = as_stream(stream);
+  cudaMemcpyAsync(&c->v.sc->budget, &budget, 8, cudaMemcpyHostToDevice, st);
+  // shrink: evict LRU until used <= budget (cache.py:270-274)
+  return run_offer(c, nullptr, 0, 1, nullptr, nullptr, nullptr, st);
+}
+
+int fx_cache_reserve_sketch(fx_cache *c, int64_t new_keys, void *stream) {
+  cudaStream_t st = as_stream(stream);
+  Scalars h;
+  int rc = read_scalars(c, &h, st);
+  if (rc) return rc;
+  const int64_t need = 2 * (h.sketch_live + new_keys) + 1024;
+  if (need <= c->v.kcap && (h.sketch_live + h.sketch_tomb + new_keys) * 2 <= c->v.kcap) return FX_OK;
+  CacheView nv = c->v;
+  nv.kcap = pow2_at_least(need > c->v.kcap ? 2 * need : c->v.kcap);
+  rc = dmalloc(&nv.kkeys, nv.kcap);
+  rc = rc ? rc : dmalloc(&nv.kval, nv.kcap);
+  rc = rc ? rc : dmalloc(&nv.kflag, nv.kcap);
+  if (rc) return rc;
+  k_fill_u64<<<grid_for(nv.kcap, 256), 256, 0, st>>>(nv.kkeys, nv.kcap, kEmpty);
+  cudaMemsetAsync(nv.kval, 0, nv.kcap * 8, st);
+  cudaMemsetAsync(nv.kflag, 0, nv.kcap, st);
+  k_sketch_rehash<<<grid_for(c->v.kcap, 256), 256, 0, st>>>(nv, c->v.kkeys, c->v.kval, c->v.kflag, c->v.kcap);
+  cudaMemsetAsync(&c->v.sc->sketch_tomb, 0, 8, st);
+  rc = cuda_check(cudaStreamSynchronize(st), "fx_cache_reserve_sketch");
+  cudaFree(c->v.kkeys);
+  cudaFree(c->v.kval);
+  cudaFree(c->v.kflag);
+  c->v = nv;
+  return rc;
+}
+
+int fx_cache_reserve_slots(fx_cache *c, int64_t slots, void *stream) {
+  cudaStream_t st = as_stream(stream);
+  if (slots <= c->v.scap) return FX_OK;
+  int rc = cuda_check(cudaStreamSynchronize(st), "fx_cache_reserve_slots");
+  if (rc) return rc;
+  CacheView nv = c->v;
+  nv.scap = slots;
+  nv.hcap = pow2_at_least(4 * slots);
+  nv.pend_cap = slots + 1024;
+  rc = dmalloc(&nv.skey, nv.scap);
+  rc = rc ? rc : dmalloc(&nv.stick, nv.scap);
+  rc = rc ? rc : dmalloc(&nv.ssize, nv.scap);
+  rc = rc ? rc : dmalloc(&nv.shits, nv.scap);
+  rc = rc ? rc : dmalloc(&nv.rows, static_cast<size_t>(nv.scap) * nv.row_ld);
+  rc = rc ? rc : dmalloc(&nv.free_stack, nv.scap);
+  rc = rc ? rc : dmalloc(&nv.hkeys, nv.hcap);
+  rc = rc ? rc : dmalloc(&nv.hslot, nv.hcap);
+  rc = rc ? rc : dmalloc(&nv.pend, nv.pend_cap);
+  if (rc) return rc;
+  const int64_t S0 = c->v.scap;
+  // old slots keep their ids; new slots are appended to the free stack
+  k_fill_u64<<<grid_for(nv.scap, 256), 256, 0, st>>>(nv.skey, nv.scap, kEmpty);
+  std::vector<long long> freeticks(1, kFree);
+  cudaMemcpyAsync(nv.skey, c->v.skey, S0 * 8, cudaMemcpyDeviceToDevice, st);
+  cudaMemcpyAsync(nv.ssize, c->v.ssize, S0 * 4, cudaMemcpyDeviceToDevice, st);
+  cudaMemsetAsync(nv.ssize + S0, 0, (nv.scap - S0) * 4, st);
+  cudaMemcpyAsync(nv.shits, c->v.shits, S0 * 4, cudaMemcpyDeviceToDevice, st);
+  cudaMemsetAsync(nv.shits + S0, 0, (nv.scap - S0) * 4, st);
+  cudaMemcpyAsync(nv.rows, c->v.rows, static_cast<size_t>(S0) * c->v.row_ld * 4, cudaMemcpyDeviceToDevice, st);
+  cudaMemcpyAsync(nv.pend, c->v.pend, c->v.pend_cap * 8, cudaMemcpyDeviceToDevice, st);
+  // ticks: copy then mark the new slots free
+  cudaMemcpyAsync(nv.stick, c->v.stick, S0 * 8, cudaMemcpyDeviceToDevice, st);
+  k_fill_u64<<<grid_for(nv.scap - S0, 256), 256, 0, st>>>(reinterpret_cast<uint64_t *>(nv.stick + S0),
+                                                           nv.scap - S0, static_cast<uint64_t>(kFree));
+  // free stack: existing free entries first (top of stack = old order), new ids below them
+  Scalars h;
+  rc = read_scalars(c, &h, st);
+  if (rc) return rc;
+  std::vector<int32_t> fs(nv.scap);
+  int64_t k = 0;
+  for (int64_t s = nv.scap - 1; s >= S0; --s) fs[k++] = static_cast<int32_t>(s);
+  std::vector<int32_t> oldfs(h.free_top > 0 ? h.free_top : 1);
+  if (h.free_top > 0) cudaMemcpy(oldfs.data(), c->v.free_stack, h.free_top * 4, cudaMemcpyDeviceToHost);
+  for (long long i = 0; i < h.free_top; ++i) fs[k++] = oldfs[i];
+  cudaMemcpy(nv.free_stack, fs.data(), k * 4, cudaMemcpyHostToDevice);
+  h.free_top = k;
+  h.hash_tomb = 0;
+  cudaMemcpy(c->v.sc, &h, sizeof(h), cudaMemcpyHostToDevice);
+  k_fill_u64<<<grid_for(nv.hcap, 256), 256, 0, st>>>(nv.hkeys, nv.hcap, kEmpty);
+  k_index_rebuild<<<grid_for(nv.scap, 256), 256, 0, st>>>(nv);
+  rc = cuda_check(cudaStreamSynchronize(st), "fx_cache_reserve_slots");
+  void *old[] = {c->v.skey, c->v.stick, c->v.ssize, c->v.shits, c->v.rows, c->v.free_stack, c->v.hkeys,
+                 c->v.hslot, c->v.pend};
+  for (void *p : old) cudaFree(p);
+  c->v = nv;
+  return rc;
+}
+
+int fx_cache_probe(fx_cache *c, const uint64_t *uniq, const int32_t *mult, const int64_t *last_ord,
+                   const int64_t *n_uniq_dev, int64_t n_uniq_host, int64_t nnz, int32_t *slot_out, void *stream) {
+  cudaStream_t st = as_stream(stream);
+  const int64_t work = n_uniq_dev ? nnz : n_uniq_host;
+  k_probe<<<grid_for(work > 0 ? work : 1, 256), 256, 0, st>>>(c->v, uniq, mult, last_ord, n_uniq_dev, n_uniq_host,
+                                                              slot_out);
+  k_advance_tick<<<1, 1, 0, st>>>(c->v.sc, nnz);
+  FX_LAUNCH_CHECK("fx_cache_probe");
+  return FX_OK;
+}
+
+int fx_cache_offer(fx_cache *c, const uint64_t *keys, int64_t n, const int32_t *sizes, const float *const *src_rows,
+                   uint8_t *accepted, void *stream) {
+  return run_offer(c, keys, n, 0, sizes, src_rows, accepted, as_stream(stream));
+}
+
+int fx_cache_apply_pending(fx_cache *c, int64_t *applied, void *stream) {
+  cudaStream_t st = as_stream(stream);
+  Scalars h;
+  int rc = read_scalars(c, &h, st);
+  if (rc) return rc;
+  const int64_t n = h.pending;
+  long long e0 = h.entries;
+  if (n > 0) {
+    // clear the pending flags first (keys stay in c->v.pend until the insert ran)
+    k_clear_pending_flags<<<grid_for(n, 256), 256, 0, st>>>(c->v);
+    rc = run_offer(c, c->v.pend, n, 1, nullptr, nullptr, nullptr, st);
+    if (rc) return rc;
+    k_pending_done<<<1, 1, 0, st>>>(c->v.sc);
+    rc = read_scalars(c, &h, st);
+    if (rc) return rc;
+  }
+  if (applied) *applied = n > 0 ? h.n_acc : 0;
+  (void)e0;
+  return FX_OK;
+}
+
+// Rank all live sketch keys by (-count, key) into ranked positions (device
+// workspace); returns the live count. Used by stage + hottest queries.
+static int rank_sketch(fx_cache *c, cudaStream_t st, int64_t *n_live, int32_t **ranked, void **tail) {
+  Scalars h;
+  int rc = read_scalars(c, &h, st);
+  if (rc) return rc;
+  const int64_t L = h.sketch_live;
+  *n_live = L;
+  if (L <= 0) return FX_OK;
+  size_t cb1 = 0, cb2 = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, cb1, (const uint64_t *)nullptr, (uint64_t *)nullptr,
+                                  (const int32_t *)nullptr, (int32_t *)nullptr, static_cast<int>(L));
+  cub::DeviceRadixSort::SortPairs(nullptr, cb2, (const long long *)nullptr, (long long *)nullptr,
+                                  (const int32_t *)nullptr, (int32_t *)nullptr, static_cast<int>(L));
+  size_t cb = cb1 > cb2 ? cb1 : cb2;
+  const size_t need = al(L * 8) * 4 + al(L * 4) * 3 + al(8) + al(cb) + al(L * 16);
+  rc = ensure_ws(c, need);
+  if (rc) return rc;
+  char *p = static_cast<char *>(c->ws);
+  uint64_t *keys = reinterpret_cast<uint64_t *>(p); p += al(L * 8);
+  uint64_t *keys2 = reinterpret_cast<uint64_t *>(p); p += al(L * 8);
+  long long *vb = reinterpret_cast<long long *>(p); p += al(L * 8);
+  long long *vb2 = reinterpret_cast<long long *>(p); p += al(L * 8);
+  int32_t *pos = reinterpret_cast<int32_t *>(p); p += al(L * 4);
+  int32_t *pos2 = reinterpret_cast<int32_t *>(p); p += al(L * 4);
+  int32_t *pos3 = reinterpret_cast<int32_t *>(p); p += al(L * 4);
+  long long *cnt = reinterpret_cast<long long *>(p); p += al(8);
+  void *tmp = p; p += al(cb);
+  cudaMemsetAsync(cnt, 0, 8, st);
+  k_sketch_collect<<<grid_for(c->v.kcap, 256), 256, 0, st>>>(c->v, keys, vb, pos, cnt);
+  // LSD: stable sort by key, then stable sort by inverted count bits
+  cub::DeviceRadixSort::SortPairs(tmp, cb, keys, keys2, pos, pos2, static_cast<int>(L), 0, 64, st);
+  k_gather_vbits<<<grid_for(L, 256), 256, 0, st>>>(c->v, pos2, L, vb);
+  cub::DeviceRadixSort::SortPairs(tmp, cb, vb, vb2, pos2, pos3, static_cast<int>(L), 0, 64, st);
+  FX_LAUNCH_CHECK("fx_cache rank sketch");
+  *ranked = pos3;
+  *tail = p;
+  return FX_OK;
+}
+
+int fx_cache_stage(fx_cache *c, int64_t limit, int64_t *staged, void *stream) {
+  cudaStream_t st = as_stream(stream);
+  Scalars h;
+  int rc = read_scalars(c, &h, st);
+  if (rc) return rc;
+  if (staged) *staged = 0;
+  if (h.budget - h.used <= 0 || h.sketch_live <= 0) return FX_OK;  // cache.py:319-320
+  int64_t L = 0;
+  int32_t *ranked = nullptr;
+  void *tail = nullptr;
+  rc = rank_sketch(c, st, &L, &ranked, &tail);
+  if (rc || L <= 0) return rc;
+  // hottest(n=limit) considers the top `limit` keys overall (cache.py:323-324)
+  const int64_t m = limit >= 0 ? (limit < L ? limit : L) : L;
+  k_stage_seq<<<1, 32, 0, st>>>(c->v, ranked, m, limit);
+  FX_LAUNCH_CHECK("fx_cache_stage");
+  rc = read_scalars(c, &h, st);
+  if (rc) return rc;
+  if (staged) *staged = h.staged;
+  return FX_OK;
+}
+
+int fx_cache_age(fx_cache *c, void *stream) {
+  cudaStream_t st = as_stream(stream);
+  k_age<<<grid_for(c->v.kcap, 256), 256, 0, st>>>(c->v);
+  FX_LAUNCH_CHECK("fx_cache_age");
+  return FX_OK;
+}
+
+int fx_cache_lookup(fx_cache *c, const uint64_t *keys, int64_t n, float *rows_out, int32_t out_ld, int32_t *slot_out,
+                    void *stream) {
+  if (n <= 0) return FX_OK;
+  k_lookup_rows<<<grid_for(n * 32, 256), 256, 0, as_stream(stream)>>>(c->v, keys, n, rows_out, out_ld, slot_out);
+  FX_LAUNCH_CHECK("fx_cache_lookup");
+  return FX_OK;
+}
+
+int fx_cache_sketch_estimate(fx_cache *c, const uint64_t *keys, int64_t n, double *out, void *stream) {
+  if (n <= 0) return FX_OK;
+  k_sketch_lookup<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(c->v, keys, n, out);
+  FX_LAUNCH_CHECK("fx_cache_sketch_estimate");
+  return FX_OK;
+}
+
+int fx_cache_sketch_bump(fx_cache *c, const uint64_t *keys, const double *weights, int64_t n, void *stream) {
+  if (n <= 0) return FX_OK;
+  k_sketch_bump<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(c->v, keys, weights, n);
+  FX_LAUNCH_CHECK("fx_cache_sketch_bump");
+  return FX_OK;
+}
+
+int fx_cache_sketch_ranked(fx_cache *c, uint64_t *keys_out, double *vals_out, int64_t cap, int64_t *n_out,
+                           void *stream) {
+  cudaStream_t st = as_stream(stream);
+  int64_t L = 0;
+  int32_t *ranked = nullptr;
+  void *tail = nullptr;
+  int rc = rank_sketch(c, st, &L, &ranked, &tail);
+  if (rc) return rc;
+  const int64_t n = L < cap ? L : cap;
+  if (n > 0) k_dump_sketch<<<grid_for(n, 256), 256, 0, st>>>(c->v, ranked, n, keys_out, vals_out);
+  *n_out = n;
+  FX_LAUNCH_CHECK("fx_cache_sketch_ranked");
+  return cuda_check(cudaStreamSynchronize(st), "fx_cache_sketch_ranked");
+}
+
+int fx_cache_lru(fx_cache *c, uint64_t *keys_out, int64_t *ticks_out, int32_t *hits_out, int64_t cap,
+                 int64_t *n_out, void *stream) {
+  cudaStream_t st = as_stream(stream);
+  Scalars h;
+  int rc = read_scalars(c, &h, st);
+  if (rc) return rc;
+  size_t cb = 0;
+  const size_t need = offer_ws_bytes(c, 0, &cb);
+  rc = ensure_ws(c, need);
+  if (rc) return rc;
+  void *cub_tmp = nullptr;
+  OfferWS w = carve_offer_ws(c, 0, &cub_tmp);
+  const int64_t S = c->v.scap;
+  k_lru_keys<<<grid_for(S, 256), 256, 0, st>>>(c->v, w);
+  cub::DeviceRadixSort::SortPairs(cub_tmp, cb, w.sort_keys_in, w.sort_keys_out, w.iota, w.lru_slot,
+                                  static_cast<int>(S), 0, 64, st);
+  const int64_t n = h.entries < cap ? h.entries : cap;
+  if (n > 0)
+    k_dump_lru<<<grid_for(n, 256), 256, 0, st>>>(c->v, w.lru_slot, n, keys_out,
+                                                  reinterpret_cast<long long *>(ticks_out), hits_out);
+  *n_out = n;
+  FX_LAUNCH_CHECK("fx_cache_lru");
+  return cuda_check(cudaStreamSynchronize(st), "fx_cache_lru");
+}
+
+int fx_cache_eviction_log(fx_cache *c, uint64_t *out, int64_t cap, int64_t *n_out, void *stream) {
+  cudaStream_t st = as_stream(stream);
+  Scalars h;
+  int rc = read_scalars(c, &h, st);
+  if (rc) return rc;
+  int64_t n = h.n_evlog < c->v.evlog_cap ? h.n_evlog : c->v.evlog_cap;
+  if (n > cap) n = cap;
+  if (n > 0) cudaMemcpyAsync(out, c->v.evlog, n * 8, cudaMemcpyDeviceToDevice, st);
+  *n_out = h.n_evlog;
+  return cuda_check(cudaStreamSynchronize(st), "fx_cache_eviction_log");
+}
+
+int fx_cache_pending(fx_cache *c, uint64_t *out, int64_t cap, int64_t *n_out, void *stream) {
+  cudaStream_t st = as_stream(stream);
+  Scalars h;
+  int rc = read_scalars(c, &h, st);
+  if (rc) return rc;
+  const int64_t n = h.pending < cap ? h.pending : cap;
+  if (n > 0) cudaMemcpyAsync(out, c->v.pend, n * 8, cudaMemcpyDeviceToDevice, st);
+  *n_out = h.pending;
+  return cuda_check(cudaStreamSynchronize(st), "fx_cache_pending");
+}
+
+}  // extern "C"
