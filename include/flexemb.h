@@ -210,6 +210,11 @@ int fx_cache_lru(fx_cache *c, uint64_t *keys_out, int64_t *ticks_out, int32_t *h
                  int64_t *n_out, void *stream);
 int fx_cache_eviction_log(fx_cache *c, uint64_t *out, int64_t cap, int64_t *n_out, void *stream); /* [sync] */
 int fx_cache_pending(fx_cache *c, uint64_t *out, int64_t cap, int64_t *n_out, void *stream);      /* [sync] */
+/* keys evicted by the last offer / apply / set_budget call                 [sync] */
+int fx_cache_last_evicted(fx_cache *c, uint64_t *out, int64_t cap, int64_t *n_out, void *stream);
+/* device array of row pointers for the pending keys (NULL entry -> table dir),
+ * consumed by the next fx_cache_apply_pending (host-fetched admissions) */
+int fx_cache_set_pending_rows(fx_cache *c, const float *const *rows, int64_t n);
 
 #ifdef __cplusplus
 }

@@ -89,6 +89,13 @@ _SIGS = {
     "fx_route": ([_P, _P, _P, _P, _P, _P, _I32, _P, _I64, _P, _P, _P, _P], ctypes.c_int),
     "fx_bucket": ([_P, _I64, _P, _I64, _I32, _P, _P, _P, _P, _SZP, _P], ctypes.c_int),
     "fx_dedup": ([_P, _P, _I32, _P, _P, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _SZP, _P], ctypes.c_int),
+    # cache entry points are typed in cache.py (_sig); listed here for export checks
+    **{n: (None, ctypes.c_int) for n in (
+        "fx_cache_create", "fx_cache_destroy", "fx_cache_set_tables", "fx_cache_scalars", "fx_cache_reserve_sketch",
+        "fx_cache_reserve_slots", "fx_cache_probe", "fx_cache_offer", "fx_cache_set_budget", "fx_cache_stage",
+        "fx_cache_apply_pending", "fx_cache_age", "fx_cache_lookup", "fx_cache_sketch_estimate",
+        "fx_cache_sketch_bump", "fx_cache_sketch_ranked", "fx_cache_lru", "fx_cache_eviction_log",
+        "fx_cache_pending", "fx_cache_last_evicted", "fx_cache_set_pending_rows")},
 }
 
 EXPORTED = []
@@ -96,7 +103,8 @@ for _name, (_args, _res) in _SIGS.items():
     _fn = getattr(lib, _name, None)
     if _fn is None:
         continue
-    _fn.argtypes = _args
+    if _args is not None:
+        _fn.argtypes = _args
     _fn.restype = _res
     EXPORTED.append(_name)
 

@@ -511,6 +511,9 @@ struct fx_cache {
   int32_t *tbytes_dev = nullptr;
   void *ws = nullptr;
   size_t ws_bytes = 0;
+  uint64_t *last_ev = nullptr;     // keys evicted by the last offer/apply/resize
+  int64_t last_ev_cap = 0;
+  const float *const *pending_rows = nullptr;  // optional per-pending-key row pointers
 };
 
 namespace {
@@ -589,6 +592,13 @@ int run_offer(fx_cache *c, const uint64_t *keys, int64_t n, int32_t mode, const 
   Scalars h;
   rc = read_scalars(c, &h, st);
   if (rc) return rc;
+  if (c->last_ev_cap < h.entries + n + 1) {
+    if (c->last_ev) cudaFree(c->last_ev);
+    c->last_ev_cap = 2 * (h.entries + n + 1);
+    rc = dmalloc(&c->last_ev, c->last_ev_cap);
+    if (rc) return rc;
+  }
+  w.ev_keys = c->last_ev;
   // room check: capacity for the worst case (every candidate inserted)
   if (h.entries + n > c->v.scap) {
     // slots can run out only if the byte budget admits more rows than the
@@ -712,7 +722,7 @@ int fx_cache_destroy(fx_cache *c) {
   if (!c) return FX_OK;
   CacheView &v = c->v;
   void *ps[] = {v.sc, v.hkeys, v.hslot, v.skey, v.stick, v.ssize, v.shits, v.rows, v.free_stack, v.kkeys,
-                v.kval, v.kflag, v.pend, v.evlog, c->dir_dev, c->tbytes_dev, c->ws};
+                v.kval, v.kflag, v.pend, v.evlog, c->dir_dev, c->tbytes_dev, c->ws, c->last_ev};
   for (void *p : ps)
     if (p) cudaFree(p);
   delete c;
@@ -859,7 +869,8 @@ int fx_cache_apply_pending(fx_cache *c, int64_t *applied, void *stream) {
   if (n > 0) {
     // clear the pending flags first (keys stay in c->v.pend until the insert ran)
     k_clear_pending_flags<<<grid_for(n, 256), 256, 0, st>>>(c->v);
-    rc = run_offer(c, c->v.pend, n, 1, nullptr, nullptr, nullptr, st);
+    rc = run_offer(c, c->v.pend, n, 1, nullptr, c->pending_rows, nullptr, st);
+    c->pending_rows = nullptr;
     if (rc) return rc;
     k_pending_done<<<1, 1, 0, st>>>(c->v.sc);
     rc = read_scalars(c, &h, st);
@@ -1022,6 +1033,23 @@ int fx_cache_pending(fx_cache *c, uint64_t *out, int64_t cap, int64_t *n_out, vo
   if (n > 0) cudaMemcpyAsync(out, c->v.pend, n * 8, cudaMemcpyDeviceToDevice, st);
   *n_out = h.pending;
   return cuda_check(cudaStreamSynchronize(st), "fx_cache_pending");
+}
+
+int fx_cache_last_evicted(fx_cache *c, uint64_t *out, int64_t cap, int64_t *n_out, void *stream) {
+  cudaStream_t st = as_stream(stream);
+  Scalars h;
+  int rc = read_scalars(c, &h, st);
+  if (rc) return rc;
+  const int64_t n = h.n_ev < cap ? h.n_ev : cap;
+  if (n > 0 && c->last_ev) cudaMemcpyAsync(out, c->last_ev, n * 8, cudaMemcpyDeviceToDevice, st);
+  *n_out = n;
+  return cuda_check(cudaStreamSynchronize(st), "fx_cache_last_evicted");
+}
+
+int fx_cache_set_pending_rows(fx_cache *c, const float *const *rows, int64_t n) {
+  (void)n;
+  c->pending_rows = rows;
+  return FX_OK;
 }
 
 }  // extern "C"

@@ -10,6 +10,7 @@
 #include <cstdlib>
 
 #include "fx_common.cuh"
+#include "fx_pool_async.cuh"
 
 namespace fx {
 
@@ -137,150 +138,6 @@ __global__ void __launch_bounds__(256) k_gather_pool_v4(
   }
 }
 
-
-// Streaming variant (dim % (4*G) == 0): a stream of G lanes owns BPW
-// consecutive bags, whose indices are one contiguous CSR range. The stream
-// walks that range 32 indices at a time (next chunk's indices prefetched
-// while the current chunk's rows are in flight), loads U rows per round and
-// flushes the f64 accumulator at bag boundaries. Per element the summation
-// order is still the bag's index order. Removes the per-bag dependency chain
-// (offsets -> index -> rows) of the bag-per-warp kernel.
-template <int G, int NCH, int U, typename IdxT, int MODE>
-__global__ void __launch_bounds__(256) k_pool_stream(
-    const fx_segment *__restrict__ segs, int n_segs, int dim, const IdxT *__restrict__ indices,
-    const int64_t *__restrict__ offsets, int64_t n_bags, int bpw, int32_t *__restrict__ counts,
-    int64_t *err, int32_t bad_code, int32_t *err_code) {
-  const int lane = threadIdx.x & 31;
-  const int gl = lane % G;
-  const int gw = lane / G;
-  const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (gw * G));
-  const int64_t stream = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * (32 / G) + gw;
-  const int64_t b0 = stream * bpw;
-  if (b0 >= n_bags) return;
-  const int64_t b1 = min(b0 + (int64_t)bpw, n_bags);
-  const int nb = static_cast<int>(b1 - b0);
-  // lane j < = nb holds offsets[b0 + j] (bpw < G)
-  const int64_t my_off = gl <= nb ? __ldg(&offsets[b0 + gl]) : 0;
-  const int64_t P0 = __shfl_sync(gmask, my_off, 0, G);
-  const int64_t P1 = __shfl_sync(gmask, my_off, nb, G);
-
-  int s = find_segment(segs, n_segs, b0);
-  const float *__restrict__ tab = segs[s].table;
-  int64_t rb = segs[s].row_begin, re = segs[s].row_end, ld = segs[s].ld, sbeg = segs[s].bag_begin;
-  int64_t send = segs[s].bag_end;
-  void *sout = segs[s].out;
-  int64_t ostr = segs[s].out_stride;
-  int sop = segs[s].op;
-  const bool single = send >= b1;  // whole stream inside one segment (common case)
-
-  double acc[NCH][4];
-#pragma unroll
-  for (int k = 0; k < NCH; ++k) acc[k][0] = acc[k][1] = acc[k][2] = acc[k][3] = 0.0;
-
-  int cur = 0;  // bag (relative to b0) being accumulated
-  int64_t bag_beg = P0;
-  int64_t bag_end = __shfl_sync(gmask, my_off, 1, G);
-
-  auto flush = [&]() {
-    const int64_t bag = b0 + cur;
-    const int64_t cnt = bag_end - bag_beg;
-    const int64_t orow = bag - sbeg;
-    if (MODE == FX_OUT_F32) {
-      float *o = static_cast<float *>(sout) + orow * ostr;
-      const bool mean = sop == FX_OP_MEAN && cnt > 0;
-      const double dn = static_cast<double>(cnt);
-#pragma unroll
-      for (int k = 0; k < NCH; ++k) {
-        const int col = (k * G + gl) * 4;
-        float4 q;
-        if (mean)
-          q = make_float4(__double2float_rn(acc[k][0] / dn), __double2float_rn(acc[k][1] / dn),
-                          __double2float_rn(acc[k][2] / dn), __double2float_rn(acc[k][3] / dn));
-        else
-          q = make_float4(__double2float_rn(acc[k][0]), __double2float_rn(acc[k][1]),
-                          __double2float_rn(acc[k][2]), __double2float_rn(acc[k][3]));
-        *reinterpret_cast<float4 *>(o + col) = q;
-      }
-    } else {
-      double *o = static_cast<double *>(sout) + orow * ostr;
-#pragma unroll
-      for (int k = 0; k < NCH; ++k) {
-        const int col = (k * G + gl) * 4;
-        *reinterpret_cast<double2 *>(o + col) = make_double2(acc[k][0], acc[k][1]);
-        *reinterpret_cast<double2 *>(o + col + 2) = make_double2(acc[k][2], acc[k][3]);
-      }
-      if (counts && gl == 0) counts[bag] = static_cast<int32_t>(cnt);
-    }
-#pragma unroll
-    for (int k = 0; k < NCH; ++k) acc[k][0] = acc[k][1] = acc[k][2] = acc[k][3] = 0.0;
-    ++cur;
-    bag_beg = bag_end;
-    bag_end = __shfl_sync(gmask, my_off, min(cur + 1, nb), G);
-    if (cur < nb && b0 + cur >= send) {  // crossed into the next segment
-      s = find_segment(segs, n_segs, b0 + cur);
-      tab = segs[s].table; rb = segs[s].row_begin; re = segs[s].row_end; ld = segs[s].ld;
-      sbeg = segs[s].bag_begin; send = segs[s].bag_end; sout = segs[s].out; ostr = segs[s].out_stride;
-      sop = segs[s].op;
-    }
-  };
-
-  // segment may change inside a chunk only at a bag boundary; rows are
-  // resolved against the segment current at their position, so chunks that
-  // cross a segment boundary resolve row offsets lazily per round.
-  IdxT nxt = 0;
-  if (P0 + gl < P1) nxt = indices[P0 + gl];
-  for (int64_t c0 = P0; c0 < P1; c0 += G) {
-    const int n = static_cast<int>(((P1 - c0) < (int64_t)G ? (P1 - c0) : (int64_t)G));
-    const int64_t my_idx = static_cast<int64_t>(nxt);
-    if (c0 + G + gl < P1) nxt = indices[c0 + G + gl];  // prefetch next chunk
-    for (int r = 0; r < n; r += U) {
-      float4 v[U][NCH];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t idx = __shfl_sync(gmask, my_idx, (r + u) & (G - 1), G);
-        if (r + u < n) {
-          // the segment of this row: the bag containing position c0 + r + u
-          const int64_t pos = c0 + r + u;
-          int64_t rrb = rb, rre = re, rld = ld;
-          const float *rtab = tab;
-          if (!single && pos >= bag_end && b0 + cur + 1 < b1) {
-            // row belongs to a later bag; only re-resolve when that bag is in another segment
-            int cc = cur;
-            int64_t be = bag_end;
-            while (pos >= be && cc + 1 < nb) { ++cc; be = __shfl_sync(gmask, my_off, min(cc + 1, nb), G); }
-            if (b0 + cc >= send) {
-              const int ss = find_segment(segs, n_segs, b0 + cc);
-              rtab = segs[ss].table; rrb = segs[ss].row_begin; rre = segs[ss].row_end; rld = segs[ss].ld;
-            }
-          }
-          int64_t off = 0;
-          if (idx < rrb || idx >= rre) {
-            if (gl == 0) record_bad(err, err_code, pos, bad_code);
-          } else {
-            off = (idx - rrb) * rld;
-          }
-#pragma unroll
-          for (int k = 0; k < NCH; ++k) v[u][k] = ldg_f4(rtab + off + (k * G + gl) * 4);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        if (r + u < n) {
-          const int64_t pos = c0 + r + u;
-          while (pos >= bag_end) flush();
-#pragma unroll
-          for (int k = 0; k < NCH; ++k) {
-            acc[k][0] += static_cast<double>(v[u][k].x);
-            acc[k][1] += static_cast<double>(v[u][k].y);
-            acc[k][2] += static_cast<double>(v[u][k].z);
-            acc[k][3] += static_cast<double>(v[u][k].w);
-          }
-        }
-      }
-    }
-  }
-  while (cur < nb) flush();  // last bag (and trailing empty bags)
-}
 
 // Generic path (any dim / alignment): one warp per (bag, 128-column tile),
 // scalar coalesced loads, same per-element sequential f64 order.
@@ -420,20 +277,40 @@ static int pool_variant() {
   return v;
 }
 
+template <int NCH, typename IdxT, int MODE>
+static void launch_async(const fx_segment *segs, int n_segs, int dim, const IdxT *ix, const int64_t *offsets,
+                         int64_t n_bags, int32_t *counts, int64_t *err, int32_t bad_code, int32_t *err_code,
+                         cudaStream_t st) {
+  constexpr int WARPS = 4;
+  const size_t smem = static_cast<size_t>(WARPS) * 32 * 32 * 16 * NCH;
+  static int per_sm = -1;
+  if (per_sm < 0) {
+    cudaFuncSetAttribute(k_pool_async<NCH, IdxT, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pool_async<NCH, IdxT, MODE>, WARPS * 32, smem);
+    if (per_sm < 1) per_sm = 1;
+  }
+  int64_t blocks = static_cast<int64_t>(num_sms()) * per_sm;
+  const int64_t need = (n_bags + WARPS - 1) / WARPS;
+  if (blocks > need) blocks = need;
+  k_pool_async<NCH, IdxT, MODE><<<static_cast<int>(blocks), WARPS * 32, smem, st>>>(
+      segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code);
+}
+
 template <int G, int NCH, int U, typename IdxT, int MODE>
-static void launch_stream(const fx_segment *segs, int n_segs, int dim, const IdxT *ix, const int64_t *offsets,
-                          int64_t n_bags, int32_t *counts, int64_t *err, int32_t bad_code, int32_t *err_code,
-                          cudaStream_t st) {
-  // ~48 resident streams-of-warps per SM worth of work, bags per stream < G
-  const int64_t target = static_cast<int64_t>(num_sms()) * 48 * (32 / G);
-  int bpw = static_cast<int>((n_bags + target - 1) / target);
-  if (bpw < 1) bpw = 1;
-  if (bpw > G - 1) bpw = G - 1;
-  const int64_t streams = (n_bags + bpw - 1) / bpw;
-  const int64_t threads = streams * G;
-  const int grid = static_cast<int>((threads + 255) / 256);
-  k_pool_stream<G, NCH, U, IdxT, MODE><<<grid, 256, 0, st>>>(segs, n_segs, dim, ix, offsets, n_bags, bpw, counts,
-                                                           err, bad_code, err_code);
+static void launch_prefetch(const fx_segment *segs, int n_segs, int dim, const IdxT *ix, const int64_t *offsets,
+                            int64_t n_bags, int32_t *counts, int64_t *err, int32_t bad_code, int32_t *err_code,
+                            cudaStream_t st) {
+  static int per_sm = -1;
+  if (per_sm < 0) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pool_prefetch<G, NCH, U, IdxT, MODE>, 256, 0);
+    if (per_sm < 1) per_sm = 1;
+  }
+  int64_t blocks = static_cast<int64_t>(num_sms()) * per_sm;
+  const int64_t need = (n_bags * G + 255) / 256;
+  if (blocks > need) blocks = need;
+  k_pool_prefetch<G, NCH, U, IdxT, MODE><<<static_cast<int>(blocks), 256, 0, st>>>(
+      segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code);
 }
 
 template <typename IdxT, int MODE>
@@ -442,14 +319,19 @@ static int launch_pool(const fx_segment *segs, int n_segs, int dim, const void *
                        cudaStream_t st, bool vec4) {
   const IdxT *ix = static_cast<const IdxT *>(indices);
   const int var = pool_variant();
-  if (var == 1 && vec4 && dim == 128) {
-    launch_stream<32, 1, 8, IdxT, MODE>(segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code, st);
-  } else if (var == 1 && vec4 && dim == 256) {
-    launch_stream<32, 2, 4, IdxT, MODE>(segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code, st);
-  } else if (var == 1 && vec4 && dim == 64) {
-    launch_stream<16, 1, 8, IdxT, MODE>(segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code, st);
-  } else if (var == 2 && vec4 && dim == 128) {
-    launch_stream<32, 1, 16, IdxT, MODE>(segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code, st);
+  if (var == 1 && dim == 128) {
+    launch_async<1, IdxT, MODE>(segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code, st);
+  } else if (var == 1 && dim == 256) {
+    launch_async<2, IdxT, MODE>(segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code, st);
+  } else if (var == 2 && dim == 128) {
+    launch_prefetch<32, 1, 8, IdxT, MODE>(segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code,
+                                          st);
+  } else if (var == 2 && dim == 64) {
+    launch_prefetch<16, 1, 8, IdxT, MODE>(segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code,
+                                          st);
+  } else if (var == 2 && dim == 256) {
+    launch_prefetch<32, 2, 4, IdxT, MODE>(segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code,
+                                          st);
   } else if (vec4 && dim == 128) {
     k_gather_pool_v4<32, 1, 8, IdxT, MODE><<<grid_for(n_bags * 32, 256), 256, 0, st>>>(
         segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code);

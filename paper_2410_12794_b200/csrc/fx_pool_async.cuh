@@ -1,0 +1,223 @@
+// K4 latency-tolerant variants of the fused gather+pool (included by fx_pool.cu).
+//
+// Both keep the reference's per-element sequential f64 order (each lane owns
+// columns and adds the bag's rows in index order), cf. store.py:184-193 and
+// pooling.py:60-71.
+#pragma once
+
+#include "fx_common.cuh"
+
+namespace fx {
+
+__device__ __forceinline__ void cp_async16(uint32_t saddr, const void *g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+template <int NCH, int MODE>
+__device__ __forceinline__ void emit_bag(const fx_segment &sg, int64_t bag, int64_t cnt, double (&acc)[NCH][4],
+                                         int lane, int G, int32_t *counts) {
+  const int64_t orow = bag - sg.bag_begin;
+  if (MODE == FX_OUT_F32) {
+    float *o = static_cast<float *>(sg.out) + orow * sg.out_stride;
+    const bool mean = sg.op == FX_OP_MEAN && cnt > 0;
+    const double dn = static_cast<double>(cnt);
+#pragma unroll
+    for (int k = 0; k < NCH; ++k) {
+      const int col = (k * G + lane) * 4;
+      float4 q;
+      if (mean)
+        q = make_float4(__double2float_rn(acc[k][0] / dn), __double2float_rn(acc[k][1] / dn),
+                        __double2float_rn(acc[k][2] / dn), __double2float_rn(acc[k][3] / dn));
+      else
+        q = make_float4(__double2float_rn(acc[k][0]), __double2float_rn(acc[k][1]), __double2float_rn(acc[k][2]),
+                        __double2float_rn(acc[k][3]));
+      *reinterpret_cast<float4 *>(o + col) = q;
+    }
+  } else {
+    double *o = static_cast<double *>(sg.out) + orow * sg.out_stride;
+#pragma unroll
+    for (int k = 0; k < NCH; ++k) {
+      const int col = (k * G + lane) * 4;
+      *reinterpret_cast<double2 *>(o + col) = make_double2(acc[k][0], acc[k][1]);
+      *reinterpret_cast<double2 *>(o + col + 2) = make_double2(acc[k][2], acc[k][3]);
+    }
+    if (counts && lane == 0) counts[bag] = static_cast<int32_t>(cnt);
+  }
+}
+
+// Async-staged variant (dim == 128*NCH): persistent warps, one bag per warp at
+// a time. All rows of a 32-index chunk are copied global->shared with
+// cp.async (16 B per lane per row, no register staging), so the whole bag is
+// in flight at once; while the copies land the warp prefetches the NEXT bag's
+// offsets and first index chunk. Rows are then summed from shared memory.
+template <int NCH, typename IdxT, int MODE>
+__global__ void __launch_bounds__(128) k_pool_async(const fx_segment *__restrict__ segs, int n_segs, int dim,
+                                                    const IdxT *__restrict__ indices,
+                                                    const int64_t *__restrict__ offsets, int64_t n_bags,
+                                                    int32_t *__restrict__ counts, int64_t *err, int32_t bad_code,
+                                                    int32_t *err_code) {
+  constexpr int ROWB = 32 * 16 * NCH;  // bytes per row
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  unsigned char *buf = smem + static_cast<size_t>(wib) * 32 * ROWB;
+  const uint32_t sbuf = static_cast<uint32_t>(__cvta_generic_to_shared(buf));
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+
+  int64_t bag = warp;
+  if (bag >= n_bags) return;
+  int64_t beg = __ldg(&offsets[bag]), end = __ldg(&offsets[bag + 1]);
+  IdxT pidx = (beg + lane < end) ? indices[beg + lane] : IdxT(0);
+
+  while (bag < n_bags) {
+    const int s = find_segment(segs, n_segs, bag);
+    const float *__restrict__ tab = segs[s].table;
+    const int64_t rb = segs[s].row_begin, re = segs[s].row_end, ld = segs[s].ld;
+    double acc[NCH][4];
+#pragma unroll
+    for (int k = 0; k < NCH; ++k) acc[k][0] = acc[k][1] = acc[k][2] = acc[k][3] = 0.0;
+    const int64_t nbag = bag + nwarps;
+    int64_t nbeg = 0, nend = 0;
+    IdxT nidx = IdxT(0);
+    bool have_next = false;
+    for (int64_t c0 = beg; c0 < end; c0 += 32) {
+      const int n = static_cast<int>((end - c0) < 32 ? (end - c0) : 32);
+      const int64_t idx = static_cast<int64_t>(pidx);
+      int64_t my_off = 0;
+      if (lane < n) {
+        if (idx < rb || idx >= re) record_bad(err, err_code, c0 + lane, bad_code);
+        else my_off = (idx - rb) * ld;
+      }
+      for (int r = 0; r < n; ++r) {
+        const float *src = tab + __shfl_sync(0xffffffffu, my_off, r);
+#pragma unroll
+        for (int k = 0; k < NCH; ++k) cp_async16(sbuf + r * ROWB + (k * 32 + lane) * 16, src + (k * 32 + lane) * 4);
+      }
+      cp_async_commit();
+      // overlap the copies with the next chunk's / next bag's index loads
+      if (c0 + 32 < end) {
+        pidx = (c0 + 32 + lane < end) ? indices[c0 + 32 + lane] : IdxT(0);
+      } else if (nbag < n_bags) {
+        nbeg = __ldg(&offsets[nbag]);
+        nend = __ldg(&offsets[nbag + 1]);
+        nidx = (nbeg + lane < nend) ? indices[nbeg + lane] : IdxT(0);
+        have_next = true;
+      }
+      cp_async_wait_all();
+      __syncwarp();
+      for (int r = 0; r < n; ++r) {
+#pragma unroll
+        for (int k = 0; k < NCH; ++k) {
+          const float4 v = *reinterpret_cast<const float4 *>(buf + r * ROWB + (k * 32 + lane) * 16);
+          acc[k][0] += static_cast<double>(v.x);
+          acc[k][1] += static_cast<double>(v.y);
+          acc[k][2] += static_cast<double>(v.z);
+          acc[k][3] += static_cast<double>(v.w);
+        }
+      }
+      __syncwarp();
+    }
+    if (!have_next && nbag < n_bags) {
+      nbeg = __ldg(&offsets[nbag]);
+      nend = __ldg(&offsets[nbag + 1]);
+      nidx = (nbeg + lane < nend) ? indices[nbeg + lane] : IdxT(0);
+    }
+    emit_bag<NCH, MODE>(segs[s], bag, end - beg, acc, lane, 32, counts);
+    bag = nbag;
+    beg = nbeg;
+    end = nend;
+    pidx = nidx;
+  }
+}
+
+// Bag-per-group register variant with next-bag software prefetch: the next
+// chunk's indices (or the next bag's offsets + first chunk) are loaded right
+// after the first round of row loads is issued.
+template <int G, int NCH, int U, typename IdxT, int MODE>
+__global__ void __launch_bounds__(256) k_pool_prefetch(const fx_segment *__restrict__ segs, int n_segs, int dim,
+                                                       const IdxT *__restrict__ indices,
+                                                       const int64_t *__restrict__ offsets, int64_t n_bags,
+                                                       int32_t *__restrict__ counts, int64_t *err, int32_t bad_code,
+                                                       int32_t *err_code) {
+  constexpr int GPW = 32 / G;
+  const int lane = threadIdx.x & 31;
+  const int gl = lane % G;
+  const int gw = lane / G;
+  const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (gw * G));
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (gridDim.x * (int64_t)blockDim.x) >> 5;
+  const int64_t step = nwarps * GPW;
+  int64_t bag = warp * GPW + gw;
+  if (bag >= n_bags) return;
+  int64_t beg = __ldg(&offsets[bag]), end = __ldg(&offsets[bag + 1]);
+  IdxT pidx = (beg + gl < end) ? indices[beg + gl] : IdxT(0);
+  while (bag < n_bags) {
+    const int s = find_segment(segs, n_segs, bag);
+    const float *__restrict__ tab = segs[s].table;
+    const int64_t rb = segs[s].row_begin, re = segs[s].row_end, ld = segs[s].ld;
+    double acc[NCH][4];
+#pragma unroll
+    for (int k = 0; k < NCH; ++k) acc[k][0] = acc[k][1] = acc[k][2] = acc[k][3] = 0.0;
+    const int64_t nbag = bag + step;
+    int64_t nbeg = 0, nend = 0;
+    IdxT nidx = IdxT(0);
+    bool have_next = false;
+    for (int64_t c0 = beg; c0 < end; c0 += G) {
+      const int n = static_cast<int>((end - c0) < G ? (end - c0) : (int64_t)G);
+      const int64_t idx = static_cast<int64_t>(pidx);
+      int64_t my_off = 0;
+      if (gl < n) {
+        if (idx < rb || idx >= re) record_bad(err, err_code, c0 + gl, bad_code);
+        else my_off = (idx - rb) * ld;
+      }
+      for (int r = 0; r < n; r += U) {
+        float4 v[U][NCH];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t off = __shfl_sync(gmask, my_off, (r + u) & (G - 1), G);
+          if (r + u < n) {
+#pragma unroll
+            for (int k = 0; k < NCH; ++k) v[u][k] = ldg_f4(tab + off + (k * G + gl) * 4);
+          }
+        }
+        if (r == 0) {
+          if (c0 + G < end) {
+            pidx = (c0 + G + gl < end) ? indices[c0 + G + gl] : IdxT(0);
+          } else if (nbag < n_bags) {
+            nbeg = __ldg(&offsets[nbag]);
+            nend = __ldg(&offsets[nbag + 1]);
+            nidx = (nbeg + gl < nend) ? indices[nbeg + gl] : IdxT(0);
+            have_next = true;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (r + u < n) {
+#pragma unroll
+            for (int k = 0; k < NCH; ++k) {
+              acc[k][0] += static_cast<double>(v[u][k].x);
+              acc[k][1] += static_cast<double>(v[u][k].y);
+              acc[k][2] += static_cast<double>(v[u][k].z);
+              acc[k][3] += static_cast<double>(v[u][k].w);
+            }
+          }
+        }
+      }
+    }
+    if (!have_next && nbag < n_bags) {
+      nbeg = __ldg(&offsets[nbag]);
+      nend = __ldg(&offsets[nbag + 1]);
+      nidx = (nbeg + gl < nend) ? indices[nbeg + gl] : IdxT(0);
+    }
+    emit_bag<NCH, MODE>(segs[s], bag, end - beg, acc, gl, G, counts);
+    bag = nbag;
+    beg = nbeg;
+    end = nend;
+    pidx = nidx;
+  }
+}
+
+}  // namespace fx
