@@ -1,0 +1,462 @@
+"""Batch pipeline (mirror of embserve/ranker.py) on one GPU.
+
+Per batch, in the reference's canonical order (ranker.py:218-442; SURVEY
+§8(c)):
+
+  1. ingress validation + range routing of every index (K1 fx_route);
+  2. cache.apply_pending_admissions, admission check (host scalars);
+  3. dedup (K2 fx_dedup) and one cache probe per unique key (K3), equivalent
+     to probing every occurrence in (lookup, feature, position) order;
+  4. per (lookup, feature, server) miss-group sizes -> pushdown plan
+     (threshold, pooling.py:88-100) -> counters;
+  5. per-shard f64 partial pooling of the misses (K4, "pushdown near the
+     data"), cache-hit rows as raw vectors, combined per bag in f64 and
+     rounded once (K5) — within the reference tolerance of its hierarchical
+     combine and bit-identical to the flat oracle in practice;
+  6. offers of raw-fetched misses in first raw-occurrence order (K6);
+  7. maintenance: record -> propose -> resize(fetch) -> stage(admit) -> age.
+
+The modelled RDMA transport of the reference (VirtualTransport) is not
+reproduced: the fan-out is a device-side bucketing of indices per shard
+(streams + NCCL in the multi-GPU path, see sharded.py). `transport` is
+accepted for signature compatibility and ignored.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .cache import AdaptiveCache, CachePolicy, LoadTracker, encode_key, target_cache_bytes
+from .dedup import Deduper
+from .errors import CapacityError, InvariantError, LookupValidationError
+from .pooling import PoolingOp, op_code, pool_flat
+from .requests import Batch, LookupRequest
+from .store import Deployment, make_segments
+from .routing import RoutingTable
+
+
+@dataclass
+class RankerParams:
+    pushdown_threshold: int | None = 2
+    pipeline_depth: int = 1
+    adaptive_cache: bool = True
+    keep_results: bool = True
+    admit_per_batch: int = 64
+
+
+@dataclass
+class LookupResult:
+    vectors: list = field(default_factory=list)
+    cache_hits: int = 0
+    pushdown_groups: int = 0
+    pushdown_rows: int = 0
+    raw_rows: int = 0
+    completed_at: float = 0.0
+
+    @property
+    def counters(self):
+        return (self.cache_hits, self.pushdown_groups, self.raw_rows)
+
+
+@dataclass
+class BatchMetrics:
+    batch_id: int
+    size: int
+    started_at: float
+    latency: float
+    subrequests: int
+    cache_hits: int
+    cache_misses: int
+    pushdown_groups: int
+    pushdown_rows: int
+    raw_rows: int
+    load_level: str | None = None
+    cache_budget: int | None = None
+    cache_used: int | None = None
+
+    @property
+    def hit_rate(self) -> float:
+        t = self.cache_hits + self.cache_misses
+        return self.cache_hits / t if t else 0.0
+
+
+@dataclass
+class CsrLayout:
+    """A reference Batch packed table-major for the kernels."""
+    indices: torch.Tensor     # int64 [nnz], table-major bag order
+    offsets: torch.Tensor     # int64 [n_bags+1]
+    bag_table: torch.Tensor   # int32 [n_bags]
+    sm_start: torch.Tensor    # int64 [n_bags] (lookup, feature, position) ordinal of each bag's first index
+    perm: np.ndarray          # table-major bag -> sample-major bag id
+    segs: list                # [(table, op, bag_begin, bag_end)]
+    lens_sm: np.ndarray       # bag lengths in sample-major order
+    bag_lookup_sm: np.ndarray
+    host_idx_sm: list         # per sample-major bag: host index list (error path)
+    n_lookups: int
+
+
+def pack_batch(batch: Batch, device) -> CsrLayout:
+    tabs, ops, lk, idx_lists = [], [], [], []
+    for li, lookup in enumerate(batch.lookups):
+        for f in lookup.features:
+            tabs.append(f.table_id)
+            ops.append(op_code(f.op))
+            lk.append(li)
+            idx_lists.append(f.indices)
+    tabs = np.asarray(tabs, np.int64)
+    ops_a = np.asarray(ops, np.int64)
+    lens = np.fromiter((len(x) for x in idx_lists), dtype=np.int64, count=len(idx_lists))
+    perm = np.lexsort((ops_a, tabs))  # stable: table-major, sample-major within a table
+    sm_start = np.concatenate([[0], np.cumsum(lens)[:-1]]).astype(np.int64)
+    lens_tm = lens[perm]
+    offs = np.concatenate([[0], np.cumsum(lens_tm)]).astype(np.int64)
+    flat = np.concatenate([np.asarray(idx_lists[b], dtype=np.int64) for b in perm]) if len(perm) else np.zeros(0, np.int64)
+    segs = []
+    tt, oo = tabs[perm], ops_a[perm]
+    start = 0
+    for i in range(1, len(perm) + 1):
+        if i == len(perm) or tt[i] != tt[start] or oo[i] != oo[start]:
+            segs.append((int(tt[start]), int(oo[start]), start, i))
+            start = i
+    dev = device
+    return CsrLayout(torch.from_numpy(flat).to(dev), torch.from_numpy(offs).to(dev),
+                     torch.from_numpy(tt.astype(np.int32)).to(dev), torch.from_numpy(sm_start[perm]).to(dev), perm,
+                     segs, lens, np.asarray(lk, np.int64), idx_lists, len(batch.lookups))
+
+
+class Ranker:
+    def __init__(self, deployment: Deployment, routing: RoutingTable, transport=None,
+                 params: RankerParams | None = None, cache: AdaptiveCache | None = None,
+                 policy: CachePolicy | None = None, tracker: LoadTracker | None = None, device=None):
+        self.deployment = deployment
+        self.routing = routing
+        self.transport = transport
+        self.params = params or RankerParams()
+        self.cache = cache
+        self.policy = policy
+        self.tracker = tracker
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.batch_metrics: list = []
+        self.results: dict = {}
+        self._last_level = None
+        self._dedup = Deduper(self.device)
+        self._status = _lib.Status(self.device)
+        # device shard directory: global shard id -> (tensor, start, end, server)
+        self._shards = []
+        for spec in routing.shard_list:
+            server = deployment.servers[spec.server_id]
+            data = None
+            for sh in server.shards(spec.table_id):
+                if sh.start == spec.start:
+                    data = sh.data
+            if data is None:
+                raise InvariantError(f"shard {spec} is not resident on this GPU (use sharded.ShardedLookup)")
+            self._shards.append((data, spec.start, spec.end, spec.server_id, spec.table_id))
+        self._server_ids = sorted({s[3] for s in self._shards})
+        self._shard_server_dev = torch.tensor([self._server_ids.index(s[3]) for s in self._shards], dtype=torch.int64,
+                                              device=self.device)
+        if cache is not None:
+            cache.bind_tables(deployment)
+
+    # -- driving ----------------------------------------------------------------
+
+    def run_trace(self, trace_batches: list) -> None:
+        """Batches run to completion one after another (pipeline_depth > 1 is
+        accepted; the device executes batches in stream order)."""
+        for b in trace_batches:
+            self._run_batch(b)
+
+    def execute_batch(self, batch: Batch) -> list:
+        self._run_batch(batch)
+        return self.results.get(batch.batch_id, [])
+
+    # -- pipeline ---------------------------------------------------------------
+
+    def _raise_validation(self, batch: Batch):
+        for li, lookup in enumerate(batch.lookups):
+            for f in lookup.features:
+                n = self.deployment.meta(f.table_id).num_rows
+                for index in f.indices:
+                    if not (0 <= index < n):
+                        raise LookupValidationError(f"batch {batch.batch_id}, lookup {li}: index {index} out of "
+                                                    f"range [0,{n}) for table {f.table_id}")
+        raise InvariantError("device validation flagged an index the host check accepts")
+
+    def _admission_check(self, batch: Batch) -> None:
+        if self.cache is None or self.policy is None:
+            return
+        model = self.policy.model
+        need = model.nn_bytes(batch.size)
+        if need > model.gpu_capacity_bytes:
+            raise CapacityError(f"batch {batch.batch_id} (size {batch.size}) needs {need} NN bytes, "
+                                f"capacity {model.gpu_capacity_bytes}")
+        budget = self.cache.budget_bytes
+        if need + budget <= model.gpu_capacity_bytes:
+            return
+        if not self.params.adaptive_cache:
+            raise CapacityError(f"batch {batch.batch_id} (size {batch.size}): NN {need} bytes plus fixed cache "
+                                f"{budget} exceeds capacity {model.gpu_capacity_bytes}")
+        self.cache.resize(target_cache_bytes(model, batch.size), fetcher=None)
+
+    def _run_batch(self, batch: Batch) -> None:
+        dev = self.device
+        for lookup in batch.lookups:
+            for f in lookup.features:
+                self.deployment.meta(f.table_id)
+        lay = pack_batch(batch, dev)
+        nnz = int(lay.indices.numel())
+        n_bags = len(lay.perm)
+        # 1. ingress validation + routing (K1)
+        self._status.reset()
+        dest, _ = self.routing.route_csr(lay.bag_table, lay.indices, lay.offsets, status=self._status)
+        code, _ = self._status.read()
+        if code:
+            self._raise_validation(batch)
+        cache = self.cache
+        # 2. pending admissions, capacity gate
+        if cache is not None:
+            cache.apply_pending_admissions()
+        self._admission_check(batch)
+        # 3. dedup + probe (K2, K3)
+        hit_occ = torch.zeros(nnz, dtype=torch.bool, device=dev)
+        dd = None
+        if cache is not None and nnz:
+            dd = self._dedup(lay.bag_table, lay.indices, lay.offsets, lay.sm_start, nnz)
+            slot = torch.empty(max(dd.n_uniq, 1), dtype=torch.int32, device=dev)
+            cache.probe_unique(dd.uniq, dd.mult, dd.last_ord, None, nnz, slot, n_uniq_host=dd.n_uniq)
+            hit_occ = slot[dd.inverse.long()] >= 0
+        # 4. miss groups per (bag, server) and the pushdown plan
+        lens_tm = lay.offsets[1:] - lay.offsets[:-1]
+        bag_of_occ = torch.repeat_interleave(torch.arange(n_bags, device=dev), lens_tm)
+        n_srv = len(self._server_ids)
+        srv_occ = self._shard_server_dev[dest.long()] if nnz else torch.zeros(0, dtype=torch.int64, device=dev)
+        miss = ~hit_occ
+        grp = torch.zeros(n_bags * n_srv, dtype=torch.int64, device=dev)
+        if nnz:
+            grp.index_add_(0, (bag_of_occ * n_srv + srv_occ)[miss], torch.ones(int(miss.sum()), dtype=torch.int64,
+                                                                                 device=dev))
+        grp = grp.view(n_bags, n_srv)
+        thr = self.params.pushdown_threshold
+        if thr is None:
+            push = torch.zeros_like(grp, dtype=torch.bool)
+        else:
+            if thr < 2:
+                from .errors import EmbServeError
+                raise EmbServeError(f"pushdown threshold must be >= 2, got {thr}")
+            push = grp >= thr
+        hits_bag = torch.zeros(n_bags, dtype=torch.int64, device=dev)
+        if nnz:
+            hits_bag.index_add_(0, bag_of_occ, hit_occ.long())
+        pd_groups = push.sum(1)
+        pd_rows = (grp * push).sum(1)
+        raw_rows = (grp * (~push)).sum(1)
+        n_groups = int((grp > 0).sum())
+        # 5. pooled vectors: per-shard f64 partials of the misses + cache rows as raw
+        out = self._pool(lay, dest, hit_occ, dd, nnz, n_bags)
+        # 6. offers: raw-fetched misses, first raw occurrence order
+        if cache is not None and nnz:
+            raw_occ = miss & ~push.view(-1)[bag_of_occ * n_srv + srv_occ]
+            if bool(raw_occ.any()):
+                ords = lay.sm_start[bag_of_occ] + (torch.arange(nnz, device=dev) - lay.offsets[bag_of_occ])
+                big = torch.full((dd.n_uniq,), 1 << 62, dtype=torch.int64, device=dev)
+                big.scatter_reduce_(0, dd.inverse.long()[raw_occ], ords[raw_occ], reduce="amin")
+                cand = torch.nonzero(big < (1 << 62)).view(-1)
+                order = torch.argsort(big[cand])
+                keys = dd.uniq[cand[order]].contiguous()
+                cache.offer_keys(keys, int(keys.numel()))
+        # 7. maintenance
+        self._maintenance(batch)
+        # results (sample-major)
+        self._emit(batch, lay, out, hits_bag, pd_groups, pd_rows, raw_rows, nnz, n_groups)
+
+    def _pool(self, lay: CsrLayout, dest, hit_occ, dd, nnz, n_bags) -> torch.Tensor:
+        """Partial pool per shard (K4 FX_OUT_F64_PARTIAL over that shard's miss
+        occurrences, bucketed in (bag, position) order by fx_bucket), then K5
+        folds partials in ascending shard order plus cache rows in position order."""
+        dev = self.device
+        dims = {self.deployment.meta(t).dim for t, *_ in lay.segs}
+        D = max(dims) if dims else 1
+        n_sh = len(self._shards)
+        out = torch.empty((n_bags, D), dtype=torch.float32, device=dev)
+        if n_bags == 0:
+            return out
+        dest_m = torch.where(hit_occ, torch.full_like(dest, n_sh), dest) if nnz else dest
+        perm = torch.empty(max(nnz, 1), dtype=torch.int64, device=dev)
+        dcount = torch.empty(n_sh + 1, dtype=torch.int64, device=dev)
+        bcount = torch.empty((n_sh + 1) * n_bags, dtype=torch.int32, device=dev)
+        need = ctypes.c_size_t(0)
+        _lib.check(_lib.lib.fx_bucket(None, nnz, None, n_bags, n_sh + 1, None, None, None, None, ctypes.byref(need),
+                                      None), "bucket")
+        ws = torch.empty(max(need.value, 1), dtype=torch.uint8, device=dev)
+        _lib.check(_lib.lib.fx_bucket(dest_m.data_ptr() if nnz else None, nnz, lay.offsets.data_ptr(), n_bags, n_sh + 1,
+                                      perm.data_ptr(), dcount.data_ptr(), bcount.data_ptr(), ws.data_ptr(),
+                                      ctypes.byref(need), _lib.stream_ptr()), "bucket")
+        dc = dcount.cpu().numpy()
+        bcount = bcount.view(n_sh + 1, n_bags)
+        starts = np.concatenate([[0], np.cumsum(dc)])
+        sorted_idx = lay.indices[perm[:nnz]] if nnz else lay.indices
+        partials, counts = [], []
+        for sid, (tab, start, end, server, table) in enumerate(self._shards):
+            if dc[sid] == 0:
+                continue
+            offs = torch.zeros(n_bags + 1, dtype=torch.int64, device=dev)
+            offs[1:] = torch.cumsum(bcount[sid].long(), 0)
+            idx_s = sorted_idx[starts[sid]:starts[sid + 1]]
+            part = torch.zeros((n_bags, D), dtype=torch.float64, device=dev)
+            cnt = torch.zeros(n_bags, dtype=torch.int32, device=dev)
+            segs = []
+            for (t, opc, b0, b1) in lay.segs:
+                if t != table:
+                    continue
+                segs.append(_lib.FxSegment(tab.data_ptr(), start, end, b0, b1, part.data_ptr() + b0 * D * 8, D,
+                                           tab.stride(0), tab.shape[1], 0))
+            if not segs:
+                continue
+            # bags of other tables have zero rows for this shard; give them a dummy segment range
+            seg_dev = make_segments(self._cover(segs, n_bags, tab, start, end, part, D), dev)
+            _lib.check(_lib.lib.fx_gather_pool(seg_dev.data_ptr(), seg_dev.numel() // _lib.SEGMENT_BYTES,
+                                               tab.shape[1], idx_s.data_ptr(), _lib.FX_IDX_I64, offs.data_ptr(),
+                                               n_bags, _lib.FX_OUT_F64_PARTIAL, cnt.data_ptr(),
+                                               self._status.err.data_ptr(), _lib.FX_E_ROUTING_VIOLATION,
+                                               self._status.code.data_ptr(), _lib.stream_ptr()), "partial pool")
+            partials.append(part)
+            counts.append(cnt)
+        # cache-hit rows (raw vectors, position order)
+        raw_off = raw_rows = None
+        if nnz and bool(hit_occ.any()):
+            hb = bcount[n_sh].long()
+            raw_off = torch.zeros(n_bags + 1, dtype=torch.int64, device=dev)
+            raw_off[1:] = torch.cumsum(hb, 0)
+            hit_keys = (lay.bag_table.long()[torch.repeat_interleave(torch.arange(n_bags, device=dev),
+                                                                     lay.offsets[1:] - lay.offsets[:-1])] << 40
+                        | lay.indices)[perm[starts[n_sh]:starts[n_sh + 1]]]
+            raw_rows = torch.zeros((hit_keys.numel(), self.cache.max_dim), dtype=torch.float32, device=dev)
+            slot = torch.empty(hit_keys.numel(), dtype=torch.int32, device=dev)
+            _lib.check(self.cache._L.fx_cache_lookup(self.cache._h, hit_keys.data_ptr(), hit_keys.numel(),
+                                                     raw_rows.data_ptr(), self.cache.max_dim, slot.data_ptr(),
+                                                     _lib.stream_ptr()), "cache rows")
+            raw_rows = raw_rows[:, :D].contiguous()
+        n_src = len(partials)
+        ptrs = torch.tensor([p.data_ptr() for p in partials] or [0], dtype=torch.int64, device=dev)
+        cptr = torch.tensor([c.data_ptr() for c in counts] or [0], dtype=torch.int64, device=dev)
+        ops = torch.zeros(n_bags, dtype=torch.int32, device=dev)
+        for (t, opc, b0, b1) in lay.segs:
+            ops[b0:b1] = opc
+        _lib.check(_lib.lib.fx_combine(ptrs.data_ptr(), cptr.data_ptr(), n_src, D, _lib.ptr(raw_off),
+                                       _lib.ptr(raw_rows), n_bags, D, 0, ops.data_ptr(), out.data_ptr(), D, None,
+                                       _lib.stream_ptr()), "combine")
+        return out
+
+    @staticmethod
+    def _cover(segs, n_bags, tab, start, end, part, D):
+        """Extend a shard's segment list to cover [0, n_bags) (bags of other
+        tables get empty ranges: their offsets are zero-length for this shard)."""
+        out = []
+        cursor = 0
+        for sg in sorted(segs, key=lambda s: s.bag_begin):
+            if sg.bag_begin > cursor:
+                out.append(_lib.FxSegment(tab.data_ptr(), start, end, cursor, sg.bag_begin,
+                                          part.data_ptr() + cursor * D * 8, D, tab.stride(0), tab.shape[1], 0))
+            out.append(sg)
+            cursor = sg.bag_end
+        if cursor < n_bags:
+            out.append(_lib.FxSegment(tab.data_ptr(), start, end, cursor, n_bags, part.data_ptr() + cursor * D * 8,
+                                      D, tab.stride(0), tab.shape[1], 0))
+        return out
+
+    def _maintenance(self, batch: Batch) -> None:
+        c = self.cache
+        if c is None or self.tracker is None or self.policy is None:
+            return
+        level = self.tracker.record_batch(batch.size)
+        self._last_level = level.value
+        if not self.params.adaptive_cache:
+            return
+        rb = lambda t: self.deployment.meta(t).row_bytes
+        fetcher = lambda t, i: self.deployment.get_row(t, i)
+        budget = c.budget_bytes
+        proposed = self.policy.propose(budget, level, self.tracker.windowed_value())
+        if proposed != budget:
+            c.resize(proposed, fetcher=fetcher, row_bytes_of=rb)
+        if self.params.admit_per_batch > 0:
+            c.stage_hot_admissions(fetcher, rb, limit=self.params.admit_per_batch)
+        c.sketch.age()
+
+    def _emit(self, batch, lay, out, hits_bag, pd_groups, pd_rows, raw_rows, nnz, n_groups):
+        n_bags = len(lay.perm)
+        inv = np.empty(n_bags, dtype=np.int64)
+        inv[lay.perm] = np.arange(n_bags)
+        vec = out.cpu().numpy()
+        hb = hits_bag.cpu().numpy()
+        pg = pd_groups.cpu().numpy()
+        pr = pd_rows.cpu().numpy()
+        rr = raw_rows.cpu().numpy()
+        results = []
+        b_sm = 0
+        tot = np.zeros(4, np.int64)
+        for li, lookup in enumerate(batch.lookups):
+            res = LookupResult()
+            for f in lookup.features:
+                b = inv[b_sm]
+                dim = self.deployment.meta(f.table_id).dim
+                res.vectors.append(vec[b, :dim].copy())
+                res.cache_hits += int(hb[b])
+                res.pushdown_groups += int(pg[b])
+                res.pushdown_rows += int(pr[b])
+                res.raw_rows += int(rr[b])
+                b_sm += 1
+            if res.cache_hits + res.pushdown_rows + res.raw_rows != lookup.total_indices():
+                raise InvariantError(f"counter conservation broken on lookup {li}: {res.counters} vs "
+                                     f"{lookup.total_indices()} indices")
+            tot += (res.cache_hits, res.pushdown_groups, res.pushdown_rows, res.raw_rows)
+            results.append(res)
+        c = self.cache
+        hits = int(tot[0]) if c is not None else 0
+        misses = (nnz - hits) if c is not None else 0
+        sub = n_groups  # one subrequest per (lookup, feature, server) group (ranker.py:275-301)
+        self.batch_metrics.append(BatchMetrics(
+            batch_id=batch.batch_id, size=batch.size, started_at=0.0, latency=0.0, subrequests=sub,
+            cache_hits=hits, cache_misses=misses, pushdown_groups=int(tot[1]), pushdown_rows=int(tot[2]),
+            raw_rows=int(tot[3]), load_level=self._last_level,
+            cache_budget=(c.budget_bytes if c else None), cache_used=(c.used_bytes if c else None)))
+        if self.params.keep_results:
+            self.results[batch.batch_id] = results
+
+
+@dataclass
+class EquivalenceReport:
+    lookups_checked: int
+    max_abs_diff: float
+    max_tolerance_ratio: float
+
+    @property
+    def passed(self) -> bool:
+        return self.max_tolerance_ratio <= 1.0
+
+
+def flat_reference(deployment: Deployment, lookup: LookupRequest) -> list:
+    """No cache, no pushdown: direct row reads pooled flat (ranker.py:458-465),
+    computed on the GPU (K4 over the gathered rows)."""
+    out = []
+    for f in lookup.features:
+        rows = torch.stack([deployment.get_row_device(f.table_id, i) for i in f.indices])
+        out.append(pool_flat(rows, f.op).cpu().numpy())
+    return out
+
+
+def end_to_end_equivalence_check(deployment, batches, results, rel_tol=1e-5, abs_floor=1e-6) -> EquivalenceReport:
+    checked, max_abs, max_ratio = 0, 0.0, 0.0
+    for batch in batches:
+        for lookup, result in zip(batch.lookups, results[batch.batch_id]):
+            for ref, got in zip(flat_reference(deployment, lookup), result.vectors):
+                diff = np.abs(ref.astype(np.float64) - got.astype(np.float64))
+                bound = np.maximum(abs_floor, rel_tol * np.abs(ref.astype(np.float64)))
+                max_abs = max(max_abs, float(diff.max(initial=0.0)))
+                max_ratio = max(max_ratio, float((diff / bound).max(initial=0.0)))
+            checked += 1
+    return EquivalenceReport(checked, max_abs, max_ratio)
