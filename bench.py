@@ -193,6 +193,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--alpha", type=float, default=None, help="override Zipf alpha (0 = uniform cold control)")
     ap.add_argument("--table-rows", type=int, default=None, help="override every table's row count (cold control)")
+    ap.add_argument("--mode", default="tablewise", choices=["tablewise", "rowwise"], help="N>1 sharding")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -207,6 +208,8 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2410_12794_b200 as P
     from paper_2410_12794_b200.engine import CsrBatch, HostLookup, LookupEngine
+    if world > 1:
+        return run_sharded(args, rank, world, local)
 
     cfg, host_batches = build_cfg(args.config, rank, args.batches, args.alpha, args.table_rows)
     dim = cfg["dim"]
@@ -327,6 +330,126 @@ def main():
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def run_sharded(args, rank, world, local):
+    """N>1: the cfg2 tables sharded across the ranks (table-wise by default,
+    SURVEY §8(e) cfg4 pattern; --mode rowwise for the cfg5 pattern), every
+    rank a requester with its own 4096-sample batch stream (weak scaling).
+    A step = route/bucket (K1) -> index all-to-all (C1) -> owner gather+pool
+    (K4) -> pooled all-to-all (C2) -> placement / combine (K5)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2410_12794_b200.sharded import ShardedLookup, rowwise_placement, tablewise_placement
+    from paper_2410_12794_b200.store import TableMeta
+    cfg, host_batches = build_cfg(args.config, rank, args.batches, args.alpha, args.table_rows)
+    rows, dim, B = cfg["table_rows"], cfg["dim"], cfg["batch"]
+    F = len(rows)
+    mode = args.mode
+    placement = (tablewise_placement if mode == "tablewise" else rowwise_placement)(rows, world)
+    metas = [TableMeta(t, n, dim) for t, n in enumerate(rows)]
+    dev = torch.device("cuda", local)
+    t0 = time.perf_counter()
+    sl = ShardedLookup(metas, placement, 0, tuple(range(F)), ("sum",) * F, B, rank, world, dev, mode=mode)
+    torch.cuda.synchronize()
+    init_s = time.perf_counter() - t0
+    batches = [(torch.from_numpy(hb.indices).to(dev), torch.from_numpy(hb.offsets).to(dev)) for hb in host_batches]
+    out = torch.empty((B, F * dim), dtype=torch.float32, device=dev)
+    sl.lookup(*batches[0], out=out, check=True)
+    for i in range(args.warmup):
+        sl.lookup(*batches[i % len(batches)], out=out, check=False)
+    torch.cuda.synchronize()
+    dist.barrier()
+    sampler = ClockSampler(local)
+    sampler.start()
+    stream = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sl.stats.c1_bytes_sent = sl.stats.c2_bytes_sent = 0
+    sl.profile = True
+    torch.cuda.synchronize()
+    dist.barrier()
+    ev0.record(stream)
+    for i in range(args.steps):
+        sl.lookup(*batches[i % len(batches)], out=out, check=False)
+    ev1.record(stream)
+    ev1.synchronize()
+    torch.cuda.synchronize()
+    dist.barrier()
+    clocks = sampler.stop()
+    ms = ev0.elapsed_time(ev1)
+    phases = sl.phase_ms()
+    sl.profile = False
+    sl.ops.check()
+    # owner-pool algorithmic bytes: every rank pools, for each requester, the
+    # rows routed to it; measured on this rank over the timed steps
+    t = torch.tensor([ms, phases.get("pool", 0.0), phases.get("a2a", 0.0)], device=dev, dtype=torch.float64)
+    tmax = t.clone()
+    dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    ms_max = float(tmax[0].item())
+    value = world * B * F * args.steps / (ms_max / 1e3)
+    # algorithmic bytes pooled on this rank per step: all ranks' bags of the tables it owns.
+    # With identical batch statistics per rank, the rank's share is rows_owned / total.
+    a2a_bytes = (sl.stats.c1_bytes_sent + sl.stats.c2_bytes_sent) / args.steps
+    total_alg = sum(algorithmic_bytes(hb, dim) for hb in host_batches) / len(host_batches)
+    if mode == "tablewise":
+        owned = sum(1 for s in placement if s.server_id == rank)
+        share = owned / F
+    else:
+        share = 1.0 / world
+    pool_bytes_step = total_alg * world * share
+    pool_ms = float(t[1].item()) / args.steps
+    achieved = pool_bytes_step / (pool_ms / 1e3) / 1e9 if pool_ms > 0 else None
+    peak, peak_src = measured_peak()
+    a2a_ms = float(t[2].item()) / args.steps
+    # e2e: pinned host CSR -> device -> sharded lookup -> pinned host out
+    e2e = None
+    if not args.no_e2e:
+        pinned = [(torch.from_numpy(hb.indices).pin_memory(), torch.from_numpy(hb.offsets).pin_memory())
+                  for hb in host_batches]
+        out_h = torch.empty((B, F * dim), dtype=torch.float32, pin_memory=True)
+        ksteps = max(3, min(args.steps, 30))
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        h2d = 0
+        for i in range(ksteps):
+            ih, oh = pinned[i % len(pinned)]
+            o = sl.lookup(ih.to(dev, non_blocking=True), oh.to(dev, non_blocking=True), out=out, check=False)
+            out_h.copy_(o, non_blocking=True)
+            stream.synchronize()
+            h2d += ih.numel() * 4 + oh.numel() * 8
+        e1.record(stream)
+        e1.synchronize()
+        te = torch.tensor([e0.elapsed_time(e1)], device=dev, dtype=torch.float64)
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * B * F * ksteps / (float(te.item()) / 1e3), "unit": "pooled lookups/s",
+               "h2d_bytes_per_step": h2d // ksteps, "d2h_bytes_per_step": out_h.numel() * 4, "steps": ksteps,
+               "api": "sharded.ShardedLookup.lookup per rank (pinned host CSR -> pinned host pooled, sync)"}
+    if rank == 0:
+        line = {
+            "metric": "pooled lookups/s (bags/s)", "value": value, "unit": "pooled lookups/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32 rows, f64 accumulate", "data": "synthetic",
+            "config": {"workload": cfg["name"] + f"-{mode}", "global_batch": B * world, "per_gpu_batch": B,
+                       "pooling": list(cfg["pooling"]) if isinstance(cfg["pooling"], tuple) else cfg["pooling"],
+                       "alpha": cfg["alpha"], "dim": dim, "tables": F, "parallelism": f"{mode}-sharded x{world}",
+                       "l2": "inputs larger than L2 (1.18 GB algorithmic bytes per rank-batch)",
+                       "init_store_s": round(init_s, 2)},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": (achieved / peak) if achieved else None, "traffic": None,
+                         "peak_source": peak_src, "kernel": "owner gather+pool (K4) launches, rank 0",
+                         "bytes_per_step": pool_bytes_step, "pool_ms_per_step": pool_ms},
+            "a2a": {"bytes_sent_per_step_rank0": a2a_bytes, "ms_per_step_rank0": a2a_ms,
+                    "gbs": (a2a_bytes / (a2a_ms / 1e3) / 1e9) if a2a_ms > 0 else None,
+                    "peak_gbs": 900.0, "note": "NCCL all_to_all_single; includes the self-slice"},
+            "gpu_launches": None,
+            "e2e": e2e, "cpu_baseline": None, "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
 
 
 if __name__ == "__main__":

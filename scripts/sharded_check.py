@@ -1,0 +1,52 @@
+"""torchrun --nproc-per-node N scripts/sharded_check.py [tablewise|rowwise]
+Sharded lookup on N GPUs vs the CPU oracle (flat f64 pool) for every rank's batch."""
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import oracle as O  # noqa: E402
+from paper_2410_12794_b200.sharded import ShardedLookup, rowwise_placement, tablewise_placement  # noqa: E402
+from paper_2410_12794_b200.store import TableMeta  # noqa: E402
+from paper_2410_12794_b200.workload import DlrmBatchGen  # noqa: E402
+
+
+def main():
+    mode = sys.argv[1] if len(sys.argv) > 1 else "tablewise"
+    local = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    rank, world = dist.get_rank(), dist.get_world_size()
+    rows = (50_000, 123, 20_000, 7, 9_999, 100_000, 31, 4_096, 64, 2)
+    ops = ("sum", "mean") * 5
+    D, B = 128, 96
+    metas = [TableMeta(t, n, D) for t, n in enumerate(rows)]
+    placement = (tablewise_placement if mode == "tablewise" else rowwise_placement)(rows, world)
+    sl = ShardedLookup(metas, placement, 0, tuple(range(len(rows))), ops, B, rank, world, f"cuda:{local}", mode=mode)
+    worst, exact, n = 0.0, 0, 0
+    for it in range(3):
+        hb = DlrmBatchGen(rows, 1.0, B, (1, 40), seed=100 * rank + it, ops=ops, permute=(mode == "rowwise")).next()
+        out = sl.lookup(torch.from_numpy(hb.indices).cuda(), torch.from_numpy(hb.offsets).cuda()).cpu().numpy()
+        for f in range(len(rows)):
+            for s in range(B):
+                b = f * B + s
+                ref = O.pool_flat(O.rows_of(0, f, D, hb.indices[hb.offsets[b]:hb.offsets[b + 1]]), ops[f])
+                got = out[s, f * D:(f + 1) * D]
+                worst = max(worst, O.tolerance_ratio(ref, got))
+                exact += ref.tobytes() == got.tobytes()
+                n += 1
+    t = torch.tensor([worst, float(n - exact)], device="cuda", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        print(f"SHARDED {mode} world={world} worst_tolerance_ratio={t[0].item():.4f} "
+              f"max_non_bit_exact_bags={int(t[1].item())} bags_per_rank={n}", flush=True)
+    ok = t[0].item() <= 1.0
+    dist.destroy_process_group()
+    sys.exit(0 if ok else 1)
+
+
+if __name__ == "__main__":
+    main()
