@@ -194,6 +194,8 @@ def main():
     ap.add_argument("--alpha", type=float, default=None, help="override Zipf alpha (0 = uniform cold control)")
     ap.add_argument("--table-rows", type=int, default=None, help="override every table's row count (cold control)")
     ap.add_argument("--mode", default="tablewise", choices=["tablewise", "rowwise"], help="N>1 sharding")
+    ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
+                    help="N>1 pooled-result exchange: fused NVLink peer stores (p2p) or NCCL all-to-all")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -340,7 +342,7 @@ def run_sharded(args, rank, world, local):
     (K4) -> pooled all-to-all (C2) -> placement / combine (K5)."""
     import torch
     import torch.distributed as dist
-    from paper_2410_12794_b200.sharded import ShardedLookup, rowwise_placement, tablewise_placement
+    from paper_2410_12794_b200.sharded import P2PShardedLookup, ShardedLookup, rowwise_placement, tablewise_placement
     from paper_2410_12794_b200.store import TableMeta
     cfg, host_batches = build_cfg(args.config, rank, args.batches, args.alpha, args.table_rows)
     rows, dim, B = cfg["table_rows"], cfg["dim"], cfg["batch"]
@@ -350,11 +352,12 @@ def run_sharded(args, rank, world, local):
     metas = [TableMeta(t, n, dim) for t, n in enumerate(rows)]
     dev = torch.device("cuda", local)
     t0 = time.perf_counter()
-    sl = ShardedLookup(metas, placement, 0, tuple(range(F)), ("sum",) * F, B, rank, world, dev, mode=mode)
+    cls = P2PShardedLookup if args.exchange == "p2p" else ShardedLookup
+    sl = cls(metas, placement, 0, tuple(range(F)), ("sum",) * F, B, rank, world, dev, mode=mode)
     torch.cuda.synchronize()
     init_s = time.perf_counter() - t0
     batches = [(torch.from_numpy(hb.indices).to(dev), torch.from_numpy(hb.offsets).to(dev)) for hb in host_batches]
-    out = torch.empty((B, F * dim), dtype=torch.float32, device=dev)
+    out = torch.empty((B, F * dim), dtype=torch.float32, device=dev) if args.exchange == "nccl" else None
     sl.lookup(*batches[0], out=out, check=True)
     for i in range(args.warmup):
         sl.lookup(*batches[i % len(batches)], out=out, check=False)
@@ -364,7 +367,8 @@ def run_sharded(args, rank, world, local):
     sampler.start()
     stream = torch.cuda.current_stream()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    sl.stats.c1_bytes_sent = sl.stats.c2_bytes_sent = 0
+    if args.exchange == "nccl":
+        sl.stats.c1_bytes_sent = sl.stats.c2_bytes_sent = 0
     sl.profile = True
     torch.cuda.synchronize()
     dist.barrier()
@@ -389,7 +393,16 @@ def run_sharded(args, rank, world, local):
     value = world * B * F * args.steps / (ms_max / 1e3)
     # algorithmic bytes pooled on this rank per step: all ranks' bags of the tables it owns.
     # With identical batch statistics per rank, the rank's share is rows_owned / total.
-    a2a_bytes = (sl.stats.c1_bytes_sent + sl.stats.c2_bytes_sent) / args.steps
+    if args.exchange == "nccl":
+        a2a_bytes = (sl.stats.c1_bytes_sent + sl.stats.c2_bytes_sent) / args.steps
+    else:
+        # bytes crossing NVLink per step from this rank as owner: pooled rows (+ indices read) to the
+        # other ranks; table-wise f32 rows, row-wise f64 partials
+        per_row = dim * (4 if mode == "tablewise" else 8)
+        rows_out = (world - 1) * (B * sum(1 for s in placement if s.server_id == rank) if mode == "tablewise"
+                                  else B * F)
+        a2a_bytes = rows_out * per_row
+    sl.ops.check() if hasattr(sl, "ops") else None
     total_alg = sum(algorithmic_bytes(hb, dim) for hb in host_batches) / len(host_batches)
     if mode == "tablewise":
         owned = sum(1 for s in placement if s.server_id == rank)
@@ -400,7 +413,7 @@ def run_sharded(args, rank, world, local):
     pool_ms = float(t[1].item()) / args.steps
     achieved = pool_bytes_step / (pool_ms / 1e3) / 1e9 if pool_ms > 0 else None
     peak, peak_src = measured_peak()
-    a2a_ms = float(t[2].item()) / args.steps
+    a2a_ms = float(t[2].item()) / args.steps if args.exchange == "nccl" else float(t[1].item()) / args.steps
     # e2e: pinned host CSR -> device -> sharded lookup -> pinned host out
     e2e = None
     if not args.no_e2e:
@@ -434,7 +447,8 @@ def run_sharded(args, rank, world, local):
             "dtype": "f32 rows, f64 accumulate", "data": "synthetic",
             "config": {"workload": cfg["name"] + f"-{mode}", "global_batch": B * world, "per_gpu_batch": B,
                        "pooling": list(cfg["pooling"]) if isinstance(cfg["pooling"], tuple) else cfg["pooling"],
-                       "alpha": cfg["alpha"], "dim": dim, "tables": F, "parallelism": f"{mode}-sharded x{world}",
+                       "alpha": cfg["alpha"], "dim": dim, "tables": F,
+                       "parallelism": f"{mode}-sharded x{world} ({args.exchange} exchange)",
                        "l2": "inputs larger than L2 (1.18 GB algorithmic bytes per rank-batch)",
                        "init_store_s": round(init_s, 2)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -443,7 +457,9 @@ def run_sharded(args, rank, world, local):
                          "bytes_per_step": pool_bytes_step, "pool_ms_per_step": pool_ms},
             "a2a": {"bytes_sent_per_step_rank0": a2a_bytes, "ms_per_step_rank0": a2a_ms,
                     "gbs": (a2a_bytes / (a2a_ms / 1e3) / 1e9) if a2a_ms > 0 else None,
-                    "peak_gbs": 900.0, "note": "NCCL all_to_all_single; includes the self-slice"},
+                    "peak_gbs": 900.0, "phases_ms_total": {k: round(v, 3) for k, v in phases.items()},
+                    "note": ("NCCL all_to_all_single; includes the self-slice" if args.exchange == "nccl" else
+                             "fused: pooled rows stored to peers inside K4; ms = the fused kernel's time")},
             "gpu_launches": None,
             "e2e": e2e, "cpu_baseline": None, "clocks": clocks,
         }

@@ -49,6 +49,8 @@ extern "C" {
 
 #define FX_OUT_F32 0              /* final pooled f32 (Mean divided once)        */
 #define FX_OUT_F64_PARTIAL 1      /* f64 partial sum (Mean deferred), see counts */
+#define FX_OUT_SYSFENCE 16        /* OR-flag: system-scope fence after the epilogue stores
+                                     (outputs written to peer GPUs over NVLink)        */
 
 const char *fx_last_error(void);
 int fx_version(void);
@@ -77,6 +79,10 @@ typedef struct fx_segment {
   int64_t ld;           /* elements between consecutive shard rows (>= dim)   */
   int32_t dim;          /* embedding dimension                                */
   int32_t op;           /* FX_OP_*                                            */
+  const void *idx;      /* optional: indices base for this segment's bags (may be a peer/IPC
+                           pointer); NULL -> the launch's `indices`                          */
+  const int64_t *offs;  /* optional: offsets of this segment's bags, offs[b - bag_begin] ..
+                           offs[b - bag_begin + 1] index into `idx`; NULL -> launch offsets  */
 } fx_segment;
 
 /* ---- K4: fused gather + pool (store.py:184-193 partial_pool,
@@ -215,6 +221,26 @@ int fx_cache_last_evicted(fx_cache *c, uint64_t *out, int64_t cap, int64_t *n_ou
 /* device array of row pointers for the pending keys (NULL entry -> table dir),
  * consumed by the next fx_cache_apply_pending (host-fetched admissions) */
 int fx_cache_set_pending_rows(fx_cache *c, const float *const *rows, int64_t n);
+
+/* ---- peer memory (NVLink P2P over CUDA IPC) and the cross-GPU barrier ----
+ * The fused exchange: an owner's K4 reads a requester's CSR batch through an
+ * IPC-mapped pointer and stores pooled rows straight into the requester's
+ * output buffer, so the pooled "all-to-all" rides on the gather's own stores
+ * (replaces ranker.py:298-347 post_subrequest/_on_response). */
+int fx_dev_alloc(size_t bytes, void **out);                       /* cudaMalloc (IPC-exportable) */
+int fx_dev_free(void *ptr);
+int fx_ipc_export(void *ptr, unsigned char handle_out[64]);      /* cudaIpcGetMemHandle */
+int fx_ipc_open(const unsigned char handle[64], void **out);     /* cudaIpcOpenMemHandle */
+int fx_ipc_close(void *ptr);
+int fx_can_access_peer(int device, int peer_device);
+int fx_memcpy_async(void *dst, const void *src, size_t bytes, void *stream);
+/* one-block barrier: release-store `epoch` into peer_flags[r][rank] for every
+ * rank r (system scope, after a system fence), then acquire-spin until
+ * my_flags[r] >= epoch for every r. peer_flags is a DEVICE array of `world`
+ * pointers (IPC-mapped flag arrays; own entry = my_flags). Spins are bounded
+ * (~10 s); on timeout *timed_out (device int32, may be NULL) is set to 1. */
+int fx_peer_barrier(int64_t *my_flags, int64_t *const *peer_flags, int32_t rank, int32_t world, int64_t epoch,
+                    int32_t *timed_out, void *stream);
 
 #ifdef __cplusplus
 }

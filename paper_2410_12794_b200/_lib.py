@@ -32,6 +32,7 @@ FX_IDX_I32 = 0
 FX_IDX_I64 = 1
 FX_OUT_F32 = 0
 FX_OUT_F64_PARTIAL = 1
+FX_OUT_SYSFENCE = 16
 
 INT64_MAX = (1 << 63) - 1
 
@@ -59,6 +60,8 @@ class FxSegment(ctypes.Structure):
         ("ld", ctypes.c_int64),
         ("dim", ctypes.c_int32),
         ("op", ctypes.c_int32),
+        ("idx", ctypes.c_void_p),
+        ("offs", ctypes.c_void_p),
     ]
 
 
@@ -89,6 +92,14 @@ _SIGS = {
     "fx_route": ([_P, _P, _P, _P, _P, _P, _I32, _P, _I64, _P, _P, _P, _P], ctypes.c_int),
     "fx_bucket": ([_P, _I64, _P, _I64, _I32, _P, _P, _P, _P, _SZP, _P], ctypes.c_int),
     "fx_dedup": ([_P, _P, _I32, _P, _P, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _SZP, _P], ctypes.c_int),
+    "fx_dev_alloc": ([ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
+    "fx_dev_free": ([_P], ctypes.c_int),
+    "fx_ipc_export": ([_P, ctypes.c_char_p], ctypes.c_int),
+    "fx_ipc_open": ([ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
+    "fx_ipc_close": ([_P], ctypes.c_int),
+    "fx_can_access_peer": ([ctypes.c_int, ctypes.c_int], ctypes.c_int),
+    "fx_memcpy_async": ([_P, _P, ctypes.c_size_t, _P], ctypes.c_int),
+    "fx_peer_barrier": ([_P, _P, _I32, _I32, _I64, _P, _P], ctypes.c_int),
     # cache entry points are typed in cache.py (_sig); listed here for export checks
     **{n: (None, ctypes.c_int) for n in (
         "fx_cache_create", "fx_cache_destroy", "fx_cache_set_tables", "fx_cache_scalars", "fx_cache_reserve_sketch",

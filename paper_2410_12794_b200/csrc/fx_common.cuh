@@ -72,6 +72,27 @@ __device__ __forceinline__ int find_segment(const fx_segment *segs, int n, int64
   return lo;
 }
 
+// Bag bounds / index base honouring the optional per-segment sources
+// (fx_segment.offs / .idx, e.g. a requester's batch mapped over NVLink).
+__device__ __forceinline__ void bag_bounds(const fx_segment *segs, int s, int64_t bag, const int64_t *offsets,
+                                           int64_t &beg, int64_t &end) {
+  const int64_t *o = segs[s].offs;
+  if (o) {
+    const int64_t j = bag - segs[s].bag_begin;
+    beg = o[j];
+    end = o[j + 1];
+  } else {
+    beg = __ldg(&offsets[bag]);
+    end = __ldg(&offsets[bag + 1]);
+  }
+}
+
+template <typename IdxT>
+__device__ __forceinline__ const IdxT *seg_indices(const fx_segment *segs, int s, const IdxT *indices) {
+  const void *p = segs[s].idx;
+  return p ? static_cast<const IdxT *>(p) : indices;
+}
+
 // Last bag b with offsets[b] <= pos (for per-occurrence kernels).
 __device__ __forceinline__ int64_t find_bag(const int64_t *offsets, int64_t n_bags, int64_t pos) {
   int64_t lo = 0, hi = n_bags;

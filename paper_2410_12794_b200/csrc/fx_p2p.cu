@@ -1,0 +1,98 @@
+// Peer memory over NVLink (CUDA IPC) and a bounded cross-GPU flag barrier.
+//
+// The fused sharded exchange (sharded.P2PShardedLookup): every rank exports
+// its staging buffers (CSR batch in, pooled rows out, barrier flags) once;
+// owners' K4 launches then read the requesters' indices and store pooled
+// rows into the requesters' output buffers directly through the mapped
+// pointers, and two barriers per step order "inputs staged" and "outputs
+// landed" across the GPUs. This replaces the reference's fan-out/response
+// messages (ranker.py:298-347) and the NCCL all-to-all of the baseline path.
+#include <cstring>
+
+#include "fx_common.cuh"
+
+namespace fx {
+
+__device__ __forceinline__ void st_release_sys(int64_t *p, int64_t v) {
+  asm volatile("st.release.sys.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ int64_t ld_acquire_sys(const int64_t *p) {
+  int64_t v;
+  asm volatile("ld.acquire.sys.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// One warp: lane r signals rank r, then lane r waits for rank r's signal.
+__global__ void k_peer_barrier(int64_t *my_flags, int64_t *const *peer_flags, int rank, int world, int64_t epoch,
+                               int32_t *timed_out) {
+  __threadfence_system();  // order every prior write of this stream (incl. peer stores) before the signal
+  for (int r = threadIdx.x; r < world; r += blockDim.x) st_release_sys(peer_flags[r] + rank, epoch);
+  for (int r = threadIdx.x; r < world; r += blockDim.x) {
+    long long spins = 0;
+    while (ld_acquire_sys(my_flags + r) < epoch) {
+      __nanosleep(200);
+      if (++spins > (1ll << 25)) {  // ~10 s: never hang the GPU on a dead peer
+        if (timed_out) atomicExch(timed_out, 1);
+        break;
+      }
+    }
+  }
+  __syncwarp();
+  __threadfence_system();
+}
+
+}  // namespace fx
+
+using namespace fx;
+
+extern "C" {
+
+int fx_dev_alloc(size_t bytes, void **out) {
+  *out = nullptr;
+  return cuda_check(cudaMalloc(out, bytes ? bytes : 1), "fx_dev_alloc");
+}
+
+int fx_dev_free(void *ptr) { return ptr ? cuda_check(cudaFree(ptr), "fx_dev_free") : FX_OK; }
+
+int fx_ipc_export(void *ptr, unsigned char handle_out[64]) {
+  cudaIpcMemHandle_t h;
+  int rc = cuda_check(cudaIpcGetMemHandle(&h, ptr), "fx_ipc_export");
+  if (rc) return rc;
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  std::memcpy(handle_out, &h, 64);
+  return FX_OK;
+}
+
+int fx_ipc_open(const unsigned char handle[64], void **out) {
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, 64);
+  *out = nullptr;
+  return cuda_check(cudaIpcOpenMemHandle(out, h, cudaIpcMemLazyEnablePeerAccess), "fx_ipc_open");
+}
+
+int fx_ipc_close(void *ptr) { return cuda_check(cudaIpcCloseMemHandle(ptr), "fx_ipc_close"); }
+
+int fx_can_access_peer(int device, int peer_device) {
+  int ok = 0;
+  if (cudaDeviceCanAccessPeer(&ok, device, peer_device) != cudaSuccess) return -1;
+  return ok;
+}
+
+int fx_memcpy_async(void *dst, const void *src, size_t bytes, void *stream) {
+  if (bytes == 0) return FX_OK;
+  return cuda_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, as_stream(stream)), "fx_memcpy_async");
+}
+
+int fx_peer_barrier(int64_t *my_flags, int64_t *const *peer_flags, int32_t rank, int32_t world, int64_t epoch,
+                    int32_t *timed_out, void *stream) {
+  if (world < 1 || world > 32 || rank < 0 || rank >= world) {
+    set_error("fx_peer_barrier: bad rank/world");
+    return FX_E_CONFIG;
+  }
+  k_peer_barrier<<<1, 32, 0, as_stream(stream)>>>(my_flags, peer_flags, rank, world, epoch, timed_out);
+  FX_LAUNCH_CHECK("fx_peer_barrier");
+  return FX_OK;
+}
+
+}  // extern "C"

@@ -42,9 +42,9 @@ __global__ void __launch_bounds__(256) k_table_init(float *__restrict__ out, int
 // are issued before any accumulation to keep U*16 B per lane in flight.
 template <int G, int NCH, int U, typename IdxT, int MODE>
 __global__ void __launch_bounds__(256) k_gather_pool_v4(
-    const fx_segment *__restrict__ segs, int n_segs, int dim, const IdxT *__restrict__ indices,
+    const fx_segment *__restrict__ segs, int n_segs, int dim, const IdxT *__restrict__ indices_g,
     const int64_t *__restrict__ offsets, int64_t n_bags, int32_t *__restrict__ counts,
-    int64_t *err, int32_t bad_code, int32_t *err_code) {
+    int64_t *err, int32_t bad_code, int32_t *err_code, bool sysfence) {
   constexpr int GPW = 32 / G;
   const int lane = threadIdx.x & 31;
   const int gl = lane % G;
@@ -57,7 +57,9 @@ __global__ void __launch_bounds__(256) k_gather_pool_v4(
     const int s = find_segment(segs, n_segs, bag);
     const float *__restrict__ tab = segs[s].table;
     const int64_t rb = segs[s].row_begin, re = segs[s].row_end, ld = segs[s].ld;
-    const int64_t beg = __ldg(&offsets[bag]), end = __ldg(&offsets[bag + 1]);
+    int64_t beg, end;
+    bag_bounds(segs, s, bag, offsets, beg, end);
+    const IdxT *indices = seg_indices(segs, s, indices_g);
 
     double acc[NCH][4];
 #pragma unroll
@@ -143,9 +145,9 @@ __global__ void __launch_bounds__(256) k_gather_pool_v4(
 // scalar coalesced loads, same per-element sequential f64 order.
 template <typename IdxT, int MODE>
 __global__ void __launch_bounds__(256) k_gather_pool_generic(
-    const fx_segment *__restrict__ segs, int n_segs, int dim, const IdxT *__restrict__ indices,
+    const fx_segment *__restrict__ segs, int n_segs, int dim, const IdxT *__restrict__ indices_g,
     const int64_t *__restrict__ offsets, int64_t n_bags, int32_t *__restrict__ counts,
-    int64_t *err, int32_t bad_code, int32_t *err_code) {
+    int64_t *err, int32_t bad_code, int32_t *err_code, bool sysfence) {
   constexpr int TILE = 128, U = 4;
   const int lane = threadIdx.x & 31;
   const int tiles = (dim + TILE - 1) / TILE;
@@ -157,7 +159,9 @@ __global__ void __launch_bounds__(256) k_gather_pool_generic(
     const int s = find_segment(segs, n_segs, bag);
     const float *__restrict__ tab = segs[s].table;
     const int64_t rb = segs[s].row_begin, re = segs[s].row_end, ld = segs[s].ld;
-    const int64_t beg = __ldg(&offsets[bag]), end = __ldg(&offsets[bag + 1]);
+    int64_t beg, end;
+    bag_bounds(segs, s, bag, offsets, beg, end);
+    const IdxT *indices = seg_indices(segs, s, indices_g);
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
     for (int64_t c0 = beg; c0 < end; c0 += 32) {
       const int n = static_cast<int>((end - c0 < 32 ? end - c0 : (int64_t)32));
@@ -206,6 +210,7 @@ __global__ void __launch_bounds__(256) k_gather_pool_generic(
     }
     if (MODE == FX_OUT_F64_PARTIAL && counts && tile == 0 && lane == 0) counts[bag] = static_cast<int32_t>(cnt);
   }
+  if (sysfence) __threadfence_system();
 }
 
 template <typename IdxT>
@@ -280,7 +285,7 @@ static int pool_variant() {
 template <int NCH, typename IdxT, int MODE>
 static void launch_async(const fx_segment *segs, int n_segs, int dim, const IdxT *ix, const int64_t *offsets,
                          int64_t n_bags, int32_t *counts, int64_t *err, int32_t bad_code, int32_t *err_code,
-                         cudaStream_t st) {
+                         cudaStream_t st, bool sf) {
   constexpr int WARPS = 4;
   const size_t smem = static_cast<size_t>(WARPS) * 32 * 32 * 16 * NCH;
   static int per_sm = -1;
@@ -294,13 +299,13 @@ static void launch_async(const fx_segment *segs, int n_segs, int dim, const IdxT
   const int64_t need = (n_bags + WARPS - 1) / WARPS;
   if (blocks > need) blocks = need;
   k_pool_async<NCH, IdxT, MODE><<<static_cast<int>(blocks), WARPS * 32, smem, st>>>(
-      segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code);
+      segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code, sf);
 }
 
 template <int G, int NCH, int U, typename IdxT, int MODE>
 static void launch_prefetch(const fx_segment *segs, int n_segs, int dim, const IdxT *ix, const int64_t *offsets,
                             int64_t n_bags, int32_t *counts, int64_t *err, int32_t bad_code, int32_t *err_code,
-                            cudaStream_t st) {
+                            cudaStream_t st, bool sf) {
   static int per_sm = -1;
   if (per_sm < 0) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pool_prefetch<G, NCH, U, IdxT, MODE>, 256, 0);
@@ -310,47 +315,47 @@ static void launch_prefetch(const fx_segment *segs, int n_segs, int dim, const I
   const int64_t need = (n_bags * G + 255) / 256;
   if (blocks > need) blocks = need;
   k_pool_prefetch<G, NCH, U, IdxT, MODE><<<static_cast<int>(blocks), 256, 0, st>>>(
-      segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code);
+      segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code, sf);
 }
 
 template <typename IdxT, int MODE>
 static int launch_pool(const fx_segment *segs, int n_segs, int dim, const void *indices, const int64_t *offsets,
                        int64_t n_bags, int32_t *counts, int64_t *err, int32_t bad_code, int32_t *err_code,
-                       cudaStream_t st, bool vec4) {
+                       cudaStream_t st, bool vec4, bool sf) {
   const IdxT *ix = static_cast<const IdxT *>(indices);
   const int var = pool_variant();
   if (var == 1 && dim == 128) {
-    launch_async<1, IdxT, MODE>(segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code, st);
+    launch_async<1, IdxT, MODE>(segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code, st, sf);
   } else if (var == 1 && dim == 256) {
-    launch_async<2, IdxT, MODE>(segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code, st);
+    launch_async<2, IdxT, MODE>(segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code, st, sf);
   } else if (var == 2 && dim == 128) {
     launch_prefetch<32, 1, 8, IdxT, MODE>(segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code,
-                                          st);
+                                          st, sf);
   } else if (var == 2 && dim == 64) {
     launch_prefetch<16, 1, 8, IdxT, MODE>(segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code,
-                                          st);
+                                          st, sf);
   } else if (var == 2 && dim == 256) {
     launch_prefetch<32, 2, 4, IdxT, MODE>(segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code,
-                                          st);
+                                          st, sf);
   } else if (vec4 && dim == 128) {
     k_gather_pool_v4<32, 1, 8, IdxT, MODE><<<grid_for(n_bags * 32, 256), 256, 0, st>>>(
-        segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code);
+        segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code, sf);
   } else if (vec4 && dim == 64) {
     k_gather_pool_v4<16, 1, 8, IdxT, MODE><<<grid_for(n_bags * 16, 256), 256, 0, st>>>(
-        segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code);
+        segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code, sf);
   } else if (vec4 && dim == 32) {
     k_gather_pool_v4<8, 1, 8, IdxT, MODE><<<grid_for(n_bags * 8, 256), 256, 0, st>>>(
-        segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code);
+        segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code, sf);
   } else if (vec4 && dim <= 256) {
     k_gather_pool_v4<32, 2, 4, IdxT, MODE><<<grid_for(n_bags * 32, 256), 256, 0, st>>>(
-        segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code);
+        segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code, sf);
   } else if (vec4 && dim <= 512) {
     k_gather_pool_v4<32, 4, 2, IdxT, MODE><<<grid_for(n_bags * 32, 256), 256, 0, st>>>(
-        segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code);
+        segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code, sf);
   } else {
     const int tiles = (dim + 127) / 128;
     k_gather_pool_generic<IdxT, MODE><<<grid_for(n_bags * tiles * 32, 256), 256, 0, st>>>(
-        segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code);
+        segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code, sf);
   }
   FX_LAUNCH_CHECK("fx_gather_pool");
   return FX_OK;
@@ -380,6 +385,8 @@ int fx_table_init(float *out, int64_t ld, uint64_t seed, int64_t table_id, int32
 int fx_gather_pool(const fx_segment *segs, int32_t n_segs, int32_t dim, const void *indices, int32_t idx_type,
                    const int64_t *offsets, int64_t n_bags, int32_t out_mode, int32_t *counts, int64_t *err,
                    int32_t bad_code, int32_t *err_code, void *stream) {
+  const bool sf = (out_mode & FX_OUT_SYSFENCE) != 0;
+  out_mode &= ~FX_OUT_SYSFENCE;
   if (n_segs < 1 || dim < 1 || (idx_type != FX_IDX_I32 && idx_type != FX_IDX_I64) ||
       (out_mode != FX_OUT_F32 && out_mode != FX_OUT_F64_PARTIAL)) {
     set_error("fx_gather_pool: bad arguments");
@@ -394,15 +401,15 @@ int fx_gather_pool(const fx_segment *segs, int32_t n_segs, int32_t dim, const vo
   if (idx_type == FX_IDX_I32) {
     return out_mode == FX_OUT_F32
                ? launch_pool<int32_t, FX_OUT_F32>(segs, n_segs, dim, indices, offsets, n_bags, counts, err, bad_code,
-                                                  err_code, st, vec4)
+                                                  err_code, st, vec4, sf)
                : launch_pool<int32_t, FX_OUT_F64_PARTIAL>(segs, n_segs, dim, indices, offsets, n_bags, counts, err,
-                                                          bad_code, err_code, st, vec4);
+                                                          bad_code, err_code, st, vec4, sf);
   }
   return out_mode == FX_OUT_F32
              ? launch_pool<int64_t, FX_OUT_F32>(segs, n_segs, dim, indices, offsets, n_bags, counts, err, bad_code,
-                                                err_code, st, vec4)
+                                                err_code, st, vec4, sf)
              : launch_pool<int64_t, FX_OUT_F64_PARTIAL>(segs, n_segs, dim, indices, offsets, n_bags, counts, err,
-                                                        bad_code, err_code, st, vec4);
+                                                        bad_code, err_code, st, vec4, sf);
 }
 
 int fx_gather_rows(const float *table, int64_t ld, int64_t row_begin, int64_t row_end, int32_t dim,

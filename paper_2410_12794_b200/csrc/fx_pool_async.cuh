@@ -54,10 +54,10 @@ __device__ __forceinline__ void emit_bag(const fx_segment &sg, int64_t bag, int6
 // offsets and first index chunk. Rows are then summed from shared memory.
 template <int NCH, typename IdxT, int MODE>
 __global__ void __launch_bounds__(128) k_pool_async(const fx_segment *__restrict__ segs, int n_segs, int dim,
-                                                    const IdxT *__restrict__ indices,
+                                                    const IdxT *__restrict__ indices_g,
                                                     const int64_t *__restrict__ offsets, int64_t n_bags,
                                                     int32_t *__restrict__ counts, int64_t *err, int32_t bad_code,
-                                                    int32_t *err_code) {
+                                                    int32_t *err_code, bool sysfence) {
   constexpr int ROWB = 32 * 16 * NCH;  // bytes per row
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31;
@@ -68,18 +68,25 @@ __global__ void __launch_bounds__(128) k_pool_async(const fx_segment *__restrict
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
 
   int64_t bag = warp;
-  if (bag >= n_bags) return;
-  int64_t beg = __ldg(&offsets[bag]), end = __ldg(&offsets[bag + 1]);
+  if (bag >= n_bags) {
+    if (sysfence) __threadfence_system();
+    return;
+  }
+  int s = find_segment(segs, n_segs, bag);
+  int64_t beg, end;
+  bag_bounds(segs, s, bag, offsets, beg, end);
+  const IdxT *indices = seg_indices(segs, s, indices_g);
   IdxT pidx = (beg + lane < end) ? indices[beg + lane] : IdxT(0);
 
   while (bag < n_bags) {
-    const int s = find_segment(segs, n_segs, bag);
     const float *__restrict__ tab = segs[s].table;
     const int64_t rb = segs[s].row_begin, re = segs[s].row_end, ld = segs[s].ld;
     double acc[NCH][4];
 #pragma unroll
     for (int k = 0; k < NCH; ++k) acc[k][0] = acc[k][1] = acc[k][2] = acc[k][3] = 0.0;
     const int64_t nbag = bag + nwarps;
+    const int ns = nbag < n_bags ? find_segment(segs, n_segs, nbag) : s;
+    const IdxT *nindices = seg_indices(segs, ns, indices_g);
     int64_t nbeg = 0, nend = 0;
     IdxT nidx = IdxT(0);
     bool have_next = false;
@@ -101,9 +108,8 @@ __global__ void __launch_bounds__(128) k_pool_async(const fx_segment *__restrict
       if (c0 + 32 < end) {
         pidx = (c0 + 32 + lane < end) ? indices[c0 + 32 + lane] : IdxT(0);
       } else if (nbag < n_bags) {
-        nbeg = __ldg(&offsets[nbag]);
-        nend = __ldg(&offsets[nbag + 1]);
-        nidx = (nbeg + lane < nend) ? indices[nbeg + lane] : IdxT(0);
+        bag_bounds(segs, ns, nbag, offsets, nbeg, nend);
+        nidx = (nbeg + lane < nend) ? nindices[nbeg + lane] : IdxT(0);
         have_next = true;
       }
       cp_async_wait_all();
@@ -121,16 +127,18 @@ __global__ void __launch_bounds__(128) k_pool_async(const fx_segment *__restrict
       __syncwarp();
     }
     if (!have_next && nbag < n_bags) {
-      nbeg = __ldg(&offsets[nbag]);
-      nend = __ldg(&offsets[nbag + 1]);
-      nidx = (nbeg + lane < nend) ? indices[nbeg + lane] : IdxT(0);
+      bag_bounds(segs, ns, nbag, offsets, nbeg, nend);
+      nidx = (nbeg + lane < nend) ? nindices[nbeg + lane] : IdxT(0);
     }
     emit_bag<NCH, MODE>(segs[s], bag, end - beg, acc, lane, 32, counts);
     bag = nbag;
+    s = ns;
+    indices = nindices;
     beg = nbeg;
     end = nend;
     pidx = nidx;
   }
+  if (sysfence) __threadfence_system();
 }
 
 // Bag-per-group register variant with next-bag software prefetch: the next
@@ -138,10 +146,10 @@ __global__ void __launch_bounds__(128) k_pool_async(const fx_segment *__restrict
 // after the first round of row loads is issued.
 template <int G, int NCH, int U, typename IdxT, int MODE>
 __global__ void __launch_bounds__(256) k_pool_prefetch(const fx_segment *__restrict__ segs, int n_segs, int dim,
-                                                       const IdxT *__restrict__ indices,
+                                                       const IdxT *__restrict__ indices_g,
                                                        const int64_t *__restrict__ offsets, int64_t n_bags,
                                                        int32_t *__restrict__ counts, int64_t *err, int32_t bad_code,
-                                                       int32_t *err_code) {
+                                                       int32_t *err_code, bool sysfence) {
   constexpr int GPW = 32 / G;
   const int lane = threadIdx.x & 31;
   const int gl = lane % G;
@@ -151,17 +159,24 @@ __global__ void __launch_bounds__(256) k_pool_prefetch(const fx_segment *__restr
   const int64_t nwarps = (gridDim.x * (int64_t)blockDim.x) >> 5;
   const int64_t step = nwarps * GPW;
   int64_t bag = warp * GPW + gw;
-  if (bag >= n_bags) return;
-  int64_t beg = __ldg(&offsets[bag]), end = __ldg(&offsets[bag + 1]);
+  if (bag >= n_bags) {
+    if (sysfence) __threadfence_system();
+    return;
+  }
+  int s = find_segment(segs, n_segs, bag);
+  int64_t beg, end;
+  bag_bounds(segs, s, bag, offsets, beg, end);
+  const IdxT *indices = seg_indices(segs, s, indices_g);
   IdxT pidx = (beg + gl < end) ? indices[beg + gl] : IdxT(0);
   while (bag < n_bags) {
-    const int s = find_segment(segs, n_segs, bag);
     const float *__restrict__ tab = segs[s].table;
     const int64_t rb = segs[s].row_begin, re = segs[s].row_end, ld = segs[s].ld;
     double acc[NCH][4];
 #pragma unroll
     for (int k = 0; k < NCH; ++k) acc[k][0] = acc[k][1] = acc[k][2] = acc[k][3] = 0.0;
     const int64_t nbag = bag + step;
+    const int ns = nbag < n_bags ? find_segment(segs, n_segs, nbag) : s;
+    const IdxT *nindices = seg_indices(segs, ns, indices_g);
     int64_t nbeg = 0, nend = 0;
     IdxT nidx = IdxT(0);
     bool have_next = false;
@@ -187,9 +202,8 @@ __global__ void __launch_bounds__(256) k_pool_prefetch(const fx_segment *__restr
           if (c0 + G < end) {
             pidx = (c0 + G + gl < end) ? indices[c0 + G + gl] : IdxT(0);
           } else if (nbag < n_bags) {
-            nbeg = __ldg(&offsets[nbag]);
-            nend = __ldg(&offsets[nbag + 1]);
-            nidx = (nbeg + gl < nend) ? indices[nbeg + gl] : IdxT(0);
+            bag_bounds(segs, ns, nbag, offsets, nbeg, nend);
+            nidx = (nbeg + gl < nend) ? nindices[nbeg + gl] : IdxT(0);
             have_next = true;
           }
         }
@@ -208,16 +222,18 @@ __global__ void __launch_bounds__(256) k_pool_prefetch(const fx_segment *__restr
       }
     }
     if (!have_next && nbag < n_bags) {
-      nbeg = __ldg(&offsets[nbag]);
-      nend = __ldg(&offsets[nbag + 1]);
-      nidx = (nbeg + gl < nend) ? indices[nbeg + gl] : IdxT(0);
+      bag_bounds(segs, ns, nbag, offsets, nbeg, nend);
+      nidx = (nbeg + gl < nend) ? nindices[nbeg + gl] : IdxT(0);
     }
     emit_bag<NCH, MODE>(segs[s], bag, end - beg, acc, gl, G, counts);
     bag = nbag;
+    s = ns;
+    indices = nindices;
     beg = nbeg;
     end = nend;
     pidx = nidx;
   }
+  if (sysfence) __threadfence_system();
 }
 
 }  // namespace fx

@@ -326,3 +326,270 @@ class ShardedLookup:
         if check:
             self.ops.check()
         return out
+
+
+# ---------------------------------------------------------------------------------------
+# Fused exchange over NVLink peer memory (no NCCL on the data path)
+# ---------------------------------------------------------------------------------------
+
+def _cai_tensor(ptr: int, shape, dtype: torch.dtype, device) -> torch.Tensor:
+    """Zero-copy torch view of a raw device allocation (__cuda_array_interface__)."""
+    typestr = {torch.float32: "<f4", torch.float64: "<f8", torch.int32: "<i4", torch.int64: "<i8"}[dtype]
+
+    class _Arr:
+        pass
+    a = _Arr()
+    a.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (int(ptr), False),
+                                  "version": 3, "strides": None}
+    return torch.as_tensor(a, device=device)
+
+
+class DevBuffer:
+    """cudaMalloc'd (IPC-exportable) buffer owned by libflexemb."""
+
+    def __init__(self, nbytes: int):
+        from . import _lib
+        self._lib = _lib
+        p = ctypes.c_void_p()
+        _lib.check(_lib.lib.fx_dev_alloc(max(int(nbytes), 1), ctypes.byref(p)), "dev alloc")
+        self.ptr = int(p.value)
+        self.nbytes = int(nbytes)
+
+    def handle(self) -> bytes:
+        buf = ctypes.create_string_buffer(64)
+        self._lib.check(self._lib.lib.fx_ipc_export(self.ptr, buf), "ipc export")
+        return buf.raw
+
+    def __del__(self):
+        try:
+            self._lib.lib.fx_dev_free(self.ptr)
+        except Exception:
+            pass
+
+
+def _ipc_open(handle: bytes) -> int:
+    from . import _lib
+    p = ctypes.c_void_p()
+    _lib.check(_lib.lib.fx_ipc_open(handle, ctypes.byref(p)), "ipc open")
+    return int(p.value)
+
+
+class P2PShardedLookup:
+    """Sharded lookup whose exchange rides on the gather+pool kernel itself.
+
+    Per step (one process per GPU):
+      requester: stage its CSR batch in an IPC-exported buffer (row-wise: K1
+                 route + fx_bucket first, so each owner's slice is a CSR of
+                 its own rows);
+      barrier A: every rank's batch is staged;
+      owner:     ONE K4 launch over all requesters' bags of the tables it
+                 hosts: indices/offsets are read through IPC-mapped pointers
+                 over NVLink, rows are gathered from local HBM, and the pooled
+                 rows are stored straight into the requester's output (table-
+                 wise: final f32 rows; row-wise: f64 partials into the
+                 requester's per-source slot), with a system-scope fence;
+      barrier B: all owners' stores have landed;
+      requester: row-wise only -> K5 combine (ascending source rank).
+    The pooled "all-to-all" therefore overlaps the HBM gather bag by bag."""
+
+    def __init__(self, metas, placement, seed: int, feature_tables, feature_ops, batch_size: int, rank: int,
+                 world: int, device, group=None, mode: str = "tablewise", max_nnz: int | None = None):
+        from . import _lib
+        from .pooling import op_code
+        self._lib = _lib
+        if mode not in ("tablewise", "rowwise"):
+            raise ConfigError(f"unknown sharding mode {mode!r}")
+        self.metas = {m.table_id: m for m in metas}
+        self.rank, self.world, self.mode, self.group = rank, world, mode, group
+        self.device = torch.device(device)
+        self.B = batch_size
+        self.ftab, self.fops = tuple(feature_tables), tuple(feature_ops)
+        self.F = len(self.ftab)
+        dims = {self.metas[t].dim for t in self.ftab}
+        if len(dims) != 1:
+            raise ConfigError("sharded lookup needs one embedding dim across features")
+        self.D = D = dims.pop()
+        B, F, W = self.B, self.F, world
+        self.n_bags = n_bags = B * F
+        self.ops = FlexOps(self.metas, placement, seed, rank, self.ftab, self.fops, B, self.device)
+        tab_owner = {}
+        for sp in placement:
+            tab_owner.setdefault(sp.table_id, set()).add(sp.server_id)
+        if mode == "tablewise":
+            for t, o in tab_owner.items():
+                if len(o) != 1:
+                    raise ConfigError(f"table-wise mode needs one owner per table (table {t})")
+            self.feat_owner = [next(iter(tab_owner[t])) for t in self.ftab]
+        self.max_nnz = int(max_nnz) if max_nnz is not None else n_bags * 64
+        dev = self.device
+        # IPC-exported staging buffers
+        self.b_idx = DevBuffer(self.max_nnz * 4)
+        self.b_flags = DevBuffer(W * 8)
+        if mode == "tablewise":
+            self.b_offs = DevBuffer((n_bags + 1) * 8)
+            self.b_out = DevBuffer(n_bags * D * 4)
+        else:
+            self.b_offs = DevBuffer(W * (n_bags + 1) * 8)
+            self.b_out = DevBuffer(W * n_bags * D * 8)
+        self.t_idx = _cai_tensor(self.b_idx.ptr, (self.max_nnz,), torch.int32, dev)
+        self.t_flags = _cai_tensor(self.b_flags.ptr, (W,), torch.int64, dev)
+        self.t_flags.zero_()
+        if mode == "tablewise":
+            self.t_offs = _cai_tensor(self.b_offs.ptr, (n_bags + 1,), torch.int64, dev)
+            self.t_out = _cai_tensor(self.b_out.ptr, (B, F * D), torch.float32, dev)
+        else:
+            self.t_offs = _cai_tensor(self.b_offs.ptr, (W, n_bags + 1), torch.int64, dev)
+            self.t_out = _cai_tensor(self.b_out.ptr, (W, n_bags, D), torch.float64, dev)
+        torch.cuda.synchronize(dev)
+        mine = [self.b_idx.handle(), self.b_offs.handle(), self.b_out.handle(), self.b_flags.handle()]
+        allh = [None] * W
+        dist.all_gather_object(allh, mine, group=group)
+        self._opened = []
+        ptrs = []
+        for q in range(W):
+            if q == rank:
+                ptrs.append((self.b_idx.ptr, self.b_offs.ptr, self.b_out.ptr, self.b_flags.ptr))
+            else:
+                opened = tuple(_ipc_open(h) for h in allh[q])
+                self._opened.extend(opened)
+                ptrs.append(opened)
+        self.peer_ptrs = ptrs
+        self.t_peer_flags = torch.tensor([p[3] for p in ptrs], dtype=torch.int64, device=dev)
+        self.t_timeout = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.epoch = 0
+        # owner segments over every requester's bags (virtual bag space)
+        segs = []
+        vb = 0
+        for q in range(W):
+            qidx, qoffs, qout, _ = ptrs[q]
+            for f in range(F):
+                t = self.ftab[f]
+                if mode == "tablewise":
+                    if self.feat_owner[f] != rank:
+                        continue
+                    data, rb, re = self.ops.local[t]
+                    out_ptr = qout + f * D * 4
+                    stride = F * D
+                    offs_ptr = qoffs + f * B * 8
+                else:
+                    if t in self.ops.local:
+                        data, rb, re = self.ops.local[t]
+                        tp = data.data_ptr()
+                    else:
+                        tp, rb, re = 0, 0, 0
+                    out_ptr = qout + (rank * n_bags + f * B) * D * 8
+                    stride = D
+                    offs_ptr = qoffs + (rank * (n_bags + 1) + f * B) * 8
+                tp = data.data_ptr() if mode == "tablewise" else tp
+                segs.append(_lib.FxSegment(tp, rb, re, vb, vb + B, out_ptr, stride, D, D, op_code(self.fops[f]),
+                                           qidx, offs_ptr))
+                vb += B
+        self.n_vbags = vb
+        from .store import make_segments
+        self.segs = make_segments(segs, dev) if segs else None
+        self.n_segs = len(segs)
+        self.bag_ops = torch.tensor(np.repeat([op_code(o) for o in self.fops], B).astype(np.int32), device=dev)
+        if mode == "rowwise":
+            self._pp = torch.tensor([self.b_out.ptr + s * n_bags * D * 8 for s in range(W)], dtype=torch.int64,
+                                    device=dev)
+            self._tmp = torch.empty((n_bags, D), dtype=torch.float32, device=dev)
+        self.profile = False
+        self.timeline = []
+
+    def _barrier(self):
+        L = self._lib
+        self.epoch += 1
+        L.check(L.lib.fx_peer_barrier(self.b_flags.ptr, self.t_peer_flags.data_ptr(), self.rank, self.world,
+                                      self.epoch, self.t_timeout.data_ptr(), L.stream_ptr()), "peer barrier")
+
+    def _mark(self, phase):
+        if not self.profile:
+            return None
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record()
+        return (phase, ev)
+
+    def _close(self, tok):
+        if tok is not None:
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record()
+            self.timeline.append((tok[0], tok[1], ev))
+
+    def phase_ms(self) -> dict:
+        torch.cuda.synchronize()
+        out = {}
+        for ph, a, b in self.timeline:
+            out[ph] = out.get(ph, 0.0) + a.elapsed_time(b)
+        self.timeline = []
+        return out
+
+    def lookup(self, indices: torch.Tensor, offsets: torch.Tensor, out: torch.Tensor | None = None,
+               check: bool = True) -> torch.Tensor:
+        """Pool this rank's batch. Returns [B, F*D] f32 (the internal output
+        buffer unless `out` is given; valid until the next call)."""
+        L = self._lib
+        B, F, D, W = self.B, self.F, self.D, self.world
+        nnz = int(indices.numel())
+        if nnz > self.max_nnz:
+            raise ConfigError(f"batch has {nnz} indices, staging holds {self.max_nnz}")
+        tok = self._mark("stage")
+        if self.mode == "tablewise":
+            # ingress validation on the requester (owners only see their own shards)
+            L.check(L.lib.fx_route(self.ops.route_off.data_ptr(), self.ops.starts.data_ptr(),
+                                   self.ops.owners.data_ptr(), self.ops.nrows.data_ptr(),
+                                   self.ops.bag_table.data_ptr(), indices.data_ptr(), L.idx_type_of(indices),
+                                   offsets.data_ptr(), self.n_bags, None, self.ops.status.err.data_ptr(),
+                                   self.ops.status.code.data_ptr(), L.stream_ptr()), "validate")
+            self.t_idx[:nnz].copy_(indices, non_blocking=True)
+            self.t_offs.copy_(offsets, non_blocking=True)
+        else:
+            send_idx, dcount, bcount = self.ops.route_bucket(indices, offsets, W)
+            self.t_idx[:nnz].copy_(send_idx, non_blocking=True)
+            # per-destination CSR offsets into the bucketed index array
+            c = torch.cumsum(bcount.reshape(-1).long(), 0)
+            flat = torch.zeros(W * self.n_bags + 1, dtype=torch.int64, device=self.device)
+            flat[1:] = c
+            self.t_offs[:, :self.n_bags].copy_(flat[:-1].view(W, self.n_bags))
+            self.t_offs[:, self.n_bags:].copy_(flat[1:].view(W, self.n_bags)[:, -1:])
+            self._counts = bcount
+        self._close(tok)
+        tok = self._mark("barrier")
+        self._barrier()
+        self._close(tok)
+        tok = self._mark("pool")
+        if self.n_segs:
+            L.check(L.lib.fx_gather_pool(self.segs.data_ptr(), self.n_segs, D, self.t_idx.data_ptr(), L.FX_IDX_I32,
+                                         None, self.n_vbags,
+                                         (L.FX_OUT_F32 if self.mode == "tablewise" else L.FX_OUT_F64_PARTIAL)
+                                         | L.FX_OUT_SYSFENCE, None, self.ops.status.err.data_ptr(),
+                                         L.FX_E_ROUTING_VIOLATION, self.ops.status.code.data_ptr(), L.stream_ptr()),
+                    "fused pool")
+        self._close(tok)
+        tok = self._mark("barrier")
+        self._barrier()
+        self._close(tok)
+        if self.mode == "tablewise":
+            res = self.t_out
+        else:
+            tok = self._mark("combine")
+            cptr = torch.tensor([self._counts[s].data_ptr() for s in range(W)], dtype=torch.int64, device=self.device)
+            L.check(L.lib.fx_combine(self._pp.data_ptr(), cptr.data_ptr(), W, D, None, None, self.n_bags, D, 0,
+                                     self.bag_ops.data_ptr(), self._tmp.data_ptr(), D, None, L.stream_ptr()),
+                    "combine")
+            res = self._tmp.view(F, B, D).transpose(0, 1).reshape(B, F * D)
+            self._close(tok)
+        if out is not None:
+            out.copy_(res)
+            res = out
+        if check:
+            self.ops.check()
+            if int(self.t_timeout.item()):
+                raise RuntimeError("peer barrier timed out (a rank stopped participating)")
+        return res
+
+    def close(self):
+        L = self._lib
+        torch.cuda.synchronize(self.device)
+        for p in self._opened:
+            L.lib.fx_ipc_close(p)
+        self._opened = []

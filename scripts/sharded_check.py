@@ -9,13 +9,15 @@ import torch.distributed as dist
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import oracle as O  # noqa: E402
-from paper_2410_12794_b200.sharded import ShardedLookup, rowwise_placement, tablewise_placement  # noqa: E402
+from paper_2410_12794_b200.sharded import (P2PShardedLookup, ShardedLookup, rowwise_placement,  # noqa: E402
+                                           tablewise_placement)
 from paper_2410_12794_b200.store import TableMeta  # noqa: E402
 from paper_2410_12794_b200.workload import DlrmBatchGen  # noqa: E402
 
 
 def main():
     mode = sys.argv[1] if len(sys.argv) > 1 else "tablewise"
+    exchange = sys.argv[2] if len(sys.argv) > 2 else "nccl"
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -25,7 +27,8 @@ def main():
     D, B = 128, 96
     metas = [TableMeta(t, n, D) for t, n in enumerate(rows)]
     placement = (tablewise_placement if mode == "tablewise" else rowwise_placement)(rows, world)
-    sl = ShardedLookup(metas, placement, 0, tuple(range(len(rows))), ops, B, rank, world, f"cuda:{local}", mode=mode)
+    cls = P2PShardedLookup if exchange == "p2p" else ShardedLookup
+    sl = cls(metas, placement, 0, tuple(range(len(rows))), ops, B, rank, world, f"cuda:{local}", mode=mode)
     worst, exact, n = 0.0, 0, 0
     for it in range(3):
         hb = DlrmBatchGen(rows, 1.0, B, (1, 40), seed=100 * rank + it, ops=ops, permute=(mode == "rowwise")).next()
@@ -41,7 +44,7 @@ def main():
     t = torch.tensor([worst, float(n - exact)], device="cuda", dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     if rank == 0:
-        print(f"SHARDED {mode} world={world} worst_tolerance_ratio={t[0].item():.4f} "
+        print(f"SHARDED {mode} {exchange} world={world} worst_tolerance_ratio={t[0].item():.4f} "
               f"max_non_bit_exact_bags={int(t[1].item())} bags_per_rank={n}", flush=True)
     ok = t[0].item() <= 1.0
     dist.destroy_process_group()

@@ -40,4 +40,4 @@ def test_host_helpers_without_gpu():
 
 def test_segment_struct_layout():
     import paper_2410_12794_b200._lib as L
-    assert L.SEGMENT_BYTES == 8 * 8 + 4 + 4
+    assert L.SEGMENT_BYTES == 8 * 8 + 4 + 4 + 2 * 8

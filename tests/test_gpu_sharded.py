@@ -10,15 +10,16 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
+@pytest.mark.parametrize("exchange", ["nccl", "p2p"])
 @pytest.mark.parametrize("mode", ["tablewise", "rowwise"])
-def test_sharded_multi_gpu(mode):
+def test_sharded_multi_gpu(mode, exchange):
     n = torch.cuda.device_count() if torch.cuda.is_available() else 0
     if n < 2:
         pytest.skip("needs >= 2 GPUs")
     w = min(n, 4)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={w}",
            "--master-addr", "127.0.0.1", "--master-port", "29571", os.path.join(ROOT, "scripts", "sharded_check.py"),
-           mode]
+           mode, exchange]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
-    assert f"SHARDED {mode}" in r.stdout
+    assert f"SHARDED {mode} {exchange}" in r.stdout
