@@ -282,23 +282,24 @@ static int pool_variant() {
   return v;
 }
 
-template <int NCH, typename IdxT, int MODE>
+template <int G, int NCH, typename IdxT, int MODE>
 static void launch_async(const fx_segment *segs, int n_segs, int dim, const IdxT *ix, const int64_t *offsets,
                          int64_t n_bags, int32_t *counts, int64_t *err, int32_t bad_code, int32_t *err_code,
                          cudaStream_t st, bool sf) {
   constexpr int WARPS = 4;
-  const size_t smem = static_cast<size_t>(WARPS) * 32 * 32 * 16 * NCH;
+  // per group: G rows x (G lanes * 16 B * NCH); 32/G groups per warp
+  const size_t smem = static_cast<size_t>(WARPS) * (32 / G) * G * G * 16 * NCH;
   static int per_sm = -1;
   if (per_sm < 0) {
-    cudaFuncSetAttribute(k_pool_async<NCH, IdxT, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_pool_async<G, NCH, IdxT, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(smem));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pool_async<NCH, IdxT, MODE>, WARPS * 32, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pool_async<G, NCH, IdxT, MODE>, WARPS * 32, smem);
     if (per_sm < 1) per_sm = 1;
   }
   int64_t blocks = static_cast<int64_t>(num_sms()) * per_sm;
-  const int64_t need = (n_bags + WARPS - 1) / WARPS;
+  const int64_t need = (n_bags + WARPS * (32 / G) - 1) / (WARPS * (32 / G));
   if (blocks > need) blocks = need;
-  k_pool_async<NCH, IdxT, MODE><<<static_cast<int>(blocks), WARPS * 32, smem, st>>>(
+  k_pool_async<G, NCH, IdxT, MODE><<<static_cast<int>(blocks), WARPS * 32, smem, st>>>(
       segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code, sf);
 }
 
@@ -325,9 +326,15 @@ static int launch_pool(const fx_segment *segs, int n_segs, int dim, const void *
   const IdxT *ix = static_cast<const IdxT *>(indices);
   const int var = pool_variant();
   if (var == 1 && dim == 128) {
-    launch_async<1, IdxT, MODE>(segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code, st, sf);
+    launch_async<32, 1, IdxT, MODE>(segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code, st, sf);
   } else if (var == 1 && dim == 256) {
-    launch_async<2, IdxT, MODE>(segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code, st, sf);
+    launch_async<32, 2, IdxT, MODE>(segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code, st, sf);
+  } else if (var == 1 && dim == 64) {
+    launch_async<16, 1, IdxT, MODE>(segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code, st, sf);
+  } else if (var == 1 && dim == 32) {
+    launch_async<8, 1, IdxT, MODE>(segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code, st, sf);
+  } else if (var == 1 && dim == 512) {
+    launch_async<32, 4, IdxT, MODE>(segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code, st, sf);
   } else if (var == 2 && dim == 128) {
     launch_prefetch<32, 1, 8, IdxT, MODE>(segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code,
                                           st, sf);

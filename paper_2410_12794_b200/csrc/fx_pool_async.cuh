@@ -47,27 +47,33 @@ __device__ __forceinline__ void emit_bag(const fx_segment &sg, int64_t bag, int6
   }
 }
 
-// Async-staged variant (dim == 128*NCH): persistent warps, one bag per warp at
-// a time. All rows of a 32-index chunk are copied global->shared with
-// cp.async (16 B per lane per row, no register staging), so the whole bag is
-// in flight at once; while the copies land the warp prefetches the NEXT bag's
-// offsets and first index chunk. Rows are then summed from shared memory.
-template <int NCH, typename IdxT, int MODE>
+// Async-staged variant (dim == 4*G*NCH): persistent warps, a group of G lanes
+// owns one bag at a time (32/G bags per warp). All rows of a G-index chunk
+// are copied global->shared with cp.async (16 B per lane per row, no
+// register staging), so the whole bag is in flight at once; while the copies
+// land the group prefetches the NEXT bag's offsets and first index chunk.
+// Rows are then summed from shared memory in index order.
+template <int G, int NCH, typename IdxT, int MODE>
 __global__ void __launch_bounds__(128) k_pool_async(const fx_segment *__restrict__ segs, int n_segs, int dim,
                                                     const IdxT *__restrict__ indices_g,
                                                     const int64_t *__restrict__ offsets, int64_t n_bags,
                                                     int32_t *__restrict__ counts, int64_t *err, int32_t bad_code,
                                                     int32_t *err_code, bool sysfence) {
-  constexpr int ROWB = 32 * 16 * NCH;  // bytes per row
+  constexpr int ROWB = G * 16 * NCH;  // bytes per row
+  constexpr int GPW = 32 / G;
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31;
+  const int gl = lane % G;
+  const int gw = lane / G;
+  const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (gw * G));
   const int wib = threadIdx.x >> 5;
-  unsigned char *buf = smem + static_cast<size_t>(wib) * 32 * ROWB;
+  unsigned char *buf = smem + (static_cast<size_t>(wib) * GPW + gw) * G * ROWB;
   const uint32_t sbuf = static_cast<uint32_t>(__cvta_generic_to_shared(buf));
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t step = nwarps * GPW;
 
-  int64_t bag = warp;
+  int64_t bag = warp * GPW + gw;
   if (bag >= n_bags) {
     if (sysfence) __threadfence_system();
     return;
@@ -76,7 +82,7 @@ __global__ void __launch_bounds__(128) k_pool_async(const fx_segment *__restrict
   int64_t beg, end;
   bag_bounds(segs, s, bag, offsets, beg, end);
   const IdxT *indices = seg_indices(segs, s, indices_g);
-  IdxT pidx = (beg + lane < end) ? indices[beg + lane] : IdxT(0);
+  IdxT pidx = (beg + gl < end) ? indices[beg + gl] : IdxT(0);
 
   while (bag < n_bags) {
     const float *__restrict__ tab = segs[s].table;
@@ -84,53 +90,53 @@ __global__ void __launch_bounds__(128) k_pool_async(const fx_segment *__restrict
     double acc[NCH][4];
 #pragma unroll
     for (int k = 0; k < NCH; ++k) acc[k][0] = acc[k][1] = acc[k][2] = acc[k][3] = 0.0;
-    const int64_t nbag = bag + nwarps;
+    const int64_t nbag = bag + step;
     const int ns = nbag < n_bags ? find_segment(segs, n_segs, nbag) : s;
     const IdxT *nindices = seg_indices(segs, ns, indices_g);
     int64_t nbeg = 0, nend = 0;
     IdxT nidx = IdxT(0);
     bool have_next = false;
-    for (int64_t c0 = beg; c0 < end; c0 += 32) {
-      const int n = static_cast<int>((end - c0) < 32 ? (end - c0) : 32);
+    for (int64_t c0 = beg; c0 < end; c0 += G) {
+      const int n = static_cast<int>((end - c0) < G ? (end - c0) : (int64_t)G);
       const int64_t idx = static_cast<int64_t>(pidx);
       int64_t my_off = 0;
-      if (lane < n) {
-        if (idx < rb || idx >= re) record_bad(err, err_code, c0 + lane, bad_code);
+      if (gl < n) {
+        if (idx < rb || idx >= re) record_bad(err, err_code, c0 + gl, bad_code);
         else my_off = (idx - rb) * ld;
       }
       for (int r = 0; r < n; ++r) {
-        const float *src = tab + __shfl_sync(0xffffffffu, my_off, r);
+        const float *src = tab + __shfl_sync(gmask, my_off, r, G);
 #pragma unroll
-        for (int k = 0; k < NCH; ++k) cp_async16(sbuf + r * ROWB + (k * 32 + lane) * 16, src + (k * 32 + lane) * 4);
+        for (int k = 0; k < NCH; ++k) cp_async16(sbuf + r * ROWB + (k * G + gl) * 16, src + (k * G + gl) * 4);
       }
       cp_async_commit();
       // overlap the copies with the next chunk's / next bag's index loads
-      if (c0 + 32 < end) {
-        pidx = (c0 + 32 + lane < end) ? indices[c0 + 32 + lane] : IdxT(0);
+      if (c0 + G < end) {
+        pidx = (c0 + G + gl < end) ? indices[c0 + G + gl] : IdxT(0);
       } else if (nbag < n_bags) {
         bag_bounds(segs, ns, nbag, offsets, nbeg, nend);
-        nidx = (nbeg + lane < nend) ? nindices[nbeg + lane] : IdxT(0);
+        nidx = (nbeg + gl < nend) ? nindices[nbeg + gl] : IdxT(0);
         have_next = true;
       }
       cp_async_wait_all();
-      __syncwarp();
+      __syncwarp(gmask);
       for (int r = 0; r < n; ++r) {
 #pragma unroll
         for (int k = 0; k < NCH; ++k) {
-          const float4 v = *reinterpret_cast<const float4 *>(buf + r * ROWB + (k * 32 + lane) * 16);
+          const float4 v = *reinterpret_cast<const float4 *>(buf + r * ROWB + (k * G + gl) * 16);
           acc[k][0] += static_cast<double>(v.x);
           acc[k][1] += static_cast<double>(v.y);
           acc[k][2] += static_cast<double>(v.z);
           acc[k][3] += static_cast<double>(v.w);
         }
       }
-      __syncwarp();
+      __syncwarp(gmask);
     }
     if (!have_next && nbag < n_bags) {
       bag_bounds(segs, ns, nbag, offsets, nbeg, nend);
-      nidx = (nbeg + lane < nend) ? nindices[nbeg + lane] : IdxT(0);
+      nidx = (nbeg + gl < nend) ? nindices[nbeg + gl] : IdxT(0);
     }
-    emit_bag<NCH, MODE>(segs[s], bag, end - beg, acc, lane, 32, counts);
+    emit_bag<NCH, MODE>(segs[s], bag, end - beg, acc, gl, G, counts);
     bag = nbag;
     s = ns;
     indices = nindices;

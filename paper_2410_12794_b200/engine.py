@@ -207,3 +207,65 @@ class HostLookup:
         torch.cuda.current_stream().synchronize()
         eng.raise_if_bad(dev_batch)
         return out_host
+
+    def stream(self, batches_host, depth: int = 3):
+        """Pipelined host API (the reference's pipeline_depth batches in
+        flight, ranker.py:161-168): yields one pinned host output per input
+        batch, in order. H2D of batch i+1, K4 of batch i and D2H of batch i-1
+        run concurrently on three streams (PCIe is full duplex), so steady
+        state is bound by the larger copy, not by their sum. A yielded tensor
+        is valid until the generator is advanced (its slot is then reused).
+        Validation errors are raised after the last batch."""
+        eng = self.engine
+        dev = eng.device
+        s_in, s_cmp, s_out = (torch.cuda.Stream(dev) for _ in range(3))
+        slots = [dict() for _ in range(depth)]
+        ev_in = [None] * depth
+        ev_cmp = [None] * depth
+        ev_out = [None] * depth
+        pending = []
+
+        def launch(bh, k):
+            sl = slots[k]
+            with torch.cuda.stream(s_in):
+                if ev_cmp[k] is not None:
+                    s_in.wait_event(ev_cmp[k])  # device inputs of slot k no longer read
+                sl["batch"] = bh.to(dev, non_blocking=True)
+                ev_in[k] = torch.cuda.Event()
+                ev_in[k].record(s_in)
+            with torch.cuda.stream(s_cmp):
+                s_cmp.wait_event(ev_in[k])
+                if ev_out[k] is not None:
+                    s_cmp.wait_event(ev_out[k])  # device output of slot k already copied out
+                B = bh.batch_size
+                if "out" not in sl or sl["out"].shape[0] != B:
+                    sl["out"] = torch.empty((B, eng.out_dim(bh)), dtype=torch.float32, device=dev)
+                eng.pool(sl["batch"], out=sl["out"], check=False, stream=s_cmp)
+                ev_cmp[k] = torch.cuda.Event()
+                ev_cmp[k].record(s_cmp)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(ev_cmp[k])
+                if "host" not in sl or sl["host"].shape != sl["out"].shape:
+                    sl["host"] = torch.empty(sl["out"].shape, dtype=torch.float32, pin_memory=True)
+                sl["host"].copy_(sl["out"], non_blocking=True)
+                ev_out[k] = torch.cuda.Event()
+                ev_out[k].record(s_out)
+
+        i = 0
+        for bh in batches_host:
+            k = i % depth
+            if len(pending) == depth:
+                kk = pending.pop(0)
+                ev_out[kk].synchronize()
+                yield slots[kk]["host"]
+            launch(bh, k)
+            pending.append(k)
+            i += 1
+        while pending:
+            kk = pending.pop(0)
+            ev_out[kk].synchronize()
+            yield slots[kk]["host"]
+        torch.cuda.synchronize(dev)
+        code, _ = eng.status.read()
+        if code:
+            eng.raise_if_bad(slots[0]["batch"])
