@@ -234,6 +234,14 @@ int fx_ipc_open(const unsigned char handle[64], void **out);     /* cudaIpcOpenM
 int fx_ipc_close(void *ptr);
 int fx_can_access_peer(int device, int peer_device);
 int fx_memcpy_async(void *dst, const void *src, size_t bytes, void *stream);
+/* table-wise push: the requester copies, for every feature f, its bag range
+ * (indices as int32 + offsets rebased to the owner's slot) into the staging
+ * of feature f's owner (dst_idx[d] / dst_offs[d]: DEVICE arrays of IPC-mapped
+ * pointers to THIS requester's slot in rank d's staging). feat_pos[f] = rank
+ * of f among its owner's features (ascending f). */
+int fx_push_csr(const void *indices, int32_t idx_type, const int64_t *offsets, int32_t B, int32_t F,
+                const int32_t *feat_owner, const int32_t *feat_pos, int32_t *const *dst_idx, int64_t *const *dst_offs,
+                int32_t sysfence, void *stream);
 /* one-block barrier: release-store `epoch` into peer_flags[r][rank] for every
  * rank r (system scope, after a system fence), then acquire-spin until
  * my_flags[r] >= epoch for every r. peer_flags is a DEVICE array of `world`

@@ -42,6 +42,39 @@ __global__ void k_peer_barrier(int64_t *my_flags, int64_t *const *peer_flags, in
   __threadfence_system();
 }
 
+// Push a requester's table-wise CSR batch to the owners' staging buffers.
+// grid (C, F): blockIdx.y = feature f (owned by rank feat_owner[f], its
+// feat_pos[f]-th owned feature); the C blocks of a feature copy disjoint
+// slices of its index range and of its B+1 rebased offsets.
+template <typename IdxT>
+__global__ void __launch_bounds__(256) k_push_csr(const IdxT *__restrict__ indices, const int64_t *__restrict__ offsets,
+                                                  int B, int F, const int32_t *__restrict__ feat_owner,
+                                                  const int32_t *__restrict__ feat_pos, int32_t *const *dst_idx,
+                                                  int64_t *const *dst_offs, bool sysfence) {
+  const int f = blockIdx.y;
+  const int d = feat_owner[f];
+  __shared__ long long s_base;
+  if (threadIdx.x == 0) {
+    long long base = 0;  // indices of the owner's earlier features in this requester's slot
+    for (int g = 0; g < f; ++g)
+      if (feat_owner[g] == d) base += offsets[(int64_t)(g + 1) * B] - offsets[(int64_t)g * B];
+    s_base = base;
+  }
+  __syncthreads();
+  const long long base = s_base;
+  const int64_t b0 = offsets[(int64_t)f * B], b1 = offsets[(int64_t)(f + 1) * B];
+  int32_t *di = dst_idx[d] + base;
+  const int64_t n = b1 - b0;
+  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t lo = blockIdx.x * per, hi = min(n, lo + per);
+  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) di[i] = static_cast<int32_t>(indices[b0 + i]);
+  int64_t *dof = dst_offs[d] + (int64_t)feat_pos[f] * B;
+  const int64_t pb = (B + 1 + gridDim.x - 1) / gridDim.x;
+  const int64_t olo = blockIdx.x * pb, ohi = min((int64_t)B + 1, olo + pb);
+  for (int64_t s = olo + threadIdx.x; s < ohi; s += blockDim.x) dof[s] = offsets[(int64_t)f * B + s] - b0 + base;
+  if (sysfence) __threadfence_system();
+}
+
 }  // namespace fx
 
 using namespace fx;
@@ -82,6 +115,24 @@ int fx_can_access_peer(int device, int peer_device) {
 int fx_memcpy_async(void *dst, const void *src, size_t bytes, void *stream) {
   if (bytes == 0) return FX_OK;
   return cuda_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, as_stream(stream)), "fx_memcpy_async");
+}
+
+int fx_push_csr(const void *indices, int32_t idx_type, const int64_t *offsets, int32_t B, int32_t F,
+                const int32_t *feat_owner, const int32_t *feat_pos, int32_t *const *dst_idx, int64_t *const *dst_offs,
+                int32_t sysfence, void *stream) {
+  if (B < 1 || F < 1) {
+    set_error("fx_push_csr: bad shape");
+    return FX_E_CONFIG;
+  }
+  dim3 grid(8, F);
+  if (idx_type == FX_IDX_I32)
+    k_push_csr<int32_t><<<grid, 256, 0, as_stream(stream)>>>(static_cast<const int32_t *>(indices), offsets, B, F,
+                                                             feat_owner, feat_pos, dst_idx, dst_offs, sysfence != 0);
+  else
+    k_push_csr<int64_t><<<grid, 256, 0, as_stream(stream)>>>(static_cast<const int64_t *>(indices), offsets, B, F,
+                                                             feat_owner, feat_pos, dst_idx, dst_offs, sysfence != 0);
+  FX_LAUNCH_CHECK("fx_push_csr");
+  return FX_OK;
 }
 
 int fx_peer_barrier(int64_t *my_flags, int64_t *const *peer_flags, int32_t rank, int32_t world, int64_t epoch,

@@ -423,21 +423,25 @@ class P2PShardedLookup:
         self.max_nnz = int(max_nnz) if max_nnz is not None else n_bags * 64
         dev = self.device
         # IPC-exported staging buffers
-        self.b_idx = DevBuffer(self.max_nnz * 4)
         self.b_flags = DevBuffer(W * 8)
         if mode == "tablewise":
-            self.b_offs = DevBuffer((n_bags + 1) * 8)
+            # owner-side staging: one slot per requester holding the indices and
+            # rebased offsets of the features this rank owns (pushed by requesters)
+            self.my_feats = [f for f in range(F) if self.feat_owner[f] == rank]
+            self.n_owned = [sum(1 for f in range(F) if self.feat_owner[f] == r) for r in range(W)]
+            self.b_idx = DevBuffer(W * self.max_nnz * 4)
+            self.b_offs = DevBuffer(W * (len(self.my_feats) * B + 1) * 8)
             self.b_out = DevBuffer(n_bags * D * 4)
         else:
+            self.b_idx = DevBuffer(self.max_nnz * 4)
             self.b_offs = DevBuffer(W * (n_bags + 1) * 8)
             self.b_out = DevBuffer(W * n_bags * D * 8)
-        self.t_idx = _cai_tensor(self.b_idx.ptr, (self.max_nnz,), torch.int32, dev)
         self.t_flags = _cai_tensor(self.b_flags.ptr, (W,), torch.int64, dev)
         self.t_flags.zero_()
         if mode == "tablewise":
-            self.t_offs = _cai_tensor(self.b_offs.ptr, (n_bags + 1,), torch.int64, dev)
             self.t_out = _cai_tensor(self.b_out.ptr, (B, F * D), torch.float32, dev)
         else:
+            self.t_idx = _cai_tensor(self.b_idx.ptr, (self.max_nnz,), torch.int32, dev)
             self.t_offs = _cai_tensor(self.b_offs.ptr, (W, n_bags + 1), torch.int64, dev)
             self.t_out = _cai_tensor(self.b_out.ptr, (W, n_bags, D), torch.float64, dev)
         torch.cuda.synchronize(dev)
@@ -460,27 +464,41 @@ class P2PShardedLookup:
         # owner segments over every requester's bags (virtual bag space)
         segs = []
         vb = 0
-        for q in range(W):
+        if mode == "tablewise":
+            # push targets: this requester's slot in every owner's staging
+            self.t_dst_idx = torch.tensor([ptrs[d][0] + rank * self.max_nnz * 4 for d in range(W)], dtype=torch.int64,
+                                          device=dev)
+            self.t_dst_offs = torch.tensor([ptrs[d][1] + rank * (self.n_owned[d] * B + 1) * 8 for d in range(W)],
+                                           dtype=torch.int64, device=dev)
+            pos = [0] * F
+            cnt = [0] * W
+            for f in range(F):
+                pos[f] = cnt[self.feat_owner[f]]
+                cnt[self.feat_owner[f]] += 1
+            self.t_feat_owner = torch.tensor(self.feat_owner, dtype=torch.int32, device=dev)
+            self.t_feat_pos = torch.tensor(pos, dtype=torch.int32, device=dev)
+            Fm = len(self.my_feats)
+            for q in range(W):
+                qout = ptrs[q][2]
+                lidx = self.b_idx.ptr + q * self.max_nnz * 4
+                loffs = self.b_offs.ptr + q * (Fm * B + 1) * 8
+                for j, f in enumerate(self.my_feats):
+                    data, rb, re = self.ops.local[self.ftab[f]]
+                    segs.append(_lib.FxSegment(data.data_ptr(), rb, re, vb, vb + B, qout + f * D * 4, F * D, D, D,
+                                               op_code(self.fops[f]), lidx, loffs + j * B * 8))
+                    vb += B
+        for q in range(W) if mode == "rowwise" else ():
             qidx, qoffs, qout, _ = ptrs[q]
             for f in range(F):
                 t = self.ftab[f]
-                if mode == "tablewise":
-                    if self.feat_owner[f] != rank:
-                        continue
+                if t in self.ops.local:
                     data, rb, re = self.ops.local[t]
-                    out_ptr = qout + f * D * 4
-                    stride = F * D
-                    offs_ptr = qoffs + f * B * 8
+                    tp = data.data_ptr()
                 else:
-                    if t in self.ops.local:
-                        data, rb, re = self.ops.local[t]
-                        tp = data.data_ptr()
-                    else:
-                        tp, rb, re = 0, 0, 0
-                    out_ptr = qout + (rank * n_bags + f * B) * D * 8
-                    stride = D
-                    offs_ptr = qoffs + (rank * (n_bags + 1) + f * B) * 8
-                tp = data.data_ptr() if mode == "tablewise" else tp
+                    tp, rb, re = 0, 0, 0
+                out_ptr = qout + (rank * n_bags + f * B) * D * 8
+                stride = D
+                offs_ptr = qoffs + (rank * (n_bags + 1) + f * B) * 8
                 segs.append(_lib.FxSegment(tp, rb, re, vb, vb + B, out_ptr, stride, D, D, op_code(self.fops[f]),
                                            qidx, offs_ptr))
                 vb += B
@@ -540,8 +558,10 @@ class P2PShardedLookup:
                                    self.ops.bag_table.data_ptr(), indices.data_ptr(), L.idx_type_of(indices),
                                    offsets.data_ptr(), self.n_bags, None, self.ops.status.err.data_ptr(),
                                    self.ops.status.code.data_ptr(), L.stream_ptr()), "validate")
-            self.t_idx[:nnz].copy_(indices, non_blocking=True)
-            self.t_offs.copy_(offsets, non_blocking=True)
+            L.check(L.lib.fx_push_csr(indices.data_ptr(), L.idx_type_of(indices), offsets.data_ptr(), B, F,
+                                      self.t_feat_owner.data_ptr(), self.t_feat_pos.data_ptr(),
+                                      self.t_dst_idx.data_ptr(), self.t_dst_offs.data_ptr(), 1, L.stream_ptr()),
+                    "push")
         else:
             send_idx, dcount, bcount = self.ops.route_bucket(indices, offsets, W)
             self.t_idx[:nnz].copy_(send_idx, non_blocking=True)
@@ -558,7 +578,7 @@ class P2PShardedLookup:
         self._close(tok)
         tok = self._mark("pool")
         if self.n_segs:
-            L.check(L.lib.fx_gather_pool(self.segs.data_ptr(), self.n_segs, D, self.t_idx.data_ptr(), L.FX_IDX_I32,
+            L.check(L.lib.fx_gather_pool(self.segs.data_ptr(), self.n_segs, D, self.b_idx.ptr, L.FX_IDX_I32,
                                          None, self.n_vbags,
                                          (L.FX_OUT_F32 if self.mode == "tablewise" else L.FX_OUT_F64_PARTIAL)
                                          | L.FX_OUT_SYSFENCE, None, self.ops.status.err.data_ptr(),
