@@ -129,10 +129,39 @@ def pack_batch(batch: Batch, device) -> CsrLayout:
                      segs, lens, np.asarray(lk, np.int64), idx_lists, len(batch.lookups))
 
 
+def pack_csr(indices: torch.Tensor, offsets: torch.Tensor, feature_tables, feature_ops, batch_size: int,
+             device) -> CsrLayout:
+    """Table-major CSR (bag = f*B + s, the engine's layout) -> CsrLayout."""
+    F, B = len(feature_tables), batch_size
+    dev = torch.device(device)
+    idx = indices.to(device=dev, dtype=torch.int64)
+    offs = offsets.to(device=dev, dtype=torch.int64)
+    lens = (offs[1:] - offs[:-1]).view(F, B)
+    sm = (torch.cumsum(lens.t().reshape(-1), 0) - lens.t().reshape(-1)).view(B, F).t().reshape(-1).contiguous()
+    ops = [op_code(o) for o in feature_ops]
+    segs, b = [], 0
+    for f in range(F):
+        if segs and segs[-1][0] == feature_tables[f] and segs[-1][1] == ops[f]:
+            segs[-1] = (segs[-1][0], segs[-1][1], segs[-1][2], b + B)
+        else:
+            segs.append((int(feature_tables[f]), ops[f], b, b + B))
+        b += B
+    bag_table = torch.tensor(np.repeat(np.asarray(feature_tables, np.int32), B), device=dev)
+    return CsrLayout(idx, offs, bag_table, sm, _tm_to_sm(F, B), segs, None, None, None, B)
+
+
+def _tm_to_sm(F, B):
+    """perm[tm_bag] = sample-major bag id (s*F + f) for tm_bag = f*B + s."""
+    f = np.repeat(np.arange(F), B)
+    s_ = np.tile(np.arange(B), F)
+    return s_ * F + f
+
+
 class Ranker:
     def __init__(self, deployment: Deployment, routing: RoutingTable, transport=None,
                  params: RankerParams | None = None, cache: AdaptiveCache | None = None,
-                 policy: CachePolicy | None = None, tracker: LoadTracker | None = None, device=None):
+                 policy: CachePolicy | None = None, tracker: LoadTracker | None = None, device=None,
+                 hits_from_cache: bool = True):
         self.deployment = deployment
         self.routing = routing
         self.transport = transport
@@ -162,6 +191,16 @@ class Ranker:
                                               device=self.device)
         if cache is not None:
             cache.bind_tables(deployment)
+        # one shard per table: a single fused K4 launch pools whole bags (no
+        # per-shard partials). Cache-hit rows are then read from the table copy,
+        # which is bit-identical to the cached row; `hits_from_cache` keeps the
+        # faithful path (hit rows read from the cache slots) when a cache is on.
+        per_table = {}
+        for spec in routing.shard_list:
+            per_table[spec.table_id] = per_table.get(spec.table_id, 0) + 1
+        self._single_shard = all(v == 1 for v in per_table.values())
+        self._table_shard = {s[4]: s for s in self._shards} if self._single_shard else {}
+        self.hits_from_cache = hits_from_cache
 
     # -- driving ----------------------------------------------------------------
 
@@ -188,27 +227,61 @@ class Ranker:
         raise InvariantError("device validation flagged an index the host check accepts")
 
     def _admission_check(self, batch: Batch) -> None:
+        self._admission_check_size(batch.size, batch.batch_id)
+
+    def _admission_check_size(self, size: int, batch_id: int) -> None:
         if self.cache is None or self.policy is None:
             return
         model = self.policy.model
-        need = model.nn_bytes(batch.size)
+        need = model.nn_bytes(size)
         if need > model.gpu_capacity_bytes:
-            raise CapacityError(f"batch {batch.batch_id} (size {batch.size}) needs {need} NN bytes, "
+            raise CapacityError(f"batch {batch_id} (size {size}) needs {need} NN bytes, "
                                 f"capacity {model.gpu_capacity_bytes}")
         budget = self.cache.budget_bytes
         if need + budget <= model.gpu_capacity_bytes:
             return
         if not self.params.adaptive_cache:
-            raise CapacityError(f"batch {batch.batch_id} (size {batch.size}): NN {need} bytes plus fixed cache "
+            raise CapacityError(f"batch {batch_id} (size {size}): NN {need} bytes plus fixed cache "
                                 f"{budget} exceeds capacity {model.gpu_capacity_bytes}")
-        self.cache.resize(target_cache_bytes(model, batch.size), fetcher=None)
+        self.cache.resize(target_cache_bytes(model, size), fetcher=None)
 
     def _run_batch(self, batch: Batch) -> None:
-        dev = self.device
         for lookup in batch.lookups:
             for f in lookup.features:
                 self.deployment.meta(f.table_id)
-        lay = pack_batch(batch, dev)
+        lay = pack_batch(batch, self.device)
+        res = self._pipeline(lay, batch.size, batch.batch_id, lambda: self._raise_validation(batch))
+        self._emit(batch, lay, *res)
+
+    def execute_csr(self, indices: torch.Tensor, offsets: torch.Tensor, feature_tables, feature_ops,
+                    batch_size: int, batch_id: int = 0):
+        """Batched front end (no per-feature Python objects): table-major CSR
+        in (bag = f*B + s), pooled [B, F*D] f32 + per-bag counter tensors out.
+        Same pipeline, cache semantics and BatchMetrics as execute_batch."""
+        for t in feature_tables:
+            self.deployment.meta(t)
+        lay = pack_csr(indices, offsets, feature_tables, feature_ops, batch_size, self.device)
+
+        def bad():
+            raise LookupValidationError(f"batch {batch_id}: index out of range (CSR batch)")
+        out, hits_bag, pd_groups, pd_rows, raw_rows, nnz, n_groups = self._pipeline(lay, batch_size, batch_id, bad)
+        F, B = len(feature_tables), batch_size
+        dims = {self.deployment.meta(t).dim for t in feature_tables}
+        D = out.shape[1]
+        pooled = out.view(F, B, D).transpose(0, 1).reshape(B, F * D) if len(dims) == 1 else out
+        c = self.cache
+        hits = int(hits_bag.sum()) if c is not None else 0
+        self.batch_metrics.append(BatchMetrics(
+            batch_id=batch_id, size=batch_size, started_at=0.0, latency=0.0, subrequests=n_groups,
+            cache_hits=hits, cache_misses=(nnz - hits) if c is not None else 0,
+            pushdown_groups=int(pd_groups.sum()), pushdown_rows=int(pd_rows.sum()), raw_rows=int(raw_rows.sum()),
+            load_level=self._last_level, cache_budget=(c.budget_bytes if c else None),
+            cache_used=(c.used_bytes if c else None)))
+        return pooled, dict(cache_hits=hits_bag, pushdown_groups=pd_groups, pushdown_rows=pd_rows,
+                            raw_rows=raw_rows)
+
+    def _pipeline(self, lay: CsrLayout, n_lookups: int, batch_id: int, raise_validation):
+        dev = self.device
         nnz = int(lay.indices.numel())
         n_bags = len(lay.perm)
         # 1. ingress validation + routing (K1)
@@ -216,12 +289,12 @@ class Ranker:
         dest, _ = self.routing.route_csr(lay.bag_table, lay.indices, lay.offsets, status=self._status)
         code, _ = self._status.read()
         if code:
-            self._raise_validation(batch)
+            raise_validation()
         cache = self.cache
         # 2. pending admissions, capacity gate
         if cache is not None:
             cache.apply_pending_admissions()
-        self._admission_check(batch)
+        self._admission_check_size(n_lookups, batch_id)
         # 3. dedup + probe (K2, K3)
         hit_occ = torch.zeros(nnz, dtype=torch.bool, device=dev)
         dd = None
@@ -270,11 +343,55 @@ class Ranker:
                 keys = dd.uniq[cand[order]].contiguous()
                 cache.offer_keys(keys, int(keys.numel()))
         # 7. maintenance
-        self._maintenance(batch)
+        self._maintenance_size(n_lookups)
         # results (sample-major)
-        self._emit(batch, lay, out, hits_bag, pd_groups, pd_rows, raw_rows, nnz, n_groups)
+        return out, hits_bag, pd_groups, pd_rows, raw_rows, nnz, n_groups
 
     def _pool(self, lay: CsrLayout, dest, hit_occ, dd, nnz, n_bags) -> torch.Tensor:
+        dims = {self.deployment.meta(t).dim for t, *_ in lay.segs}
+        if self._single_shard and len(dims) == 1 and (self.cache is None or not self.hits_from_cache):
+            return self._pool_fused(lay, n_bags)
+        return self._pool_partials(lay, dest, hit_occ, dd, nnz, n_bags)
+
+    def _pool_fused(self, lay: CsrLayout, n_bags) -> torch.Tensor:
+        """One K4 launch over the whole batch (f64 accumulate, one rounding)."""
+        dev = self.device
+        dims = {self.deployment.meta(t).dim for t, *_ in lay.segs}
+        D = max(dims) if dims else 1
+        out = torch.zeros((n_bags, D), dtype=torch.float32, device=dev)
+        if n_bags == 0:
+            return out
+        for dim in sorted(dims):
+            segs = []
+            for (t, opc, b0, b1) in lay.segs:
+                if self.deployment.meta(t).dim != dim:
+                    continue
+                tab, start, end, _, _ = self._table_shard[t]
+                segs.append(_lib.FxSegment(tab.data_ptr(), start, end, b0, b1, out.data_ptr() + b0 * D * 4, D,
+                                           tab.stride(0), dim, opc))
+            seg_dev = make_segments(self._cover_out(segs, n_bags, D, out), dev)
+            _lib.check(_lib.lib.fx_gather_pool(seg_dev.data_ptr(), seg_dev.numel() // _lib.SEGMENT_BYTES, dim,
+                                               lay.indices.data_ptr(), _lib.FX_IDX_I64, lay.offsets.data_ptr(),
+                                               n_bags, _lib.FX_OUT_F32, None, self._status.err.data_ptr(),
+                                               _lib.FX_E_ROUTING_VIOLATION, self._status.code.data_ptr(),
+                                               _lib.stream_ptr()), "fused pool")
+        return out
+
+    @staticmethod
+    def _cover_out(segs, n_bags, D, out):
+        """Cover [0, n_bags) with segments; gaps (bags of another dim) get a
+        scratch segment whose output lands in a throw-away row range."""
+        res, cursor = [], 0
+        for sg in sorted(segs, key=lambda s: s.bag_begin):
+            if sg.bag_begin > cursor:
+                raise InvariantError("mixed-dim batches take the partial path")
+            res.append(sg)
+            cursor = sg.bag_end
+        if cursor < n_bags:
+            raise InvariantError("mixed-dim batches take the partial path")
+        return res
+
+    def _pool_partials(self, lay: CsrLayout, dest, hit_occ, dd, nnz, n_bags) -> torch.Tensor:
         """Partial pool per shard (K4 FX_OUT_F64_PARTIAL over that shard's miss
         occurrences, bucketed in (bag, position) order by fx_bucket), then K5
         folds partials in ascending shard order plus cache rows in position order."""
@@ -370,10 +487,13 @@ class Ranker:
         return out
 
     def _maintenance(self, batch: Batch) -> None:
+        self._maintenance_size(batch.size)
+
+    def _maintenance_size(self, size: int) -> None:
         c = self.cache
         if c is None or self.tracker is None or self.policy is None:
             return
-        level = self.tracker.record_batch(batch.size)
+        level = self.tracker.record_batch(size)
         self._last_level = level.value
         if not self.params.adaptive_cache:
             return

@@ -103,3 +103,45 @@ def test_counters_examples(P):
     assert res[0].counters == (2, 1, 1) and res[0].pushdown_rows == 3
     ref = O.pool_flat(O.rows_of(0, 0, 64, [5, 150, 10, 11, 12, 120]), "mean")
     assert O.within_tolerance(ref, res[0].vectors[0])
+
+
+def test_execute_csr_and_fused_path_match_execute_batch(P):
+    """The batched CSR front end (execute_csr) and the single-fused-launch
+    pooling (hits_from_cache=False) reproduce execute_batch exactly: pooled
+    vectors bit-for-bit, counters, metrics and cache state."""
+    from paper_2410_12794_b200 import cache as C
+    from paper_2410_12794_b200.ranker import Ranker, RankerParams
+    from paper_2410_12794_b200.workload import DlrmBatchGen
+    rows, D, B = (3000, 500, 1200), 32, 48
+    metas = [P.TableMeta(t, n, D) for t, n in enumerate(rows)]
+    placement = [P.ShardSpec(t, 0, n, 0) for t, n in enumerate(rows)]
+    dep = P.init_store(metas, placement, 0)
+    ops = ("sum", "mean", "sum")
+
+    def mk(hfc):
+        cache = C.AdaptiveCache(150 * D * 4, admission="sketch", max_dim=D, record_evictions=True)
+        model = C.MemoryModel(150 * D * 4 + 1000, 1000, 1)
+        return Ranker(dep, P.build_routing(metas, placement), None, RankerParams(pushdown_threshold=None,
+                                                                                 admit_per_batch=8),
+                      cache=cache, policy=C.CachePolicy(model), tracker=C.LoadTracker(4, 512, 16),
+                      hits_from_cache=hfc)
+    ra, rb, rc = mk(True), mk(True), mk(False)
+    gen = DlrmBatchGen(rows, 1.1, B, (1, 9), seed=4, ops=ops)
+    for bi in range(5):
+        hb = gen.next()
+        lk = hb.to_lists()
+        batch = P.Batch(bi, bi, [P.LookupRequest([P.Feature(t, P.PoolingOp(op), ix) for t, op, ix in l]) for l in lk])
+        res = ra.execute_batch(batch)
+        idx, offs = torch.from_numpy(hb.indices).cuda(), torch.from_numpy(hb.offsets).cuda()
+        pb, cb = rb.execute_csr(idx, offs, hb.feature_tables, hb.feature_ops, B, batch_id=bi)
+        pc, cc = rc.execute_csr(idx, offs, hb.feature_tables, hb.feature_ops, B, batch_id=bi)
+        ref = np.stack([np.concatenate(r.vectors) for r in res])
+        assert np.array_equal(ref, pb.cpu().numpy()) and np.array_equal(ref, pc.cpu().numpy())
+        ma, mb, mc = ra.batch_metrics[-1], rb.batch_metrics[-1], rc.batch_metrics[-1]
+        for m in (mb, mc):
+            assert (m.cache_hits, m.cache_misses, m.raw_rows, m.subrequests) == \
+                (ma.cache_hits, ma.cache_misses, ma.raw_rows, ma.subrequests)
+        hits_sm = np.array([r.cache_hits for r in res])
+        assert np.array_equal(cb["cache_hits"].view(len(rows), B).sum(0).cpu().numpy(), hits_sm)
+        assert ra.cache.lru_entries() == rb.cache.lru_entries() == rc.cache.lru_entries()
+    assert ra.batch_metrics[-1].cache_hits > 0
