@@ -194,6 +194,8 @@ def main():
     ap.add_argument("--alpha", type=float, default=None, help="override Zipf alpha (0 = uniform cold control)")
     ap.add_argument("--table-rows", type=int, default=None, help="override every table's row count (cold control)")
     ap.add_argument("--mode", default="tablewise", choices=["tablewise", "rowwise"], help="N>1 sharding")
+    ap.add_argument("--replicate-rows", type=int, default=0,
+                    help="N>1 table-wise: replicate tables with <= this many rows on every rank (hybrid placement)")
     ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
                     help="N>1 pooled-result exchange: fused NVLink peer stores (p2p) or NCCL all-to-all")
     args = ap.parse_args()
@@ -359,12 +361,24 @@ def run_sharded(args, rank, world, local):
     rows, dim, B = cfg["table_rows"], cfg["dim"], cfg["batch"]
     F = len(rows)
     mode = args.mode
-    placement = (tablewise_placement if mode == "tablewise" else rowwise_placement)(rows, world)
+    repl = [t for t, n in enumerate(rows) if n <= args.replicate_rows] if mode == "tablewise" else []
+    big = [t for t in range(F) if t not in repl]
+    if mode == "tablewise":
+        sub = tablewise_placement([rows[t] for t in big], world)
+        from paper_2410_12794_b200.store import ShardSpec
+        placement = [ShardSpec(big[s.table_id], s.start, s.end, s.server_id) for s in sub]
+    else:
+        placement = rowwise_placement(rows, world)
     metas = [TableMeta(t, n, dim) for t, n in enumerate(rows)]
     dev = torch.device("cuda", local)
     t0 = time.perf_counter()
-    cls = P2PShardedLookup if args.exchange == "p2p" else ShardedLookup
-    sl = cls(metas, placement, 0, tuple(range(F)), ("sum",) * F, B, rank, world, dev, mode=mode)
+    if args.exchange == "p2p":
+        sl = P2PShardedLookup(metas, placement, 0, tuple(range(F)), ("sum",) * F, B, rank, world, dev, mode=mode,
+                              replicated_tables=repl)
+    else:
+        if repl:
+            raise SystemExit("--replicate-rows needs --exchange p2p")
+        sl = ShardedLookup(metas, placement, 0, tuple(range(F)), ("sum",) * F, B, rank, world, dev, mode=mode)
     torch.cuda.synchronize()
     init_s = time.perf_counter() - t0
     batches = [(torch.from_numpy(hb.indices).to(dev), torch.from_numpy(hb.offsets).to(dev)) for hb in host_batches]
@@ -398,6 +412,9 @@ def run_sharded(args, rank, world, local):
     # owner-pool algorithmic bytes: every rank pools, for each requester, the
     # rows routed to it; measured on this rank over the timed steps
     t = torch.tensor([ms, phases.get("pool", 0.0), phases.get("a2a", 0.0)], device=dev, dtype=torch.float64)
+    allpool = [torch.zeros(1, device=dev, dtype=torch.float64) for _ in range(world)]
+    dist.all_gather(allpool, t[1:2].clone())
+    pool_ms_ranks = [round(float(x.item()) / args.steps, 4) for x in allpool]
     tmax = t.clone()
     dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
     ms_max = float(tmax[0].item())
@@ -417,7 +434,7 @@ def run_sharded(args, rank, world, local):
     total_alg = sum(algorithmic_bytes(hb, dim) for hb in host_batches) / len(host_batches)
     if mode == "tablewise":
         owned = sum(1 for s in placement if s.server_id == rank)
-        share = owned / F
+        share = (owned * world + len(repl)) / (F * world)
     else:
         share = 1.0 / world
     pool_bytes_step = total_alg * world * share
@@ -459,13 +476,15 @@ def run_sharded(args, rank, world, local):
             "config": {"workload": cfg["name"] + f"-{mode}", "global_batch": B * world, "per_gpu_batch": B,
                        "pooling": list(cfg["pooling"]) if isinstance(cfg["pooling"], tuple) else cfg["pooling"],
                        "alpha": cfg["alpha"], "dim": dim, "tables": F,
-                       "parallelism": f"{mode}-sharded x{world} ({args.exchange} exchange)",
+                       "parallelism": f"{mode}-sharded x{world} ({args.exchange} exchange)"
+                                      + (f", {len(repl)} small tables replicated" if repl else ""),
                        "l2": "inputs larger than L2 (1.18 GB algorithmic bytes per rank-batch)",
                        "init_store_s": round(init_s, 2)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": None,
                          "peak_source": peak_src, "kernel": "owner gather+pool (K4) launches, rank 0",
-                         "bytes_per_step": pool_bytes_step, "pool_ms_per_step": pool_ms},
+                         "bytes_per_step": pool_bytes_step, "pool_ms_per_step": pool_ms,
+                         "pool_ms_per_step_all_ranks": pool_ms_ranks},
             "a2a": {"bytes_sent_per_step_rank0": a2a_bytes, "ms_per_step_rank0": a2a_ms,
                     "gbs": (a2a_bytes / (a2a_ms / 1e3) / 1e9) if a2a_ms > 0 else None,
                     "peak_gbs": 900.0, "phases_ms_total": {k: round(v, 3) for k, v in phases.items()},

@@ -201,6 +201,23 @@ class Ranker:
         self._single_shard = all(v == 1 for v in per_table.values())
         self._table_shard = {s[4]: s for s in self._shards} if self._single_shard else {}
         self.hits_from_cache = hits_from_cache
+        self.profile = False
+        self.stage_ms: dict = {}
+        self._marks = []
+
+    def _mark(self, name):
+        if self.profile:
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record()
+            self._marks.append((name, ev))
+
+    def _flush_marks(self):
+        if not self.profile or not self._marks:
+            return
+        self._marks[-1][1].synchronize()
+        for (n0, e0), (_, e1) in zip(self._marks[:-1], self._marks[1:]):
+            self.stage_ms[n0] = self.stage_ms.get(n0, 0.0) + e0.elapsed_time(e1)
+        self._marks = []
 
     # -- driving ----------------------------------------------------------------
 
@@ -285,6 +302,7 @@ class Ranker:
         nnz = int(lay.indices.numel())
         n_bags = len(lay.perm)
         # 1. ingress validation + routing (K1)
+        self._mark("route")
         self._status.reset()
         dest, _ = self.routing.route_csr(lay.bag_table, lay.indices, lay.offsets, status=self._status)
         code, _ = self._status.read()
@@ -292,10 +310,12 @@ class Ranker:
             raise_validation()
         cache = self.cache
         # 2. pending admissions, capacity gate
+        self._mark("apply_pending")
         if cache is not None:
             cache.apply_pending_admissions()
         self._admission_check_size(n_lookups, batch_id)
         # 3. dedup + probe (K2, K3)
+        self._mark("dedup_probe")
         hit_occ = torch.zeros(nnz, dtype=torch.bool, device=dev)
         dd = None
         if cache is not None and nnz:
@@ -304,6 +324,7 @@ class Ranker:
             cache.probe_unique(dd.uniq, dd.mult, dd.last_ord, None, nnz, slot, n_uniq_host=dd.n_uniq)
             hit_occ = slot[dd.inverse.long()] >= 0
         # 4. miss groups per (bag, server) and the pushdown plan
+        self._mark("plan")
         lens_tm = lay.offsets[1:] - lay.offsets[:-1]
         bag_of_occ = torch.repeat_interleave(torch.arange(n_bags, device=dev), lens_tm)
         n_srv = len(self._server_ids)
@@ -330,7 +351,9 @@ class Ranker:
         raw_rows = (grp * (~push)).sum(1)
         n_groups = int((grp > 0).sum())
         # 5. pooled vectors: per-shard f64 partials of the misses + cache rows as raw
+        self._mark("pool")
         out = self._pool(lay, dest, hit_occ, dd, nnz, n_bags)
+        self._mark("offers")
         # 6. offers: raw-fetched misses, first raw occurrence order
         if cache is not None and nnz:
             raw_occ = miss & ~push.view(-1)[bag_of_occ * n_srv + srv_occ]
@@ -343,7 +366,10 @@ class Ranker:
                 keys = dd.uniq[cand[order]].contiguous()
                 cache.offer_keys(keys, int(keys.numel()))
         # 7. maintenance
+        self._mark("maintenance")
         self._maintenance_size(n_lookups)
+        self._mark("end")
+        self._flush_marks()
         # results (sample-major)
         return out, hits_bag, pd_groups, pd_rows, raw_rows, nnz, n_groups
 

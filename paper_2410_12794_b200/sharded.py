@@ -393,10 +393,18 @@ class P2PShardedLookup:
     The pooled "all-to-all" therefore overlaps the HBM gather bag by bag."""
 
     def __init__(self, metas, placement, seed: int, feature_tables, feature_ops, batch_size: int, rank: int,
-                 world: int, device, group=None, mode: str = "tablewise", max_nnz: int | None = None):
+                 world: int, device, group=None, mode: str = "tablewise", max_nnz: int | None = None,
+                 replicated_tables=()):
+        """`replicated_tables` (table-wise mode): tables held in full by every
+        rank and pooled locally for the rank's own batch (no exchange); they
+        must not appear in `placement`. The other tables are table-sharded."""
         from . import _lib
         from .pooling import op_code
+        from .store import table_block_device
         self._lib = _lib
+        self.replicated = set(replicated_tables)
+        if self.replicated and mode != "tablewise":
+            raise ConfigError("replicated tables are supported in table-wise mode only")
         if mode not in ("tablewise", "rowwise"):
             raise ConfigError(f"unknown sharding mode {mode!r}")
         self.metas = {m.table_id: m for m in metas}
@@ -412,6 +420,11 @@ class P2PShardedLookup:
         B, F, W = self.B, self.F, world
         self.n_bags = n_bags = B * F
         self.ops = FlexOps(self.metas, placement, seed, rank, self.ftab, self.fops, B, self.device)
+        for t in self.replicated:
+            if any(sp.table_id == t for sp in placement):
+                raise ConfigError(f"replicated table {t} must not be in the sharded placement")
+            self.ops.local[t] = (table_block_device(seed, t, self.metas[t].dim, 0, self.metas[t].num_rows,
+                                                    device=self.device), 0, self.metas[t].num_rows)
         tab_owner = {}
         for sp in placement:
             tab_owner.setdefault(sp.table_id, set()).add(sp.server_id)
@@ -419,7 +432,9 @@ class P2PShardedLookup:
             for t, o in tab_owner.items():
                 if len(o) != 1:
                     raise ConfigError(f"table-wise mode needs one owner per table (table {t})")
-            self.feat_owner = [next(iter(tab_owner[t])) for t in self.ftab]
+            # requester-relative owner: replicated features are served by the requester itself
+            self.tw_owner = [(-1 if t in self.replicated else next(iter(tab_owner[t]))) for t in self.ftab]
+            self.feat_owner = [rank if o < 0 else o for o in self.tw_owner]
         self.max_nnz = int(max_nnz) if max_nnz is not None else n_bags * 64
         dev = self.device
         # IPC-exported staging buffers
@@ -427,10 +442,13 @@ class P2PShardedLookup:
         if mode == "tablewise":
             # owner-side staging: one slot per requester holding the indices and
             # rebased offsets of the features this rank owns (pushed by requesters)
-            self.my_feats = [f for f in range(F) if self.feat_owner[f] == rank]
-            self.n_owned = [sum(1 for f in range(F) if self.feat_owner[f] == r) for r in range(W)]
+            n_repl = sum(1 for o in self.tw_owner if o < 0)
+            # slot (q -> d) holds d's table-wise features, plus the replicated ones when q == d
+            self.slot_feats = lambda q, d: [f for f in range(F) if self.tw_owner[f] == d or
+                                            (self.tw_owner[f] < 0 and q == d)]
+            self.slot_stride = [sum(1 for o in self.tw_owner if o == d) + n_repl for d in range(W)]
             self.b_idx = DevBuffer(W * self.max_nnz * 4)
-            self.b_offs = DevBuffer(W * (len(self.my_feats) * B + 1) * 8)
+            self.b_offs = DevBuffer(W * (self.slot_stride[rank] * B + 1) * 8)
             self.b_out = DevBuffer(n_bags * D * 4)
         else:
             self.b_idx = DevBuffer(self.max_nnz * 4)
@@ -468,21 +486,19 @@ class P2PShardedLookup:
             # push targets: this requester's slot in every owner's staging
             self.t_dst_idx = torch.tensor([ptrs[d][0] + rank * self.max_nnz * 4 for d in range(W)], dtype=torch.int64,
                                           device=dev)
-            self.t_dst_offs = torch.tensor([ptrs[d][1] + rank * (self.n_owned[d] * B + 1) * 8 for d in range(W)],
+            self.t_dst_offs = torch.tensor([ptrs[d][1] + rank * (self.slot_stride[d] * B + 1) * 8 for d in range(W)],
                                            dtype=torch.int64, device=dev)
             pos = [0] * F
-            cnt = [0] * W
-            for f in range(F):
-                pos[f] = cnt[self.feat_owner[f]]
-                cnt[self.feat_owner[f]] += 1
+            for d in range(W):
+                for j, f in enumerate(self.slot_feats(rank, d)):
+                    pos[f] = j
             self.t_feat_owner = torch.tensor(self.feat_owner, dtype=torch.int32, device=dev)
             self.t_feat_pos = torch.tensor(pos, dtype=torch.int32, device=dev)
-            Fm = len(self.my_feats)
             for q in range(W):
                 qout = ptrs[q][2]
                 lidx = self.b_idx.ptr + q * self.max_nnz * 4
-                loffs = self.b_offs.ptr + q * (Fm * B + 1) * 8
-                for j, f in enumerate(self.my_feats):
+                loffs = self.b_offs.ptr + q * (self.slot_stride[rank] * B + 1) * 8
+                for j, f in enumerate(self.slot_feats(q, rank)):
                     data, rb, re = self.ops.local[self.ftab[f]]
                     segs.append(_lib.FxSegment(data.data_ptr(), rb, re, vb, vb + B, qout + f * D * 4, F * D, D, D,
                                                op_code(self.fops[f]), lidx, loffs + j * B * 8))

@@ -64,6 +64,7 @@ def main():
                         policy=C.CachePolicy(model), tracker=C.LoadTracker(16, 10 ** 9, 0),
                         hits_from_cache=bool(a.hits_from_cache))
             times, hits = [], []
+            rk.profile = True
             for i, (idx, offs) in enumerate(dev_batches):
                 torch.cuda.synchronize()
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -71,6 +72,8 @@ def main():
                 rk.execute_csr(idx, offs, batches[i].feature_tables, batches[i].feature_ops, B, batch_id=i)
                 e1.record()
                 e1.synchronize()
+                if i == a.warm:
+                    rk.stage_ms = {}
                 if i >= a.warm:
                     times.append(e0.elapsed_time(e1))
                     hits.append(rk.batch_metrics[-1].hit_rate)
@@ -79,7 +82,9 @@ def main():
                               "hit_rate": sum(hits) / len(hits), "ms_per_batch": ms,
                               "pooled_lookups_per_s": B * T / (ms / 1e3), "tables": T, "rows": N, "dim": D,
                               "batch": B, "pooling": a.pooling, "init_store_s": round(init_s, 2),
-                              "hits_from_cache": bool(a.hits_from_cache)}), flush=True)
+                              "hits_from_cache": bool(a.hits_from_cache),
+                              "stage_ms_per_batch": {k: round(v / len(times), 3) for k, v in rk.stage_ms.items()}}),
+                  flush=True)
             del rk, cache
             torch.cuda.empty_cache()
 

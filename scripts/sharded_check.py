@@ -27,8 +27,17 @@ def main():
     D, B = 128, 96
     metas = [TableMeta(t, n, D) for t, n in enumerate(rows)]
     placement = (tablewise_placement if mode == "tablewise" else rowwise_placement)(rows, world)
-    cls = P2PShardedLookup if exchange == "p2p" else ShardedLookup
-    sl = cls(metas, placement, 0, tuple(range(len(rows))), ops, B, rank, world, f"cuda:{local}", mode=mode)
+    if exchange == "p2phybrid":
+        from paper_2410_12794_b200.store import ShardSpec
+        repl = [t for t, n in enumerate(rows) if n < 5000]
+        big = [t for t in range(len(rows)) if t not in repl]
+        sub = tablewise_placement([rows[t] for t in big], world)
+        placement = [ShardSpec(big[s.table_id], s.start, s.end, s.server_id) for s in sub]
+        sl = P2PShardedLookup(metas, placement, 0, tuple(range(len(rows))), ops, B, rank, world, f"cuda:{local}",
+                              mode=mode, replicated_tables=repl)
+    else:
+        cls = P2PShardedLookup if exchange == "p2p" else ShardedLookup
+        sl = cls(metas, placement, 0, tuple(range(len(rows))), ops, B, rank, world, f"cuda:{local}", mode=mode)
     worst, exact, n = 0.0, 0, 0
     for it in range(3):
         hb = DlrmBatchGen(rows, 1.0, B, (1, 40), seed=100 * rank + it, ops=ops, permute=(mode == "rowwise")).next()
