@@ -216,6 +216,9 @@ int fx_cache_lru(fx_cache *c, uint64_t *keys_out, int64_t *ticks_out, int32_t *h
                  int64_t *n_out, void *stream);
 int fx_cache_eviction_log(fx_cache *c, uint64_t *out, int64_t cap, int64_t *n_out, void *stream); /* [sync] */
 int fx_cache_pending(fx_cache *c, uint64_t *out, int64_t cap, int64_t *n_out, void *stream);      /* [sync] */
+/* 1 (default): resolve ordered offers with the exact run-parallel kernel when
+ * every row has one size; 0: always use the sequential reference loop */
+int fx_cache_set_parallel(fx_cache *c, int32_t on);
 /* keys evicted by the last offer / apply / set_budget call                 [sync] */
 int fx_cache_last_evicted(fx_cache *c, uint64_t *out, int64_t cap, int64_t *n_out, void *stream);
 /* device array of row pointers for the pending keys (NULL entry -> table dir),

@@ -176,6 +176,7 @@ def _sig():
         "fx_cache_pending": [P, P, I64, ctypes.POINTER(I64), P],
         "fx_cache_last_evicted": [P, P, I64, ctypes.POINTER(I64), P],
         "fx_cache_set_pending_rows": [P, P, I64],
+        "fx_cache_set_parallel": [P, I32],
     }
     for n, a in sigs.items():
         f = getattr(L, n)
@@ -309,6 +310,11 @@ class AdaptiveCache:
             tb[t] = b
         dirs = (FxTableDir * max(len(self._dir), 1))(*self._dir)
         _lib.check(self._L.fx_cache_set_tables(self._h, dirs, len(self._dir), tb, n_t), "cache tables")
+
+    def set_parallel_offers(self, on: bool) -> None:
+        """Exact run-parallel ordered offers (uniform row size) vs the
+        sequential reference loop; both give identical results."""
+        _lib.check(self._L.fx_cache_set_parallel(self._h, 1 if on else 0), "set parallel")
 
     def set_row_bytes(self, table_id: int, nbytes: int):
         if self._row_bytes.get(table_id) != nbytes:

@@ -20,6 +20,7 @@
 // precomputed, parallel-gathered inputs (sketch estimates, LRU order); the
 // hash-index and row-copy side effects are applied afterwards in parallel.
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_select.cuh>
 
 #include <climits>
 #include <vector>
@@ -231,6 +232,10 @@ struct OfferWS {
   long long *sort_keys_in;
   long long *sort_keys_out;
   int32_t *iota;
+  int32_t *par_flag;
+  int32_t *par_iota;
+  int32_t *par_cand;
+  int64_t *par_m;
 };
 
 __global__ void k_offer_prep(CacheView c, const uint64_t *keys, int64_t n, const int32_t *sizes, OfferWS w) {
@@ -318,6 +323,181 @@ __global__ void k_offer_seq(CacheView c, const uint64_t *keys, int64_t n, int32_
   sc->n_acc = n_acc;
   sc->n_ev = n_ev;
   sc->n_evlog = n_log;
+}
+
+
+// ---------------------------------------------------------------- parallel ordered offers
+// Exact parallel form of k_offer_seq when every candidate and every cached
+// entry has the same size S (uniform dims). With cap = budget / S slots:
+//  * the first (cap - entries) non-present candidates are inserted without
+//    eviction (used + S <= budget, cache.py:250 is not reached);
+//  * afterwards every accept evicts exactly one LRU entry. The LRU queue is
+//    V = [existing entries by tick] ++ [accepted candidates in order]; with
+//    head h, candidate j is accepted iff est(c_j) >= est(V[h]) (sketch) or
+//    always ("always" admission / apply-pending).
+// Decisions come in runs. Accept-run from (j, h): c_{j+t} is accepted iff
+// est(c_{j+t}) >= est(V[h+t]) for all earlier t; reject-run from (j, h):
+// c_{j+t} is rejected iff est(c_{j+t}) < est(V[h]). Each run is resolved with
+// one block-wide compare + first-false reduction over a window of at most
+// min(1024, cap) candidates, so V[h+t] never refers to a candidate accepted
+// inside the same window. Ticks, slots and evictions are then assigned in
+// parallel exactly as the sequential loop would.
+struct ParWS {
+  const int32_t *cand;   // compacted non-present candidate positions (ascending)
+  int64_t m;             // number of compacted candidates
+  const int64_t *m_dev;  // optional device count (overrides m)
+};
+
+__device__ __forceinline__ double est_v(const CacheView &c, const OfferWS &w, long long k, long long e0,
+                                        long long k_vic) {
+  if (k < e0) return k < k_vic ? w.est_vic[k] : k_est(c, c.skey[w.lru_slot[k]]);
+  return w.est_cand[w.acc_j[k - e0]];
+}
+
+__global__ void __launch_bounds__(1024) k_offer_par(CacheView c, const uint64_t *keys, int32_t mode, OfferWS w,
+                                                    ParWS pw, int64_t k_vic, int32_t S, uint8_t *accepted,
+                                                    int32_t record) {
+  __shared__ long long sh_first;
+  __shared__ long long st[8];  // j, h, n_acc, n_ev, tick, ftop, n_log, entries
+  const int tid = threadIdx.x;
+  Scalars *sc = c.sc;
+  const long long m = pw.m_dev ? *pw.m_dev : pw.m;
+  const long long e0 = sc->entries;
+  const long long cap = sc->budget / S;
+  if (tid == 0) {
+    st[0] = 0; st[1] = 0; st[2] = 0; st[3] = 0;
+    st[4] = sc->tick; st[5] = sc->free_top; st[6] = sc->n_evlog; st[7] = e0;
+  }
+  __syncthreads();
+  // phase 0: entries beyond cap (budget shrank): evict LRU heads
+  {
+    const long long over = e0 > cap ? e0 - cap : 0;
+    for (long long k = tid; k < over; k += blockDim.x) {
+      const int32_t vs = w.lru_slot[k];
+      const uint64_t key = c.skey[vs];
+      w.ev_keys[k] = key;
+      if (record && st[6] + k < c.evlog_cap) c.evlog[st[6] + k] = key;
+      c.stick[vs] = kFree;
+      c.skey[vs] = kEmpty;
+      c.free_stack[st[5] + k] = vs;
+    }
+    __syncthreads();
+    if (tid == 0 && over) {
+      st[1] = over; st[3] = over; st[5] += over; st[6] += record ? over : 0; st[7] = cap;
+    }
+    __syncthreads();
+  }
+  if (S > sc->budget) {  // every candidate is larger than the whole budget
+    for (long long t = tid; t < m; t += blockDim.x) if (accepted) accepted[pw.cand[t]] = 0;
+    __syncthreads();
+    if (tid == 0) {
+      sc->entries = st[7]; sc->used = st[7] * S; sc->free_top = st[5];
+      sc->n_acc = 0; sc->n_ev = st[3]; sc->n_evlog = st[6];
+    }
+    return;
+  }
+  // phase 1: free slots, no eviction
+  {
+    const long long fr = cap - st[7];
+    const long long nf = fr < m ? (fr > 0 ? fr : 0) : m;
+    for (long long t = tid; t < nf; t += blockDim.x) {
+      const int32_t j = pw.cand[t];
+      const int32_t s = c.free_stack[st[5] - 1 - t];
+      c.skey[s] = keys[j];
+      c.stick[s] = st[4] + t + 1;
+      c.ssize[s] = S;
+      c.shits[s] = 0;
+      w.acc_slot[t] = s;
+      w.acc_j[t] = j;
+      if (accepted) accepted[j] = 1;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      st[0] = nf; st[2] = nf; st[4] += nf; st[5] -= nf; st[7] += nf;
+    }
+    __syncthreads();
+  }
+  // phase 2: full cache, runs of accepts / rejects
+  const bool always = (mode != 0) || (c.admission != 0);
+  const long long win_max = cap < 1024 ? cap : 1024;
+  bool accept_mode = true;
+  while (true) {
+    const long long j = st[0], h = st[1], nacc = st[2];
+    if (j >= m || win_max <= 0) break;
+    const long long win = (m - j) < win_max ? (m - j) : win_max;
+    if (tid == 0) sh_first = win;
+    __syncthreads();
+    if (tid < win) {
+      bool ok;
+      const double ec = w.est_cand[pw.cand[j + tid]];
+      if (always) ok = accept_mode;
+      else if (accept_mode) ok = ec >= est_v(c, w, h + tid, e0, k_vic);
+      else ok = ec < est_v(c, w, h, e0, k_vic);
+      if (!ok) atomicMin(&sh_first, (long long)tid);
+    }
+    __syncthreads();
+    const long long run = sh_first;
+    if (accept_mode) {
+      // candidates j .. j+run-1 accepted; each evicts V[h + t]
+      for (long long t = tid; t < run; t += blockDim.x) {
+        const long long k = h + t;
+        const int32_t vs = k < e0 ? w.lru_slot[k] : w.acc_slot[k - e0];
+        const uint64_t old = c.skey[vs];
+        w.ev_keys[st[3] + t] = old;
+        if (record && st[6] + t < c.evlog_cap) c.evlog[st[6] + t] = old;
+      }
+      __syncthreads();
+      for (long long t = tid; t < run; t += blockDim.x) {
+        const long long k = h + t;
+        const int32_t vs = k < e0 ? w.lru_slot[k] : w.acc_slot[k - e0];
+        const int32_t jj = pw.cand[j + t];
+        c.skey[vs] = keys[jj];
+        c.stick[vs] = st[4] + t + 1;
+        c.ssize[vs] = S;
+        c.shits[vs] = 0;
+        w.acc_slot[nacc + t] = vs;
+        w.acc_j[nacc + t] = jj;
+        if (accepted) accepted[jj] = 1;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        st[0] += run; st[1] += run; st[2] += run; st[3] += run; st[4] += run;
+        st[6] += record ? run : 0;
+      }
+    } else {
+      for (long long t = tid; t < run; t += blockDim.x)
+        if (accepted) accepted[pw.cand[j + t]] = 0;
+      __syncthreads();
+      if (tid == 0) st[0] += run;
+    }
+    __syncthreads();
+    if (run < win || always) accept_mode = always ? true : !accept_mode;
+    __syncthreads();
+  }
+  if (tid == 0) {
+    sc->tick = st[4];
+    sc->free_top = st[5];
+    sc->entries = st[7];
+    sc->used = st[7] * S;
+    sc->n_acc = st[2];
+    sc->n_ev = st[3];
+    sc->n_evlog = st[6];
+  }
+}
+
+__global__ void k_mark_absent(const uint8_t *present, int64_t n, int32_t *flag) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    flag[i] = present[i] ? 0 : 1;
+}
+
+__global__ void k_present_accept(const uint8_t *present, int64_t n, int32_t mode, uint8_t *accepted) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    if (present[i] && accepted) accepted[i] = mode == 0 ? 1 : 0;
+}
+
+__global__ void k_iota32(int32_t *p, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = static_cast<int32_t>(i);
 }
 
 __global__ void k_hash_erase(CacheView c, OfferWS w) {
@@ -511,6 +691,8 @@ struct fx_cache {
   int32_t *tbytes_dev = nullptr;
   void *ws = nullptr;
   size_t ws_bytes = 0;
+  int32_t uniform = 0;             // common row size of every table (0 unset, -1 mixed)
+  int parallel_offers = 1;         // use k_offer_par when sizes are uniform
   uint64_t *last_ev = nullptr;     // keys evicted by the last offer/apply/resize
   int64_t last_ev_cap = 0;
   const float *const *pending_rows = nullptr;  // optional per-pending-key row pointers
@@ -556,8 +738,13 @@ size_t offer_ws_bytes(fx_cache *c, int64_t n, size_t *cub_bytes) {
                                   (const int32_t *)nullptr, (int32_t *)nullptr, static_cast<int>(S));
   *cub_bytes = cb;
   const int64_t nn = n > 0 ? n : 1;
-  return al(nn * 8) + al(nn * 4) + al(nn) + al(S * 4) + al(S * 8) + al(S * 4) + al(nn * 4) + al(S * 8 + nn * 8) +
-         al(S * 8) * 2 + al(S * 4) + al(cb);
+  size_t cs = 0;
+  cub::DeviceSelect::Flagged(nullptr, cs, (const int32_t *)nullptr, (const int32_t *)nullptr, (int32_t *)nullptr,
+                             (int64_t *)nullptr, static_cast<int>(nn));
+  if (cs > cb) cb = cs;
+  *cub_bytes = cb;
+  return al(nn * 8) + al(nn * 4) + al(nn) + al(S * 4) + al(S * 8) + al(S * 4 + nn * 4) + al(nn * 4) +
+         al(S * 8 + nn * 8) + al(S * 8) * 2 + al(S * 4) + al(nn * 4) * 3 + al(8) + al(cb);
 }
 
 OfferWS carve_offer_ws(fx_cache *c, int64_t n, void **cub_tmp) {
@@ -570,12 +757,16 @@ OfferWS carve_offer_ws(fx_cache *c, int64_t n, void **cub_tmp) {
   w.present = reinterpret_cast<uint8_t *>(p); p += al(nn);
   w.lru_slot = reinterpret_cast<int32_t *>(p); p += al(S * 4);
   w.est_vic = reinterpret_cast<double *>(p); p += al(S * 8);
-  w.acc_slot = reinterpret_cast<int32_t *>(p); p += al(S * 4);
+  w.acc_slot = reinterpret_cast<int32_t *>(p); p += al(S * 4 + nn * 4);
   w.acc_j = reinterpret_cast<int32_t *>(p); p += al(nn * 4);
   w.ev_keys = reinterpret_cast<uint64_t *>(p); p += al(S * 8 + nn * 8);
   w.sort_keys_in = reinterpret_cast<long long *>(p); p += al(S * 8);
   w.sort_keys_out = reinterpret_cast<long long *>(p); p += al(S * 8);
   w.iota = reinterpret_cast<int32_t *>(p); p += al(S * 4);
+  w.par_flag = reinterpret_cast<int32_t *>(p); p += al(nn * 4);
+  w.par_iota = reinterpret_cast<int32_t *>(p); p += al(nn * 4);
+  w.par_cand = reinterpret_cast<int32_t *>(p); p += al(nn * 4);
+  w.par_m = reinterpret_cast<int64_t *>(p); p += al(8);
   *cub_tmp = p;
   return w;
 }
@@ -624,7 +815,21 @@ int run_offer(fx_cache *c, const uint64_t *keys, int64_t n, int32_t mode, const 
     else
       k_vic = 0;
   }
-  k_offer_seq<<<1, 32, 0, st>>>(c->v, keys, n, mode, w, k_vic, accepted, c->record);
+  const bool par = c->parallel_offers && c->uniform > 0 && sizes == nullptr && n > 0;
+  if (par) {
+    // compact the non-present candidates, then resolve decisions run by run
+    k_mark_absent<<<grid_for(n, 256), 256, 0, st>>>(w.present, n, w.par_flag);
+    k_iota32<<<grid_for(n, 256), 256, 0, st>>>(w.par_iota, n);
+    cub::DeviceSelect::Flagged(cub_tmp, cb, w.par_iota, w.par_flag, w.par_cand, w.par_m, static_cast<int>(n), st);
+    k_present_accept<<<grid_for(n, 256), 256, 0, st>>>(w.present, n, mode, accepted);
+    ParWS pw{w.par_cand, n, w.par_m};
+    k_offer_par<<<1, 1024, 0, st>>>(c->v, keys, mode, w, pw, k_vic, c->uniform, accepted, c->record);
+  } else if (c->uniform > 0 && n == 0 && h.used > h.budget) {
+    ParWS pw{w.par_cand, 0, nullptr};
+    k_offer_par<<<1, 1024, 0, st>>>(c->v, keys, mode, w, pw, k_vic, c->uniform, accepted, c->record);
+  } else {
+    k_offer_seq<<<1, 32, 0, st>>>(c->v, keys, n, mode, w, k_vic, accepted, c->record);
+  }
   k_hash_erase<<<grid_for(h.entries + n + 1, 256), 256, 0, st>>>(c->v, w);
   if (n > 0) k_install<<<grid_for(n * 32, 256), 256, 0, st>>>(c->v, w, keys, src_rows);
   FX_LAUNCH_CHECK("fx_cache offer");
@@ -733,6 +938,11 @@ int fx_cache_set_tables(fx_cache *c, const fx_table_dir *dir, int32_t n_dir, con
                         int32_t n_tables) {
   c->dir_host.assign(dir, dir + n_dir);
   c->tbytes_host.assign(table_bytes, table_bytes + n_tables);
+  for (int32_t b : c->tbytes_host) {  // sticky: once two sizes are seen, stay on the general path
+    if (b <= 0 || c->uniform < 0) continue;
+    if (c->uniform == 0) c->uniform = b;
+    else if (c->uniform != b) c->uniform = -1;
+  }
   int max_dim = 0;
   for (auto &d : c->dir_host) max_dim = d.dim > max_dim ? d.dim : max_dim;
   for (int32_t b : c->tbytes_host) max_dim = b / 4 > max_dim ? b / 4 : max_dim;
@@ -1033,6 +1243,11 @@ int fx_cache_pending(fx_cache *c, uint64_t *out, int64_t cap, int64_t *n_out, vo
   if (n > 0) cudaMemcpyAsync(out, c->v.pend, n * 8, cudaMemcpyDeviceToDevice, st);
   *n_out = h.pending;
   return cuda_check(cudaStreamSynchronize(st), "fx_cache_pending");
+}
+
+int fx_cache_set_parallel(fx_cache *c, int32_t on) {
+  c->parallel_offers = on ? 1 : 0;
+  return FX_OK;
 }
 
 int fx_cache_last_evicted(fx_cache *c, uint64_t *out, int64_t cap, int64_t *n_out, void *stream) {

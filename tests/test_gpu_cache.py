@@ -202,3 +202,50 @@ def test_batched_probe_equals_per_occurrence_probe(C):
         assert a.lru_entries() == b.lru_entries()
         assert a.sketch.ranked() == b.sketch.ranked()
         assert (a.tick, a.hits, a.misses) == (b.tick, b.hits, b.misses)
+
+
+@pytest.mark.parametrize("admission", ["sketch", "always"])
+def test_parallel_offers_equal_sequential_loop(C, admission):
+    """The run-parallel ordered-offer kernel (uniform row size) makes exactly
+    the decisions of the sequential reference loop: same accepts, LRU order,
+    ticks, eviction log and sketch, across fills, steady state, shrinks and
+    grow-stage-apply cycles, with windows larger and smaller than the cache."""
+    rng = np.random.default_rng(1)
+    for cap_rows in (7, 300, 5000):
+        caches = []
+        for par in (True, False):
+            c = C.AdaptiveCache(cap_rows * ROW_BYTES, admission=admission, record_evictions=True, max_dim=4,
+                                slot_capacity=4 * cap_rows + 8)
+            c.set_row_bytes(0, ROW_BYTES)
+            c.set_parallel_offers(par)
+            caches.append(c)
+        ones = torch.ones(4, dtype=torch.float32, device=caches[0].device)
+        for step in range(6):
+            keys = [(0, int(k)) for k in rng.zipf(1.3, size=4 * cap_rows) % (20 * cap_rows)]
+            for c in caches:
+                c.apply_pending_admissions()
+                _probe_batch(C, c, keys)
+            # offers: distinct misses in first-occurrence order (some present keys mixed in)
+            seen = list(dict.fromkeys(keys))
+            accs = []
+            for c in caches:
+                kk = C._u64([C.encode_key(*k) for k in seen]).to(c.device)
+                src = torch.full((len(seen),), ones.data_ptr(), dtype=torch.int64, device=c.device)
+                acc = torch.zeros(len(seen), dtype=torch.uint8, device=c.device)
+                c.offer_keys(kk, len(seen), src, acc)
+                accs.append(acc.cpu().numpy())
+            assert np.array_equal(accs[0], accs[1])
+            if step == 3:
+                for c in caches:
+                    c.resize(int(cap_rows * 0.6) * ROW_BYTES, fetcher=None)
+            if step == 4:
+                for c in caches:
+                    c.resize(cap_rows * ROW_BYTES, fetcher=lambda t, i: vec(), row_bytes_of=lambda t: ROW_BYTES)
+            for c in caches:
+                c.stage_hot_admissions(lambda t, i: vec(), lambda t: ROW_BYTES, limit=16)
+                c.sketch.age()
+            a, b = caches
+            assert a.lru_entries() == b.lru_entries(), (cap_rows, step)
+            assert (a.used_bytes, a.tick, a.hits, a.misses) == (b.used_bytes, b.tick, b.hits, b.misses)
+            assert a.sketch.ranked() == b.sketch.ranked()
+        assert caches[0].eviction_log == caches[1].eviction_log
