@@ -282,25 +282,50 @@ static int pool_variant() {
   return v;
 }
 
-template <int G, int NCH, typename IdxT, int MODE>
-static void launch_async(const fx_segment *segs, int n_segs, int dim, const IdxT *ix, const int64_t *offsets,
-                         int64_t n_bags, int32_t *counts, int64_t *err, int32_t bad_code, int32_t *err_code,
-                         cudaStream_t st, bool sf) {
+template <int G, int NCH, int CR, typename IdxT, int MODE>
+static void launch_async_cr(const fx_segment *segs, int n_segs, int dim, const IdxT *ix, const int64_t *offsets,
+                            int64_t n_bags, int32_t *counts, int64_t *err, int32_t bad_code, int32_t *err_code,
+                            cudaStream_t st, bool sf) {
   constexpr int WARPS = 4;
-  // per group: G rows x (G lanes * 16 B * NCH); 32/G groups per warp
-  const size_t smem = static_cast<size_t>(WARPS) * (32 / G) * G * G * 16 * NCH;
+  // per group: CR rows x (G lanes * 16 B * NCH); 32/G groups per warp
+  const size_t smem = static_cast<size_t>(WARPS) * (32 / G) * CR * G * 16 * NCH;
   static int per_sm = -1;
   if (per_sm < 0) {
-    cudaFuncSetAttribute(k_pool_async<G, NCH, IdxT, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_pool_async<G, NCH, CR, IdxT, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(smem));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pool_async<G, NCH, IdxT, MODE>, WARPS * 32, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pool_async<G, NCH, CR, IdxT, MODE>, WARPS * 32, smem);
     if (per_sm < 1) per_sm = 1;
   }
   int64_t blocks = static_cast<int64_t>(num_sms()) * per_sm;
   const int64_t need = (n_bags + WARPS * (32 / G) - 1) / (WARPS * (32 / G));
   if (blocks > need) blocks = need;
-  k_pool_async<G, NCH, IdxT, MODE><<<static_cast<int>(blocks), WARPS * 32, smem, st>>>(
+  k_pool_async<G, NCH, CR, IdxT, MODE><<<static_cast<int>(blocks), WARPS * 32, smem, st>>>(
       segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code, sf);
+}
+
+static int pool_chunk_rows() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("FX_POOL_CR");
+    v = e ? atoi(e) : 32;
+  }
+  return v;
+}
+
+template <int G, int NCH, typename IdxT, int MODE>
+static void launch_async(const fx_segment *segs, int n_segs, int dim, const IdxT *ix, const int64_t *offsets,
+                         int64_t n_bags, int32_t *counts, int64_t *err, int32_t bad_code, int32_t *err_code,
+                         cudaStream_t st, bool sf) {
+  const int cr = pool_chunk_rows();
+  if (G == 32 && cr == 24)
+    launch_async_cr<G, NCH, (G >= 24 ? 24 : G), IdxT, MODE>(segs, n_segs, dim, ix, offsets, n_bags, counts, err,
+                                                          bad_code, err_code, st, sf);
+  else if (G >= 16 && cr == 16)
+    launch_async_cr<G, NCH, (G >= 16 ? 16 : G), IdxT, MODE>(segs, n_segs, dim, ix, offsets, n_bags, counts, err,
+                                                          bad_code, err_code, st, sf);
+  else
+    launch_async_cr<G, NCH, G, IdxT, MODE>(segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code,
+                                           st, sf);
 }
 
 template <int NCH, int RING, int WARPS, typename IdxT, int MODE>

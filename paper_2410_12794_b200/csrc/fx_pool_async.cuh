@@ -53,12 +53,15 @@ __device__ __forceinline__ void emit_bag(const fx_segment &sg, int64_t bag, int6
 // register staging), so the whole bag is in flight at once; while the copies
 // land the group prefetches the NEXT bag's offsets and first index chunk.
 // Rows are then summed from shared memory in index order.
-template <int G, int NCH, typename IdxT, int MODE>
+template <int G, int NCH, int CR, typename IdxT, int MODE>
 __global__ void __launch_bounds__(128) k_pool_async(const fx_segment *__restrict__ segs, int n_segs, int dim,
                                                     const IdxT *__restrict__ indices_g,
                                                     const int64_t *__restrict__ offsets, int64_t n_bags,
                                                     int32_t *__restrict__ counts, int64_t *err, int32_t bad_code,
                                                     int32_t *err_code, bool sysfence) {
+  // CR = rows staged per chunk (<= G): smaller chunks -> less shared memory
+  // per warp -> more resident warps.
+  static_assert(CR <= G, "chunk rows <= lanes per group");
   constexpr int ROWB = G * 16 * NCH;  // bytes per row
   constexpr int GPW = 32 / G;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -67,7 +70,7 @@ __global__ void __launch_bounds__(128) k_pool_async(const fx_segment *__restrict
   const int gw = lane / G;
   const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (gw * G));
   const int wib = threadIdx.x >> 5;
-  unsigned char *buf = smem + (static_cast<size_t>(wib) * GPW + gw) * G * ROWB;
+  unsigned char *buf = smem + (static_cast<size_t>(wib) * GPW + gw) * CR * ROWB;
   const uint32_t sbuf = static_cast<uint32_t>(__cvta_generic_to_shared(buf));
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -82,7 +85,7 @@ __global__ void __launch_bounds__(128) k_pool_async(const fx_segment *__restrict
   int64_t beg, end;
   bag_bounds(segs, s, bag, offsets, beg, end);
   const IdxT *indices = seg_indices(segs, s, indices_g);
-  IdxT pidx = (beg + gl < end) ? indices[beg + gl] : IdxT(0);
+  IdxT pidx = (gl < CR && beg + gl < end) ? indices[beg + gl] : IdxT(0);
 
   while (bag < n_bags) {
     const float *__restrict__ tab = segs[s].table;
@@ -96,31 +99,62 @@ __global__ void __launch_bounds__(128) k_pool_async(const fx_segment *__restrict
     int64_t nbeg = 0, nend = 0;
     IdxT nidx = IdxT(0);
     bool have_next = false;
-    for (int64_t c0 = beg; c0 < end; c0 += G) {
-      const int n = static_cast<int>((end - c0) < G ? (end - c0) : (int64_t)G);
+    for (int64_t c0 = beg; c0 < end; c0 += CR) {
+      const int n = static_cast<int>((end - c0) < CR ? (end - c0) : (int64_t)CR);
       const int64_t idx = static_cast<int64_t>(pidx);
       int64_t my_off = 0;
       if (gl < n) {
         if (idx < rb || idx >= re) record_bad(err, err_code, c0 + gl, bad_code);
         else my_off = (idx - rb) * ld;
       }
-      for (int r = 0; r < n; ++r) {
+      // issue: 4 rows per step so the shuffles / address math overlap
+      int r = 0;
+      for (; r + 4 <= n; r += 4) {
+        const float *src[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) src[u] = tab + __shfl_sync(gmask, my_off, r + u, G);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int k = 0; k < NCH; ++k)
+            cp_async16(sbuf + (r + u) * ROWB + (k * G + gl) * 16, src[u] + (k * G + gl) * 4);
+      }
+      for (; r < n; ++r) {
         const float *src = tab + __shfl_sync(gmask, my_off, r, G);
 #pragma unroll
         for (int k = 0; k < NCH; ++k) cp_async16(sbuf + r * ROWB + (k * G + gl) * 16, src + (k * G + gl) * 4);
       }
       cp_async_commit();
       // overlap the copies with the next chunk's / next bag's index loads
-      if (c0 + G < end) {
-        pidx = (c0 + G + gl < end) ? indices[c0 + G + gl] : IdxT(0);
+      if (c0 + CR < end) {
+        pidx = (gl < CR && c0 + CR + gl < end) ? indices[c0 + CR + gl] : IdxT(0);
       } else if (nbag < n_bags) {
         bag_bounds(segs, ns, nbag, offsets, nbeg, nend);
-        nidx = (nbeg + gl < nend) ? nindices[nbeg + gl] : IdxT(0);
+        nidx = (gl < CR && nbeg + gl < nend) ? nindices[nbeg + gl] : IdxT(0);
         have_next = true;
       }
       cp_async_wait_all();
       __syncwarp(gmask);
-      for (int r = 0; r < n; ++r) {
+      // accumulate in row order; 4 rows' shared loads in flight at a time
+      r = 0;
+      for (; r + 4 <= n; r += 4) {
+        float4 v[4][NCH];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int k = 0; k < NCH; ++k)
+            v[u][k] = *reinterpret_cast<const float4 *>(buf + (r + u) * ROWB + (k * G + gl) * 16);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int k = 0; k < NCH; ++k) {
+            acc[k][0] += static_cast<double>(v[u][k].x);
+            acc[k][1] += static_cast<double>(v[u][k].y);
+            acc[k][2] += static_cast<double>(v[u][k].z);
+            acc[k][3] += static_cast<double>(v[u][k].w);
+          }
+      }
+      for (; r < n; ++r) {
 #pragma unroll
         for (int k = 0; k < NCH; ++k) {
           const float4 v = *reinterpret_cast<const float4 *>(buf + r * ROWB + (k * G + gl) * 16);
@@ -134,7 +168,7 @@ __global__ void __launch_bounds__(128) k_pool_async(const fx_segment *__restrict
     }
     if (!have_next && nbag < n_bags) {
       bag_bounds(segs, ns, nbag, offsets, nbeg, nend);
-      nidx = (nbeg + gl < nend) ? nindices[nbeg + gl] : IdxT(0);
+      nidx = (gl < CR && nbeg + gl < nend) ? nindices[nbeg + gl] : IdxT(0);
     }
     emit_bag<NCH, MODE>(segs[s], bag, end - beg, acc, gl, G, counts);
     bag = nbag;
@@ -146,7 +180,6 @@ __global__ void __launch_bounds__(128) k_pool_async(const fx_segment *__restrict
   }
   if (sysfence) __threadfence_system();
 }
-
 
 __device__ __forceinline__ void cp_async_wait_n(int n) {
   switch (n) {

@@ -67,13 +67,13 @@ def main():
             rk.profile = True
             for i, (idx, offs) in enumerate(dev_batches):
                 torch.cuda.synchronize()
+                if i == a.warm:
+                    rk.stage_ms = {}
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()
                 rk.execute_csr(idx, offs, batches[i].feature_tables, batches[i].feature_ops, B, batch_id=i)
                 e1.record()
                 e1.synchronize()
-                if i == a.warm:
-                    rk.stage_ms = {}
                 if i >= a.warm:
                     times.append(e0.elapsed_time(e1))
                     hits.append(rk.batch_metrics[-1].hit_rate)
