@@ -123,7 +123,10 @@ def build_cfg(cfg_key, rank, n_batches, alpha=None, table_rows=None):
     if alpha is not None:
         cfg["alpha"] = alpha
         cfg["name"] = cfg["name"] + f"-alpha{alpha:g}"
-    gen = DlrmBatchGen(cfg["table_rows"], cfg["alpha"], cfg["batch"], cfg["pooling"], seed=1000 * rank)
+    # cfg5 (row-wise fan-out) uses a fixed bijective row permutation so hot rows
+    # do not all land on shard 0 (SURVEY §7 hard part 4)
+    gen = DlrmBatchGen(cfg["table_rows"], cfg["alpha"], cfg["batch"], cfg["pooling"], seed=1000 * rank,
+                       permute=cfg.get("permute", False))
     return cfg, [gen.next() for _ in range(n_batches)]
 
 

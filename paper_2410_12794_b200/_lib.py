@@ -15,7 +15,7 @@ import torch
 from . import errors
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libflexemb.so")
+LIB_PATH = os.environ.get("FX_LIB_PATH", os.path.join(_HERE, "libflexemb.so"))  # override: A/B builds
 
 FX_OK = 0
 FX_E_CONFIG = 1

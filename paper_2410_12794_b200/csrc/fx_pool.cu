@@ -307,7 +307,7 @@ static int pool_chunk_rows() {
   static int v = -1;
   if (v < 0) {
     const char *e = getenv("FX_POOL_CR");
-    v = e ? atoi(e) : 32;
+    v = e ? atoi(e) : 16;
   }
   return v;
 }
@@ -319,6 +319,12 @@ static void launch_async(const fx_segment *segs, int n_segs, int dim, const IdxT
   const int cr = pool_chunk_rows();
   if (G == 32 && cr == 24)
     launch_async_cr<G, NCH, (G >= 24 ? 24 : G), IdxT, MODE>(segs, n_segs, dim, ix, offsets, n_bags, counts, err,
+                                                          bad_code, err_code, st, sf);
+  else if (G >= 8 && cr == 8)
+    launch_async_cr<G, NCH, 8, IdxT, MODE>(segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code,
+                                           st, sf);
+  else if (G >= 12 && cr == 12)
+    launch_async_cr<G, NCH, (G >= 12 ? 12 : G), IdxT, MODE>(segs, n_segs, dim, ix, offsets, n_bags, counts, err,
                                                           bad_code, err_code, st, sf);
   else if (G >= 16 && cr == 16)
     launch_async_cr<G, NCH, (G >= 16 ? 16 : G), IdxT, MODE>(segs, n_segs, dim, ix, offsets, n_bags, counts, err,

@@ -53,8 +53,11 @@ __device__ __forceinline__ void emit_bag(const fx_segment &sg, int64_t bag, int6
 // register staging), so the whole bag is in flight at once; while the copies
 // land the group prefetches the NEXT bag's offsets and first index chunk.
 // Rows are then summed from shared memory in index order.
+#ifndef FX_POOL_MINB
+#define FX_POOL_MINB 6
+#endif
 template <int G, int NCH, int CR, typename IdxT, int MODE>
-__global__ void __launch_bounds__(128) k_pool_async(const fx_segment *__restrict__ segs, int n_segs, int dim,
+__global__ void __launch_bounds__(128, FX_POOL_MINB) k_pool_async(const fx_segment *__restrict__ segs, int n_segs, int dim,
                                                     const IdxT *__restrict__ indices_g,
                                                     const int64_t *__restrict__ offsets, int64_t n_bags,
                                                     int32_t *__restrict__ counts, int64_t *err, int32_t bad_code,

@@ -139,5 +139,8 @@ CONFIGS = {
     "cfg4": dict(name="dlrm-rm2-100x10Mx128-tablewise", table_rows=(10_000_000,) * 100, dim=128, batch=4096,
                  pooling=20, alpha=1.05),
     "cfg5": dict(name="fanout-200x1Mx128-rowwise", table_rows=(1_000_000,) * 200, dim=128, batch=4096,
-                 pooling=100, alpha=1.0),
+                 pooling=100, alpha=1.0, permute=True),
+    # cfg4 row-reduced variant for the 1->2->4->8 curve
+    "cfg4r": dict(name="dlrm-rm2-100x1Mx128-tablewise-rowreduced", table_rows=(1_000_000,) * 100, dim=128,
+                  batch=4096, pooling=20, alpha=1.05),
 }
