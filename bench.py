@@ -376,8 +376,9 @@ def run_sharded(args, rank, world, local):
     dev = torch.device("cuda", local)
     t0 = time.perf_counter()
     if args.exchange == "p2p":
+        max_nnz = int(max(int(hb.offsets[-1]) for hb in host_batches) * 1.05) + 1024
         sl = P2PShardedLookup(metas, placement, 0, tuple(range(F)), ("sum",) * F, B, rank, world, dev, mode=mode,
-                              replicated_tables=repl)
+                              replicated_tables=repl, max_nnz=max_nnz)
     else:
         if repl:
             raise SystemExit("--replicate-rows needs --exchange p2p")

@@ -245,6 +245,16 @@ int fx_memcpy_async(void *dst, const void *src, size_t bytes, void *stream);
 int fx_push_csr(const void *indices, int32_t idx_type, const int64_t *offsets, int32_t B, int32_t F,
                 const int32_t *feat_owner, const int32_t *feat_pos, int32_t *const *dst_idx, int64_t *const *dst_offs,
                 int32_t sysfence, void *stream);
+/* row-wise push: counts[d*n_bags+b] (int32, W*n_bags+1 entries) = indices of
+ * bag b routed to rank d (K1 range routing); scan = exclusive prefix over
+ * (d, b); then every index is scattered, stable per destination, into rank
+ * d's staging slot dst_idx[d] (int32) and rank d's per-bag offsets
+ * dst_offs[d][0..n_bags] are written (IPC-mapped pointers, DEVICE arrays).
+ * workspace: query with ws == NULL. */
+int fx_rw_push(const int64_t *route_off, const int64_t *starts, const int32_t *owners, const int32_t *bag_table,
+               const void *indices, int32_t idx_type, const int64_t *offsets, int64_t n_bags, int32_t W,
+               int32_t *counts, int64_t *scan, int32_t *const *dst_idx, int64_t *const *dst_offs, void *ws,
+               size_t *ws_bytes, void *stream);
 /* one-block barrier: release-store `epoch` into peer_flags[r][rank] for every
  * rank r (system scope, after a system fence), then acquire-spin until
  * my_flags[r] >= epoch for every r. peer_flags is a DEVICE array of `world`

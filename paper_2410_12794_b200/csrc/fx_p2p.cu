@@ -7,6 +7,8 @@
 // pointers, and two barriers per step order "inputs staged" and "outputs
 // landed" across the GPUs. This replaces the reference's fan-out/response
 // messages (ranker.py:298-347) and the NCCL all-to-all of the baseline path.
+#include <cub/device/device_scan.cuh>
+
 #include <cstring>
 
 #include "fx_common.cuh"
@@ -75,6 +77,99 @@ __global__ void __launch_bounds__(256) k_push_csr(const IdxT *__restrict__ indic
   if (sysfence) __threadfence_system();
 }
 
+
+// ---- row-wise push (routing.py:117-148 group_by_server, per destination rank)
+__device__ __forceinline__ int route_dest(const int64_t *route_off, const int64_t *starts, const int32_t *owners,
+                                          int t, int64_t idx) {
+  int64_t lo = route_off[t], hi = route_off[t + 1];
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (starts[mid] <= idx) lo = mid + 1; else hi = mid;
+  }
+  // out-of-range indices (flagged by the requester's ingress validation) go to
+  // shard 0's owner, which records a routing violation instead of reading them
+  return owners[lo > route_off[t] ? lo - 1 : route_off[t]];
+}
+
+// one warp per bag: counts[d * n_bags + b] = #indices of bag b owned by rank d
+template <typename IdxT>
+__global__ void __launch_bounds__(256) k_rw_count(const int64_t *route_off, const int64_t *starts,
+                                                  const int32_t *owners, const int32_t *bag_table,
+                                                  const IdxT *indices, const int64_t *offsets, int64_t n_bags,
+                                                  int W, int32_t *counts) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t b = warp; b < n_bags; b += nw) {
+    const int t = bag_table[b];
+    const int64_t beg = offsets[b], end = offsets[b + 1];
+    int cnt[32];  // per-destination counts (warp-uniform, register-resident after unrolling)
+#pragma unroll
+    for (int d = 0; d < 32; ++d) cnt[d] = 0;
+    for (int64_t c0 = beg; c0 < end; c0 += 32) {
+      const int my_d = (c0 + lane < end)
+                           ? route_dest(route_off, starts, owners, t, static_cast<int64_t>(indices[c0 + lane]))
+                           : -1;
+#pragma unroll
+      for (int d = 0; d < 32; ++d)
+        if (d < W) cnt[d] += __popc(__ballot_sync(0xffffffffu, my_d == d));
+    }
+#pragma unroll
+    for (int d = 0; d < 32; ++d)
+      if (d < W && lane == 0) counts[(int64_t)d * n_bags + b] = cnt[d];
+  }
+}
+
+// one warp per bag: stable per-destination scatter of the bag's indices into
+// rank d's staging slot (IPC pointer dst_idx[d]) at scan[d*n_bags+b] - scan[d*n_bags] + rank
+template <typename IdxT>
+__global__ void __launch_bounds__(256) k_rw_push(const int64_t *route_off, const int64_t *starts,
+                                                 const int32_t *owners, const int32_t *bag_table,
+                                                 const IdxT *indices, const int64_t *offsets, int64_t n_bags, int W,
+                                                 const int64_t *scan, int32_t *const *dst_idx, bool sysfence) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t b = warp; b < n_bags; b += nw) {
+    const int t = bag_table[b];
+    const int64_t beg = offsets[b], end = offsets[b + 1];
+    int64_t run[32];
+#pragma unroll
+    for (int d = 0; d < 32; ++d)
+      run[d] = d < W ? scan[(int64_t)d * n_bags + b] - scan[(int64_t)d * n_bags] : 0;
+    for (int64_t c0 = beg; c0 < end; c0 += 32) {
+      const bool on = c0 + lane < end;
+      int64_t idx = 0;
+      int my_d = -1;
+      if (on) {
+        idx = static_cast<int64_t>(indices[c0 + lane]);
+        my_d = route_dest(route_off, starts, owners, t, idx);
+      }
+#pragma unroll
+      for (int d = 0; d < 32; ++d) {
+        if (d < W) {
+          const unsigned m = __ballot_sync(0xffffffffu, my_d == d);
+          if (my_d == d) dst_idx[d][run[d] + __popc(m & lt)] = static_cast<int32_t>(idx);
+          run[d] += __popc(m);
+        }
+      }
+    }
+  }
+  if (sysfence) __threadfence_system();
+}
+
+// per-destination bag offsets into rank d's slot: dst_offs[d][b] = scan[d*n+b] - scan[d*n], b in [0, n]
+__global__ void k_rw_push_offsets(const int64_t *scan, int64_t n_bags, int W, int64_t *const *dst_offs,
+                                  bool sysfence) {
+  const int64_t total = (int64_t)W * (n_bags + 1);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t d = i / (n_bags + 1), b = i % (n_bags + 1);
+    dst_offs[d][b] = scan[d * n_bags + b] - scan[d * n_bags];
+  }
+  if (sysfence) __threadfence_system();
+}
+
 }  // namespace fx
 
 using namespace fx;
@@ -132,6 +227,44 @@ int fx_push_csr(const void *indices, int32_t idx_type, const int64_t *offsets, i
     k_push_csr<int64_t><<<grid, 256, 0, as_stream(stream)>>>(static_cast<const int64_t *>(indices), offsets, B, F,
                                                              feat_owner, feat_pos, dst_idx, dst_offs, sysfence != 0);
   FX_LAUNCH_CHECK("fx_push_csr");
+  return FX_OK;
+}
+
+int fx_rw_push(const int64_t *route_off, const int64_t *starts, const int32_t *owners, const int32_t *bag_table,
+               const void *indices, int32_t idx_type, const int64_t *offsets, int64_t n_bags, int32_t W,
+               int32_t *counts, int64_t *scan, int32_t *const *dst_idx, int64_t *const *dst_offs, void *ws,
+               size_t *ws_bytes, void *stream) {
+  if (W < 1 || W > 32 || n_bags < 0) {
+    set_error("fx_rw_push: bad arguments");
+    return FX_E_CONFIG;
+  }
+  const int64_t n = static_cast<int64_t>(W) * n_bags + 1;
+  size_t need = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, need, (const int32_t *)nullptr, (int64_t *)nullptr, static_cast<int>(n));
+  if (ws == nullptr) {
+    *ws_bytes = need;
+    return FX_OK;
+  }
+  cudaStream_t st = as_stream(stream);
+  cudaMemsetAsync(counts, 0, n * sizeof(int32_t), st);
+  const int grid = grid_for(n_bags * 32, 256);
+  if (idx_type == FX_IDX_I32)
+    k_rw_count<int32_t><<<grid, 256, 0, st>>>(route_off, starts, owners, bag_table,
+                                              static_cast<const int32_t *>(indices), offsets, n_bags, W, counts);
+  else
+    k_rw_count<int64_t><<<grid, 256, 0, st>>>(route_off, starts, owners, bag_table,
+                                              static_cast<const int64_t *>(indices), offsets, n_bags, W, counts);
+  cub::DeviceScan::ExclusiveSum(ws, need, counts, scan, static_cast<int>(n), st);
+  if (idx_type == FX_IDX_I32)
+    k_rw_push<int32_t><<<grid, 256, 0, st>>>(route_off, starts, owners, bag_table,
+                                             static_cast<const int32_t *>(indices), offsets, n_bags, W, scan, dst_idx,
+                                             true);
+  else
+    k_rw_push<int64_t><<<grid, 256, 0, st>>>(route_off, starts, owners, bag_table,
+                                             static_cast<const int64_t *>(indices), offsets, n_bags, W, scan, dst_idx,
+                                             true);
+  k_rw_push_offsets<<<grid_for((int64_t)W * (n_bags + 1), 256), 256, 0, st>>>(scan, n_bags, W, dst_offs, true);
+  FX_LAUNCH_CHECK("fx_rw_push");
   return FX_OK;
 }
 

@@ -451,7 +451,8 @@ class P2PShardedLookup:
             self.b_offs = DevBuffer(W * (self.slot_stride[rank] * B + 1) * 8)
             self.b_out = DevBuffer(n_bags * D * 4)
         else:
-            self.b_idx = DevBuffer(self.max_nnz * 4)
+            # owner-side staging: per requester slot, its indices routed here and per-bag offsets
+            self.b_idx = DevBuffer(W * self.max_nnz * 4)
             self.b_offs = DevBuffer(W * (n_bags + 1) * 8)
             self.b_out = DevBuffer(W * n_bags * D * 8)
         self.t_flags = _cai_tensor(self.b_flags.ptr, (W,), torch.int64, dev)
@@ -459,9 +460,13 @@ class P2PShardedLookup:
         if mode == "tablewise":
             self.t_out = _cai_tensor(self.b_out.ptr, (B, F * D), torch.float32, dev)
         else:
-            self.t_idx = _cai_tensor(self.b_idx.ptr, (self.max_nnz,), torch.int32, dev)
-            self.t_offs = _cai_tensor(self.b_offs.ptr, (W, n_bags + 1), torch.int64, dev)
             self.t_out = _cai_tensor(self.b_out.ptr, (W, n_bags, D), torch.float64, dev)
+            self.t_counts = torch.zeros(W * n_bags + 1, dtype=torch.int32, device=dev)
+            self.t_scan = torch.zeros(W * n_bags + 1, dtype=torch.int64, device=dev)
+            need = ctypes.c_size_t(0)
+            _lib.check(_lib.lib.fx_rw_push(None, None, None, None, None, 0, None, n_bags, W, None, None, None, None,
+                                           None, ctypes.byref(need), None), "rw push ws")
+            self.t_ws = torch.empty(max(need.value, 1), dtype=torch.uint8, device=dev)
         torch.cuda.synchronize(dev)
         mine = [self.b_idx.handle(), self.b_offs.handle(), self.b_out.handle(), self.b_flags.handle()]
         allh = [None] * W
@@ -503,8 +508,15 @@ class P2PShardedLookup:
                     segs.append(_lib.FxSegment(data.data_ptr(), rb, re, vb, vb + B, qout + f * D * 4, F * D, D, D,
                                                op_code(self.fops[f]), lidx, loffs + j * B * 8))
                     vb += B
+        if mode == "rowwise":
+            self.t_dst_idx = torch.tensor([ptrs[d][0] + rank * self.max_nnz * 4 for d in range(W)], dtype=torch.int64,
+                                          device=dev)
+            self.t_dst_offs = torch.tensor([ptrs[d][1] + rank * (n_bags + 1) * 8 for d in range(W)],
+                                           dtype=torch.int64, device=dev)
         for q in range(W) if mode == "rowwise" else ():
-            qidx, qoffs, qout, _ = ptrs[q]
+            qout = ptrs[q][2]
+            lidx = self.b_idx.ptr + q * self.max_nnz * 4
+            loffs = self.b_offs.ptr + q * (n_bags + 1) * 8
             for f in range(F):
                 t = self.ftab[f]
                 if t in self.ops.local:
@@ -512,11 +524,8 @@ class P2PShardedLookup:
                     tp = data.data_ptr()
                 else:
                     tp, rb, re = 0, 0, 0
-                out_ptr = qout + (rank * n_bags + f * B) * D * 8
-                stride = D
-                offs_ptr = qoffs + (rank * (n_bags + 1) + f * B) * 8
-                segs.append(_lib.FxSegment(tp, rb, re, vb, vb + B, out_ptr, stride, D, D, op_code(self.fops[f]),
-                                           qidx, offs_ptr))
+                segs.append(_lib.FxSegment(tp, rb, re, vb, vb + B, qout + (rank * n_bags + f * B) * D * 8, D, D, D,
+                                           op_code(self.fops[f]), lidx, loffs + f * B * 8))
                 vb += B
         self.n_vbags = vb
         from .store import make_segments
@@ -579,15 +588,18 @@ class P2PShardedLookup:
                                       self.t_dst_idx.data_ptr(), self.t_dst_offs.data_ptr(), 1, L.stream_ptr()),
                     "push")
         else:
-            send_idx, dcount, bcount = self.ops.route_bucket(indices, offsets, W)
-            self.t_idx[:nnz].copy_(send_idx, non_blocking=True)
-            # per-destination CSR offsets into the bucketed index array
-            c = torch.cumsum(bcount.reshape(-1).long(), 0)
-            flat = torch.zeros(W * self.n_bags + 1, dtype=torch.int64, device=self.device)
-            flat[1:] = c
-            self.t_offs[:, :self.n_bags].copy_(flat[:-1].view(W, self.n_bags))
-            self.t_offs[:, self.n_bags:].copy_(flat[1:].view(W, self.n_bags)[:, -1:])
-            self._counts = bcount
+            o = self.ops
+            L.check(L.lib.fx_route(o.route_off.data_ptr(), o.starts.data_ptr(), o.owners.data_ptr(),
+                                   o.nrows.data_ptr(), o.bag_table.data_ptr(), indices.data_ptr(),
+                                   L.idx_type_of(indices), offsets.data_ptr(), self.n_bags, None,
+                                   o.status.err.data_ptr(), o.status.code.data_ptr(), L.stream_ptr()), "validate")
+            wsb = ctypes.c_size_t(self.t_ws.numel())
+            L.check(L.lib.fx_rw_push(o.route_off.data_ptr(), o.starts.data_ptr(), o.owners.data_ptr(),
+                                     o.bag_table.data_ptr(), indices.data_ptr(), L.idx_type_of(indices),
+                                     offsets.data_ptr(), self.n_bags, W, self.t_counts.data_ptr(),
+                                     self.t_scan.data_ptr(), self.t_dst_idx.data_ptr(), self.t_dst_offs.data_ptr(),
+                                     self.t_ws.data_ptr(), ctypes.byref(wsb), L.stream_ptr()), "rw push")
+            self._counts = self.t_counts[:W * self.n_bags].view(W, self.n_bags)
         self._close(tok)
         tok = self._mark("barrier")
         self._barrier()
