@@ -29,7 +29,8 @@ from embserve.routing import build_routing, group_by_server  # noqa: E402
 from embserve.store import ShardSpec, TableMeta, init_store, row_values, table_block  # noqa: E402
 from embserve.transport.topology import assign_mapping_aware, create_connections  # noqa: E402
 from embserve.transport.virtual import EventLoop, TransportParams, VirtualTransport  # noqa: E402
-from embserve.workload import ZipfSampler  # noqa: E402
+from embserve.workload import (CoOccurrence, Fluctuation, TableWorkload, WorkloadConfig,  # noqa: E402
+                               ZipfSampler, generate_trace, save_trace)
 
 
 def prf_fixtures():
@@ -263,7 +264,22 @@ def _run_and_record(rk, batches, name, metas, placement):
     return rec
 
 
+def trace_fixtures():
+    """Reference generate_trace + save_trace output (workload.py:160-221)."""
+    cfgs = {
+        "trace_a.txt": (WorkloadConfig(tables=[TableWorkload(0, 1.0), TableWorkload(1, 0.5, weight=2.0, op=PoolingOp.MEAN)],
+                                       lookups_per_batch=12, indices_per_lookup=(2, 9), features_per_lookup=2,
+                                       fluctuation=Fluctuation(0.4, 5), duration_batches=6, seed=11,
+                                       co_occurrence=CoOccurrence(3, 0.3)), {0: 500, 1: 60}),
+        "trace_b.txt": (WorkloadConfig(tables=[TableWorkload(3, 1.2)], lookups_per_batch=7, indices_per_lookup=(4, 4),
+                                       duration_batches=4, seed=2), {3: 1000}),
+    }
+    for name, (cfg, rows) in cfgs.items():
+        save_trace(generate_trace(cfg, rows), os.path.join(HERE, name))
+
+
 if __name__ == "__main__":
+    trace_fixtures()
     prf_fixtures()
     pool_fixtures()
     routing_fixtures()

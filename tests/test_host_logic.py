@@ -74,3 +74,49 @@ def test_resolve_out_of_range_and_unknown_table():
             rt.resolve(0, bad)
     with pytest.raises(LookupValidationError):
         rt.resolve(9, 0)
+
+
+# names exported by the reference package (embserve/__init__.py:13-28)
+REFERENCE_EXPORTS = (
+    "AdaptiveCache CachePolicy LoadLevel LoadTracker MemoryModel CapacityError ConfigError EmbServeError "
+    "FlowControlError InvariantError LookupValidationError RoutingViolationError TraceParseError PartialResult "
+    "PlanMode PoolingOp combine_partials pool_flat Batch Feature LookupRequest RoutingTable build_routing "
+    "group_by_server Deployment ServerStore ShardSpec TableMeta init_store Trace WorkloadConfig generate_trace "
+    "load_trace save_trace").split()
+
+
+def test_reference_public_api_is_exported():
+    import paper_2410_12794_b200 as P
+    missing = [n for n in REFERENCE_EXPORTS if not hasattr(P, n)]
+    assert not missing, missing
+
+
+def test_cache_control_logic_host_side():
+    from paper_2410_12794_b200.cache import (CachePolicy, LoadLevel, LoadTracker, MemoryModel,
+                                             max_batch_for_cache, target_cache_bytes)
+    from paper_2410_12794_b200.errors import CapacityError
+    m = MemoryModel(gpu_capacity_bytes=1000, nn_fixed_bytes=200, nn_per_sample_bytes=1)
+    assert target_cache_bytes(m, 400) == 400 and target_cache_bytes(m, 800) == 0
+    with pytest.raises(CapacityError):
+        target_cache_bytes(m, 900)
+    assert max_batch_for_cache(m, 400) == 400 and max_batch_for_cache(m, 0) == 800
+    with pytest.raises(ConfigError):
+        MemoryModel(gpu_capacity_bytes=10, nn_fixed_bytes=20, nn_per_sample_bytes=1)
+    tr = LoadTracker(window=4, high_watermark=512, low_watermark=128)
+    for _ in range(4):
+        lvl = tr.record_batch(600)
+    assert lvl is LoadLevel.HIGH
+    tr = LoadTracker(window=2, high_watermark=100, low_watermark=10)
+    tr.record_batch(500)
+    tr.record_batch(50)
+    assert tr.record_batch(50) is LoadLevel.NORMAL
+    assert LoadTracker(window=4, high_watermark=512, low_watermark=128, stat="max").record_batch(600) is LoadLevel.HIGH
+    pm = MemoryModel(gpu_capacity_bytes=10_000, nn_fixed_bytes=1_000, nn_per_sample_bytes=10)
+    pol = CachePolicy(model=pm, hysteresis_fraction=0.0)
+    assert pol.propose(1_000, LoadLevel.HIGH, windowed_batch=100) <= 1_000
+    assert pol.propose(9_000, LoadLevel.LOW, windowed_batch=800) >= 9_000
+    assert pol.propose(0, LoadLevel.NORMAL, windowed_batch=100) == 8_000
+    pol = CachePolicy(model=pm, hysteresis_fraction=0.05)
+    assert pol.propose(7_800, LoadLevel.NORMAL, windowed_batch=100) == 7_800
+    assert pol.propose(7_000, LoadLevel.NORMAL, windowed_batch=100) == 8_000
+    assert CachePolicy(model=pm, hysteresis_fraction=0.0).propose(5_000, LoadLevel.HIGH, windowed_batch=2_000) == 0
