@@ -197,6 +197,8 @@ def main():
     ap.add_argument("--alpha", type=float, default=None, help="override Zipf alpha (0 = uniform cold control)")
     ap.add_argument("--table-rows", type=int, default=None, help="override every table's row count (cold control)")
     ap.add_argument("--mode", default="tablewise", choices=["tablewise", "rowwise"], help="N>1 sharding")
+    ap.add_argument("--graph", type=int, default=0,
+                    help="N=1: capture this many batch launches per CUDA graph and time graph replays")
     ap.add_argument("--replicate-rows", type=int, default=0,
                     help="N>1 table-wise: replicate tables with <= this many rows on every rank (hybrid placement)")
     ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
@@ -249,13 +251,27 @@ def main():
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    ev0.record(stream)
     launches = 0
     tot_bytes = 0
-    for i in range(args.steps):
-        eng.pool(batches[i % len(batches)], out=outs[i % 2], check=False)
-        launches += 1
-        tot_bytes += bytes_per[i % len(batches)]
+    if args.graph > 0:
+        gb = [batches[i % len(batches)] for i in range(args.graph)]
+        gouts = [outs[i % 2] for i in range(args.graph)]
+        graph = eng.capture(gb, gouts)
+        graph.replay()
+        torch.cuda.synchronize()
+        reps = max(1, args.steps // args.graph)
+        args.steps = reps * args.graph
+        ev0.record(stream)
+        for _ in range(reps):
+            graph.replay()
+        launches = args.steps
+        tot_bytes = sum(bytes_per[i % len(batches)] for i in range(args.graph)) * reps
+    else:
+        ev0.record(stream)
+        for i in range(args.steps):
+            eng.pool(batches[i % len(batches)], out=outs[i % 2], check=False)
+            launches += 1
+            tot_bytes += bytes_per[i % len(batches)]
     ev1.record(stream)
     ev1.synchronize()
     torch.cuda.synchronize()
@@ -330,14 +346,15 @@ def main():
             "config": {"workload": cfg["name"], "global_batch": B * world, "per_gpu_batch": B,
                        "pooling": list(cfg["pooling"]) if isinstance(cfg["pooling"], tuple) else cfg["pooling"],
                        "alpha": cfg["alpha"], "dim": dim, "tables": len(cfg["table_rows"]),
-                       "parallelism": "single" if world == 1 else f"replicas{world}",
+                       "parallelism": ("single" if world == 1 else f"replicas{world}")
+                                      + (f", CUDA graph of {args.graph} launches" if args.graph else ""),
                        "l2": f"inputs larger than L2: {len(batches)} distinct batches cycled, "
                              f"{bytes_per[0] / 1e9:.2f} GB algorithmic bytes/batch over "
                              f"{sum(cfg['table_rows']) * dim * 4 / 1e9:.1f} GB of tables",
                        "init_store_s": round(init_s, 2)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": tr, "peak_source": peak_src,
-                         "kernel": os.environ.get("FX_POOL_VARIANT_NAME", "fx::k_pool_stream<32,1,8,int,0>"),
+                         "kernel": f"fx::k_pool_async<G={min(32, dim // 4)},CR=16> (cp.async-staged gather+pool, D={dim})",
                          "bytes_per_launch": tot_bytes / launches, "launch_ms": kernel_ms},
             "gpu_launches": launches,
             "e2e": e2e,
@@ -398,6 +415,7 @@ def run_sharded(args, rank, world, local):
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if args.exchange == "nccl":
         sl.stats.c1_bytes_sent = sl.stats.c2_bytes_sent = 0
+    l0 = getattr(sl, "launches", None)
     sl.profile = True
     torch.cuda.synchronize()
     dist.barrier()
@@ -411,6 +429,7 @@ def run_sharded(args, rank, world, local):
     clocks = sampler.stop()
     ms = ev0.elapsed_time(ev1)
     phases = sl.phase_ms()
+    l1 = getattr(sl, "launches", None)
     sl.profile = False
     sl.ops.check()
     # owner-pool algorithmic bytes: every rank pools, for each requester, the
@@ -494,7 +513,7 @@ def run_sharded(args, rank, world, local):
                     "peak_gbs": 900.0, "phases_ms_total": {k: round(v, 3) for k, v in phases.items()},
                     "note": ("NCCL all_to_all_single; includes the self-slice" if args.exchange == "nccl" else
                              "fused: pooled rows stored to peers inside K4; ms = the fused kernel's time")},
-            "gpu_launches": None,
+            "gpu_launches": (l1 - l0) if l0 is not None else None,
             "e2e": e2e, "cpu_baseline": None, "clocks": clocks,
         }
         print(json.dumps(line), flush=True)

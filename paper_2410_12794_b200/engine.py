@@ -154,6 +154,21 @@ class LookupEngine:
             self.raise_if_bad(batch)
         return out
 
+    def capture(self, batches, outs, stream=None):
+        """Capture one K4 launch per (batch, out) pair into a CUDA graph
+        (small batches are launch-bound: cfg1 moves ~21 MB per batch). The
+        segment descriptors are uploaded before capture; replay with
+        graph.replay(); check status with raise_if_bad() afterwards."""
+        for b, o in zip(batches, outs):
+            self._segments(b, o)
+        torch.cuda.synchronize(self.device)
+        g = torch.cuda.CUDAGraph()
+        s = stream or torch.cuda.Stream(self.device)
+        with torch.cuda.graph(g, stream=s):
+            for b, o in zip(batches, outs):
+                self.pool(b, out=o, check=False)
+        return g
+
     def raise_if_bad(self, batch: CsrBatch, batch_id: int = 0) -> None:
         """[sync] Raise LookupValidationError for the first bad index in
         (lookup, feature, position) order, with the reference's message

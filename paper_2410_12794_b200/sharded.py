@@ -538,8 +538,10 @@ class P2PShardedLookup:
             self._tmp = torch.empty((n_bags, D), dtype=torch.float32, device=dev)
         self.profile = False
         self.timeline = []
+        self.launches = 0  # our kernels launched (libflexemb), for bench accounting
 
     def _barrier(self):
+        self.launches += 1
         L = self._lib
         self.epoch += 1
         L.check(L.lib.fx_peer_barrier(self.b_flags.ptr, self.t_peer_flags.data_ptr(), self.rank, self.world,
@@ -583,6 +585,7 @@ class P2PShardedLookup:
                                    self.ops.bag_table.data_ptr(), indices.data_ptr(), L.idx_type_of(indices),
                                    offsets.data_ptr(), self.n_bags, None, self.ops.status.err.data_ptr(),
                                    self.ops.status.code.data_ptr(), L.stream_ptr()), "validate")
+            self.launches += 2  # k_route (validate) + k_push_csr
             L.check(L.lib.fx_push_csr(indices.data_ptr(), L.idx_type_of(indices), offsets.data_ptr(), B, F,
                                       self.t_feat_owner.data_ptr(), self.t_feat_pos.data_ptr(),
                                       self.t_dst_idx.data_ptr(), self.t_dst_offs.data_ptr(), 1, L.stream_ptr()),
@@ -600,12 +603,14 @@ class P2PShardedLookup:
                                      self.t_scan.data_ptr(), self.t_dst_idx.data_ptr(), self.t_dst_offs.data_ptr(),
                                      self.t_ws.data_ptr(), ctypes.byref(wsb), L.stream_ptr()), "rw push")
             self._counts = self.t_counts[:W * self.n_bags].view(W, self.n_bags)
+            self.launches += 4  # k_route (validate), k_rw_count, k_rw_push, k_rw_push_offsets
         self._close(tok)
         tok = self._mark("barrier")
         self._barrier()
         self._close(tok)
         tok = self._mark("pool")
         if self.n_segs:
+            self.launches += 1
             L.check(L.lib.fx_gather_pool(self.segs.data_ptr(), self.n_segs, D, self.b_idx.ptr, L.FX_IDX_I32,
                                          None, self.n_vbags,
                                          (L.FX_OUT_F32 if self.mode == "tablewise" else L.FX_OUT_F64_PARTIAL)
@@ -621,6 +626,7 @@ class P2PShardedLookup:
         else:
             tok = self._mark("combine")
             cptr = torch.tensor([self._counts[s].data_ptr() for s in range(W)], dtype=torch.int64, device=self.device)
+            self.launches += 1
             L.check(L.lib.fx_combine(self._pp.data_ptr(), cptr.data_ptr(), W, D, None, None, self.n_bags, D, 0,
                                      self.bag_ops.data_ptr(), self._tmp.data_ptr(), D, None, L.stream_ptr()),
                     "combine")
