@@ -436,6 +436,10 @@ class P2PShardedLookup:
             self.tw_owner = [(-1 if t in self.replicated else next(iter(tab_owner[t]))) for t in self.ftab]
             self.feat_owner = [rank if o < 0 else o for o in self.tw_owner]
         self.max_nnz = int(max_nnz) if max_nnz is not None else n_bags * 64
+        # every rank must use the same slot geometry (requesters address peers' slots)
+        agreed = [None] * W
+        dist.all_gather_object(agreed, self.max_nnz, group=group)
+        self.max_nnz = max(agreed)
         dev = self.device
         # IPC-exported staging buffers
         self.b_flags = DevBuffer(W * 8)

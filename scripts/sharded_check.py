@@ -35,9 +35,13 @@ def main():
         placement = [ShardSpec(big[s.table_id], s.start, s.end, s.server_id) for s in sub]
         sl = P2PShardedLookup(metas, placement, 0, tuple(range(len(rows))), ops, B, rank, world, f"cuda:{local}",
                               mode=mode, replicated_tables=repl)
+    elif exchange == "p2p":
+        # per-rank staging requirement differs (ragged batches): the class must agree on one geometry
+        sl = P2PShardedLookup(metas, placement, 0, tuple(range(len(rows))), ops, B, rank, world, f"cuda:{local}",
+                              mode=mode, max_nnz=B * len(rows) * 40 + 97 * rank)
     else:
-        cls = P2PShardedLookup if exchange == "p2p" else ShardedLookup
-        sl = cls(metas, placement, 0, tuple(range(len(rows))), ops, B, rank, world, f"cuda:{local}", mode=mode)
+        sl = ShardedLookup(metas, placement, 0, tuple(range(len(rows))), ops, B, rank, world, f"cuda:{local}",
+                           mode=mode)
     worst, exact, n = 0.0, 0, 0
     for it in range(3):
         hb = DlrmBatchGen(rows, 1.0, B, (1, 40), seed=100 * rank + it, ops=ops, permute=(mode == "rowwise")).next()
