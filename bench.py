@@ -197,6 +197,8 @@ def main():
     ap.add_argument("--alpha", type=float, default=None, help="override Zipf alpha (0 = uniform cold control)")
     ap.add_argument("--table-rows", type=int, default=None, help="override every table's row count (cold control)")
     ap.add_argument("--mode", default="tablewise", choices=["tablewise", "rowwise"], help="N>1 sharding")
+    ap.add_argument("--partial", default="f64", choices=["f64", "f32"],
+                    help="N>1 row-wise partial format (f32 = the reference's PartialResult semantics)")
     ap.add_argument("--graph", type=int, default=0,
                     help="N=1: capture this many batch launches per CUDA graph and time graph replays")
     ap.add_argument("--replicate-rows", type=int, default=0,
@@ -395,7 +397,7 @@ def run_sharded(args, rank, world, local):
     if args.exchange == "p2p":
         max_nnz = int(max(int(hb.offsets[-1]) for hb in host_batches) * 1.05) + 1024
         sl = P2PShardedLookup(metas, placement, 0, tuple(range(F)), ("sum",) * F, B, rank, world, dev, mode=mode,
-                              replicated_tables=repl, max_nnz=max_nnz)
+                              replicated_tables=repl, max_nnz=max_nnz, partial_dtype=args.partial)
     else:
         if repl:
             raise SystemExit("--replicate-rows needs --exchange p2p")
@@ -449,7 +451,7 @@ def run_sharded(args, rank, world, local):
     else:
         # bytes crossing NVLink per step from this rank as owner: pooled rows (+ indices read) to the
         # other ranks; table-wise f32 rows, row-wise f64 partials
-        per_row = dim * (4 if mode == "tablewise" else 8)
+        per_row = dim * (4 if mode == "tablewise" or args.partial == "f32" else 8)
         rows_out = (world - 1) * (B * sum(1 for s in placement if s.server_id == rank) if mode == "tablewise"
                                   else B * F)
         a2a_bytes = rows_out * per_row
@@ -500,7 +502,8 @@ def run_sharded(args, rank, world, local):
                        "pooling": list(cfg["pooling"]) if isinstance(cfg["pooling"], tuple) else cfg["pooling"],
                        "alpha": cfg["alpha"], "dim": dim, "tables": F,
                        "parallelism": f"{mode}-sharded x{world} ({args.exchange} exchange)"
-                                      + (f", {len(repl)} small tables replicated" if repl else ""),
+                                      + (f", {len(repl)} small tables replicated" if repl else "")
+                                      + (f", {args.partial} partials" if mode == "rowwise" else ""),
                        "l2": "inputs larger than L2 (1.18 GB algorithmic bytes per rank-batch)",
                        "init_store_s": round(init_s, 2)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

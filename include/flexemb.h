@@ -49,6 +49,8 @@ extern "C" {
 
 #define FX_OUT_F32 0              /* final pooled f32 (Mean divided once)        */
 #define FX_OUT_F64_PARTIAL 1      /* f64 partial sum (Mean deferred), see counts */
+#define FX_OUT_F32_PARTIAL 2      /* f64-accumulated partial sum rounded to f32 (Mean deferred):
+                                     PartialResult.vector semantics, pooling.py:35-47 */
 #define FX_OUT_SYSFENCE 16        /* OR-flag: system-scope fence after the epilogue stores
                                      (outputs written to peer GPUs over NVLink)        */
 
@@ -116,13 +118,14 @@ int fx_gather_rows(const float *table, int64_t ld, int64_t row_begin, int64_t ro
  * out[b] = f32( sum_{s=0..n_src-1} partials[s][b] (f64, ascending s)
  *               + sum_{k} raw rows of bag b in position order (f64) )
  * Mean divides by (sum_s counts[s][b] + raw count) once.
- * partials: device array of n_src pointers to [n_bags, dim] f64 (row stride
+ * partials: device array of n_src pointers to [n_bags, dim] f64 (f32 when
+ * partial_is_f32: each partial already rounded once, as PartialResult) (row stride
  * p_stride); counts: n_src pointers to int32[n_bags] (NULL -> partial absent
  * for every bag). raw_offsets/raw_rows: optional CSR of f32 raw vectors
  * (raw_rows row stride = dim), may be NULL. ops: int32[n_bags] or NULL (all
  * `op`). out row stride = out_stride. Bags with nothing to combine get
  * zeros and set *err_code = FX_E_EMPTY if err_code != NULL. */
-int fx_combine(const double *const *partials, const int32_t *const *counts, int32_t n_src,
+int fx_combine(const void *const *partials, int32_t partial_is_f32, const int32_t *const *counts, int32_t n_src,
                int64_t p_stride, const int64_t *raw_offsets, const float *raw_rows,
                int64_t n_bags, int32_t dim, int32_t op, const int32_t *ops,
                float *out, int64_t out_stride, int32_t *err_code, void *stream);

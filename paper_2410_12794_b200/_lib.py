@@ -32,6 +32,7 @@ FX_IDX_I32 = 0
 FX_IDX_I64 = 1
 FX_OUT_F32 = 0
 FX_OUT_F64_PARTIAL = 1
+FX_OUT_F32_PARTIAL = 2
 FX_OUT_SYSFENCE = 16
 
 INT64_MAX = (1 << 63) - 1
@@ -88,7 +89,7 @@ _SIGS = {
     "fx_table_init": ([_P, _I64, _U64, _I64, _I32, _I64, _I64, _P], ctypes.c_int),
     "fx_gather_pool": ([_P, _I32, _I32, _P, _I32, _P, _I64, _I32, _P, _P, _I32, _P, _P], ctypes.c_int),
     "fx_gather_rows": ([_P, _I64, _I64, _I64, _I32, _P, _I32, _I64, _P, _P, _P, _P], ctypes.c_int),
-    "fx_combine": ([_P, _P, _I32, _I64, _P, _P, _I64, _I32, _I32, _P, _P, _I64, _P, _P], ctypes.c_int),
+    "fx_combine": ([_P, _I32, _P, _I32, _I64, _P, _P, _I64, _I32, _I32, _P, _P, _I64, _P, _P], ctypes.c_int),
     "fx_route": ([_P, _P, _P, _P, _P, _P, _I32, _P, _I64, _P, _P, _P, _P], ctypes.c_int),
     "fx_bucket": ([_P, _I64, _P, _I64, _I32, _P, _P, _P, _P, _SZP, _P], ctypes.c_int),
     "fx_dedup": ([_P, _P, _I32, _P, _P, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _SZP, _P], ctypes.c_int),

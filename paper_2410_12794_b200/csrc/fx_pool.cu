@@ -125,6 +125,17 @@ __global__ void __launch_bounds__(256) k_gather_pool_v4(
           *reinterpret_cast<float4 *>(o + col) = q;
         }
       }
+    } else if (MODE == FX_OUT_F32_PARTIAL) {
+      float *o = static_cast<float *>(segs[s].out) + orow * segs[s].out_stride;
+#pragma unroll
+      for (int k = 0; k < NCH; ++k) {
+        const int col = (k * G + gl) * 4;
+        if (NCH == 1 || col < dim)
+          *reinterpret_cast<float4 *>(o + col) =
+              make_float4(__double2float_rn(acc[k][0]), __double2float_rn(acc[k][1]),
+                          __double2float_rn(acc[k][2]), __double2float_rn(acc[k][3]));
+      }
+      if (counts && gl == 0) counts[bag] = static_cast<int32_t>(cnt);
     } else {
       double *o = static_cast<double *>(segs[s].out) + orow * segs[s].out_stride;
 #pragma unroll
@@ -203,12 +214,15 @@ __global__ void __launch_bounds__(256) k_gather_pool_generic(
         float *o = static_cast<float *>(segs[s].out) + orow * segs[s].out_stride;
         const double v = (segs[s].op == FX_OP_MEAN && cnt > 0) ? acc[k] / static_cast<double>(cnt) : acc[k];
         o[col] = __double2float_rn(v);
+      } else if (MODE == FX_OUT_F32_PARTIAL) {
+        float *o = static_cast<float *>(segs[s].out) + orow * segs[s].out_stride;
+        o[col] = __double2float_rn(acc[k]);
       } else {
         double *o = static_cast<double *>(segs[s].out) + orow * segs[s].out_stride;
         o[col] = acc[k];
       }
     }
-    if (MODE == FX_OUT_F64_PARTIAL && counts && tile == 0 && lane == 0) counts[bag] = static_cast<int32_t>(cnt);
+    if (MODE != FX_OUT_F32 && counts && tile == 0 && lane == 0) counts[bag] = static_cast<int32_t>(cnt);
   }
   if (sysfence) __threadfence_system();
 }
@@ -235,7 +249,7 @@ __global__ void __launch_bounds__(256) k_gather_rows(const float *__restrict__ t
 // ----------------------------------------------------------------- K5
 // One warp per bag, lanes over columns (stride 32): fold partial sums in
 // ascending source order, then raw rows in position order, in f64; round once.
-__global__ void __launch_bounds__(256) k_combine(const double *const *__restrict__ partials,
+__global__ void __launch_bounds__(256) k_combine(const void *const *__restrict__ partials, int p_f32,
                                                  const int32_t *const *__restrict__ counts, int n_src,
                                                  int64_t p_stride, const int64_t *__restrict__ raw_offsets,
                                                  const float *__restrict__ raw_rows, int64_t n_bags, int dim,
@@ -260,7 +274,9 @@ __global__ void __launch_bounds__(256) k_combine(const double *const *__restrict
       double acc = 0.0;
       for (int s = 0; s < n_src; ++s) {
         const int32_t cs = counts && counts[s] ? counts[s][b] : 1;
-        if (cs > 0) acc += partials[s][b * p_stride + c];
+        if (cs > 0)
+          acc += p_f32 ? static_cast<double>(static_cast<const float *>(partials[s])[b * p_stride + c])
+                       : static_cast<const double *>(partials[s])[b * p_stride + c];
       }
       for (int64_t r = r0; r < r1; ++r) acc += static_cast<double>(raw_rows[r * dim + c]);
       if (bop == FX_OP_MEAN && total > 0) acc /= static_cast<double>(total);
@@ -451,7 +467,7 @@ int fx_gather_pool(const fx_segment *segs, int32_t n_segs, int32_t dim, const vo
   const bool sf = (out_mode & FX_OUT_SYSFENCE) != 0;
   out_mode &= ~FX_OUT_SYSFENCE;
   if (n_segs < 1 || dim < 1 || (idx_type != FX_IDX_I32 && idx_type != FX_IDX_I64) ||
-      (out_mode != FX_OUT_F32 && out_mode != FX_OUT_F64_PARTIAL)) {
+      (out_mode != FX_OUT_F32 && out_mode != FX_OUT_F64_PARTIAL && out_mode != FX_OUT_F32_PARTIAL)) {
     set_error("fx_gather_pool: bad arguments");
     return FX_E_CONFIG;
   }
@@ -461,6 +477,13 @@ int fx_gather_pool(const fx_segment *segs, int32_t n_segs, int32_t dim, const vo
   // base pointers 16-B aligned, checked host-side by the Python binding).
   const bool vec4 = (dim % 4) == 0;
   cudaStream_t st = as_stream(stream);
+  if (out_mode == FX_OUT_F32_PARTIAL) {
+    return idx_type == FX_IDX_I32
+               ? launch_pool<int32_t, FX_OUT_F32_PARTIAL>(segs, n_segs, dim, indices, offsets, n_bags, counts, err,
+                                                          bad_code, err_code, st, vec4, sf)
+               : launch_pool<int64_t, FX_OUT_F32_PARTIAL>(segs, n_segs, dim, indices, offsets, n_bags, counts, err,
+                                                          bad_code, err_code, st, vec4, sf);
+  }
   if (idx_type == FX_IDX_I32) {
     return out_mode == FX_OUT_F32
                ? launch_pool<int32_t, FX_OUT_F32>(segs, n_segs, dim, indices, offsets, n_bags, counts, err, bad_code,
@@ -495,7 +518,8 @@ int fx_gather_rows(const float *table, int64_t ld, int64_t row_begin, int64_t ro
   return FX_OK;
 }
 
-int fx_combine(const double *const *partials, const int32_t *const *counts, int32_t n_src, int64_t p_stride,
+int fx_combine(const void *const *partials, int32_t partial_is_f32, const int32_t *const *counts, int32_t n_src,
+               int64_t p_stride,
                const int64_t *raw_offsets, const float *raw_rows, int64_t n_bags, int32_t dim, int32_t op,
                const int32_t *ops, float *out, int64_t out_stride, int32_t *err_code, void *stream) {
   if (dim < 1 || n_src < 0 || n_bags < 0) {
@@ -504,7 +528,8 @@ int fx_combine(const double *const *partials, const int32_t *const *counts, int3
   }
   if (n_bags == 0) return FX_OK;
   k_combine<<<grid_for(n_bags * 32, 256), 256, 0, as_stream(stream)>>>(
-      partials, counts, n_src, p_stride, raw_offsets, raw_rows, n_bags, dim, op, ops, out, out_stride, err_code);
+      partials, partial_is_f32, counts, n_src, p_stride, raw_offsets, raw_rows, n_bags, dim, op, ops, out, out_stride,
+      err_code);
   FX_LAUNCH_CHECK("fx_combine");
   return FX_OK;
 }

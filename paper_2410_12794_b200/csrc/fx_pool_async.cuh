@@ -35,6 +35,16 @@ __device__ __forceinline__ void emit_bag(const fx_segment &sg, int64_t bag, int6
                         __double2float_rn(acc[k][3]));
       *reinterpret_cast<float4 *>(o + col) = q;
     }
+  } else if (MODE == FX_OUT_F32_PARTIAL) {
+    float *o = static_cast<float *>(sg.out) + orow * sg.out_stride;
+#pragma unroll
+    for (int k = 0; k < NCH; ++k) {
+      const int col = (k * G + lane) * 4;
+      *reinterpret_cast<float4 *>(o + col) =
+          make_float4(__double2float_rn(acc[k][0]), __double2float_rn(acc[k][1]), __double2float_rn(acc[k][2]),
+                      __double2float_rn(acc[k][3]));
+    }
+    if (counts && lane == 0) counts[bag] = static_cast<int32_t>(cnt);
   } else {
     double *o = static_cast<double *>(sg.out) + orow * sg.out_stride;
 #pragma unroll

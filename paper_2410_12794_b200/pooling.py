@@ -123,7 +123,7 @@ def combine_rows_device(partials: torch.Tensor | None, counts: torch.Tensor | No
         raw = raw.to(device=dev, dtype=torch.float32).contiguous()
         raw_off = torch.tensor([0, raw.shape[0]], dtype=torch.int64, device=dev)
     st = _lib.Status(dev)
-    _lib.check(_lib.lib.fx_combine(_lib.ptr(ptrs), _lib.ptr(cnts), n_src, D, _lib.ptr(raw_off),
+    _lib.check(_lib.lib.fx_combine(_lib.ptr(ptrs), 0, _lib.ptr(cnts), n_src, D, _lib.ptr(raw_off),
                                    _lib.ptr(raw) if raw_off is not None else None, 1, D, op_code(op), None,
                                    out.data_ptr(), D, st.code.data_ptr(), _lib.stream_ptr()), "combine")
     code, _ = st.read()

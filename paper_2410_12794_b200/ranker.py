@@ -490,7 +490,7 @@ class Ranker:
         ops = torch.zeros(n_bags, dtype=torch.int32, device=dev)
         for (t, opc, b0, b1) in lay.segs:
             ops[b0:b1] = opc
-        _lib.check(_lib.lib.fx_combine(ptrs.data_ptr(), cptr.data_ptr(), n_src, D, _lib.ptr(raw_off),
+        _lib.check(_lib.lib.fx_combine(ptrs.data_ptr(), 0, cptr.data_ptr(), n_src, D, _lib.ptr(raw_off),
                                        _lib.ptr(raw_rows), n_bags, D, 0, ops.data_ptr(), out.data_ptr(), D, None,
                                        _lib.stream_ptr()), "combine")
         return out

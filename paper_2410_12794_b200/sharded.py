@@ -168,7 +168,7 @@ class FlexOps:
         W, n_bags, D = parts.shape
         ptrs = torch.tensor([parts[s].data_ptr() for s in range(W)], dtype=torch.int64, device=self.device)
         cptr = torch.tensor([cnts[s].data_ptr() for s in range(W)], dtype=torch.int64, device=self.device)
-        L.check(L.lib.fx_combine(ptrs.data_ptr(), cptr.data_ptr(), W, D, None, None, n_bags, D, 0, bag_ops.data_ptr(),
+        L.check(L.lib.fx_combine(ptrs.data_ptr(), 0, cptr.data_ptr(), W, D, None, None, n_bags, D, 0, bag_ops.data_ptr(),
                                  out.data_ptr(), D, None, L.stream_ptr()), "combine")
 
     def check(self):
@@ -394,7 +394,7 @@ class P2PShardedLookup:
 
     def __init__(self, metas, placement, seed: int, feature_tables, feature_ops, batch_size: int, rank: int,
                  world: int, device, group=None, mode: str = "tablewise", max_nnz: int | None = None,
-                 replicated_tables=()):
+                 replicated_tables=(), partial_dtype: str = "f64"):
         """`replicated_tables` (table-wise mode): tables held in full by every
         rank and pooled locally for the rank's own batch (no exchange); they
         must not appear in `placement`. The other tables are table-sharded."""
@@ -403,6 +403,11 @@ class P2PShardedLookup:
         from .store import table_block_device
         self._lib = _lib
         self.replicated = set(replicated_tables)
+        if partial_dtype not in ("f64", "f32"):
+            raise ConfigError("partial_dtype must be 'f64' or 'f32'")
+        # row-wise partials: f64 (bit-exact vs flat) or f32 (PartialResult semantics of the
+        # reference, pooling.py:35-47 / combine_partials double rounding; half the NVLink bytes)
+        self.pesz = 8 if partial_dtype == "f64" else 4
         if self.replicated and mode != "tablewise":
             raise ConfigError("replicated tables are supported in table-wise mode only")
         if mode not in ("tablewise", "rowwise"):
@@ -458,13 +463,14 @@ class P2PShardedLookup:
             # owner-side staging: per requester slot, its indices routed here and per-bag offsets
             self.b_idx = DevBuffer(W * self.max_nnz * 4)
             self.b_offs = DevBuffer(W * (n_bags + 1) * 8)
-            self.b_out = DevBuffer(W * n_bags * D * 8)
+            self.b_out = DevBuffer(W * n_bags * D * self.pesz)
         self.t_flags = _cai_tensor(self.b_flags.ptr, (W,), torch.int64, dev)
         self.t_flags.zero_()
         if mode == "tablewise":
             self.t_out = _cai_tensor(self.b_out.ptr, (B, F * D), torch.float32, dev)
         else:
-            self.t_out = _cai_tensor(self.b_out.ptr, (W, n_bags, D), torch.float64, dev)
+            self.t_out = _cai_tensor(self.b_out.ptr, (W, n_bags, D), torch.float64 if self.pesz == 8 else torch.float32,
+                                     dev)
             self.t_counts = torch.zeros(W * n_bags + 1, dtype=torch.int32, device=dev)
             self.t_scan = torch.zeros(W * n_bags + 1, dtype=torch.int64, device=dev)
             need = ctypes.c_size_t(0)
@@ -528,8 +534,8 @@ class P2PShardedLookup:
                     tp = data.data_ptr()
                 else:
                     tp, rb, re = 0, 0, 0
-                segs.append(_lib.FxSegment(tp, rb, re, vb, vb + B, qout + (rank * n_bags + f * B) * D * 8, D, D, D,
-                                           op_code(self.fops[f]), lidx, loffs + f * B * 8))
+                segs.append(_lib.FxSegment(tp, rb, re, vb, vb + B, qout + (rank * n_bags + f * B) * D * self.pesz, D,
+                                           D, D, op_code(self.fops[f]), lidx, loffs + f * B * 8))
                 vb += B
         self.n_vbags = vb
         from .store import make_segments
@@ -537,8 +543,8 @@ class P2PShardedLookup:
         self.n_segs = len(segs)
         self.bag_ops = torch.tensor(np.repeat([op_code(o) for o in self.fops], B).astype(np.int32), device=dev)
         if mode == "rowwise":
-            self._pp = torch.tensor([self.b_out.ptr + s * n_bags * D * 8 for s in range(W)], dtype=torch.int64,
-                                    device=dev)
+            self._pp = torch.tensor([self.b_out.ptr + s * n_bags * D * self.pesz for s in range(W)],
+                                    dtype=torch.int64, device=dev)
             self._tmp = torch.empty((n_bags, D), dtype=torch.float32, device=dev)
         self.profile = False
         self.timeline = []
@@ -617,7 +623,8 @@ class P2PShardedLookup:
             self.launches += 1
             L.check(L.lib.fx_gather_pool(self.segs.data_ptr(), self.n_segs, D, self.b_idx.ptr, L.FX_IDX_I32,
                                          None, self.n_vbags,
-                                         (L.FX_OUT_F32 if self.mode == "tablewise" else L.FX_OUT_F64_PARTIAL)
+                                         (L.FX_OUT_F32 if self.mode == "tablewise" else
+                                          (L.FX_OUT_F64_PARTIAL if self.pesz == 8 else L.FX_OUT_F32_PARTIAL))
                                          | L.FX_OUT_SYSFENCE, None, self.ops.status.err.data_ptr(),
                                          L.FX_E_ROUTING_VIOLATION, self.ops.status.code.data_ptr(), L.stream_ptr()),
                     "fused pool")
@@ -631,7 +638,8 @@ class P2PShardedLookup:
             tok = self._mark("combine")
             cptr = torch.tensor([self._counts[s].data_ptr() for s in range(W)], dtype=torch.int64, device=self.device)
             self.launches += 1
-            L.check(L.lib.fx_combine(self._pp.data_ptr(), cptr.data_ptr(), W, D, None, None, self.n_bags, D, 0,
+            L.check(L.lib.fx_combine(self._pp.data_ptr(), 1 if self.pesz == 4 else 0, cptr.data_ptr(), W, D, None,
+                                     None, self.n_bags, D, 0,
                                      self.bag_ops.data_ptr(), self._tmp.data_ptr(), D, None, L.stream_ptr()),
                     "combine")
             res = self._tmp.view(F, B, D).transpose(0, 1).reshape(B, F * D)

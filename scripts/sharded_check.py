@@ -35,6 +35,9 @@ def main():
         placement = [ShardSpec(big[s.table_id], s.start, s.end, s.server_id) for s in sub]
         sl = P2PShardedLookup(metas, placement, 0, tuple(range(len(rows))), ops, B, rank, world, f"cuda:{local}",
                               mode=mode, replicated_tables=repl)
+    elif exchange == "p2pf32":
+        sl = P2PShardedLookup(metas, placement, 0, tuple(range(len(rows))), ops, B, rank, world, f"cuda:{local}",
+                              mode=mode, partial_dtype="f32")
     elif exchange == "p2p":
         # per-rank staging requirement differs (ragged batches): the class must agree on one geometry
         sl = P2PShardedLookup(metas, placement, 0, tuple(range(len(rows))), ops, B, rank, world, f"cuda:{local}",

@@ -36,3 +36,17 @@ def test_sharded_hybrid_replicated_p2p():
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "SHARDED tablewise p2phybrid" in r.stdout
+
+
+def test_sharded_rowwise_f32_partials():
+    """f32 partials (the reference's PartialResult format): within tolerance of flat."""
+    n = torch.cuda.device_count() if torch.cuda.is_available() else 0
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    w = min(n, 4)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={w}",
+           "--master-addr", "127.0.0.1", "--master-port", "29573", os.path.join(ROOT, "scripts", "sharded_check.py"),
+           "rowwise", "p2pf32"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "SHARDED rowwise p2pf32" in r.stdout
