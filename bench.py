@@ -8,8 +8,8 @@ N=1 workload = BASELINE.json configs[1]: Criteo-Kaggle-shaped, 26 tables
 (real cardinalities) x dim 128 fp32, batch 4096, pooling factor U[1,40],
 Zipf alpha 1.05, single B200. A step = one batch through
 the fused gather+pool (validation included). N>1 (torchrun, one rank per
-GPU) runs N replicas on disjoint batch streams (cfg2 is a single-GPU config,
-SURVEY §8(e): "replicas only"), weak scaling, max-over-ranks device time.
+GPU) runs the cfg2 tables sharded across the GPUs with the fused NVLink
+exchange (see run_sharded), weak scaling, max-over-ranks device time.
 
 Prints ONE JSON line on rank 0.
 """
@@ -201,8 +201,9 @@ def main():
                     help="N>1 row-wise partial format (f32 = the reference's PartialResult semantics)")
     ap.add_argument("--graph", type=int, default=0,
                     help="N=1: capture this many batch launches per CUDA graph and time graph replays")
-    ap.add_argument("--replicate-rows", type=int, default=0,
-                    help="N>1 table-wise: replicate tables with <= this many rows on every rank (hybrid placement)")
+    ap.add_argument("--replicate-rows", type=int, default=1_000_000,
+                    help="N>1 table-wise: replicate tables with <= this many rows on every rank (hybrid "
+                         "placement: small tables data-parallel, big tables table-sharded); 0 = pure table-wise")
     ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
                     help="N>1 pooled-result exchange: fused NVLink peer stores (p2p) or NCCL all-to-all")
     args = ap.parse_args()
@@ -370,11 +371,16 @@ def main():
 
 
 def run_sharded(args, rank, world, local):
-    """N>1: the cfg2 tables sharded across the ranks (table-wise by default,
-    SURVEY §8(e) cfg4 pattern; --mode rowwise for the cfg5 pattern), every
-    rank a requester with its own 4096-sample batch stream (weak scaling).
-    A step = route/bucket (K1) -> index all-to-all (C1) -> owner gather+pool
-    (K4) -> pooled all-to-all (C2) -> placement / combine (K5)."""
+    """N>1: the cfg2 tables sharded across the ranks, every rank a requester
+    with its own 4096-sample batch stream (weak scaling). Default placement is
+    hybrid table-wise: tables <= 1M rows replicated on every rank and pooled
+    locally, the big tables table-sharded (SURVEY §8(e) cfg4 pattern); use
+    --replicate-rows 0 for pure table-wise, --mode rowwise for the cfg5
+    pattern. Default exchange is fused over NVLink (--exchange p2p): a step =
+    validate + push index slices into the owners' staging (P2P stores) ->
+    barrier -> one owner gather+pool (K4) launch storing pooled rows into the
+    requesters' buffers -> barrier (-> K5 combine, row-wise). --exchange nccl
+    runs the all-to-all baseline (K1 route/bucket -> C1 -> K4 -> C2)."""
     import torch
     import torch.distributed as dist
     from paper_2410_12794_b200.sharded import P2PShardedLookup, ShardedLookup, rowwise_placement, tablewise_placement
@@ -383,7 +389,10 @@ def run_sharded(args, rank, world, local):
     rows, dim, B = cfg["table_rows"], cfg["dim"], cfg["batch"]
     F = len(rows)
     mode = args.mode
-    repl = [t for t, n in enumerate(rows) if n <= args.replicate_rows] if mode == "tablewise" else []
+    repl = ([t for t, n in enumerate(rows) if n <= args.replicate_rows]
+            if mode == "tablewise" and args.exchange == "p2p" else [])
+    if len(repl) == F:  # everything would be replicated: keep at least the largest table sharded
+        repl.remove(max(range(F), key=lambda t: rows[t]))
     big = [t for t in range(F) if t not in repl]
     if mode == "tablewise":
         sub = tablewise_placement([rows[t] for t in big], world)

@@ -69,7 +69,16 @@ __global__ void __launch_bounds__(256) k_push_csr(const IdxT *__restrict__ indic
   const int64_t n = b1 - b0;
   const int64_t per = (n + gridDim.x - 1) / gridDim.x;
   const int64_t lo = blockIdx.x * per, hi = min(n, lo + per);
-  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) di[i] = static_cast<int32_t>(indices[b0 + i]);
+  // 4 independent loads in flight per thread before the peer stores
+  int64_t i = lo + threadIdx.x;
+  for (; i + 3 * blockDim.x < hi; i += 4 * blockDim.x) {
+    IdxT v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = indices[b0 + i + u * blockDim.x];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) di[i + u * blockDim.x] = static_cast<int32_t>(v[u]);
+  }
+  for (; i < hi; i += blockDim.x) di[i] = static_cast<int32_t>(indices[b0 + i]);
   int64_t *dof = dst_offs[d] + (int64_t)feat_pos[f] * B;
   const int64_t pb = (B + 1 + gridDim.x - 1) / gridDim.x;
   const int64_t olo = blockIdx.x * pb, ohi = min((int64_t)B + 1, olo + pb);
@@ -219,7 +228,11 @@ int fx_push_csr(const void *indices, int32_t idx_type, const int64_t *offsets, i
     set_error("fx_push_csr: bad shape");
     return FX_E_CONFIG;
   }
-  dim3 grid(8, F);
+  // ~4 waves of 256-thread blocks over the SMs, split evenly across features
+  int per_f = (num_sms() * 8 + F - 1) / F;
+  if (per_f < 1) per_f = 1;
+  if (per_f > 64) per_f = 64;
+  dim3 grid(per_f, F);
   if (idx_type == FX_IDX_I32)
     k_push_csr<int32_t><<<grid, 256, 0, as_stream(stream)>>>(static_cast<const int32_t *>(indices), offsets, B, F,
                                                              feat_owner, feat_pos, dst_idx, dst_offs, sysfence != 0);
