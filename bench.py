@@ -153,19 +153,21 @@ def run_reference(args, rank, world):
     (oracle port of Ranker.execute_batch) on all host cores, rank 0 only."""
     if rank != 0:
         return
-    from oracle.cpu_pipeline import RefPipelinePort, time_parallel
+    from oracle.cpu_pipeline import ParallelPort, RefPipelinePort
     cfg, batches = build_cfg("cfg2", 0, 1)
     hb = batches[0]
     port = RefPipelinePort(0, cfg["table_rows"], cfg["dim"], row_cap=20_000)
-    procs = os.cpu_count() or 1
-    per_proc = 8
-    for _ in range(args.warmup):
-        time_parallel(port, hb, 2, procs)
+    pp = ParallelPort(port, hb)
+    procs = pp.procs
+    per_proc = 128  # ~3,300 bags per process per step (~50-100 ms of CPU work)
+    for i in range(args.warmup):
+        pp.step(per_proc, offset=i)
     rates, walls = [], []
-    for _ in range(args.steps):
-        r, procs, wall = time_parallel(port, hb, per_proc, procs)
+    for i in range(args.steps):
+        r, wall = pp.step(per_proc, offset=7 * i)
         rates.append(r)
         walls.append(wall)
+    pp.close()
     value = statistics.median(rates)
     F = len(hb.feature_tables)
     line = {

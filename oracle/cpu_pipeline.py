@@ -79,19 +79,38 @@ def _worker(samples):
     return time.perf_counter() - t0, len(samples) * len(hb.feature_tables)
 
 
+class ParallelPort:
+    """Persistent forked worker pool over disjoint sample slices (BASELINE.md
+    CPU-baseline plan: os.cpu_count() processes, embarrassingly parallel)."""
+
+    def __init__(self, port, hb, procs: int | None = None):
+        import multiprocessing as mp
+        global _STATE
+        _STATE = (port, hb)
+        self.procs = procs or os.cpu_count() or 1
+        self.hb = hb
+        self.pool = mp.get_context("fork").Pool(self.procs)
+
+    def step(self, samples_per_proc: int, offset: int = 0):
+        """One step: every process pools its own slice; returns (bags/s, wall s)."""
+        B = self.hb.batch_size
+        slices = [[(offset + p * samples_per_proc + i) % B for i in range(samples_per_proc)]
+                  for p in range(self.procs)]
+        t0 = time.perf_counter()
+        res = self.pool.map(_worker, slices)
+        wall = time.perf_counter() - t0
+        return sum(r[1] for r in res) / wall, wall
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
+
+
 def time_parallel(port, hb, samples_per_proc: int, procs: int | None = None):
-    """Embarrassingly parallel over forked processes on disjoint sample slices
-    (BASELINE.md CPU-baseline plan). Returns (bags/s, procs, wall seconds)."""
-    import multiprocessing as mp
-    global _STATE
-    _STATE = (port, hb)
-    procs = procs or os.cpu_count() or 1
-    B = hb.batch_size
-    slices = [[(p * samples_per_proc + i) % B for i in range(samples_per_proc)] for p in range(procs)]
-    ctx = mp.get_context("fork")
-    t0 = time.perf_counter()
-    with ctx.Pool(procs) as pool:
-        res = pool.map(_worker, slices)
-    wall = time.perf_counter() - t0
-    bags = sum(r[1] for r in res)
-    return bags / wall, procs, wall
+    """One-shot variant of ParallelPort.step (includes the fork)."""
+    pp = ParallelPort(port, hb, procs)
+    try:
+        r, wall = pp.step(samples_per_proc)
+    finally:
+        pp.close()
+    return r, pp.procs, wall
