@@ -417,28 +417,15 @@ __global__ void __launch_bounds__(1024) k_offer_par(CacheView c, const uint64_t 
     }
     __syncthreads();
   }
-  // phase 2: full cache, runs of accepts / rejects
+  // phase 2: full cache
   const bool always = (mode != 0) || (c.admission != 0);
-  const long long win_max = cap < 1024 ? cap : 1024;
-  bool accept_mode = true;
-  while (true) {
-    const long long j = st[0], h = st[1], nacc = st[2];
-    if (j >= m || win_max <= 0) break;
-    const long long win = (m - j) < win_max ? (m - j) : win_max;
-    if (tid == 0) sh_first = win;
-    __syncthreads();
-    if (tid < win) {
-      bool ok;
-      const double ec = w.est_cand[pw.cand[j + tid]];
-      if (always) ok = accept_mode;
-      else if (accept_mode) ok = ec >= est_v(c, w, h + tid, e0, k_vic);
-      else ok = ec < est_v(c, w, h, e0, k_vic);
-      if (!ok) atomicMin(&sh_first, (long long)tid);
-    }
-    __syncthreads();
-    const long long run = sh_first;
-    if (accept_mode) {
-      // candidates j .. j+run-1 accepted; each evicts V[h + t]
+  if (always) {
+    // every candidate accepted, each evicting V[h + t] (windows <= cap so
+    // victims never refer to candidates accepted inside the same window)
+    const long long win_max = cap < 1024 ? cap : 1024;
+    while (win_max > 0 && st[0] < m) {
+      const long long j = st[0], h = st[1], nacc = st[2];
+      const long long run = (m - j) < win_max ? (m - j) : win_max;
       for (long long t = tid; t < run; t += blockDim.x) {
         const long long k = h + t;
         const int32_t vs = k < e0 ? w.lru_slot[k] : w.acc_slot[k - e0];
@@ -464,15 +451,98 @@ __global__ void __launch_bounds__(1024) k_offer_par(CacheView c, const uint64_t 
         st[0] += run; st[1] += run; st[2] += run; st[3] += run; st[4] += run;
         st[6] += record ? run : 0;
       }
-    } else {
-      for (long long t = tid; t < run; t += blockDim.x)
-        if (accepted) accepted[pw.cand[j + t]] = 0;
       __syncthreads();
-      if (tid == 0) st[0] += run;
     }
-    __syncthreads();
-    if (run < win || always) accept_mode = always ? true : !accept_mode;
-    __syncthreads();
+  } else {
+    // sketch admission: tiles of T <= min(1024, cap) candidates. Lane q of warp 0
+    // builds mask_q (bit b = est(c_q) >= est(V[h + a0 + b]), a0 = accepts before
+    // its 32-chunk); one thread then resolves the chunk with a register chain
+    // (a += (mask_q >> a) & 1) — the exact sequential decisions, ~a dozen
+    // cycles each regardless of how often accept and reject alternate.
+    __shared__ double s_ec[1024];
+    __shared__ double s_ev[1024 + 32];
+    __shared__ unsigned s_mask[32];
+    __shared__ int s_acc[1024];
+    __shared__ int s_rank[1024];
+    __shared__ int s_chunk_a;
+    const long long tmax = cap < 1024 ? cap : 1024;
+    while (tmax > 0 && st[0] < m) {
+      const long long j = st[0], h = st[1], nacc = st[2];
+      const int T = static_cast<int>((m - j) < tmax ? (m - j) : tmax);
+      for (int t = tid; t < T; t += blockDim.x) s_ec[t] = w.est_cand[pw.cand[j + t]];
+      for (int t = tid; t < T + 32; t += blockDim.x) s_ev[t] = t < cap ? est_v(c, w, h + t, e0, k_vic) : 0.0;
+      __syncthreads();
+      if (tid < 32) {
+        int a0 = 0;  // accepts so far in this tile
+        for (int c0 = 0; c0 < T; c0 += 32) {
+          const int q = c0 + tid;
+          unsigned mask = 0;
+          if (q < T) {
+            const double ec = s_ec[q];
+#pragma unroll
+            for (int b = 0; b < 32; ++b) mask |= (ec >= s_ev[a0 + b] ? 1u : 0u) << b;
+          }
+          s_mask[tid] = mask;
+          __syncwarp();
+          if (tid == 0) {
+            unsigned mk[32];
+#pragma unroll
+            for (int u = 0; u < 32; ++u) mk[u] = s_mask[u];
+            const int n = (T - c0) < 32 ? (T - c0) : 32;
+            int a = 0;
+#pragma unroll
+            for (int u = 0; u < 32; ++u) {
+              if (u < n) {
+                const int acc = (mk[u] >> a) & 1u;
+                s_acc[c0 + u] = acc;
+                s_rank[c0 + u] = a0 + a;
+                a += acc;
+              }
+            }
+            s_chunk_a = a;
+          }
+          __syncwarp();
+          a0 += s_chunk_a;
+          __syncwarp();
+        }
+        if (tid == 0) s_chunk_a = a0;
+      }
+      __syncthreads();
+      const int na = s_chunk_a;
+      // evicted keys (read before any slot is overwritten), then installs
+      for (int t = tid; t < T; t += blockDim.x) {
+        if (!s_acc[t]) continue;
+        const long long k = h + s_rank[t];
+        const int32_t vs = k < e0 ? w.lru_slot[k] : w.acc_slot[k - e0];
+        const uint64_t old = c.skey[vs];
+        w.ev_keys[st[3] + s_rank[t]] = old;
+        if (record && st[6] + s_rank[t] < c.evlog_cap) c.evlog[st[6] + s_rank[t]] = old;
+      }
+      __syncthreads();
+      for (int t = tid; t < T; t += blockDim.x) {
+        const int32_t jj = pw.cand[j + t];
+        if (!s_acc[t]) {
+          if (accepted) accepted[jj] = 0;
+          continue;
+        }
+        const int r = s_rank[t];
+        const long long k = h + r;
+        const int32_t vs = k < e0 ? w.lru_slot[k] : w.acc_slot[k - e0];
+        c.skey[vs] = keys[jj];
+        c.stick[vs] = st[4] + r + 1;
+        c.ssize[vs] = S;
+        c.shits[vs] = 0;
+        w.acc_slot[nacc + r] = vs;
+        w.acc_j[nacc + r] = jj;
+        if (accepted) accepted[jj] = 1;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        st[0] += T; st[1] += na; st[2] += na; st[3] += na; st[4] += na;
+        st[6] += record ? na : 0;
+      }
+      __syncthreads();
+    }
   }
   if (tid == 0) {
     sc->tick = st[4];
