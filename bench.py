@@ -199,6 +199,9 @@ def main():
     ap.add_argument("--alpha", type=float, default=None, help="override Zipf alpha (0 = uniform cold control)")
     ap.add_argument("--table-rows", type=int, default=None, help="override every table's row count (cold control)")
     ap.add_argument("--mode", default="tablewise", choices=["tablewise", "rowwise"], help="N>1 sharding")
+    ap.add_argument("--sync", action="store_true",
+                    help="N>1 fused exchange: synchronous steps (2 barriers each) instead of the pipelined stream "
+                         "(push of step k+1 overlapping the gather of step k, one barrier per step)")
     ap.add_argument("--partial", default="f64", choices=["f64", "f32"],
                     help="N>1 row-wise partial format (f32 = the reference's PartialResult semantics)")
     ap.add_argument("--graph", type=int, default=0,
@@ -432,9 +435,14 @@ def run_sharded(args, rank, world, local):
     sl.profile = True
     torch.cuda.synchronize()
     dist.barrier()
+    pipelined = args.exchange == "p2p" and not args.sync
     ev0.record(stream)
-    for i in range(args.steps):
-        sl.lookup(*batches[i % len(batches)], out=out, check=False)
+    if pipelined:
+        for _ in sl.stream((batches[i % len(batches)] for i in range(args.steps)), check=False):
+            pass
+    else:
+        for i in range(args.steps):
+            sl.lookup(*batches[i % len(batches)], out=out, check=False)
     ev1.record(stream)
     ev1.synchronize()
     torch.cuda.synchronize()
@@ -514,7 +522,8 @@ def run_sharded(args, rank, world, local):
                        "alpha": cfg["alpha"], "dim": dim, "tables": F,
                        "parallelism": f"{mode}-sharded x{world} ({args.exchange} exchange)"
                                       + (f", {len(repl)} small tables replicated" if repl else "")
-                                      + (f", {args.partial} partials" if mode == "rowwise" else ""),
+                                      + (f", {args.partial} partials" if mode == "rowwise" else "")
+                                      + (", pipelined (depth 2)" if args.exchange == "p2p" and not args.sync else ""),
                        "l2": "inputs larger than L2 (1.18 GB algorithmic bytes per rank-batch)",
                        "init_store_s": round(init_s, 2)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -310,6 +310,10 @@ static void launch_async_cr(const fx_segment *segs, int n_segs, int dim, const I
     cudaFuncSetAttribute(k_pool_async<G, NCH, CR, IdxT, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(smem));
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pool_async<G, NCH, CR, IdxT, MODE>, WARPS * 32, smem);
+    // FX_POOL_MAXB caps resident blocks per SM (leaves room for a concurrent
+    // push kernel in the pipelined sharded mode)
+    const char *e = getenv("FX_POOL_MAXB");
+    if (e && atoi(e) > 0 && per_sm > atoi(e)) per_sm = atoi(e);
     if (per_sm < 1) per_sm = 1;
   }
   int64_t blocks = static_cast<int64_t>(num_sms()) * per_sm;

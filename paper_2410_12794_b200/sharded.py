@@ -446,7 +446,7 @@ class P2PShardedLookup:
         dist.all_gather_object(agreed, self.max_nnz, group=group)
         self.max_nnz = max(agreed)
         dev = self.device
-        # IPC-exported staging buffers
+        # IPC-exported staging buffers, two sets (pipelined mode alternates them)
         self.b_flags = DevBuffer(W * 8)
         if mode == "tablewise":
             # owner-side staging: one slot per requester holding the indices and
@@ -456,27 +456,30 @@ class P2PShardedLookup:
             self.slot_feats = lambda q, d: [f for f in range(F) if self.tw_owner[f] == d or
                                             (self.tw_owner[f] < 0 and q == d)]
             self.slot_stride = [sum(1 for o in self.tw_owner if o == d) + n_repl for d in range(W)]
-            self.b_idx = DevBuffer(W * self.max_nnz * 4)
-            self.b_offs = DevBuffer(W * (self.slot_stride[rank] * B + 1) * 8)
-            self.b_out = DevBuffer(n_bags * D * 4)
+            offs_slot = lambda d: (self.slot_stride[d] * B + 1) * 8
+            out_set = n_bags * D * 4
         else:
-            # owner-side staging: per requester slot, its indices routed here and per-bag offsets
-            self.b_idx = DevBuffer(W * self.max_nnz * 4)
-            self.b_offs = DevBuffer(W * (n_bags + 1) * 8)
-            self.b_out = DevBuffer(W * n_bags * D * self.pesz)
+            offs_slot = lambda d: (n_bags + 1) * 8
+            out_set = W * n_bags * D * self.pesz
+        self.idx_set = W * self.max_nnz * 4               # bytes per set, uniform across ranks
+        self.offs_set = [W * offs_slot(d) for d in range(W)]
+        self.out_set = out_set
+        self.b_idx = DevBuffer(2 * self.idx_set)
+        self.b_offs = DevBuffer(2 * self.offs_set[rank])
+        self.b_out = DevBuffer(2 * self.out_set)
         self.t_flags = _cai_tensor(self.b_flags.ptr, (W,), torch.int64, dev)
         self.t_flags.zero_()
         if mode == "tablewise":
-            self.t_out = _cai_tensor(self.b_out.ptr, (B, F * D), torch.float32, dev)
+            self.t_out = [_cai_tensor(self.b_out.ptr + p * out_set, (B, F * D), torch.float32, dev) for p in (0, 1)]
         else:
-            self.t_out = _cai_tensor(self.b_out.ptr, (W, n_bags, D), torch.float64 if self.pesz == 8 else torch.float32,
-                                     dev)
-            self.t_counts = torch.zeros(W * n_bags + 1, dtype=torch.int32, device=dev)
-            self.t_scan = torch.zeros(W * n_bags + 1, dtype=torch.int64, device=dev)
+            pdt = torch.float64 if self.pesz == 8 else torch.float32
+            self.t_out = [_cai_tensor(self.b_out.ptr + p * out_set, (W, n_bags, D), pdt, dev) for p in (0, 1)]
+            self.t_counts = [torch.zeros(W * n_bags + 1, dtype=torch.int32, device=dev) for _ in (0, 1)]
+            self.t_scan = [torch.zeros(W * n_bags + 1, dtype=torch.int64, device=dev) for _ in (0, 1)]
             need = ctypes.c_size_t(0)
             _lib.check(_lib.lib.fx_rw_push(None, None, None, None, None, 0, None, n_bags, W, None, None, None, None,
                                            None, ctypes.byref(need), None), "rw push ws")
-            self.t_ws = torch.empty(max(need.value, 1), dtype=torch.uint8, device=dev)
+            self.t_ws = [torch.empty(max(need.value, 1), dtype=torch.uint8, device=dev) for _ in (0, 1)]
         torch.cuda.synchronize(dev)
         mine = [self.b_idx.handle(), self.b_offs.handle(), self.b_out.handle(), self.b_flags.handle()]
         allh = [None] * W
@@ -494,58 +497,56 @@ class P2PShardedLookup:
         self.t_peer_flags = torch.tensor([p[3] for p in ptrs], dtype=torch.int64, device=dev)
         self.t_timeout = torch.zeros(1, dtype=torch.int32, device=dev)
         self.epoch = 0
-        # owner segments over every requester's bags (virtual bag space)
-        segs = []
-        vb = 0
+        from .store import make_segments
+        self.segs, self.t_dst_idx, self.t_dst_offs = [], [], []
+        for p in (0, 1):
+            # push targets: this requester's slot (set p) in every owner's staging
+            self.t_dst_idx.append(torch.tensor([ptrs[d][0] + p * self.idx_set + rank * self.max_nnz * 4
+                                                for d in range(W)], dtype=torch.int64, device=dev))
+            self.t_dst_offs.append(torch.tensor([ptrs[d][1] + p * self.offs_set[d] + rank * offs_slot(d)
+                                                 for d in range(W)], dtype=torch.int64, device=dev))
+            # owner segments over every requester's bags (virtual bag space), set p
+            segs = []
+            vb = 0
+            for q in range(W):
+                qout = ptrs[q][2] + p * out_set
+                lidx = self.b_idx.ptr + p * self.idx_set + q * self.max_nnz * 4
+                loffs = self.b_offs.ptr + p * self.offs_set[rank] + q * offs_slot(rank)
+                if mode == "tablewise":
+                    for j, f in enumerate(self.slot_feats(q, rank)):
+                        data, rb, re = self.ops.local[self.ftab[f]]
+                        segs.append(_lib.FxSegment(data.data_ptr(), rb, re, vb, vb + B, qout + f * D * 4, F * D, D,
+                                                   D, op_code(self.fops[f]), lidx, loffs + j * B * 8))
+                        vb += B
+                else:
+                    for f in range(F):
+                        t = self.ftab[f]
+                        if t in self.ops.local:
+                            data, rb, re = self.ops.local[t]
+                            tp = data.data_ptr()
+                        else:
+                            tp, rb, re = 0, 0, 0
+                        segs.append(_lib.FxSegment(tp, rb, re, vb, vb + B,
+                                                   qout + (rank * n_bags + f * B) * D * self.pesz, D, D, D,
+                                                   op_code(self.fops[f]), lidx, loffs + f * B * 8))
+                        vb += B
+            self.n_vbags = vb
+            self.n_segs = len(segs)
+            self.segs.append(make_segments(segs, dev) if segs else None)
         if mode == "tablewise":
-            # push targets: this requester's slot in every owner's staging
-            self.t_dst_idx = torch.tensor([ptrs[d][0] + rank * self.max_nnz * 4 for d in range(W)], dtype=torch.int64,
-                                          device=dev)
-            self.t_dst_offs = torch.tensor([ptrs[d][1] + rank * (self.slot_stride[d] * B + 1) * 8 for d in range(W)],
-                                           dtype=torch.int64, device=dev)
             pos = [0] * F
             for d in range(W):
                 for j, f in enumerate(self.slot_feats(rank, d)):
                     pos[f] = j
             self.t_feat_owner = torch.tensor(self.feat_owner, dtype=torch.int32, device=dev)
             self.t_feat_pos = torch.tensor(pos, dtype=torch.int32, device=dev)
-            for q in range(W):
-                qout = ptrs[q][2]
-                lidx = self.b_idx.ptr + q * self.max_nnz * 4
-                loffs = self.b_offs.ptr + q * (self.slot_stride[rank] * B + 1) * 8
-                for j, f in enumerate(self.slot_feats(q, rank)):
-                    data, rb, re = self.ops.local[self.ftab[f]]
-                    segs.append(_lib.FxSegment(data.data_ptr(), rb, re, vb, vb + B, qout + f * D * 4, F * D, D, D,
-                                               op_code(self.fops[f]), lidx, loffs + j * B * 8))
-                    vb += B
-        if mode == "rowwise":
-            self.t_dst_idx = torch.tensor([ptrs[d][0] + rank * self.max_nnz * 4 for d in range(W)], dtype=torch.int64,
-                                          device=dev)
-            self.t_dst_offs = torch.tensor([ptrs[d][1] + rank * (n_bags + 1) * 8 for d in range(W)],
-                                           dtype=torch.int64, device=dev)
-        for q in range(W) if mode == "rowwise" else ():
-            qout = ptrs[q][2]
-            lidx = self.b_idx.ptr + q * self.max_nnz * 4
-            loffs = self.b_offs.ptr + q * (n_bags + 1) * 8
-            for f in range(F):
-                t = self.ftab[f]
-                if t in self.ops.local:
-                    data, rb, re = self.ops.local[t]
-                    tp = data.data_ptr()
-                else:
-                    tp, rb, re = 0, 0, 0
-                segs.append(_lib.FxSegment(tp, rb, re, vb, vb + B, qout + (rank * n_bags + f * B) * D * self.pesz, D,
-                                           D, D, op_code(self.fops[f]), lidx, loffs + f * B * 8))
-                vb += B
-        self.n_vbags = vb
-        from .store import make_segments
-        self.segs = make_segments(segs, dev) if segs else None
-        self.n_segs = len(segs)
         self.bag_ops = torch.tensor(np.repeat([op_code(o) for o in self.fops], B).astype(np.int32), device=dev)
         if mode == "rowwise":
-            self._pp = torch.tensor([self.b_out.ptr + s * n_bags * D * self.pesz for s in range(W)],
-                                    dtype=torch.int64, device=dev)
-            self._tmp = torch.empty((n_bags, D), dtype=torch.float32, device=dev)
+            self._pp = [torch.tensor([self.b_out.ptr + p * out_set + s * n_bags * D * self.pesz for s in range(W)],
+                                     dtype=torch.int64, device=dev) for p in (0, 1)]
+            self._cptr = [torch.tensor([self.t_counts[p].data_ptr() + s * n_bags * 4 for s in range(W)],
+                                       dtype=torch.int64, device=dev) for p in (0, 1)]
+            self._tmp = [torch.empty((n_bags, D), dtype=torch.float32, device=dev) for _ in (0, 1)]
         self.profile = False
         self.timeline = []
         self.launches = 0  # our kernels launched (libflexemb), for bench accounting
@@ -578,80 +579,141 @@ class P2PShardedLookup:
         self.timeline = []
         return out
 
-    def lookup(self, indices: torch.Tensor, offsets: torch.Tensor, out: torch.Tensor | None = None,
-               check: bool = True) -> torch.Tensor:
-        """Pool this rank's batch. Returns [B, F*D] f32 (the internal output
-        buffer unless `out` is given; valid until the next call)."""
+    def _stage(self, indices, offsets, p, stream=None):
+        """Ingress validation + push of this rank's batch into every owner's
+        staging (set p)."""
         L = self._lib
-        B, F, D, W = self.B, self.F, self.D, self.world
+        B, F, W = self.B, self.F, self.world
         nnz = int(indices.numel())
         if nnz > self.max_nnz:
             raise ConfigError(f"batch has {nnz} indices, staging holds {self.max_nnz}")
-        tok = self._mark("stage")
+        o = self.ops
+        sp = L.stream_ptr(stream)
+        L.check(L.lib.fx_route(o.route_off.data_ptr(), o.starts.data_ptr(), o.owners.data_ptr(), o.nrows.data_ptr(),
+                               o.bag_table.data_ptr(), indices.data_ptr(), L.idx_type_of(indices), offsets.data_ptr(),
+                               self.n_bags, None, o.status.err.data_ptr(), o.status.code.data_ptr(), sp),
+                "validate")
         if self.mode == "tablewise":
-            # ingress validation on the requester (owners only see their own shards)
-            L.check(L.lib.fx_route(self.ops.route_off.data_ptr(), self.ops.starts.data_ptr(),
-                                   self.ops.owners.data_ptr(), self.ops.nrows.data_ptr(),
-                                   self.ops.bag_table.data_ptr(), indices.data_ptr(), L.idx_type_of(indices),
-                                   offsets.data_ptr(), self.n_bags, None, self.ops.status.err.data_ptr(),
-                                   self.ops.status.code.data_ptr(), L.stream_ptr()), "validate")
             self.launches += 2  # k_route (validate) + k_push_csr
             L.check(L.lib.fx_push_csr(indices.data_ptr(), L.idx_type_of(indices), offsets.data_ptr(), B, F,
                                       self.t_feat_owner.data_ptr(), self.t_feat_pos.data_ptr(),
-                                      self.t_dst_idx.data_ptr(), self.t_dst_offs.data_ptr(), 1, L.stream_ptr()),
-                    "push")
+                                      self.t_dst_idx[p].data_ptr(), self.t_dst_offs[p].data_ptr(), 1, sp), "push")
         else:
-            o = self.ops
-            L.check(L.lib.fx_route(o.route_off.data_ptr(), o.starts.data_ptr(), o.owners.data_ptr(),
-                                   o.nrows.data_ptr(), o.bag_table.data_ptr(), indices.data_ptr(),
-                                   L.idx_type_of(indices), offsets.data_ptr(), self.n_bags, None,
-                                   o.status.err.data_ptr(), o.status.code.data_ptr(), L.stream_ptr()), "validate")
-            wsb = ctypes.c_size_t(self.t_ws.numel())
+            wsb = ctypes.c_size_t(self.t_ws[p].numel())
             L.check(L.lib.fx_rw_push(o.route_off.data_ptr(), o.starts.data_ptr(), o.owners.data_ptr(),
                                      o.bag_table.data_ptr(), indices.data_ptr(), L.idx_type_of(indices),
-                                     offsets.data_ptr(), self.n_bags, W, self.t_counts.data_ptr(),
-                                     self.t_scan.data_ptr(), self.t_dst_idx.data_ptr(), self.t_dst_offs.data_ptr(),
-                                     self.t_ws.data_ptr(), ctypes.byref(wsb), L.stream_ptr()), "rw push")
-            self._counts = self.t_counts[:W * self.n_bags].view(W, self.n_bags)
+                                     offsets.data_ptr(), self.n_bags, W, self.t_counts[p].data_ptr(),
+                                     self.t_scan[p].data_ptr(), self.t_dst_idx[p].data_ptr(),
+                                     self.t_dst_offs[p].data_ptr(), self.t_ws[p].data_ptr(), ctypes.byref(wsb), sp),
+                    "rw push")
             self.launches += 4  # k_route (validate), k_rw_count, k_rw_push, k_rw_push_offsets
+
+    def _gather(self, p):
+        """ONE K4 launch over every requester's bags of this rank's tables,
+        pooled rows stored into the requesters' output buffers (set p)."""
+        L = self._lib
+        if not self.n_segs:
+            return
+        self.launches += 1
+        mode = (L.FX_OUT_F32 if self.mode == "tablewise" else
+                (L.FX_OUT_F64_PARTIAL if self.pesz == 8 else L.FX_OUT_F32_PARTIAL))
+        L.check(L.lib.fx_gather_pool(self.segs[p].data_ptr(), self.n_segs, self.D, self.b_idx.ptr, L.FX_IDX_I32,
+                                     None, self.n_vbags, mode | L.FX_OUT_SYSFENCE, None,
+                                     self.ops.status.err.data_ptr(), L.FX_E_ROUTING_VIOLATION,
+                                     self.ops.status.code.data_ptr(), L.stream_ptr()), "fused pool")
+
+    def _result(self, p):
+        """Pooled [B, F*D] f32 of the step that used set p (row-wise: K5 first)."""
+        if self.mode == "tablewise":
+            return self.t_out[p]
+        L = self._lib
+        B, F, D, W = self.B, self.F, self.D, self.world
+        self.launches += 1
+        L.check(L.lib.fx_combine(self._pp[p].data_ptr(), 1 if self.pesz == 4 else 0, self._cptr[p].data_ptr(), W, D,
+                                 None, None, self.n_bags, D, 0, self.bag_ops.data_ptr(), self._tmp[p].data_ptr(), D,
+                                 None, L.stream_ptr()), "combine")
+        return self._tmp[p].view(F, B, D).transpose(0, 1).reshape(B, F * D)
+
+    def _check(self):
+        self.ops.check()
+        if int(self.t_timeout.item()):
+            raise RuntimeError("peer barrier timed out (a rank stopped participating)")
+
+    def lookup(self, indices: torch.Tensor, offsets: torch.Tensor, out: torch.Tensor | None = None,
+               check: bool = True) -> torch.Tensor:
+        """Pool this rank's batch synchronously (stage -> barrier -> fused
+        gather -> barrier). Returns [B, F*D] f32 (the internal output buffer
+        unless `out` is given; valid until the next call)."""
+        tok = self._mark("stage")
+        self._stage(indices, offsets, 0)
         self._close(tok)
         tok = self._mark("barrier")
         self._barrier()
         self._close(tok)
         tok = self._mark("pool")
-        if self.n_segs:
-            self.launches += 1
-            L.check(L.lib.fx_gather_pool(self.segs.data_ptr(), self.n_segs, D, self.b_idx.ptr, L.FX_IDX_I32,
-                                         None, self.n_vbags,
-                                         (L.FX_OUT_F32 if self.mode == "tablewise" else
-                                          (L.FX_OUT_F64_PARTIAL if self.pesz == 8 else L.FX_OUT_F32_PARTIAL))
-                                         | L.FX_OUT_SYSFENCE, None, self.ops.status.err.data_ptr(),
-                                         L.FX_E_ROUTING_VIOLATION, self.ops.status.code.data_ptr(), L.stream_ptr()),
-                    "fused pool")
+        self._gather(0)
         self._close(tok)
         tok = self._mark("barrier")
         self._barrier()
         self._close(tok)
-        if self.mode == "tablewise":
-            res = self.t_out
-        else:
-            tok = self._mark("combine")
-            cptr = torch.tensor([self._counts[s].data_ptr() for s in range(W)], dtype=torch.int64, device=self.device)
-            self.launches += 1
-            L.check(L.lib.fx_combine(self._pp.data_ptr(), 1 if self.pesz == 4 else 0, cptr.data_ptr(), W, D, None,
-                                     None, self.n_bags, D, 0,
-                                     self.bag_ops.data_ptr(), self._tmp.data_ptr(), D, None, L.stream_ptr()),
-                    "combine")
-            res = self._tmp.view(F, B, D).transpose(0, 1).reshape(B, F * D)
-            self._close(tok)
+        tok = self._mark("combine")
+        res = self._result(0)
+        self._close(tok)
         if out is not None:
             out.copy_(res)
             res = out
         if check:
-            self.ops.check()
-            if int(self.t_timeout.item()):
-                raise RuntimeError("peer barrier timed out (a rank stopped participating)")
+            self._check()
         return res
+
+    def stream(self, batches, check: bool = True):
+        """Pipelined lookups (the reference's pipeline_depth = 2): yields the
+        pooled [B, F*D] of every (indices, offsets) batch, in order, one step
+        behind submission. The push of step k+1 runs on a side stream while
+        step k's fused gather runs, staging / outputs alternate between two
+        buffer sets, and ONE barrier per step certifies both "every rank's push
+        of step k landed" and "every rank's gather of step k-1 is done". A
+        yielded tensor is valid until the generator is advanced twice; consume
+        it on the current stream."""
+        main = torch.cuda.current_stream(self.device)
+        side = torch.cuda.Stream(self.device)
+        ev_bar = None
+        k = 0
+        for indices, offsets in batches:
+            p = k % 2
+            with torch.cuda.stream(side):
+                if ev_bar is not None:
+                    side.wait_event(ev_bar)  # set p's previous readers (gather k-2) certified done
+                tok = self._mark("stage")
+                self._stage(indices, offsets, p, stream=side)
+                self._close(tok)
+                ev_push = torch.cuda.Event()
+                ev_push.record(side)
+            main.wait_event(ev_push)
+            tok = self._mark("barrier")
+            self._barrier()
+            self._close(tok)
+            ev_bar = torch.cuda.Event()
+            ev_bar.record(main)
+            if k >= 1:
+                tok = self._mark("combine")
+                res = self._result(1 - p)
+                self._close(tok)
+                yield res
+            tok = self._mark("pool")
+            self._gather(p)
+            self._close(tok)
+            k += 1
+        if k:
+            tok = self._mark("barrier")
+            self._barrier()
+            self._close(tok)
+            tok = self._mark("combine")
+            res = self._result((k - 1) % 2)
+            self._close(tok)
+            yield res
+        if check:
+            self._check()
 
     def close(self):
         L = self._lib

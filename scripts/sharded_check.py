@@ -18,6 +18,8 @@ from paper_2410_12794_b200.workload import DlrmBatchGen  # noqa: E402
 def main():
     mode = sys.argv[1] if len(sys.argv) > 1 else "tablewise"
     exchange = sys.argv[2] if len(sys.argv) > 2 else "nccl"
+    pipelined = exchange.endswith("-pipe")
+    exchange = exchange[:-5] if pipelined else exchange
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -46,9 +48,18 @@ def main():
         sl = ShardedLookup(metas, placement, 0, tuple(range(len(rows))), ops, B, rank, world, f"cuda:{local}",
                            mode=mode)
     worst, exact, n = 0.0, 0, 0
-    for it in range(3):
-        hb = DlrmBatchGen(rows, 1.0, B, (1, 40), seed=100 * rank + it, ops=ops, permute=(mode == "rowwise")).next()
-        out = sl.lookup(torch.from_numpy(hb.indices).cuda(), torch.from_numpy(hb.offsets).cuda()).cpu().numpy()
+    hbs = [DlrmBatchGen(rows, 1.0, B, (1, 40), seed=100 * rank + it, ops=ops, permute=(mode == "rowwise")).next()
+           for it in range(4)]
+    if pipelined:
+        dev_b = [(torch.from_numpy(hb.indices).cuda(), torch.from_numpy(hb.offsets).cuda()) for hb in hbs]
+        torch.cuda.synchronize()
+        outs = [o.cpu().numpy() for o in sl.stream(dev_b)]
+    for it in range(4):
+        hb = hbs[it]
+        if pipelined:
+            out = outs[it]
+        else:
+            out = sl.lookup(torch.from_numpy(hb.indices).cuda(), torch.from_numpy(hb.offsets).cuda()).cpu().numpy()
         for f in range(len(rows)):
             for s in range(B):
                 b = f * B + s
@@ -60,7 +71,7 @@ def main():
     t = torch.tensor([worst, float(n - exact)], device="cuda", dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     if rank == 0:
-        print(f"SHARDED {mode} {exchange} world={world} worst_tolerance_ratio={t[0].item():.4f} "
+        print(f"SHARDED {mode} {exchange}{'-pipe' if pipelined else ''} world={world} worst_tolerance_ratio={t[0].item():.4f} "
               f"max_non_bit_exact_bags={int(t[1].item())} bags_per_rank={n}", flush=True)
     ok = t[0].item() <= 1.0
     dist.destroy_process_group()
