@@ -23,6 +23,8 @@
 #include <cub/device/device_select.cuh>
 
 #include <climits>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "fx_common.cuh"
@@ -465,14 +467,36 @@ __global__ void __launch_bounds__(1024) k_offer_par(CacheView c, const uint64_t 
     __shared__ int s_acc[1024];
     __shared__ int s_rank[1024];
     __shared__ int s_chunk_a;
+    __shared__ int s_ffa, s_ffr;
     const long long tmax = cap < 1024 ? cap : 1024;
     while (tmax > 0 && st[0] < m) {
       const long long j = st[0], h = st[1], nacc = st[2];
       const int T = static_cast<int>((m - j) < tmax ? (m - j) : tmax);
       for (int t = tid; t < T; t += blockDim.x) s_ec[t] = w.est_cand[pw.cand[j + t]];
       for (int t = tid; t < T + 32; t += blockDim.x) s_ev[t] = t < cap ? est_v(c, w, h + t, e0, k_vic) : 0.0;
+      if (tid == 0) { s_ffa = T; s_ffr = T; }
       __syncthreads();
-      if (tid < 32) {
+      // run detection: accept-run (c_t >= V[h+t]) or reject-run (c_t < V[h])
+      if (tid < T) {
+        if (!(s_ec[tid] >= s_ev[tid])) atomicMin(&s_ffa, tid);
+        if (!(s_ec[tid] < s_ev[0])) atomicMin(&s_ffr, tid);
+      }
+      __syncthreads();
+      const int ffa = s_ffa, ffr = s_ffr;
+      const bool bulk = ffa >= 256 || ffr >= 256 || ffa == T || ffr == T;
+      if (bulk) {
+        // long run: decisions are the prefix run, no chain needed
+        const bool acc_run = ffa >= ffr;
+        const int run = acc_run ? ffa : ffr;
+        for (int t = tid; t < T; t += blockDim.x) {
+          s_acc[t] = (t < run && acc_run) ? 1 : 0;
+          s_rank[t] = t;
+        }
+        if (tid == 0) {
+          s_chunk_a = acc_run ? run : 0;
+          s_ffr = run;  // decisions resolved in this tile
+        }
+      } else if (tid < 32) {
         int a0 = 0;  // accepts so far in this tile
         for (int c0 = 0; c0 < T; c0 += 32) {
           const int q = c0 + tid;
@@ -505,12 +529,16 @@ __global__ void __launch_bounds__(1024) k_offer_par(CacheView c, const uint64_t 
           a0 += s_chunk_a;
           __syncwarp();
         }
-        if (tid == 0) s_chunk_a = a0;
+        if (tid == 0) {
+          s_chunk_a = a0;
+          s_ffr = T;
+        }
       }
       __syncthreads();
       const int na = s_chunk_a;
+      const int R = s_ffr;  // decisions resolved in this tile (bulk run or the whole tile)
       // evicted keys (read before any slot is overwritten), then installs
-      for (int t = tid; t < T; t += blockDim.x) {
+      for (int t = tid; t < R; t += blockDim.x) {
         if (!s_acc[t]) continue;
         const long long k = h + s_rank[t];
         const int32_t vs = k < e0 ? w.lru_slot[k] : w.acc_slot[k - e0];
@@ -519,7 +547,7 @@ __global__ void __launch_bounds__(1024) k_offer_par(CacheView c, const uint64_t 
         if (record && st[6] + s_rank[t] < c.evlog_cap) c.evlog[st[6] + s_rank[t]] = old;
       }
       __syncthreads();
-      for (int t = tid; t < T; t += blockDim.x) {
+      for (int t = tid; t < R; t += blockDim.x) {
         const int32_t jj = pw.cand[j + t];
         if (!s_acc[t]) {
           if (accepted) accepted[jj] = 0;
@@ -538,7 +566,7 @@ __global__ void __launch_bounds__(1024) k_offer_par(CacheView c, const uint64_t 
       }
       __syncthreads();
       if (tid == 0) {
-        st[0] += T; st[1] += na; st[2] += na; st[3] += na; st[4] += na;
+        st[0] += R; st[1] += na; st[2] += na; st[3] += na; st[4] += na;
         st[6] += record ? na : 0;
       }
       __syncthreads();
@@ -872,6 +900,12 @@ int run_offer(fx_cache *c, const uint64_t *keys, int64_t n, int32_t mode, const 
       return FX_E_CAPACITY;
     }
   }
+  static const bool prof = getenv("FX_CACHE_PROFILE") != nullptr;
+  cudaEvent_t pe[5];
+  if (prof) {
+    for (auto &e : pe) cudaEventCreate(&e);
+    cudaEventRecord(pe[0], st);
+  }
   if (n > 0) k_offer_prep<<<grid_for(n, 256), 256, 0, st>>>(c->v, keys, n, sizes, w);
   int64_t k_vic = 0;
   if (h.entries > 0) {
@@ -885,6 +919,7 @@ int run_offer(fx_cache *c, const uint64_t *keys, int64_t n, int32_t mode, const 
     else
       k_vic = 0;
   }
+  if (prof) cudaEventRecord(pe[1], st);
   const bool par = c->parallel_offers && c->uniform > 0 && sizes == nullptr && n > 0;
   if (par) {
     // compact the non-present candidates, then resolve decisions run by run
@@ -900,9 +935,21 @@ int run_offer(fx_cache *c, const uint64_t *keys, int64_t n, int32_t mode, const 
   } else {
     k_offer_seq<<<1, 32, 0, st>>>(c->v, keys, n, mode, w, k_vic, accepted, c->record);
   }
+  if (prof) cudaEventRecord(pe[2], st);
   k_hash_erase<<<grid_for(h.entries + n + 1, 256), 256, 0, st>>>(c->v, w);
   if (n > 0) k_install<<<grid_for(n * 32, 256), 256, 0, st>>>(c->v, w, keys, src_rows);
   FX_LAUNCH_CHECK("fx_cache offer");
+  if (prof) {
+    cudaEventRecord(pe[3], st);
+    cudaEventSynchronize(pe[3]);
+    float a = 0, b = 0, cc = 0;
+    cudaEventElapsedTime(&a, pe[0], pe[1]);
+    cudaEventElapsedTime(&b, pe[1], pe[2]);
+    cudaEventElapsedTime(&cc, pe[2], pe[3]);
+    fprintf(stderr, "[fx_cache offer] n=%lld entries=%lld prep+sort %.3f ms, decide %.3f ms, index+rows %.3f ms\n",
+            (long long)n, (long long)h.entries, a, b, cc);
+    for (auto &e : pe) cudaEventDestroy(e);
+  }
   // keep the index below half tombstones
   rc = read_scalars(c, &h, st);
   if (rc) return rc;
