@@ -354,41 +354,6 @@ static void launch_async(const fx_segment *segs, int n_segs, int dim, const IdxT
                                            st, sf);
 }
 
-template <int NCH, int RING, int WARPS, typename IdxT, int MODE>
-static void launch_ring(const fx_segment *segs, int n_segs, int dim, const IdxT *ix, const int64_t *offsets,
-                        int64_t n_bags, int32_t *counts, int64_t *err, int32_t bad_code, int32_t *err_code,
-                        cudaStream_t st, bool sf) {
-  const size_t smem = static_cast<size_t>(WARPS) * RING * 32 * 16 * NCH;
-  static int per_sm = -1;
-  if (per_sm < 0) {
-    cudaFuncSetAttribute(k_pool_ring<NCH, RING, IdxT, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pool_ring<NCH, RING, IdxT, MODE>, WARPS * 32, smem);
-    if (per_sm < 1) per_sm = 1;
-  }
-  int64_t blocks = static_cast<int64_t>(num_sms()) * per_sm;
-  const int64_t need = (n_bags + WARPS - 1) / WARPS;
-  if (blocks > need) blocks = need;
-  k_pool_ring<NCH, RING, IdxT, MODE><<<static_cast<int>(blocks), WARPS * 32, smem, st>>>(
-      segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code, sf);
-}
-
-template <int G, int NCH, int U, typename IdxT, int MODE>
-static void launch_prefetch(const fx_segment *segs, int n_segs, int dim, const IdxT *ix, const int64_t *offsets,
-                            int64_t n_bags, int32_t *counts, int64_t *err, int32_t bad_code, int32_t *err_code,
-                            cudaStream_t st, bool sf) {
-  static int per_sm = -1;
-  if (per_sm < 0) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pool_prefetch<G, NCH, U, IdxT, MODE>, 256, 0);
-    if (per_sm < 1) per_sm = 1;
-  }
-  int64_t blocks = static_cast<int64_t>(num_sms()) * per_sm;
-  const int64_t need = (n_bags * G + 255) / 256;
-  if (blocks > need) blocks = need;
-  k_pool_prefetch<G, NCH, U, IdxT, MODE><<<static_cast<int>(blocks), 256, 0, st>>>(
-      segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code, sf);
-}
-
 template <typename IdxT, int MODE>
 static int launch_pool(const fx_segment *segs, int n_segs, int dim, const void *indices, const int64_t *offsets,
                        int64_t n_bags, int32_t *counts, int64_t *err, int32_t bad_code, int32_t *err_code,
@@ -405,21 +370,6 @@ static int launch_pool(const fx_segment *segs, int n_segs, int dim, const void *
     launch_async<8, 1, IdxT, MODE>(segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code, st, sf);
   } else if (var == 1 && dim == 512) {
     launch_async<32, 4, IdxT, MODE>(segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code, st, sf);
-  } else if (var == 3 && dim == 128) {
-    launch_ring<1, 64, 2, IdxT, MODE>(segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code, st, sf);
-  } else if (var == 4 && dim == 128) {
-    launch_ring<1, 48, 4, IdxT, MODE>(segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code, st, sf);
-  } else if (var == 5 && dim == 128) {
-    launch_ring<1, 96, 1, IdxT, MODE>(segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code, st, sf);
-  } else if (var == 2 && dim == 128) {
-    launch_prefetch<32, 1, 8, IdxT, MODE>(segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code,
-                                          st, sf);
-  } else if (var == 2 && dim == 64) {
-    launch_prefetch<16, 1, 8, IdxT, MODE>(segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code,
-                                          st, sf);
-  } else if (var == 2 && dim == 256) {
-    launch_prefetch<32, 2, 4, IdxT, MODE>(segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code,
-                                          st, sf);
   } else if (vec4 && dim == 128) {
     k_gather_pool_v4<32, 1, 8, IdxT, MODE><<<grid_for(n_bags * 32, 256), 256, 0, st>>>(
         segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code, sf);

@@ -194,248 +194,4 @@ __global__ void __launch_bounds__(128, FX_POOL_MINB) k_pool_async(const fx_segme
   if (sysfence) __threadfence_system();
 }
 
-__device__ __forceinline__ void cp_async_wait_n(int n) {
-  switch (n) {
-    case 0: asm volatile("cp.async.wait_group 0;" ::: "memory"); break;
-    case 1: asm volatile("cp.async.wait_group 1;" ::: "memory"); break;
-    case 2: asm volatile("cp.async.wait_group 2;" ::: "memory"); break;
-    default: asm volatile("cp.async.wait_group 3;" ::: "memory"); break;
-  }
-}
-
-// One chunk = up to 32 consecutive indices of one bag.
-template <typename IdxT>
-struct PoolChunk {
-  int64_t bag;   // -1 when past the warp's last bag
-  int64_t c0;    // first CSR position of the chunk
-  int64_t end;   // bag end (CSR)
-  int64_t cnt;   // bag length
-  int s;         // segment
-  int n;         // rows in the chunk
-  int first;     // chunk opens the bag
-  int last;      // chunk closes the bag
-  IdxT idx;      // this lane's index (position c0 + lane), prefetched
-};
-
-// Ring-staged variant (dim == 128*NCH): persistent warps; each warp owns a
-// shared-memory ring of RING rows and keeps up to 4 chunks (cp.async groups)
-// in flight, issuing the next chunks while it sums the oldest one, so the
-// accumulate/emit work overlaps the row fetches. Chunks of one bag are summed
-// in order (per-element sequential f64, as the reference).
-template <int NCH, int RING, typename IdxT, int MODE>
-__global__ void __launch_bounds__(128) k_pool_ring(const fx_segment *__restrict__ segs, int n_segs, int dim,
-                                                   const IdxT *__restrict__ indices_g,
-                                                   const int64_t *__restrict__ offsets, int64_t n_bags,
-                                                   int32_t *__restrict__ counts, int64_t *err, int32_t bad_code,
-                                                   int32_t *err_code, bool sysfence) {
-  constexpr int ROWB = 32 * 16 * NCH;
-  constexpr int MAXF = 4;
-  extern __shared__ __align__(16) unsigned char smem[];
-  const int lane = threadIdx.x & 31;
-  const int wib = threadIdx.x >> 5;
-  unsigned char *ring = smem + static_cast<size_t>(wib) * RING * ROWB;
-  const uint32_t sring = static_cast<uint32_t>(__cvta_generic_to_shared(ring));
-  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-
-  auto open_bag = [&](int64_t bag) {
-    PoolChunk<IdxT> c;
-    c.bag = bag;
-    if (bag >= n_bags) {
-      c.bag = -1;
-      return c;
-    }
-    c.s = find_segment(segs, n_segs, bag);
-    int64_t beg, end;
-    bag_bounds(segs, c.s, bag, offsets, beg, end);
-    const IdxT *ix = seg_indices(segs, c.s, indices_g);
-    c.c0 = beg;
-    c.end = end;
-    c.cnt = end - beg;
-    c.n = static_cast<int>(end - beg < 32 ? end - beg : 32);
-    c.first = 1;
-    c.last = (beg + 32 >= end) ? 1 : 0;
-    c.idx = (beg + lane < end) ? ix[beg + lane] : IdxT(0);
-    return c;
-  };
-  auto advance = [&](const PoolChunk<IdxT> &x) {
-    if (x.last) return open_bag(x.bag + nwarps);
-    PoolChunk<IdxT> c = x;
-    c.c0 = x.c0 + 32;
-    c.n = static_cast<int>(x.end - c.c0 < 32 ? x.end - c.c0 : 32);
-    c.first = 0;
-    c.last = (c.c0 + 32 >= x.end) ? 1 : 0;
-    const IdxT *ix = seg_indices(segs, c.s, indices_g);
-    c.idx = (c.c0 + lane < x.end) ? ix[c.c0 + lane] : IdxT(0);
-    return c;
-  };
-
-  PoolChunk<IdxT> q[MAXF];   // in-flight chunks (oldest first)
-  int qhead[MAXF];           // ring row where each chunk starts
-  int nq = 0, head = 0, used = 0;
-  PoolChunk<IdxT> nxt = open_bag(warp);
-  double acc[NCH][4];
-#pragma unroll
-  for (int k = 0; k < NCH; ++k) acc[k][0] = acc[k][1] = acc[k][2] = acc[k][3] = 0.0;
-
-  while (true) {
-    // issue as many chunks as fit
-    while (nxt.bag >= 0 && nq < MAXF && used + nxt.n <= RING) {
-      const fx_segment &sg = segs[nxt.s];
-      const float *__restrict__ tab = sg.table;
-      const int64_t idx = static_cast<int64_t>(nxt.idx);
-      int64_t my_off = 0;
-      if (lane < nxt.n) {
-        if (idx < sg.row_begin || idx >= sg.row_end) record_bad(err, err_code, nxt.c0 + lane, bad_code);
-        else my_off = (idx - sg.row_begin) * sg.ld;
-      }
-      const int start = (head + used) % RING;
-      for (int r = 0; r < nxt.n; ++r) {
-        const float *src = tab + __shfl_sync(0xffffffffu, my_off, r);
-        const int row = (start + r) % RING;
-#pragma unroll
-        for (int k = 0; k < NCH; ++k)
-          cp_async16(sring + row * ROWB + (k * 32 + lane) * 16, src + (k * 32 + lane) * 4);
-      }
-      cp_async_commit();
-      // shift the queue entry in (small fixed-size queue, register-resident after unrolling)
-#pragma unroll
-      for (int i = 0; i < MAXF; ++i)
-        if (i == nq) {
-          q[i] = nxt;
-          qhead[i] = start;
-        }
-      ++nq;
-      used += nxt.n;
-      nxt = advance(nxt);  // prefetch the following chunk's indices
-    }
-    if (nq == 0) break;
-    cp_async_wait_n(nq - 1);  // the oldest chunk has landed
-    __syncwarp();
-    const PoolChunk<IdxT> x = q[0];
-    const int xs = qhead[0];
-    for (int r = 0; r < x.n; ++r) {
-      const int row = (xs + r) % RING;
-#pragma unroll
-      for (int k = 0; k < NCH; ++k) {
-        const float4 v = *reinterpret_cast<const float4 *>(ring + row * ROWB + (k * 32 + lane) * 16);
-        acc[k][0] += static_cast<double>(v.x);
-        acc[k][1] += static_cast<double>(v.y);
-        acc[k][2] += static_cast<double>(v.z);
-        acc[k][3] += static_cast<double>(v.w);
-      }
-    }
-    __syncwarp();
-    if (x.last) {
-      emit_bag<NCH, MODE>(segs[x.s], x.bag, x.cnt, acc, lane, 32, counts);
-#pragma unroll
-      for (int k = 0; k < NCH; ++k) acc[k][0] = acc[k][1] = acc[k][2] = acc[k][3] = 0.0;
-    }
-    head = (head + x.n) % RING;
-    used -= x.n;
-#pragma unroll
-    for (int i = 0; i < MAXF - 1; ++i) {
-      q[i] = q[i + 1];
-      qhead[i] = qhead[i + 1];
-    }
-    --nq;
-  }
-  if (sysfence) __threadfence_system();
-}
-
-// Bag-per-group register variant with next-bag software prefetch: the next
-// chunk's indices (or the next bag's offsets + first chunk) are loaded right
-// after the first round of row loads is issued.
-template <int G, int NCH, int U, typename IdxT, int MODE>
-__global__ void __launch_bounds__(256) k_pool_prefetch(const fx_segment *__restrict__ segs, int n_segs, int dim,
-                                                       const IdxT *__restrict__ indices_g,
-                                                       const int64_t *__restrict__ offsets, int64_t n_bags,
-                                                       int32_t *__restrict__ counts, int64_t *err, int32_t bad_code,
-                                                       int32_t *err_code, bool sysfence) {
-  constexpr int GPW = 32 / G;
-  const int lane = threadIdx.x & 31;
-  const int gl = lane % G;
-  const int gw = lane / G;
-  const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (gw * G));
-  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = (gridDim.x * (int64_t)blockDim.x) >> 5;
-  const int64_t step = nwarps * GPW;
-  int64_t bag = warp * GPW + gw;
-  if (bag >= n_bags) {
-    if (sysfence) __threadfence_system();
-    return;
-  }
-  int s = find_segment(segs, n_segs, bag);
-  int64_t beg, end;
-  bag_bounds(segs, s, bag, offsets, beg, end);
-  const IdxT *indices = seg_indices(segs, s, indices_g);
-  IdxT pidx = (beg + gl < end) ? indices[beg + gl] : IdxT(0);
-  while (bag < n_bags) {
-    const float *__restrict__ tab = segs[s].table;
-    const int64_t rb = segs[s].row_begin, re = segs[s].row_end, ld = segs[s].ld;
-    double acc[NCH][4];
-#pragma unroll
-    for (int k = 0; k < NCH; ++k) acc[k][0] = acc[k][1] = acc[k][2] = acc[k][3] = 0.0;
-    const int64_t nbag = bag + step;
-    const int ns = nbag < n_bags ? find_segment(segs, n_segs, nbag) : s;
-    const IdxT *nindices = seg_indices(segs, ns, indices_g);
-    int64_t nbeg = 0, nend = 0;
-    IdxT nidx = IdxT(0);
-    bool have_next = false;
-    for (int64_t c0 = beg; c0 < end; c0 += G) {
-      const int n = static_cast<int>((end - c0) < G ? (end - c0) : (int64_t)G);
-      const int64_t idx = static_cast<int64_t>(pidx);
-      int64_t my_off = 0;
-      if (gl < n) {
-        if (idx < rb || idx >= re) record_bad(err, err_code, c0 + gl, bad_code);
-        else my_off = (idx - rb) * ld;
-      }
-      for (int r = 0; r < n; r += U) {
-        float4 v[U][NCH];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int64_t off = __shfl_sync(gmask, my_off, (r + u) & (G - 1), G);
-          if (r + u < n) {
-#pragma unroll
-            for (int k = 0; k < NCH; ++k) v[u][k] = ldg_f4(tab + off + (k * G + gl) * 4);
-          }
-        }
-        if (r == 0) {
-          if (c0 + G < end) {
-            pidx = (c0 + G + gl < end) ? indices[c0 + G + gl] : IdxT(0);
-          } else if (nbag < n_bags) {
-            bag_bounds(segs, ns, nbag, offsets, nbeg, nend);
-            nidx = (nbeg + gl < nend) ? nindices[nbeg + gl] : IdxT(0);
-            have_next = true;
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          if (r + u < n) {
-#pragma unroll
-            for (int k = 0; k < NCH; ++k) {
-              acc[k][0] += static_cast<double>(v[u][k].x);
-              acc[k][1] += static_cast<double>(v[u][k].y);
-              acc[k][2] += static_cast<double>(v[u][k].z);
-              acc[k][3] += static_cast<double>(v[u][k].w);
-            }
-          }
-        }
-      }
-    }
-    if (!have_next && nbag < n_bags) {
-      bag_bounds(segs, ns, nbag, offsets, nbeg, nend);
-      nidx = (nbeg + gl < nend) ? nindices[nbeg + gl] : IdxT(0);
-    }
-    emit_bag<NCH, MODE>(segs[s], bag, end - beg, acc, gl, G, counts);
-    bag = nbag;
-    s = ns;
-    indices = nindices;
-    beg = nbeg;
-    end = nend;
-    pidx = nidx;
-  }
-  if (sysfence) __threadfence_system();
-}
-
 }  // namespace fx
