@@ -169,9 +169,12 @@ int fx_dedup(const int32_t *bag_table, const void *indices, int32_t idx_type,
  *      FrequencySketch) ------------------------------------------------------
  * Keys are u64 (table << 40 | row). The handle owns its device memory
  * (cudaMalloc at create / reserve; documented exception to "no allocation").
- * Scalars (fx_cache_scalars order): budget, used, tick, hits, misses, entries,
- * free_top, sketch_live, sketch_tomb, hash_tomb, pending, n_evlog, n_acc,
- * n_ev, n_cand, staged. Calls marked [sync] read scalars back to the host. */
+ * Scalars (fx_cache_scalars order, 18 x int64): budget, used, tick, hits,
+ * misses, entries, free_top, sketch_live, sketch_tomb, hash_tomb, pending,
+ * n_evlog, n_acc, n_ev, n_cand, staged, err, n_ov. err: 1 = an insert or
+ * shrink found nothing left to evict (the reference raises KeyError from
+ * OrderedDict.popitem there), 2 = pooled-key fingerprint collision.
+ * Calls marked [sync] read scalars back to the host. */
 typedef struct fx_cache fx_cache;
 typedef struct fx_table_dir {   /* where rows of `table` in [row_begin,row_end) live */
   const float *base;
@@ -188,7 +191,7 @@ int fx_cache_create(fx_cache **out, int64_t slot_capacity, int32_t max_dim, int3
 int fx_cache_destroy(fx_cache *c);
 int fx_cache_set_tables(fx_cache *c, const fx_table_dir *dir, int32_t n_dir, const int32_t *table_bytes,
                         int32_t n_tables);                                     /* host arrays */
-int fx_cache_scalars(fx_cache *c, int64_t *out16, void *stream);               /* [sync] */
+int fx_cache_scalars(fx_cache *c, int64_t *out18, void *stream);               /* [sync] */
 int fx_cache_reserve_sketch(fx_cache *c, int64_t new_keys, void *stream);      /* [sync] */
 int fx_cache_reserve_slots(fx_cache *c, int64_t slots, void *stream);          /* [sync] */
 /* get() per unique key (cache.py:189-202): hit -> last_tick = tick0 +
@@ -227,6 +230,35 @@ int fx_cache_last_evicted(fx_cache *c, uint64_t *out, int64_t cap, int64_t *n_ou
 /* device array of row pointers for the pending keys (NULL entry -> table dir),
  * consumed by the next fx_cache_apply_pending (host-fetched admissions) */
 int fx_cache_set_pending_rows(fx_cache *c, const float *const *rows, int64_t n);
+/* tick += n (the batch's probes when no row probe call advances it) */
+int fx_cache_advance_tick(fx_cache *c, int64_t n, void *stream);
+
+/* ---- pooled-result keyspace (cache.py:204-223; ranker.py:243-249,412-414) ----
+ * Key of a bag = ("pooled", table, op, sorted(indices)), represented by two
+ * 64-bit multiset fingerprints (fx_bag_fingerprint):
+ *   sA = sum mix64(x ^ 0xA0761D6478BD642F), sB = sum mix64(x ^ 0xE7037ED1A0B428DB)  (mod 2^64)
+ *   A = mix64(sA ^ mix64(mix64(table ^ SALT_A) + op) ^ (L * SALT_B)) | 2^63
+ *   B = mix64(sB ^ mix64(mix64(table ^ SALT_B) + op) ^ (L * SALT_A))
+ * A indexes the shared LRU / budget (disjoint from row keys), B is verified on
+ * every match (mismatch -> scalars.err = 2). */
+int fx_bag_fingerprint(const int32_t *bag_table, const int32_t *bag_op, const void *indices, int32_t idx_type,
+                       const int64_t *offsets, int64_t n_bags, uint64_t *key_a, uint64_t *key_b, void *stream);
+/* slot of each pooled key (-1 absent); no state change */
+int fx_cache_pooled_find(fx_cache *c, const uint64_t *key_a, const uint64_t *key_b, int64_t n, int32_t *slot_out,
+                         void *stream);
+/* pooled_get hits: last_tick = tick + pos[i] + 1 (max per slot), hits += 1;
+ * the tick is advanced by the caller (fx_cache_probe nnz / advance_tick) */
+int fx_cache_pooled_touch(fx_cache *c, const int32_t *slot, const int64_t *pos, int64_t n, void *stream);
+/* out[i] = cached row of slot[i] (rows with slot -1 untouched); optional
+ * size_out[i] = the entry's bytes (0 for slot -1) */
+int fx_cache_read_slots(fx_cache *c, const int32_t *slot, int64_t n, float *out, int32_t out_ld, int32_t *size_out,
+                        void *stream);
+/* ordered pooled_put of n vectors src_rows[j] (device array of device
+ * pointers), sizes[j] bytes (or uniform_size when sizes == NULL): evict LRU to
+ * fit, fresh tick, insert at MRU; a resident key is replaced in place
+ * (position kept, used += size again: the reference's _insert quirk).  [sync] */
+int fx_cache_pooled_put(fx_cache *c, const uint64_t *key_a, const uint64_t *key_b, int64_t n, const int32_t *sizes,
+                        int32_t uniform_size, const float *const *src_rows, void *stream);
 
 /* ---- peer memory (NVLink P2P over CUDA IPC) and the cross-GPU barrier ----
  * The fused exchange: an owner's K4 reads a requester's CSR batch through an

@@ -5,13 +5,13 @@ Reference paths are relative to /root/reference/pkg/src/embserve.
 
 from __future__ import annotations
 
-import heapq
+from collections import OrderedDict
 from dataclasses import dataclass, field
 
 import numpy as np
 
 __all__ = [
-    "mix64", "table_base", "rows_of", "table_block",
+    "mix64", "table_base", "rows_of", "table_block", "pooled_fingerprint",
     "seq_sum_f64", "pool_flat", "combine_partials", "plan_modes",
     "Placement", "resolve_many", "group_feature",
     "ZipfSampler", "dedup_keys", "make_keys",
@@ -39,6 +39,29 @@ def mix64(x) -> np.ndarray:
         x = (x ^ (x >> _U64(30))) * _M1
         x = (x ^ (x >> _U64(27))) * _M2
         return x ^ (x >> _U64(31))
+
+
+_SALT_A = _U64(0xA0761D6478BD642F)
+_SALT_B = _U64(0xE7037ED1A0B428DB)
+_OPC = {"sum": 0, "mean": 1}
+
+
+def pooled_fingerprint(table_id: int, op: str, indices):
+    """The B200 cache's identifier (A, B) for the reference's pooled key
+    ("pooled", table, op, sorted(indices)) (cache.py:209), restated from
+    include/flexemb.h (fx_bag_fingerprint): order-independent sums of
+    mix64(x ^ salt), finalised with table, op and L. Used by tests to map the
+    reference's tuple keys onto device keys."""
+    x = np.asarray(list(indices), dtype=np.int64).view(_U64)
+    with np.errstate(over="ignore"):
+        sa = _U64(int(mix64(x ^ _SALT_A).sum(dtype=_U64)) if x.size else 0)
+        sb = _U64(int(mix64(x ^ _SALT_B).sum(dtype=_U64)) if x.size else 0)
+        t = _U64(table_id)
+        opc = _U64(_OPC[op])
+        L = _U64(x.size)
+        a = mix64(sa ^ mix64(mix64(t ^ _SALT_A) + opc) ^ (L * _SALT_B)) | _U64(1 << 63)
+        b = mix64(sb ^ mix64(mix64(t ^ _SALT_B) + opc) ^ (L * _SALT_A))
+    return int(a), int(b)
 
 
 def table_base(seed: int, table_id: int) -> np.uint64:
@@ -255,38 +278,32 @@ class CachePolicyO:
 class CacheOracle:
     """Restatement of AdaptiveCache + FrequencySketch (cache.py:114-352).
 
-    LRU order is kept as ascending last_tick (every hit/insert takes a fresh
-    tick, cache.py:193-201,262-263), via a lazy min-heap instead of an
-    ordered dict. Keys are (table, row) tuples."""
+    Entries live in an insertion-ordered dict in LRU order, like the
+    reference's OrderedDict: hits move to the end (cache.py:199-201),
+    inserts append (cache.py:262-263), eviction pops the front. Row keys are
+    (table, row) tuples; pooled-result keys (cache.py:204-223) are
+    ("pooled", table, op, tuple(sorted(indices))). entry = [last_tick, size,
+    hits, vector-or-None]."""
 
-    def __init__(self, budget_bytes: int, admission="sketch", decay=0.5, prune=0.25):
+    def __init__(self, budget_bytes: int, admission="sketch", decay=0.5, prune=0.25, pooled=False):
         self.budget = int(budget_bytes)
         self.admission = admission
         self.decay, self.prune = decay, prune
+        self.pooled = pooled
         self.used = 0
         self.tick = 0
         self.hits = 0
         self.misses = 0
-        self.entries: dict = {}     # key -> [last_tick, size, hits]
-        self._heap: list = []       # (last_tick, key) lazy
+        self.entries: OrderedDict = OrderedDict()
         self.sketch: dict = {}
         self.pending: list = []     # (key, size)
         self.evictions: list = []
 
-    # -- order
-    def _push(self, key):
-        heapq.heappush(self._heap, (self.entries[key][0], key))
-
     def _victim(self):
-        while True:
-            t, k = self._heap[0]
-            e = self.entries.get(k)
-            if e is not None and e[0] == t:
-                return k
-            heapq.heappop(self._heap)
+        return next(iter(self.entries))
 
     def lru_keys(self):
-        return [k for k, _ in sorted(self.entries.items(), key=lambda kv: kv[1][0])]
+        return list(self.entries)
 
     # -- probe (cache.py:189-202)
     def get(self, key) -> bool:
@@ -299,8 +316,26 @@ class CacheOracle:
         self.hits += 1
         e[2] += 1
         e[0] = self.tick
-        self._push(key)
+        self.entries.move_to_end(key)
         return True
+
+    # -- pooled-result keyspace (cache.py:204-223)
+    def pooled_get(self, key):
+        if not self.pooled:
+            return None
+        self.tick += 1
+        e = self.entries.get(key)
+        if e is None:
+            return None
+        e[2] += 1
+        e[0] = self.tick
+        self.entries.move_to_end(key)
+        return e[3]
+
+    def pooled_put(self, key, vector) -> None:
+        if not self.pooled:
+            return
+        self._insert(key, int(np.asarray(vector).size) * 4, vector)
 
     # -- admission (cache.py:237-280)
     def offer(self, key, size) -> bool:
@@ -314,24 +349,25 @@ class CacheOracle:
                 return False
         return self._insert(key, size)
 
-    def _insert(self, key, size) -> bool:
+    def _insert(self, key, size, vector=None) -> bool:
+        """cache.py:256-268. No presence check: re-inserting a resident key
+        keeps its position and adds its size again (only pooled_put can)."""
         if size > self.budget:
             return False
         while self.used + size > self.budget:
-            self._evict_one()
+            self._evict_one()       # KeyError on an empty dict, like the reference
         self.tick += 1
-        self.entries[key] = [self.tick, size, 0]
-        self._push(key)
+        self.entries[key] = [self.tick, size, 0, vector]
         self.used += size
-        assert self.used <= self.budget
+        if self.used > self.budget:
+            raise AssertionError(f"cache used {self.used} exceeds budget {self.budget}")
         return True
 
     def _evict_one(self):
-        v = self._victim()
-        heapq.heappop(self._heap)
-        self.used -= self.entries.pop(v)[1]
-        self.evictions.append(v)
-        return v
+        k, e = self.entries.popitem(last=False)
+        self.used -= e[1]
+        self.evictions.append(k)
+        return k
 
     # -- resize / staging (cache.py:290-352)
     def resize(self, new_budget, row_bytes_of=None, fetch=False):
@@ -355,6 +391,8 @@ class CacheOracle:
             return staged
         pend = {k for k, _ in self.pending}
         for key in self.hottest(limit if limit is not None else len(self.sketch)):
+            if not (isinstance(key, tuple) and len(key) == 2):
+                continue
             if key in self.entries or key in pend:
                 continue
             size = row_bytes_of(key[0])
@@ -511,10 +549,18 @@ class PipelineOracle:
                 c.resize(m.target(bb.n_lookups))
         order = bb.sm_order()
         hitmask = {}
+        pooled_hit = {}
         hits = misses = 0
         for b in order:
             t = int(bb.bag_table[b])
             hm = np.zeros(bb.offsets[b + 1] - bb.offsets[b], bool)
+            if c is not None and c.pooled:  # ranker.py:238-245: pooled probe first
+                v = c.pooled_get(("pooled", t, bb.bag_op[b], tuple(sorted(int(i) for i in bb.bag_indices(b)))))
+                if v is not None:
+                    pooled_hit[int(b)] = v
+                    hitmask[int(b)] = np.ones_like(hm)
+                    hits += hm.size
+                    continue
             if c is not None:
                 for k, r in enumerate(bb.bag_indices(b)):
                     hm[k] = c.get((t, int(r)))
@@ -531,6 +577,10 @@ class PipelineOracle:
             t = int(bb.bag_table[b])
             ix = bb.bag_indices(b)
             hm = hitmask[b]
+            if b in pooled_hit:  # ranker.py:403-404
+                vectors[b] = pooled_hit[b]
+                counters[b] = (int(hm.size), 0, 0, 0)
+                continue
             miss_pos = np.nonzero(~hm)[0]
             partials, raw = [], {}
             for p in np.nonzero(hm)[0]:
@@ -554,6 +604,8 @@ class PipelineOracle:
                 if not hm[p]:
                     offers.setdefault((t, int(ix[p])), None)
             vectors[b] = combine_partials(partials, [raw[p] for p in sorted(raw)], bb.bag_op[b])
+            if c is not None and c.pooled:  # ranker.py:412-414
+                c.pooled_put(("pooled", t, bb.bag_op[b], tuple(sorted(int(i) for i in ix))), vectors[b])
             counters[b] = tuple(cg)
             pd_groups += cg[1]
             pd_rows += cg[2]
@@ -574,5 +626,5 @@ class PipelineOracle:
                 c.age()
         self.metrics.append(dict(batch_id=bb.batch_id, size=bb.n_lookups, hits=hits, misses=misses,
                                  pushdown_groups=pd_groups, pushdown_rows=pd_rows, raw_rows=raw_rows,
-                                 load_level=level, offers=list(offers)))
+                                 load_level=level, offers=list(offers), pooled_hits=sorted(pooled_hit)))
         return vectors, counters, hitmask

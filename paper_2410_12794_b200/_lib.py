@@ -109,7 +109,10 @@ _SIGS = {
         "fx_cache_reserve_slots", "fx_cache_probe", "fx_cache_offer", "fx_cache_set_budget", "fx_cache_stage",
         "fx_cache_apply_pending", "fx_cache_age", "fx_cache_lookup", "fx_cache_sketch_estimate",
         "fx_cache_sketch_bump", "fx_cache_sketch_ranked", "fx_cache_lru", "fx_cache_eviction_log",
-        "fx_cache_pending", "fx_cache_last_evicted", "fx_cache_set_pending_rows", "fx_cache_set_parallel")},
+        "fx_cache_pending", "fx_cache_last_evicted", "fx_cache_set_pending_rows", "fx_cache_set_parallel",
+        "fx_cache_advance_tick", "fx_cache_pooled_find", "fx_cache_pooled_touch", "fx_cache_read_slots",
+        "fx_cache_pooled_put")},
+    "fx_bag_fingerprint": ([_P, _P, _P, _I32, _P, _I64, _P, _P, _P], ctypes.c_int),
 }
 
 EXPORTED = []

@@ -134,16 +134,38 @@ class ResizeReport:
 
 
 _SC = ("budget", "used", "tick", "hits", "misses", "entries", "free_top", "sketch_live", "sketch_tomb",
-       "hash_tomb", "pending", "n_evlog", "n_acc", "n_ev", "n_cand", "staged")
+       "hash_tomb", "pending", "n_evlog", "n_acc", "n_ev", "n_cand", "staged", "err", "n_ov")
+
+POOLED_BIT = 1 << 63
 
 
 def encode_key(table_id: int, index: int) -> int:
     return (int(table_id) << ROW_BITS) | int(index)
 
 
-def decode_key(k: int):
+def decode_key(k: int, pooled_names: dict | None = None):
+    """Row key -> (table, row); pooled fingerprint -> the reference's
+    ("pooled", table, op, sorted indices) key when known, else ("pooled", A)."""
     k = int(k) & ((1 << 64) - 1)
+    if k & POOLED_BIT:
+        if pooled_names is not None and k in pooled_names:
+            return pooled_names[k]
+        return ("pooled", k)
     return (k >> ROW_BITS, k & ((1 << ROW_BITS) - 1))
+
+
+def bag_fingerprints(bag_table: torch.Tensor, bag_op: torch.Tensor, indices: torch.Tensor, offsets: torch.Tensor):
+    """Pooled-result keys (A, B) of every CSR bag (fx_bag_fingerprint)."""
+    n = int(offsets.numel()) - 1
+    dev = offsets.device
+    ka = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+    kb = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+    if n > 0:
+        idx = indices if indices.numel() else torch.zeros(1, dtype=torch.int64, device=dev)
+        _lib.check(_lib.lib.fx_bag_fingerprint(bag_table.data_ptr(), bag_op.data_ptr(), idx.data_ptr(),
+                                               _lib.idx_type_of(idx), offsets.data_ptr(), n, ka.data_ptr(),
+                                               kb.data_ptr(), _lib.stream_ptr()), "bag fingerprint")
+    return ka[:n], kb[:n]
 
 
 def _u64(keys) -> torch.Tensor:
@@ -177,6 +199,11 @@ def _sig():
         "fx_cache_last_evicted": [P, P, I64, ctypes.POINTER(I64), P],
         "fx_cache_set_pending_rows": [P, P, I64],
         "fx_cache_set_parallel": [P, I32],
+        "fx_cache_advance_tick": [P, I64, P],
+        "fx_cache_pooled_find": [P, P, P, I64, P, P],
+        "fx_cache_pooled_touch": [P, P, P, I64, P],
+        "fx_cache_read_slots": [P, P, I64, P, I32, P, P],
+        "fx_cache_pooled_put": [P, P, P, I64, P, I32, P, P],
     }
     for n, a in sigs.items():
         f = getattr(L, n)
@@ -252,13 +279,11 @@ class AdaptiveCache:
                  slot_capacity: int | None = None, sketch_capacity: int = 4096, device=None):
         if admission not in ("sketch", "always"):
             raise ConfigError(f"unknown admission policy '{admission}'")
-        if pooled_results:
-            raise ConfigError("pooled-result cache keyspace is not implemented in the B200 build yet "
-                              "(SURVEY §8(f) rank 2)")
         self._L = _sig()
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.admission = admission
-        self.pooled_results_enabled = False
+        self.pooled_results_enabled = bool(pooled_results)
+        self._pooled_names: dict = {}   # fingerprint A -> reference key (API puts)
         self.record_evictions = record_evictions
         self.max_dim = max_dim
         self._row_bytes: dict = {}      # table -> row bytes (device tbytes)
@@ -295,8 +320,9 @@ class AdaptiveCache:
     def _reserve_sketch(self, n_new: int):
         _lib.check(self._L.fx_cache_reserve_sketch(self._h, int(n_new), _lib.stream_ptr()), "reserve sketch")
 
-    def _reserve_slots_for(self, budget: int):
-        sizes = [b for b in self._row_bytes.values() if b > 0] or [4]
+    def _reserve_slots_for(self, budget: int, extra_size: int | None = None):
+        sizes = [b for b in self._row_bytes.values() if b > 0] + ([int(extra_size)] if extra_size else [])
+        sizes = sizes or [4]
         need = budget // min(sizes) + 1
         if need > self._slots:
             new = max(need, 2 * self._slots)
@@ -397,7 +423,7 @@ class AdaptiveCache:
         _lib.check(self._L.fx_cache_lru(self._h, keys.data_ptr(), ticks.data_ptr(), hits.data_ptr(), cap,
                                         ctypes.byref(n), _lib.stream_ptr()), "cache lru")
         k = keys[:n.value].cpu().numpy().view(np.uint64)
-        return [(decode_key(int(a)), int(t), int(h)) for a, t, h in
+        return [(decode_key(int(a), self._pooled_names), int(t), int(h)) for a, t, h in
                 zip(k, ticks[:n.value].cpu().numpy(), hits[:n.value].cpu().numpy())]
 
     def lru_keys(self) -> list:
@@ -415,7 +441,7 @@ class AdaptiveCache:
                    "eviction log")
         if n.value > cap:
             raise InvariantError("eviction log overflowed its device buffer")
-        return [decode_key(int(a)) for a in out[:n.value].cpu().numpy().view(np.uint64)]
+        return [decode_key(int(a), self._pooled_names) for a in out[:n.value].cpu().numpy().view(np.uint64)]
 
     def _last_evicted(self):
         s = self._scalars()
@@ -424,7 +450,7 @@ class AdaptiveCache:
         n = ctypes.c_int64(0)
         _lib.check(self._L.fx_cache_last_evicted(self._h, out.data_ptr(), cap, ctypes.byref(n), _lib.stream_ptr()),
                    "last evicted")
-        return [decode_key(int(a)) for a in out[:n.value].cpu().numpy().view(np.uint64)]
+        return [decode_key(int(a), self._pooled_names) for a in out[:n.value].cpu().numpy().view(np.uint64)]
 
     # -- batched device API (used by the engine) ------------------------------------------
 
@@ -461,11 +487,96 @@ class AdaptiveCache:
         dim = self._row_bytes.get(table_id, 4 * self.max_dim) // 4
         return rows[0, :dim].cpu().numpy()
 
+    # -- pooled-result keyspace (cache.py:204-223) --------------------------------------
+
+    def check_state(self) -> None:
+        """[sync] Raise what the reference raises when a cache operation hit
+        one of its failure paths (recorded device-side in scalars.err)."""
+        err = self._scalars()["err"]
+        if err == 1:
+            raise KeyError("popitem(): dictionary is empty (cache.py:270: nothing left to evict; "
+                           "leaked pooled bytes exceed the budget)")
+        if err == 2:
+            raise InvariantError("pooled-result key fingerprint collision (different index multisets share A)")
+
+    def _pooled_key(self, table_id: int, op, indices):
+        from .pooling import op_code
+        dev = self.device
+        idx = torch.as_tensor(np.asarray(list(indices), dtype=np.int64)).to(dev)
+        offs = torch.tensor([0, idx.numel()], dtype=torch.int64, device=dev)
+        bt = torch.tensor([int(table_id)], dtype=torch.int32, device=dev)
+        bo = torch.tensor([op_code(op)], dtype=torch.int32, device=dev)
+        ka, kb = bag_fingerprints(bt, bo, idx, offs)
+        opv = op.value if hasattr(op, "value") else str(op)
+        name = ("pooled", int(table_id), opv, tuple(sorted(int(i) for i in indices)))
+        return ka, kb, name
+
+    def pooled_find(self, key_a: torch.Tensor, key_b: torch.Tensor, slot_out: torch.Tensor) -> None:
+        n = int(key_a.numel())
+        if n:
+            _lib.check(self._L.fx_cache_pooled_find(self._h, key_a.data_ptr(), key_b.data_ptr(), n,
+                                                    slot_out.data_ptr(), _lib.stream_ptr()), "pooled find")
+
+    def pooled_touch(self, slot: torch.Tensor, pos: torch.Tensor) -> None:
+        n = int(slot.numel())
+        if n:
+            _lib.check(self._L.fx_cache_pooled_touch(self._h, slot.data_ptr(), pos.data_ptr(), n,
+                                                     _lib.stream_ptr()), "pooled touch")
+
+    def advance_tick(self, n: int) -> None:
+        if n:
+            _lib.check(self._L.fx_cache_advance_tick(self._h, int(n), _lib.stream_ptr()), "advance tick")
+
+    def read_slots(self, slot: torch.Tensor, out: torch.Tensor, sizes: torch.Tensor | None = None) -> None:
+        n = int(slot.numel())
+        if n:
+            _lib.check(self._L.fx_cache_read_slots(self._h, slot.data_ptr(), n, out.data_ptr(), out.stride(0),
+                                                   _lib.ptr(sizes), _lib.stream_ptr()), "read slots")
+
+    def pooled_put_many(self, key_a: torch.Tensor, key_b: torch.Tensor, rows: torch.Tensor,
+                        nbytes: int, sel: torch.Tensor | None = None) -> None:
+        """Ordered pooled_put of rows[i] (or rows[sel[i]]) under keys (A, B)[i]."""
+        n = int(key_a.numel())
+        if n == 0:
+            return
+        self._reserve_slots_for(self.budget_bytes, int(nbytes))
+        base = rows.data_ptr()
+        stride = rows.stride(0) * rows.element_size()
+        rid = sel if sel is not None else torch.arange(n, device=self.device)
+        ptrs = (rid.to(torch.int64) * stride + base).contiguous()
+        _lib.check(self._L.fx_cache_pooled_put(self._h, key_a.data_ptr(), key_b.data_ptr(), n, None, int(nbytes),
+                                               ptrs.data_ptr(), _lib.stream_ptr()), "pooled put")
+
     def pooled_get(self, table_id: int, op, indices):
-        return None  # keyspace disabled (cache.py:207-208)
+        """Pooled-result probe (cache.py:204-217): disabled -> None without a
+        tick; otherwise tick += 1, hit refreshes recency and returns the vector."""
+        if not self.pooled_results_enabled:
+            return None
+        ka, kb, _ = self._pooled_key(table_id, op, indices)
+        slot = torch.empty(1, dtype=torch.int32, device=self.device)
+        self.pooled_find(ka, kb, slot)
+        self.pooled_touch(slot, torch.zeros(1, dtype=torch.int64, device=self.device))
+        self.advance_tick(1)
+        self.check_state()
+        if int(slot.item()) < 0:
+            return None
+        out = torch.zeros((1, self.max_dim), dtype=torch.float32, device=self.device)
+        size = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.read_slots(slot, out, size)
+        return out[0, :int(size.item()) // 4].cpu().numpy()
 
     def pooled_put(self, table_id: int, op, indices, vector) -> None:
-        return None
+        """cache.py:219-223: unconditional insert of a pooled vector."""
+        if not self.pooled_results_enabled:
+            return
+        vec = vector if isinstance(vector, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(vector))
+        vec = vec.to(device=self.device, dtype=torch.float32).reshape(1, -1).contiguous()
+        ka, kb, name = self._pooled_key(table_id, op, indices)
+        self._pooled_names[int(ka.item()) & ((1 << 64) - 1)] = name
+        if vec.numel() > self.max_dim:
+            raise ConfigError(f"pooled vector of {vec.numel()} floats exceeds the cache's max_dim {self.max_dim}")
+        self.pooled_put_many(ka, kb, vec, vec.numel() * 4)
+        self.check_state()
 
     def offer(self, table_id: int, index: int, vector) -> bool:
         """Admission attempt for a raw-fetched row (cache.py:237-254)."""

@@ -41,6 +41,9 @@ struct Scalars {
   long long budget, used, tick, hits, misses, entries;
   long long free_top, sketch_live, sketch_tomb, hash_tomb, pending;
   long long n_evlog, n_acc, n_ev, n_cand, staged;
+  long long err;   // 1: eviction queue exhausted (the reference's popitem on an empty
+                   //    OrderedDict), 2: pooled-key fingerprint collision
+  long long n_ov;  // in-place pooled re-puts recorded by the last put call
 };
 
 struct CacheView {
@@ -49,6 +52,7 @@ struct CacheView {
   int32_t *hslot;
   int64_t hcap;
   uint64_t *skey;
+  uint64_t *skey2;  // second fingerprint of pooled-result keys (0 for row keys)
   long long *stick;
   int32_t *ssize;
   int32_t *shits;
@@ -180,6 +184,7 @@ __global__ void k_cache_init(CacheView c) {
   for (int64_t i = i0; i < c.scap; i += stride) {
     c.stick[i] = kFree;
     c.skey[i] = kEmpty;
+    c.skey2[i] = 0;
     c.free_stack[i] = static_cast<int32_t>(c.scap - 1 - i);  // pops give 0, 1, 2, ...
   }
 }
@@ -284,7 +289,9 @@ __global__ void k_offer_seq(CacheView c, const uint64_t *keys, int64_t n, int32_
     c.free_stack[ftop++] = s;
     --entries;
   };
+  long long err = 0;
   while (used > budget && entries > 0) evict_head();  // resize shrink (cache.py:270-274)
+  if (used > budget) err = 1;  // only leaked pooled bytes left: the reference's popitem raises
   for (int64_t j = 0; j < n; ++j) {
     const uint64_t key = keys[j];
     const int32_t size = w.size_cand[j];
@@ -304,7 +311,12 @@ __global__ void k_offer_seq(CacheView c, const uint64_t *keys, int64_t n, int32_
         continue;
       }
     }
-    while (used + size > budget) evict_head();
+    while (used + size > budget && entries > 0) evict_head();
+    if (used + size > budget) {  // queue exhausted (leaked pooled bytes): reference KeyError
+      err = 1;
+      if (accepted) accepted[j] = 0;
+      break;
+    }
     ++tick;
     const int32_t s = c.free_stack[--ftop];
     c.skey[s] = key;
@@ -325,6 +337,7 @@ __global__ void k_offer_seq(CacheView c, const uint64_t *keys, int64_t n, int32_
   sc->n_acc = n_acc;
   sc->n_ev = n_ev;
   sc->n_evlog = n_log;
+  if (err) sc->err = err;
 }
 
 
@@ -365,7 +378,14 @@ __global__ void __launch_bounds__(1024) k_offer_par(CacheView c, const uint64_t 
   Scalars *sc = c.sc;
   const long long m = pw.m_dev ? *pw.m_dev : pw.m;
   const long long e0 = sc->entries;
-  const long long cap = sc->budget / S;
+  // bytes leaked by in-place pooled re-puts (cache.py:256-263 adds the size
+  // again without a new entry) occupy budget units that no eviction frees
+  const long long ph = sc->used / S > e0 ? sc->used / S - e0 : 0;
+  long long cap = sc->budget / S - ph;
+  if (cap < 0) {
+    cap = 0;
+    if (tid == 0) sc->err = 1;
+  }
   if (tid == 0) {
     st[0] = 0; st[1] = 0; st[2] = 0; st[3] = 0;
     st[4] = sc->tick; st[5] = sc->free_top; st[6] = sc->n_evlog; st[7] = e0;
@@ -393,7 +413,7 @@ __global__ void __launch_bounds__(1024) k_offer_par(CacheView c, const uint64_t 
     for (long long t = tid; t < m; t += blockDim.x) if (accepted) accepted[pw.cand[t]] = 0;
     __syncthreads();
     if (tid == 0) {
-      sc->entries = st[7]; sc->used = st[7] * S; sc->free_top = st[5];
+      sc->entries = st[7]; sc->used = (st[7] + ph) * S; sc->free_top = st[5];
       sc->n_acc = 0; sc->n_ev = st[3]; sc->n_evlog = st[6];
     }
     return;
@@ -419,6 +439,7 @@ __global__ void __launch_bounds__(1024) k_offer_par(CacheView c, const uint64_t 
     }
     __syncthreads();
   }
+  if (cap == 0 && st[0] < m && tid == 0) sc->err = 1;  // nothing left to evict: reference KeyError
   // phase 2: full cache
   const bool always = (mode != 0) || (c.admission != 0);
   if (always) {
@@ -576,7 +597,7 @@ __global__ void __launch_bounds__(1024) k_offer_par(CacheView c, const uint64_t 
     sc->tick = st[4];
     sc->free_top = st[5];
     sc->entries = st[7];
-    sc->used = st[7] * S;
+    sc->used = (st[7] + ph) * S;
     sc->n_acc = st[2];
     sc->n_ev = st[3];
     sc->n_evlog = st[6];
@@ -622,6 +643,194 @@ __global__ void __launch_bounds__(256) k_install(CacheView c, OfferWS w, const u
     int32_t dim = c.ssize[s] / 4;
     const float *src = src_rows ? src_rows[j] : nullptr;
     if (!src) src = dir_row(c, key, &dim);
+    float *dst = c.rows + static_cast<int64_t>(s) * c.row_ld;
+    if (src)
+      for (int i = lane; i < dim; i += 32) dst[i] = src[i];
+  }
+}
+
+// ---------------------------------------------------------------- pooled-result keyspace
+// (cache.py:204-223, ranker.py:243-249,412-414). Keys are the bag
+// fingerprints of fx_bag_fingerprint: A (top bit set) indexes the shared
+// hash/LRU/budget, B is verified per slot.
+
+__global__ void k_pooled_find(CacheView c, const uint64_t *key_a, const uint64_t *key_b, int64_t n,
+                              int32_t *slot_out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t s = h_find(c, key_a[i]);
+    if (s >= 0 && c.skey2[s] != key_b[i]) {  // same A, different multiset
+      atomicExch(reinterpret_cast<unsigned long long *>(&c.sc->err), 2ull);
+      s = -1;
+    }
+    slot_out[i] = s;
+  }
+}
+
+// pooled_get hits: last_tick = tick0 + pos + 1 (latest probe of the entry in
+// this batch), entry.hits += 1 per probe; the tick itself advances with the
+// batch's row probes (fx_cache_probe / fx_cache_advance_tick).
+__global__ void k_pooled_touch(CacheView c, const int32_t *slot, const int64_t *pos, int64_t n) {
+  const long long tick0 = c.sc->tick;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t s = slot[i];
+    if (s < 0) continue;
+    atomicMax(&c.stick[s], tick0 + pos[i] + 1);
+    atomicAdd(&c.shits[s], 1);
+  }
+}
+
+// one warp per item: copy the row of slot[i] (if >= 0) into out[i]
+__global__ void k_read_slots(CacheView c, const int32_t *slot, int64_t n, float *out, int32_t out_ld,
+                             int32_t *size_out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp; i < n; i += nw) {
+    const int32_t s = slot[i];
+    if (size_out && lane == 0) size_out[i] = s < 0 ? 0 : c.ssize[s];
+    if (s < 0) continue;
+    const int32_t dim = c.ssize[s] / 4;
+    const float *src = c.rows + static_cast<int64_t>(s) * c.row_ld;
+    for (int k = lane; k < dim && k < out_ld; k += 32) out[i * out_ld + k] = src[k];
+  }
+}
+
+struct PutWS {
+  int32_t *present_slot;  // slot of key j at call start (-1 absent)
+  int32_t *prev;          // previous put of the same key in this call (-1 none)
+  int32_t *slot_of;       // slot holding key j right after put j (-1 skipped)
+  int32_t *iota;
+  int32_t *perm;
+  uint64_t *keys_sorted;
+  int32_t *ov_slot;       // in-place re-puts (slot, j)
+  int32_t *ov_j;
+  int32_t *writer;        // [slots] last put that wrote the slot (valid for recorded slots)
+};
+
+__global__ void k_put_prep(CacheView c, const uint64_t *key_a, const uint64_t *key_b, int64_t n,
+                           const int32_t *sizes, int32_t uniform_size, OfferWS w, PutWS pw) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    int32_t s = h_find(c, key_a[j]);
+    if (s >= 0 && c.skey2[s] != key_b[j]) {
+      atomicExch(reinterpret_cast<unsigned long long *>(&c.sc->err), 2ull);
+      s = -1;
+    }
+    pw.present_slot[j] = s;
+    w.size_cand[j] = sizes ? sizes[j] : uniform_size;
+    pw.iota[j] = static_cast<int32_t>(j);
+  }
+}
+
+// after a stable sort of (key_a, j): prev[j] = the previous put of the same key
+__global__ void k_put_prev(const uint64_t *keys_sorted, const int32_t *perm, int64_t n, const uint64_t *key_b,
+                           PutWS pw, Scalars *sc) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t j = perm[p];
+    int32_t pv = -1;
+    if (p > 0 && keys_sorted[p - 1] == keys_sorted[p]) {
+      pv = perm[p - 1];
+      if (key_b[pv] != key_b[j]) atomicExch(reinterpret_cast<unsigned long long *>(&sc->err), 2ull);
+    }
+    pw.prev[j] = pv;
+  }
+}
+
+// Ordered pooled_put loop (cache.py:219-223 -> _insert, cache.py:256-268):
+// no admission test; evict LRU until the size fits, take a tick, insert at
+// MRU. A key that is still resident (put twice in one batch, or re-put
+// through the API) is replaced IN PLACE by the reference's OrderedDict
+// assignment: its LRU position is kept, hits restart at 0 and used_bytes
+// grows by the size again without a new entry (the bytes are never freed).
+__global__ void k_put_seq(CacheView c, const uint64_t *key_a, const uint64_t *key_b, int64_t n, OfferWS w,
+                          PutWS pw, int32_t record) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  Scalars *sc = c.sc;
+  long long used = sc->used, budget = sc->budget, tick = sc->tick, entries = sc->entries, ftop = sc->free_top;
+  const long long e0 = entries;
+  long long h = 0, n_acc = 0, n_ov = 0, n_ev = 0, n_log = sc->n_evlog, err = 0;
+  auto head_slot = [&](long long q) -> int32_t { return q < e0 ? w.lru_slot[q] : w.acc_slot[q - e0]; };
+  for (int64_t j = 0; j < n; ++j) {
+    const uint64_t key = key_a[j];
+    const int32_t size = w.size_cand[j];
+    if (size < 0 || size > budget) {  // _insert: size > budget -> False, no tick
+      pw.slot_of[j] = -1;
+      continue;
+    }
+    const int32_t pv = pw.prev[j];
+    const int32_t live = pv >= 0 ? pw.slot_of[pv] : pw.present_slot[j];
+    while (used + size > budget && h < e0 + n_acc) {
+      const int32_t s = head_slot(h);
+      ++h;
+      used -= c.ssize[s];
+      const uint64_t k = c.skey[s];
+      w.ev_keys[n_ev++] = k;
+      if (record && n_log < c.evlog_cap) c.evlog[n_log] = k;
+      if (record) ++n_log;
+      c.stick[s] = kFree;
+      c.skey[s] = kEmpty;
+      c.free_stack[ftop++] = s;
+      --entries;
+    }
+    if (used + size > budget) {  // queue exhausted: the reference's popitem raises KeyError
+      err = 1;
+      break;
+    }
+    ++tick;
+    if (live >= 0 && c.skey[live] == key) {  // still resident: replace in place
+      c.shits[live] = 0;
+      c.ssize[live] = size;
+      pw.writer[live] = static_cast<int32_t>(j);
+      pw.ov_slot[n_ov] = live;
+      pw.ov_j[n_ov] = static_cast<int32_t>(j);
+      ++n_ov;
+      used += size;
+      pw.slot_of[j] = live;
+      continue;
+    }
+    const int32_t s = c.free_stack[--ftop];
+    c.skey[s] = key;
+    c.skey2[s] = key_b[j];
+    c.stick[s] = tick;
+    c.ssize[s] = size;
+    c.shits[s] = 0;
+    pw.writer[s] = static_cast<int32_t>(j);
+    w.acc_slot[n_acc] = s;
+    w.acc_j[n_acc] = static_cast<int32_t>(j);
+    ++n_acc;
+    used += size;
+    ++entries;
+    pw.slot_of[j] = s;
+  }
+  sc->used = used;
+  sc->tick = tick;
+  sc->entries = entries;
+  sc->free_top = ftop;
+  sc->n_acc = n_acc;
+  sc->n_ov = n_ov;
+  sc->n_ev = n_ev;
+  sc->n_evlog = n_log;
+  if (err) sc->err = err;
+}
+
+// one warp per recorded put (fresh inserts, then in-place re-puts): index it
+// and copy its vector, unless evicted again or overwritten by a later put
+__global__ void __launch_bounds__(256) k_install_put(CacheView c, OfferWS w, PutWS pw, const uint64_t *key_a,
+                                                     const uint64_t *key_b, const float *const *src_rows) {
+  const long long na = c.sc->n_acc, no = c.sc->n_ov;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t a = warp; a < na + no; a += nw) {
+    const int32_t s = a < na ? w.acc_slot[a] : pw.ov_slot[a - na];
+    const int32_t j = a < na ? w.acc_j[a] : pw.ov_j[a - na];
+    const uint64_t key = key_a[j];
+    if (c.skey[s] != key || c.stick[s] == kFree || pw.writer[s] != j) continue;
+    if (lane == 0) {
+      h_insert(c, key, s);
+      c.skey2[s] = key_b[j];
+    }
+    const int32_t dim = c.ssize[s] / 4;
+    const float *src = src_rows[j];
     float *dst = c.rows + static_cast<int64_t>(s) * c.row_ld;
     if (src)
       for (int i = lane; i < dim; i += 32) dst[i] = src[i];
@@ -1009,6 +1218,7 @@ int fx_cache_create(fx_cache **out, int64_t slot_capacity, int32_t max_dim, int3
   rc = rc ? rc : dmalloc(&v.hkeys, v.hcap);
   rc = rc ? rc : dmalloc(&v.hslot, v.hcap);
   rc = rc ? rc : dmalloc(&v.skey, v.scap);
+  rc = rc ? rc : dmalloc(&v.skey2, v.scap);
   rc = rc ? rc : dmalloc(&v.stick, v.scap);
   rc = rc ? rc : dmalloc(&v.ssize, v.scap);
   rc = rc ? rc : dmalloc(&v.shits, v.scap);
@@ -1043,7 +1253,7 @@ int fx_cache_create(fx_cache **out, int64_t slot_capacity, int32_t max_dim, int3
 int fx_cache_destroy(fx_cache *c) {
   if (!c) return FX_OK;
   CacheView &v = c->v;
-  void *ps[] = {v.sc, v.hkeys, v.hslot, v.skey, v.stick, v.ssize, v.shits, v.rows, v.free_stack, v.kkeys,
+  void *ps[] = {v.sc, v.hkeys, v.hslot, v.skey, v.skey2, v.stick, v.ssize, v.shits, v.rows, v.free_stack, v.kkeys,
                 v.kval, v.kflag, v.pend, v.evlog, c->dir_dev, c->tbytes_dev, c->ws, c->last_ev};
   for (void *p : ps)
     if (p) cudaFree(p);
@@ -1122,6 +1332,7 @@ int fx_cache_reserve_slots(fx_cache *c, int64_t slots, void *stream) {
   nv.hcap = pow2_at_least(4 * slots);
   nv.pend_cap = slots + 1024;
   rc = dmalloc(&nv.skey, nv.scap);
+  rc = rc ? rc : dmalloc(&nv.skey2, nv.scap);
   rc = rc ? rc : dmalloc(&nv.stick, nv.scap);
   rc = rc ? rc : dmalloc(&nv.ssize, nv.scap);
   rc = rc ? rc : dmalloc(&nv.shits, nv.scap);
@@ -1136,6 +1347,8 @@ int fx_cache_reserve_slots(fx_cache *c, int64_t slots, void *stream) {
   k_fill_u64<<<grid_for(nv.scap, 256), 256, 0, st>>>(nv.skey, nv.scap, kEmpty);
   std::vector<long long> freeticks(1, kFree);
   cudaMemcpyAsync(nv.skey, c->v.skey, S0 * 8, cudaMemcpyDeviceToDevice, st);
+  cudaMemsetAsync(nv.skey2, 0, nv.scap * 8, st);
+  cudaMemcpyAsync(nv.skey2, c->v.skey2, S0 * 8, cudaMemcpyDeviceToDevice, st);
   cudaMemcpyAsync(nv.ssize, c->v.ssize, S0 * 4, cudaMemcpyDeviceToDevice, st);
   cudaMemsetAsync(nv.ssize + S0, 0, (nv.scap - S0) * 4, st);
   cudaMemcpyAsync(nv.shits, c->v.shits, S0 * 4, cudaMemcpyDeviceToDevice, st);
@@ -1163,7 +1376,7 @@ int fx_cache_reserve_slots(fx_cache *c, int64_t slots, void *stream) {
   k_fill_u64<<<grid_for(nv.hcap, 256), 256, 0, st>>>(nv.hkeys, nv.hcap, kEmpty);
   k_index_rebuild<<<grid_for(nv.scap, 256), 256, 0, st>>>(nv);
   rc = cuda_check(cudaStreamSynchronize(st), "fx_cache_reserve_slots");
-  void *old[] = {c->v.skey, c->v.stick, c->v.ssize, c->v.shits, c->v.rows, c->v.free_stack, c->v.hkeys,
+  void *old[] = {c->v.skey, c->v.skey2, c->v.stick, c->v.ssize, c->v.shits, c->v.rows, c->v.free_stack, c->v.hkeys,
                  c->v.hslot, c->v.pend};
   for (void *p : old) cudaFree(p);
   c->v = nv;
@@ -1360,6 +1573,108 @@ int fx_cache_pending(fx_cache *c, uint64_t *out, int64_t cap, int64_t *n_out, vo
   if (n > 0) cudaMemcpyAsync(out, c->v.pend, n * 8, cudaMemcpyDeviceToDevice, st);
   *n_out = h.pending;
   return cuda_check(cudaStreamSynchronize(st), "fx_cache_pending");
+}
+
+int fx_cache_advance_tick(fx_cache *c, int64_t n, void *stream) {
+  k_advance_tick<<<1, 1, 0, as_stream(stream)>>>(c->v.sc, n);
+  FX_LAUNCH_CHECK("fx_cache_advance_tick");
+  return FX_OK;
+}
+
+int fx_cache_pooled_find(fx_cache *c, const uint64_t *key_a, const uint64_t *key_b, int64_t n, int32_t *slot_out,
+                         void *stream) {
+  if (n <= 0) return FX_OK;
+  k_pooled_find<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(c->v, key_a, key_b, n, slot_out);
+  FX_LAUNCH_CHECK("fx_cache_pooled_find");
+  return FX_OK;
+}
+
+int fx_cache_pooled_touch(fx_cache *c, const int32_t *slot, const int64_t *pos, int64_t n, void *stream) {
+  if (n <= 0) return FX_OK;
+  k_pooled_touch<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(c->v, slot, pos, n);
+  FX_LAUNCH_CHECK("fx_cache_pooled_touch");
+  return FX_OK;
+}
+
+int fx_cache_read_slots(fx_cache *c, const int32_t *slot, int64_t n, float *out, int32_t out_ld, int32_t *size_out,
+                        void *stream) {
+  if (n <= 0) return FX_OK;
+  k_read_slots<<<grid_for(n * 32, 256), 256, 0, as_stream(stream)>>>(c->v, slot, n, out, out_ld, size_out);
+  FX_LAUNCH_CHECK("fx_cache_read_slots");
+  return FX_OK;
+}
+
+int fx_cache_pooled_put(fx_cache *c, const uint64_t *key_a, const uint64_t *key_b, int64_t n, const int32_t *sizes,
+                        int32_t uniform_size, const float *const *src_rows, void *stream) {
+  cudaStream_t st = as_stream(stream);
+  if (n <= 0) return FX_OK;
+  if (!key_a || !key_b || !src_rows || (!sizes && uniform_size <= 0)) {
+    set_error("fx_cache_pooled_put: bad arguments");
+    return FX_E_CONFIG;
+  }
+  if (sizes) c->uniform = -1;
+  else if (c->uniform == 0) c->uniform = uniform_size;
+  else if (c->uniform > 0 && c->uniform != uniform_size) c->uniform = -1;
+  size_t cb = 0;
+  const size_t base = offer_ws_bytes(c, n, &cb);
+  size_t cb2 = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, cb2, (const uint64_t *)nullptr, (uint64_t *)nullptr,
+                                  (const int32_t *)nullptr, (int32_t *)nullptr, static_cast<int>(n));
+  const int64_t S = c->v.scap;
+  const size_t extra = al(n * 4) * 7 + al(n * 8) + al(S * 4) + al(cb2);
+  int rc = ensure_ws(c, base + extra);
+  if (rc) return rc;
+  void *cub_tmp = nullptr;
+  OfferWS w = carve_offer_ws(c, n, &cub_tmp);
+  char *p = static_cast<char *>(c->ws) + base;
+  PutWS pw;
+  pw.present_slot = reinterpret_cast<int32_t *>(p); p += al(n * 4);
+  pw.prev = reinterpret_cast<int32_t *>(p); p += al(n * 4);
+  pw.slot_of = reinterpret_cast<int32_t *>(p); p += al(n * 4);
+  pw.iota = reinterpret_cast<int32_t *>(p); p += al(n * 4);
+  pw.perm = reinterpret_cast<int32_t *>(p); p += al(n * 4);
+  pw.ov_slot = reinterpret_cast<int32_t *>(p); p += al(n * 4);
+  pw.ov_j = reinterpret_cast<int32_t *>(p); p += al(n * 4);
+  pw.keys_sorted = reinterpret_cast<uint64_t *>(p); p += al(n * 8);
+  pw.writer = reinterpret_cast<int32_t *>(p); p += al(S * 4);
+  void *cub2 = p;
+  Scalars h;
+  rc = read_scalars(c, &h, st);
+  if (rc) return rc;
+  if (c->last_ev_cap < h.entries + n + 1) {
+    if (c->last_ev) cudaFree(c->last_ev);
+    c->last_ev_cap = 2 * (h.entries + n + 1);
+    rc = dmalloc(&c->last_ev, c->last_ev_cap);
+    if (rc) return rc;
+  }
+  w.ev_keys = c->last_ev;
+  // entries never exceed budget / size (every insert first evicts to fit)
+  if (h.entries + n > S && (sizes || h.budget / uniform_size > S)) {
+    set_error("fx_cache_pooled_put: slot capacity below the budget's entry count; call fx_cache_reserve_slots");
+    return FX_E_CAPACITY;
+  }
+  k_put_prep<<<grid_for(n, 256), 256, 0, st>>>(c->v, key_a, key_b, n, sizes, uniform_size, w, pw);
+  cub::DeviceRadixSort::SortPairs(cub2, cb2, key_a, pw.keys_sorted, pw.iota, pw.perm, static_cast<int>(n), 0, 64,
+                                  st);
+  k_put_prev<<<grid_for(n, 256), 256, 0, st>>>(pw.keys_sorted, pw.perm, n, key_b, pw, c->v.sc);
+  if (h.entries > 0) {
+    k_lru_keys<<<grid_for(S, 256), 256, 0, st>>>(c->v, w);
+    cub::DeviceRadixSort::SortPairs(cub_tmp, cb, w.sort_keys_in, w.sort_keys_out, w.iota, w.lru_slot,
+                                    static_cast<int>(S), 0, 64, st);
+  }
+  k_put_seq<<<1, 32, 0, st>>>(c->v, key_a, key_b, n, w, pw, c->record);
+  k_hash_erase<<<grid_for(h.entries + n + 1, 256), 256, 0, st>>>(c->v, w);
+  k_install_put<<<grid_for(n * 32, 256), 256, 0, st>>>(c->v, w, pw, key_a, key_b, src_rows);
+  FX_LAUNCH_CHECK("fx_cache_pooled_put");
+  rc = read_scalars(c, &h, st);
+  if (rc) return rc;
+  if ((h.hash_tomb + h.entries) * 2 > c->v.hcap) {
+    k_fill_u64<<<grid_for(c->v.hcap, 256), 256, 0, st>>>(c->v.hkeys, c->v.hcap, kEmpty);
+    k_index_rebuild<<<grid_for(c->v.scap, 256), 256, 0, st>>>(c->v);
+    cudaMemsetAsync(&c->v.sc->hash_tomb, 0, sizeof(long long), st);
+    FX_LAUNCH_CHECK("fx_cache index rebuild");
+  }
+  return FX_OK;
 }
 
 int fx_cache_set_parallel(fx_cache *c, int32_t on) {

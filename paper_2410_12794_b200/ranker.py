@@ -33,7 +33,7 @@ import torch
 from . import _lib
 from .cache import AdaptiveCache, CachePolicy, LoadTracker, encode_key, target_cache_bytes
 from .dedup import Deduper
-from .errors import CapacityError, InvariantError, LookupValidationError
+from .errors import CapacityError, ConfigError, InvariantError, LookupValidationError
 from .pooling import PoolingOp, op_code, pool_flat
 from .requests import Batch, LookupRequest
 from .store import Deployment, make_segments
@@ -314,6 +314,16 @@ class Ranker:
         if cache is not None:
             cache.apply_pending_admissions()
         self._admission_check_size(n_lookups, batch_id)
+        full_nnz = nnz
+        lens_full = lay.offsets[1:] - lay.offsets[:-1]
+        pooled = None
+        n_ticks = nnz
+        if cache is not None and cache.pooled_results_enabled and n_bags:
+            # 2b. pooled-result probe per bag (ranker.py:238-245), then only the
+            # residual bags go through row probes, pooling and offers
+            self._mark("pooled_probe")
+            pooled, lay, dest, n_ticks = self._pooled_probe(lay, dest, lens_full, n_bags)
+            nnz = int(lay.indices.numel())
         # 3. dedup + probe (K2, K3)
         self._mark("dedup_probe")
         hit_occ = torch.zeros(nnz, dtype=torch.bool, device=dev)
@@ -321,8 +331,11 @@ class Ranker:
         if cache is not None and nnz:
             dd = self._dedup(lay.bag_table, lay.indices, lay.offsets, lay.sm_start, nnz)
             slot = torch.empty(max(dd.n_uniq, 1), dtype=torch.int32, device=dev)
-            cache.probe_unique(dd.uniq, dd.mult, dd.last_ord, None, nnz, slot, n_uniq_host=dd.n_uniq)
+            last = dd.last_ord if pooled is None else pooled[5][dd.last_ord]
+            cache.probe_unique(dd.uniq, dd.mult, last, None, n_ticks, slot, n_uniq_host=dd.n_uniq)
             hit_occ = slot[dd.inverse.long()] >= 0
+        elif cache is not None and n_ticks:
+            cache.advance_tick(n_ticks)
         # 4. miss groups per (bag, server) and the pushdown plan
         self._mark("plan")
         lens_tm = lay.offsets[1:] - lay.offsets[:-1]
@@ -346,6 +359,8 @@ class Ranker:
         hits_bag = torch.zeros(n_bags, dtype=torch.int64, device=dev)
         if nnz:
             hits_bag.index_add_(0, bag_of_occ, hit_occ.long())
+        if pooled is not None:  # a pooled hit counts every index as a cache hit (ranker.py:242-243)
+            hits_bag += torch.where(pooled[1], lens_full, torch.zeros_like(lens_full))
         pd_groups = push.sum(1)
         pd_rows = (grp * push).sum(1)
         raw_rows = (grp * (~push)).sum(1)
@@ -353,6 +368,8 @@ class Ranker:
         # 5. pooled vectors: per-shard f64 partials of the misses + cache rows as raw
         self._mark("pool")
         out = self._pool(lay, dest, hit_occ, dd, nnz, n_bags)
+        if pooled is not None:
+            self._pooled_finish(lay, pooled, out, n_bags)
         self._mark("offers")
         # 6. offers: raw-fetched misses, first raw occurrence order
         if cache is not None and nnz:
@@ -371,7 +388,63 @@ class Ranker:
         self._mark("end")
         self._flush_marks()
         # results (sample-major)
-        return out, hits_bag, pd_groups, pd_rows, raw_rows, nnz, n_groups
+        return out, hits_bag, pd_groups, pd_rows, raw_rows, full_nnz, n_groups
+
+    def _pooled_probe(self, lay: CsrLayout, dest, lens, n_bags):
+        """Fingerprint every bag, find its pooled entry, apply the hits'
+        recency at their tick positions, and cut the hit bags out of the CSR.
+        Ticks run in sample-major order: one per pooled_get, then one per row
+        probe of a missed bag (ranker.py:238-251)."""
+        from .cache import bag_fingerprints
+        dev = self.device
+        cache = self.cache
+        ops = torch.empty(n_bags, dtype=torch.int32, device=dev)
+        for (t, opc, b0, b1) in lay.segs:
+            ops[b0:b1] = opc
+        ka, kb = bag_fingerprints(lay.bag_table, ops, lay.indices, lay.offsets)
+        pslot = torch.empty(n_bags, dtype=torch.int32, device=dev)
+        cache.pooled_find(ka, kb, pslot)
+        phit = pslot >= 0
+        cost = 1 + torch.where(phit, torch.zeros_like(lens), lens)       # table-major bags
+        perm = torch.as_tensor(lay.perm, dtype=torch.int64, device=dev)   # tm bag -> sm bag
+        cost_sm = torch.empty_like(cost)
+        cost_sm[perm] = cost
+        pos = (torch.cumsum(cost_sm, 0) - cost_sm)[perm]                  # tick offset of each bag's pooled_get
+        cache.pooled_touch(pslot, pos)
+        keep_bag = ~phit
+        lens_r = torch.where(keep_bag, lens, torch.zeros_like(lens))
+        offs_r = torch.zeros(n_bags + 1, dtype=torch.int64, device=dev)
+        offs_r[1:] = torch.cumsum(lens_r, 0)
+        keep_occ = torch.repeat_interleave(keep_bag, lens)
+        # dedup wants dense sample-major ordinals of the residual occurrences;
+        # tick_of[ord] maps them back to the row probe's tick offset
+        lr_sm = torch.empty_like(lens_r)
+        lr_sm[perm] = lens_r
+        smc = (torch.cumsum(lr_sm, 0) - lr_sm)[perm]
+        nnz_r = int(offs_r[-1])
+        bag_occ = torch.repeat_interleave(torch.arange(n_bags, device=dev), lens_r)
+        within = torch.arange(nnz_r, device=dev) - offs_r[bag_occ]
+        tick_of = torch.empty(max(nnz_r, 1), dtype=torch.int64, device=dev)
+        tick_of[smc[bag_occ] + within] = pos[bag_occ] + 1 + within
+        rl = CsrLayout(lay.indices[keep_occ], offs_r, lay.bag_table, smc, lay.perm, lay.segs, lay.lens_sm,
+                       lay.bag_lookup_sm, lay.host_idx_sm, lay.n_lookups)
+        n_ticks = int(cost.sum())
+        return (pslot, phit, ka, kb, perm, tick_of), rl, dest[keep_occ], n_ticks
+
+    def _pooled_finish(self, lay: CsrLayout, pooled, out, n_bags):
+        """Hit bags take the cached vector; every other bag is put, in
+        sample-major (finish) order, before the row offers (ranker.py:401-414)."""
+        pslot, phit, ka, kb, perm, _ = pooled
+        cache = self.cache
+        cache.read_slots(pslot, out)
+        order_tm = torch.argsort(perm)                # tm bags in sample-major order
+        put_tm = order_tm[~phit[order_tm]]
+        if put_tm.numel():
+            dims = [self.deployment.meta(t).dim for t, *_ in lay.segs]
+            if len(set(dims)) != 1:
+                raise ConfigError("pooled-result keyspace with mixed table dims in one batch is not supported")
+            cache.pooled_put_many(ka[put_tm].contiguous(), kb[put_tm].contiguous(), out, dims[0] * 4, sel=put_tm)
+        cache.check_state()
 
     def _pool(self, lay: CsrLayout, dest, hit_occ, dd, nnz, n_bags) -> torch.Tensor:
         dims = {self.deployment.meta(t).dim for t, *_ in lay.segs}

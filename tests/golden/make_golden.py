@@ -216,6 +216,72 @@ def ranker_fixtures():
         json.dump(out, fh)
 
 
+def _key_json(k):
+    if isinstance(k, tuple) and len(k) == 4 and k[0] == "pooled":
+        return ["pooled", k[1], k[2], list(k[3])]
+    return list(k)
+
+
+def pooled_fixtures():
+    """Ranker with the pooled-result keyspace on (cache.py:204-223,
+    ranker.py:238-249,401-414), 1 server: small tables and short bags so
+    bag multisets repeat within and across batches (pooled hits, in-place
+    re-puts and their leaked bytes)."""
+    out = []
+    rng = np.random.default_rng(9)
+    for thr, budget_rows, n_batches, name, rows0, L in ((2, 400, 6, "pooled_thr2", 40, (1, 3)),
+                                                       (None, 300, 6, "pooled_thrNone", 40, (1, 3)),
+                                                       (2, 40, 8, "pooled_churn", 40, (1, 3)),
+                                                       (2, 60, 12, "pooled_leak", 6, (1, 1))):
+        metas = [TableMeta(0, rows0, 16), TableMeta(1, 600, 16)]
+        placement = [ShardSpec(0, 0, rows0, 0), ShardSpec(1, 0, 600, 0)]
+        budget = 64 * budget_rows
+        model = MemoryModel(gpu_capacity_bytes=budget + 1000 + 100, nn_fixed_bytes=1000, nn_per_sample_bytes=1)
+        cache = AdaptiveCache(budget_bytes=budget, admission="sketch", pooled_results=True, record_evictions=True)
+        policy = CachePolicy(model=model, hysteresis_fraction=0.05)
+        tracker = LoadTracker(window=4, high_watermark=512, low_watermark=16)
+        rk = _ranker(metas, placement, cache, policy, tracker, threshold=thr, admit=8)
+        batches = _zipf_batches(rng, metas, n_batches=n_batches, lookups=(20, 30), L=L, alpha=1.2, mean_p=0.3)
+        rec = dict(name=name, metas=[[m.table_id, m.num_rows, m.dim] for m in metas],
+                   placement=[[s.table_id, s.start, s.end, s.server_id] for s in placement], threshold=thr,
+                   cache=dict(budget=budget, admission="sketch",
+                              model=[model.gpu_capacity_bytes, model.nn_fixed_bytes, model.nn_per_sample_bytes],
+                              hyst=0.05, tracker=[4, 512, 16], admit=8),
+                   batches=[], results=[], counters=[], metrics=[], per_batch_lru=[], per_batch_used=[],
+                   raised_at=None)
+        for b in batches:
+            rec["batches"].append([[[f.table_id, f.op.value, f.indices] for f in lk.features] for lk in b.lookups])
+            try:
+                rk.execute_batch(b)
+            except KeyError:
+                rec["raised_at"] = b.batch_id
+                break
+            res = rk.results[b.batch_id]
+            rec["results"].append([[[float(x) for x in v.view(np.uint32).astype(np.float64)] for v in r.vectors]
+                                   for r in res])
+            rec["counters"].append([[r.cache_hits, r.pushdown_groups, r.pushdown_rows, r.raw_rows] for r in res])
+            m = rk.batch_metrics[-1]
+            rec["metrics"].append(dict(hits=m.cache_hits, misses=m.cache_misses, pushdown_groups=m.pushdown_groups,
+                                       pushdown_rows=m.pushdown_rows, raw_rows=m.raw_rows, load_level=m.load_level,
+                                       budget=m.cache_budget, used=m.cache_used, subrequests=m.subrequests))
+            rec["per_batch_lru"].append([_key_json(k) for k in rk.cache._entries])
+            rec["per_batch_used"].append(rk.cache.used_bytes)
+        rec["evictions"] = [_key_json(k) for k in rk.cache.eviction_log]
+        out.append(rec)
+    # API-level example (test_cache.py:222-228) plus an in-place re-put
+    c = AdaptiveCache(budget_bytes=3 * 64, pooled_results=True, record_evictions=True)
+    v = lambda x: np.full(16, x, np.float32)
+    c.pooled_put(0, PoolingOp.SUM, [2, 1], v(9.0))
+    c.offer(0, 5, v(1.0))
+    c.pooled_put(0, PoolingOp.SUM, [1, 2], v(7.0))   # resident: replaced in place, used += 64
+    got = c.pooled_get(0, PoolingOp.SUM, [1, 2])
+    c.pooled_put(1, PoolingOp.MEAN, [3], v(4.0))       # evicts the LRU entry
+    api = dict(lru=[_key_json(k) for k in c._entries], used=c.used_bytes, tick=c.tick,
+               got=[float(x) for x in got], evictions=[_key_json(k) for k in c.eviction_log])
+    with open(os.path.join(HERE, "pooled.json"), "w") as fh:
+        json.dump(dict(ranker=out, api=api), fh)
+
+
 def _zipf_batches(rng, metas, n_batches, lookups, L, alpha, mean_p=0.0):
     samplers = {m.table_id: ZipfSampler(m.num_rows, alpha) for m in metas}
     batches = []
@@ -286,5 +352,6 @@ if __name__ == "__main__":
     zipf_fixtures()
     cache_fixtures()
     ranker_fixtures()
+    pooled_fixtures()
     for f in sorted(os.listdir(HERE)):
         print(f, os.path.getsize(os.path.join(HERE, f)))

@@ -161,3 +161,62 @@ def test_pipeline_oracle_vs_reference_ranker(golden_dir, which):
     if po.cache is not None:
         assert [list(k) for k in po.cache.evictions] == rec["evictions"]
         assert sorted([[k[0], k[1], v] for k, v in po.cache.sketch.items()]) == rec["final_sketch"]
+
+
+def _kj(k):
+    if isinstance(k, tuple) and len(k) == 4 and k[0] == "pooled":
+        return ["pooled", k[1], k[2], list(k[3])]
+    return list(k)
+
+
+@pytest.mark.parametrize("which", [0, 1, 2, 3])
+def test_pipeline_oracle_pooled_keyspace_vs_reference(golden_dir, which):
+    """Pooled-result keyspace (cache.py:204-223, ranker.py:238-249,401-414):
+    per-batch vectors, counters, metrics, LRU (row + pooled keys), used bytes
+    (including the bytes leaked by in-place re-puts) and the eviction log."""
+    rec = json.load(open(os.path.join(golden_dir, "pooled.json")))["ranker"][which]
+    po, _ = _pipeline_for(rec)
+    po.cache.pooled = True
+    for bi, lookups in enumerate(rec["batches"]):
+        bb = O.bag_batch_from_lists([[(t, op, ix) for t, op, ix in lk] for lk in lookups], batch_id=bi)
+        vecs, counters, _ = po.run(bb)
+        m, ref_m = po.metrics[-1], rec["metrics"][bi]
+        for key in ("hits", "misses", "pushdown_groups", "pushdown_rows", "raw_rows"):
+            assert m[key] == ref_m[key], (bi, key)
+        b = 0
+        for li, lk in enumerate(lookups):
+            agg = [0, 0, 0, 0]
+            for fp in range(len(lk)):
+                for q in range(4):
+                    agg[q] += counters[b][q]
+                ref_bits = np.array(rec["results"][bi][li][fp], dtype=np.uint32).view(np.float32)
+                assert vecs[b].tobytes() == ref_bits.tobytes(), (bi, li, fp)
+                b += 1
+            assert agg == rec["counters"][bi][li]
+        assert [_kj(k) for k in po.cache.lru_keys()] == rec["per_batch_lru"][bi], bi
+        assert po.cache.used == rec["per_batch_used"][bi]
+    assert [_kj(k) for k in po.cache.evictions] == rec["evictions"]
+
+
+def test_cache_oracle_pooled_api(golden_dir):
+    api = json.load(open(os.path.join(golden_dir, "pooled.json")))["api"]
+    c = O.CacheOracle(3 * 64, pooled=True)
+    v = lambda x: np.full(16, x, np.float32)
+    c.pooled_put(("pooled", 0, "sum", (1, 2)), v(9.0))
+    c.offer((0, 5), 64)
+    c.pooled_put(("pooled", 0, "sum", (1, 2)), v(7.0))
+    got = c.pooled_get(("pooled", 0, "sum", (1, 2)))
+    c.pooled_put(("pooled", 1, "mean", (3,)), v(4.0))
+    assert [_kj(k) for k in c.lru_keys()] == api["lru"]
+    assert (c.used, c.tick) == (api["used"], api["tick"])
+    assert [float(x) for x in got] == api["got"]
+    assert [_kj(k) for k in c.evictions] == api["evictions"]
+
+
+def test_pooled_fingerprint_is_a_multiset_key():
+    a = O.pooled_fingerprint(3, "sum", [5, 1, 5, 9])
+    assert a == O.pooled_fingerprint(3, "sum", [9, 5, 1, 5])
+    assert a != O.pooled_fingerprint(3, "sum", [5, 1, 9])
+    assert a != O.pooled_fingerprint(3, "mean", [5, 1, 5, 9])
+    assert a != O.pooled_fingerprint(4, "sum", [5, 1, 5, 9])
+    assert a[0] >> 63 == 1
