@@ -20,6 +20,7 @@
 // precomputed, parallel-gathered inputs (sketch estimates, LRU order); the
 // hash-index and row-copy side effects are applied afterwards in parallel.
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
 
 #include <climits>
@@ -44,6 +45,7 @@ struct Scalars {
   long long err;   // 1: eviction queue exhausted (the reference's popitem on an empty
                    //    OrderedDict), 2: pooled-key fingerprint collision
   long long n_ov;  // in-place pooled re-puts recorded by the last put call
+  long long n_par_puts;  // put calls resolved by the parallel closed form (cumulative)
 };
 
 struct CacheView {
@@ -254,9 +256,12 @@ __global__ void k_offer_prep(CacheView c, const uint64_t *keys, int64_t n, const
   }
 }
 
-__global__ void k_lru_keys(CacheView c, OfferWS w) {
+// LRU sort keys: ticks, free slots mapped to free_key (> every live tick) so
+// the radix sort only needs the low lru_bits(tick) bits.
+__global__ void k_lru_keys(CacheView c, OfferWS w, long long free_key) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < c.scap; i += (int64_t)gridDim.x * blockDim.x) {
-    w.sort_keys_in[i] = c.stick[i];
+    const long long t = c.stick[i];
+    w.sort_keys_in[i] = t == kFree ? free_key : t;
     w.iota[i] = static_cast<int32_t>(i);
   }
 }
@@ -705,6 +710,14 @@ struct PutWS {
   int32_t *ov_slot;       // in-place re-puts (slot, j)
   int32_t *ov_j;
   int32_t *writer;        // [slots] last put that wrote the slot (valid for recorded slots)
+  // parallel path (uniform sizes)
+  int32_t *run_in;        // sorted position if it starts a key run, else 0
+  int32_t *run_start;     // inclusive max-scan of run_in
+  int32_t *first;         // first put of j's key in this call
+  int32_t *lastj;         // [first put] last put of that key (its vector wins)
+  int32_t *fresh;         // 1 for the first put of a key
+  int32_t *rank;          // exclusive prefix of fresh
+  int32_t *fail;          // device flag: parallel preconditions violated -> sequential loop
 };
 
 __global__ void k_put_prep(CacheView c, const uint64_t *key_a, const uint64_t *key_b, int64_t n,
@@ -735,6 +748,112 @@ __global__ void k_put_prev(const uint64_t *keys_sorted, const int32_t *perm, int
   }
 }
 
+__global__ void k_put_heads(const uint64_t *keys_sorted, int64_t n, PutWS pw) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x)
+    pw.run_in[p] = (p == 0 || keys_sorted[p - 1] != keys_sorted[p]) ? static_cast<int32_t>(p) : 0;
+}
+
+__global__ void k_put_links(const uint64_t *keys_sorted, int64_t n, PutWS pw) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t j = pw.perm[p];
+    const int32_t f = pw.perm[pw.run_start[p]];
+    pw.first[j] = f;
+    pw.fresh[j] = (f == j) ? 1 : 0;
+    if (p == n - 1 || keys_sorted[p + 1] != keys_sorted[p]) pw.lastj[f] = j;
+  }
+}
+
+// Parallel form of k_put_seq for one entry size S (uniform dims). With
+// units0 = used / S (entries + leaked units), cap = budget / S and e0 live
+// entries, put i (0-based) leaves ev(i) = max(0, units0 + i + 1 - cap)
+// evictions behind it, taken from the queue V = [entries by LRU] ++ [first
+// puts of each key, in order]. If every re-put finds its key still resident
+// (queue position e0 + rank(first) >= ev(i)), no key was resident at call
+// start and the queue never runs dry, the loop's outcome is closed-form:
+// V[0, E) evicted (E = ev(n-1)), surviving first puts installed with tick
+// tick0 + i + 1 and the vector of their key's last put, used = (units0 + n -
+// E) * S. Otherwise `fail` is raised and k_put_seq runs instead.
+__global__ void k_putp_verify(CacheView c, int64_t n, int32_t S, PutWS pw) {
+  const Scalars *sc = c.sc;
+  const long long units0 = sc->used / S, cap = sc->budget / S, e0 = sc->entries;
+  bool bad = (sc->used % S) != 0 || S > sc->budget;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n && !bad;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (pw.present_slot[i] >= 0) bad = true;
+    const long long ev = units0 + i + 1 - cap > 0 ? units0 + i + 1 - cap : 0;
+    if (ev > e0 + pw.rank[i]) bad = true;
+    if (!pw.fresh[i] && e0 + pw.rank[pw.first[i]] < ev) bad = true;
+  }
+  if (bad) atomicExch(pw.fail, 1);
+}
+
+__global__ void k_putp_evict(CacheView c, int64_t n, int32_t S, OfferWS w, PutWS pw, int32_t record) {
+  if (*pw.fail) return;
+  const Scalars *sc = c.sc;
+  const long long units0 = sc->used / S, cap = sc->budget / S, e0 = sc->entries;
+  const long long E = units0 + n - cap > 0 ? units0 + n - cap : 0;
+  const long long ee = E < e0 ? E : e0;
+  const long long ftop = sc->free_top, log0 = sc->n_evlog;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < ee; k += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t s = w.lru_slot[k];
+    const uint64_t key = c.skey[s];
+    w.ev_keys[k] = key;
+    if (record && log0 + k < c.evlog_cap) c.evlog[log0 + k] = key;
+    c.stick[s] = kFree;
+    c.skey[s] = kEmpty;
+    c.free_stack[ftop + k] = s;
+  }
+}
+
+__global__ void k_putp_insert(CacheView c, const uint64_t *key_a, const uint64_t *key_b, int64_t n, int32_t S,
+                              OfferWS w, PutWS pw, int32_t record) {
+  if (*pw.fail) return;
+  const Scalars *sc = c.sc;
+  const long long units0 = sc->used / S, cap = sc->budget / S, e0 = sc->entries;
+  const long long E = units0 + n - cap > 0 ? units0 + n - cap : 0;
+  const long long ee = E < e0 ? E : e0, fe = E - ee;  // evicted entries / evicted first puts
+  const long long ftop = sc->free_top + ee, log0 = sc->n_evlog, tick0 = sc->tick;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    if (!pw.fresh[j]) continue;
+    const long long r = pw.rank[j];
+    if (r < fe) {  // inserted and evicted again within the call
+      w.ev_keys[e0 + r] = key_a[j];
+      if (record && log0 + e0 + r < c.evlog_cap) c.evlog[log0 + e0 + r] = key_a[j];
+      continue;
+    }
+    const long long u = r - fe;
+    const int32_t s = c.free_stack[ftop - 1 - u];
+    const int32_t lj = pw.lastj[j];
+    c.skey[s] = key_a[j];
+    c.skey2[s] = key_b[j];
+    c.stick[s] = tick0 + j + 1;
+    c.ssize[s] = S;
+    c.shits[s] = 0;
+    pw.writer[s] = lj;
+    w.acc_slot[u] = s;
+    w.acc_j[u] = lj;
+  }
+}
+
+__global__ void k_putp_finish(CacheView c, int64_t n, int32_t S, PutWS pw, int32_t record) {
+  if (*pw.fail) return;
+  Scalars *sc = c.sc;
+  const long long units0 = sc->used / S, cap = sc->budget / S, e0 = sc->entries;
+  const long long E = units0 + n - cap > 0 ? units0 + n - cap : 0;
+  const long long ee = E < e0 ? E : e0, fe = E - ee;
+  const long long F = pw.rank[n - 1] + pw.fresh[n - 1];
+  const long long inst = F - fe;
+  sc->used = (units0 + n - E) * S;
+  sc->tick += n;
+  sc->entries = e0 - ee + inst;
+  sc->free_top = sc->free_top + ee - inst;
+  sc->n_acc = inst;
+  sc->n_ov = 0;
+  sc->n_ev = E;
+  if (record) sc->n_evlog += E;
+  sc->n_par_puts += 1;
+}
+
 // Ordered pooled_put loop (cache.py:219-223 -> _insert, cache.py:256-268):
 // no admission test; evict LRU until the size fits, take a tick, insert at
 // MRU. A key that is still resident (put twice in one batch, or re-put
@@ -742,8 +861,9 @@ __global__ void k_put_prev(const uint64_t *keys_sorted, const int32_t *perm, int
 // assignment: its LRU position is kept, hits restart at 0 and used_bytes
 // grows by the size again without a new entry (the bytes are never freed).
 __global__ void k_put_seq(CacheView c, const uint64_t *key_a, const uint64_t *key_b, int64_t n, OfferWS w,
-                          PutWS pw, int32_t record) {
+                          PutWS pw, int32_t record, int32_t only_on_fail) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (only_on_fail && *pw.fail == 0) return;
   Scalars *sc = c.sc;
   long long used = sc->used, budget = sc->budget, tick = sc->tick, entries = sc->entries, ftop = sc->free_top;
   const long long e0 = entries;
@@ -985,6 +1105,14 @@ __global__ void k_dump_sketch(CacheView c, const int32_t *pos, int64_t n, uint64
 
 static inline size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 
+// bits needed for LRU sort keys when every live tick is <= tick (free slots
+// sort last as (1 << bits) - 1)
+static inline int lru_bits(long long tick) {
+  int b = 1;
+  while (b < 63 && (1ll << b) - 1 <= tick) ++b;
+  return b;
+}
+
 }  // namespace fx
 
 using namespace fx;
@@ -1119,9 +1247,9 @@ int run_offer(fx_cache *c, const uint64_t *keys, int64_t n, int32_t mode, const 
   int64_t k_vic = 0;
   if (h.entries > 0) {
     const int64_t S = c->v.scap;
-    k_lru_keys<<<grid_for(S, 256), 256, 0, st>>>(c->v, w);
+    k_lru_keys<<<grid_for(S, 256), 256, 0, st>>>(c->v, w, (1ll << lru_bits(h.tick)) - 1);
     cub::DeviceRadixSort::SortPairs(cub_tmp, cb, w.sort_keys_in, w.sort_keys_out, w.iota, w.lru_slot,
-                                    static_cast<int>(S), 0, 64, st);
+                                    static_cast<int>(S), 0, lru_bits(h.tick), st);
     k_vic = h.entries < n ? h.entries : n;
     if (mode == 0 && c->v.admission == 0 && k_vic > 0)
       k_vic_prep<<<grid_for(k_vic, 256), 256, 0, st>>>(c->v, w, k_vic);
@@ -1540,9 +1668,9 @@ int fx_cache_lru(fx_cache *c, uint64_t *keys_out, int64_t *ticks_out, int32_t *h
   void *cub_tmp = nullptr;
   OfferWS w = carve_offer_ws(c, 0, &cub_tmp);
   const int64_t S = c->v.scap;
-  k_lru_keys<<<grid_for(S, 256), 256, 0, st>>>(c->v, w);
+  k_lru_keys<<<grid_for(S, 256), 256, 0, st>>>(c->v, w, (1ll << lru_bits(h.tick)) - 1);
   cub::DeviceRadixSort::SortPairs(cub_tmp, cb, w.sort_keys_in, w.sort_keys_out, w.iota, w.lru_slot,
-                                  static_cast<int>(S), 0, 64, st);
+                                  static_cast<int>(S), 0, lru_bits(h.tick), st);
   const int64_t n = h.entries < cap ? h.entries : cap;
   if (n > 0)
     k_dump_lru<<<grid_for(n, 256), 256, 0, st>>>(c->v, w.lru_slot, n, keys_out,
@@ -1617,11 +1745,16 @@ int fx_cache_pooled_put(fx_cache *c, const uint64_t *key_a, const uint64_t *key_
   else if (c->uniform > 0 && c->uniform != uniform_size) c->uniform = -1;
   size_t cb = 0;
   const size_t base = offer_ws_bytes(c, n, &cb);
-  size_t cb2 = 0;
+  size_t cb2 = 0, cb3 = 0, cb4 = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, cb2, (const uint64_t *)nullptr, (uint64_t *)nullptr,
                                   (const int32_t *)nullptr, (int32_t *)nullptr, static_cast<int>(n));
+  cub::DeviceScan::InclusiveScan(nullptr, cb3, (const int32_t *)nullptr, (int32_t *)nullptr, cub::Max(),
+                                 static_cast<int>(n));
+  cub::DeviceScan::ExclusiveSum(nullptr, cb4, (const int32_t *)nullptr, (int32_t *)nullptr, static_cast<int>(n));
+  if (cb3 > cb2) cb2 = cb3;
+  if (cb4 > cb2) cb2 = cb4;
   const int64_t S = c->v.scap;
-  const size_t extra = al(n * 4) * 7 + al(n * 8) + al(S * 4) + al(cb2);
+  const size_t extra = al(n * 4) * 13 + al(n * 8) + al(S * 4) + al(8) + al(cb2);
   int rc = ensure_ws(c, base + extra);
   if (rc) return rc;
   void *cub_tmp = nullptr;
@@ -1637,6 +1770,13 @@ int fx_cache_pooled_put(fx_cache *c, const uint64_t *key_a, const uint64_t *key_
   pw.ov_j = reinterpret_cast<int32_t *>(p); p += al(n * 4);
   pw.keys_sorted = reinterpret_cast<uint64_t *>(p); p += al(n * 8);
   pw.writer = reinterpret_cast<int32_t *>(p); p += al(S * 4);
+  pw.run_in = reinterpret_cast<int32_t *>(p); p += al(n * 4);
+  pw.run_start = reinterpret_cast<int32_t *>(p); p += al(n * 4);
+  pw.first = reinterpret_cast<int32_t *>(p); p += al(n * 4);
+  pw.lastj = reinterpret_cast<int32_t *>(p); p += al(n * 4);
+  pw.fresh = reinterpret_cast<int32_t *>(p); p += al(n * 4);
+  pw.rank = reinterpret_cast<int32_t *>(p); p += al(n * 4);
+  pw.fail = reinterpret_cast<int32_t *>(p); p += al(8);
   void *cub2 = p;
   Scalars h;
   rc = read_scalars(c, &h, st);
@@ -1658,11 +1798,23 @@ int fx_cache_pooled_put(fx_cache *c, const uint64_t *key_a, const uint64_t *key_
                                   st);
   k_put_prev<<<grid_for(n, 256), 256, 0, st>>>(pw.keys_sorted, pw.perm, n, key_b, pw, c->v.sc);
   if (h.entries > 0) {
-    k_lru_keys<<<grid_for(S, 256), 256, 0, st>>>(c->v, w);
+    k_lru_keys<<<grid_for(S, 256), 256, 0, st>>>(c->v, w, (1ll << lru_bits(h.tick)) - 1);
     cub::DeviceRadixSort::SortPairs(cub_tmp, cb, w.sort_keys_in, w.sort_keys_out, w.iota, w.lru_slot,
-                                    static_cast<int>(S), 0, 64, st);
+                                    static_cast<int>(S), 0, lru_bits(h.tick), st);
   }
-  k_put_seq<<<1, 32, 0, st>>>(c->v, key_a, key_b, n, w, pw, c->record);
+  const bool par = c->parallel_offers && !sizes && c->uniform > 0 && c->uniform == uniform_size;
+  if (par) {
+    cudaMemsetAsync(pw.fail, 0, 4, st);
+    k_put_heads<<<grid_for(n, 256), 256, 0, st>>>(pw.keys_sorted, n, pw);
+    cub::DeviceScan::InclusiveScan(cub2, cb2, pw.run_in, pw.run_start, cub::Max(), static_cast<int>(n), st);
+    k_put_links<<<grid_for(n, 256), 256, 0, st>>>(pw.keys_sorted, n, pw);
+    cub::DeviceScan::ExclusiveSum(cub2, cb2, pw.fresh, pw.rank, static_cast<int>(n), st);
+    k_putp_verify<<<grid_for(n, 256), 256, 0, st>>>(c->v, n, uniform_size, pw);
+    k_putp_evict<<<grid_for(h.entries + 1, 256), 256, 0, st>>>(c->v, n, uniform_size, w, pw, c->record);
+    k_putp_insert<<<grid_for(n, 256), 256, 0, st>>>(c->v, key_a, key_b, n, uniform_size, w, pw, c->record);
+    k_putp_finish<<<1, 1, 0, st>>>(c->v, n, uniform_size, pw, c->record);
+  }
+  k_put_seq<<<1, 32, 0, st>>>(c->v, key_a, key_b, n, w, pw, c->record, par ? 1 : 0);
   k_hash_erase<<<grid_for(h.entries + n + 1, 256), 256, 0, st>>>(c->v, w);
   k_install_put<<<grid_for(n * 32, 256), 256, 0, st>>>(c->v, w, pw, key_a, key_b, src_rows);
   FX_LAUNCH_CHECK("fx_cache_pooled_put");

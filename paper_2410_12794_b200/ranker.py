@@ -436,6 +436,8 @@ class Ranker:
         sample-major (finish) order, before the row offers (ranker.py:401-414)."""
         pslot, phit, ka, kb, perm, _ = pooled
         cache = self.cache
+        if self.profile:
+            self.last_pooled_hits = int(phit.sum())
         cache.read_slots(pslot, out)
         order_tm = torch.argsort(perm)                # tm bags in sample-major order
         put_tm = order_tm[~phit[order_tm]]

@@ -32,7 +32,9 @@ def main():
     ap.add_argument("--rows", type=int, default=10_000_000)
     ap.add_argument("--dim", type=int, default=128)
     ap.add_argument("--batch", type=int, default=4096)
-    ap.add_argument("--pooling", type=int, default=20)
+    ap.add_argument("--pooling", default="20", help="L, or lo,hi for ragged bags")
+    ap.add_argument("--pooled", type=int, default=0, help="pooled-result keyspace on (cache.py:204-223)")
+    ap.add_argument("--threshold", default="none", help="pushdown threshold (none or an int >= 2)")
     ap.add_argument("--alphas", default="0.6,0.8,1.0,1.2")
     ap.add_argument("--cache-pct", default="1,2,5")
     ap.add_argument("--batches", type=int, default=6)
@@ -41,6 +43,9 @@ def main():
     a = ap.parse_args()
     torch.cuda.set_device(0)
     T, N, D, B = a.tables, a.rows, a.dim, a.batch
+    pool = tuple(int(x) for x in a.pooling.split(","))
+    pool = pool if len(pool) == 2 else (pool[0], pool[0])
+    thr = None if a.threshold == "none" else int(a.threshold)
     metas = [P.TableMeta(t, N, D) for t in range(T)]
     placement = [P.ShardSpec(t, 0, N, 0) for t in range(T)]
     t0 = time.perf_counter()
@@ -48,7 +53,7 @@ def main():
     torch.cuda.synchronize()
     init_s = time.perf_counter() - t0
     for alpha in [float(x) for x in a.alphas.split(",")]:
-        gen = DlrmBatchGen((N,) * T, alpha, B, a.pooling, seed=7)
+        gen = DlrmBatchGen((N,) * T, alpha, B, pool, seed=7)
         batches = [gen.next() for _ in range(a.warm + a.batches)]
         dev_batches = [(torch.from_numpy(hb.indices).cuda(), torch.from_numpy(hb.offsets).cuda())
                        for hb in batches]
@@ -58,9 +63,9 @@ def main():
             per_sample = 1
             model = C.MemoryModel(budget + 1_000 + B * per_sample, 1_000, per_sample)
             cache = C.AdaptiveCache(budget, admission="sketch", max_dim=D, slot_capacity=rows_cached + 1,
-                                    sketch_capacity=4 * B * a.pooling * T)
+                                    sketch_capacity=4 * B * pool[1] * T, pooled_results=bool(a.pooled))
             rk = Ranker(dep, P.build_routing(metas, placement), None,
-                        RankerParams(pushdown_threshold=None, admit_per_batch=64), cache=cache,
+                        RankerParams(pushdown_threshold=thr, admit_per_batch=64), cache=cache,
                         policy=C.CachePolicy(model), tracker=C.LoadTracker(16, 10 ** 9, 0),
                         hits_from_cache=bool(a.hits_from_cache))
             times, hits = [], []
@@ -81,7 +86,9 @@ def main():
             print(json.dumps({"alpha": alpha, "cache_pct": pct, "cache_rows": rows_cached,
                               "hit_rate": sum(hits) / len(hits), "ms_per_batch": ms,
                               "pooled_lookups_per_s": B * T / (ms / 1e3), "tables": T, "rows": N, "dim": D,
-                              "batch": B, "pooling": a.pooling, "init_store_s": round(init_s, 2),
+                              "batch": B, "pooling": list(pool), "init_store_s": round(init_s, 2),
+                              "pooled_keyspace": bool(a.pooled), "threshold": thr,
+                              "pooled_hit_bags_last": getattr(rk, "last_pooled_hits", None),
                               "hits_from_cache": bool(a.hits_from_cache),
                               "stage_ms_per_batch": {k: round(v / len(times), 3) for k, v in rk.stage_ms.items()}}),
                   flush=True)

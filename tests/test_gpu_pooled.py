@@ -50,10 +50,12 @@ def _build(P, rec):
     return dep, rk
 
 
+@pytest.mark.parametrize("parallel", [True, False])
 @pytest.mark.parametrize("which", [0, 1, 2, 3])
-def test_pooled_ranker_replays_reference(P, golden_dir, which):
+def test_pooled_ranker_replays_reference(P, golden_dir, which, parallel):
     rec = json.load(open(os.path.join(golden_dir, "pooled.json")))["ranker"][which]
     dep, rk = _build(P, rec)
+    rk.cache.set_parallel_offers(parallel)
     for bi, lookups in enumerate(rec["batches"]):
         batch = P.Batch(bi, bi, [P.LookupRequest([P.Feature(t, P.PoolingOp(op), ix) for t, op, ix in lk])
                                  for lk in lookups])
@@ -74,6 +76,7 @@ def test_pooled_ranker_replays_reference(P, golden_dir, which):
         assert rk.cache.lru_keys() == [_dev_key(k) for k in rec["per_batch_lru"][bi]], bi
         assert rk.cache.used_bytes == rec["per_batch_used"][bi]
     assert rk.cache.eviction_log == [_dev_key(k) for k in rec["evictions"]]
+    print(rec["name"], "parallel put calls:", rk.cache._scalars()["n_par_puts"], "of", len(rec["batches"]))
 
 
 def test_pooled_api_matches_reference(P, golden_dir):
@@ -117,3 +120,50 @@ def test_pooled_result_cache_short_circuits(P):
     assert np.array_equal(r1[0].vectors[0], r2[0].vectors[0])
     assert r2[0].cache_hits == 4 and r2[0].pushdown_groups == 0 and r2[0].raw_rows == 0
     assert rk.batch_metrics[-1].subrequests == 0
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_parallel_puts_equal_sequential(P, seed):
+    """Closed-form parallel pooled_put (uniform size) == the ordered loop:
+    random put streams with many re-puts, pre-filled caches and evictions."""
+    from paper_2410_12794_b200.cache import AdaptiveCache
+    rng = np.random.default_rng(seed)
+    D = 16
+    budget = 64 * int(rng.integers(50, 400))
+    caches = [AdaptiveCache(budget, pooled_results=True, record_evictions=True, max_dim=D) for _ in range(2)]
+    caches[1].set_parallel_offers(False)
+    dev = torch.device("cuda")
+    par_calls = []
+    for step in range(12):
+        n = int(rng.integers(1, 600))
+        universe = int(rng.integers(5, 2000))
+        ids = rng.integers(0, universe, n)
+        if step % 4 != 3:  # keys resident at call start force the ordered loop; mostly avoid them
+            ids = ids + (step + 1) * 1_000_000
+        ka = torch.from_numpy((ids.astype(np.uint64) * np.uint64(2654435761) | np.uint64(1 << 63)).view(np.int64))
+        kb = torch.from_numpy(ids.astype(np.int64) * 7 + 1)
+        rows = torch.from_numpy(rng.standard_normal((n, D)).astype(np.float32)).to(dev)
+        row_key = int(rng.integers(0, 50))
+        for c in caches:
+            c.pooled_put_many(ka.to(dev), kb.to(dev), rows, D * 4)
+            if step % 3 == 1:  # a row offer in between (mixed keyspaces)
+                c.offer(0, row_key, np.ones(D, np.float32))
+        s0, s1 = caches[0]._scalars(), caches[1]._scalars()
+        for k in ("used", "tick", "entries", "err"):
+            assert s0[k] == s1[k], (step, k)
+        assert caches[0].lru_entries() == caches[1].lru_entries(), step
+        assert caches[0].eviction_log == caches[1].eviction_log
+        par_calls.append(s0["n_par_puts"])
+        keys = [k for k, _, _ in caches[0].lru_entries() if k[0] == "pooled"]
+        if keys:
+            ka_l = torch.tensor([k[1] - (1 << 64) for k in keys], dtype=torch.int64, device=dev)
+            outs = []
+            for c in caches:
+                out = torch.zeros((len(keys), D), dtype=torch.float32, device=dev)
+                slot = torch.empty(len(keys), dtype=torch.int32, device=dev)
+                c._L.fx_cache_lookup(c._h, ka_l.data_ptr(), len(keys), out.data_ptr(), D, slot.data_ptr(), None)
+                assert bool((slot >= 0).all())
+                outs.append(out.cpu())
+            assert torch.equal(outs[0], outs[1])
+    assert caches[1]._scalars()["n_par_puts"] == 0
+    assert par_calls[-1] > 0  # the closed form resolved at least some calls
