@@ -129,6 +129,12 @@ int fx_combine(const void *const *partials, int32_t partial_is_f32, const int32_
                int64_t p_stride, const int64_t *raw_offsets, const float *raw_rows,
                int64_t n_bags, int32_t dim, int32_t op, const int32_t *ops,
                float *out, int64_t out_stride, int32_t *err_code, void *stream);
+/* fx_combine with raw vectors given as row pointers (raw_ptrs[r], e.g. rows
+ * in a peer GPU's shard read over NVLink) instead of a packed raw_rows array */
+int fx_combine_ptr(const void *const *partials, int32_t partial_is_f32, const int32_t *const *counts, int32_t n_src,
+                   int64_t p_stride, const int64_t *raw_offsets, const float *const *raw_ptrs, int64_t n_bags,
+                   int32_t dim, int32_t op, const int32_t *ops, float *out, int64_t out_stride, int32_t *err_code,
+                   void *stream);
 
 /* ---- K1: range routing (routing.py:87-97 resolve_many, 117-148) ---------
  * For occurrence i of a bag of table t:
@@ -290,6 +296,22 @@ int fx_rw_push(const int64_t *route_off, const int64_t *starts, const int32_t *o
                const void *indices, int32_t idx_type, const int64_t *offsets, int64_t n_bags, int32_t W,
                int32_t *counts, int64_t *scan, int32_t *const *dst_idx, int64_t *const *dst_offs, void *ws,
                size_t *ws_bytes, void *stream);
+/* planned row-wise push (pooling.py:88-100 plan_hierarchical per (bag,
+ * rank), ranker.py:263-301): counts as fx_rw_push; a (bag, rank) group of
+ * >= threshold indices is pushed to the owner (pushdown, its counts entry
+ * kept for K5), a smaller group is RAW-FETCHED: its count is zeroed and each
+ * of its indices gets raw_ptr[raw_off[b] + k] (position order within the bag)
+ * = the row's address in the owning shard, shard_base[sid] + (idx -
+ * starts[sid]) * ld — an IPC-mapped peer pointer for other ranks' shards,
+ * read by fx_combine_ptr over NVLink. raw_off: int64[n_bags+1]; raw_ptr:
+ * capacity nnz; counters (optional): int32[3][n_bags] = pushdown_groups,
+ * pushdown_rows, raw_rows per bag. workspace: query with ws == NULL. */
+int fx_rw_push_planned(const int64_t *route_off, const int64_t *starts, const int32_t *owners, const int64_t *nrows,
+                       const int32_t *bag_table, const void *indices, int32_t idx_type, const int64_t *offsets,
+                       int64_t n_bags, int32_t W, int32_t threshold, int32_t *counts, int64_t *scan,
+                       int32_t *const *dst_idx, int64_t *const *dst_offs, const float *const *shard_base, int64_t ld,
+                       int64_t *raw_off, const float **raw_ptr, int32_t *counters, void *ws, size_t *ws_bytes,
+                       void *stream);
 /* one-block barrier: release-store `epoch` into peer_flags[r][rank] for every
  * rank r (system scope, after a system fence), then acquire-spin until
  * my_flags[r] >= epoch for every r. peer_flags is a DEVICE array of `world`

@@ -179,6 +179,132 @@ __global__ void k_rw_push_offsets(const int64_t *scan, int64_t n_bags, int W, in
   if (sysfence) __threadfence_system();
 }
 
+// ---- planned row-wise push (pooling.py:88-100 plan_hierarchical per (bag, rank))
+// thread per bag: a group of >= threshold indices is pushed down (kept in
+// counts), a smaller one is raw-fetched (its count is zeroed so the push and
+// the K5 partial lookup skip it); raw_cnt[b] = raw rows of bag b; counters
+// [3][n_bags] = (pushdown_groups, pushdown_rows, raw_rows) (ranker.py:281-293).
+__global__ void k_rw_plan(int32_t *counts, int64_t n_bags, int W, int32_t threshold, int32_t *raw_cnt,
+                          int32_t *counters) {
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < n_bags; b += (int64_t)gridDim.x * blockDim.x) {
+    int pg = 0, pr = 0, rr = 0;
+    for (int d = 0; d < W; ++d) {
+      const int64_t i = (int64_t)d * n_bags + b;
+      const int c = counts[i];
+      if (c <= 0) continue;
+      if (c >= threshold) {
+        ++pg;
+        pr += c;
+      } else {
+        rr += c;
+        counts[i] = 0;
+      }
+    }
+    raw_cnt[b] = rr;
+    if (counters) {
+      counters[b] = pg;
+      counters[n_bags + b] = pr;
+      counters[2 * n_bags + b] = rr;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) raw_cnt[n_bags] = 0;
+}
+
+__device__ __forceinline__ int route_shard(const int64_t *route_off, const int64_t *starts, int t, int64_t idx) {
+  int64_t lo = route_off[t], hi = route_off[t + 1];
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (starts[mid] <= idx) lo = mid + 1; else hi = mid;
+  }
+  return static_cast<int>(lo > route_off[t] ? lo - 1 : route_off[t]);
+}
+
+// one warp per bag, indices in position order: raw-fetched ones (their
+// (bag, rank) group was zeroed by k_rw_plan) get the address of their row in
+// the owning shard — a peer (IPC-mapped) pointer for other ranks' shards, read
+// later by K5 over NVLink (the PlanMode.RAW_FETCH / RDMA-read analogue).
+template <typename IdxT>
+__global__ void __launch_bounds__(256) k_rw_raw(const int64_t *route_off, const int64_t *starts,
+                                                const int32_t *owners, const int64_t *nrows,
+                                                const int32_t *bag_table, const IdxT *indices,
+                                                const int64_t *offsets, int64_t n_bags, const int32_t *counts,
+                                                const int64_t *raw_off, const float *const *shard_base, int64_t ld,
+                                                const float **raw_ptr) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t b = warp; b < n_bags; b += nw) {
+    const int64_t r0 = raw_off[b];
+    if (raw_off[b + 1] == r0) continue;
+    const int t = bag_table[b];
+    const int64_t beg = offsets[b], end = offsets[b + 1];
+    int64_t run = r0;
+    for (int64_t c0 = beg; c0 < end; c0 += 32) {
+      bool raw = false;
+      const float *ptr = nullptr;
+      if (c0 + lane < end) {
+        int64_t idx = static_cast<int64_t>(indices[c0 + lane]);
+        const int sid = route_shard(route_off, starts, t, idx);
+        const int d = owners[sid];
+        raw = counts[(int64_t)d * n_bags + b] == 0;
+        // invalid indices (flagged by ingress validation) are clamped into the shard
+        const int64_t lo = starts[sid];
+        const int64_t hi = sid + 1 < route_off[t + 1] ? starts[sid + 1] : nrows[t];
+        idx = idx < lo ? lo : (idx >= hi ? hi - 1 : idx);
+        ptr = shard_base[sid] + (idx - lo) * ld;
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, raw);
+      if (raw) raw_ptr[run + __popc(m & lt)] = ptr;
+      run += __popc(m);
+    }
+  }
+}
+
+// k_rw_push restricted to pushed-down groups (counts[d][b] > 0 after the plan)
+template <typename IdxT>
+__global__ void __launch_bounds__(256) k_rw_push_planned(const int64_t *route_off, const int64_t *starts,
+                                                         const int32_t *owners, const int32_t *bag_table,
+                                                         const IdxT *indices, const int64_t *offsets, int64_t n_bags,
+                                                         int W, const int32_t *counts, const int64_t *scan,
+                                                         int32_t *const *dst_idx) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t b = warp; b < n_bags; b += nw) {
+    const int t = bag_table[b];
+    const int64_t beg = offsets[b], end = offsets[b + 1];
+    int64_t run[32];
+    unsigned pushed = 0;
+#pragma unroll
+    for (int d = 0; d < 32; ++d) {
+      run[d] = d < W ? scan[(int64_t)d * n_bags + b] - scan[(int64_t)d * n_bags] : 0;
+      if (d < W && counts[(int64_t)d * n_bags + b] > 0) pushed |= 1u << d;
+    }
+    if (!pushed) continue;
+    for (int64_t c0 = beg; c0 < end; c0 += 32) {
+      const bool on = c0 + lane < end;
+      int64_t idx = 0;
+      int my_d = -1;
+      if (on) {
+        idx = static_cast<int64_t>(indices[c0 + lane]);
+        my_d = route_dest(route_off, starts, owners, t, idx);
+        if (!((pushed >> my_d) & 1u)) my_d = -1;
+      }
+#pragma unroll
+      for (int d = 0; d < 32; ++d) {
+        if (d < W && ((pushed >> d) & 1u)) {
+          const unsigned m = __ballot_sync(0xffffffffu, my_d == d);
+          if (my_d == d) dst_idx[d][run[d] + __popc(m & lt)] = static_cast<int32_t>(idx);
+          run[d] += __popc(m);
+        }
+      }
+    }
+  }
+  __threadfence_system();
+}
+
 }  // namespace fx
 
 using namespace fx;
@@ -278,6 +404,66 @@ int fx_rw_push(const int64_t *route_off, const int64_t *starts, const int32_t *o
                                              true);
   k_rw_push_offsets<<<grid_for((int64_t)W * (n_bags + 1), 256), 256, 0, st>>>(scan, n_bags, W, dst_offs, true);
   FX_LAUNCH_CHECK("fx_rw_push");
+  return FX_OK;
+}
+
+int fx_rw_push_planned(const int64_t *route_off, const int64_t *starts, const int32_t *owners, const int64_t *nrows,
+                       const int32_t *bag_table, const void *indices, int32_t idx_type, const int64_t *offsets,
+                       int64_t n_bags, int32_t W, int32_t threshold, int32_t *counts, int64_t *scan,
+                       int32_t *const *dst_idx, int64_t *const *dst_offs, const float *const *shard_base, int64_t ld,
+                       int64_t *raw_off, const float **raw_ptr, int32_t *counters, void *ws, size_t *ws_bytes,
+                       void *stream) {
+  if (W < 1 || W > 32 || n_bags < 0 || threshold < 2) {
+    set_error("fx_rw_push_planned: bad arguments (threshold must be >= 2)");
+    return FX_E_CONFIG;
+  }
+  const int64_t n = static_cast<int64_t>(W) * n_bags + 1;
+  size_t c1 = 0, c2 = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, c1, (const int32_t *)nullptr, (int64_t *)nullptr, static_cast<int>(n));
+  cub::DeviceScan::ExclusiveSum(nullptr, c2, (const int32_t *)nullptr, (int64_t *)nullptr,
+                                static_cast<int>(n_bags + 1));
+  const size_t cub_bytes = ((c1 > c2 ? c1 : c2) + 255) & ~size_t(255);
+  const size_t need = cub_bytes + static_cast<size_t>(n_bags + 1) * 4;
+  if (ws == nullptr) {
+    *ws_bytes = need;
+    return FX_OK;
+  }
+  if (*ws_bytes < need) {
+    set_error("fx_rw_push_planned: workspace too small");
+    return FX_E_CONFIG;
+  }
+  int32_t *raw_cnt = reinterpret_cast<int32_t *>(static_cast<char *>(ws) + cub_bytes);
+  size_t cb = cub_bytes;
+  cudaStream_t st = as_stream(stream);
+  cudaMemsetAsync(counts, 0, n * sizeof(int32_t), st);
+  const int grid = grid_for(n_bags * 32, 256);
+  if (idx_type == FX_IDX_I32)
+    k_rw_count<int32_t><<<grid, 256, 0, st>>>(route_off, starts, owners, bag_table,
+                                              static_cast<const int32_t *>(indices), offsets, n_bags, W, counts);
+  else
+    k_rw_count<int64_t><<<grid, 256, 0, st>>>(route_off, starts, owners, bag_table,
+                                              static_cast<const int64_t *>(indices), offsets, n_bags, W, counts);
+  k_rw_plan<<<grid_for(n_bags + 1, 256), 256, 0, st>>>(counts, n_bags, W, threshold, raw_cnt, counters);
+  cub::DeviceScan::ExclusiveSum(ws, cb, raw_cnt, raw_off, static_cast<int>(n_bags + 1), st);
+  cb = cub_bytes;
+  cub::DeviceScan::ExclusiveSum(ws, cb, counts, scan, static_cast<int>(n), st);
+  if (idx_type == FX_IDX_I32) {
+    k_rw_raw<int32_t><<<grid, 256, 0, st>>>(route_off, starts, owners, nrows, bag_table,
+                                            static_cast<const int32_t *>(indices), offsets, n_bags, counts, raw_off,
+                                            shard_base, ld, raw_ptr);
+    k_rw_push_planned<int32_t><<<grid, 256, 0, st>>>(route_off, starts, owners, bag_table,
+                                                     static_cast<const int32_t *>(indices), offsets, n_bags, W,
+                                                     counts, scan, dst_idx);
+  } else {
+    k_rw_raw<int64_t><<<grid, 256, 0, st>>>(route_off, starts, owners, nrows, bag_table,
+                                            static_cast<const int64_t *>(indices), offsets, n_bags, counts, raw_off,
+                                            shard_base, ld, raw_ptr);
+    k_rw_push_planned<int64_t><<<grid, 256, 0, st>>>(route_off, starts, owners, bag_table,
+                                                     static_cast<const int64_t *>(indices), offsets, n_bags, W,
+                                                     counts, scan, dst_idx);
+  }
+  k_rw_push_offsets<<<grid_for((int64_t)W * (n_bags + 1), 256), 256, 0, st>>>(scan, n_bags, W, dst_offs, true);
+  FX_LAUNCH_CHECK("fx_rw_push_planned");
   return FX_OK;
 }
 

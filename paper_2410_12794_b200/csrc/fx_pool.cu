@@ -252,7 +252,8 @@ __global__ void __launch_bounds__(256) k_gather_rows(const float *__restrict__ t
 __global__ void __launch_bounds__(256) k_combine(const void *const *__restrict__ partials, int p_f32,
                                                  const int32_t *const *__restrict__ counts, int n_src,
                                                  int64_t p_stride, const int64_t *__restrict__ raw_offsets,
-                                                 const float *__restrict__ raw_rows, int64_t n_bags, int dim,
+                                                 const float *__restrict__ raw_rows,
+                                                 const float *const *__restrict__ raw_ptrs, int64_t n_bags, int dim,
                                                  int op, const int32_t *__restrict__ ops, float *__restrict__ out,
                                                  int64_t out_stride, int32_t *err_code) {
   const int lane = threadIdx.x & 31;
@@ -278,7 +279,10 @@ __global__ void __launch_bounds__(256) k_combine(const void *const *__restrict__
           acc += p_f32 ? static_cast<double>(static_cast<const float *>(partials[s])[b * p_stride + c])
                        : static_cast<const double *>(partials[s])[b * p_stride + c];
       }
-      for (int64_t r = r0; r < r1; ++r) acc += static_cast<double>(raw_rows[r * dim + c]);
+      if (raw_ptrs)
+        for (int64_t r = r0; r < r1; ++r) acc += static_cast<double>(raw_ptrs[r][c]);
+      else
+        for (int64_t r = r0; r < r1; ++r) acc += static_cast<double>(raw_rows[r * dim + c]);
       if (bop == FX_OP_MEAN && total > 0) acc /= static_cast<double>(total);
       out[b * out_stride + c] = __double2float_rn(acc);
     }
@@ -482,9 +486,25 @@ int fx_combine(const void *const *partials, int32_t partial_is_f32, const int32_
   }
   if (n_bags == 0) return FX_OK;
   k_combine<<<grid_for(n_bags * 32, 256), 256, 0, as_stream(stream)>>>(
-      partials, partial_is_f32, counts, n_src, p_stride, raw_offsets, raw_rows, n_bags, dim, op, ops, out, out_stride,
-      err_code);
+      partials, partial_is_f32, counts, n_src, p_stride, raw_offsets, raw_rows, nullptr, n_bags, dim, op, ops, out,
+      out_stride, err_code);
   FX_LAUNCH_CHECK("fx_combine");
+  return FX_OK;
+}
+
+int fx_combine_ptr(const void *const *partials, int32_t partial_is_f32, const int32_t *const *counts, int32_t n_src,
+                   int64_t p_stride, const int64_t *raw_offsets, const float *const *raw_ptrs, int64_t n_bags,
+                   int32_t dim, int32_t op, const int32_t *ops, float *out, int64_t out_stride, int32_t *err_code,
+                   void *stream) {
+  if (dim < 1 || n_src < 0 || n_bags < 0) {
+    set_error("fx_combine_ptr: bad arguments");
+    return FX_E_CONFIG;
+  }
+  if (n_bags == 0) return FX_OK;
+  k_combine<<<grid_for(n_bags * 32, 256), 256, 0, as_stream(stream)>>>(
+      partials, partial_is_f32, counts, n_src, p_stride, raw_offsets, nullptr, raw_ptrs, n_bags, dim, op, ops, out,
+      out_stride, err_code);
+  FX_LAUNCH_CHECK("fx_combine_ptr");
   return FX_OK;
 }
 

@@ -66,7 +66,10 @@ def rowwise_placement(table_rows, world: int):
 class FlexOps:
     """Device compute of the sharded path, all in libflexemb kernels."""
 
-    def __init__(self, metas: dict, placement, seed: int, rank: int, feature_tables, feature_ops, B: int, device):
+    def __init__(self, metas: dict, placement, seed: int, rank: int, feature_tables, feature_ops, B: int, device,
+                 ipc_shards: bool = False):
+        """`ipc_shards`: allocate the local shards with cudaMalloc (fx_dev_alloc)
+        so peers can map them (raw fetch over NVLink)."""
         from . import _lib
         from .store import table_block_device
         self._lib = _lib
@@ -76,19 +79,27 @@ class FlexOps:
         self.ftab = tuple(feature_tables)
         self.fops = tuple(feature_ops)
         self.local = {}
+        self.shard_bufs = {}
         for sp in placement:
             if sp.server_id == rank:
-                data = table_block_device(seed, sp.table_id, metas[sp.table_id].dim, sp.start, sp.end,
-                                          device=self.device)
+                D = metas[sp.table_id].dim
+                out = None
+                if ipc_shards:
+                    buf = DevBuffer((sp.end - sp.start) * D * 4)
+                    self.shard_bufs[sp.table_id] = buf
+                    out = _cai_tensor(buf.ptr, (sp.end - sp.start, D), torch.float32, self.device)
+                data = table_block_device(seed, sp.table_id, D, sp.start, sp.end, device=self.device, out=out)
                 self.local[sp.table_id] = (data, sp.start, sp.end)
         n_t = max(metas) + 1
         route_off = np.zeros(n_t + 1, np.int64)
         starts, owners = [], []
+        self.shard_list = []  # routing order (table, start): global shard ids
         for t in range(n_t):
             sh = sorted((s for s in placement if s.table_id == t), key=lambda s: s.start)
             route_off[t + 1] = route_off[t] + len(sh)
             starts += [s.start for s in sh]
             owners += [s.server_id for s in sh]
+            self.shard_list += sh
         nrows = np.array([metas[t].num_rows if t in metas else 0 for t in range(n_t)], np.int64)
         dev = self.device
         self.route_off = torch.from_numpy(route_off).to(dev)
@@ -394,10 +405,21 @@ class P2PShardedLookup:
 
     def __init__(self, metas, placement, seed: int, feature_tables, feature_ops, batch_size: int, rank: int,
                  world: int, device, group=None, mode: str = "tablewise", max_nnz: int | None = None,
-                 replicated_tables=(), partial_dtype: str = "f64"):
+                 replicated_tables=(), partial_dtype: str = "f64", pushdown_threshold: int | None = None):
         """`replicated_tables` (table-wise mode): tables held in full by every
         rank and pooled locally for the rank's own batch (no exchange); they
-        must not appear in `placement`. The other tables are table-sharded."""
+        must not appear in `placement`. The other tables are table-sharded.
+
+        `pushdown_threshold` (row-wise mode): the reference's hierarchical
+        plan (pooling.py:88-100, ranker.py:263-301). A (bag, rank) group of at
+        least `threshold` indices is pushed down to its owner (one partial);
+        a smaller group is raw-fetched: the requester's K5 reads its rows
+        straight from the owner's shard over NVLink (peer loads through
+        IPC-mapped shard memory, the analogue of the reference's RDMA READ)
+        and combines them after the partials in position order, as
+        combine_partials does (pooling.py:103-123). Per-bag counters
+        (pushdown_groups, pushdown_rows, raw_rows) come with every result
+        (`counters()`). None pushes every group down."""
         from . import _lib
         from .pooling import op_code
         from .store import table_block_device
@@ -410,6 +432,12 @@ class P2PShardedLookup:
         self.pesz = 8 if partial_dtype == "f64" else 4
         if self.replicated and mode != "tablewise":
             raise ConfigError("replicated tables are supported in table-wise mode only")
+        self.threshold = pushdown_threshold
+        if pushdown_threshold is not None:
+            if mode != "rowwise":
+                raise ConfigError("pushdown_threshold applies to row-wise mode (table-wise bags are one group)")
+            if pushdown_threshold < 2:
+                raise ConfigError(f"pushdown threshold must be >= 2, got {pushdown_threshold}")
         if mode not in ("tablewise", "rowwise"):
             raise ConfigError(f"unknown sharding mode {mode!r}")
         self.metas = {m.table_id: m for m in metas}
@@ -424,7 +452,8 @@ class P2PShardedLookup:
         self.D = D = dims.pop()
         B, F, W = self.B, self.F, world
         self.n_bags = n_bags = B * F
-        self.ops = FlexOps(self.metas, placement, seed, rank, self.ftab, self.fops, B, self.device)
+        self.ops = FlexOps(self.metas, placement, seed, rank, self.ftab, self.fops, B, self.device,
+                           ipc_shards=pushdown_threshold is not None)
         for t in self.replicated:
             if any(sp.table_id == t for sp in placement):
                 raise ConfigError(f"replicated table {t} must not be in the sharded placement")
@@ -477,8 +506,17 @@ class P2PShardedLookup:
             self.t_counts = [torch.zeros(W * n_bags + 1, dtype=torch.int32, device=dev) for _ in (0, 1)]
             self.t_scan = [torch.zeros(W * n_bags + 1, dtype=torch.int64, device=dev) for _ in (0, 1)]
             need = ctypes.c_size_t(0)
-            _lib.check(_lib.lib.fx_rw_push(None, None, None, None, None, 0, None, n_bags, W, None, None, None, None,
-                                           None, ctypes.byref(need), None), "rw push ws")
+            if pushdown_threshold is None:
+                _lib.check(_lib.lib.fx_rw_push(None, None, None, None, None, 0, None, n_bags, W, None, None, None,
+                                               None, None, ctypes.byref(need), None), "rw push ws")
+            else:
+                _lib.check(_lib.lib.fx_rw_push_planned(None, None, None, None, None, None, 0, None, n_bags, W,
+                                                       int(pushdown_threshold), None, None, None, None, None, 0,
+                                                       None, None, None, None, ctypes.byref(need), None),
+                           "rw push ws")
+                self.t_raw_off = [torch.zeros(n_bags + 1, dtype=torch.int64, device=dev) for _ in (0, 1)]
+                self.t_raw_ptr = [torch.zeros(max(self.max_nnz, 1), dtype=torch.int64, device=dev) for _ in (0, 1)]
+                self.t_counters = [torch.zeros((3, n_bags), dtype=torch.int32, device=dev) for _ in (0, 1)]
             self.t_ws = [torch.empty(max(need.value, 1), dtype=torch.uint8, device=dev) for _ in (0, 1)]
         torch.cuda.synchronize(dev)
         mine = [self.b_idx.handle(), self.b_offs.handle(), self.b_out.handle(), self.b_flags.handle()]
@@ -495,6 +533,20 @@ class P2PShardedLookup:
                 ptrs.append(opened)
         self.peer_ptrs = ptrs
         self.t_peer_flags = torch.tensor([p[3] for p in ptrs], dtype=torch.int64, device=dev)
+        if pushdown_threshold is not None:
+            # every shard's base address as seen from this rank (raw fetch targets)
+            mine_sh = {t: buf.handle() for t, buf in self.ops.shard_bufs.items()}
+            all_sh = [None] * W
+            dist.all_gather_object(all_sh, mine_sh, group=group)
+            bases = []
+            for sp in self.ops.shard_list:
+                if sp.server_id == rank:
+                    bases.append(self.ops.local[sp.table_id][0].data_ptr())
+                else:
+                    p_ = _ipc_open(all_sh[sp.server_id][sp.table_id])
+                    self._opened.append(p_)
+                    bases.append(p_)
+            self.t_shard_base = torch.tensor(bases, dtype=torch.int64, device=dev)
         self.t_timeout = torch.zeros(1, dtype=torch.int32, device=dev)
         self.epoch = 0
         from .store import make_segments
@@ -598,6 +650,19 @@ class P2PShardedLookup:
             L.check(L.lib.fx_push_csr(indices.data_ptr(), L.idx_type_of(indices), offsets.data_ptr(), B, F,
                                       self.t_feat_owner.data_ptr(), self.t_feat_pos.data_ptr(),
                                       self.t_dst_idx[p].data_ptr(), self.t_dst_offs[p].data_ptr(), 1, sp), "push")
+        elif self.threshold is not None:
+            wsb = ctypes.c_size_t(self.t_ws[p].numel())
+            L.check(L.lib.fx_rw_push_planned(o.route_off.data_ptr(), o.starts.data_ptr(), o.owners.data_ptr(),
+                                             o.nrows.data_ptr(), o.bag_table.data_ptr(), indices.data_ptr(),
+                                             L.idx_type_of(indices), offsets.data_ptr(), self.n_bags, W,
+                                             int(self.threshold), self.t_counts[p].data_ptr(),
+                                             self.t_scan[p].data_ptr(), self.t_dst_idx[p].data_ptr(),
+                                             self.t_dst_offs[p].data_ptr(), self.t_shard_base.data_ptr(), self.D,
+                                             self.t_raw_off[p].data_ptr(), self.t_raw_ptr[p].data_ptr(),
+                                             self.t_counters[p].data_ptr(), self.t_ws[p].data_ptr(),
+                                             ctypes.byref(wsb), sp), "rw push planned")
+            # k_route, k_rw_count, k_rw_plan, k_rw_raw, k_rw_push_planned, k_rw_push_offsets
+            self.launches += 6
         else:
             wsb = ctypes.c_size_t(self.t_ws[p].numel())
             L.check(L.lib.fx_rw_push(o.route_off.data_ptr(), o.starts.data_ptr(), o.owners.data_ptr(),
@@ -629,10 +694,25 @@ class P2PShardedLookup:
         L = self._lib
         B, F, D, W = self.B, self.F, self.D, self.world
         self.launches += 1
-        L.check(L.lib.fx_combine(self._pp[p].data_ptr(), 1 if self.pesz == 4 else 0, self._cptr[p].data_ptr(), W, D,
-                                 None, None, self.n_bags, D, 0, self.bag_ops.data_ptr(), self._tmp[p].data_ptr(), D,
-                                 None, L.stream_ptr()), "combine")
+        self._last_set = p
+        if self.threshold is not None:
+            L.check(L.lib.fx_combine_ptr(self._pp[p].data_ptr(), 1 if self.pesz == 4 else 0, self._cptr[p].data_ptr(),
+                                         W, D, self.t_raw_off[p].data_ptr(), self.t_raw_ptr[p].data_ptr(), self.n_bags,
+                                         D, 0, self.bag_ops.data_ptr(), self._tmp[p].data_ptr(), D, None,
+                                         L.stream_ptr()), "combine")
+        else:
+            L.check(L.lib.fx_combine(self._pp[p].data_ptr(), 1 if self.pesz == 4 else 0, self._cptr[p].data_ptr(), W,
+                                     D, None, None, self.n_bags, D, 0, self.bag_ops.data_ptr(), self._tmp[p].data_ptr(),
+                                     D, None, L.stream_ptr()), "combine")
         return self._tmp[p].view(F, B, D).transpose(0, 1).reshape(B, F * D)
+
+    def counters(self) -> torch.Tensor:
+        """Per-bag (pushdown_groups, pushdown_rows, raw_rows) of the last result,
+        int32 [3, F*B] in table-major bag order (ranker.py:281-293; row-wise
+        mode with a pushdown threshold)."""
+        if self.threshold is None:
+            raise ConfigError("counters need pushdown_threshold (row-wise mode)")
+        return self.t_counters[self._last_set]
 
     def _check(self):
         self.ops.check()

@@ -37,6 +37,11 @@ def main():
         placement = [ShardSpec(big[s.table_id], s.start, s.end, s.server_id) for s in sub]
         sl = P2PShardedLookup(metas, placement, 0, tuple(range(len(rows))), ops, B, rank, world, f"cuda:{local}",
                               mode=mode, replicated_tables=repl)
+    elif exchange in ("p2pthr", "p2pthr32"):
+        # reference plan: groups < 2 raw-fetched over NVLink, larger ones pushed down
+        sl = P2PShardedLookup(metas, placement, 0, tuple(range(len(rows))), ops, B, rank, world, f"cuda:{local}",
+                              mode=mode, partial_dtype="f32" if exchange == "p2pthr32" else "f64",
+                              pushdown_threshold=2)
     elif exchange == "p2pf32":
         sl = P2PShardedLookup(metas, placement, 0, tuple(range(len(rows))), ops, B, rank, world, f"cuda:{local}",
                               mode=mode, partial_dtype="f32")
@@ -53,13 +58,35 @@ def main():
     if pipelined:
         dev_b = [(torch.from_numpy(hb.indices).cuda(), torch.from_numpy(hb.offsets).cuda()) for hb in hbs]
         torch.cuda.synchronize()
-        outs = [o.cpu().numpy() for o in sl.stream(dev_b)]
+        outs, cnts = [], []
+        for o in sl.stream(dev_b):
+            outs.append(o.cpu().numpy())
+            if exchange.startswith("p2pthr"):
+                cnts.append(sl.counters().cpu().numpy())
+    planned = exchange.startswith("p2pthr")
+    hier_exact = cnt_bad = 0
+    if planned:
+        pl = O.Placement.from_specs({m.table_id: m.num_rows for m in metas},
+                                    [(sp.table_id, sp.start, sp.end, sp.server_id) for sp in placement])
+        po = O.PipelineOracle(0, {m.table_id: D for m in metas}, pl, threshold=2)
     for it in range(4):
         hb = hbs[it]
         if pipelined:
             out = outs[it]
         else:
             out = sl.lookup(torch.from_numpy(hb.indices).cuda(), torch.from_numpy(hb.offsets).cuda()).cpu().numpy()
+        if planned:
+            cnt = cnts[it] if pipelined else sl.counters().cpu().numpy()
+            nb = len(rows) * B
+            bb = O.BagBatch(hb.offsets.astype(np.int64), hb.indices.astype(np.int64),
+                            np.repeat(np.arange(len(rows)), B), [ops[f] for f in range(len(rows)) for _ in range(B)],
+                            np.tile(np.arange(B), len(rows)), np.repeat(np.arange(len(rows)), B), B)
+            vecs, counters, _ = po.run(bb)
+            for b in range(nb):
+                f, s_ = divmod(b, B)
+                cnt_bad += tuple(int(x) for x in cnt[:, b]) != counters[b][1:]
+                if exchange == "p2pthr32":  # f32 partials + raw rows: the reference's own combine
+                    hier_exact += vecs[b].tobytes() != out[s_, f * D:(f + 1) * D].tobytes()
         for f in range(len(rows)):
             for s in range(B):
                 b = f * B + s
@@ -68,12 +95,14 @@ def main():
                 worst = max(worst, O.tolerance_ratio(ref, got))
                 exact += ref.tobytes() == got.tobytes()
                 n += 1
-    t = torch.tensor([worst, float(n - exact)], device="cuda", dtype=torch.float64)
+    t = torch.tensor([worst, float(n - exact), float(cnt_bad), float(hier_exact)], device="cuda",
+                     dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     if rank == 0:
         print(f"SHARDED {mode} {exchange}{'-pipe' if pipelined else ''} world={world} worst_tolerance_ratio={t[0].item():.4f} "
-              f"max_non_bit_exact_bags={int(t[1].item())} bags_per_rank={n}", flush=True)
-    ok = t[0].item() <= 1.0
+              f"max_non_bit_exact_bags={int(t[1].item())} bags_per_rank={n} counter_mismatches={int(t[2].item())} "
+              f"non_bit_exact_vs_reference_combine={int(t[3].item())}", flush=True)
+    ok = t[0].item() <= 1.0 and t[2].item() == 0 and t[3].item() == 0
     dist.destroy_process_group()
     sys.exit(0 if ok else 1)
 

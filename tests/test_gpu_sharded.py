@@ -50,3 +50,22 @@ def test_sharded_rowwise_f32_partials():
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "SHARDED rowwise p2pf32" in r.stdout
+
+
+@pytest.mark.parametrize("exchange", ["p2pthr", "p2pthr32", "p2pthr32-pipe"])
+def test_sharded_rowwise_planned_raw_fetch(exchange):
+    """Reference plan (threshold 2) in row-wise mode: singleton (bag, rank)
+    groups raw-fetched over NVLink by the requester, larger ones pushed down.
+    Per-bag counters equal the reference plan's; with f32 partials the result
+    is bit-identical to the reference's hierarchical combine_partials."""
+    n = torch.cuda.device_count() if torch.cuda.is_available() else 0
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    w = min(n, 4)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={w}",
+           "--master-addr", "127.0.0.1", "--master-port", "29574", os.path.join(ROOT, "scripts", "sharded_check.py"),
+           "rowwise", exchange]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert f"SHARDED rowwise {exchange}" in r.stdout
+    assert "counter_mismatches=0" in r.stdout and "non_bit_exact_vs_reference_combine=0" in r.stdout
