@@ -209,6 +209,9 @@ def main():
     ap.add_argument("--replicate-rows", type=int, default=1_000_000,
                     help="N>1 table-wise: replicate tables with <= this many rows on every rank (hybrid "
                          "placement: small tables data-parallel, big tables table-sharded); 0 = pure table-wise")
+    ap.add_argument("--threshold", type=int, default=0,
+                    help="N>1 row-wise fused exchange: the reference's pushdown threshold (groups below it are "
+                         "raw-fetched over NVLink by the requester); 0 = push every group down")
     ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
                     help="N>1 pooled-result exchange: fused NVLink peer stores (p2p) or NCCL all-to-all")
     args = ap.parse_args()
@@ -411,7 +414,8 @@ def run_sharded(args, rank, world, local):
     if args.exchange == "p2p":
         max_nnz = int(max(int(hb.offsets[-1]) for hb in host_batches) * 1.05) + 1024
         sl = P2PShardedLookup(metas, placement, 0, tuple(range(F)), ("sum",) * F, B, rank, world, dev, mode=mode,
-                              replicated_tables=repl, max_nnz=max_nnz, partial_dtype=args.partial)
+                              replicated_tables=repl, max_nnz=max_nnz, partial_dtype=args.partial,
+                              pushdown_threshold=(args.threshold or None) if mode == "rowwise" else None)
     else:
         if repl:
             raise SystemExit("--replicate-rows needs --exchange p2p")
@@ -523,6 +527,8 @@ def run_sharded(args, rank, world, local):
                        "parallelism": f"{mode}-sharded x{world} ({args.exchange} exchange)"
                                       + (f", {len(repl)} small tables replicated" if repl else "")
                                       + (f", {args.partial} partials" if mode == "rowwise" else "")
+                                      + (f", pushdown threshold {args.threshold} (raw fetch over NVLink below)"
+                                         if mode == "rowwise" and args.threshold else "")
                                       + (", pipelined (depth 2)" if args.exchange == "p2p" and not args.sync else ""),
                        "l2": "inputs larger than L2 (1.18 GB algorithmic bytes per rank-batch)",
                        "init_store_s": round(init_s, 2)},

@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(256) k_gather_pool_generic(
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const int col = tile * TILE + k * 32 + lane;
-      if (col >= dim) continue;
+      if (col >= dim || (MODE != FX_OUT_F32 && cnt == 0)) continue;  // empty partial: absent, not stored
       if (MODE == FX_OUT_F32) {
         float *o = static_cast<float *>(segs[s].out) + orow * segs[s].out_stride;
         const double v = (segs[s].op == FX_OP_MEAN && cnt > 0) ? acc[k] / static_cast<double>(cnt) : acc[k];

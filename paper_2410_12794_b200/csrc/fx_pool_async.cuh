@@ -36,6 +36,10 @@ __device__ __forceinline__ void emit_bag(const fx_segment &sg, int64_t bag, int6
       *reinterpret_cast<float4 *>(o + col) = q;
     }
   } else if (MODE == FX_OUT_F32_PARTIAL) {
+    // an empty partial is absent (count 0, never read by K5): skip the store,
+    // which for row-wise shards is mostly a remote NVLink write
+    if (counts && lane == 0) counts[bag] = static_cast<int32_t>(cnt);
+    if (cnt == 0) return;
     float *o = static_cast<float *>(sg.out) + orow * sg.out_stride;
 #pragma unroll
     for (int k = 0; k < NCH; ++k) {
@@ -44,8 +48,9 @@ __device__ __forceinline__ void emit_bag(const fx_segment &sg, int64_t bag, int6
           make_float4(__double2float_rn(acc[k][0]), __double2float_rn(acc[k][1]), __double2float_rn(acc[k][2]),
                       __double2float_rn(acc[k][3]));
     }
-    if (counts && lane == 0) counts[bag] = static_cast<int32_t>(cnt);
   } else {
+    if (counts && lane == 0) counts[bag] = static_cast<int32_t>(cnt);
+    if (cnt == 0) return;
     double *o = static_cast<double *>(sg.out) + orow * sg.out_stride;
 #pragma unroll
     for (int k = 0; k < NCH; ++k) {
@@ -53,7 +58,6 @@ __device__ __forceinline__ void emit_bag(const fx_segment &sg, int64_t bag, int6
       *reinterpret_cast<double2 *>(o + col) = make_double2(acc[k][0], acc[k][1]);
       *reinterpret_cast<double2 *>(o + col + 2) = make_double2(acc[k][2], acc[k][3]);
     }
-    if (counts && lane == 0) counts[bag] = static_cast<int32_t>(cnt);
   }
 }
 

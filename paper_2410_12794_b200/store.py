@@ -131,7 +131,9 @@ def pool_csr_device(table: torch.Tensor, row_begin: int, row_end: int, indices: 
     n_bags = offsets.numel() - 1
     D = table.shape[1]
     if out is None:
-        out = torch.empty((n_bags, D), dtype=torch.float64 if partial else torch.float32, device=dev)
+        # partial mode leaves empty bags' rows unwritten (count 0 = partial absent)
+        out = (torch.zeros if partial else torch.empty)((n_bags, D), dtype=torch.float64 if partial else torch.float32,
+                                                        device=dev)
     seg = _lib.FxSegment(table.data_ptr(), row_begin, row_end, 0, n_bags, out.data_ptr(), out.stride(0),
                          table.stride(0), D, op_code(op))
     segs = make_segments([seg], dev)
