@@ -208,6 +208,18 @@ class HostLookup:
     def __init__(self, engine: LookupEngine):
         self.engine = engine
         self._out_host = {}
+        self._streams = {}
+
+    def _stream_state(self, depth: int) -> dict:
+        st = self._streams.get(depth)
+        if st is None:
+            dev = self.engine.device
+            st = {"streams": tuple(torch.cuda.Stream(dev) for _ in range(3)),
+                  "slots": [{"idx": None, "offs": None, "out": None, "host": None, "used": False, "batch": None,
+                             "ev_in": torch.cuda.Event(), "ev_cmp": torch.cuda.Event(),
+                             "ev_out": torch.cuda.Event()} for _ in range(depth)]}
+            self._streams[depth] = st
+        return st
 
     def lookup(self, batch_host: CsrBatch, out_host: torch.Tensor | None = None) -> torch.Tensor:
         eng = self.engine
@@ -228,57 +240,65 @@ class HostLookup:
         flight, ranker.py:161-168): yields one pinned host output per input
         batch, in order. H2D of batch i+1, K4 of batch i and D2H of batch i-1
         run concurrently on three streams (PCIe is full duplex), so steady
-        state is bound by the larger copy, not by their sum. A yielded tensor
-        is valid until the generator is advanced (its slot is then reused).
-        Validation errors are raised after the last batch."""
+        state is bound by the larger copy, not by their sum. Device staging,
+        outputs, pinned host outputs and events are allocated once per
+        (depth, output shape) and reused across calls, so the steady state
+        allocates nothing. A yielded tensor is valid until the generator is
+        advanced (its slot is then reused). Validation errors are raised
+        after the last batch."""
         eng = self.engine
         dev = eng.device
-        s_in, s_cmp, s_out = (torch.cuda.Stream(dev) for _ in range(3))
-        slots = [dict() for _ in range(depth)]
-        ev_in = [None] * depth
-        ev_cmp = [None] * depth
-        ev_out = [None] * depth
+        st = self._stream_state(depth)
+        s_in, s_cmp, s_out = st["streams"]
+        slots = st["slots"]
         pending = []
 
         def launch(bh, k):
             sl = slots[k]
+            nnz, nb = int(bh.indices.numel()), int(bh.offsets.numel())
+            B = bh.batch_size
+            odim = eng.out_dim(bh)
+            if (sl["idx"] is None or sl["idx"].numel() < nnz or sl["idx"].dtype != bh.indices.dtype
+                    or sl["offs"].numel() < nb or tuple(sl["out"].shape) != (B, odim)):
+                torch.cuda.synchronize(dev)  # (re)size the slot: nothing of it may still be in flight
+                sl["idx"] = torch.empty(max(nnz, 1) + nnz // 8, dtype=bh.indices.dtype, device=dev)
+                sl["offs"] = torch.empty(nb, dtype=torch.int64, device=dev)
+                sl["out"] = torch.empty((B, odim), dtype=torch.float32, device=dev)
+                sl["host"] = torch.empty((B, odim), dtype=torch.float32, pin_memory=True)
+                sl["used"] = False
             with torch.cuda.stream(s_in):
-                if ev_cmp[k] is not None:
-                    s_in.wait_event(ev_cmp[k])  # device inputs of slot k no longer read
-                sl["batch"] = bh.to(dev, non_blocking=True)
-                ev_in[k] = torch.cuda.Event()
-                ev_in[k].record(s_in)
+                if sl["used"]:
+                    s_in.wait_event(sl["ev_cmp"])  # the slot's device inputs are no longer read
+                sl["idx"][:nnz].copy_(bh.indices, non_blocking=True)
+                sl["offs"][:nb].copy_(bh.offsets, non_blocking=True)
+                sl["ev_in"].record(s_in)
             with torch.cuda.stream(s_cmp):
-                s_cmp.wait_event(ev_in[k])
-                if ev_out[k] is not None:
-                    s_cmp.wait_event(ev_out[k])  # device output of slot k already copied out
-                B = bh.batch_size
-                if "out" not in sl or sl["out"].shape[0] != B:
-                    sl["out"] = torch.empty((B, eng.out_dim(bh)), dtype=torch.float32, device=dev)
-                eng.pool(sl["batch"], out=sl["out"], check=False, stream=s_cmp)
-                ev_cmp[k] = torch.cuda.Event()
-                ev_cmp[k].record(s_cmp)
+                s_cmp.wait_event(sl["ev_in"])
+                if sl["used"]:
+                    s_cmp.wait_event(sl["ev_out"])  # the slot's device output was copied out
+                dbatch = CsrBatch(sl["idx"][:nnz], sl["offs"][:nb], bh.feature_tables, bh.feature_ops, B)
+                sl["batch"] = dbatch
+                eng.pool(dbatch, out=sl["out"], check=False, stream=s_cmp)
+                sl["ev_cmp"].record(s_cmp)
             with torch.cuda.stream(s_out):
-                s_out.wait_event(ev_cmp[k])
-                if "host" not in sl or sl["host"].shape != sl["out"].shape:
-                    sl["host"] = torch.empty(sl["out"].shape, dtype=torch.float32, pin_memory=True)
+                s_out.wait_event(sl["ev_cmp"])
                 sl["host"].copy_(sl["out"], non_blocking=True)
-                ev_out[k] = torch.cuda.Event()
-                ev_out[k].record(s_out)
+                sl["ev_out"].record(s_out)
+            sl["used"] = True
 
         i = 0
         for bh in batches_host:
             k = i % depth
             if len(pending) == depth:
                 kk = pending.pop(0)
-                ev_out[kk].synchronize()
+                slots[kk]["ev_out"].synchronize()
                 yield slots[kk]["host"]
             launch(bh, k)
             pending.append(k)
             i += 1
         while pending:
             kk = pending.pop(0)
-            ev_out[kk].synchronize()
+            slots[kk]["ev_out"].synchronize()
             yield slots[kk]["host"]
         torch.cuda.synchronize(dev)
         code, _ = eng.status.read()

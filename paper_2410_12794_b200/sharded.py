@@ -602,10 +602,14 @@ class P2PShardedLookup:
         self.profile = False
         self.timeline = []
         self.launches = 0  # our kernels launched (libflexemb), for bench accounting
+        self._barrier_waits = []
 
     def _barrier(self):
         self.launches += 1
         L = self._lib
+        for ev in self._barrier_waits:  # consumers of the output set the next step reuses
+            torch.cuda.current_stream(self.device).wait_event(ev)
+        self._barrier_waits = []
         self.epoch += 1
         L.check(L.lib.fx_peer_barrier(self.b_flags.ptr, self.t_peer_flags.data_ptr(), self.rank, self.world,
                                       self.epoch, self.t_timeout.data_ptr(), L.stream_ptr()), "peer barrier")
@@ -759,11 +763,14 @@ class P2PShardedLookup:
         side = torch.cuda.Stream(self.device)
         ev_bar = None
         k = 0
-        for indices, offsets in batches:
+        for item in batches:
+            indices, offsets = item[0], item[1]
             p = k % 2
             with torch.cuda.stream(side):
+                if len(item) > 2 and item[2] is not None:
+                    side.wait_event(item[2])  # the batch's inputs are ready (e.g. an H2D copy)
                 if ev_bar is not None:
-                    side.wait_event(ev_bar)  # set p's previous readers (gather k-2) certified done
+                    side.wait_event(ev_bar)  # set p free: gathers and combine of step k-2 done
                 tok = self._mark("stage")
                 self._stage(indices, offsets, p, stream=side)
                 self._close(tok)
@@ -773,12 +780,17 @@ class P2PShardedLookup:
             tok = self._mark("barrier")
             self._barrier()
             self._close(tok)
-            ev_bar = torch.cuda.Event()
-            ev_bar.record(main)
+            res = None
             if k >= 1:
                 tok = self._mark("combine")
                 res = self._result(1 - p)
                 self._close(tok)
+            # certifies for the restaging of set 1-p at step k+1: every owner's
+            # gather of step k-1 is done (barrier k) and so is this rank's
+            # combine of step k-1, which reads set 1-p's counts / raw lists
+            ev_bar = torch.cuda.Event()
+            ev_bar.record(main)
+            if res is not None:
                 yield res
             tok = self._mark("pool")
             self._gather(p)
@@ -794,6 +806,58 @@ class P2PShardedLookup:
             yield res
         if check:
             self._check()
+
+    def stream_host(self, host_batches, check: bool = True):
+        """End-to-end pipelined API: pinned host (indices, offsets) in, pinned
+        host pooled [B, F*D] f32 out, one per batch, in order. H2D copies run
+        on their own stream into 3 rotating device slots, the fused exchange
+        runs as in `stream()`, and each result's D2H runs on a copy stream
+        overlapping the next step's gather; the barrier that lets owners
+        overwrite that output set waits for the copy. A yielded tensor is
+        valid until the generator is advanced."""
+        dev = self.device
+        main = torch.cuda.current_stream(dev)
+        s_h2d, s_d2h = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        slots = [dict(idx=None, offs=None, ev=torch.cuda.Event(), used=None) for _ in range(3)]
+        host = [torch.empty((self.B, self.F * self.D), dtype=torch.float32, pin_memory=True) for _ in range(2)]
+        ev_d2h = [torch.cuda.Event() for _ in range(2)]
+        consumed = {}
+
+        def dev_iter():
+            for j, (ih, oh) in enumerate(host_batches):
+                sl = slots[j % 3]
+                with torch.cuda.stream(s_h2d):
+                    if j >= 3:
+                        s_h2d.wait_event(consumed.pop(j - 3))  # step j-3's push has read the slot
+                    if sl["idx"] is None or sl["idx"].numel() < ih.numel() or sl["idx"].dtype != ih.dtype:
+                        sl["idx"] = torch.empty(max(int(ih.numel()), 1), dtype=ih.dtype, device=dev)
+                        sl["offs"] = torch.empty(oh.numel(), dtype=torch.int64, device=dev)
+                    di, do = sl["idx"][:ih.numel()], sl["offs"][:oh.numel()]
+                    di.copy_(ih, non_blocking=True)
+                    do.copy_(oh, non_blocking=True)
+                    sl["ev"].record(s_h2d)
+                yield di, do, sl["ev"]
+
+        prev = None
+        for i, res in enumerate(self.stream(dev_iter(), check=check)):
+            ev = torch.cuda.Event()
+            ev.record(main)  # pushes of steps <= i+1 are done by now in main's order
+            consumed[i] = ev
+            k = i % 2
+            if self.mode == "rowwise":
+                res.record_stream(s_d2h)  # a fresh [B, F*D] copy of the K5 output: keep it alive for the D2H
+            with torch.cuda.stream(s_d2h):
+                s_d2h.wait_event(ev)
+                host[k].copy_(res, non_blocking=True)
+                ev_d2h[k].record(s_d2h)
+            self._barrier_waits.append(ev_d2h[k])
+            if prev is not None:
+                ev_d2h[prev].synchronize()
+                yield host[prev]
+            prev = k
+        if prev is not None:
+            ev_d2h[prev].synchronize()
+            yield host[prev]
 
     def close(self):
         L = self._lib

@@ -18,7 +18,8 @@ from paper_2410_12794_b200.workload import DlrmBatchGen  # noqa: E402
 def main():
     mode = sys.argv[1] if len(sys.argv) > 1 else "tablewise"
     exchange = sys.argv[2] if len(sys.argv) > 2 else "nccl"
-    pipelined = exchange.endswith("-pipe")
+    hosted = exchange.endswith("-host")  # pinned host in/out through stream_host
+    pipelined = exchange.endswith("-pipe") or hosted
     exchange = exchange[:-5] if pipelined else exchange
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -59,8 +60,11 @@ def main():
         dev_b = [(torch.from_numpy(hb.indices).cuda(), torch.from_numpy(hb.offsets).cuda()) for hb in hbs]
         torch.cuda.synchronize()
         outs, cnts = [], []
-        for o in sl.stream(dev_b):
-            outs.append(o.cpu().numpy())
+        if hosted:
+            dev_b = [(torch.from_numpy(hb.indices).pin_memory(), torch.from_numpy(hb.offsets).pin_memory())
+                     for hb in hbs]
+        for o in (sl.stream_host(dev_b) if hosted else sl.stream(dev_b)):
+            outs.append(o.cpu().numpy().copy())
             if exchange.startswith("p2pthr"):
                 cnts.append(sl.counters().cpu().numpy())
     planned = exchange.startswith("p2pthr")
@@ -99,7 +103,7 @@ def main():
                      dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     if rank == 0:
-        print(f"SHARDED {mode} {exchange}{'-pipe' if pipelined else ''} world={world} worst_tolerance_ratio={t[0].item():.4f} "
+        print(f"SHARDED {mode} {exchange}{('-host' if hosted else '-pipe') if pipelined else ''} world={world} worst_tolerance_ratio={t[0].item():.4f} "
               f"max_non_bit_exact_bags={int(t[1].item())} bags_per_rank={n} counter_mismatches={int(t[2].item())} "
               f"non_bit_exact_vs_reference_combine={int(t[3].item())}", flush=True)
     ok = t[0].item() <= 1.0 and t[2].item() == 0 and t[3].item() == 0

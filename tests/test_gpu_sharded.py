@@ -10,7 +10,7 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("exchange", ["nccl", "p2p", "p2p-pipe"])
+@pytest.mark.parametrize("exchange", ["nccl", "p2p", "p2p-pipe", "p2p-host"])
 @pytest.mark.parametrize("mode", ["tablewise", "rowwise"])
 def test_sharded_multi_gpu(mode, exchange):
     n = torch.cuda.device_count() if torch.cuda.is_available() else 0
