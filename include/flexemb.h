@@ -238,6 +238,9 @@ int fx_cache_last_evicted(fx_cache *c, uint64_t *out, int64_t cap, int64_t *n_ou
 /* device array of row pointers for the pending keys (NULL entry -> table dir),
  * consumed by the next fx_cache_apply_pending (host-fetched admissions) */
 int fx_cache_set_pending_rows(fx_cache *c, const float *const *rows, int64_t n);
+/* device base of the cache's row storage and its row stride in floats
+ * (valid until the next fx_cache_reserve_slots) */
+int fx_cache_rows(fx_cache *c, const float **rows, int64_t *ld);
 /* tick += n (the batch's probes when no row probe call advances it) */
 int fx_cache_advance_tick(fx_cache *c, int64_t n, void *stream);
 
@@ -307,13 +310,17 @@ int fx_rw_push(const int64_t *route_off, const int64_t *starts, const int32_t *o
  * starts[sid]) * ld — an IPC-mapped peer pointer for other ranks' shards,
  * read by fx_combine_ptr over NVLink. raw_off: int64[n_bags+1]; raw_ptr:
  * capacity nnz; counters (optional): int32[3][n_bags] = pushdown_groups,
- * pushdown_rows, raw_rows per bag. workspace: query with ws == NULL. */
+ * pushdown_rows, raw_rows per bag. hit_slot (optional, int32 per
+ * occurrence): occurrences with a cache slot >= 0 are served by the
+ * requester's cache — excluded from the groups, and joined to the raw list at
+ * their position as cache_rows + slot * cache_ld (cache hits combine as raw
+ * vectors, ranker.py:409-411). workspace: query with ws == NULL. */
 int fx_rw_push_planned(const int64_t *route_off, const int64_t *starts, const int32_t *owners, const int64_t *nrows,
                        const int32_t *bag_table, const void *indices, int32_t idx_type, const int64_t *offsets,
                        int64_t n_bags, int32_t W, int32_t threshold, int32_t *counts, int64_t *scan,
                        int32_t *const *dst_idx, int64_t *const *dst_offs, const float *const *shard_base, int64_t ld,
-                       int64_t *raw_off, const float **raw_ptr, int32_t *counters, void *ws, size_t *ws_bytes,
-                       void *stream);
+                       int64_t *raw_off, const float **raw_ptr, int32_t *counters, const int32_t *hit_slot,
+                       const float *cache_rows, int64_t cache_ld, void *ws, size_t *ws_bytes, void *stream);
 /* one-block barrier: release-store `epoch` into peer_flags[r][rank] for every
  * rank r (system scope, after a system fence), then acquire-spin until
  * my_flags[r] >= epoch for every r. peer_flags is a DEVICE array of `world`

@@ -104,7 +104,7 @@ _SIGS = {
     "fx_push_csr": ([_P, _I32, _P, _I32, _I32, _P, _P, _P, _P, _I32, _P], ctypes.c_int),
     "fx_rw_push": ([_P, _P, _P, _P, _P, _I32, _P, _I64, _I32, _P, _P, _P, _P, _P, _SZP, _P], ctypes.c_int),
     "fx_rw_push_planned": ([_P, _P, _P, _P, _P, _P, _I32, _P, _I64, _I32, _I32, _P, _P, _P, _P, _P, _I64, _P, _P, _P,
-                            _P, _SZP, _P], ctypes.c_int),
+                            _P, _P, _I64, _P, _SZP, _P], ctypes.c_int),
     "fx_combine_ptr": ([_P, _I32, _P, _I32, _I64, _P, _P, _I64, _I32, _I32, _P, _P, _I64, _P, _P], ctypes.c_int),
     # cache entry points are typed in cache.py (_sig); listed here for export checks
     **{n: (None, ctypes.c_int) for n in (
@@ -114,7 +114,7 @@ _SIGS = {
         "fx_cache_sketch_bump", "fx_cache_sketch_ranked", "fx_cache_lru", "fx_cache_eviction_log",
         "fx_cache_pending", "fx_cache_last_evicted", "fx_cache_set_pending_rows", "fx_cache_set_parallel",
         "fx_cache_advance_tick", "fx_cache_pooled_find", "fx_cache_pooled_touch", "fx_cache_read_slots",
-        "fx_cache_pooled_put")},
+        "fx_cache_pooled_put", "fx_cache_rows")},
     "fx_bag_fingerprint": ([_P, _P, _P, _I32, _P, _I64, _P, _P, _P], ctypes.c_int),
 }
 

@@ -200,6 +200,7 @@ def _sig():
         "fx_cache_set_pending_rows": [P, P, I64],
         "fx_cache_set_parallel": [P, I32],
         "fx_cache_advance_tick": [P, I64, P],
+        "fx_cache_rows": [P, ctypes.POINTER(P), ctypes.POINTER(I64)],
         "fx_cache_pooled_find": [P, P, P, I64, P, P],
         "fx_cache_pooled_touch": [P, P, P, I64, P],
         "fx_cache_read_slots": [P, P, I64, P, I32, P, P],
@@ -522,6 +523,21 @@ class AdaptiveCache:
         if n:
             _lib.check(self._L.fx_cache_pooled_touch(self._h, slot.data_ptr(), pos.data_ptr(), n,
                                                      _lib.stream_ptr()), "pooled touch")
+
+    def rows_base(self):
+        """(device pointer, row stride in floats) of the slot row storage."""
+        p, ld = ctypes.c_void_p(), ctypes.c_int64()
+        _lib.check(self._L.fx_cache_rows(self._h, ctypes.byref(p), ctypes.byref(ld)), "cache rows")
+        return int(p.value or 0), int(ld.value)
+
+    def bind_dir(self, entries) -> None:
+        """Register row locations [(base_ptr, row_begin, row_end, ld, table, dim)]
+        — e.g. IPC-mapped shards of peer GPUs, read over NVLink by admissions."""
+        self._dir = [FxTableDir(*e) for e in entries]
+        for e in entries:
+            self._row_bytes[int(e[4])] = int(e[5]) * 4
+        self._upload_tables()
+        self._reserve_slots_for(self.budget_bytes)
 
     def advance_tick(self, n: int) -> None:
         if n:

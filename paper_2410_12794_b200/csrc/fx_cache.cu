@@ -1703,6 +1703,12 @@ int fx_cache_pending(fx_cache *c, uint64_t *out, int64_t cap, int64_t *n_out, vo
   return cuda_check(cudaStreamSynchronize(st), "fx_cache_pending");
 }
 
+int fx_cache_rows(fx_cache *c, const float **rows, int64_t *ld) {
+  *rows = c->v.rows;
+  *ld = c->v.row_ld;
+  return FX_OK;
+}
+
 int fx_cache_advance_tick(fx_cache *c, int64_t n, void *stream) {
   k_advance_tick<<<1, 1, 0, as_stream(stream)>>>(c->v.sc, n);
   FX_LAUNCH_CHECK("fx_cache_advance_tick");

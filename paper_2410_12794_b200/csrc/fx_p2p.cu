@@ -105,7 +105,8 @@ template <typename IdxT>
 __global__ void __launch_bounds__(256) k_rw_count(const int64_t *route_off, const int64_t *starts,
                                                   const int32_t *owners, const int32_t *bag_table,
                                                   const IdxT *indices, const int64_t *offsets, int64_t n_bags,
-                                                  int W, int32_t *counts) {
+                                                  int W, int32_t *counts, const int32_t *hit_slot = nullptr,
+                                                  int32_t *hit_cnt = nullptr) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -115,10 +116,14 @@ __global__ void __launch_bounds__(256) k_rw_count(const int64_t *route_off, cons
     int cnt[32];  // per-destination counts (warp-uniform, register-resident after unrolling)
 #pragma unroll
     for (int d = 0; d < 32; ++d) cnt[d] = 0;
+    int hits = 0;
     for (int64_t c0 = beg; c0 < end; c0 += 32) {
-      const int my_d = (c0 + lane < end)
+      const bool on = c0 + lane < end;
+      const bool hit = on && hit_slot && hit_slot[c0 + lane] >= 0;  // served by the requester's cache
+      const int my_d = (on && !hit)
                            ? route_dest(route_off, starts, owners, t, static_cast<int64_t>(indices[c0 + lane]))
                            : -1;
+      hits += __popc(__ballot_sync(0xffffffffu, hit));
 #pragma unroll
       for (int d = 0; d < 32; ++d)
         if (d < W) cnt[d] += __popc(__ballot_sync(0xffffffffu, my_d == d));
@@ -126,6 +131,7 @@ __global__ void __launch_bounds__(256) k_rw_count(const int64_t *route_off, cons
 #pragma unroll
     for (int d = 0; d < 32; ++d)
       if (d < W && lane == 0) counts[(int64_t)d * n_bags + b] = cnt[d];
+    if (hit_cnt && lane == 0) hit_cnt[b] = hits;
   }
 }
 
@@ -185,7 +191,7 @@ __global__ void k_rw_push_offsets(const int64_t *scan, int64_t n_bags, int W, in
 // the K5 partial lookup skip it); raw_cnt[b] = raw rows of bag b; counters
 // [3][n_bags] = (pushdown_groups, pushdown_rows, raw_rows) (ranker.py:281-293).
 __global__ void k_rw_plan(int32_t *counts, int64_t n_bags, int W, int32_t threshold, int32_t *raw_cnt,
-                          int32_t *counters) {
+                          int32_t *counters, const int32_t *hit_cnt) {
   for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < n_bags; b += (int64_t)gridDim.x * blockDim.x) {
     int pg = 0, pr = 0, rr = 0;
     for (int d = 0; d < W; ++d) {
@@ -200,7 +206,7 @@ __global__ void k_rw_plan(int32_t *counts, int64_t n_bags, int W, int32_t thresh
         counts[i] = 0;
       }
     }
-    raw_cnt[b] = rr;
+    raw_cnt[b] = rr + (hit_cnt ? hit_cnt[b] : 0);  // cache hits join the raw vectors (ranker.py:409-411)
     if (counters) {
       counters[b] = pg;
       counters[n_bags + b] = pr;
@@ -229,7 +235,8 @@ __global__ void __launch_bounds__(256) k_rw_raw(const int64_t *route_off, const 
                                                 const int32_t *bag_table, const IdxT *indices,
                                                 const int64_t *offsets, int64_t n_bags, const int32_t *counts,
                                                 const int64_t *raw_off, const float *const *shard_base, int64_t ld,
-                                                const float **raw_ptr) {
+                                                const float **raw_ptr, const int32_t *hit_slot,
+                                                const float *cache_rows, int64_t cache_ld) {
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -243,7 +250,11 @@ __global__ void __launch_bounds__(256) k_rw_raw(const int64_t *route_off, const 
     for (int64_t c0 = beg; c0 < end; c0 += 32) {
       bool raw = false;
       const float *ptr = nullptr;
-      if (c0 + lane < end) {
+      const int32_t hs = (c0 + lane < end && hit_slot) ? hit_slot[c0 + lane] : -1;
+      if (hs >= 0) {
+        raw = true;
+        ptr = cache_rows + static_cast<int64_t>(hs) * cache_ld;
+      } else if (c0 + lane < end) {
         int64_t idx = static_cast<int64_t>(indices[c0 + lane]);
         const int sid = route_shard(route_off, starts, t, idx);
         const int d = owners[sid];
@@ -267,7 +278,7 @@ __global__ void __launch_bounds__(256) k_rw_push_planned(const int64_t *route_of
                                                          const int32_t *owners, const int32_t *bag_table,
                                                          const IdxT *indices, const int64_t *offsets, int64_t n_bags,
                                                          int W, const int32_t *counts, const int64_t *scan,
-                                                         int32_t *const *dst_idx) {
+                                                         int32_t *const *dst_idx, const int32_t *hit_slot) {
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -287,7 +298,7 @@ __global__ void __launch_bounds__(256) k_rw_push_planned(const int64_t *route_of
       const bool on = c0 + lane < end;
       int64_t idx = 0;
       int my_d = -1;
-      if (on) {
+      if (on && !(hit_slot && hit_slot[c0 + lane] >= 0)) {
         idx = static_cast<int64_t>(indices[c0 + lane]);
         my_d = route_dest(route_off, starts, owners, t, idx);
         if (!((pushed >> my_d) & 1u)) my_d = -1;
@@ -411,8 +422,8 @@ int fx_rw_push_planned(const int64_t *route_off, const int64_t *starts, const in
                        const int32_t *bag_table, const void *indices, int32_t idx_type, const int64_t *offsets,
                        int64_t n_bags, int32_t W, int32_t threshold, int32_t *counts, int64_t *scan,
                        int32_t *const *dst_idx, int64_t *const *dst_offs, const float *const *shard_base, int64_t ld,
-                       int64_t *raw_off, const float **raw_ptr, int32_t *counters, void *ws, size_t *ws_bytes,
-                       void *stream) {
+                       int64_t *raw_off, const float **raw_ptr, int32_t *counters, const int32_t *hit_slot,
+                       const float *cache_rows, int64_t cache_ld, void *ws, size_t *ws_bytes, void *stream) {
   if (W < 1 || W > 32 || n_bags < 0 || threshold < 2) {
     set_error("fx_rw_push_planned: bad arguments (threshold must be >= 2)");
     return FX_E_CONFIG;
@@ -423,7 +434,7 @@ int fx_rw_push_planned(const int64_t *route_off, const int64_t *starts, const in
   cub::DeviceScan::ExclusiveSum(nullptr, c2, (const int32_t *)nullptr, (int64_t *)nullptr,
                                 static_cast<int>(n_bags + 1));
   const size_t cub_bytes = ((c1 > c2 ? c1 : c2) + 255) & ~size_t(255);
-  const size_t need = cub_bytes + static_cast<size_t>(n_bags + 1) * 4;
+  const size_t need = cub_bytes + static_cast<size_t>(n_bags + 1) * 4 * 2;
   if (ws == nullptr) {
     *ws_bytes = need;
     return FX_OK;
@@ -433,34 +444,37 @@ int fx_rw_push_planned(const int64_t *route_off, const int64_t *starts, const in
     return FX_E_CONFIG;
   }
   int32_t *raw_cnt = reinterpret_cast<int32_t *>(static_cast<char *>(ws) + cub_bytes);
+  int32_t *hit_cnt = hit_slot ? raw_cnt + (n_bags + 1) : nullptr;
   size_t cb = cub_bytes;
   cudaStream_t st = as_stream(stream);
   cudaMemsetAsync(counts, 0, n * sizeof(int32_t), st);
   const int grid = grid_for(n_bags * 32, 256);
   if (idx_type == FX_IDX_I32)
     k_rw_count<int32_t><<<grid, 256, 0, st>>>(route_off, starts, owners, bag_table,
-                                              static_cast<const int32_t *>(indices), offsets, n_bags, W, counts);
+                                              static_cast<const int32_t *>(indices), offsets, n_bags, W, counts,
+                                              hit_slot, hit_cnt);
   else
     k_rw_count<int64_t><<<grid, 256, 0, st>>>(route_off, starts, owners, bag_table,
-                                              static_cast<const int64_t *>(indices), offsets, n_bags, W, counts);
-  k_rw_plan<<<grid_for(n_bags + 1, 256), 256, 0, st>>>(counts, n_bags, W, threshold, raw_cnt, counters);
+                                              static_cast<const int64_t *>(indices), offsets, n_bags, W, counts,
+                                              hit_slot, hit_cnt);
+  k_rw_plan<<<grid_for(n_bags + 1, 256), 256, 0, st>>>(counts, n_bags, W, threshold, raw_cnt, counters, hit_cnt);
   cub::DeviceScan::ExclusiveSum(ws, cb, raw_cnt, raw_off, static_cast<int>(n_bags + 1), st);
   cb = cub_bytes;
   cub::DeviceScan::ExclusiveSum(ws, cb, counts, scan, static_cast<int>(n), st);
   if (idx_type == FX_IDX_I32) {
     k_rw_raw<int32_t><<<grid, 256, 0, st>>>(route_off, starts, owners, nrows, bag_table,
                                             static_cast<const int32_t *>(indices), offsets, n_bags, counts, raw_off,
-                                            shard_base, ld, raw_ptr);
+                                            shard_base, ld, raw_ptr, hit_slot, cache_rows, cache_ld);
     k_rw_push_planned<int32_t><<<grid, 256, 0, st>>>(route_off, starts, owners, bag_table,
                                                      static_cast<const int32_t *>(indices), offsets, n_bags, W,
-                                                     counts, scan, dst_idx);
+                                                     counts, scan, dst_idx, hit_slot);
   } else {
     k_rw_raw<int64_t><<<grid, 256, 0, st>>>(route_off, starts, owners, nrows, bag_table,
                                             static_cast<const int64_t *>(indices), offsets, n_bags, counts, raw_off,
-                                            shard_base, ld, raw_ptr);
+                                            shard_base, ld, raw_ptr, hit_slot, cache_rows, cache_ld);
     k_rw_push_planned<int64_t><<<grid, 256, 0, st>>>(route_off, starts, owners, bag_table,
                                                      static_cast<const int64_t *>(indices), offsets, n_bags, W,
-                                                     counts, scan, dst_idx);
+                                                     counts, scan, dst_idx, hit_slot);
   }
   k_rw_push_offsets<<<grid_for((int64_t)W * (n_bags + 1), 256), 256, 0, st>>>(scan, n_bags, W, dst_offs, true);
   FX_LAUNCH_CHECK("fx_rw_push_planned");

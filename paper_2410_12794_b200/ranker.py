@@ -328,12 +328,14 @@ class Ranker:
         self._mark("dedup_probe")
         hit_occ = torch.zeros(nnz, dtype=torch.bool, device=dev)
         dd = None
+        self._occ_slot = None
         if cache is not None and nnz:
             dd = self._dedup(lay.bag_table, lay.indices, lay.offsets, lay.sm_start, nnz)
             slot = torch.empty(max(dd.n_uniq, 1), dtype=torch.int32, device=dev)
             last = dd.last_ord if pooled is None else pooled[5][dd.last_ord]
             cache.probe_unique(dd.uniq, dd.mult, last, None, n_ticks, slot, n_uniq_host=dd.n_uniq)
-            hit_occ = slot[dd.inverse.long()] >= 0
+            self._occ_slot = slot[dd.inverse.long()]
+            hit_occ = self._occ_slot >= 0
         elif cache is not None and n_ticks:
             cache.advance_tick(n_ticks)
         # 4. miss groups per (bag, server) and the pushdown plan

@@ -343,6 +343,10 @@ class ShardedLookup:
 # Fused exchange over NVLink peer memory (no NCCL on the data path)
 # ---------------------------------------------------------------------------------------
 
+def _ptr(t):
+    return None if t is None else t.data_ptr()
+
+
 def _cai_tensor(ptr: int, shape, dtype: torch.dtype, device) -> torch.Tensor:
     """Zero-copy torch view of a raw device allocation (__cuda_array_interface__)."""
     typestr = {torch.float32: "<f4", torch.float64: "<f8", torch.int32: "<i4", torch.int64: "<i8"}[dtype]
@@ -512,8 +516,8 @@ class P2PShardedLookup:
             else:
                 _lib.check(_lib.lib.fx_rw_push_planned(None, None, None, None, None, None, 0, None, n_bags, W,
                                                        int(pushdown_threshold), None, None, None, None, None, 0,
-                                                       None, None, None, None, ctypes.byref(need), None),
-                           "rw push ws")
+                                                       None, None, None, None, None, 0, None, ctypes.byref(need),
+                                                       None), "rw push ws")
                 self.t_raw_off = [torch.zeros(n_bags + 1, dtype=torch.int64, device=dev) for _ in (0, 1)]
                 self.t_raw_ptr = [torch.zeros(max(self.max_nnz, 1), dtype=torch.int64, device=dev) for _ in (0, 1)]
                 self.t_counters = [torch.zeros((3, n_bags), dtype=torch.int32, device=dev) for _ in (0, 1)]
@@ -635,9 +639,10 @@ class P2PShardedLookup:
         self.timeline = []
         return out
 
-    def _stage(self, indices, offsets, p, stream=None):
+    def _stage(self, indices, offsets, p, stream=None, hit_slot=None, cache_rows=0, cache_ld=0):
         """Ingress validation + push of this rank's batch into every owner's
-        staging (set p)."""
+        staging (set p). Row-wise planned mode: occurrences with
+        hit_slot >= 0 are served from the requester's cache rows."""
         L = self._lib
         B, F, W = self.B, self.F, self.world
         nnz = int(indices.numel())
@@ -663,8 +668,8 @@ class P2PShardedLookup:
                                              self.t_scan[p].data_ptr(), self.t_dst_idx[p].data_ptr(),
                                              self.t_dst_offs[p].data_ptr(), self.t_shard_base.data_ptr(), self.D,
                                              self.t_raw_off[p].data_ptr(), self.t_raw_ptr[p].data_ptr(),
-                                             self.t_counters[p].data_ptr(), self.t_ws[p].data_ptr(),
-                                             ctypes.byref(wsb), sp), "rw push planned")
+                                             self.t_counters[p].data_ptr(), _ptr(hit_slot), cache_rows, cache_ld,
+                                             self.t_ws[p].data_ptr(), ctypes.byref(wsb), sp), "rw push planned")
             # k_route, k_rw_count, k_rw_plan, k_rw_raw, k_rw_push_planned, k_rw_push_offsets
             self.launches += 6
         else:
@@ -806,6 +811,22 @@ class P2PShardedLookup:
             yield res
         if check:
             self._check()
+
+    def pool_cached(self, indices: torch.Tensor, offsets: torch.Tensor, hit_slot: torch.Tensor | None,
+                    cache=None) -> torch.Tensor:
+        """One synchronous step for a requester that has a cache (row-wise
+        planned mode): occurrences with hit_slot >= 0 are combined from the
+        cache's rows, the rest follow the plan (pushdown to the owner or raw
+        fetch over NVLink). Returns the table-major pooled [F*B, D] f32."""
+        if self.threshold is None:
+            raise ConfigError("pool_cached needs the planned row-wise mode (pushdown_threshold)")
+        rows, ld = cache.rows_base() if (cache is not None and hit_slot is not None) else (0, 0)
+        self._stage(indices, offsets, 0, hit_slot=hit_slot, cache_rows=rows, cache_ld=ld)
+        self._barrier()
+        self._gather(0)
+        self._barrier()
+        self._result(0)
+        return self._tmp[0]
 
     def stream_host(self, host_batches, check: bool = True):
         """End-to-end pipelined API: pinned host (indices, offsets) in, pinned

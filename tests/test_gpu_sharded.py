@@ -69,3 +69,21 @@ def test_sharded_rowwise_planned_raw_fetch(exchange):
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert f"SHARDED rowwise {exchange}" in r.stdout
     assert "counter_mismatches=0" in r.stdout and "non_bit_exact_vs_reference_combine=0" in r.stdout
+
+
+@pytest.mark.parametrize("args", [["2"], ["none"], ["2", "pooled"]])
+def test_sharded_ranker_with_per_gpu_caches(args):
+    """Ranker pipeline on every rank with its own GPU cache over a sharded
+    store (ShardedRanker): metrics, counters, LRU order and eviction log
+    equal the canonical-order oracle batch by batch; vectors within the
+    reference tolerance."""
+    n = torch.cuda.device_count() if torch.cuda.is_available() else 0
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    w = min(n, 4)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={w}",
+           "--master-addr", "127.0.0.1", "--master-port", "29575",
+           os.path.join(ROOT, "scripts", "sharded_ranker_check.py"), *args]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "SHARDED_RANKER" in r.stdout and "lru_mismatch_batches=0" in r.stdout
