@@ -436,26 +436,38 @@ def run_sharded(args, rank, world, local):
     if args.exchange == "nccl":
         sl.stats.c1_bytes_sent = sl.stats.c2_bytes_sent = 0
     l0 = getattr(sl, "launches", None)
-    sl.profile = True
     torch.cuda.synchronize()
     dist.barrier()
     pipelined = args.exchange == "p2p" and not args.sync
+
+    def run_steps(n):
+        if pipelined:
+            for _ in sl.stream((batches[i % len(batches)] for i in range(n)), check=False):
+                pass
+        else:
+            for i in range(n):
+                sl.lookup(*batches[i % len(batches)], out=out, check=False)
+
     ev0.record(stream)
-    if pipelined:
-        for _ in sl.stream((batches[i % len(batches)] for i in range(args.steps)), check=False):
-            pass
-    else:
-        for i in range(args.steps):
-            sl.lookup(*batches[i % len(batches)], out=out, check=False)
+    run_steps(args.steps)
     ev1.record(stream)
     ev1.synchronize()
     torch.cuda.synchronize()
     dist.barrier()
     clocks = sampler.stop()
     ms = ev0.elapsed_time(ev1)
-    phases = sl.phase_ms()
     l1 = getattr(sl, "launches", None)
+    # per-phase device times from a separate profiled pass (events on every
+    # phase would perturb the timed region)
+    prof_steps = min(args.steps, 50)
+    if args.exchange == "nccl":
+        sl.stats.c1_bytes_sent = sl.stats.c2_bytes_sent = 0
+    sl.profile = True
+    run_steps(prof_steps)
+    torch.cuda.synchronize()
+    phases = {k: v * args.steps / prof_steps for k, v in sl.phase_ms().items()}
     sl.profile = False
+    dist.barrier()
     sl.ops.check()
     # owner-pool algorithmic bytes: every rank pools, for each requester, the
     # rows routed to it; measured on this rank over the timed steps
@@ -470,7 +482,7 @@ def run_sharded(args, rank, world, local):
     # algorithmic bytes pooled on this rank per step: all ranks' bags of the tables it owns.
     # With identical batch statistics per rank, the rank's share is rows_owned / total.
     if args.exchange == "nccl":
-        a2a_bytes = (sl.stats.c1_bytes_sent + sl.stats.c2_bytes_sent) / args.steps
+        a2a_bytes = (sl.stats.c1_bytes_sent + sl.stats.c2_bytes_sent) / prof_steps
     else:
         # bytes crossing NVLink per step from this rank as owner: pooled rows (+ indices read) to the
         # other ranks; table-wise f32 rows, row-wise f64 partials
