@@ -107,7 +107,8 @@ class FlexOps:
         self.owners = torch.tensor(owners, dtype=torch.int32, device=dev)
         self.nrows = torch.from_numpy(nrows).to(dev)
         self.bag_table = torch.tensor(np.repeat(np.array(self.ftab, np.int32), B), device=dev)
-        self.status = _lib.Status(dev)
+        self.status = _lib.Status(dev)        # requester-side ingress validation (K1)
+        self.owner_status = _lib.Status(dev)  # owner-side: rows routed here that it does not host (K4)
         self._ws = None
         self._seg_cache = {}
 
@@ -123,6 +124,10 @@ class FlexOps:
                                self.nrows.data_ptr(), self.bag_table.data_ptr(), idx.data_ptr(), L.FX_IDX_I64,
                                offsets.data_ptr(), n_bags, dest.data_ptr(), self.status.err.data_ptr(),
                                self.status.code.data_ptr(), L.stream_ptr()), "route")
+        # an invalid index (flagged above, raised by check()) still needs a
+        # destination so every rank's split sizes agree: rank 0, which then
+        # records a routing violation instead of reading it
+        dest.clamp_(min=0)
         need = ctypes.c_size_t(0)
         L.check(L.lib.fx_bucket(None, nnz, None, n_bags, world, None, None, None, None, ctypes.byref(need), None))
         if self._ws is None or self._ws.numel() < need.value:
@@ -170,8 +175,8 @@ class FlexOps:
         seg = self._segments(out, feats, partial)
         L.check(L.lib.fx_gather_pool(seg.data_ptr(), len(feats), out.shape[-1], recv_idx.data_ptr(), L.FX_IDX_I32,
                                      offs.data_ptr(), n, L.FX_OUT_F64_PARTIAL if partial else L.FX_OUT_F32,
-                                     L.ptr(counts), self.status.err.data_ptr(), L.FX_E_ROUTING_VIOLATION,
-                                     self.status.code.data_ptr(), L.stream_ptr()), "owner pool")
+                                     L.ptr(counts), self.owner_status.err.data_ptr(), L.FX_E_ROUTING_VIOLATION,
+                                     self.owner_status.code.data_ptr(), L.stream_ptr()), "owner pool")
 
     def combine(self, parts, cnts, bag_ops, out):
         """K5: fold per-source f64 partials in ascending source rank."""
@@ -182,12 +187,31 @@ class FlexOps:
         L.check(L.lib.fx_combine(ptrs.data_ptr(), 0, cptr.data_ptr(), W, D, None, None, n_bags, D, 0, bag_ops.data_ptr(),
                                  out.data_ptr(), D, None, L.stream_ptr()), "combine")
 
-    def check(self):
+    def check(self, batch=None, batch_id: int = 0):
+        """[sync] Raise for a flagged index: LookupValidationError with the
+        reference's message (ranker.py:184-193) when this rank's own batch
+        held it (`batch` = (indices, offsets) of that batch), else
+        RoutingViolationError (an owner was sent a row it does not host)."""
         code, pos = self.status.read()
+        ocode, _ = self.owner_status.read()
+        if not code and not ocode:
+            return
+        self.status.reset()
+        self.owner_status.reset()
         if code:
-            self.status.reset()
-            exc = LookupValidationError if code == self._lib.FX_E_LOOKUP_VALIDATION else RoutingViolationError
-            raise exc(f"bad index at CSR position {pos} on rank {self.rank}")
+            if batch is not None:
+                idx, offs = batch
+                offs_h = offs.cpu().numpy()
+                if 0 <= pos < int(offs_h[-1]):
+                    b = int(np.searchsorted(offs_h, pos, side="right") - 1)
+                    f, smp = divmod(b, self.B)
+                    t = self.ftab[f]
+                    n = int(self.nrows[t].item())
+                    raise LookupValidationError(f"batch {batch_id}, lookup {smp}: index {int(idx[pos].item())} "
+                                                f"out of range [0,{n}) for table {t}")
+            raise LookupValidationError(f"batch {batch_id}: index out of range at CSR position {pos} "
+                                        f"(rank {self.rank})")
+        raise RoutingViolationError(f"rank {self.rank} was sent a row it does not host")
 
 
 @dataclass
@@ -335,7 +359,7 @@ class ShardedLookup:
             self.ops.combine(recv_part, recv_cnts, self.bag_ops, tmp)
             out.view(B, F, D).copy_(tmp.view(F, B, D).transpose(0, 1))
         if check:
-            self.ops.check()
+            self.ops.check((indices, offsets))
         return out
 
 
@@ -646,6 +670,7 @@ class P2PShardedLookup:
         L = self._lib
         B, F, W = self.B, self.F, self.world
         nnz = int(indices.numel())
+        self._last_batch = (indices, offsets)
         if nnz > self.max_nnz:
             raise ConfigError(f"batch has {nnz} indices, staging holds {self.max_nnz}")
         o = self.ops
@@ -693,8 +718,8 @@ class P2PShardedLookup:
                 (L.FX_OUT_F64_PARTIAL if self.pesz == 8 else L.FX_OUT_F32_PARTIAL))
         L.check(L.lib.fx_gather_pool(self.segs[p].data_ptr(), self.n_segs, self.D, self.b_idx.ptr, L.FX_IDX_I32,
                                      None, self.n_vbags, mode | L.FX_OUT_SYSFENCE, None,
-                                     self.ops.status.err.data_ptr(), L.FX_E_ROUTING_VIOLATION,
-                                     self.ops.status.code.data_ptr(), L.stream_ptr()), "fused pool")
+                                     self.ops.owner_status.err.data_ptr(), L.FX_E_ROUTING_VIOLATION,
+                                     self.ops.owner_status.code.data_ptr(), L.stream_ptr()), "fused pool")
 
     def _result(self, p):
         """Pooled [B, F*D] f32 of the step that used set p (row-wise: K5 first)."""
@@ -724,7 +749,7 @@ class P2PShardedLookup:
         return self.t_counters[self._last_set]
 
     def _check(self):
-        self.ops.check()
+        self.ops.check(getattr(self, "_last_batch", None))
         if int(self.t_timeout.item()):
             raise RuntimeError("peer barrier timed out (a rank stopped participating)")
 

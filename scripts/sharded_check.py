@@ -99,14 +99,35 @@ def main():
                 worst = max(worst, O.tolerance_ratio(ref, got))
                 exact += ref.tobytes() == got.tobytes()
                 n += 1
-    t = torch.tensor([worst, float(n - exact), float(cnt_bad), float(hier_exact)], device="cuda",
+    # ingress validation (ranker.py:184-193): an out-of-range index on rank 1's
+    # batch raises LookupValidationError there; every rank recovers next step
+    val_bad = 0.0
+    if exchange in ("p2p", "nccl") and not pipelined and world > 1:
+        from paper_2410_12794_b200.errors import LookupValidationError, RoutingViolationError
+        hb = hbs[0]
+        idx = hb.indices.copy()
+        if rank == 1:
+            idx[hb.offsets[3 * B + 5]] = rows[3] + 7  # table 3, sample 5
+        got = None
+        try:
+            sl.lookup(torch.from_numpy(idx).cuda(), torch.from_numpy(hb.offsets).cuda())
+        except (LookupValidationError, RoutingViolationError) as e:
+            got = type(e).__name__
+        if rank == 1 and got != "LookupValidationError":
+            val_bad = 1.0
+        dist.barrier()
+        out = sl.lookup(torch.from_numpy(hb.indices).cuda(), torch.from_numpy(hb.offsets).cuda()).cpu().numpy()
+        ref = O.pool_flat(O.rows_of(0, 0, D, hb.indices[hb.offsets[0]:hb.offsets[1]]), ops[0])
+        val_bad += 0.0 if O.within_tolerance(ref, out[0, :D]) else 1.0
+    t = torch.tensor([worst, float(n - exact), float(cnt_bad), float(hier_exact), val_bad], device="cuda",
                      dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     if rank == 0:
         print(f"SHARDED {mode} {exchange}{('-host' if hosted else '-pipe') if pipelined else ''} world={world} worst_tolerance_ratio={t[0].item():.4f} "
               f"max_non_bit_exact_bags={int(t[1].item())} bags_per_rank={n} counter_mismatches={int(t[2].item())} "
-              f"non_bit_exact_vs_reference_combine={int(t[3].item())}", flush=True)
-    ok = t[0].item() <= 1.0 and t[2].item() == 0 and t[3].item() == 0
+              f"non_bit_exact_vs_reference_combine={int(t[3].item())} validation_failures={int(t[4].item())}",
+              flush=True)
+    ok = t[0].item() <= 1.0 and t[2].item() == 0 and t[3].item() == 0 and t[4].item() == 0
     dist.destroy_process_group()
     sys.exit(0 if ok else 1)
 

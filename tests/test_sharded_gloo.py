@@ -72,7 +72,7 @@ class OracleOps:
         acc[mean] = acc[mean] / tot[mean].double().unsqueeze(1)
         out.copy_(acc.float())
 
-    def check(self):
+    def check(self, batch=None, batch_id=0):
         pass
 
 
