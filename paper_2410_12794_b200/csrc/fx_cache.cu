@@ -970,6 +970,31 @@ __global__ void k_sketch_collect(CacheView c, uint64_t *out_keys, long long *out
   }
 }
 
+// top-k preselection for stage(limit): histogram of the top 16 bits of the
+// (descending-count) sort key over live sketch keys
+__global__ void k_sketch_hist(CacheView c, int32_t *hist) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < c.kcap; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = c.kkeys[i];
+    if (k == kEmpty || k == kTomb) continue;
+    const long long vb = ~__double_as_longlong(c.kval[i]) & LLONG_MAX;
+    atomicAdd(&hist[vb >> 47], 1);
+  }
+}
+
+// live keys whose bin <= max_bin (every key that can be among the top k)
+__global__ void k_sketch_collect_upto(CacheView c, int32_t max_bin, uint64_t *out_keys, int32_t *out_pos,
+                                      long long *count) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < c.kcap; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = c.kkeys[i];
+    if (k == kEmpty || k == kTomb) continue;
+    const long long vb = ~__double_as_longlong(c.kval[i]) & LLONG_MAX;
+    if ((vb >> 47) > max_bin) continue;
+    const long long p = atomicAdd(reinterpret_cast<unsigned long long *>(count), 1ull);
+    out_keys[p] = k;
+    out_pos[p] = static_cast<int32_t>(i);
+  }
+}
+
 // ranked keys -> pending (sequential room accounting, cache.py:323-342)
 __global__ void k_stage_seq(CacheView c, const int32_t *ranked_pos, int64_t m, int64_t limit) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
@@ -1589,6 +1614,62 @@ static int rank_sketch(fx_cache *c, cudaStream_t st, int64_t *n_live, int32_t **
   return FX_OK;
 }
 
+// Exact top-k of the sketch by (-count, key) without sorting every key: a
+// 65536-bin histogram of the sort key's top bits finds the bin holding the
+// k-th key; only keys in that bin or hotter are collected and fully ranked.
+static int rank_sketch_topk(fx_cache *c, cudaStream_t st, int64_t k, int64_t *n_cand, int32_t **ranked) {
+  constexpr int kBins = 1 << 16;
+  int rc = ensure_ws(c, al(kBins * 4));
+  if (rc) return rc;
+  int32_t *hist = static_cast<int32_t *>(c->ws);
+  cudaMemsetAsync(hist, 0, kBins * 4, st);
+  k_sketch_hist<<<grid_for(c->v.kcap, 256), 256, 0, st>>>(c->v, hist);
+  std::vector<int32_t> h(kBins);
+  rc = cuda_check(cudaMemcpyAsync(h.data(), hist, kBins * 4, cudaMemcpyDeviceToHost, st), "sketch hist");
+  if (rc) return rc;
+  rc = cuda_check(cudaStreamSynchronize(st), "sketch hist sync");
+  if (rc) return rc;
+  int64_t cum = 0;
+  int bin = kBins - 1;
+  for (int b = 0; b < kBins; ++b) {
+    cum += h[b];
+    if (cum >= k) {
+      bin = b;
+      break;
+    }
+  }
+  const int64_t C = cum;  // keys in bins <= bin
+  *n_cand = C;
+  if (C <= 0) return FX_OK;
+  size_t cb1 = 0, cb2 = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, cb1, (const uint64_t *)nullptr, (uint64_t *)nullptr,
+                                  (const int32_t *)nullptr, (int32_t *)nullptr, static_cast<int>(C));
+  cub::DeviceRadixSort::SortPairs(nullptr, cb2, (const long long *)nullptr, (long long *)nullptr,
+                                  (const int32_t *)nullptr, (int32_t *)nullptr, static_cast<int>(C));
+  size_t cb = cb1 > cb2 ? cb1 : cb2;
+  const size_t need = al(C * 8) * 4 + al(C * 4) * 3 + al(8) + al(cb);
+  rc = ensure_ws(c, need);
+  if (rc) return rc;
+  char *p = static_cast<char *>(c->ws);
+  uint64_t *keys = reinterpret_cast<uint64_t *>(p); p += al(C * 8);
+  uint64_t *keys2 = reinterpret_cast<uint64_t *>(p); p += al(C * 8);
+  long long *vb = reinterpret_cast<long long *>(p); p += al(C * 8);
+  long long *vb2 = reinterpret_cast<long long *>(p); p += al(C * 8);
+  int32_t *pos = reinterpret_cast<int32_t *>(p); p += al(C * 4);
+  int32_t *pos2 = reinterpret_cast<int32_t *>(p); p += al(C * 4);
+  int32_t *pos3 = reinterpret_cast<int32_t *>(p); p += al(C * 4);
+  long long *cnt = reinterpret_cast<long long *>(p); p += al(8);
+  void *tmp = p;
+  cudaMemsetAsync(cnt, 0, 8, st);
+  k_sketch_collect_upto<<<grid_for(c->v.kcap, 256), 256, 0, st>>>(c->v, bin, keys, pos, cnt);
+  cub::DeviceRadixSort::SortPairs(tmp, cb, keys, keys2, pos, pos2, static_cast<int>(C), 0, 64, st);
+  k_gather_vbits<<<grid_for(C, 256), 256, 0, st>>>(c->v, pos2, C, vb);
+  cub::DeviceRadixSort::SortPairs(tmp, cb, vb, vb2, pos2, pos3, static_cast<int>(C), 0, 64, st);
+  FX_LAUNCH_CHECK("fx_cache rank sketch top-k");
+  *ranked = pos3;
+  return FX_OK;
+}
+
 int fx_cache_stage(fx_cache *c, int64_t limit, int64_t *staged, void *stream) {
   cudaStream_t st = as_stream(stream);
   Scalars h;
@@ -1599,7 +1680,11 @@ int fx_cache_stage(fx_cache *c, int64_t limit, int64_t *staged, void *stream) {
   int64_t L = 0;
   int32_t *ranked = nullptr;
   void *tail = nullptr;
-  rc = rank_sketch(c, st, &L, &ranked, &tail);
+  if (limit >= 0 && limit * 16 < h.sketch_live) {
+    rc = rank_sketch_topk(c, st, limit, &L, &ranked);  // L = candidates, a superset of the top `limit`
+  } else {
+    rc = rank_sketch(c, st, &L, &ranked, &tail);
+  }
   if (rc || L <= 0) return rc;
   // hottest(n=limit) considers the top `limit` keys overall (cache.py:323-324)
   const int64_t m = limit >= 0 ? (limit < L ? limit : L) : L;
