@@ -177,9 +177,10 @@ int fx_dedup(const int32_t *bag_table, const void *indices, int32_t idx_type,
  *      FrequencySketch) ------------------------------------------------------
  * Keys are u64 (table << 40 | row). The handle owns its device memory
  * (cudaMalloc at create / reserve; documented exception to "no allocation").
- * Scalars (fx_cache_scalars order, 19 x int64): budget, used, tick, hits,
+ * Scalars (fx_cache_scalars order, 21 x int64): budget, used, tick, hits,
  * misses, entries, free_top, sketch_live, sketch_tomb, hash_tomb, pending,
- * n_evlog, n_acc, n_ev, n_cand, staged, err, n_ov, n_par_puts. err: 1 = an insert or
+ * n_evlog, n_acc, n_ev, n_cand, staged, err, n_ov, n_par_puts, tiles_bulk,
+ * tiles_chain (offer-resolution statistics). err: 1 = an insert or
  * shrink found nothing left to evict (the reference raises KeyError from
  * OrderedDict.popitem there), 2 = pooled-key fingerprint collision.
  * Calls marked [sync] read scalars back to the host. */
@@ -199,7 +200,7 @@ int fx_cache_create(fx_cache **out, int64_t slot_capacity, int32_t max_dim, int3
 int fx_cache_destroy(fx_cache *c);
 int fx_cache_set_tables(fx_cache *c, const fx_table_dir *dir, int32_t n_dir, const int32_t *table_bytes,
                         int32_t n_tables);                                     /* host arrays */
-int fx_cache_scalars(fx_cache *c, int64_t *out19, void *stream);               /* [sync] */
+int fx_cache_scalars(fx_cache *c, int64_t *out21, void *stream);               /* [sync] */
 int fx_cache_reserve_sketch(fx_cache *c, int64_t new_keys, void *stream);      /* [sync] */
 int fx_cache_reserve_slots(fx_cache *c, int64_t slots, void *stream);          /* [sync] */
 /* get() per unique key (cache.py:189-202): hit -> last_tick = tick0 +

@@ -134,7 +134,7 @@ class ResizeReport:
 
 
 _SC = ("budget", "used", "tick", "hits", "misses", "entries", "free_top", "sketch_live", "sketch_tomb",
-       "hash_tomb", "pending", "n_evlog", "n_acc", "n_ev", "n_cand", "staged", "err", "n_ov", "n_par_puts")
+       "hash_tomb", "pending", "n_evlog", "n_acc", "n_ev", "n_cand", "staged", "err", "n_ov", "n_par_puts", "tiles_bulk", "tiles_chain")
 
 POOLED_BIT = 1 << 63
 

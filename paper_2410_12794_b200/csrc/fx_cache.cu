@@ -46,6 +46,7 @@ struct Scalars {
                    //    OrderedDict), 2: pooled-key fingerprint collision
   long long n_ov;  // in-place pooled re-puts recorded by the last put call
   long long n_par_puts;  // put calls resolved by the parallel closed form (cumulative)
+  long long tiles_bulk, tiles_chain;  // k_offer_par sketch tiles resolved as one run / by the chain (cumulative)
 };
 
 struct CacheView {
@@ -510,6 +511,9 @@ __global__ void __launch_bounds__(1024) k_offer_par(CacheView c, const uint64_t 
       __syncthreads();
       const int ffa = s_ffa, ffr = s_ffr;
       const bool bulk = ffa >= 256 || ffr >= 256 || ffa == T || ffr == T;
+      if (tid == 0) {
+        if (bulk) sc->tiles_bulk += 1; else sc->tiles_chain += 1;
+      }
       if (bulk) {
         // long run: decisions are the prefix run, no chain needed
         const bool acc_run = ffa >= ffr;

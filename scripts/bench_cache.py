@@ -89,6 +89,7 @@ def main():
                               "batch": B, "pooling": list(pool), "init_store_s": round(init_s, 2),
                               "pooled_keyspace": bool(a.pooled), "threshold": thr,
                               "pooled_hit_bags_last": getattr(rk, "last_pooled_hits", None),
+                              "offer_tiles": {k: cache._scalars()[k] for k in ("tiles_bulk", "tiles_chain")},
                               "hits_from_cache": bool(a.hits_from_cache),
                               "stage_ms_per_batch": {k: round(v / len(times), 3) for k, v in rk.stage_ms.items()}}),
                   flush=True)
