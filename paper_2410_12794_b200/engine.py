@@ -74,6 +74,7 @@ class LookupEngine:
                     self.tables[t] = sh.data
         self.status = _lib.Status(self.device)
         self._segs: OrderedDict = OrderedDict()
+        self._seg_cap = 16  # cached segment descriptor sets (raised by capture)
 
     def dim_of(self, t: int) -> int:
         return self.dep.meta(t).dim
@@ -97,7 +98,7 @@ class LookupEngine:
             col += D
         seg = make_segments(segs, self.device)
         self._segs[key] = seg
-        if len(self._segs) > 16:
+        if len(self._segs) > self._seg_cap:
             self._segs.popitem(last=False)
         return seg
 
@@ -154,11 +155,59 @@ class LookupEngine:
             self.raise_if_bad(batch)
         return out
 
+    def prepare_many(self, batches, outs=None) -> "ManyPlan":
+        """Build (once) the segment descriptors for pooling several
+        independent requests in ONE K4 launch (see pool_many); the returned
+        plan relaunches with no host-side work beyond the launch itself, for
+        serving loops whose request slots are reused."""
+        if not batches:
+            raise ConfigError("prepare_many: no requests")
+        dims = {self.dim_of(t) for b in batches for t in b.feature_tables}
+        if len(dims) != 1:
+            raise ConfigError("pool_many needs one embedding dim across requests")
+        D = dims.pop()
+        if len({b.indices.dtype for b in batches}) != 1:
+            raise ConfigError("pool_many needs one index dtype across requests")
+        if outs is None:
+            outs = [torch.empty((b.batch_size, self.out_dim(b)), dtype=torch.float32, device=self.device)
+                    for b in batches]
+        segs, vb = [], 0
+        for b, o in zip(batches, outs):
+            B = b.batch_size
+            if b.n_bags != B * b.n_features:
+                raise ConfigError("offsets must describe batch_size * n_features table-major bags")
+            for f, (t, op) in enumerate(zip(b.feature_tables, b.feature_ops)):
+                if t not in self.tables:
+                    raise ConfigError(f"table {t} is not resident as one shard on {self.device}")
+                tab = self.tables[t]
+                segs.append(_lib.FxSegment(tab.data_ptr(), 0, tab.shape[0], vb, vb + B,
+                                           o.data_ptr() + f * D * 4, o.stride(0), tab.stride(0), D, op_code(op),
+                                           b.indices.data_ptr(), b.offsets.data_ptr() + f * B * 8))
+                vb += B
+        return ManyPlan(self, list(batches), outs, make_segments(segs, self.device), len(segs), vb, D)
+
+    def pool_many(self, batches, outs=None, check: bool = True, stream=None):
+        """Pool several independent requests (e.g. the concurrent request
+        streams of SURVEY §8(d) cfg5, or small serving requests) in ONE K4
+        launch: every (request, feature) is a segment carrying its own index
+        and offset arrays (fx_segment.idx / .offs), laid out one after the
+        other in a virtual bag space, so small requests share one grid instead
+        of paying a launch each. Same arithmetic and bit-identical results as
+        pool() per request. Returns the list of [B_r, sum D] outputs."""
+        if not batches:
+            return []
+        plan = self.prepare_many(batches, outs)
+        plan.launch(stream)
+        if check:
+            plan.check()
+        return plan.outs
+
     def capture(self, batches, outs, stream=None):
         """Capture one K4 launch per (batch, out) pair into a CUDA graph
         (small batches are launch-bound: cfg1 moves ~21 MB per batch). The
         segment descriptors are uploaded before capture; replay with
         graph.replay(); check status with raise_if_bad() afterwards."""
+        self._seg_cap = max(self._seg_cap, len(batches) + 16)  # every descriptor set stays resident
         for b, o in zip(batches, outs):
             self._segments(b, o)
         torch.cuda.synchronize(self.device)
@@ -177,6 +226,14 @@ class LookupEngine:
         if not code:
             return
         self.status.reset()
+        best = self._first_bad(batch)
+        if best is None:
+            raise LookupValidationError(f"batch {batch_id}: an index was out of range (batch changed since launch)")
+        s, f, index, t, n = best
+        raise LookupValidationError(f"batch {batch_id}, lookup {s}: index {index} out of range [0,{n}) for table {t}")
+
+    def _first_bad(self, batch: CsrBatch):
+        """First out-of-range index in (lookup, feature, position) order, or None."""
         offs = batch.offsets.cpu().numpy()
         idx = batch.indices.cpu().numpy()
         B = batch.batch_size
@@ -191,13 +248,43 @@ class LookupEngine:
                     cand = (s, f, int(seg[bad[0]]), t, n)
                     if best is None or cand[:2] < best[:2]:
                         best = cand
-        s, f, index, t, n = best
-        raise LookupValidationError(f"batch {batch_id}, lookup {s}: index {index} out of range [0,{n}) for table {t}")
+        return best
 
 
 def algorithmic_bytes(batch_nnz: int, n_bags: int, dim: int, idx_bytes: int = 4) -> int:
     """per bag L*D*4 (rows) + L*idx (indices) + 8 (offset) + D*4 (pooled write)."""
     return batch_nnz * dim * 4 + batch_nnz * idx_bytes + n_bags * 8 + n_bags * dim * 4
+
+
+class ManyPlan:
+    """Prepared multi-request K4 launch (LookupEngine.prepare_many)."""
+
+    def __init__(self, eng, batches, outs, segs, n_segs, n_vbags, dim):
+        self.eng, self.batches, self.outs = eng, batches, outs
+        self.segs, self.n_segs, self.n_vbags, self.dim = segs, n_segs, n_vbags, dim
+        self._idx_type = _lib.idx_type_of(batches[0].indices)
+        self._idx0 = batches[0].indices.data_ptr()
+
+    def launch(self, stream=None) -> None:
+        e = self.eng
+        _lib.check(_lib.lib.fx_gather_pool(self.segs.data_ptr(), self.n_segs, self.dim, self._idx0, self._idx_type,
+                                           None, self.n_vbags, _lib.FX_OUT_F32, None, e.status.err.data_ptr(),
+                                           _lib.FX_E_LOOKUP_VALIDATION, e.status.code.data_ptr(),
+                                           _lib.stream_ptr(stream)), "gather_pool many")
+
+    def check(self) -> None:
+        """[sync] LookupValidationError naming the first request with a bad index."""
+        e = self.eng
+        code, _ = e.status.read()
+        if not code:
+            return
+        e.status.reset()
+        for r, b in enumerate(self.batches):
+            best = e._first_bad(b)
+            if best is not None:
+                s, f, index, t, n = best
+                raise LookupValidationError(f"request {r}, lookup {s}: index {index} out of range "
+                                            f"[0,{n}) for table {t}")
 
 
 class HostLookup:

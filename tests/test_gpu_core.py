@@ -168,6 +168,41 @@ def test_engine_pool_vs_oracle(P, dim, B, L):
     assert exact == F * B  # f64 sequential accumulation: bit-identical to the flat oracle
 
 
+@pytest.mark.parametrize("dim", [64, 128, 12])
+def test_pool_many_requests_one_launch(P, dim):
+    """LookupEngine.pool_many: many independent requests in ONE K4 launch,
+    bit-identical to pooling each request on its own (and to the oracle)."""
+    from paper_2410_12794_b200.workload import DlrmBatchGen
+    tables = (1000, 37, 5000)
+    dims = (dim,) * 3
+    ops = ("sum", "mean", "sum")
+    dep = P.init_store([P.TableMeta(t, n, dim) for t, n in enumerate(tables)],
+                       [P.ShardSpec(t, 0, n, 0) for t, n in enumerate(tables)], seed=0)
+    eng = P.LookupEngine(dep)
+    reqs, hbs = [], []
+    for r in range(9):
+        hb = DlrmBatchGen(tables, 1.05, 8 + 7 * r, (0, 12), seed=50 + r, ops=ops).next()
+        hbs.append(hb)
+        reqs.append(P.CsrBatch(torch.from_numpy(hb.indices).cuda(), torch.from_numpy(hb.offsets).cuda(),
+                               hb.feature_tables, hb.feature_ops, hb.batch_size))
+    outs = eng.pool_many(reqs)
+    for hb, req, o in zip(hbs, reqs, outs):
+        single = eng.pool(req).cpu().numpy()
+        assert o.cpu().numpy().tobytes() == single.tobytes()
+        ref = _oracle_pool(hb, dims)
+        B = hb.batch_size
+        for f in range(3):
+            for s in range(B):
+                b = f * B + s
+                if hb.offsets[b + 1] > hb.offsets[b]:  # empty bags pool to 0 (no reference value)
+                    assert ref[b].tobytes() == single[s, f * dim:(f + 1) * dim].tobytes()
+    bad = reqs[4].indices.clone()
+    bad[3] = 10 ** 6
+    reqs[4] = P.CsrBatch(bad, reqs[4].offsets, reqs[4].feature_tables, reqs[4].feature_ops, reqs[4].batch_size)
+    with pytest.raises(P.LookupValidationError, match=r"request 4, lookup"):
+        eng.pool_many(reqs)
+
+
 def test_engine_mixed_dims_and_int64(P):
     tables, dims = (300, 500), (16, 64)
     dep, hb = _engine_batch(P, tables, dims, 32, (1, 6), 0.8, seed=1)
