@@ -183,7 +183,16 @@ def run_reference(args, rank, world):
                                    "threshold 2, cache off, tables row-reduced to 20K rows)"},
         "e2e": {"value": value, "unit": "pooled lookups/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    emit(line, args)
+
+
+def emit(line: dict, args) -> None:
+    """Print the bench JSON line; with --report DIR also write it as a
+    summary in the reference's MetricsReport schema (bench/report.py)."""
     print(json.dumps(line), flush=True)
+    if getattr(args, "report", None):
+        from paper_2410_12794_b200.report import from_bench_line
+        from_bench_line(line).write(args.report)
 
 
 def main():
@@ -212,6 +221,8 @@ def main():
     ap.add_argument("--threshold", type=int, default=0,
                     help="N>1 row-wise fused exchange: the reference's pushdown threshold (groups below it are "
                          "raw-fetched over NVLink by the requester); 0 = push every group down")
+    ap.add_argument("--report", default=None,
+                    help="also write the line as a MetricsReport-schema summary (+ text report) into this dir")
     ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
                     help="N>1 pooled-result exchange: fused NVLink peer stores (p2p) or NCCL all-to-all")
     args = ap.parse_args()
@@ -378,7 +389,7 @@ def main():
             "cpu_baseline": cpu,
             "clocks": clocks,
         }
-        print(json.dumps(line), flush=True)
+        emit(line, args)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -575,7 +586,7 @@ def run_sharded(args, rank, world, local):
             "gpu_launches": (l1 - l0) if l0 is not None else None,
             "e2e": e2e, "cpu_baseline": None, "clocks": clocks,
         }
-        print(json.dumps(line), flush=True)
+        emit(line, args)
     dist.barrier()
     dist.destroy_process_group()
 

@@ -344,6 +344,23 @@ def trace_fixtures():
         save_trace(generate_trace(cfg, rows), os.path.join(HERE, name))
 
 
+def report_fixtures():
+    """bench/report.py: percentiles and the MetricsReport text/machine forms."""
+    from embserve.bench.report import MetricsReport, RunMetrics, percentiles
+    rng = np.random.default_rng(3)
+    cases = [[], [5.0], [3.0, 1.0, 2.0], [float(x) for x in rng.random(37)], [float(x) for x in rng.integers(0, 9, 100)]]
+    pct = [percentiles(c) for c in cases]
+    rep = MetricsReport(experiment="golden-x", seed=7, backend="virtual", fingerprint="abc123",
+                        config={"b": 2, "a": [1, 2]},
+                        runs=[RunMetrics(label="r1", makespan=12.5, throughput=3.25, counters={"z": 1, "a": 2},
+                                         latency_stages={"net": percentiles([1.0, 2.0, 4.0])},
+                                         extras={"note": "x"}),
+                              RunMetrics(label="r2")],
+                        comparison={"speedup": 1.5}, invariants={"ok": True})
+    with open(os.path.join(HERE, "report.json"), "w") as fh:
+        json.dump(dict(cases=cases, percentiles=pct, machine=rep.to_machine(), text=rep.to_text()), fh)
+
+
 if __name__ == "__main__":
     trace_fixtures()
     prf_fixtures()
@@ -353,5 +370,6 @@ if __name__ == "__main__":
     cache_fixtures()
     ranker_fixtures()
     pooled_fixtures()
+    report_fixtures()
     for f in sorted(os.listdir(HERE)):
         print(f, os.path.getsize(os.path.join(HERE, f)))

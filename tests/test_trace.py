@@ -69,3 +69,49 @@ def test_batch_to_host_csr_is_table_major():
     assert hb.feature_tables == (0, 1) and hb.feature_ops == ("sum", "mean")
     assert hb.offsets.tolist() == [0, 2, 3, 4, 7]
     assert hb.indices.tolist() == [1, 2, 4, 3, 5, 6, 7]
+
+
+def test_dlrm_dataset_loader_and_converter(tmp_path):
+    """Fast CSR loader for DLRM lookup datasets (indices, offsets, lengths;
+    table-major bags) and the dlrm-tensors external trace converter."""
+    import torch
+    from paper_2410_12794_b200.trace import convert_external_trace, iter_dlrm_batches
+    rng = np.random.default_rng(0)
+    T, N, B = 3, 10, 4
+    lengths = rng.integers(1, 5, (T, N))
+    offsets = np.concatenate([[0], np.cumsum(lengths.reshape(-1))])
+    indices = rng.integers(0, 1000, int(offsets[-1]))
+    path = tmp_path / "day.pt"
+    torch.save((torch.from_numpy(indices), torch.from_numpy(offsets), torch.from_numpy(lengths)), path)
+    hbs = list(iter_dlrm_batches(str(path), B, ops=("sum", "mean", "sum")))
+    assert len(hbs) == N // B
+    for k, hb in enumerate(hbs):
+        for t in range(T):
+            for s in range(B):
+                b = t * N + k * B + s
+                got = hb.indices[hb.offsets[t * B + s]:hb.offsets[t * B + s + 1]]
+                assert list(got) == list(indices[offsets[b]:offsets[b + 1]])
+    tr = convert_external_trace(str(path), "dlrm-tensors", batch_size=B, ops=("sum", "mean", "sum"))
+    assert len(tr.batches) == 2 and tr.batches[1].lookups[2].features[1].op.value == "mean"
+    assert tr.batches[0].lookups[0].features[0].indices == list(indices[offsets[0]:offsets[1]])
+    with pytest.raises(NotImplementedError):
+        convert_external_trace(str(path), "criteo-raw")
+
+
+def test_metrics_report_schema_vs_reference(golden_dir):
+    """MetricsReport / percentiles reproduce the reference's text and
+    canonical machine forms (bench/report.py) byte for byte."""
+    import json
+    from paper_2410_12794_b200.report import MetricsReport, RunMetrics, percentiles
+    g = json.load(open(f"{golden_dir}/report.json"))
+    for c, p in zip(g["cases"], g["percentiles"]):
+        assert percentiles(c) == p
+    rep = MetricsReport(experiment="golden-x", seed=7, backend="virtual", fingerprint="abc123",
+                        config={"b": 2, "a": [1, 2]},
+                        runs=[RunMetrics(label="r1", makespan=12.5, throughput=3.25, throughput_unit="lookups/tick",
+                                         counters={"z": 1, "a": 2},
+                                         latency_stages={"net": percentiles([1.0, 2.0, 4.0])}, extras={"note": "x"}),
+                              RunMetrics(label="r2", throughput_unit="lookups/tick")],
+                        comparison={"speedup": 1.5}, invariants={"ok": True})
+    assert rep.to_machine() == g["machine"]
+    assert rep.to_text() == g["text"]
