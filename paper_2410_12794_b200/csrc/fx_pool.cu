@@ -296,8 +296,10 @@ using namespace fx;
 static int pool_variant() {
   static int v = -1;
   if (v < 0) {
+    // 2 (default): TMA bulk-copy staging for D = 64 / 128, cp.async otherwise;
+    // 1: cp.async staging everywhere; 0: register-staged v4
     const char *e = getenv("FX_POOL_VARIANT");
-    v = e ? atoi(e) : 1;
+    v = e ? atoi(e) : 2;
   }
   return v;
 }
@@ -324,6 +326,26 @@ static void launch_async_cr(const fx_segment *segs, int n_segs, int dim, const I
   const int64_t need = (n_bags + WARPS * (32 / G) - 1) / (WARPS * (32 / G));
   if (blocks > need) blocks = need;
   k_pool_async<G, NCH, CR, IdxT, MODE><<<static_cast<int>(blocks), WARPS * 32, smem, st>>>(
+      segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code, sf);
+}
+
+template <int G, int NCH, int CR, typename IdxT, int MODE>
+static void launch_bulk_cr(const fx_segment *segs, int n_segs, int dim, const IdxT *ix, const int64_t *offsets,
+                           int64_t n_bags, int32_t *counts, int64_t *err, int32_t bad_code, int32_t *err_code,
+                           cudaStream_t st, bool sf) {
+  constexpr int WARPS = 4;
+  const size_t smem = static_cast<size_t>(WARPS) * (32 / G) * (CR * G * 16 * NCH + 8);
+  static int per_sm = -1;
+  if (per_sm < 0) {
+    cudaFuncSetAttribute(k_pool_bulk<G, NCH, CR, IdxT, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pool_bulk<G, NCH, CR, IdxT, MODE>, WARPS * 32, smem);
+    if (per_sm < 1) per_sm = 1;
+  }
+  int64_t blocks = static_cast<int64_t>(num_sms()) * per_sm;
+  const int64_t need = (n_bags + WARPS * (32 / G) - 1) / (WARPS * (32 / G));
+  if (blocks > need) blocks = need;
+  k_pool_bulk<G, NCH, CR, IdxT, MODE><<<static_cast<int>(blocks), WARPS * 32, smem, st>>>(
       segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code, sf);
 }
 
@@ -364,15 +386,21 @@ static int launch_pool(const fx_segment *segs, int n_segs, int dim, const void *
                        cudaStream_t st, bool vec4, bool sf) {
   const IdxT *ix = static_cast<const IdxT *>(indices);
   const int var = pool_variant();
-  if (var == 1 && dim == 128) {
+  if (var == 2 && dim == 128) {
+    launch_bulk_cr<32, 1, 16, IdxT, MODE>(segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code, st,
+                                         sf);
+  } else if (var == 2 && dim == 64) {
+    launch_bulk_cr<16, 1, 16, IdxT, MODE>(segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code, st,
+                                         sf);
+  } else if (var >= 1 && dim == 128) {
     launch_async<32, 1, IdxT, MODE>(segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code, st, sf);
-  } else if (var == 1 && dim == 256) {
+  } else if (var >= 1 && dim == 256) {
     launch_async<32, 2, IdxT, MODE>(segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code, st, sf);
-  } else if (var == 1 && dim == 64) {
+  } else if (var >= 1 && dim == 64) {
     launch_async<16, 1, IdxT, MODE>(segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code, st, sf);
-  } else if (var == 1 && dim == 32) {
+  } else if (var >= 1 && dim == 32) {
     launch_async<8, 1, IdxT, MODE>(segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code, st, sf);
-  } else if (var == 1 && dim == 512) {
+  } else if (var >= 1 && dim == 512) {
     launch_async<32, 4, IdxT, MODE>(segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code, st, sf);
   } else if (vec4 && dim == 128) {
     k_gather_pool_v4<32, 1, 8, IdxT, MODE><<<grid_for(n_bags * 32, 256), 256, 0, st>>>(

@@ -15,6 +15,33 @@ __device__ __forceinline__ void cp_async16(uint32_t saddr, const void *g) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
+// ---- TMA bulk-copy staging (cp.async.bulk + mbarrier transaction counts)
+__device__ __forceinline__ void mbar_init(uint32_t mbar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mbar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t mbar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(mbar),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(mbar)
+               : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 template <int NCH, int MODE>
 __device__ __forceinline__ void emit_bag(const fx_segment &sg, int64_t bag, int64_t cnt, double (&acc)[NCH][4],
                                          int lane, int G, int32_t *counts) {
@@ -181,6 +208,133 @@ __global__ void __launch_bounds__(128, FX_POOL_MINB) k_pool_async(const fx_segme
           acc[k][3] += static_cast<double>(v.w);
         }
       }
+      __syncwarp(gmask);
+    }
+    if (!have_next && nbag < n_bags) {
+      bag_bounds(segs, ns, nbag, offsets, nbeg, nend);
+      nidx = (gl < CR && nbeg + gl < nend) ? nindices[nbeg + gl] : IdxT(0);
+    }
+    emit_bag<NCH, MODE>(segs[s], bag, end - beg, acc, gl, G, counts);
+    bag = nbag;
+    s = ns;
+    indices = nindices;
+    beg = nbeg;
+    end = nend;
+    pidx = nidx;
+  }
+  if (sysfence) __threadfence_system();
+}
+
+}  // namespace fx
+
+
+namespace fx {
+
+// Bulk-copy variant of k_pool_async (FX_POOL_VARIANT=2): each row of a chunk
+// is ONE cp.async.bulk (TMA engine, G*16*NCH bytes) issued by one lane and
+// completing on the group's mbarrier, instead of G 16-byte cp.async per row.
+// Same order of accumulation (index order, f64 per column).
+template <int G, int NCH, int CR, typename IdxT, int MODE>
+__global__ void __launch_bounds__(128, FX_POOL_MINB) k_pool_bulk(const fx_segment *__restrict__ segs, int n_segs,
+                                                                int dim, const IdxT *__restrict__ indices_g,
+                                                                const int64_t *__restrict__ offsets, int64_t n_bags,
+                                                                int32_t *__restrict__ counts, int64_t *err,
+                                                                int32_t bad_code, int32_t *err_code, bool sysfence) {
+  static_assert(CR <= G, "chunk rows <= lanes per group");
+  constexpr int ROWB = G * 16 * NCH;
+  constexpr int GPW = 32 / G;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31;
+  const int gl = lane % G;
+  const int gw = lane / G;
+  const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (gw * G));
+  const int wib = threadIdx.x >> 5;
+  const int grp = wib * GPW + gw;
+  unsigned char *buf = smem + static_cast<size_t>(grp) * CR * ROWB;
+  const uint32_t sbuf = static_cast<uint32_t>(__cvta_generic_to_shared(buf));
+  const uint32_t mbar = static_cast<uint32_t>(__cvta_generic_to_shared(
+      smem + static_cast<size_t>(blockDim.x / 32) * GPW * CR * ROWB + grp * 8));
+  if (gl == 0) mbar_init(mbar, 1);
+  fence_proxy_async_smem();
+  __syncwarp();
+  uint32_t phase = 0;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t step = nwarps * GPW;
+
+  int64_t bag = warp * GPW + gw;
+  if (bag >= n_bags) {
+    if (sysfence) __threadfence_system();
+    return;
+  }
+  int s = find_segment(segs, n_segs, bag);
+  int64_t beg, end;
+  bag_bounds(segs, s, bag, offsets, beg, end);
+  const IdxT *indices = seg_indices(segs, s, indices_g);
+  IdxT pidx = (gl < CR && beg + gl < end) ? indices[beg + gl] : IdxT(0);
+
+  while (bag < n_bags) {
+    const float *__restrict__ tab = segs[s].table;
+    const int64_t rb = segs[s].row_begin, re = segs[s].row_end, ld = segs[s].ld;
+    double acc[NCH][4];
+#pragma unroll
+    for (int k = 0; k < NCH; ++k) acc[k][0] = acc[k][1] = acc[k][2] = acc[k][3] = 0.0;
+    const int64_t nbag = bag + step;
+    const int ns = nbag < n_bags ? find_segment(segs, n_segs, nbag) : s;
+    const IdxT *nindices = seg_indices(segs, ns, indices_g);
+    int64_t nbeg = 0, nend = 0;
+    IdxT nidx = IdxT(0);
+    bool have_next = false;
+    for (int64_t c0 = beg; c0 < end; c0 += CR) {
+      const int n = static_cast<int>((end - c0) < CR ? (end - c0) : (int64_t)CR);
+      const int64_t idx = static_cast<int64_t>(pidx);
+      int64_t my_off = 0;
+      if (gl < n) {
+        if (idx < rb || idx >= re) record_bad(err, err_code, c0 + gl, bad_code);
+        else my_off = (idx - rb) * ld;
+      }
+      if (gl == 0) mbar_expect_tx(mbar, static_cast<uint32_t>(n) * ROWB);
+      __syncwarp(gmask);
+      if (gl < n) bulk_g2s(sbuf + gl * ROWB, tab + my_off, ROWB, mbar);
+      // overlap the copies with the next chunk's / next bag's index loads
+      if (c0 + CR < end) {
+        pidx = (gl < CR && c0 + CR + gl < end) ? indices[c0 + CR + gl] : IdxT(0);
+      } else if (nbag < n_bags) {
+        bag_bounds(segs, ns, nbag, offsets, nbeg, nend);
+        nidx = (gl < CR && nbeg + gl < nend) ? nindices[nbeg + gl] : IdxT(0);
+        have_next = true;
+      }
+      mbar_wait(mbar, phase);
+      phase ^= 1u;
+      int r = 0;
+      for (; r + 4 <= n; r += 4) {
+        float4 v[4][NCH];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int k = 0; k < NCH; ++k)
+            v[u][k] = *reinterpret_cast<const float4 *>(buf + (r + u) * ROWB + (k * G + gl) * 16);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int k = 0; k < NCH; ++k) {
+            acc[k][0] += static_cast<double>(v[u][k].x);
+            acc[k][1] += static_cast<double>(v[u][k].y);
+            acc[k][2] += static_cast<double>(v[u][k].z);
+            acc[k][3] += static_cast<double>(v[u][k].w);
+          }
+      }
+      for (; r < n; ++r) {
+#pragma unroll
+        for (int k = 0; k < NCH; ++k) {
+          const float4 v = *reinterpret_cast<const float4 *>(buf + r * ROWB + (k * G + gl) * 16);
+          acc[k][0] += static_cast<double>(v.x);
+          acc[k][1] += static_cast<double>(v.y);
+          acc[k][2] += static_cast<double>(v.z);
+          acc[k][3] += static_cast<double>(v.w);
+        }
+      }
+      fence_proxy_async_smem();  // generic reads of buf before the next bulk writes into it
       __syncwarp(gmask);
     }
     if (!have_next && nbag < n_bags) {
