@@ -1,9 +1,10 @@
 #!/bin/bash
-# K4 variant A/B: cp.async (1) vs TMA bulk copies (2), cfg2 and the cold control
+# K4 variant A/B on cfg2 and the cold control
 cd "$(dirname "$0")/.."
-FX_POOL_VARIANT=2 python -m pytest tests/test_gpu_core.py -q -x 2>&1 | tail -1
+VARS=${VARS:-"1 2"}
+for v in $VARS; do FX_POOL_VARIANT=$v python -m pytest tests/test_gpu_core.py -q -x 2>&1 | tail -1; done
 for rep in 1 2; do
-for v in 1 2; do
+for v in $VARS; do
   FX_POOL_VARIANT=$v python bench.py --steps 200 --warmup 10 --no-cpu --no-e2e 2>/dev/null | tail -1 > gpurun_out/ab_cfg2_$v.json
   FX_POOL_VARIANT=$v python bench.py --steps 100 --warmup 10 --no-cpu --no-e2e --alpha 0 --table-rows 4000000 2>/dev/null | tail -1 > gpurun_out/ab_cold_$v.json
   for w in cfg2 cold; do
