@@ -329,7 +329,7 @@ static void launch_async_cr(const fx_segment *segs, int n_segs, int dim, const I
       segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code, sf);
 }
 
-template <int G, int NCH, int CR, typename IdxT, int MODE>
+template <int G, int NCH, int CR, typename IdxT, int MODE, int MINB = FX_POOL_MINB>
 static void launch_bulk_cr(const fx_segment *segs, int n_segs, int dim, const IdxT *ix, const int64_t *offsets,
                            int64_t n_bags, int32_t *counts, int64_t *err, int32_t bad_code, int32_t *err_code,
                            cudaStream_t st, bool sf) {
@@ -337,15 +337,16 @@ static void launch_bulk_cr(const fx_segment *segs, int n_segs, int dim, const Id
   const size_t smem = static_cast<size_t>(WARPS) * (32 / G) * (CR * G * 16 * NCH + 8);
   static int per_sm = -1;
   if (per_sm < 0) {
-    cudaFuncSetAttribute(k_pool_bulk<G, NCH, CR, IdxT, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_pool_bulk<G, NCH, CR, IdxT, MODE, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(smem));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pool_bulk<G, NCH, CR, IdxT, MODE>, WARPS * 32, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pool_bulk<G, NCH, CR, IdxT, MODE, MINB>, WARPS * 32,
+                                                  smem);
     if (per_sm < 1) per_sm = 1;
   }
   int64_t blocks = static_cast<int64_t>(num_sms()) * per_sm;
   const int64_t need = (n_bags + WARPS * (32 / G) - 1) / (WARPS * (32 / G));
   if (blocks > need) blocks = need;
-  k_pool_bulk<G, NCH, CR, IdxT, MODE><<<static_cast<int>(blocks), WARPS * 32, smem, st>>>(
+  k_pool_bulk<G, NCH, CR, IdxT, MODE, MINB><<<static_cast<int>(blocks), WARPS * 32, smem, st>>>(
       segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code, sf);
 }
 
@@ -386,10 +387,12 @@ static int launch_pool(const fx_segment *segs, int n_segs, int dim, const void *
                        cudaStream_t st, bool vec4, bool sf) {
   const IdxT *ix = static_cast<const IdxT *>(indices);
   const int var = pool_variant();
-  if (var == 2 && dim == 128) {
-    launch_bulk_cr<32, 1, 16, IdxT, MODE>(segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code, st,
-                                         sf);
-  } else if (var == 2 && dim == 64) {
+  if (var >= 2 && dim == 128) {
+    // 12-row chunks, <= 72 registers: 7 blocks (28 warps) per SM; tuned on B200
+    // against 16-row / 6-block and 8..14-row / 7..10-block configurations
+    launch_bulk_cr<32, 1, 12, IdxT, MODE, 7>(segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code,
+                                             st, sf);
+  } else if (var >= 2 && dim == 64) {
     launch_bulk_cr<16, 1, 16, IdxT, MODE>(segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code, st,
                                          sf);
   } else if (var >= 1 && dim == 128) {

@@ -234,8 +234,8 @@ namespace fx {
 // is ONE cp.async.bulk (TMA engine, G*16*NCH bytes) issued by one lane and
 // completing on the group's mbarrier, instead of G 16-byte cp.async per row.
 // Same order of accumulation (index order, f64 per column).
-template <int G, int NCH, int CR, typename IdxT, int MODE>
-__global__ void __launch_bounds__(128, FX_POOL_MINB) k_pool_bulk(const fx_segment *__restrict__ segs, int n_segs,
+template <int G, int NCH, int CR, typename IdxT, int MODE, int MINB = FX_POOL_MINB>
+__global__ void __launch_bounds__(128, MINB) k_pool_bulk(const fx_segment *__restrict__ segs, int n_segs,
                                                                 int dim, const IdxT *__restrict__ indices_g,
                                                                 const int64_t *__restrict__ offsets, int64_t n_bags,
                                                                 int32_t *__restrict__ counts, int64_t *err,
