@@ -376,9 +376,8 @@ def main():
                        "init_store_s": round(init_s, 2)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": tr, "peak_source": peak_src,
-                         "kernel": (f"fx::k_pool_bulk<G={min(32, dim // 4)},CR={12 if dim == 128 else 16}> "
-                                    f"(TMA bulk-copy staged gather+pool, "
-                                    f"D={dim})" if os.environ.get("FX_POOL_VARIANT", "2") == "2" and dim in (64, 128)
+                         "kernel": (f"fx::k_pool_bulk<G=32,CR=12> (TMA bulk-copy staged gather+pool, "
+                                    f"D={dim})" if os.environ.get("FX_POOL_VARIANT", "2") == "2" and dim == 128
                                     else f"fx::k_pool_async<G={min(32, dim // 4)},CR=16> (cp.async-staged gather+pool, "
                                          f"D={dim})"),
                          "bytes_per_launch": tot_bytes / launches, "launch_ms": kernel_ms,

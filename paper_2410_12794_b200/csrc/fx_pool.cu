@@ -296,7 +296,7 @@ using namespace fx;
 static int pool_variant() {
   static int v = -1;
   if (v < 0) {
-    // 2 (default): TMA bulk-copy staging for D = 64 / 128, cp.async otherwise;
+    // 2 (default): TMA bulk-copy staging for D = 128 (512-B rows), cp.async otherwise;
     // 1: cp.async staging everywhere; 0: register-staged v4
     const char *e = getenv("FX_POOL_VARIANT");
     v = e ? atoi(e) : 2;
@@ -392,11 +392,6 @@ static int launch_pool(const fx_segment *segs, int n_segs, int dim, const void *
     // against 16-row / 6-block and 8..14-row / 7..10-block configurations
     launch_bulk_cr<32, 1, 12, IdxT, MODE, 7>(segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code,
                                              st, sf);
-  } else if (var >= 2 && dim == 64) {
-    launch_bulk_cr<16, 1, 16, IdxT, MODE>(segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code, st,
-                                         sf);
-  } else if (var >= 1 && dim == 128) {
-    launch_async<32, 1, IdxT, MODE>(segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code, st, sf);
   } else if (var >= 1 && dim == 256) {
     launch_async<32, 2, IdxT, MODE>(segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code, st, sf);
   } else if (var >= 1 && dim == 64) {
