@@ -246,6 +246,8 @@ struct OfferWS {
   int32_t *par_iota;
   int32_t *par_cand;
   int64_t *par_m;
+  double *est_cc;      // est_cand in compacted candidate order (contiguous tile loads)
+  long long *pstate;   // decide -> apply hand-off (see k_offer_par)
 };
 
 __global__ void k_offer_prep(CacheView c, const uint64_t *keys, int64_t n, const int32_t *sizes, OfferWS w) {
@@ -375,10 +377,23 @@ __device__ __forceinline__ double est_v(const CacheView &c, const OfferWS &w, lo
   return w.est_cand[w.acc_j[k - e0]];
 }
 
+__global__ void k_est_compact(const OfferWS w, ParWS pw) {
+  const long long m = pw.m_dev ? *pw.m_dev : pw.m;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < m; t += (int64_t)gridDim.x * blockDim.x)
+    w.est_cc[t] = w.est_cand[pw.cand[t]];
+}
+
+// pstate layout (written by k_offer_par, read by k_offer_apply)
+enum { PS_E0 = 0, PS_H0, PS_NF, PS_N2, PS_TICK0, PS_LOG0, PS_EV0, PS_VALID };
+
+// Decisions only: phases 0/1 and the phase-2 accept/reject sequence. The
+// evictions and installs of phase-2 accepts are applied afterwards by
+// k_offer_apply, in parallel over the accept ranks, so each tile costs one
+// contiguous load of candidate / victim estimates plus the shared-memory
+// resolution.
 __global__ void __launch_bounds__(1024) k_offer_par(CacheView c, const uint64_t *keys, int32_t mode, OfferWS w,
                                                     ParWS pw, int64_t k_vic, int32_t S, uint8_t *accepted,
                                                     int32_t record) {
-  __shared__ long long sh_first;
   __shared__ long long st[8];  // j, h, n_acc, n_ev, tick, ftop, n_log, entries
   const int tid = threadIdx.x;
   Scalars *sc = c.sc;
@@ -395,6 +410,7 @@ __global__ void __launch_bounds__(1024) k_offer_par(CacheView c, const uint64_t 
   if (tid == 0) {
     st[0] = 0; st[1] = 0; st[2] = 0; st[3] = 0;
     st[4] = sc->tick; st[5] = sc->free_top; st[6] = sc->n_evlog; st[7] = e0;
+    w.pstate[PS_VALID] = 0;
   }
   __syncthreads();
   // phase 0: entries beyond cap (budget shrank): evict LRU heads
@@ -446,42 +462,19 @@ __global__ void __launch_bounds__(1024) k_offer_par(CacheView c, const uint64_t 
     __syncthreads();
   }
   if (cap == 0 && st[0] < m && tid == 0) sc->err = 1;  // nothing left to evict: reference KeyError
-  // phase 2: full cache
+  // phase 2 (full cache): every accept evicts the queue head V[h]. Only the
+  // decisions are taken here; acc_j[n_acc + r] = candidate of accept rank r.
+  const long long j0 = st[0], h0 = st[1], nacc0 = st[2];
   const bool always = (mode != 0) || (c.admission != 0);
   if (always) {
-    // every candidate accepted, each evicting V[h + t] (windows <= cap so
-    // victims never refer to candidates accepted inside the same window)
-    const long long win_max = cap < 1024 ? cap : 1024;
-    while (win_max > 0 && st[0] < m) {
-      const long long j = st[0], h = st[1], nacc = st[2];
-      const long long run = (m - j) < win_max ? (m - j) : win_max;
-      for (long long t = tid; t < run; t += blockDim.x) {
-        const long long k = h + t;
-        const int32_t vs = k < e0 ? w.lru_slot[k] : w.acc_slot[k - e0];
-        const uint64_t old = c.skey[vs];
-        w.ev_keys[st[3] + t] = old;
-        if (record && st[6] + t < c.evlog_cap) c.evlog[st[6] + t] = old;
-      }
-      __syncthreads();
-      for (long long t = tid; t < run; t += blockDim.x) {
-        const long long k = h + t;
-        const int32_t vs = k < e0 ? w.lru_slot[k] : w.acc_slot[k - e0];
-        const int32_t jj = pw.cand[j + t];
-        c.skey[vs] = keys[jj];
-        c.stick[vs] = st[4] + t + 1;
-        c.ssize[vs] = S;
-        c.shits[vs] = 0;
-        w.acc_slot[nacc + t] = vs;
-        w.acc_j[nacc + t] = jj;
-        if (accepted) accepted[jj] = 1;
-      }
-      __syncthreads();
-      if (tid == 0) {
-        st[0] += run; st[1] += run; st[2] += run; st[3] += run; st[4] += run;
-        st[6] += record ? run : 0;
-      }
-      __syncthreads();
+    for (long long t = j0 + tid; t < m; t += blockDim.x) {
+      const int32_t jj = pw.cand[t];
+      w.acc_j[nacc0 + (t - j0)] = jj;
+      if (accepted) accepted[jj] = 1;
     }
+    __syncthreads();
+    if (tid == 0 && cap > 0) { st[2] += m - j0; st[0] = m; }
+    __syncthreads();
   } else {
     // sketch admission: tiles of T <= min(1024, cap) candidates. Lane q of warp 0
     // builds mask_q (bit b = est(c_q) >= est(V[h + a0 + b]), a0 = accepts before
@@ -499,7 +492,7 @@ __global__ void __launch_bounds__(1024) k_offer_par(CacheView c, const uint64_t 
     while (tmax > 0 && st[0] < m) {
       const long long j = st[0], h = st[1], nacc = st[2];
       const int T = static_cast<int>((m - j) < tmax ? (m - j) : tmax);
-      for (int t = tid; t < T; t += blockDim.x) s_ec[t] = w.est_cand[pw.cand[j + t]];
+      for (int t = tid; t < T; t += blockDim.x) s_ec[t] = w.est_cc[j + t];
       for (int t = tid; t < T + 32; t += blockDim.x) s_ev[t] = t < cap ? est_v(c, w, h + t, e0, k_vic) : 0.0;
       if (tid == 0) { s_ffa = T; s_ffr = T; }
       __syncthreads();
@@ -567,50 +560,85 @@ __global__ void __launch_bounds__(1024) k_offer_par(CacheView c, const uint64_t 
       __syncthreads();
       const int na = s_chunk_a;
       const int R = s_ffr;  // decisions resolved in this tile (bulk run or the whole tile)
-      // evicted keys (read before any slot is overwritten), then installs
-      for (int t = tid; t < R; t += blockDim.x) {
-        if (!s_acc[t]) continue;
-        const long long k = h + s_rank[t];
-        const int32_t vs = k < e0 ? w.lru_slot[k] : w.acc_slot[k - e0];
-        const uint64_t old = c.skey[vs];
-        w.ev_keys[st[3] + s_rank[t]] = old;
-        if (record && st[6] + s_rank[t] < c.evlog_cap) c.evlog[st[6] + s_rank[t]] = old;
-      }
-      __syncthreads();
       for (int t = tid; t < R; t += blockDim.x) {
         const int32_t jj = pw.cand[j + t];
-        if (!s_acc[t]) {
-          if (accepted) accepted[jj] = 0;
-          continue;
-        }
-        const int r = s_rank[t];
-        const long long k = h + r;
-        const int32_t vs = k < e0 ? w.lru_slot[k] : w.acc_slot[k - e0];
-        c.skey[vs] = keys[jj];
-        c.stick[vs] = st[4] + r + 1;
-        c.ssize[vs] = S;
-        c.shits[vs] = 0;
-        w.acc_slot[nacc + r] = vs;
-        w.acc_j[nacc + r] = jj;
-        if (accepted) accepted[jj] = 1;
+        if (s_acc[t]) w.acc_j[nacc + s_rank[t]] = jj;
+        if (accepted) accepted[jj] = s_acc[t] ? 1 : 0;
       }
-      __syncthreads();
+      __syncthreads();  // acc_j of this tile visible to the next tile's victim estimates
       if (tid == 0) {
-        st[0] += R; st[1] += na; st[2] += na; st[3] += na; st[4] += na;
-        st[6] += record ? na : 0;
+        st[0] += R; st[1] += na; st[2] += na;
       }
       __syncthreads();
     }
   }
   if (tid == 0) {
-    sc->tick = st[4];
+    const long long n2 = st[2] - nacc0;  // phase-2 accepts, each evicting one queue head
+    w.pstate[PS_E0] = e0;
+    w.pstate[PS_H0] = h0;
+    w.pstate[PS_NF] = nacc0;
+    w.pstate[PS_N2] = n2;
+    w.pstate[PS_TICK0] = st[4];  // tick after phase 1
+    w.pstate[PS_LOG0] = st[6];
+    w.pstate[PS_EV0] = st[3];
+    w.pstate[PS_VALID] = 1;
+    sc->tick = st[4] + n2;
     sc->free_top = st[5];
     sc->entries = st[7];
     sc->used = (st[7] + ph) * S;
     sc->n_acc = st[2];
-    sc->n_ev = st[3];
-    sc->n_evlog = st[6];
+    sc->n_ev = st[3] + n2;
+    sc->n_evlog = st[6] + (record ? n2 : 0);
   }
+}
+
+// Side effects of the phase-2 accepts, in parallel over accept ranks r:
+// accept r evicts queue position k = h0 + r of V = [existing entries by LRU]
+// ++ [accepted candidates in order] and takes its slot with tick tick0+r+1.
+// Victims at k >= e0 are candidates accepted earlier in the same call; their
+// slot is followed back to the entry (or free slot) they took. Only the
+// final occupant of a slot writes it (an accept evicted again later in the
+// call leaves its slot to the accept that evicted it).
+__device__ __forceinline__ int32_t apply_slot(const OfferWS &w, long long k, long long e0, long long h0,
+                                              long long nf) {
+  // slot that queue position k occupies
+  while (k >= e0) {
+    const long long i = k - e0;  // index in the accepted list
+    if (i < nf) return w.acc_slot[i];
+    k = h0 + (i - nf);           // phase-2 accept: the slot of its own victim
+  }
+  return w.lru_slot[k];
+}
+
+__global__ void k_offer_apply_keys(CacheView c, const uint64_t *keys, OfferWS w, int32_t record) {
+  if (!w.pstate[PS_VALID]) return;
+  const long long e0 = w.pstate[PS_E0], h0 = w.pstate[PS_H0], nf = w.pstate[PS_NF], n2 = w.pstate[PS_N2];
+  const long long log0 = w.pstate[PS_LOG0], ev0 = w.pstate[PS_EV0];
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n2;
+       r += (long long)gridDim.x * blockDim.x) {
+    const long long k = h0 + r;
+    const uint64_t key = k < e0 ? c.skey[w.lru_slot[k]] : keys[w.acc_j[k - e0]];
+    w.ev_keys[ev0 + r] = key;
+    if (record && log0 + r < c.evlog_cap) c.evlog[log0 + r] = key;
+    w.acc_slot[nf + r] = apply_slot(w, k, e0, h0, nf);
+  }
+}
+
+__global__ void k_offer_apply_slots(CacheView c, const uint64_t *keys, OfferWS w, int32_t S) {
+  if (!w.pstate[PS_VALID]) return;
+  const long long e0 = w.pstate[PS_E0], h0 = w.pstate[PS_H0], nf = w.pstate[PS_NF], n2 = w.pstate[PS_N2];
+  const long long tick0 = w.pstate[PS_TICK0];
+  const long long hend = h0 + n2;  // final queue head
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n2;
+       r += (long long)gridDim.x * blockDim.x) {
+    if (e0 + nf + r < hend) continue;  // evicted again within this call
+    const int32_t s = w.acc_slot[nf + r];
+    c.skey[s] = keys[w.acc_j[nf + r]];
+    c.stick[s] = tick0 + r + 1;
+    c.ssize[s] = S;
+    c.shits[s] = 0;
+  }
+  // phase-1 entries evicted within the call: their slot now belongs to a phase-2 accept
 }
 
 __global__ void k_mark_absent(const uint8_t *present, int64_t n, int32_t *flag) {
@@ -1208,7 +1236,7 @@ size_t offer_ws_bytes(fx_cache *c, int64_t n, size_t *cub_bytes) {
   if (cs > cb) cb = cs;
   *cub_bytes = cb;
   return al(nn * 8) + al(nn * 4) + al(nn) + al(S * 4) + al(S * 8) + al(S * 4 + nn * 4) + al(nn * 4) +
-         al(S * 8 + nn * 8) + al(S * 8) * 2 + al(S * 4) + al(nn * 4) * 3 + al(8) + al(cb);
+         al(S * 8 + nn * 8) + al(S * 8) * 2 + al(S * 4) + al(nn * 4) * 3 + al(8) + al(nn * 8) + al(64) + al(cb);
 }
 
 OfferWS carve_offer_ws(fx_cache *c, int64_t n, void **cub_tmp) {
@@ -1231,6 +1259,8 @@ OfferWS carve_offer_ws(fx_cache *c, int64_t n, void **cub_tmp) {
   w.par_iota = reinterpret_cast<int32_t *>(p); p += al(nn * 4);
   w.par_cand = reinterpret_cast<int32_t *>(p); p += al(nn * 4);
   w.par_m = reinterpret_cast<int64_t *>(p); p += al(8);
+  w.est_cc = reinterpret_cast<double *>(p); p += al(nn * 8);
+  w.pstate = reinterpret_cast<long long *>(p); p += al(64);
   *cub_tmp = p;
   return w;
 }
@@ -1294,7 +1324,10 @@ int run_offer(fx_cache *c, const uint64_t *keys, int64_t n, int32_t mode, const 
     cub::DeviceSelect::Flagged(cub_tmp, cb, w.par_iota, w.par_flag, w.par_cand, w.par_m, static_cast<int>(n), st);
     k_present_accept<<<grid_for(n, 256), 256, 0, st>>>(w.present, n, mode, accepted);
     ParWS pw{w.par_cand, n, w.par_m};
+    k_est_compact<<<grid_for(n, 256), 256, 0, st>>>(w, pw);
     k_offer_par<<<1, 1024, 0, st>>>(c->v, keys, mode, w, pw, k_vic, c->uniform, accepted, c->record);
+    k_offer_apply_keys<<<grid_for(n, 256), 256, 0, st>>>(c->v, keys, w, c->record);
+    k_offer_apply_slots<<<grid_for(n, 256), 256, 0, st>>>(c->v, keys, w, c->uniform);
   } else if (c->uniform > 0 && n == 0 && h.used > h.budget) {
     ParWS pw{w.par_cand, 0, nullptr};
     k_offer_par<<<1, 1024, 0, st>>>(c->v, keys, mode, w, pw, k_vic, c->uniform, accepted, c->record);
