@@ -507,12 +507,18 @@ def run_sharded(args, rank, world, local):
         # bytes crossing NVLink per step from this rank as owner: pooled rows (+ indices read) to the
         # other ranks; table-wise f32 rows, row-wise f64 partials
         per_row = dim * (4 if mode == "tablewise" or args.partial == "f32" else 8)
-        rows_out = (world - 1) * (B * sum(1 for s in placement if s.server_id == rank) if mode == "tablewise"
-                                  else B * F)
+        if mode == "tablewise" and hasattr(sl, "execu"):
+            # (requester, feature) pairs this rank pools for OTHER requesters
+            rows_out = B * sum(1 for q in range(world) if q != rank for f in range(F) if sl.execu[q][f] == rank)
+        else:
+            rows_out = (world - 1) * (B * sum(1 for s in placement if s.server_id == rank) if mode == "tablewise"
+                                      else B * F)
         a2a_bytes = rows_out * per_row
     sl.ops.check() if hasattr(sl, "ops") else None
     total_alg = sum(algorithmic_bytes(hb, dim) for hb in host_batches) / len(host_batches)
-    if mode == "tablewise":
+    if mode == "tablewise" and hasattr(sl, "execu"):
+        share = sum(1 for q in range(world) for f in range(F) if sl.execu[q][f] == rank) / (F * world)
+    elif mode == "tablewise":
         owned = sum(1 for s in placement if s.server_id == rank)
         share = (owned * world + len(repl)) / (F * world)
     else:

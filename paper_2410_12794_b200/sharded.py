@@ -433,7 +433,8 @@ class P2PShardedLookup:
 
     def __init__(self, metas, placement, seed: int, feature_tables, feature_ops, batch_size: int, rank: int,
                  world: int, device, group=None, mode: str = "tablewise", max_nnz: int | None = None,
-                 replicated_tables=(), partial_dtype: str = "f64", pushdown_threshold: int | None = None):
+                 replicated_tables=(), partial_dtype: str = "f64", pushdown_threshold: int | None = None,
+                 balance_replicated: bool = True):
         """`replicated_tables` (table-wise mode): tables held in full by every
         rank and pooled locally for the rank's own batch (no exchange); they
         must not appear in `placement`. The other tables are table-sharded.
@@ -494,9 +495,12 @@ class P2PShardedLookup:
             for t, o in tab_owner.items():
                 if len(o) != 1:
                     raise ConfigError(f"table-wise mode needs one owner per table (table {t})")
-            # requester-relative owner: replicated features are served by the requester itself
             self.tw_owner = [(-1 if t in self.replicated else next(iter(tab_owner[t]))) for t in self.ftab]
-            self.feat_owner = [rank if o < 0 else o for o in self.tw_owner]
+            # executor of every (requester, feature): the owner for sharded tables;
+            # replicated tables can be pooled by ANY rank, so they are spread to
+            # even out the per-rank gather work (deterministic: same on every rank)
+            self.execu = self._assign_executors(W, balance_replicated)
+            self.feat_owner = list(self.execu[rank])
         self.max_nnz = int(max_nnz) if max_nnz is not None else n_bags * 64
         # every rank must use the same slot geometry (requesters address peers' slots)
         agreed = [None] * W
@@ -508,11 +512,9 @@ class P2PShardedLookup:
         if mode == "tablewise":
             # owner-side staging: one slot per requester holding the indices and
             # rebased offsets of the features this rank owns (pushed by requesters)
-            n_repl = sum(1 for o in self.tw_owner if o < 0)
-            # slot (q -> d) holds d's table-wise features, plus the replicated ones when q == d
-            self.slot_feats = lambda q, d: [f for f in range(F) if self.tw_owner[f] == d or
-                                            (self.tw_owner[f] < 0 and q == d)]
-            self.slot_stride = [sum(1 for o in self.tw_owner if o == d) + n_repl for d in range(W)]
+            # slot (q -> d): the features requester q has executed by rank d
+            self.slot_feats = lambda q, d: [f for f in range(F) if self.execu[q][f] == d]
+            self.slot_stride = [max(len(self.slot_feats(q, d)) for q in range(W)) for d in range(W)]
             offs_slot = lambda d: (self.slot_stride[d] * B + 1) * 8
             out_set = n_bags * D * 4
         else:
@@ -631,6 +633,29 @@ class P2PShardedLookup:
         self.timeline = []
         self.launches = 0  # our kernels launched (libflexemb), for bench accounting
         self._barrier_waits = []
+
+    def _assign_executors(self, W: int, balance: bool):
+        """[q][f] -> rank that pools requester q's bags of feature f. Sharded
+        features go to their owner (W units of B bags each); a requester's
+        replicated features stay local while its rank is under the mean load
+        ceil(total / W), the rest go to the least-loaded rank."""
+        F = self.F
+        execu = [[self.tw_owner[f] if self.tw_owner[f] >= 0 else q for f in range(F)] for q in range(W)]
+        repl = [f for f in range(F) if self.tw_owner[f] < 0]
+        if not balance or not repl:
+            return execu
+        load = [0] * W
+        for f in range(F):
+            if self.tw_owner[f] >= 0:
+                load[self.tw_owner[f]] += W
+        cap = -(-(sum(load) + len(repl) * W) // W)
+        for q in range(W):
+            for f in repl:
+                d = q if load[q] < cap else min(range(W), key=lambda r: (load[r], r != q, r))
+                execu[q][f] = d
+                load[d] += 1
+        self.exec_load = load
+        return execu
 
     def _barrier(self):
         self.launches += 1
