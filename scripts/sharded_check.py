@@ -99,6 +99,28 @@ def main():
                 worst = max(worst, O.tolerance_ratio(ref, got))
                 exact += ref.tobytes() == got.tobytes()
                 n += 1
+    # edge cases: a batch whose bags are all empty, and one with every other bag empty
+    empty_bad = 0.0
+    if not pipelined and exchange in ("p2p", "nccl", "p2pf32", "p2phybrid"):
+        F = len(rows)
+        offs0 = torch.zeros(F * B + 1, dtype=torch.int64, device="cuda")
+        o = sl.lookup(torch.zeros(0, dtype=torch.int32, device="cuda"), offs0).cpu().numpy()
+        empty_bad += float(np.abs(o).max()) if o.size else 0.0
+        hb = hbs[1]
+        lens = np.diff(hb.offsets)
+        keep = np.arange(F * B) % 2 == 0
+        new_lens = np.where(keep, lens, 0)
+        new_offs = np.concatenate([[0], np.cumsum(new_lens)]).astype(np.int64)
+        new_idx = np.concatenate([hb.indices[hb.offsets[b]:hb.offsets[b + 1]] for b in range(F * B) if keep[b]])
+        o = sl.lookup(torch.from_numpy(new_idx).cuda(), torch.from_numpy(new_offs).cuda()).cpu().numpy()
+        for b in range(F * B):
+            f, s_ = divmod(b, B)
+            got = o[s_, f * D:(f + 1) * D]
+            if keep[b]:
+                ref = O.pool_flat(O.rows_of(0, f, D, new_idx[new_offs[b]:new_offs[b + 1]]), ops[f])
+                empty_bad += 0.0 if O.within_tolerance(ref, got) else 1.0
+            else:
+                empty_bad += float(np.abs(got).max())
     # ingress validation (ranker.py:184-193): an out-of-range index on rank 1's
     # batch raises LookupValidationError there; every rank recovers next step
     val_bad = 0.0
@@ -119,15 +141,15 @@ def main():
         out = sl.lookup(torch.from_numpy(hb.indices).cuda(), torch.from_numpy(hb.offsets).cuda()).cpu().numpy()
         ref = O.pool_flat(O.rows_of(0, 0, D, hb.indices[hb.offsets[0]:hb.offsets[1]]), ops[0])
         val_bad += 0.0 if O.within_tolerance(ref, out[0, :D]) else 1.0
-    t = torch.tensor([worst, float(n - exact), float(cnt_bad), float(hier_exact), val_bad], device="cuda",
-                     dtype=torch.float64)
+    t = torch.tensor([worst, float(n - exact), float(cnt_bad), float(hier_exact), val_bad, empty_bad],
+                     device="cuda", dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     if rank == 0:
         print(f"SHARDED {mode} {exchange}{('-host' if hosted else '-pipe') if pipelined else ''} world={world} worst_tolerance_ratio={t[0].item():.4f} "
               f"max_non_bit_exact_bags={int(t[1].item())} bags_per_rank={n} counter_mismatches={int(t[2].item())} "
-              f"non_bit_exact_vs_reference_combine={int(t[3].item())} validation_failures={int(t[4].item())}",
-              flush=True)
-    ok = t[0].item() <= 1.0 and t[2].item() == 0 and t[3].item() == 0 and t[4].item() == 0
+              f"non_bit_exact_vs_reference_combine={int(t[3].item())} validation_failures={int(t[4].item())} "
+              f"empty_bag_failures={t[5].item():g}", flush=True)
+    ok = t[0].item() <= 1.0 and t[2].item() == 0 and t[3].item() == 0 and t[4].item() == 0 and t[5].item() == 0
     dist.destroy_process_group()
     sys.exit(0 if ok else 1)
 
