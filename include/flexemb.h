@@ -124,7 +124,9 @@ int fx_gather_rows(const float *table, int64_t ld, int64_t row_begin, int64_t ro
  * partial_is_f32: each partial already rounded once, as PartialResult) (row stride
  * p_stride); counts: n_src pointers to int32[n_bags] (NULL -> partial absent
  * for every bag). raw_offsets/raw_rows: optional CSR of f32 raw vectors
- * (raw_rows row stride = dim), may be NULL. ops: int32[n_bags] or NULL (all
+ * (raw_rows row stride = dim), may be NULL. When dim % 4 == 0 the kernel
+ * reads and writes 16-byte vectors: partial rows, raw rows and out rows must
+ * then start on 16-byte boundaries. ops: int32[n_bags] or NULL (all
  * `op`). out row stride = out_stride. Bags with nothing to combine get
  * zeros and set *err_code = FX_E_EMPTY if err_code != NULL. */
 int fx_combine(const void *const *partials, int32_t partial_is_f32, const int32_t *const *counts, int32_t n_src,

@@ -101,7 +101,7 @@ __device__ __forceinline__ int route_dest(const int64_t *route_off, const int64_
 }
 
 // one warp per bag: counts[d * n_bags + b] = #indices of bag b owned by rank d
-template <typename IdxT>
+template <typename IdxT, int WM>
 __global__ void __launch_bounds__(256) k_rw_count(const int64_t *route_off, const int64_t *starts,
                                                   const int32_t *owners, const int32_t *bag_table,
                                                   const IdxT *indices, const int64_t *offsets, int64_t n_bags,
@@ -113,9 +113,9 @@ __global__ void __launch_bounds__(256) k_rw_count(const int64_t *route_off, cons
   for (int64_t b = warp; b < n_bags; b += nw) {
     const int t = bag_table[b];
     const int64_t beg = offsets[b], end = offsets[b + 1];
-    int cnt[32];  // per-destination counts (warp-uniform, register-resident after unrolling)
+    int cnt[WM];  // per-destination counts (warp-uniform, register-resident after unrolling)
 #pragma unroll
-    for (int d = 0; d < 32; ++d) cnt[d] = 0;
+    for (int d = 0; d < WM; ++d) cnt[d] = 0;
     int hits = 0;
     for (int64_t c0 = beg; c0 < end; c0 += 32) {
       const bool on = c0 + lane < end;
@@ -125,11 +125,11 @@ __global__ void __launch_bounds__(256) k_rw_count(const int64_t *route_off, cons
                            : -1;
       hits += __popc(__ballot_sync(0xffffffffu, hit));
 #pragma unroll
-      for (int d = 0; d < 32; ++d)
+      for (int d = 0; d < WM; ++d)
         if (d < W) cnt[d] += __popc(__ballot_sync(0xffffffffu, my_d == d));
     }
 #pragma unroll
-    for (int d = 0; d < 32; ++d)
+    for (int d = 0; d < WM; ++d)
       if (d < W && lane == 0) counts[(int64_t)d * n_bags + b] = cnt[d];
     if (hit_cnt && lane == 0) hit_cnt[b] = hits;
   }
@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(256) k_rw_count(const int64_t *route_off, cons
 
 // one warp per bag: stable per-destination scatter of the bag's indices into
 // rank d's staging slot (IPC pointer dst_idx[d]) at scan[d*n_bags+b] - scan[d*n_bags] + rank
-template <typename IdxT>
+template <typename IdxT, int WM>
 __global__ void __launch_bounds__(256) k_rw_push(const int64_t *route_off, const int64_t *starts,
                                                  const int32_t *owners, const int32_t *bag_table,
                                                  const IdxT *indices, const int64_t *offsets, int64_t n_bags, int W,
@@ -146,13 +146,19 @@ __global__ void __launch_bounds__(256) k_rw_push(const int64_t *route_off, const
   const unsigned lt = (1u << lane) - 1u;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  int32_t *dst[WM];
+  int64_t base[WM];
+#pragma unroll
+  for (int d = 0; d < WM; ++d) {
+    dst[d] = d < W ? dst_idx[d] : nullptr;
+    base[d] = d < W ? scan[(int64_t)d * n_bags] : 0;
+  }
   for (int64_t b = warp; b < n_bags; b += nw) {
     const int t = bag_table[b];
     const int64_t beg = offsets[b], end = offsets[b + 1];
-    int64_t run[32];
+    int run[WM];
 #pragma unroll
-    for (int d = 0; d < 32; ++d)
-      run[d] = d < W ? scan[(int64_t)d * n_bags + b] - scan[(int64_t)d * n_bags] : 0;
+    for (int d = 0; d < WM; ++d) run[d] = d < W ? static_cast<int>(scan[(int64_t)d * n_bags + b] - base[d]) : 0;
     for (int64_t c0 = beg; c0 < end; c0 += 32) {
       const bool on = c0 + lane < end;
       int64_t idx = 0;
@@ -162,10 +168,10 @@ __global__ void __launch_bounds__(256) k_rw_push(const int64_t *route_off, const
         my_d = route_dest(route_off, starts, owners, t, idx);
       }
 #pragma unroll
-      for (int d = 0; d < 32; ++d) {
+      for (int d = 0; d < WM; ++d) {
         if (d < W) {
           const unsigned m = __ballot_sync(0xffffffffu, my_d == d);
-          if (my_d == d) dst_idx[d][run[d] + __popc(m & lt)] = static_cast<int32_t>(idx);
+          if (my_d == d) dst[d][run[d] + __popc(m & lt)] = static_cast<int32_t>(idx);
           run[d] += __popc(m);
         }
       }
@@ -273,7 +279,7 @@ __global__ void __launch_bounds__(256) k_rw_raw(const int64_t *route_off, const 
 }
 
 // k_rw_push restricted to pushed-down groups (counts[d][b] > 0 after the plan)
-template <typename IdxT>
+template <typename IdxT, int WM>
 __global__ void __launch_bounds__(256) k_rw_push_planned(const int64_t *route_off, const int64_t *starts,
                                                          const int32_t *owners, const int32_t *bag_table,
                                                          const IdxT *indices, const int64_t *offsets, int64_t n_bags,
@@ -283,14 +289,21 @@ __global__ void __launch_bounds__(256) k_rw_push_planned(const int64_t *route_of
   const unsigned lt = (1u << lane) - 1u;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  int32_t *dst[WM];
+  int64_t base[WM];
+#pragma unroll
+  for (int d = 0; d < WM; ++d) {
+    dst[d] = d < W ? dst_idx[d] : nullptr;
+    base[d] = d < W ? scan[(int64_t)d * n_bags] : 0;
+  }
   for (int64_t b = warp; b < n_bags; b += nw) {
     const int t = bag_table[b];
     const int64_t beg = offsets[b], end = offsets[b + 1];
-    int64_t run[32];
+    int run[WM];
     unsigned pushed = 0;
 #pragma unroll
-    for (int d = 0; d < 32; ++d) {
-      run[d] = d < W ? scan[(int64_t)d * n_bags + b] - scan[(int64_t)d * n_bags] : 0;
+    for (int d = 0; d < WM; ++d) {
+      run[d] = d < W ? static_cast<int>(scan[(int64_t)d * n_bags + b] - base[d]) : 0;
       if (d < W && counts[(int64_t)d * n_bags + b] > 0) pushed |= 1u << d;
     }
     if (!pushed) continue;
@@ -304,10 +317,10 @@ __global__ void __launch_bounds__(256) k_rw_push_planned(const int64_t *route_of
         if (!((pushed >> my_d) & 1u)) my_d = -1;
       }
 #pragma unroll
-      for (int d = 0; d < 32; ++d) {
+      for (int d = 0; d < WM; ++d) {
         if (d < W && ((pushed >> d) & 1u)) {
           const unsigned m = __ballot_sync(0xffffffffu, my_d == d);
-          if (my_d == d) dst_idx[d][run[d] + __popc(m & lt)] = static_cast<int32_t>(idx);
+          if (my_d == d) dst[d][run[d] + __popc(m & lt)] = static_cast<int32_t>(idx);
           run[d] += __popc(m);
         }
       }
@@ -315,6 +328,17 @@ __global__ void __launch_bounds__(256) k_rw_push_planned(const int64_t *route_of
   }
   __threadfence_system();
 }
+
+static inline int wm_for(int W) { return W <= 2 ? 2 : W <= 4 ? 4 : W <= 8 ? 8 : W <= 16 ? 16 : 32; }
+
+#define FX_WM_SWITCH(W, CALL) \
+  switch (wm_for(W)) {        \
+    case 2: CALL(2); break;   \
+    case 4: CALL(4); break;   \
+    case 8: CALL(8); break;   \
+    case 16: CALL(16); break; \
+    default: CALL(32); break; \
+  }
 
 }  // namespace fx
 
@@ -398,21 +422,27 @@ int fx_rw_push(const int64_t *route_off, const int64_t *starts, const int32_t *o
   cudaStream_t st = as_stream(stream);
   cudaMemsetAsync(counts, 0, n * sizeof(int32_t), st);
   const int grid = grid_for(n_bags * 32, 256);
-  if (idx_type == FX_IDX_I32)
-    k_rw_count<int32_t><<<grid, 256, 0, st>>>(route_off, starts, owners, bag_table,
-                                              static_cast<const int32_t *>(indices), offsets, n_bags, W, counts);
-  else
-    k_rw_count<int64_t><<<grid, 256, 0, st>>>(route_off, starts, owners, bag_table,
-                                              static_cast<const int64_t *>(indices), offsets, n_bags, W, counts);
+#define FX_COUNT(WM)                                                                                          \
+  if (idx_type == FX_IDX_I32)                                                                                 \
+    k_rw_count<int32_t, WM><<<grid, 256, 0, st>>>(route_off, starts, owners, bag_table,                       \
+                                                  static_cast<const int32_t *>(indices), offsets, n_bags, W, counts); \
+  else                                                                                                        \
+    k_rw_count<int64_t, WM><<<grid, 256, 0, st>>>(route_off, starts, owners, bag_table,                       \
+                                                  static_cast<const int64_t *>(indices), offsets, n_bags, W, counts);
+  FX_WM_SWITCH(W, FX_COUNT)
+#undef FX_COUNT
   cub::DeviceScan::ExclusiveSum(ws, need, counts, scan, static_cast<int>(n), st);
-  if (idx_type == FX_IDX_I32)
-    k_rw_push<int32_t><<<grid, 256, 0, st>>>(route_off, starts, owners, bag_table,
-                                             static_cast<const int32_t *>(indices), offsets, n_bags, W, scan, dst_idx,
-                                             true);
-  else
-    k_rw_push<int64_t><<<grid, 256, 0, st>>>(route_off, starts, owners, bag_table,
-                                             static_cast<const int64_t *>(indices), offsets, n_bags, W, scan, dst_idx,
-                                             true);
+#define FX_PUSH(WM)                                                                                            \
+  if (idx_type == FX_IDX_I32)                                                                                  \
+    k_rw_push<int32_t, WM><<<grid, 256, 0, st>>>(route_off, starts, owners, bag_table,                         \
+                                                 static_cast<const int32_t *>(indices), offsets, n_bags, W, scan,   \
+                                                 dst_idx, true);                                               \
+  else                                                                                                         \
+    k_rw_push<int64_t, WM><<<grid, 256, 0, st>>>(route_off, starts, owners, bag_table,                         \
+                                                 static_cast<const int64_t *>(indices), offsets, n_bags, W, scan,   \
+                                                 dst_idx, true);
+  FX_WM_SWITCH(W, FX_PUSH)
+#undef FX_PUSH
   k_rw_push_offsets<<<grid_for((int64_t)W * (n_bags + 1), 256), 256, 0, st>>>(scan, n_bags, W, dst_offs, true);
   FX_LAUNCH_CHECK("fx_rw_push");
   return FX_OK;
@@ -449,14 +479,17 @@ int fx_rw_push_planned(const int64_t *route_off, const int64_t *starts, const in
   cudaStream_t st = as_stream(stream);
   cudaMemsetAsync(counts, 0, n * sizeof(int32_t), st);
   const int grid = grid_for(n_bags * 32, 256);
-  if (idx_type == FX_IDX_I32)
-    k_rw_count<int32_t><<<grid, 256, 0, st>>>(route_off, starts, owners, bag_table,
-                                              static_cast<const int32_t *>(indices), offsets, n_bags, W, counts,
-                                              hit_slot, hit_cnt);
-  else
-    k_rw_count<int64_t><<<grid, 256, 0, st>>>(route_off, starts, owners, bag_table,
-                                              static_cast<const int64_t *>(indices), offsets, n_bags, W, counts,
-                                              hit_slot, hit_cnt);
+#define FX_COUNT(WM)                                                                                        \
+  if (idx_type == FX_IDX_I32)                                                                               \
+    k_rw_count<int32_t, WM><<<grid, 256, 0, st>>>(route_off, starts, owners, bag_table,                     \
+                                                  static_cast<const int32_t *>(indices), offsets, n_bags, W, \
+                                                  counts, hit_slot, hit_cnt);                               \
+  else                                                                                                      \
+    k_rw_count<int64_t, WM><<<grid, 256, 0, st>>>(route_off, starts, owners, bag_table,                     \
+                                                  static_cast<const int64_t *>(indices), offsets, n_bags, W, \
+                                                  counts, hit_slot, hit_cnt);
+  FX_WM_SWITCH(W, FX_COUNT)
+#undef FX_COUNT
   k_rw_plan<<<grid_for(n_bags + 1, 256), 256, 0, st>>>(counts, n_bags, W, threshold, raw_cnt, counters, hit_cnt);
   cub::DeviceScan::ExclusiveSum(ws, cb, raw_cnt, raw_off, static_cast<int>(n_bags + 1), st);
   cb = cub_bytes;
@@ -465,16 +498,22 @@ int fx_rw_push_planned(const int64_t *route_off, const int64_t *starts, const in
     k_rw_raw<int32_t><<<grid, 256, 0, st>>>(route_off, starts, owners, nrows, bag_table,
                                             static_cast<const int32_t *>(indices), offsets, n_bags, counts, raw_off,
                                             shard_base, ld, raw_ptr, hit_slot, cache_rows, cache_ld);
-    k_rw_push_planned<int32_t><<<grid, 256, 0, st>>>(route_off, starts, owners, bag_table,
-                                                     static_cast<const int32_t *>(indices), offsets, n_bags, W,
-                                                     counts, scan, dst_idx, hit_slot);
+#define FX_PP(WM)                                                                                             \
+  k_rw_push_planned<int32_t, WM><<<grid, 256, 0, st>>>(route_off, starts, owners, bag_table,                   \
+                                                       static_cast<const int32_t *>(indices), offsets, n_bags, W, \
+                                                       counts, scan, dst_idx, hit_slot);
+    FX_WM_SWITCH(W, FX_PP)
+#undef FX_PP
   } else {
     k_rw_raw<int64_t><<<grid, 256, 0, st>>>(route_off, starts, owners, nrows, bag_table,
                                             static_cast<const int64_t *>(indices), offsets, n_bags, counts, raw_off,
                                             shard_base, ld, raw_ptr, hit_slot, cache_rows, cache_ld);
-    k_rw_push_planned<int64_t><<<grid, 256, 0, st>>>(route_off, starts, owners, bag_table,
-                                                     static_cast<const int64_t *>(indices), offsets, n_bags, W,
-                                                     counts, scan, dst_idx, hit_slot);
+#define FX_PP(WM)                                                                                             \
+  k_rw_push_planned<int64_t, WM><<<grid, 256, 0, st>>>(route_off, starts, owners, bag_table,                   \
+                                                       static_cast<const int64_t *>(indices), offsets, n_bags, W, \
+                                                       counts, scan, dst_idx, hit_slot);
+    FX_WM_SWITCH(W, FX_PP)
+#undef FX_PP
   }
   k_rw_push_offsets<<<grid_for((int64_t)W * (n_bags + 1), 256), 256, 0, st>>>(scan, n_bags, W, dst_offs, true);
   FX_LAUNCH_CHECK("fx_rw_push_planned");

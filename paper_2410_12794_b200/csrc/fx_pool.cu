@@ -289,9 +289,79 @@ __global__ void __launch_bounds__(256) k_combine(const void *const *__restrict__
   }
 }
 
+// K5 with 16-byte accesses (dim % 4 == 0, 16-B aligned rows): each lane owns
+// 4 consecutive columns; per column the same order as k_combine (partials by
+// ascending source, then raw rows in order, f64, one rounding).
+__global__ void __launch_bounds__(256) k_combine_v4(const void *const *__restrict__ partials, int p_f32,
+                                                    const int32_t *const *__restrict__ counts, int n_src,
+                                                    int64_t p_stride, const int64_t *__restrict__ raw_offsets,
+                                                    const float *__restrict__ raw_rows,
+                                                    const float *const *__restrict__ raw_ptrs, int64_t n_bags,
+                                                    int dim, int op, const int32_t *__restrict__ ops,
+                                                    float *__restrict__ out, int64_t out_stride, int32_t *err_code) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (gridDim.x * (int64_t)blockDim.x) >> 5;
+  for (int64_t b = warp; b < n_bags; b += nwarps) {
+    int64_t total = 0;
+    unsigned present = 0;  // n_src <= 32
+    for (int s = 0; s < n_src; ++s) {
+      const int32_t c = counts && counts[s] ? counts[s][b] : 1;
+      if (c > 0) {
+        total += c;
+        present |= 1u << s;
+      }
+    }
+    int64_t r0 = 0, r1 = 0;
+    if (raw_offsets) {
+      r0 = raw_offsets[b];
+      r1 = raw_offsets[b + 1];
+    }
+    total += r1 - r0;
+    if (present == 0 && r1 == r0 && err_code && lane == 0) atomicExch(err_code, FX_E_EMPTY);
+    const int bop = ops ? ops[b] : op;
+    for (int c = lane * 4; c < dim; c += 128) {
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      for (int s = 0; s < n_src; ++s) {
+        if (!((present >> s) & 1u)) continue;
+        if (p_f32) {
+          const float4 v = *reinterpret_cast<const float4 *>(static_cast<const float *>(partials[s]) + b * p_stride + c);
+          a0 += static_cast<double>(v.x); a1 += static_cast<double>(v.y);
+          a2 += static_cast<double>(v.z); a3 += static_cast<double>(v.w);
+        } else {
+          const double *pp = static_cast<const double *>(partials[s]) + b * p_stride + c;
+          const double2 u = *reinterpret_cast<const double2 *>(pp);
+          const double2 w = *reinterpret_cast<const double2 *>(pp + 2);
+          a0 += u.x; a1 += u.y; a2 += w.x; a3 += w.y;
+        }
+      }
+      for (int64_t r = r0; r < r1; ++r) {
+        const float *row = raw_ptrs ? raw_ptrs[r] : raw_rows + r * dim;
+        const float4 v = *reinterpret_cast<const float4 *>(row + c);
+        a0 += static_cast<double>(v.x); a1 += static_cast<double>(v.y);
+        a2 += static_cast<double>(v.z); a3 += static_cast<double>(v.w);
+      }
+      if (bop == FX_OP_MEAN && total > 0) {
+        const double dn = static_cast<double>(total);
+        a0 /= dn; a1 /= dn; a2 /= dn; a3 /= dn;
+      }
+      *reinterpret_cast<float4 *>(out + b * out_stride + c) =
+          make_float4(__double2float_rn(a0), __double2float_rn(a1), __double2float_rn(a2), __double2float_rn(a3));
+    }
+  }
+}
+
 }  // namespace fx
 
 using namespace fx;
+
+// 16-byte path when every row start is 16-B aligned
+static bool combine_vec4_ok(const void *const *partials, int32_t n_src, int64_t p_stride, int64_t dim,
+                            int64_t out_stride, const float *out) {
+  (void)partials;
+  return n_src <= 32 && dim % 4 == 0 && p_stride % 4 == 0 && out_stride % 4 == 0 &&
+         (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+}
 
 static int pool_variant() {
   static int v = -1;
@@ -511,9 +581,14 @@ int fx_combine(const void *const *partials, int32_t partial_is_f32, const int32_
     return FX_E_CONFIG;
   }
   if (n_bags == 0) return FX_OK;
-  k_combine<<<grid_for(n_bags * 32, 256), 256, 0, as_stream(stream)>>>(
-      partials, partial_is_f32, counts, n_src, p_stride, raw_offsets, raw_rows, nullptr, n_bags, dim, op, ops, out,
-      out_stride, err_code);
+  if (combine_vec4_ok(partials, n_src, p_stride, dim, out_stride, out) && (reinterpret_cast<uintptr_t>(raw_rows) & 15) == 0)
+    k_combine_v4<<<grid_for(n_bags * 32, 256), 256, 0, as_stream(stream)>>>(
+        partials, partial_is_f32, counts, n_src, p_stride, raw_offsets, raw_rows, nullptr, n_bags, dim, op, ops, out,
+        out_stride, err_code);
+  else
+    k_combine<<<grid_for(n_bags * 32, 256), 256, 0, as_stream(stream)>>>(
+        partials, partial_is_f32, counts, n_src, p_stride, raw_offsets, raw_rows, nullptr, n_bags, dim, op, ops,
+        out, out_stride, err_code);
   FX_LAUNCH_CHECK("fx_combine");
   return FX_OK;
 }
@@ -527,9 +602,14 @@ int fx_combine_ptr(const void *const *partials, int32_t partial_is_f32, const in
     return FX_E_CONFIG;
   }
   if (n_bags == 0) return FX_OK;
-  k_combine<<<grid_for(n_bags * 32, 256), 256, 0, as_stream(stream)>>>(
-      partials, partial_is_f32, counts, n_src, p_stride, raw_offsets, nullptr, raw_ptrs, n_bags, dim, op, ops, out,
-      out_stride, err_code);
+  if (combine_vec4_ok(partials, n_src, p_stride, dim, out_stride, out))
+    k_combine_v4<<<grid_for(n_bags * 32, 256), 256, 0, as_stream(stream)>>>(
+        partials, partial_is_f32, counts, n_src, p_stride, raw_offsets, nullptr, raw_ptrs, n_bags, dim, op, ops, out,
+        out_stride, err_code);
+  else
+    k_combine<<<grid_for(n_bags * 32, 256), 256, 0, as_stream(stream)>>>(
+        partials, partial_is_f32, counts, n_src, p_stride, raw_offsets, nullptr, raw_ptrs, n_bags, dim, op, ops,
+        out, out_stride, err_code);
   FX_LAUNCH_CHECK("fx_combine_ptr");
   return FX_OK;
 }
