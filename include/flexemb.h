@@ -134,11 +134,14 @@ int fx_combine(const void *const *partials, int32_t partial_is_f32, const int32_
                int64_t n_bags, int32_t dim, int32_t op, const int32_t *ops,
                float *out, int64_t out_stride, int32_t *err_code, void *stream);
 /* fx_combine with raw vectors given as row pointers (raw_ptrs[r], e.g. rows
- * in a peer GPU's shard read over NVLink) instead of a packed raw_rows array */
+ * in a peer GPU's shard read over NVLink; NULL = none) instead of a packed
+ * raw_rows array. sample_major_B > 0: bags are table-major (b = f*B + s) and
+ * bag b is written to out + s * out_stride + f * dim, i.e. straight into a
+ * sample-major [B, F*dim] batch output; 0: out + b * out_stride. */
 int fx_combine_ptr(const void *const *partials, int32_t partial_is_f32, const int32_t *const *counts, int32_t n_src,
                    int64_t p_stride, const int64_t *raw_offsets, const float *const *raw_ptrs, int64_t n_bags,
                    int32_t dim, int32_t op, const int32_t *ops, float *out, int64_t out_stride, int32_t *err_code,
-                   void *stream);
+                   int64_t sample_major_B, void *stream);
 
 /* ---- K1: range routing (routing.py:87-97 resolve_many, 117-148) ---------
  * For occurrence i of a bag of table t:

@@ -105,7 +105,7 @@ _SIGS = {
     "fx_rw_push": ([_P, _P, _P, _P, _P, _I32, _P, _I64, _I32, _P, _P, _P, _P, _P, _SZP, _P], ctypes.c_int),
     "fx_rw_push_planned": ([_P, _P, _P, _P, _P, _P, _I32, _P, _I64, _I32, _I32, _P, _P, _P, _P, _P, _I64, _P, _P, _P,
                             _P, _P, _I64, _P, _SZP, _P], ctypes.c_int),
-    "fx_combine_ptr": ([_P, _I32, _P, _I32, _I64, _P, _P, _I64, _I32, _I32, _P, _P, _I64, _P, _P], ctypes.c_int),
+    "fx_combine_ptr": ([_P, _I32, _P, _I32, _I64, _P, _P, _I64, _I32, _I32, _P, _P, _I64, _P, _I64, _P], ctypes.c_int),
     # cache entry points are typed in cache.py (_sig); listed here for export checks
     **{n: (None, ctypes.c_int) for n in (
         "fx_cache_create", "fx_cache_destroy", "fx_cache_set_tables", "fx_cache_scalars", "fx_cache_reserve_sketch",

@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(256) k_combine(const void *const *__restrict__
                                                  const float *__restrict__ raw_rows,
                                                  const float *const *__restrict__ raw_ptrs, int64_t n_bags, int dim,
                                                  int op, const int32_t *__restrict__ ops, float *__restrict__ out,
-                                                 int64_t out_stride, int32_t *err_code) {
+                                                 int64_t out_stride, int32_t *err_code, int64_t sm_B) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (gridDim.x * (int64_t)blockDim.x) >> 5;
@@ -284,7 +284,8 @@ __global__ void __launch_bounds__(256) k_combine(const void *const *__restrict__
       else
         for (int64_t r = r0; r < r1; ++r) acc += static_cast<double>(raw_rows[r * dim + c]);
       if (bop == FX_OP_MEAN && total > 0) acc /= static_cast<double>(total);
-      out[b * out_stride + c] = __double2float_rn(acc);
+      float *orow = sm_B > 0 ? out + (b % sm_B) * out_stride + (b / sm_B) * dim : out + b * out_stride;
+      orow[c] = __double2float_rn(acc);
     }
   }
 }
@@ -298,7 +299,8 @@ __global__ void __launch_bounds__(256) k_combine_v4(const void *const *__restric
                                                     const float *__restrict__ raw_rows,
                                                     const float *const *__restrict__ raw_ptrs, int64_t n_bags,
                                                     int dim, int op, const int32_t *__restrict__ ops,
-                                                    float *__restrict__ out, int64_t out_stride, int32_t *err_code) {
+                                                    float *__restrict__ out, int64_t out_stride, int32_t *err_code,
+                                                    int64_t sm_B) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (gridDim.x * (int64_t)blockDim.x) >> 5;
@@ -345,7 +347,8 @@ __global__ void __launch_bounds__(256) k_combine_v4(const void *const *__restric
         const double dn = static_cast<double>(total);
         a0 /= dn; a1 /= dn; a2 /= dn; a3 /= dn;
       }
-      *reinterpret_cast<float4 *>(out + b * out_stride + c) =
+      float *orow = sm_B > 0 ? out + (b % sm_B) * out_stride + (b / sm_B) * dim : out + b * out_stride;
+      *reinterpret_cast<float4 *>(orow + c) =
           make_float4(__double2float_rn(a0), __double2float_rn(a1), __double2float_rn(a2), __double2float_rn(a3));
     }
   }
@@ -584,11 +587,11 @@ int fx_combine(const void *const *partials, int32_t partial_is_f32, const int32_
   if (combine_vec4_ok(partials, n_src, p_stride, dim, out_stride, out) && (reinterpret_cast<uintptr_t>(raw_rows) & 15) == 0)
     k_combine_v4<<<grid_for(n_bags * 32, 256), 256, 0, as_stream(stream)>>>(
         partials, partial_is_f32, counts, n_src, p_stride, raw_offsets, raw_rows, nullptr, n_bags, dim, op, ops, out,
-        out_stride, err_code);
+        out_stride, err_code, 0);
   else
     k_combine<<<grid_for(n_bags * 32, 256), 256, 0, as_stream(stream)>>>(
         partials, partial_is_f32, counts, n_src, p_stride, raw_offsets, raw_rows, nullptr, n_bags, dim, op, ops,
-        out, out_stride, err_code);
+        out, out_stride, err_code, 0);
   FX_LAUNCH_CHECK("fx_combine");
   return FX_OK;
 }
@@ -596,7 +599,7 @@ int fx_combine(const void *const *partials, int32_t partial_is_f32, const int32_
 int fx_combine_ptr(const void *const *partials, int32_t partial_is_f32, const int32_t *const *counts, int32_t n_src,
                    int64_t p_stride, const int64_t *raw_offsets, const float *const *raw_ptrs, int64_t n_bags,
                    int32_t dim, int32_t op, const int32_t *ops, float *out, int64_t out_stride, int32_t *err_code,
-                   void *stream) {
+                   int64_t sample_major_B, void *stream) {
   if (dim < 1 || n_src < 0 || n_bags < 0) {
     set_error("fx_combine_ptr: bad arguments");
     return FX_E_CONFIG;
@@ -605,11 +608,11 @@ int fx_combine_ptr(const void *const *partials, int32_t partial_is_f32, const in
   if (combine_vec4_ok(partials, n_src, p_stride, dim, out_stride, out))
     k_combine_v4<<<grid_for(n_bags * 32, 256), 256, 0, as_stream(stream)>>>(
         partials, partial_is_f32, counts, n_src, p_stride, raw_offsets, nullptr, raw_ptrs, n_bags, dim, op, ops, out,
-        out_stride, err_code);
+        out_stride, err_code, sample_major_B);
   else
     k_combine<<<grid_for(n_bags * 32, 256), 256, 0, as_stream(stream)>>>(
         partials, partial_is_f32, counts, n_src, p_stride, raw_offsets, nullptr, raw_ptrs, n_bags, dim, op, ops,
-        out, out_stride, err_code);
+        out, out_stride, err_code, sample_major_B);
   FX_LAUNCH_CHECK("fx_combine_ptr");
   return FX_OK;
 }

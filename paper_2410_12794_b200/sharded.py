@@ -746,24 +746,24 @@ class P2PShardedLookup:
                                      self.ops.owner_status.err.data_ptr(), L.FX_E_ROUTING_VIOLATION,
                                      self.ops.owner_status.code.data_ptr(), L.stream_ptr()), "fused pool")
 
-    def _result(self, p):
-        """Pooled [B, F*D] f32 of the step that used set p (row-wise: K5 first)."""
+    def _result(self, p, sample_major: bool = True):
+        """Pooled [B, F*D] f32 of the step that used set p (row-wise: K5 first,
+        writing sample-major rows directly; table-major [F*B, D] when
+        sample_major is False)."""
         if self.mode == "tablewise":
             return self.t_out[p]
         L = self._lib
         B, F, D, W = self.B, self.F, self.D, self.world
         self.launches += 1
         self._last_set = p
-        if self.threshold is not None:
-            L.check(L.lib.fx_combine_ptr(self._pp[p].data_ptr(), 1 if self.pesz == 4 else 0, self._cptr[p].data_ptr(),
-                                         W, D, self.t_raw_off[p].data_ptr(), self.t_raw_ptr[p].data_ptr(), self.n_bags,
-                                         D, 0, self.bag_ops.data_ptr(), self._tmp[p].data_ptr(), D, None,
-                                         L.stream_ptr()), "combine")
-        else:
-            L.check(L.lib.fx_combine(self._pp[p].data_ptr(), 1 if self.pesz == 4 else 0, self._cptr[p].data_ptr(), W,
-                                     D, None, None, self.n_bags, D, 0, self.bag_ops.data_ptr(), self._tmp[p].data_ptr(),
-                                     D, None, L.stream_ptr()), "combine")
-        return self._tmp[p].view(F, B, D).transpose(0, 1).reshape(B, F * D)
+        planned = self.threshold is not None
+        L.check(L.lib.fx_combine_ptr(self._pp[p].data_ptr(), 1 if self.pesz == 4 else 0, self._cptr[p].data_ptr(),
+                                     W, D, self.t_raw_off[p].data_ptr() if planned else None,
+                                     self.t_raw_ptr[p].data_ptr() if planned else None, self.n_bags, D, 0,
+                                     self.bag_ops.data_ptr(), self._tmp[p].data_ptr(),
+                                     F * D if sample_major else D, None, B if sample_major else 0,
+                                     L.stream_ptr()), "combine")
+        return self._tmp[p].view(B, F * D) if sample_major else self._tmp[p]
 
     def counters(self) -> torch.Tensor:
         """Per-bag (pushdown_groups, pushdown_rows, raw_rows) of the last result,
@@ -875,8 +875,7 @@ class P2PShardedLookup:
         self._barrier()
         self._gather(0)
         self._barrier()
-        self._result(0)
-        return self._tmp[0]
+        return self._result(0, sample_major=False)
 
     def stream_host(self, host_batches, check: bool = True):
         """End-to-end pipelined API: pinned host (indices, offsets) in, pinned
@@ -915,8 +914,6 @@ class P2PShardedLookup:
             ev.record(main)  # pushes of steps <= i+1 are done by now in main's order
             consumed[i] = ev
             k = i % 2
-            if self.mode == "rowwise":
-                res.record_stream(s_d2h)  # a fresh [B, F*D] copy of the K5 output: keep it alive for the D2H
             with torch.cuda.stream(s_d2h):
                 s_d2h.wait_event(ev)
                 host[k].copy_(res, non_blocking=True)
