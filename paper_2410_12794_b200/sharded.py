@@ -26,6 +26,7 @@ run it under gloo with a test double for the ops).
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -816,6 +817,9 @@ class P2PShardedLookup:
         it on the current stream."""
         main = torch.cuda.current_stream(self.device)
         side = torch.cuda.Stream(self.device)
+        # the gather runs on a high-priority stream so its blocks are scheduled
+        # ahead of the concurrent push (same program order via stream waits)
+        hp = torch.cuda.Stream(self.device, priority=-1) if os.environ.get("FX_GATHER_PRIORITY", "1") == "1" else None
         ev_bar = None
         k = 0
         for item in batches:
@@ -848,7 +852,13 @@ class P2PShardedLookup:
             if res is not None:
                 yield res
             tok = self._mark("pool")
-            self._gather(p)
+            if hp is not None:
+                hp.wait_stream(main)
+                with torch.cuda.stream(hp):
+                    self._gather(p)
+                main.wait_stream(hp)
+            else:
+                self._gather(p)
             self._close(tok)
             k += 1
         if k:
