@@ -457,8 +457,10 @@ class AdaptiveCache:
 
     def probe_unique(self, uniq: torch.Tensor, mult: torch.Tensor, last_ord: torch.Tensor, n_uniq_dev, nnz: int,
                      slot_out: torch.Tensor | None = None, n_uniq_host: int = 0):
-        """K3 over a batch's unique keys (first-occurrence order from fx_dedup)."""
-        self._reserve_sketch(nnz)
+        """K3 over a batch's unique keys (first-occurrence order from fx_dedup).
+        `nnz` is the tick advance (every probe of the batch); the sketch can
+        gain at most one new key per unique key."""
+        self._reserve_sketch(n_uniq_host if (n_uniq_dev is None and n_uniq_host) else nnz)
         _lib.check(self._L.fx_cache_probe(self._h, uniq.data_ptr(), mult.data_ptr(), last_ord.data_ptr(),
                                           _lib.ptr(n_uniq_dev), int(n_uniq_host), int(nnz), _lib.ptr(slot_out),
                                           _lib.stream_ptr()), "cache probe")

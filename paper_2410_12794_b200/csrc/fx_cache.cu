@@ -1005,11 +1005,19 @@ __global__ void k_sketch_collect(CacheView c, uint64_t *out_keys, long long *out
 // top-k preselection for stage(limit): histogram of the top 16 bits of the
 // (descending-count) sort key over live sketch keys
 __global__ void k_sketch_hist(CacheView c, int32_t *hist) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < c.kcap; i += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t k = c.kkeys[i];
-    if (k == kEmpty || k == kTomb) continue;
-    const long long vb = ~__double_as_longlong(c.kval[i]) & LLONG_MAX;
-    atomicAdd(&hist[vb >> 47], 1);
+  // decayed counts take few distinct values: lanes hitting the same bin are
+  // merged (one atomic per distinct bin per warp instead of one per key)
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); i0 < c.kcap; i0 += stride) {
+    const int64_t i = i0 + lane;
+    int bin = -1;
+    if (i < c.kcap) {
+      const uint64_t k = c.kkeys[i];
+      if (k != kEmpty && k != kTomb) bin = static_cast<int>((~__double_as_longlong(c.kval[i]) & LLONG_MAX) >> 47);
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, bin);
+    if (bin >= 0 && lane == __ffs(peers) - 1) atomicAdd(&hist[bin], __popc(peers));
   }
 }
 
