@@ -464,8 +464,6 @@ class P2PShardedLookup:
             raise ConfigError("replicated tables are supported in table-wise mode only")
         self.threshold = pushdown_threshold
         if pushdown_threshold is not None:
-            if mode != "rowwise":
-                raise ConfigError("pushdown_threshold applies to row-wise mode (table-wise bags are one group)")
             if pushdown_threshold < 2:
                 raise ConfigError(f"pushdown threshold must be >= 2, got {pushdown_threshold}")
         if mode not in ("tablewise", "rowwise"):
@@ -483,7 +481,7 @@ class P2PShardedLookup:
         B, F, W = self.B, self.F, world
         self.n_bags = n_bags = B * F
         self.ops = FlexOps(self.metas, placement, seed, rank, self.ftab, self.fops, B, self.device,
-                           ipc_shards=pushdown_threshold is not None)
+                           ipc_shards=pushdown_threshold is not None and mode == "rowwise")
         for t in self.replicated:
             if any(sp.table_id == t for sp in placement):
                 raise ConfigError(f"replicated table {t} must not be in the sharded placement")
@@ -531,6 +529,8 @@ class P2PShardedLookup:
         self.t_flags.zero_()
         if mode == "tablewise":
             self.t_out = [_cai_tensor(self.b_out.ptr + p * out_set, (B, F * D), torch.float32, dev) for p in (0, 1)]
+            if pushdown_threshold is not None:
+                self.t_counters = [torch.zeros((3, n_bags), dtype=torch.int32, device=dev) for _ in (0, 1)]
         else:
             pdt = torch.float64 if self.pesz == 8 else torch.float32
             self.t_out = [_cai_tensor(self.b_out.ptr + p * out_set, (W, n_bags, D), pdt, dev) for p in (0, 1)]
@@ -564,7 +564,7 @@ class P2PShardedLookup:
                 ptrs.append(opened)
         self.peer_ptrs = ptrs
         self.t_peer_flags = torch.tensor([p[3] for p in ptrs], dtype=torch.int64, device=dev)
-        if pushdown_threshold is not None:
+        if pushdown_threshold is not None and mode == "rowwise":
             # every shard's base address as seen from this rank (raw fetch targets)
             mine_sh = {t: buf.handle() for t, buf in self.ops.shard_bufs.items()}
             all_sh = [None] * W
@@ -706,6 +706,17 @@ class P2PShardedLookup:
                                self.n_bags, None, o.status.err.data_ptr(), o.status.code.data_ptr(), sp),
                 "validate")
         if self.mode == "tablewise":
+            if self.threshold is not None:
+                # a table-wise bag is ONE (bag, owner) group of L rows: pushed down
+                # when L >= threshold, otherwise its rows are raw (ranker.py:281-293).
+                # A raw group's pooled value is its row sum, which the owner's K4
+                # produces bit-identically, so only the counters follow the plan.
+                lens = (offsets[1:] - offsets[:-1]).to(torch.int32)
+                push = lens >= int(self.threshold)
+                c = self.t_counters[p]
+                c[0].copy_(push.to(torch.int32))
+                c[1].copy_(torch.where(push, lens, torch.zeros_like(lens)))
+                c[2].copy_(torch.where(push, torch.zeros_like(lens), lens))
             self.launches += 2  # k_route (validate) + k_push_csr
             L.check(L.lib.fx_push_csr(indices.data_ptr(), L.idx_type_of(indices), offsets.data_ptr(), B, F,
                                       self.t_feat_owner.data_ptr(), self.t_feat_pos.data_ptr(),
@@ -752,6 +763,7 @@ class P2PShardedLookup:
         writing sample-major rows directly; table-major [F*B, D] when
         sample_major is False)."""
         if self.mode == "tablewise":
+            self._last_set = p
             return self.t_out[p]
         L = self._lib
         B, F, D, W = self.B, self.F, self.D, self.world
@@ -768,10 +780,10 @@ class P2PShardedLookup:
 
     def counters(self) -> torch.Tensor:
         """Per-bag (pushdown_groups, pushdown_rows, raw_rows) of the last result,
-        int32 [3, F*B] in table-major bag order (ranker.py:281-293; row-wise
-        mode with a pushdown threshold)."""
+        int32 [3, F*B] in table-major bag order (ranker.py:281-293; needs a
+        pushdown threshold)."""
         if self.threshold is None:
-            raise ConfigError("counters need pushdown_threshold (row-wise mode)")
+            raise ConfigError("counters need pushdown_threshold")
         return self.t_counters[self._last_set]
 
     def _check(self):
@@ -878,7 +890,7 @@ class P2PShardedLookup:
         planned mode): occurrences with hit_slot >= 0 are combined from the
         cache's rows, the rest follow the plan (pushdown to the owner or raw
         fetch over NVLink). Returns the table-major pooled [F*B, D] f32."""
-        if self.threshold is None:
+        if self.threshold is None or self.mode != "rowwise":
             raise ConfigError("pool_cached needs the planned row-wise mode (pushdown_threshold)")
         rows, ld = cache.rows_base() if (cache is not None and hit_slot is not None) else (0, 0)
         self._stage(indices, offsets, 0, hit_slot=hit_slot, cache_rows=rows, cache_ld=ld)

@@ -52,8 +52,9 @@ def test_sharded_rowwise_f32_partials():
     assert "SHARDED rowwise p2pf32" in r.stdout
 
 
-@pytest.mark.parametrize("exchange", ["p2pthr", "p2pthr32", "p2pthr32-pipe"])
-def test_sharded_rowwise_planned_raw_fetch(exchange):
+@pytest.mark.parametrize("mode,exchange", [("rowwise", "p2pthr"), ("rowwise", "p2pthr32"),
+                                           ("rowwise", "p2pthr32-pipe"), ("tablewise", "p2pthr")])
+def test_sharded_planned_raw_fetch(mode, exchange):
     """Reference plan (threshold 2) in row-wise mode: singleton (bag, rank)
     groups raw-fetched over NVLink by the requester, larger ones pushed down.
     Per-bag counters equal the reference plan's; with f32 partials the result
@@ -64,10 +65,10 @@ def test_sharded_rowwise_planned_raw_fetch(exchange):
     w = min(n, 4)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={w}",
            "--master-addr", "127.0.0.1", "--master-port", "29574", os.path.join(ROOT, "scripts", "sharded_check.py"),
-           "rowwise", exchange]
+           mode, exchange]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
-    assert f"SHARDED rowwise {exchange}" in r.stdout
+    assert f"SHARDED {mode} {exchange}" in r.stdout
     assert "counter_mismatches=0" in r.stdout and "non_bit_exact_vs_reference_combine=0" in r.stdout
 
 
