@@ -520,38 +520,40 @@ __global__ void __launch_bounds__(1024) k_offer_par(CacheView c, const uint64_t 
           s_ffr = run;  // decisions resolved in this tile
         }
       } else if (tid < 32) {
+        // Run peeling per 32-candidate chunk: from the first unresolved
+        // candidate u0 (queue offset a0), an accept-run lasts while
+        // c_{u0+t} >= V[h + a0 + t] and a reject-run while c_{u0+t} < V[h + a0];
+        // the candidate at u0 always starts one of them, so every step
+        // resolves >= 1 decision with two ballots (no per-decision chain).
         int a0 = 0;  // accepts so far in this tile
         for (int c0 = 0; c0 < T; c0 += 32) {
           const int q = c0 + tid;
-          unsigned mask = 0;
-          if (q < T) {
-            const double ec = s_ec[q];
-#pragma unroll
-            for (int b = 0; b < 32; ++b) mask |= (ec >= s_ev[a0 + b] ? 1u : 0u) << b;
-          }
-          s_mask[tid] = mask;
-          __syncwarp();
-          if (tid == 0) {
-            unsigned mk[32];
-#pragma unroll
-            for (int u = 0; u < 32; ++u) mk[u] = s_mask[u];
-            const int n = (T - c0) < 32 ? (T - c0) : 32;
-            int a = 0;
-#pragma unroll
-            for (int u = 0; u < 32; ++u) {
-              if (u < n) {
-                const int acc = (mk[u] >> a) & 1u;
-                s_acc[c0 + u] = acc;
-                s_rank[c0 + u] = a0 + a;
-                a += acc;
+          const int nq = (T - c0) < 32 ? (T - c0) : 32;
+          const double ec = q < T ? s_ec[q] : 0.0;
+          int u0 = 0;
+          while (u0 < nq) {
+            const bool mine = tid >= u0 && tid < nq;
+            const unsigned fa = __ballot_sync(0xffffffffu, mine && !(ec >= s_ev[a0 + (tid - u0)]));
+            const int end_a = fa ? __ffs(fa) - 1 : nq;  // accept-run [u0, end_a)
+            if (end_a > u0) {
+              if (mine && tid < end_a) {
+                s_acc[q] = 1;
+                s_rank[q] = a0 + (tid - u0);
               }
+              a0 += end_a - u0;
+              u0 = end_a;
+              continue;
             }
-            s_chunk_a = a;
+            const unsigned fr = __ballot_sync(0xffffffffu, mine && !(ec < s_ev[a0]));
+            const int end_r = fr ? __ffs(fr) - 1 : nq;  // reject-run [u0, end_r)
+            if (mine && tid < end_r) {
+              s_acc[q] = 0;
+              s_rank[q] = a0;
+            }
+            u0 = end_r;
           }
-          __syncwarp();
-          a0 += s_chunk_a;
-          __syncwarp();
         }
+        __syncwarp();
         if (tid == 0) {
           s_chunk_a = a0;
           s_ffr = T;
