@@ -383,6 +383,9 @@ __global__ void k_est_compact(const OfferWS w, ParWS pw) {
     w.est_cc[t] = w.est_cand[pw.cand[t]];
 }
 
+constexpr int OFFER_TILE = 4096;  // candidates per resolver tile (dynamic shared memory)
+constexpr size_t OFFER_SMEM = (2 * OFFER_TILE + 32) * sizeof(double) + 2 * OFFER_TILE * sizeof(int);
+
 // pstate layout (written by k_offer_par, read by k_offer_apply)
 enum { PS_E0 = 0, PS_H0, PS_NF, PS_N2, PS_TICK0, PS_LOG0, PS_EV0, PS_VALID };
 
@@ -476,19 +479,17 @@ __global__ void __launch_bounds__(1024) k_offer_par(CacheView c, const uint64_t 
     if (tid == 0 && cap > 0) { st[2] += m - j0; st[0] = m; }
     __syncthreads();
   } else {
-    // sketch admission: tiles of T <= min(1024, cap) candidates. Lane q of warp 0
-    // builds mask_q (bit b = est(c_q) >= est(V[h + a0 + b]), a0 = accepts before
-    // its 32-chunk); one thread then resolves the chunk with a register chain
-    // (a += (mask_q >> a) & 1) — the exact sequential decisions, ~a dozen
-    // cycles each regardless of how often accept and reject alternate.
-    __shared__ double s_ec[1024];
-    __shared__ double s_ev[1024 + 32];
-    __shared__ unsigned s_mask[32];
-    __shared__ int s_acc[1024];
-    __shared__ int s_rank[1024];
+    // sketch admission: tiles of T <= min(OFFER_TILE, cap) candidates; a tile
+    // that is one accept- or reject-run is applied at once, otherwise warp 0
+    // peels it run by run, 32 candidates at a time (see below).
+    extern __shared__ __align__(16) unsigned char offer_smem[];
+    double *s_ec = reinterpret_cast<double *>(offer_smem);
+    double *s_ev = s_ec + OFFER_TILE;
+    int *s_acc = reinterpret_cast<int *>(s_ev + OFFER_TILE + 32);
+    int *s_rank = s_acc + OFFER_TILE;
     __shared__ int s_chunk_a;
     __shared__ int s_ffa, s_ffr;
-    const long long tmax = cap < 1024 ? cap : 1024;
+    const long long tmax = cap < OFFER_TILE ? cap : OFFER_TILE;
     while (tmax > 0 && st[0] < m) {
       const long long j = st[0], h = st[1], nacc = st[2];
       const int T = static_cast<int>((m - j) < tmax ? (m - j) : tmax);
@@ -497,13 +498,13 @@ __global__ void __launch_bounds__(1024) k_offer_par(CacheView c, const uint64_t 
       if (tid == 0) { s_ffa = T; s_ffr = T; }
       __syncthreads();
       // run detection: accept-run (c_t >= V[h+t]) or reject-run (c_t < V[h])
-      if (tid < T) {
-        if (!(s_ec[tid] >= s_ev[tid])) atomicMin(&s_ffa, tid);
-        if (!(s_ec[tid] < s_ev[0])) atomicMin(&s_ffr, tid);
+      for (int t = tid; t < T; t += blockDim.x) {
+        if (!(s_ec[t] >= s_ev[t])) atomicMin(&s_ffa, t);
+        if (!(s_ec[t] < s_ev[0])) atomicMin(&s_ffr, t);
       }
       __syncthreads();
       const int ffa = s_ffa, ffr = s_ffr;
-      const bool bulk = ffa >= 256 || ffr >= 256 || ffa == T || ffr == T;
+      const bool bulk = ffa == T || ffr == T;  // whole tile one run; otherwise peel every chunk
       if (tid == 0) {
         if (bulk) sc->tiles_bulk += 1; else sc->tiles_chain += 1;
       }
@@ -1326,6 +1327,11 @@ int run_offer(fx_cache *c, const uint64_t *keys, int64_t n, int32_t mode, const 
       k_vic = 0;
   }
   if (prof) cudaEventRecord(pe[1], st);
+  static bool offer_smem_set = false;
+  if (!offer_smem_set) {
+    cudaFuncSetAttribute(k_offer_par, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(OFFER_SMEM));
+    offer_smem_set = true;
+  }
   const bool par = c->parallel_offers && c->uniform > 0 && sizes == nullptr && n > 0;
   if (par) {
     // compact the non-present candidates, then resolve decisions run by run
@@ -1335,12 +1341,12 @@ int run_offer(fx_cache *c, const uint64_t *keys, int64_t n, int32_t mode, const 
     k_present_accept<<<grid_for(n, 256), 256, 0, st>>>(w.present, n, mode, accepted);
     ParWS pw{w.par_cand, n, w.par_m};
     k_est_compact<<<grid_for(n, 256), 256, 0, st>>>(w, pw);
-    k_offer_par<<<1, 1024, 0, st>>>(c->v, keys, mode, w, pw, k_vic, c->uniform, accepted, c->record);
+    k_offer_par<<<1, 1024, OFFER_SMEM, st>>>(c->v, keys, mode, w, pw, k_vic, c->uniform, accepted, c->record);
     k_offer_apply_keys<<<grid_for(n, 256), 256, 0, st>>>(c->v, keys, w, c->record);
     k_offer_apply_slots<<<grid_for(n, 256), 256, 0, st>>>(c->v, keys, w, c->uniform);
   } else if (c->uniform > 0 && n == 0 && h.used > h.budget) {
     ParWS pw{w.par_cand, 0, nullptr};
-    k_offer_par<<<1, 1024, 0, st>>>(c->v, keys, mode, w, pw, k_vic, c->uniform, accepted, c->record);
+    k_offer_par<<<1, 1024, OFFER_SMEM, st>>>(c->v, keys, mode, w, pw, k_vic, c->uniform, accepted, c->record);
   } else {
     k_offer_seq<<<1, 32, 0, st>>>(c->v, keys, n, mode, w, k_vic, accepted, c->record);
   }
