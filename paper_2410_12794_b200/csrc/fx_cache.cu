@@ -248,6 +248,7 @@ struct OfferWS {
   int64_t *par_m;
   double *est_cc;      // est_cand in compacted candidate order (contiguous tile loads)
   long long *pstate;   // decide -> apply hand-off (see k_offer_par)
+  long long lru_valid; // lru_slot[0, lru_valid) holds the LRU-ordered prefix
 };
 
 __global__ void k_offer_prep(CacheView c, const uint64_t *keys, int64_t n, const int32_t *sizes, OfferWS w) {
@@ -266,6 +267,33 @@ __global__ void k_lru_keys(CacheView c, OfferWS w, long long free_key) {
     const long long t = c.stick[i];
     w.sort_keys_in[i] = t == kFree ? free_key : t;
     w.iota[i] = static_cast<int32_t>(i);
+  }
+}
+
+// partial LRU order: histogram of the live ticks' top bits, then only the
+// slots in the oldest bins (a superset of the `need` oldest) are sorted
+__global__ void k_lru_hist(CacheView c, int shift, int32_t *hist) {
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); i0 < c.scap; i0 += stride) {
+    const int64_t i = i0 + lane;
+    int bin = -1;
+    if (i < c.scap) {
+      const long long t = c.stick[i];
+      if (t != kFree) bin = static_cast<int>(t >> shift);
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, bin);
+    if (bin >= 0 && lane == __ffs(peers) - 1) atomicAdd(&hist[bin], __popc(peers));
+  }
+}
+
+__global__ void k_lru_collect(CacheView c, int shift, int32_t max_bin, OfferWS w, unsigned long long *count) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < c.scap; i += (int64_t)gridDim.x * blockDim.x) {
+    const long long t = c.stick[i];
+    if (t == kFree || (t >> shift) > max_bin) continue;
+    const unsigned long long p = atomicAdd(count, 1ull);
+    w.sort_keys_in[p] = t;
+    w.iota[p] = static_cast<int32_t>(i);
   }
 }
 
@@ -373,7 +401,10 @@ struct ParWS {
 
 __device__ __forceinline__ double est_v(const CacheView &c, const OfferWS &w, long long k, long long e0,
                                         long long k_vic) {
-  if (k < e0) return k < k_vic ? w.est_vic[k] : k_est(c, c.skey[w.lru_slot[k]]);
+  if (k < e0) {
+    if (k < k_vic) return w.est_vic[k];
+    return k < w.lru_valid ? k_est(c, c.skey[w.lru_slot[k]]) : 0.0;  // beyond: padding, never a victim
+  }
   return w.est_cand[w.acc_j[k - e0]];
 }
 
@@ -1199,6 +1230,7 @@ struct fx_cache {
   uint64_t *last_ev = nullptr;     // keys evicted by the last offer/apply/resize
   int64_t last_ev_cap = 0;
   const float *const *pending_rows = nullptr;  // optional per-pending-key row pointers
+  int32_t *lru_hist = nullptr;     // 65536 bins + counter for the partial LRU order
 };
 
 namespace {
@@ -1231,6 +1263,51 @@ int read_scalars(fx_cache *c, Scalars *h, cudaStream_t st) {
   int rc = cuda_check(cudaMemcpyAsync(h, c->v.sc, sizeof(Scalars), cudaMemcpyDeviceToHost, st), "scalars");
   if (rc) return rc;
   return cuda_check(cudaStreamSynchronize(st), "scalars sync");
+}
+
+// LRU order of the live slots into w.lru_slot: the full order, or — when only
+// the `need` oldest entries can be touched (uniform entry size: every accept
+// evicts one entry) and need is small — just a sorted prefix covering them.
+int sort_lru(fx_cache *c, cudaStream_t st, OfferWS &w, void *cub_tmp, size_t cb, const Scalars &h, int64_t need) {
+  const int64_t S = c->v.scap;
+  const int bits = lru_bits(h.tick);
+  w.lru_valid = h.entries;
+  if (h.entries <= 0) return FX_OK;
+  if (c->uniform <= 0 || need * 4 >= h.entries || bits <= 16) {
+    k_lru_keys<<<grid_for(S, 256), 256, 0, st>>>(c->v, w, (1ll << bits) - 1);
+    cub::DeviceRadixSort::SortPairs(cub_tmp, cb, w.sort_keys_in, w.sort_keys_out, w.iota, w.lru_slot,
+                                    static_cast<int>(S), 0, bits, st);
+    return cuda_check(cudaGetLastError(), "sort_lru");
+  }
+  constexpr int kBins = 1 << 16;
+  const int shift = bits - 16;
+  if (!c->lru_hist) {
+    int rc = dmalloc(&c->lru_hist, kBins + 4);
+    if (rc) return rc;
+  }
+  cudaMemsetAsync(c->lru_hist, 0, (kBins + 4) * 4, st);
+  k_lru_hist<<<grid_for(S, 256), 256, 0, st>>>(c->v, shift, c->lru_hist);
+  std::vector<int32_t> hh(kBins);
+  int rc = cuda_check(cudaMemcpyAsync(hh.data(), c->lru_hist, kBins * 4, cudaMemcpyDeviceToHost, st), "lru hist");
+  if (rc) return rc;
+  rc = cuda_check(cudaStreamSynchronize(st), "lru hist sync");
+  if (rc) return rc;
+  int64_t cum = 0;
+  int b = kBins - 1;
+  for (int i = 0; i < kBins; ++i) {
+    cum += hh[i];
+    if (cum >= need) {
+      b = i;
+      break;
+    }
+  }
+  unsigned long long *cnt = reinterpret_cast<unsigned long long *>(c->lru_hist + kBins);
+  cudaMemsetAsync(cnt, 0, 8, st);
+  k_lru_collect<<<grid_for(S, 256), 256, 0, st>>>(c->v, shift, b, w, cnt);
+  cub::DeviceRadixSort::SortPairs(cub_tmp, cb, w.sort_keys_in, w.sort_keys_out, w.iota, w.lru_slot,
+                                  static_cast<int>(cum), 0, bits, st);
+  w.lru_valid = cum;
+  return cuda_check(cudaGetLastError(), "sort_lru partial");
 }
 
 // Layout one offer workspace for n candidates over the cache's slot capacity.
@@ -1315,11 +1392,18 @@ int run_offer(fx_cache *c, const uint64_t *keys, int64_t n, int32_t mode, const 
   }
   if (n > 0) k_offer_prep<<<grid_for(n, 256), 256, 0, st>>>(c->v, keys, n, sizes, w);
   int64_t k_vic = 0;
+  w.lru_valid = 0;
   if (h.entries > 0) {
-    const int64_t S = c->v.scap;
-    k_lru_keys<<<grid_for(S, 256), 256, 0, st>>>(c->v, w, (1ll << lru_bits(h.tick)) - 1);
-    cub::DeviceRadixSort::SortPairs(cub_tmp, cb, w.sort_keys_in, w.sort_keys_out, w.iota, w.lru_slot,
-                                    static_cast<int>(S), 0, lru_bits(h.tick), st);
+    // entries that can be evicted: the over-budget excess plus one per candidate
+    int64_t over = 0;
+    if (c->uniform > 0) {
+      const long long S1 = c->uniform;
+      const long long ph = h.used / S1 > h.entries ? h.used / S1 - h.entries : 0;
+      const long long capn = h.budget / S1 - ph;
+      over = h.entries > capn ? h.entries - (capn > 0 ? capn : 0) : 0;
+    }
+    rc = sort_lru(c, st, w, cub_tmp, cb, h, over + n + 1);
+    if (rc) return rc;
     k_vic = h.entries < n ? h.entries : n;
     if (mode == 0 && c->v.admission == 0 && k_vic > 0)
       k_vic_prep<<<grid_for(k_vic, 256), 256, 0, st>>>(c->v, w, k_vic);
@@ -1460,7 +1544,7 @@ int fx_cache_destroy(fx_cache *c) {
   if (!c) return FX_OK;
   CacheView &v = c->v;
   void *ps[] = {v.sc, v.hkeys, v.hslot, v.skey, v.skey2, v.stick, v.ssize, v.shits, v.rows, v.free_stack, v.kkeys,
-                v.kval, v.kflag, v.pend, v.evlog, c->dir_dev, c->tbytes_dev, c->ws, c->last_ev};
+                v.kval, v.kflag, v.pend, v.evlog, c->dir_dev, c->tbytes_dev, c->ws, c->last_ev, c->lru_hist};
   for (void *p : ps)
     if (p) cudaFree(p);
   delete c;
@@ -1941,10 +2025,14 @@ int fx_cache_pooled_put(fx_cache *c, const uint64_t *key_a, const uint64_t *key_
   cub::DeviceRadixSort::SortPairs(cub2, cb2, key_a, pw.keys_sorted, pw.iota, pw.perm, static_cast<int>(n), 0, 64,
                                   st);
   k_put_prev<<<grid_for(n, 256), 256, 0, st>>>(pw.keys_sorted, pw.perm, n, key_b, pw, c->v.sc);
+  w.lru_valid = 0;
   if (h.entries > 0) {
-    k_lru_keys<<<grid_for(S, 256), 256, 0, st>>>(c->v, w, (1ll << lru_bits(h.tick)) - 1);
-    cub::DeviceRadixSort::SortPairs(cub_tmp, cb, w.sort_keys_in, w.sort_keys_out, w.iota, w.lru_slot,
-                                    static_cast<int>(S), 0, lru_bits(h.tick), st);
+    const long long S1 = uniform_size > 0 ? uniform_size : 1;
+    const long long ph = h.used / S1 > h.entries ? h.used / S1 - h.entries : 0;
+    const long long capn = h.budget / S1 - ph;
+    const int64_t over = h.entries > capn ? h.entries - (capn > 0 ? capn : 0) : 0;
+    rc = sort_lru(c, st, w, cub_tmp, cb, h, sizes ? h.entries : over + n + 1);
+    if (rc) return rc;
   }
   const bool par = c->parallel_offers && !sizes && c->uniform > 0 && c->uniform == uniform_size;
   if (par) {

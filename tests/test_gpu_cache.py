@@ -249,3 +249,47 @@ def test_parallel_offers_equal_sequential_loop(C, admission):
             assert (a.used_bytes, a.tick, a.hits, a.misses) == (b.used_bytes, b.tick, b.hits, b.misses)
             assert a.sketch.ranked() == b.sketch.ranked()
         assert caches[0].eviction_log == caches[1].eviction_log
+
+
+@pytest.mark.parametrize("thr", [None, 2])
+def test_ranker_large_cache_vs_oracle(thr):
+    """A cache much larger than each batch's offers (the partial LRU-order
+    path: only the oldest entries that can be evicted are ordered) against
+    the canonical-order oracle: per-batch metrics, LRU order and evictions."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import oracle as O
+    import paper_2410_12794_b200 as P
+    from paper_2410_12794_b200 import cache as C
+    from paper_2410_12794_b200.ranker import Ranker, RankerParams
+    from paper_2410_12794_b200.workload import DlrmBatchGen
+    rows, D, B = (60_000, 40_000, 60_000, 9_000), 16, 64
+    metas = [P.TableMeta(t, n, D) for t, n in enumerate(rows)]
+    placement = [P.ShardSpec(t, 0, n, 0) for t, n in enumerate(rows)]
+    dep = P.init_store(metas, placement, 0)
+    budget = 8_000 * D * 4
+    model = (budget + 1000 + B, 1000, 1)
+    cache = C.AdaptiveCache(budget, admission="sketch", record_evictions=True, max_dim=D)
+    rk = Ranker(dep, P.build_routing(metas, placement), None, RankerParams(pushdown_threshold=thr, admit_per_batch=64),
+                cache=cache, policy=C.CachePolicy(C.MemoryModel(*model)), tracker=C.LoadTracker(4, 10 ** 9, 0))
+    pl = O.Placement.from_specs({m.table_id: m.num_rows for m in metas},
+                                [(s.table_id, s.start, s.end, s.server_id) for s in placement])
+    oc = O.CacheOracle(budget, admission="sketch")
+    po = O.PipelineOracle(0, {m.table_id: D for m in metas}, pl, threshold=thr, cache=oc,
+                          policy=O.CachePolicyO(O.MemoryModelO(*model)), tracker=O.LoadTrackerO(4, 10 ** 9, 0),
+                          admit_per_batch=64)
+    gen = DlrmBatchGen(rows, 0.9, B, (1, 8), seed=5)
+    F = len(rows)
+    for it in range(24):
+        hb = gen.next()
+        rk.execute_csr(torch.from_numpy(hb.indices).cuda(), torch.from_numpy(hb.offsets).cuda(), tuple(range(F)),
+                       ("sum",) * F, B, batch_id=it)
+        bb = O.BagBatch(hb.offsets.astype(np.int64), hb.indices.astype(np.int64), np.repeat(np.arange(F), B),
+                        ["sum"] * (F * B), np.tile(np.arange(B), F), np.repeat(np.arange(F), B), B, it)
+        po.run(bb)
+        m, om = rk.batch_metrics[-1], po.metrics[-1]
+        assert (m.cache_hits, m.cache_misses, m.raw_rows) == (om["hits"], om["misses"], om["raw_rows"]), it
+        assert rk.cache.lru_keys() == oc.lru_keys(), it
+    assert rk.cache.eviction_log == oc.evictions
+    if thr is None:  # the cache filled and evicted with most entries outside the sorted prefix
+        assert len(oc.evictions) > 0 and len(oc.lru_keys()) > 5_000
