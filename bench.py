@@ -378,8 +378,8 @@ def main():
                          "frac": achieved / peak, "traffic": tr, "peak_source": peak_src,
                          "kernel": (f"fx::k_pool_bulk<G=32,CR=12> (TMA bulk-copy staged gather+pool, "
                                     f"D={dim})" if os.environ.get("FX_POOL_VARIANT", "2") == "2" and dim == 128
-                                    else f"fx::k_pool_async<G={min(32, dim // 4)},CR=16> (cp.async-staged gather+pool, "
-                                         f"D={dim})"),
+                                    else f"fx::k_pool_async<G={min(32, dim // 4)},CR={12 if dim == 64 else 16}> "
+                                         f"(cp.async-staged gather+pool, D={dim})"),
                          "bytes_per_launch": tot_bytes / launches, "launch_ms": kernel_ms,
                          "note": ("L2-assisted: Zipf hot rows and the small tables are served from the 126 MB "
                                   "L2, so DRAM traffic (ncu, `traffic`) is well below the algorithmic bytes and "
