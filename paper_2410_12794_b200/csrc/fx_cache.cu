@@ -46,7 +46,7 @@ struct Scalars {
                    //    OrderedDict), 2: pooled-key fingerprint collision
   long long n_ov;  // in-place pooled re-puts recorded by the last put call
   long long n_par_puts;  // put calls resolved by the parallel closed form (cumulative)
-  long long tiles_bulk, tiles_chain;  // k_offer_par sketch tiles resolved as one run / by the chain (cumulative)
+  long long tiles_bulk, tiles_chain;  // k_offer_par sketch tiles resolved as one run / by peeling (cumulative)
 };
 
 struct CacheView {
@@ -388,11 +388,12 @@ __global__ void k_offer_seq(CacheView c, const uint64_t *keys, int64_t n, int32_
 //    always ("always" admission / apply-pending).
 // Decisions come in runs. Accept-run from (j, h): c_{j+t} is accepted iff
 // est(c_{j+t}) >= est(V[h+t]) for all earlier t; reject-run from (j, h):
-// c_{j+t} is rejected iff est(c_{j+t}) < est(V[h]). Each run is resolved with
-// one block-wide compare + first-false reduction over a window of at most
-// min(1024, cap) candidates, so V[h+t] never refers to a candidate accepted
-// inside the same window. Ticks, slots and evictions are then assigned in
-// parallel exactly as the sequential loop would.
+// c_{j+t} is rejected iff est(c_{j+t}) < est(V[h]). A tile of at most
+// min(OFFER_TILE, cap) candidates (so V[h+t] never refers to a candidate
+// accepted inside the same tile) is applied at once when it is a single run,
+// otherwise warp 0 peels it run by run 32 candidates at a time. Ticks, slots
+// and evictions are then assigned in parallel (k_offer_apply_*) exactly as
+// the sequential loop would.
 struct ParWS {
   const int32_t *cand;   // compacted non-present candidate positions (ascending)
   int64_t m;             // number of compacted candidates
