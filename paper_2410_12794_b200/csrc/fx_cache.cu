@@ -1412,10 +1412,12 @@ int run_offer(fx_cache *c, const uint64_t *keys, int64_t n, int32_t mode, const 
       k_vic = 0;
   }
   if (prof) cudaEventRecord(pe[1], st);
-  static bool offer_smem_set = false;
-  if (!offer_smem_set) {
+  static bool offer_smem_set[64] = {false};  // per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!offer_smem_set[dev & 63]) {
     cudaFuncSetAttribute(k_offer_par, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(OFFER_SMEM));
-    offer_smem_set = true;
+    offer_smem_set[dev & 63] = true;
   }
   const bool par = c->parallel_offers && c->uniform > 0 && sizes == nullptr && n > 0;
   if (par) {

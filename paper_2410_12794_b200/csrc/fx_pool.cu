@@ -384,8 +384,12 @@ static void launch_async_cr(const fx_segment *segs, int n_segs, int dim, const I
   constexpr int WARPS = 4;
   // per group: CR rows x (G lanes * 16 B * NCH); 32/G groups per warp
   const size_t smem = static_cast<size_t>(WARPS) * (32 / G) * CR * G * 16 * NCH;
-  static int per_sm = -1;
-  if (per_sm < 0) {
+  // function attributes and occupancy are per device: cache them per device
+  static int per_sm_dev[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int &per_sm = per_sm_dev[dev & 63];
+  if (per_sm <= 0) {
     cudaFuncSetAttribute(k_pool_async<G, NCH, CR, IdxT, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(smem));
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pool_async<G, NCH, CR, IdxT, MODE>, WARPS * 32, smem);
@@ -408,8 +412,11 @@ static void launch_bulk_cr(const fx_segment *segs, int n_segs, int dim, const Id
                            cudaStream_t st, bool sf) {
   constexpr int WARPS = 4;
   const size_t smem = static_cast<size_t>(WARPS) * (32 / G) * (CR * G * 16 * NCH + 8);
-  static int per_sm = -1;
-  if (per_sm < 0) {
+  static int per_sm_dev[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int &per_sm = per_sm_dev[dev & 63];
+  if (per_sm <= 0) {
     cudaFuncSetAttribute(k_pool_bulk<G, NCH, CR, IdxT, MODE, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(smem));
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pool_bulk<G, NCH, CR, IdxT, MODE, MINB>, WARPS * 32,
