@@ -346,9 +346,8 @@ class Ranker:
         srv_occ = self._shard_server_dev[dest.long()] if nnz else torch.zeros(0, dtype=torch.int64, device=dev)
         miss = ~hit_occ
         grp = torch.zeros(n_bags * n_srv, dtype=torch.int64, device=dev)
-        if nnz:
-            grp.index_add_(0, (bag_of_occ * n_srv + srv_occ)[miss], torch.ones(int(miss.sum()), dtype=torch.int64,
-                                                                                 device=dev))
+        if nnz:  # misses per (bag, server); hits add 0 (no host sync for a mask count)
+            grp.index_add_(0, bag_of_occ * n_srv + srv_occ, miss.to(torch.int64))
         grp = grp.view(n_bags, n_srv)
         thr = self.params.pushdown_threshold
         if thr is None:
@@ -376,11 +375,15 @@ class Ranker:
         # 6. offers: raw-fetched misses, first raw occurrence order
         if cache is not None and nnz:
             raw_occ = miss & ~push.view(-1)[bag_of_occ * n_srv + srv_occ]
-            if bool(raw_occ.any()):
-                ords = lay.sm_start[bag_of_occ] + (torch.arange(nnz, device=dev) - lay.offsets[bag_of_occ])
-                big = torch.full((dd.n_uniq,), 1 << 62, dtype=torch.int64, device=dev)
-                big.scatter_reduce_(0, dd.inverse.long()[raw_occ], ords[raw_occ], reduce="amin")
-                cand = torch.nonzero(big < (1 << 62)).view(-1)
+            # first raw occurrence (sample-major ordinal) of every unique key; keys
+            # without a raw occurrence keep BIG (masked scatter: one host sync, for the count)
+            BIG = 1 << 62
+            ords = lay.sm_start[bag_of_occ] + (torch.arange(nnz, device=dev) - lay.offsets[bag_of_occ])
+            big = torch.full((dd.n_uniq,), BIG, dtype=torch.int64, device=dev)
+            big.scatter_reduce_(0, dd.inverse.long(), torch.where(raw_occ, ords, torch.full_like(ords, BIG)),
+                                reduce="amin")
+            cand = torch.nonzero(big < BIG).view(-1)
+            if cand.numel():
                 order = torch.argsort(big[cand])
                 keys = dd.uniq[cand[order]].contiguous()
                 cache.offer_keys(keys, int(keys.numel()))
