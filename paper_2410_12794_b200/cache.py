@@ -636,6 +636,8 @@ class AdaptiveCache:
         staged = ctypes.c_int64(0)
         _lib.check(self._L.fx_cache_stage(self._h, -1 if limit is None else int(limit), ctypes.byref(staged),
                                           _lib.stream_ptr()), "stage")
+        if staged.value == 0:
+            return []
         keys = self._pending_keys()[before:before + staged.value]
         known = {d.table for d in self._dir}
         for key in keys:
