@@ -11,6 +11,7 @@ time of the whole pipeline, and pooled lookups/s.
 """
 
 import argparse
+import gc
 import json
 import os
 import sys
@@ -59,6 +60,8 @@ def main():
                        for hb in batches]
         for pct in [float(x) for x in a.cache_pct.split(",")]:
             rows_cached = int(T * N * pct / 100)
+            free, total = torch.cuda.mem_get_info()
+            print(f"alpha {alpha} cache {pct}%: {free / 2**30:.1f} of {total / 2**30:.1f} GiB free", file=sys.stderr)
             budget = rows_cached * D * 4
             per_sample = 1
             model = C.MemoryModel(budget + 1_000 + B * per_sample, 1_000, per_sample)
@@ -94,6 +97,7 @@ def main():
                               "stage_ms_per_batch": {k: round(v / len(times), 3) for k, v in rk.stage_ms.items()}}),
                   flush=True)
             del rk, cache
+            gc.collect()
             torch.cuda.empty_cache()
 
 
