@@ -12,6 +12,7 @@ the Python side and u64 `table << 40 | row` on the device.
 from __future__ import annotations
 
 import ctypes
+import weakref
 from collections import deque
 from dataclasses import dataclass, field
 from enum import Enum
@@ -222,7 +223,9 @@ class FrequencySketch:
     """View of the device sketch (cache.py:114-144): exact decayed counts."""
 
     def __init__(self, cache: "AdaptiveCache", decay: float, prune_below: float = 0.25):
-        self._c = cache
+        # a weak back-reference: a cache <-> sketch cycle would keep the
+        # device buffers alive after `del cache` until the next GC pass
+        self._c = weakref.proxy(cache)
         self.decay = decay
         self.prune_below = prune_below
 

@@ -293,3 +293,24 @@ def test_ranker_large_cache_vs_oracle(thr):
     assert rk.cache.eviction_log == oc.evictions
     if thr is None:  # the cache filled and evicted with most entries outside the sorted prefix
         assert len(oc.evictions) > 0 and len(oc.lru_keys()) > 5_000
+
+
+def test_cache_frees_device_memory_on_del(C):
+    """Dropping the last reference to a cache returns its device buffers at
+    once (no cache <-> sketch cycle waiting for a GC pass)."""
+    import gc
+    torch.cuda.synchronize()
+    gc.disable()
+    try:
+        free0, _ = torch.cuda.mem_get_info()
+        cache = C.AdaptiveCache(1 << 30, admission="sketch", max_dim=128, slot_capacity=1 << 21)
+        cache.offer(0, 1, np.ones(128, np.float32))
+        torch.cuda.synchronize()
+        free1, _ = torch.cuda.mem_get_info()
+        assert free0 - free1 >= (1 << 21) * 512  # the row store alone
+        del cache
+        torch.cuda.synchronize()
+        free2, _ = torch.cuda.mem_get_info()
+        assert free0 - free2 < 64 << 20, (free0, free1, free2)
+    finally:
+        gc.enable()
