@@ -232,6 +232,9 @@ def main():
     if args.impl == "reference":
         return run_reference(args, rank, world)
 
+    # NCCL's own log lines (e.g. "NCCL version ..." under NCCL_DEBUG=WARN)
+    # default to stdout; keep stdout to the one JSON line
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     import torch
     import torch.distributed as dist
     torch.cuda.set_device(local)
@@ -531,6 +534,9 @@ def run_sharded(args, rank, world, local):
     # e2e: pinned host CSR -> device -> sharded lookup -> pinned host out
     e2e = None
     if not args.no_e2e:
+        # pinned staging next to this rank's GPU (multi-socket boxes)
+        from paper_2410_12794_b200.numa import bind_to_device
+        bind_to_device(local)
         pinned = [(torch.from_numpy(hb.indices).pin_memory(), torch.from_numpy(hb.offsets).pin_memory())
                   for hb in host_batches]
         out_h = torch.empty((B, F * dim), dtype=torch.float32, pin_memory=True)

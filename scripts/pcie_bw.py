@@ -1,10 +1,19 @@
 """Host<->device copy bandwidth on this box (pinned memory), for the e2e roofline."""
 import json
+import os
+import sys
+
 import torch
 
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
 torch.cuda.set_device(0)
 dev = torch.device("cuda", 0)
 res = {}
+if "--numa" in sys.argv:
+    from paper_2410_12794_b200.numa import bind_to_device, device_local_cpus
+    res["local_cpus"] = len(device_local_cpus(0))
+    res["bound"] = len(bind_to_device(0))
+res["cpus"] = len(os.sched_getaffinity(0))
 for mb in (9.6, 54.5, 218):
     n = int(mb * 1e6 / 4)
     h = torch.empty(n, dtype=torch.float32, pin_memory=True)

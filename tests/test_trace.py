@@ -115,3 +115,9 @@ def test_metrics_report_schema_vs_reference(golden_dir):
                         comparison={"speedup": 1.5}, invariants={"ok": True})
     assert rep.to_machine() == g["machine"]
     assert rep.to_text() == g["text"]
+
+
+def test_numa_cpulist_parser():
+    from paper_2410_12794_b200.numa import _parse_cpulist
+    assert _parse_cpulist("0-3,8,10-11\n") == [0, 1, 2, 3, 8, 10, 11]
+    assert _parse_cpulist("") == []
