@@ -70,7 +70,7 @@ SEGMENT_BYTES = ctypes.sizeof(FxSegment)
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
-        f"{LIB_PATH} is missing: build it with `python -m paper_2410_12794_b200.build` "
+        f"{LIB_PATH} is missing: build it with `python paper_2410_12794_b200/build.py` "
         "(there is no CPU fallback for the lookup path)")
 
 lib = ctypes.CDLL(LIB_PATH)

@@ -1,6 +1,6 @@
 """Build libflexemb.so (sm_100a) in-tree with nvcc.
 
-    python -m paper_2410_12794_b200.build [--verbose] [--force]
+    python paper_2410_12794_b200/build.py [--verbose] [--force]
 
 Each csrc/*.cu compiles to build/<name>.o (rebuilt when the source or a
 header changed), then links into paper_2410_12794_b200/libflexemb.so with the
