@@ -41,3 +41,17 @@ def test_host_helpers_without_gpu():
 def test_segment_struct_layout():
     import paper_2410_12794_b200._lib as L
     assert L.SEGMENT_BYTES == 8 * 8 + 4 + 4 + 2 * 8
+
+
+def test_build_entry_does_not_need_the_library():
+    """__graft_entry__.build() must work on a fresh checkout where
+    libflexemb.so does not exist yet: loading the build module may not run
+    the package __init__ (which refuses to import without the library)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys, __graft_entry__ as g; m = g._build_module(); "
+            "assert callable(m.build) and m.LIB.endswith('libflexemb.so'); "
+            "assert 'paper_2410_12794_b200' not in sys.modules")
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
