@@ -494,7 +494,7 @@ def flat_pool_batch(seed, dims: dict, bb: BagBatch, chunk_rows=1 << 20) -> dict:
                 acc[m] += vals[starts[m] + k]
             for n, b in enumerate(cb):
                 v = acc[n]
-                if bb.bag_op[b] == "mean":
+                if bb.bag_op[b] == "mean" and lens[n]:  # empty bags stay 0 (the reference rejects them)
                     v = v / lens[n]
                 out[int(b)] = v.astype(np.float32)
             i = j
