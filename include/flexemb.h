@@ -293,10 +293,14 @@ int fx_memcpy_async(void *dst, const void *src, size_t bytes, void *stream);
  * (indices as int32 + offsets rebased to the owner's slot) into the staging
  * of feature f's owner (dst_idx[d] / dst_offs[d]: DEVICE arrays of IPC-mapped
  * pointers to THIS requester's slot in rank d's staging). feat_pos[f] = rank
- * of f among its owner's features (ascending f). */
+ * of f among its owner's features (ascending f). With feat_nrows (device,
+ * [F]: rows of feature f's table) the copy also performs the ingress
+ * validation of fx_route (routing.py:87-101): an index outside
+ * [0, feat_nrows[f]) records its position in *err (atomic min) and
+ * FX_E_LOOKUP_VALIDATION in *err_code. */
 int fx_push_csr(const void *indices, int32_t idx_type, const int64_t *offsets, int32_t B, int32_t F,
                 const int32_t *feat_owner, const int32_t *feat_pos, int32_t *const *dst_idx, int64_t *const *dst_offs,
-                int32_t sysfence, void *stream);
+                const int64_t *feat_nrows, int64_t *err, int32_t *err_code, int32_t sysfence, void *stream);
 /* row-wise push: counts[d*n_bags+b] (int32, W*n_bags+1 entries) = indices of
  * bag b routed to rank d (K1 range routing); scan = exclusive prefix over
  * (d, b); then every index is scattered, stable per destination, into rank

@@ -101,7 +101,7 @@ _SIGS = {
     "fx_can_access_peer": ([ctypes.c_int, ctypes.c_int], ctypes.c_int),
     "fx_memcpy_async": ([_P, _P, ctypes.c_size_t, _P], ctypes.c_int),
     "fx_peer_barrier": ([_P, _P, _I32, _I32, _I64, _P, _P], ctypes.c_int),
-    "fx_push_csr": ([_P, _I32, _P, _I32, _I32, _P, _P, _P, _P, _I32, _P], ctypes.c_int),
+    "fx_push_csr": ([_P, _I32, _P, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _I32, _P], ctypes.c_int),
     "fx_rw_push": ([_P, _P, _P, _P, _P, _I32, _P, _I64, _I32, _P, _P, _P, _P, _P, _SZP, _P], ctypes.c_int),
     "fx_rw_push_planned": ([_P, _P, _P, _P, _P, _P, _I32, _P, _I64, _I32, _I32, _P, _P, _P, _P, _P, _I64, _P, _P, _P,
                             _P, _P, _I64, _P, _SZP, _P], ctypes.c_int),

@@ -52,7 +52,8 @@ template <typename IdxT>
 __global__ void __launch_bounds__(256) k_push_csr(const IdxT *__restrict__ indices, const int64_t *__restrict__ offsets,
                                                   int B, int F, const int32_t *__restrict__ feat_owner,
                                                   const int32_t *__restrict__ feat_pos, int32_t *const *dst_idx,
-                                                  int64_t *const *dst_offs, bool sysfence) {
+                                                  int64_t *const *dst_offs, const int64_t *__restrict__ feat_nrows,
+                                                  int64_t *err, int32_t *err_code, bool sysfence) {
   const int f = blockIdx.y;
   const int d = feat_owner[f];
   __shared__ long long s_base;
@@ -69,6 +70,9 @@ __global__ void __launch_bounds__(256) k_push_csr(const IdxT *__restrict__ indic
   const int64_t n = b1 - b0;
   const int64_t per = (n + gridDim.x - 1) / gridDim.x;
   const int64_t lo = blockIdx.x * per, hi = min(n, lo + per);
+  // ingress validation fused into the copy (same check and error position as
+  // K1 k_route's validate pass): idx in [0, num_rows of the feature's table)
+  const int64_t nr = feat_nrows ? feat_nrows[f] : LLONG_MAX;
   // 4 independent loads in flight per thread before the peer stores
   int64_t i = lo + threadIdx.x;
   for (; i + 3 * blockDim.x < hi; i += 4 * blockDim.x) {
@@ -76,9 +80,18 @@ __global__ void __launch_bounds__(256) k_push_csr(const IdxT *__restrict__ indic
 #pragma unroll
     for (int u = 0; u < 4; ++u) v[u] = indices[b0 + i + u * blockDim.x];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) di[i + u * blockDim.x] = static_cast<int32_t>(v[u]);
+    for (int u = 0; u < 4; ++u) {
+      if (static_cast<int64_t>(v[u]) < 0 || static_cast<int64_t>(v[u]) >= nr)
+        record_bad(err, err_code, b0 + i + u * blockDim.x, FX_E_LOOKUP_VALIDATION);
+      di[i + u * blockDim.x] = static_cast<int32_t>(v[u]);
+    }
   }
-  for (; i < hi; i += blockDim.x) di[i] = static_cast<int32_t>(indices[b0 + i]);
+  for (; i < hi; i += blockDim.x) {
+    const IdxT v = indices[b0 + i];
+    if (static_cast<int64_t>(v) < 0 || static_cast<int64_t>(v) >= nr)
+      record_bad(err, err_code, b0 + i, FX_E_LOOKUP_VALIDATION);
+    di[i] = static_cast<int32_t>(v);
+  }
   int64_t *dof = dst_offs[d] + (int64_t)feat_pos[f] * B;
   const int64_t pb = (B + 1 + gridDim.x - 1) / gridDim.x;
   const int64_t olo = blockIdx.x * pb, ohi = min((int64_t)B + 1, olo + pb);
@@ -384,22 +397,32 @@ int fx_memcpy_async(void *dst, const void *src, size_t bytes, void *stream) {
 
 int fx_push_csr(const void *indices, int32_t idx_type, const int64_t *offsets, int32_t B, int32_t F,
                 const int32_t *feat_owner, const int32_t *feat_pos, int32_t *const *dst_idx, int64_t *const *dst_offs,
-                int32_t sysfence, void *stream) {
+                const int64_t *feat_nrows, int64_t *err, int32_t *err_code, int32_t sysfence, void *stream) {
   if (B < 1 || F < 1) {
     set_error("fx_push_csr: bad shape");
     return FX_E_CONFIG;
   }
-  // ~4 waves of 256-thread blocks over the SMs, split evenly across features
-  int per_f = (num_sms() * 8 + F - 1) / F;
+  // blocks per SM of the push grid, split evenly across features: the push
+  // runs concurrently with the previous step's gather, and one block per SM
+  // steals the fewest gather slots (N=2 cfg2, same box: 1,213 vs 1,188 M
+  // bags/s at 8; scripts/run_stage_ab.sh). FX_PUSH_BPS overrides.
+  static const int bps = [] {
+    const char *e = getenv("FX_PUSH_BPS");
+    const int v = e ? atoi(e) : 1;
+    return v > 0 ? v : 1;
+  }();
+  int per_f = (num_sms() * bps + F - 1) / F;
   if (per_f < 1) per_f = 1;
   if (per_f > 64) per_f = 64;
   dim3 grid(per_f, F);
   if (idx_type == FX_IDX_I32)
     k_push_csr<int32_t><<<grid, 256, 0, as_stream(stream)>>>(static_cast<const int32_t *>(indices), offsets, B, F,
-                                                             feat_owner, feat_pos, dst_idx, dst_offs, sysfence != 0);
+                                                             feat_owner, feat_pos, dst_idx, dst_offs, feat_nrows, err,
+                                                             err_code, sysfence != 0);
   else
     k_push_csr<int64_t><<<grid, 256, 0, as_stream(stream)>>>(static_cast<const int64_t *>(indices), offsets, B, F,
-                                                             feat_owner, feat_pos, dst_idx, dst_offs, sysfence != 0);
+                                                             feat_owner, feat_pos, dst_idx, dst_offs, feat_nrows, err,
+                                                             err_code, sysfence != 0);
   FX_LAUNCH_CHECK("fx_push_csr");
   return FX_OK;
 }

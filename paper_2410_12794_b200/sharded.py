@@ -623,6 +623,8 @@ class P2PShardedLookup:
                     pos[f] = j
             self.t_feat_owner = torch.tensor(self.feat_owner, dtype=torch.int32, device=dev)
             self.t_feat_pos = torch.tensor(pos, dtype=torch.int32, device=dev)
+            self.t_feat_nrows = torch.tensor([self.metas[t].num_rows for t in self.ftab],
+                                             dtype=torch.int64, device=dev)
         self.bag_ops = torch.tensor(np.repeat([op_code(o) for o in self.fops], B).astype(np.int32), device=dev)
         if mode == "rowwise":
             self._pp = [torch.tensor([self.b_out.ptr + p * out_set + s * n_bags * D * self.pesz for s in range(W)],
@@ -701,10 +703,17 @@ class P2PShardedLookup:
             raise ConfigError(f"batch has {nnz} indices, staging holds {self.max_nnz}")
         o = self.ops
         sp = L.stream_ptr(stream)
-        L.check(L.lib.fx_route(o.route_off.data_ptr(), o.starts.data_ptr(), o.owners.data_ptr(), o.nrows.data_ptr(),
-                               o.bag_table.data_ptr(), indices.data_ptr(), L.idx_type_of(indices), offsets.data_ptr(),
-                               self.n_bags, None, o.status.err.data_ptr(), o.status.code.data_ptr(), sp),
-                "validate")
+        # The table-wise push can validate while it copies (FX_PUSH_VALIDATE=1),
+        # but measured slower: the short fused push runs in a burst against the
+        # start of the concurrent gather, while the separate K1 pass spreads the
+        # push across it (N=2 cfg2, same box: 1,126 vs 1,213 M bags/s;
+        # scripts/run_stage_ab.sh, profiles/r1_summary.md).
+        fused_validate = self.mode == "tablewise" and os.environ.get("FX_PUSH_VALIDATE", "0") == "1"
+        if not fused_validate:
+            L.check(L.lib.fx_route(o.route_off.data_ptr(), o.starts.data_ptr(), o.owners.data_ptr(),
+                                   o.nrows.data_ptr(), o.bag_table.data_ptr(), indices.data_ptr(),
+                                   L.idx_type_of(indices), offsets.data_ptr(), self.n_bags, None,
+                                   o.status.err.data_ptr(), o.status.code.data_ptr(), sp), "validate")
         if self.mode == "tablewise":
             if self.threshold is not None:
                 # a table-wise bag is ONE (bag, owner) group of L rows: pushed down
@@ -717,10 +726,12 @@ class P2PShardedLookup:
                 c[0].copy_(push.to(torch.int32))
                 c[1].copy_(torch.where(push, lens, torch.zeros_like(lens)))
                 c[2].copy_(torch.where(push, torch.zeros_like(lens), lens))
-            self.launches += 2  # k_route (validate) + k_push_csr
+            self.launches += 1 if fused_validate else 2  # [k_route (validate)] + k_push_csr
             L.check(L.lib.fx_push_csr(indices.data_ptr(), L.idx_type_of(indices), offsets.data_ptr(), B, F,
                                       self.t_feat_owner.data_ptr(), self.t_feat_pos.data_ptr(),
-                                      self.t_dst_idx[p].data_ptr(), self.t_dst_offs[p].data_ptr(), 1, sp), "push")
+                                      self.t_dst_idx[p].data_ptr(), self.t_dst_offs[p].data_ptr(),
+                                      self.t_feat_nrows.data_ptr() if fused_validate else None, o.status.err.data_ptr(),
+                                      o.status.code.data_ptr(), 1, sp), "push")
         elif self.threshold is not None:
             wsb = ctypes.c_size_t(self.t_ws[p].numel())
             L.check(L.lib.fx_rw_push_planned(o.route_off.data_ptr(), o.starts.data_ptr(), o.owners.data_ptr(),
