@@ -62,7 +62,12 @@ class ClockSampler:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
                                           "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=self.f, stderr=subprocess.DEVNULL)
-            time.sleep(0.3)
+            # nvidia-smi start-up is slow when several ranks launch it at once:
+            # wait for its first sample so a short timed region is still covered
+            t_end = time.time() + 5.0
+            while time.time() < t_end and os.path.getsize(self.f.name) == 0:
+                time.sleep(0.05)
+            time.sleep(0.1)
         except Exception:
             self.proc = None
 
@@ -93,7 +98,6 @@ class ClockSampler:
                     reasons.add(n)
         if not sm:
             return None
-        # keep the samples under load (top 75% of the observed clocks)
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "samples": len(sm), "reasons": sorted(reasons)}
 
 
