@@ -206,6 +206,8 @@ int fx_cache_destroy(fx_cache *c);
 int fx_cache_set_tables(fx_cache *c, const fx_table_dir *dir, int32_t n_dir, const int32_t *table_bytes,
                         int32_t n_tables);                                     /* host arrays */
 int fx_cache_scalars(fx_cache *c, int64_t *out21, void *stream);               /* [sync] */
+const void *fx_cache_scalars_device(fx_cache *c);  /* the 21 scalars in device memory (async snapshots) */
+int fx_cache_capacity(fx_cache *c, int64_t *out3);  /* slot, index and sketch table capacities */
 int fx_cache_reserve_sketch(fx_cache *c, int64_t new_keys, void *stream);      /* [sync] */
 int fx_cache_reserve_slots(fx_cache *c, int64_t slots, void *stream);          /* [sync] */
 /* get() per unique key (cache.py:189-202): hit -> last_tick = tick0 +
@@ -338,6 +340,36 @@ int fx_rw_push_planned(const int64_t *route_off, const int64_t *starts, const in
  * (~10 s); on timeout *timed_out (device int32, may be NULL) is set to 1. */
 int fx_peer_barrier(int64_t *my_flags, int64_t *const *peer_flags, int32_t rank, int32_t world, int64_t epoch,
                     int32_t *timed_out, void *stream);
+
+
+/* ---- fused per-batch cache step (fx_step.cu) ------------------------------
+ * One Ranker batch's locality layer with no host synchronisation
+ * (ranker.py:218-442 + cache.py:189-352 in the canonical order of SURVEY
+ * §8(c)): apply_pending_admissions -> validation + dedup -> probe -> plan
+ * (pushdown threshold, 0 = None) -> offers of raw-fetched misses; then
+ * fx_step_maintain: stage_hot_admissions(limit) -> sketch age. Domain: row
+ * keys of one entry size (dim*4 bytes) for every table, one shard per table
+ * on this GPU, no pooled-result keyspace. Errors raised on the device (bad
+ * index -> LookupValidationError, sketch capacity -> CapacityError) are read
+ * back with fx_step_scalars; a rejected batch leaves the cache untouched.
+ * Capturable in a CUDA graph once fx_step_prepare has run. */
+typedef struct fx_step fx_step;
+/* `slots` batches may be in flight (RankerParams.pipeline_depth): start(k)
+ * runs apply_pending + validation + probes of batch k, offer(k) its offers,
+ * maintain(k) stage + age; the reference interleaves them as S0 S1 F0 S2 F1
+ * ... (ranker.py:161-182), each phase reading the cache as it is then. */
+int fx_step_create(fx_step **out, fx_cache *cache, int64_t max_nnz, int64_t max_bags, const float *const *table_base,
+                   const int64_t *table_ld, const int64_t *table_rows, int32_t n_tables, int32_t dim,
+                   int64_t stage_limit_cap, int32_t slots);                     /* [sync] */
+int fx_step_destroy(fx_step *s);
+int fx_step_prepare(fx_step *s, void *stream);  /* LRU queue (re)build when another call moved entries */
+int fx_step_start(fx_step *s, int32_t slot, const int32_t *bag_table, const void *indices, int32_t idx_type,
+                  const int64_t *offsets, const int64_t *sm_start, int64_t n_bags, int64_t nnz, int32_t threshold,
+                  int32_t *hits_bag, int32_t *pd_groups, int32_t *pd_rows, int32_t *raw_rows, void *stream);
+int fx_step_offer(fx_step *s, int32_t slot, void *stream);
+int fx_step_maintain(fx_step *s, int32_t slot, int64_t stage_limit, int32_t do_age, void *stream);
+int fx_step_scalars(fx_step *s, int32_t slot, int64_t *out, int64_t n, void *stream);   /* [sync] */
+const void *fx_step_scalars_device(fx_step *s, int32_t slot);
 
 #ifdef __cplusplus
 }

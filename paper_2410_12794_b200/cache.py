@@ -206,11 +206,13 @@ def _sig():
         "fx_cache_pooled_touch": [P, P, P, I64, P],
         "fx_cache_read_slots": [P, P, I64, P, I32, P, P],
         "fx_cache_pooled_put": [P, P, P, I64, P, I32, P, P],
+        "fx_cache_scalars_device": [P],
+        "fx_cache_capacity": [P, P],
     }
     for n, a in sigs.items():
         f = getattr(L, n)
         f.argtypes = a
-        f.restype = ctypes.c_int
+        f.restype = ctypes.c_void_p if n == "fx_cache_scalars_device" else ctypes.c_int
     return L
 
 
@@ -261,6 +263,18 @@ class FrequencySketch:
         v = vals[:n.value].cpu().numpy()
         return [(decode_key(int(a)), float(b)) for a, b in zip(k, v)]
 
+    def ranked_arrays(self):
+        """[sync] (u64 keys, f64 counts) numpy arrays in (-count, key) order."""
+        c = self._c
+        n_live = c._scalars()["sketch_live"]
+        cap = max(1, n_live)
+        keys = torch.empty(cap, dtype=torch.int64, device=c.device)
+        vals = torch.empty(cap, dtype=torch.float64, device=c.device)
+        n = ctypes.c_int64(0)
+        _lib.check(c._L.fx_cache_sketch_ranked(c._h, keys.data_ptr(), vals.data_ptr(), cap, ctypes.byref(n),
+                                               _lib.stream_ptr()), "sketch ranked")
+        return keys[:n.value].cpu().numpy().view(np.uint64), vals[:n.value].cpu().numpy()
+
     def hottest(self, n: int, exclude=()) -> list:
         skip = set(exclude)
         return [k for k, _ in self.ranked() if k not in skip][:n]
@@ -304,6 +318,7 @@ class AdaptiveCache:
                                                1 if record_evictions else 0), "cache create")
         self._h = h
         self._slots = int(slot_capacity)
+        self._budget = int(budget_bytes)   # host mirror: the budget only changes through resize()
         self.sketch = FrequencySketch(self, sketch_decay)
 
     def __del__(self):
@@ -320,6 +335,16 @@ class AdaptiveCache:
         out = (ctypes.c_int64 * len(_SC))()
         _lib.check(self._L.fx_cache_scalars(self._h, out, _lib.stream_ptr()), "cache scalars")
         return dict(zip(_SC, list(out)))
+
+    def capacity(self) -> dict:
+        out = (ctypes.c_int64 * 3)()
+        _lib.check(self._L.fx_cache_capacity(self._h, out), "cache capacity")
+        return dict(slots=out[0], index=out[1], sketch=out[2])
+
+    def scalars_tensor(self) -> torch.Tensor:
+        """Zero-copy int64 view of the device scalars (_SC order), for async snapshots."""
+        from .step import _dev_view
+        return _dev_view(self._L.fx_cache_scalars_device(self._h), len(_SC), self.device)
 
     def _reserve_sketch(self, n_new: int):
         _lib.check(self._L.fx_cache_reserve_sketch(self._h, int(n_new), _lib.stream_ptr()), "reserve sketch")
@@ -374,7 +399,7 @@ class AdaptiveCache:
 
     @property
     def budget_bytes(self) -> int:
-        return self._scalars()["budget"]
+        return self._budget
 
     @property
     def used_bytes(self) -> int:
@@ -429,6 +454,38 @@ class AdaptiveCache:
         k = keys[:n.value].cpu().numpy().view(np.uint64)
         return [(decode_key(int(a), self._pooled_names), int(t), int(h)) for a, t, h in
                 zip(k, ticks[:n.value].cpu().numpy(), hits[:n.value].cpu().numpy())]
+
+    def lru_arrays(self):
+        """[sync] (u64 keys, int64 last_tick, int32 hits) numpy arrays in LRU order."""
+        n_e = self._scalars()["entries"]
+        cap = max(1, n_e)
+        keys = torch.empty(cap, dtype=torch.int64, device=self.device)
+        ticks = torch.empty(cap, dtype=torch.int64, device=self.device)
+        hits = torch.empty(cap, dtype=torch.int32, device=self.device)
+        n = ctypes.c_int64(0)
+        _lib.check(self._L.fx_cache_lru(self._h, keys.data_ptr(), ticks.data_ptr(), hits.data_ptr(), cap,
+                                        ctypes.byref(n), _lib.stream_ptr()), "cache lru")
+        k = n.value
+        return keys[:k].cpu().numpy().view(np.uint64), ticks[:k].cpu().numpy(), hits[:k].cpu().numpy()
+
+    def eviction_log_array(self):
+        """[sync] the eviction log as a u64 numpy array (record_evictions=True)."""
+        n_tot = self._scalars()["n_evlog"]
+        cap = max(1, n_tot)
+        out = torch.empty(cap, dtype=torch.int64, device=self.device)
+        n = ctypes.c_int64(0)
+        _lib.check(self._L.fx_cache_eviction_log(self._h, out.data_ptr(), cap, ctypes.byref(n), _lib.stream_ptr()),
+                   "eviction log")
+        if n.value > cap:
+            raise InvariantError("eviction log overflowed its device buffer")
+        return out[:n.value].cpu().numpy().view(np.uint64)
+
+    def sketch_arrays(self):
+        """[sync] (u64 keys sorted ascending, f64 counts) of the live sketch."""
+        ranked = self.sketch.ranked_arrays()
+        k, v = ranked
+        o = np.argsort(k, kind="stable")
+        return k[o], v[o]
 
     def lru_keys(self) -> list:
         return [e[0] for e in self.lru_entries()]
@@ -624,6 +681,7 @@ class AdaptiveCache:
         rep = ResizeReport(old_budget=old, new_budget=int(new_budget))
         self._reserve_slots_for(int(new_budget))
         _lib.check(self._L.fx_cache_set_budget(self._h, int(new_budget), _lib.stream_ptr()), "resize")
+        self._budget = int(new_budget)
         if self._scalars()["n_ev"]:
             rep.evicted = self._last_evicted()
         if new_budget > old and fetcher is not None:

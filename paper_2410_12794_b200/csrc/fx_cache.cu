@@ -28,151 +28,9 @@
 #include <cstdlib>
 #include <vector>
 
-#include "fx_common.cuh"
+#include "fx_cache.cuh"
 
 namespace fx {
-
-constexpr uint64_t kEmpty = ~0ull;
-constexpr uint64_t kTomb = ~0ull - 1;
-constexpr long long kFree = LLONG_MAX;
-constexpr int kRowBitsC = 40;
-constexpr uint64_t kRowMask = (1ull << kRowBitsC) - 1;
-
-struct Scalars {
-  long long budget, used, tick, hits, misses, entries;
-  long long free_top, sketch_live, sketch_tomb, hash_tomb, pending;
-  long long n_evlog, n_acc, n_ev, n_cand, staged;
-  long long err;   // 1: eviction queue exhausted (the reference's popitem on an empty
-                   //    OrderedDict), 2: pooled-key fingerprint collision
-  long long n_ov;  // in-place pooled re-puts recorded by the last put call
-  long long n_par_puts;  // put calls resolved by the parallel closed form (cumulative)
-  long long tiles_bulk, tiles_chain;  // k_offer_par sketch tiles resolved as one run / by peeling (cumulative)
-};
-
-struct CacheView {
-  Scalars *sc;
-  uint64_t *hkeys;
-  int32_t *hslot;
-  int64_t hcap;
-  uint64_t *skey;
-  uint64_t *skey2;  // second fingerprint of pooled-result keys (0 for row keys)
-  long long *stick;
-  int32_t *ssize;
-  int32_t *shits;
-  float *rows;
-  int64_t scap;
-  int32_t row_ld;
-  int32_t *free_stack;
-  uint64_t *kkeys;
-  double *kval;
-  uint8_t *kflag;
-  int64_t kcap;
-  uint64_t *pend;
-  int64_t pend_cap;
-  uint64_t *evlog;
-  int64_t evlog_cap;
-  const fx_table_dir *dir;
-  int32_t n_dir;
-  const int32_t *tbytes;
-  int32_t n_tbytes;
-  int32_t admission;
-  double decay, prune;
-};
-
-// ---------------------------------------------------------------- hashing
-__device__ __forceinline__ int32_t h_find(const CacheView &c, uint64_t key) {
-  const uint64_t m = static_cast<uint64_t>(c.hcap - 1);
-  uint64_t h = hash_key(key) & m;
-  for (int64_t probe = 0; probe < c.hcap; ++probe) {
-    const uint64_t k = c.hkeys[h];
-    if (k == key) return c.hslot[h];
-    if (k == kEmpty) return -1;
-    h = (h + 1) & m;
-  }
-  return -1;
-}
-
-__device__ __forceinline__ void h_insert(const CacheView &c, uint64_t key, int32_t slot) {
-  const uint64_t m = static_cast<uint64_t>(c.hcap - 1);
-  uint64_t h = hash_key(key) & m;
-  while (true) {
-    const unsigned long long prev =
-        atomicCAS(reinterpret_cast<unsigned long long *>(&c.hkeys[h]), (unsigned long long)kEmpty,
-                  (unsigned long long)key);
-    if (prev == kEmpty || prev == key) {
-      c.hslot[h] = slot;
-      return;
-    }
-    h = (h + 1) & m;
-  }
-}
-
-__device__ __forceinline__ bool h_erase(const CacheView &c, uint64_t key) {
-  const uint64_t m = static_cast<uint64_t>(c.hcap - 1);
-  uint64_t h = hash_key(key) & m;
-  for (int64_t probe = 0; probe < c.hcap; ++probe) {
-    const uint64_t k = c.hkeys[h];
-    if (k == key) {
-      c.hkeys[h] = kTomb;
-      return true;
-    }
-    if (k == kEmpty) return false;
-    h = (h + 1) & m;
-  }
-  return false;
-}
-
-__device__ __forceinline__ int64_t k_find(const CacheView &c, uint64_t key) {
-  const uint64_t m = static_cast<uint64_t>(c.kcap - 1);
-  uint64_t h = hash_key(key) & m;
-  for (int64_t probe = 0; probe < c.kcap; ++probe) {
-    const uint64_t k = c.kkeys[h];
-    if (k == key) return static_cast<int64_t>(h);
-    if (k == kEmpty) return -1;
-    h = (h + 1) & m;
-  }
-  return -1;
-}
-
-__device__ __forceinline__ double k_est(const CacheView &c, uint64_t key) {
-  const int64_t i = k_find(c, key);
-  return i >= 0 ? c.kval[i] : 0.0;
-}
-
-// insert-or-add (returns true when the key was new)
-__device__ __forceinline__ bool k_add(const CacheView &c, uint64_t key, double w) {
-  const uint64_t m = static_cast<uint64_t>(c.kcap - 1);
-  uint64_t h = hash_key(key) & m;
-  while (true) {
-    const unsigned long long prev =
-        atomicCAS(reinterpret_cast<unsigned long long *>(&c.kkeys[h]), (unsigned long long)kEmpty,
-                  (unsigned long long)key);
-    if (prev == kEmpty || prev == key) {
-      atomicAdd(&c.kval[h], w);
-      return prev == kEmpty;
-    }
-    h = (h + 1) & m;
-  }
-}
-
-__device__ __forceinline__ int32_t table_bytes_of(const CacheView &c, uint64_t key) {
-  const int64_t t = static_cast<int64_t>(key >> kRowBitsC);
-  return (t >= 0 && t < c.n_tbytes) ? c.tbytes[t] : -1;
-}
-
-__device__ __forceinline__ const float *dir_row(const CacheView &c, uint64_t key, int32_t *dim) {
-  const int32_t t = static_cast<int32_t>(key >> kRowBitsC);
-  const int64_t r = static_cast<int64_t>(key & kRowMask);
-  for (int i = 0; i < c.n_dir; ++i) {
-    const fx_table_dir &d = c.dir[i];
-    if (d.table == t && r >= d.row_begin && r < d.row_end) {
-      *dim = d.dim;
-      return d.base + (r - d.row_begin) * d.ld;
-    }
-  }
-  *dim = 0;
-  return nullptr;
-}
 
 // ---------------------------------------------------------------- init
 __global__ void k_cache_init(CacheView c) {
@@ -1217,22 +1075,6 @@ static inline int lru_bits(long long tick) {
 
 using namespace fx;
 
-struct fx_cache {
-  CacheView v;
-  int32_t record;
-  std::vector<fx_table_dir> dir_host;
-  std::vector<int32_t> tbytes_host;
-  fx_table_dir *dir_dev = nullptr;
-  int32_t *tbytes_dev = nullptr;
-  void *ws = nullptr;
-  size_t ws_bytes = 0;
-  int32_t uniform = 0;             // common row size of every table (0 unset, -1 mixed)
-  int parallel_offers = 1;         // use k_offer_par when sizes are uniform
-  uint64_t *last_ev = nullptr;     // keys evicted by the last offer/apply/resize
-  int64_t last_ev_cap = 0;
-  const float *const *pending_rows = nullptr;  // optional per-pending-key row pointers
-  int32_t *lru_hist = nullptr;     // 65536 bins + counter for the partial LRU order
-};
 
 namespace {
 
@@ -1501,7 +1343,7 @@ int fx_cache_create(fx_cache **out, int64_t slot_capacity, int32_t max_dim, int3
   v.hcap = pow2_at_least(4 * v.scap);
   v.kcap = pow2_at_least(sketch_capacity > 0 ? 2 * sketch_capacity : 4096);
   v.pend_cap = v.scap + 1024;
-  v.evlog_cap = record_evictions ? 1 << 20 : 0;
+  v.evlog_cap = record_evictions ? (8 * v.scap > (1 << 20) ? 8 * v.scap : (1 << 20)) : 0;
   v.admission = admission;
   v.decay = decay;
   v.prune = prune_below;
@@ -1547,7 +1389,7 @@ int fx_cache_destroy(fx_cache *c) {
   if (!c) return FX_OK;
   CacheView &v = c->v;
   void *ps[] = {v.sc, v.hkeys, v.hslot, v.skey, v.skey2, v.stick, v.ssize, v.shits, v.rows, v.free_stack, v.kkeys,
-                v.kval, v.kflag, v.pend, v.evlog, c->dir_dev, c->tbytes_dev, c->ws, c->last_ev, c->lru_hist};
+                v.kval, v.kflag, v.pend, v.evlog, c->dir_dev, c->tbytes_dev, c->ws, c->last_ev, c->lru_hist, c->q};
   for (void *p : ps)
     if (p) cudaFree(p);
   delete c;
@@ -1582,7 +1424,17 @@ int fx_cache_scalars(fx_cache *c, int64_t *out, void *stream) {
   return FX_OK;
 }
 
+const void *fx_cache_scalars_device(fx_cache *c) { return c->v.sc; }
+
+int fx_cache_capacity(fx_cache *c, int64_t *out3) {
+  out3[0] = c->v.scap;
+  out3[1] = c->v.hcap;
+  out3[2] = c->v.kcap;
+  return FX_OK;
+}
+
 int fx_cache_set_budget(fx_cache *c, int64_t budget, void *stream) {
+  c->queue_valid = 0;
   cudaStream_t st = as_stream(stream);
   cudaMemcpyAsync(&c->v.sc->budget, &budget, 8, cudaMemcpyHostToDevice, st);
   // shrink: evict LRU until used <= budget (cache.py:270-274)
@@ -1616,6 +1468,7 @@ int fx_cache_reserve_sketch(fx_cache *c, int64_t new_keys, void *stream) {
 }
 
 int fx_cache_reserve_slots(fx_cache *c, int64_t slots, void *stream) {
+  c->queue_valid = 0;
   cudaStream_t st = as_stream(stream);
   if (slots <= c->v.scap) return FX_OK;
   int rc = cuda_check(cudaStreamSynchronize(st), "fx_cache_reserve_slots");
@@ -1678,6 +1531,7 @@ int fx_cache_reserve_slots(fx_cache *c, int64_t slots, void *stream) {
 
 int fx_cache_probe(fx_cache *c, const uint64_t *uniq, const int32_t *mult, const int64_t *last_ord,
                    const int64_t *n_uniq_dev, int64_t n_uniq_host, int64_t nnz, int32_t *slot_out, void *stream) {
+  c->queue_valid = 0;
   cudaStream_t st = as_stream(stream);
   const int64_t work = n_uniq_dev ? nnz : n_uniq_host;
   k_probe<<<grid_for(work > 0 ? work : 1, 256), 256, 0, st>>>(c->v, uniq, mult, last_ord, n_uniq_dev, n_uniq_host,
@@ -1689,10 +1543,12 @@ int fx_cache_probe(fx_cache *c, const uint64_t *uniq, const int32_t *mult, const
 
 int fx_cache_offer(fx_cache *c, const uint64_t *keys, int64_t n, const int32_t *sizes, const float *const *src_rows,
                    uint8_t *accepted, void *stream) {
+  c->queue_valid = 0;
   return run_offer(c, keys, n, 0, sizes, src_rows, accepted, as_stream(stream));
 }
 
 int fx_cache_apply_pending(fx_cache *c, int64_t *applied, void *stream) {
+  c->queue_valid = 0;
   cudaStream_t st = as_stream(stream);
   Scalars h;
   int rc = read_scalars(c, &h, st);
@@ -1935,6 +1791,7 @@ int fx_cache_rows(fx_cache *c, const float **rows, int64_t *ld) {
 }
 
 int fx_cache_advance_tick(fx_cache *c, int64_t n, void *stream) {
+  c->queue_valid = 0;
   k_advance_tick<<<1, 1, 0, as_stream(stream)>>>(c->v.sc, n);
   FX_LAUNCH_CHECK("fx_cache_advance_tick");
   return FX_OK;
@@ -1949,6 +1806,7 @@ int fx_cache_pooled_find(fx_cache *c, const uint64_t *key_a, const uint64_t *key
 }
 
 int fx_cache_pooled_touch(fx_cache *c, const int32_t *slot, const int64_t *pos, int64_t n, void *stream) {
+  c->queue_valid = 0;
   if (n <= 0) return FX_OK;
   k_pooled_touch<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(c->v, slot, pos, n);
   FX_LAUNCH_CHECK("fx_cache_pooled_touch");
@@ -1965,6 +1823,7 @@ int fx_cache_read_slots(fx_cache *c, const int32_t *slot, int64_t n, float *out,
 
 int fx_cache_pooled_put(fx_cache *c, const uint64_t *key_a, const uint64_t *key_b, int64_t n, const int32_t *sizes,
                         int32_t uniform_size, const float *const *src_rows, void *stream) {
+  c->queue_valid = 0;
   cudaStream_t st = as_stream(stream);
   if (n <= 0) return FX_OK;
   if (!key_a || !key_b || !src_rows || (!sizes && uniform_size <= 0)) {

@@ -1,0 +1,1468 @@
+// Fused per-batch cache step: the whole locality layer of one Ranker batch
+// (embserve ranker.py:218-442 with cache.py:189-352) as one stream of device
+// kernels with NO host synchronisation, so a batch can be captured in a CUDA
+// graph and overlapped with the gather+pool kernel (K4) on another stream.
+//
+// Domain (checked by the host before it chooses this path): row keys only
+// (no pooled-result keyspace), one entry size S for every table, one shard
+// per table on this GPU. Order and semantics are the canonical order of
+// SURVEY §8(c), bit-exact with the reference's AdaptiveCache:
+//
+//   1. apply_pending_admissions: staged keys inserted in order, always-admit
+//      _insert (cache.py:344-352, 256-268) — one warp;
+//   2. ingress validation + per-batch dedup (K2): u64 key table<<40|row,
+//      multiplicity, first / last (lookup, feature, position) ordinal. A bad
+//      index sets an error word and every later kernel of the batch is a
+//      no-op, so a rejected batch leaves the cache untouched
+//      (ranker.py:184-193 validates before any probe);
+//   3. probe (K3) once per unique key: a key cached at batch start hits on
+//      every occurrence, last_tick = tick0 + last ordinal + 1, hits += mult;
+//      a missing key bumps the exact sketch by its multiplicity
+//      (cache.py:189-202);
+//   4. plan + per-bag counters: a bag is one (lookup, feature, server) group;
+//      misses >= threshold push down, else they are raw-fetched
+//      (pooling.py:88-100; threshold None = every miss raw);
+//   5. offers of the raw-fetched misses in first raw-occurrence order
+//      (ranker.py:338-340, 417-423; cache.py:237-268);
+//   6. stage_hot_admissions(limit) (cache.py:311-342) and sketch age
+//      (cache.py:128-136) — fx_step_maintain.
+//
+// The offers (5) are the order-dependent part. With one entry size, after
+// the F free units are used every accept evicts exactly one entry, so the
+// eviction queue is V = [entries in LRU order] and accept r evicts V[r - F].
+// Candidate j (j >= F) is accepted iff est(c_j) >= est(V[a_j]), a_j = number
+// of phase-2 accepts before j. Every candidate was bumped this batch, so
+// est(c_j) >= minC >= 1 and a victim with est <= minC accepts whoever comes:
+// only "hard" victims (est > minC; ~0.1% of V on cfg3) can reject. One warp
+// walks the hard victims: it jumps over the easy stretch between two hard
+// victims (each easy victim takes the next candidate), and for a hard victim
+// of estimate e finds the next candidate with est >= e (a shared-memory
+// table of per-block maxima plus one coalesced 256-candidate probe). The
+// rejected intervals it emits fully determine the decisions; ticks, slots,
+// evictions, hash updates and row copies are then applied in parallel over
+// accept ranks. Batches outside that domain (more accepts than entries, a
+// cache above budget) run an exact single-thread loop instead
+// (ks_seq_offer), chosen on the device.
+//
+// The LRU order is kept as an explicit queue (fx_cache.q): each step
+// compacts it to [entries not hit this batch, old order] ++ [hit entries by
+// last ordinal] — the reference's OrderedDict after the probes — and appends
+// the accepts, so no tick sort is needed.
+
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
+#include <cub/iterator/counting_input_iterator.cuh>
+
+#include <climits>
+#include <cstring>
+#include <vector>
+
+#include "fx_cache.cuh"
+
+namespace fx {
+namespace stp {
+
+constexpr int kFine = 256;          // candidates per fine probe of the offer chain
+constexpr int kTopkBins = 1 << 16;  // radix-select digit histogram (16-bit digits)
+
+enum { MODE_NONE = 0, MODE_PAR = 1, MODE_SEQ = 2 };
+
+// Device-resident per-step state (all per-batch control lives here so the
+// captured graph needs no host input).
+struct StepScalars {
+  long long err;           // 0 ok, 1 bad index (batch rejected), 2 sketch capacity, 3 invariant
+  unsigned long long err_at;  // min over bad occurrences of (sample-major ordinal << 32 | CSR position)
+  long long epoch;         // batch counter (slot hit marks)
+  long long n_uniq, n_cand, n_hitu, n_nonhit, n_hard, n_rej, n_off;
+  long long e0, F, mode, n_acc, n_ev, ftop0, log0;
+  long long tick0, tick_base;
+  long long minc_bits;     // min candidate estimate (bits of a positive double)
+  long long b_hits, b_misses, b_groups;   // this batch
+  long long b_applied;     // pending admissions installed at batch start
+  long long b_pd_groups, b_pd_rows, b_raw_rows;     // per-batch sums of the per-bag counters
+  long long rebuild_index, rehash_sketch, rehash_n;
+  long long stage_on, topk_live, topk_krem, topk_n;  // stage(limit) radix select
+  unsigned long long topk_hi, topk_lo;               // selected prefix of (vinv, key)
+  long long topk_digit;
+  long long qlen_new;
+  long long pad[8];
+};
+
+struct DEnt {       // per dedup-hash slot (one 16-byte line for the atomics)
+  int32_t mult, first, last, hit;
+};
+
+struct StepView {
+  StepScalars *ss;   // this batch's slot
+  StepScalars *gs;   // global (epoch counter)
+  // dedup hash
+  uint64_t *dkey;
+  DEnt *dent;
+  double *dC;        // sketch estimate after this batch's bump (misses)
+  int32_t *dfraw;    // first raw-occurrence ordinal (threshold mode)
+  int64_t dcap;
+  int32_t *uniq;     // claimed dedup slots
+  int32_t *inv;      // per occurrence (CSR position) -> dedup slot
+  int32_t *cand_by_first;  // [max_nnz] scatter by ordinal
+  int32_t *hit_by_last;    // [max_nnz]
+  int32_t *cand;     // compacted candidates (dedup slots) in first raw-occurrence order
+  uint64_t *ckey;    // [max_nnz] this slot's candidate keys (kept from start to offer)
+  double *estv;      // [max_nnz] candidate estimates at offer time
+  int32_t *pres;     // [max_nnz] 1 = candidate absent at offer time
+  int32_t *cidx;     // [max_nnz] absent candidates (positions into ckey)
+  uint64_t *okey;    // [max_nnz] absent candidate keys in offer order
+  int32_t *hits_ord; // compacted hit cache slots in last-ordinal order
+  double *cC;        // candidate estimates in offer order
+  double *bmax;      // per kFine-block max of cC
+  int32_t *q;        // the cache's LRU queue (fx_cache.q)
+  int32_t *qnew;     // [scap] V = compacted queue
+  int32_t *sflag;    // [scap] epoch of the last hit
+  double *E;         // [scap] victim estimates
+  int32_t *hardf;    // [scap] hard-victim flags
+  int32_t *hard;     // [scap] compacted hard positions
+  int32_t *rj_beg, *rj_end;  // reject intervals
+  int32_t *acc;      // [max_nnz] accept flags, then ranks
+  int32_t *rank;
+  int32_t *accslot;  // [max_nnz] slot taken by accept r (sequential mode)
+  int32_t *accj;     // [max_nnz] candidate index of accept r (sequential mode)
+  int64_t max_nnz;
+  // per-table row source and validation bounds (dense by table id)
+  const float *const *tbase;
+  const int64_t *tld;
+  const int64_t *trows;
+  int32_t n_tables;
+  int32_t S;         // entry size in bytes
+  int32_t dim;       // floats per row
+  // rehash / top-k temporaries
+  uint64_t *tk_key;
+  uint64_t *tk_vinv;
+  double *tk_val;
+  uint8_t *tk_flag;
+  int64_t tk_cap;
+  int32_t *tk_hist;
+  int32_t *tk_sel;   // selected top-k list positions
+};
+
+// ---------------------------------------------------------------- helpers
+__device__ __forceinline__ bool aborted(const StepView &v) { return v.ss->err != 0; }
+
+__device__ __forceinline__ long long warp_sum(long long x) {
+  for (int o = 16; o; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+  return x;
+}
+
+// warp-aggregated atomicAdd of a per-lane count; returns this lane's base
+__device__ __forceinline__ long long warp_append(unsigned long long *ctr, int want) {
+  const unsigned m = __ballot_sync(0xffffffffu, want);
+  const int lane = threadIdx.x & 31;
+  unsigned long long base = 0;
+  if (m) {
+    const int leader = __ffs(m) - 1;
+    if (lane == leader) base = atomicAdd(ctr, (unsigned long long)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, leader);
+  }
+  return (long long)base + __popc(m & ((1u << lane) - 1u));
+}
+
+__device__ __forceinline__ const float *row_src(const StepView &v, uint64_t key) {
+  const int64_t t = static_cast<int64_t>(key >> kRowBitsC);
+  const int64_t r = static_cast<int64_t>(key & kRowMask);
+  return v.tbase[t] + r * v.tld[t];
+}
+
+// copy one row (dim floats) with the calling warp
+__device__ __forceinline__ void warp_copy_row(float *dst, const float *src, int dim, int lane) {
+  if ((dim & 3) == 0 && ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
+    const float4 *s4 = reinterpret_cast<const float4 *>(src);
+    float4 *d4 = reinterpret_cast<float4 *>(dst);
+    for (int i = lane; i < dim / 4; i += 32) d4[i] = __ldg(&s4[i]);
+  } else {
+    for (int i = lane; i < dim; i += 32) dst[i] = __ldg(&src[i]);
+  }
+}
+
+__device__ __forceinline__ double sketch_add_val(const CacheView &c, uint64_t key, double w, bool *born) {
+  const uint64_t m = static_cast<uint64_t>(c.kcap - 1);
+  uint64_t h = hash_key(key) & m;
+  while (true) {
+    const unsigned long long prev =
+        atomicCAS(reinterpret_cast<unsigned long long *>(&c.kkeys[h]), (unsigned long long)kEmpty,
+                  (unsigned long long)key);
+    if (prev == kEmpty || prev == key) {
+      const double old = atomicAdd(&c.kval[h], w);
+      *born = prev == kEmpty;
+      return old + w;
+    }
+    h = (h + 1) & m;
+  }
+}
+
+// ---------------------------------------------------------------- 0. start
+__global__ void ks_begin(CacheView c, StepView v, int64_t max_nnz) {
+  StepScalars *s = v.ss;
+  s->err = 0;
+  s->err_at = ~0ull;
+  v.gs->epoch += 1;  // global batch counter (slot hit marks)
+  s->epoch = v.gs->epoch;
+  s->n_uniq = s->n_cand = s->n_hitu = s->n_nonhit = s->n_hard = s->n_rej = s->n_off = 0;
+  s->n_acc = s->n_ev = 0;
+  s->mode = MODE_NONE;
+  s->minc_bits = LLONG_MAX;
+  s->b_hits = s->b_misses = s->b_groups = 0;
+  s->b_applied = 0;
+  s->b_pd_groups = s->b_pd_rows = s->b_raw_rows = 0;
+  // sketch room for this batch's new keys (bounded by the batch's nnz)
+  const Scalars *sc = c.sc;
+  const long long live = sc->sketch_live, tomb = sc->sketch_tomb;
+  s->rehash_sketch = ((live + tomb + max_nnz) * 10 > c.kcap * 7) ? 1 : 0;
+  s->rehash_n = 0;
+  if ((live + max_nnz) * 10 > c.kcap * 7) s->err = 2;  // sketch_capacity too small for this batch
+}
+
+// in-place sketch rehash (drops tombstones): collect -> clear -> reinsert
+__global__ void ks_sketch_collect(CacheView c, StepView v) {
+  if (!v.ss->rehash_sketch) return;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < c.kcap; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = c.kkeys[i];
+    const bool live = k != kEmpty && k != kTomb;
+    const long long p = warp_append(reinterpret_cast<unsigned long long *>(&v.ss->rehash_n), live);
+    if (live) {
+      v.tk_key[p] = k;
+      v.tk_val[p] = c.kval[i];
+      v.tk_flag[p] = c.kflag[i];
+    }
+  }
+}
+
+__global__ void ks_sketch_clear(CacheView c, StepView v) {
+  if (!v.ss->rehash_sketch) return;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < c.kcap; i += (int64_t)gridDim.x * blockDim.x) {
+    c.kkeys[i] = kEmpty;
+    c.kval[i] = 0.0;
+    c.kflag[i] = 0;
+  }
+}
+
+__global__ void ks_sketch_reinsert(CacheView c, StepView v) {
+  if (!v.ss->rehash_sketch) return;
+  const long long n = v.ss->rehash_n;
+  const uint64_t m = static_cast<uint64_t>(c.kcap - 1);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = v.tk_key[i];
+    uint64_t h = hash_key(k) & m;
+    while (atomicCAS(reinterpret_cast<unsigned long long *>(&c.kkeys[h]), (unsigned long long)kEmpty,
+                     (unsigned long long)k) != kEmpty)
+      h = (h + 1) & m;
+    c.kval[h] = v.tk_val[i];
+    c.kflag[h] = v.tk_flag[i];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) c.sc->sketch_tomb = 0;
+}
+
+// ---------------------------------------------------------------- 1. apply pending
+// cache.py:344-352: install the keys staged by the last maintenance, in
+// order, always-admit (_insert evicts the LRU head until the entry fits).
+// One warp: lane 0 decides, the warp copies each installed row.
+__global__ void ks_apply_pending(CacheView c, StepView v) {
+  const int lane = threadIdx.x & 31;
+  if (blockIdx.x != 0 || threadIdx.x >= 32 || aborted(v)) return;
+  Scalars *sc = c.sc;
+  const long long n = sc->pending;
+  if (n <= 0) return;
+  const long long S = v.S;
+  long long e = sc->entries, head = 0, ftop = sc->free_top, tick = sc->tick, nlog = sc->n_evlog, tombs = 0;
+  long long applied = 0;
+  long long qlen = e;
+  for (long long i = 0; i < n; ++i) {
+    const uint64_t key = c.pend[i];
+    int32_t slot = -1;
+    if (lane == 0) {
+      const int64_t kp = k_find(c, key);
+      if (kp >= 0) c.kflag[kp] = 0;
+      const bool present = h_find(c, key) >= 0;
+      if (!present && S <= sc->budget) {
+        while ((e + 1) * S > sc->budget && e > 0) {  // evict the LRU head
+          const int32_t vs = v.q[head];
+          v.q[head] = -1;
+          ++head;
+          const uint64_t ok = c.skey[vs];
+          if (c.evlog_cap > 0 && nlog < c.evlog_cap) c.evlog[nlog] = ok;
+          if (c.evlog_cap > 0) ++nlog;
+          tombs += h_erase(c, ok) ? 1 : 0;
+          c.stick[vs] = kFree;
+          c.skey[vs] = kEmpty;
+          c.free_stack[ftop++] = vs;
+          --e;
+        }
+        slot = c.free_stack[--ftop];
+        ++tick;
+        c.skey[slot] = key;
+        c.skey2[slot] = 0;
+        c.stick[slot] = tick;
+        c.ssize[slot] = static_cast<int32_t>(S);
+        c.shits[slot] = 0;
+        h_insert(c, key, slot);
+        v.q[qlen++] = slot;
+        ++e;
+        ++applied;
+      }
+    }
+    slot = __shfl_sync(0xffffffffu, slot, 0);
+    if (slot >= 0) warp_copy_row(c.rows + static_cast<int64_t>(slot) * c.row_ld, row_src(v, key), v.dim, lane);
+  }
+  if (lane == 0) {
+    sc->entries = e;
+    sc->used = e * S;
+    sc->free_top = ftop;
+    sc->tick = tick;
+    sc->n_evlog = nlog;
+    sc->hash_tomb += tombs;
+    sc->pending = 0;
+    v.ss->b_applied = applied;
+  }
+}
+
+// ---------------------------------------------------------------- 2. validate + dedup
+// A warp takes 32 consecutive bags; its lanes walk the bags' occurrences 32
+// at a time, each lane locating its bag with a 5-step shuffle search over the
+// 33 bag offsets the warp holds.
+template <typename IdxT>
+__global__ void __launch_bounds__(256) ks_dedup(StepView v, const int32_t *__restrict__ bag_table,
+                                                const IdxT *__restrict__ idx, const int64_t *__restrict__ offsets,
+                                                const int64_t *__restrict__ sm_start, int64_t n_bags) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const uint64_t dm = static_cast<uint64_t>(v.dcap - 1);
+  for (int64_t b0 = warp * 32; b0 < n_bags; b0 += nw * 32) {
+    const int64_t nb = n_bags - b0 < 32 ? n_bags - b0 : 32;
+    const int64_t my = b0 + (lane < nb ? lane : nb - 1);
+    const int64_t off = lane < nb ? __ldg(&offsets[b0 + lane]) : __ldg(&offsets[b0 + nb]);
+    const int64_t end = __ldg(&offsets[b0 + nb]);
+    const int32_t tab = __ldg(&bag_table[my]);
+    const int64_t sms = __ldg(&sm_start[my]);
+    const int64_t start = __shfl_sync(0xffffffffu, off, 0);
+    for (int64_t p0 = start; p0 < end; p0 += 32) {
+      const int64_t p = p0 + lane;
+      // bag j: last lane with off_j <= p
+      int lo = 0, hi = static_cast<int>(nb);
+#pragma unroll
+      for (int it = 0; it < 6; ++it) {
+        const int mid = (lo + hi) >> 1;
+        const int64_t om = __shfl_sync(0xffffffffu, off, mid & 31);
+        if (hi - lo > 1) {
+          if (om <= p) lo = mid; else hi = mid;
+        }
+      }
+      const int j = lo;
+      const int64_t bo = __shfl_sync(0xffffffffu, off, j);
+      const int32_t t = __shfl_sync(0xffffffffu, tab, j);
+      const int64_t sm = __shfl_sync(0xffffffffu, sms, j);
+      const bool act = p < end;
+      int claimed = 0;
+      int32_t u = -1;
+      int ord = 0;
+      if (act) {
+        const int64_t r = static_cast<int64_t>(idx[p]);
+        ord = static_cast<int>(sm + (p - bo));
+        const bool okt = t >= 0 && t < v.n_tables;
+        if (!okt || r < 0 || r >= v.trows[t]) {
+          atomicMin(reinterpret_cast<unsigned long long *>(&v.ss->err_at),
+                    (static_cast<unsigned long long>(ord) << 32) | static_cast<unsigned long long>(p & 0xffffffff));
+          v.ss->err = 1;
+        } else {
+          const uint64_t key = (static_cast<uint64_t>(t) << kRowBitsC) | static_cast<uint64_t>(r);
+          uint64_t h = hash_key(key) & dm;
+          while (true) {
+            const unsigned long long prev = atomicCAS(reinterpret_cast<unsigned long long *>(&v.dkey[h]),
+                                                      (unsigned long long)kEmpty, (unsigned long long)key);
+            if (prev == kEmpty) { claimed = 1; break; }
+            if (prev == key) break;
+            h = (h + 1) & dm;
+          }
+          u = static_cast<int32_t>(h);
+          DEnt *e = &v.dent[u];
+          atomicAdd(&e->mult, 1);
+          atomicMin(&e->first, ord);
+          atomicMax(&e->last, ord);
+          v.inv[p] = u;
+        }
+      }
+      const long long pos = warp_append(reinterpret_cast<unsigned long long *>(&v.ss->n_uniq), claimed);
+      if (claimed) v.uniq[pos] = u;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- 3. probe
+__global__ void __launch_bounds__(256) ks_probe(CacheView c, StepView v, int32_t threshold_on) {
+  if (aborted(v)) return;
+  const long long n = v.ss->n_uniq;
+  const long long tick0 = c.sc->tick;
+  const long long epoch = v.ss->epoch;
+  long long hits = 0, misses = 0, born = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t u = v.uniq[i];
+    const uint64_t key = v.dkey[u];
+    DEnt e = v.dent[u];
+    const int32_t s = h_find(c, key);
+    if (s >= 0) {
+      c.stick[s] = tick0 + e.last + 1;
+      c.shits[s] += e.mult;
+      v.sflag[s] = static_cast<int32_t>(epoch);
+      v.hit_by_last[e.last] = s;
+      hits += e.mult;
+    } else {
+      bool b = false;
+      sketch_add_val(c, key, static_cast<double>(e.mult), &b);
+      born += b ? 1 : 0;
+      misses += e.mult;
+      if (!threshold_on) v.cand_by_first[e.first] = u;
+    }
+    v.dent[u].hit = s;
+  }
+  hits = warp_sum(hits);
+  misses = warp_sum(misses);
+  born = warp_sum(born);
+  if ((threadIdx.x & 31) == 0) {
+    if (hits) atomicAdd(reinterpret_cast<unsigned long long *>(&c.sc->hits), (unsigned long long)hits);
+    if (misses) atomicAdd(reinterpret_cast<unsigned long long *>(&c.sc->misses), (unsigned long long)misses);
+    if (born) atomicAdd(reinterpret_cast<unsigned long long *>(&c.sc->sketch_live), (unsigned long long)born);
+    if (hits) atomicAdd(reinterpret_cast<unsigned long long *>(&v.ss->b_hits), (unsigned long long)hits);
+    if (misses) atomicAdd(reinterpret_cast<unsigned long long *>(&v.ss->b_misses), (unsigned long long)misses);
+  }
+}
+
+__global__ void ks_after_probe(CacheView c, StepView v, int64_t nnz) {
+  if (aborted(v)) return;
+  v.ss->tick0 = c.sc->tick;
+  c.sc->tick += nnz;  // one tick per probed occurrence (cache.py:193)
+}
+
+// ---------------------------------------------------------------- 4. plan + counters
+// warp per bag: misses m; threshold t > 0 and m >= t -> one pushdown group,
+// else the misses are raw rows (and raw occurrences feed the offers)
+__global__ void __launch_bounds__(256) ks_bag_plan(StepView v, const int64_t *__restrict__ offsets,
+                                                   const int64_t *__restrict__ sm_start, int64_t n_bags,
+                                                   int32_t threshold, int32_t *hits_bag, int32_t *pd_groups,
+                                                   int32_t *pd_rows, int32_t *raw_rows) {
+  if (aborted(v)) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  long long groups = 0, pdg = 0, pdr = 0, raw = 0;
+  for (int64_t b = warp; b < n_bags; b += nw) {
+    const int64_t beg = __ldg(&offsets[b]), end = __ldg(&offsets[b + 1]);
+    int m = 0;
+    for (int64_t p = beg + lane; p < end; p += 32) m += v.dent[v.inv[p]].hit < 0 ? 1 : 0;
+    for (int o = 16; o; o >>= 1) m += __shfl_xor_sync(0xffffffffu, m, o);
+    const int L = static_cast<int>(end - beg);
+    const bool push = threshold > 0 && m >= threshold;
+    if (lane == 0) {
+      if (hits_bag) hits_bag[b] = L - m;
+      if (pd_groups) pd_groups[b] = (push && m > 0) ? 1 : 0;
+      if (pd_rows) pd_rows[b] = push ? m : 0;
+      if (raw_rows) raw_rows[b] = push ? 0 : m;
+      groups += m > 0 ? 1 : 0;
+      pdg += (push && m > 0) ? 1 : 0;
+      pdr += push ? m : 0;
+      raw += push ? 0 : m;
+    }
+    if (threshold > 0 && !push && m > 0) {
+      const int64_t sm = __ldg(&sm_start[b]);
+      for (int64_t p = beg + lane; p < end; p += 32) {
+        const int32_t u = v.inv[p];
+        if (v.dent[u].hit < 0) atomicMin(&v.dfraw[u], static_cast<int32_t>(sm + (p - beg)));
+      }
+    }
+  }
+  if (lane == 0) {
+    if (groups) atomicAdd(reinterpret_cast<unsigned long long *>(&v.ss->b_groups), (unsigned long long)groups);
+    if (pdg) atomicAdd(reinterpret_cast<unsigned long long *>(&v.ss->b_pd_groups), (unsigned long long)pdg);
+    if (pdr) atomicAdd(reinterpret_cast<unsigned long long *>(&v.ss->b_pd_rows), (unsigned long long)pdr);
+    if (raw) atomicAdd(reinterpret_cast<unsigned long long *>(&v.ss->b_raw_rows), (unsigned long long)raw);
+  }
+}
+
+__global__ void ks_cand_scatter_raw(StepView v) {
+  if (aborted(v)) return;
+  const long long n = v.ss->n_uniq;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t u = v.uniq[i];
+    const int32_t f = v.dfraw[u];
+    if (f != INT_MAX) v.cand_by_first[f] = u;
+  }
+}
+
+// ---------------------------------------------------------------- 5. offers
+struct NonNeg {
+  __host__ __device__ __forceinline__ bool operator()(const int32_t &x) const { return x >= 0; }
+};
+
+struct QueueKeep {
+  const int32_t *sflag;
+  const long long *epoch;
+  __device__ __forceinline__ bool operator()(const int32_t &s) const {
+    return s >= 0 && static_cast<long long>(sflag[s]) != *epoch;
+  }
+};
+
+__global__ void ks_cand_keys(StepView v) {
+  if (aborted(v)) return;
+  const long long n = v.ss->n_cand;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+    v.ckey[j] = v.dkey[v.cand[j]];
+}
+
+// offer time: a candidate installed since the probes (apply_pending of a
+// later batch when several are in flight) is present -> offer() returns True
+// with no side effect (cache.py:245-246); the rest keep their order
+__global__ void ks_offer_prep(CacheView c, StepView v, int64_t max_nnz) {
+  const bool on = !aborted(v);
+  const long long n = on ? v.ss->n_cand : 0;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < max_nnz; j += (int64_t)gridDim.x * blockDim.x) {
+    int32_t f = 0;
+    if (j < n) {
+      const uint64_t key = v.ckey[j];
+      f = h_find(c, key) < 0 ? 1 : 0;
+      if (f) v.estv[j] = k_est(c, key);
+    }
+    v.pres[j] = f;
+  }
+}
+
+// candidate estimates in offer order, their minimum and per-block maxima
+__global__ void __launch_bounds__(kFine) ks_cand_est(StepView v) {
+  if (aborted(v)) return;
+  const long long n = v.ss->n_off;
+  __shared__ double red[kFine / 32];
+  for (int64_t b = blockIdx.x; b * kFine < n; b += gridDim.x) {
+    const int64_t j = b * kFine + threadIdx.x;
+    double x = 0.0, mn = 1e300;
+    if (j < n) {
+      const int32_t i = v.cidx[j];
+      x = v.estv[i];
+      v.cC[j] = x;
+      v.okey[j] = v.ckey[i];
+      mn = x;
+    }
+    double mx = x;
+    for (int o = 16; o; o >>= 1) {
+      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    }
+    if ((threadIdx.x & 31) == 0 && mn < 1e300)
+      atomicMin(reinterpret_cast<long long *>(&v.ss->minc_bits), __double_as_longlong(mn));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double m2 = red[0];
+      for (int w = 1; w < kFine / 32; ++w) m2 = fmax(m2, red[w]);
+      v.bmax[b] = m2;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void ks_queue_append_hits(StepView v) {
+  if (aborted(v)) return;
+  const long long nh = v.ss->n_hitu, base = v.ss->n_nonhit;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nh; i += (int64_t)gridDim.x * blockDim.x)
+    v.qnew[base + i] = v.hits_ord[i];
+}
+
+// decisions' domain: F free units, parallel (accepts <= entries) or sequential
+__global__ void ks_offer_plan(CacheView c, StepView v) {
+  if (aborted(v)) return;
+  StepScalars *s = v.ss;
+  const Scalars *sc = c.sc;
+  const long long e0 = sc->entries;  // q[0, e0) = the entries in LRU order
+  s->e0 = e0;
+  const long long n = s->n_off, S = v.S, budget = sc->budget;
+  s->ftop0 = sc->free_top;
+  s->log0 = sc->n_evlog;
+  s->tick_base = sc->tick;  // each insert takes the next tick (cache.py:262)
+  if (n == 0) { s->mode = MODE_NONE; return; }
+  if (S > budget) { s->mode = MODE_NONE; s->F = 0; return; }  // size > budget: every offer -> False
+  const long long cap = budget / S;
+  const long long F = cap > e0 ? (cap - e0 < n ? cap - e0 : n) : 0;
+  s->F = F;
+  s->mode = (e0 <= cap && n - F <= e0) ? MODE_PAR : MODE_SEQ;
+}
+
+// victim estimates for V[0, n - F) and hard flags (est > minC)
+__global__ void ks_victim_est(CacheView c, StepView v, int64_t scap) {
+  if (aborted(v)) return;
+  const StepScalars *s = v.ss;
+  const bool on = s->mode == MODE_PAR && c.admission == 0;
+  const long long need = on ? s->n_off - s->F : 0;
+  const double minc = __longlong_as_double(s->minc_bits);
+  for (int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; h < scap; h += (int64_t)gridDim.x * blockDim.x) {
+    int32_t f = 0;
+    if (h < need) {
+      const double e = k_est(c, c.skey[v.q[h]]);
+      v.E[h] = e;
+      f = e > minc ? 1 : 0;
+    }
+    v.hardf[h] = f;
+  }
+}
+
+// first j in [x, n) with cC[j] >= e (n if none); whole warp, uniform result
+__device__ __forceinline__ long long next_ge(const StepView &v, const double *sbm, long long nblk, long long n,
+                                             long long x, double e, int lane) {
+  // fine probe of [x, x + kFine): 8 coalesced loads per lane, issued first
+  double f[kFine / 32];
+#pragma unroll
+  for (int i = 0; i < kFine / 32; ++i) {
+    const long long j = x + i * 32 + lane;
+    f[i] = j < n ? v.cC[j] : -1.0;
+  }
+  // meanwhile: first block at or after blk(x + kFine) whose max reaches e
+  long long B = nblk;
+  for (long long b0 = (x + kFine) / kFine; b0 < nblk; b0 += 32) {
+    const long long b = b0 + lane;
+    const unsigned m = __ballot_sync(0xffffffffu, b < nblk && sbm[b] >= e);
+    if (m) { B = b0 + __ffs(m) - 1; break; }
+  }
+#pragma unroll
+  for (int i = 0; i < kFine / 32; ++i) {
+    const unsigned m = __ballot_sync(0xffffffffu, f[i] >= e);
+    if (m) return x + i * 32 + __ffs(m) - 1;
+  }
+  if (B >= nblk) return n;
+  const long long lo = B * kFine > x + kFine ? B * kFine : x + kFine;
+#pragma unroll
+  for (int i = 0; i < kFine / 32; ++i) {
+    const long long j = lo + i * 32 + lane;
+    f[i] = (j < n && j < (B + 1) * kFine) ? v.cC[j] : -1.0;
+  }
+#pragma unroll
+  for (int i = 0; i < kFine / 32; ++i) {
+    const unsigned m = __ballot_sync(0xffffffffu, f[i] >= e);
+    if (m) return lo + i * 32 + __ffs(m) - 1;
+  }
+  return n;  // not reached: bmax[B] >= e
+}
+
+// The decision chain over hard victims (one block; warp 0 walks, the block
+// first stages the per-block maxima in shared memory).
+__global__ void __launch_bounds__(1024) ks_chain(StepView v) {
+  extern __shared__ double sbm[];
+  if (aborted(v) || v.ss->mode != MODE_PAR) return;
+  const long long n = v.ss->n_off, F = v.ss->F, nh = v.ss->n_hard;
+  const long long nblk = (n + kFine - 1) / kFine;
+  for (long long b = threadIdx.x; b < nblk; b += blockDim.x) sbm[b] = v.bmax[b];
+  __syncthreads();
+  if (threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
+  long long x = F, h = 0, nrej = 0;
+  for (long long k0 = 0; k0 < nh; k0 += 32) {
+    const long long kk = k0 + lane;
+    const int32_t hp = kk < nh ? v.hard[kk] : 0;
+    const double he = kk < nh ? v.E[hp] : 0.0;
+    const int cnt = nh - k0 < 32 ? static_cast<int>(nh - k0) : 32;
+    bool stop = false;
+    for (int t = 0; t < cnt; ++t) {
+      const long long b = __shfl_sync(0xffffffffu, hp, t);
+      const double e = __shfl_sync(0xffffffffu, he, t);
+      const long long gap = b - h;
+      if (x + gap >= n) { x = n; stop = true; break; }  // candidates run out in an easy stretch
+      x += gap;
+      h = b;
+      const long long j = next_ge(v, sbm, nblk, n, x, e, lane);
+      if (j > x) {
+        if (lane == 0) {
+          v.rj_beg[nrej] = static_cast<int32_t>(x);
+          v.rj_end[nrej] = static_cast<int32_t>(j);
+        }
+        ++nrej;
+      }
+      if (j >= n) { x = n; stop = true; break; }
+      x = j + 1;
+      h = b + 1;
+    }
+    if (stop) break;
+  }
+  if (lane == 0) v.ss->n_rej = nrej;
+}
+
+// accept flag per candidate (0 inside a reject interval)
+__global__ void ks_accept_flags(StepView v, int64_t max_nnz) {
+  if (aborted(v)) return;
+  const long long n = v.ss->n_off, nr = v.ss->n_rej, mode = v.ss->mode;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < max_nnz; j += (int64_t)gridDim.x * blockDim.x) {
+    int32_t a = 0;
+    if (j < n && mode == MODE_PAR) {
+      // last interval with beg <= j
+      long long lo = 0, hi = nr;
+      while (lo < hi) {
+        const long long mid = (lo + hi) >> 1;
+        if (v.rj_beg[mid] <= j) lo = mid + 1; else hi = mid;
+      }
+      a = (lo > 0 && j < v.rj_end[lo - 1]) ? 0 : 1;
+    }
+    v.acc[j] = a;
+  }
+}
+
+// side effects of the accepts, warp per candidate: accept rank r takes a free
+// slot (r < F) or evicts V[r - F] and takes its slot; tick tick_base + r + 1
+__global__ void __launch_bounds__(256) ks_apply(CacheView c, StepView v) {
+  if (aborted(v) || v.ss->mode != MODE_PAR) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const long long n = v.ss->n_off, F = v.ss->F, e0 = v.ss->e0, ftop0 = v.ss->ftop0, log0 = v.ss->log0;
+  const long long tick_base = v.ss->tick_base;
+  // n_ev = accepts beyond the free units (a prefix of V)
+  const long long n_acc = n > 0 ? v.rank[n - 1] + v.acc[n - 1] : 0;
+  const long long n_ev = n_acc > F ? n_acc - F : 0;
+  long long tombs = 0;
+  for (int64_t j = warp; j < n; j += nw) {
+    if (!v.acc[j]) continue;
+    const long long r = v.rank[j];
+    const uint64_t key = v.okey[j];
+    int32_t slot;
+    if (r < F) {
+      slot = c.free_stack[ftop0 - 1 - r];
+    } else {
+      const long long q = r - F;
+      slot = v.q[q];
+      if (lane == 0) {
+        const uint64_t ok = c.skey[slot];
+        if (c.evlog_cap > 0 && log0 + q < c.evlog_cap) c.evlog[log0 + q] = ok;
+        tombs += h_erase(c, ok) ? 1 : 0;
+      }
+    }
+    if (lane == 0) {
+      c.skey[slot] = key;
+      c.skey2[slot] = 0;
+      c.stick[slot] = tick_base + r + 1;
+      c.ssize[slot] = v.S;
+      c.shits[slot] = 0;
+      h_insert(c, key, slot);
+      v.qnew[e0 - n_ev + r] = slot;
+    }
+    warp_copy_row(c.rows + static_cast<int64_t>(slot) * c.row_ld, row_src(v, key), v.dim, lane);
+  }
+  if (lane == 0 && tombs) atomicAdd(reinterpret_cast<unsigned long long *>(&c.sc->hash_tomb), (unsigned long long)tombs);
+}
+
+// surviving victims move to the queue front: qnew[i] = q[n_ev + i]
+__global__ void ks_queue_survivors(CacheView c, StepView v) {
+  if (aborted(v)) return;
+  const StepScalars *s = v.ss;
+  if (s->mode == MODE_SEQ) return;  // ks_seq_offer wrote qnew
+  long long n_ev = 0;
+  if (s->mode == MODE_PAR) {
+    const long long n = s->n_off;
+    const long long n_acc = n > 0 ? v.rank[n - 1] + v.acc[n - 1] : 0;
+    n_ev = n_acc > s->F ? n_acc - s->F : 0;
+  }
+  const long long keep = s->e0 - n_ev;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < keep; i += (int64_t)gridDim.x * blockDim.x)
+    v.qnew[i] = v.q[n_ev + i];
+}
+
+__global__ void ks_queue_commit(StepView v, int64_t scap) {
+  if (aborted(v)) return;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < scap; i += (int64_t)gridDim.x * blockDim.x)
+    v.q[i] = v.qnew[i];
+}
+
+__global__ void ks_offer_finish(CacheView c, StepView v) {
+  if (aborted(v)) return;
+  StepScalars *s = v.ss;
+  Scalars *sc = c.sc;
+  if (s->mode == MODE_PAR) {
+    const long long n = s->n_off;
+    const long long n_acc = n > 0 ? v.rank[n - 1] + v.acc[n - 1] : 0;
+    const long long n_ev = n_acc > s->F ? n_acc - s->F : 0;
+    const long long fr = n_acc < s->F ? n_acc : s->F;
+    s->n_acc = n_acc;
+    s->n_ev = n_ev;
+    sc->entries = s->e0 + fr;
+    sc->used = sc->entries * v.S;
+    sc->tick = s->tick_base + n_acc;
+    sc->free_top = s->ftop0 - fr;
+    if (c.evlog_cap > 0) sc->n_evlog = s->log0 + n_ev;
+    sc->n_acc = n_acc;
+    sc->n_ev = n_ev;
+    s->qlen_new = sc->entries;
+  } else if (s->mode == MODE_NONE) {
+    s->qlen_new = s->e0;
+  }
+  // keep the cache index below half tombstones (rebuilt by the next two kernels)
+  s->rebuild_index = ((sc->hash_tomb + sc->entries) * 2 > c.hcap) ? 1 : 0;
+}
+
+// Exact sequential offers for batches outside the parallel domain
+// (cache.py:237-268; V grows by this call's own accepts, or the cache is
+// above budget). Single thread; rows are copied by ks_seq_rows.
+__global__ void ks_seq_offer(CacheView c, StepView v) {
+  if (aborted(v) || v.ss->mode != MODE_SEQ || threadIdx.x != 0 || blockIdx.x != 0) return;
+  StepScalars *s = v.ss;
+  Scalars *sc = c.sc;
+  const long long n = s->n_off, e0 = s->e0, S = v.S, budget = sc->budget;
+  long long e = e0, h = 0, n_acc = 0, ftop = sc->free_top, tick = s->tick_base, nlog = sc->n_evlog, tombs = 0;
+  const bool sketch = c.admission == 0;
+  auto vslot = [&](long long q) -> int32_t { return q < e0 ? v.q[q] : v.accslot[q - e0]; };
+  for (long long j = 0; j < n; ++j) {
+    const double cj = v.cC[j];
+    if ((e + 1) * S > budget) {
+      if (sketch && e > 0) {
+        const int32_t vs = vslot(h);
+        const double ve = h < e0 ? k_est(c, c.skey[vs]) : v.cC[v.accj[h - e0]];
+        if (cj < ve) continue;
+      }
+      while ((e + 1) * S > budget && e > 0) {
+        const int32_t vs = vslot(h);
+        ++h;
+        const uint64_t ok = c.skey[vs];
+        if (c.evlog_cap > 0 && nlog < c.evlog_cap) c.evlog[nlog] = ok;
+        if (c.evlog_cap > 0) ++nlog;
+        tombs += h_erase(c, ok) ? 1 : 0;
+        c.stick[vs] = kFree;
+        c.skey[vs] = kEmpty;
+        c.free_stack[ftop++] = vs;
+        --e;
+      }
+      if ((e + 1) * S > budget) continue;  // cannot fit (budget < S handled by the plan)
+    }
+    const uint64_t key = v.okey[j];
+    const int32_t slot = c.free_stack[--ftop];
+    ++tick;
+    c.skey[slot] = key;
+    c.skey2[slot] = 0;
+    c.stick[slot] = tick;
+    c.ssize[slot] = static_cast<int32_t>(S);
+    c.shits[slot] = 0;
+    h_insert(c, key, slot);
+    v.accslot[n_acc] = slot;
+    v.accj[n_acc] = static_cast<int32_t>(j);
+    ++n_acc;
+    ++e;
+  }
+  // queue: V[h, e0 + n_acc) still resident, in order
+  long long w = 0;
+  for (long long q = h; q < e0 + n_acc; ++q) v.qnew[w++] = vslot(q);
+  sc->entries = e;
+  sc->used = e * S;
+  sc->tick = tick;
+  sc->free_top = ftop;
+  sc->n_evlog = nlog;
+  sc->hash_tomb += tombs;
+  sc->n_acc = n_acc;
+  s->n_acc = n_acc;
+  s->n_ev = h;
+  s->qlen_new = e;
+}
+
+__global__ void __launch_bounds__(256) ks_seq_rows(CacheView c, StepView v) {
+  if (aborted(v) || v.ss->mode != MODE_SEQ) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const long long na = v.ss->n_acc;
+  for (int64_t a = warp; a < na; a += nw) {
+    const int32_t slot = v.accslot[a];
+    const uint64_t key = v.okey[v.accj[a]];
+    if (c.skey[slot] != key || c.stick[slot] == kFree) continue;  // evicted again in the same call
+    warp_copy_row(c.rows + static_cast<int64_t>(slot) * c.row_ld, row_src(v, key), v.dim, lane);
+  }
+}
+
+__global__ void ks_index_clear(CacheView c, StepView v) {
+  if (!v.ss->rebuild_index) return;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < c.hcap; i += (int64_t)gridDim.x * blockDim.x)
+    c.hkeys[i] = kEmpty;
+}
+
+__global__ void ks_index_fill(CacheView c, StepView v) {
+  if (!v.ss->rebuild_index) return;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < c.scap; i += (int64_t)gridDim.x * blockDim.x)
+    if (c.stick[i] != kFree) h_insert(c, c.skey[i], static_cast<int32_t>(i));
+  if (blockIdx.x == 0 && threadIdx.x == 0) c.sc->hash_tomb = 0;
+}
+
+// reset the dedup slots this batch claimed (lazy clear: O(unique keys))
+__global__ void ks_dedup_reset(StepView v) {
+  const long long n = v.ss->n_uniq;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t u = v.uniq[i];
+    v.dkey[u] = kEmpty;
+    v.dent[u] = DEnt{0, INT_MAX, -1, -1};
+    v.dfraw[u] = INT_MAX;
+  }
+}
+
+// ---------------------------------------------------------------- 6. stage(limit)
+// stage_hot_admissions(limit) (cache.py:311-342): hottest(limit) ranks every
+// sketch key by (-count, key) and takes the top `limit`; cached / pending
+// keys and keys larger than the spare room are skipped. Exact top-k by a
+// radix select over the 128-bit key (~bits(count), key) with 16-bit digits;
+// every kernel is a no-op unless room > 0.
+__device__ __forceinline__ uint64_t vinv_of(double x) {
+  return static_cast<uint64_t>(~__double_as_longlong(x) & LLONG_MAX);  // ascending = descending count
+}
+
+__global__ void ks_stage_begin(CacheView c, StepView v, int64_t limit) {
+  StepScalars *s = v.ss;
+  const Scalars *sc = c.sc;
+  s->stage_on = (s->err == 0 && limit > 0 && sc->budget - sc->used > 0 && sc->sketch_live > 0) ? 1 : 0;
+  s->topk_live = 0;
+  s->topk_krem = limit;
+  s->topk_hi = s->topk_lo = 0;
+  s->topk_digit = 0;
+  s->topk_n = 0;
+}
+
+__global__ void ks_topk_collect(CacheView c, StepView v) {
+  if (!v.ss->stage_on) return;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < c.kcap; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = c.kkeys[i];
+    const bool live = k != kEmpty && k != kTomb;
+    const long long p = warp_append(reinterpret_cast<unsigned long long *>(&v.ss->topk_live), live);
+    if (live) {
+      v.tk_key[p] = k;
+      v.tk_vinv[p] = vinv_of(c.kval[i]);
+    }
+  }
+}
+
+// digit d (0..7): d < 4 from vinv (most significant first), then from key
+__device__ __forceinline__ uint32_t digit_of(uint64_t hi, uint64_t lo, int d) {
+  return d < 4 ? static_cast<uint32_t>((hi >> (48 - 16 * d)) & 0xffff)
+               : static_cast<uint32_t>((lo >> (48 - 16 * (d - 4))) & 0xffff);
+}
+
+__device__ __forceinline__ bool prefix_match(uint64_t hi, uint64_t lo, uint64_t phi, uint64_t plo, int d) {
+  // digits [0, d) equal
+  if (d == 0) return true;
+  if (d <= 4) {
+    const int sh = 64 - 16 * d;
+    return (hi >> sh) == (phi >> sh);
+  }
+  if (hi != phi) return false;
+  const int sh = 64 - 16 * (d - 4);
+  return sh >= 64 ? true : (lo >> sh) == (plo >> sh);
+}
+
+__global__ void ks_topk_hist(StepView v, int d) {
+  if (!v.ss->stage_on || v.ss->topk_digit == 8) return;
+  const long long n = v.ss->topk_live;
+  const uint64_t phi = v.ss->topk_hi, plo = v.ss->topk_lo;
+  const int lane = threadIdx.x & 31;
+  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); i0 < n;
+       i0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = i0 + lane;
+    int bin = -1;
+    if (i < n) {
+      const uint64_t hi = v.tk_vinv[i], lo = v.tk_key[i];
+      if (prefix_match(hi, lo, phi, plo, d)) bin = static_cast<int>(digit_of(hi, lo, d));
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, bin);
+    if (bin >= 0 && lane == __ffs(peers) - 1) atomicAdd(&v.tk_hist[bin], __popc(peers));
+  }
+}
+
+// one block: the digit holding the k-th remaining key; keys below it are in
+__global__ void __launch_bounds__(1024) ks_topk_select(StepView v, int d) {
+  if (!v.ss->stage_on || v.ss->topk_digit == 8) return;
+  __shared__ long long part[1024];
+  const int per = kTopkBins / 1024;
+  long long sum = 0;
+  for (int i = 0; i < per; ++i) sum += v.tk_hist[threadIdx.x * per + i];
+  part[threadIdx.x] = sum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long k = v.ss->topk_krem;
+    long long cum = 0;
+    int g = kTopkBins - 1;
+    bool found = false;
+    for (int t = 0; t < 1024 && !found; ++t) {
+      if (cum + part[t] < k) { cum += part[t]; continue; }
+      for (int i = 0; i < per; ++i) {
+        const long long hc = v.tk_hist[t * per + i];
+        if (cum + hc >= k) { g = t * per + i; found = true; break; }
+        cum += hc;
+      }
+    }
+    if (!found) {  // fewer than k keys in total: take everything (prefix = max)
+      v.ss->topk_hi = ~0ull;
+      v.ss->topk_lo = ~0ull;
+      v.ss->topk_digit = 8;
+    } else {
+      v.ss->topk_krem = k - cum;
+      if (d < 4) v.ss->topk_hi |= static_cast<uint64_t>(g) << (48 - 16 * d);
+      else v.ss->topk_lo |= static_cast<uint64_t>(g) << (48 - 16 * (d - 4));
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kTopkBins; i += blockDim.x) v.tk_hist[i] = 0;
+}
+
+// the (vinv, key) <= threshold entries: exactly min(limit, live) of them
+__global__ void ks_topk_gather(StepView v) {
+  if (!v.ss->stage_on) return;
+  const long long n = v.ss->topk_live;
+  const uint64_t thi = v.ss->topk_hi, tlo = v.ss->topk_lo;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t hi = v.tk_vinv[i], lo = v.tk_key[i];
+    const bool in = hi < thi || (hi == thi && lo <= tlo);
+    const long long p = warp_append(reinterpret_cast<unsigned long long *>(&v.ss->topk_n), in);
+    if (in) v.tk_sel[p] = static_cast<int32_t>(i);
+  }
+}
+
+// rank the <= limit selected keys, then the ordered staging loop (one block)
+__global__ void __launch_bounds__(1024) ks_stage_finish(CacheView c, StepView v, int64_t limit) {
+  if (!v.ss->stage_on) return;
+  extern __shared__ unsigned char smem_raw[];
+  const long long m = v.ss->topk_n;
+  uint64_t *hi = reinterpret_cast<uint64_t *>(smem_raw);
+  uint64_t *lo = hi + limit;
+  int32_t *ord = reinterpret_cast<int32_t *>(lo + limit);
+  for (long long i = threadIdx.x; i < m; i += blockDim.x) {
+    const int32_t p = v.tk_sel[i];
+    hi[i] = v.tk_vinv[p];
+    lo[i] = v.tk_key[p];
+  }
+  __syncthreads();
+  // rank by counting (keys are distinct)
+  for (long long i = threadIdx.x; i < m; i += blockDim.x) {
+    long long r = 0;
+    for (long long j = 0; j < m; ++j) r += (hi[j] < hi[i] || (hi[j] == hi[i] && lo[j] < lo[i])) ? 1 : 0;
+    ord[r] = static_cast<int32_t>(i);
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  Scalars *sc = c.sc;
+  long long room = sc->budget - sc->used;
+  long long staged = 0, pend = sc->pending;
+  for (long long r = 0; r < m; ++r) {
+    const uint64_t key = lo[ord[r]];
+    const int64_t kp = k_find(c, key);
+    if (kp < 0 || c.kflag[kp] || h_find(c, key) >= 0) continue;
+    const long long size = v.S;
+    if (size > room) continue;
+    if (pend >= c.pend_cap) break;
+    c.pend[pend++] = key;
+    c.kflag[kp] = 1;
+    room -= size;
+    ++staged;
+    if (staged >= limit) break;
+  }
+  sc->pending = pend;
+  sc->staged = staged;
+}
+
+// sketch age (cache.py:128-136): halve, prune below prune_below
+__global__ void ks_age(CacheView c, StepView v) {
+  if (v.ss->err) return;
+  long long dead = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < c.kcap; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = c.kkeys[i];
+    if (k == kEmpty || k == kTomb) continue;
+    const double x = c.kval[i] * c.decay;
+    if (x < c.prune) {
+      c.kkeys[i] = kTomb;
+      c.kval[i] = 0.0;
+      c.kflag[i] = 0;
+      ++dead;
+    } else {
+      c.kval[i] = x;
+    }
+  }
+  dead = warp_sum(dead);
+  if ((threadIdx.x & 31) == 0 && dead) {
+    atomicAdd(reinterpret_cast<unsigned long long *>(&c.sc->sketch_live), (unsigned long long)(-dead));
+    atomicAdd(reinterpret_cast<unsigned long long *>(&c.sc->sketch_tomb), (unsigned long long)dead);
+  }
+}
+
+}  // namespace stp
+}  // namespace fx
+
+using namespace fx;
+using namespace fx::stp;
+
+struct fx_step {
+  fx_cache *cache = nullptr;
+  StepView v{};
+  StepScalars *ss_base = nullptr;  // [slots + 1]: per in-flight batch, then the global block
+  uint64_t *ckey_base = nullptr;   // [slots * max_nnz]
+  int32_t slots = 1;
+  int64_t max_nnz = 0, max_bags = 0;
+  int64_t scap = 0;
+  void *cub_tmp = nullptr;
+  size_t cub_bytes = 0;
+  std::vector<void *> allocs;
+  int chain_smem = 0;
+  int stage_smem = 0;
+  int64_t stage_limit_cap = 0;
+};
+
+namespace {
+
+template <typename T>
+int salloc(fx_step *s, T **p, size_t n) {
+  *p = nullptr;
+  if (n == 0) n = 1;
+  cudaError_t e = cudaMalloc(reinterpret_cast<void **>(p), n * sizeof(T));
+  if (e != cudaSuccess) return cuda_check(e, "fx_step: cudaMalloc");
+  s->allocs.push_back(*p);
+  return FX_OK;
+}
+
+int64_t pow2_ge(int64_t x) {
+  int64_t p = 1024;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+__global__ void k_init_dedup(StepView v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < v.dcap; i += (int64_t)gridDim.x * blockDim.x) {
+    v.dkey[i] = kEmpty;
+    v.dent[i] = DEnt{0, INT_MAX, -1, -1};
+    v.dfraw[i] = INT_MAX;
+  }
+}
+
+__global__ void k_lru_sortkeys(CacheView c, long long *keys, int32_t *vals, long long free_key) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < c.scap; i += (int64_t)gridDim.x * blockDim.x) {
+    const long long t = c.stick[i];
+    keys[i] = t == kFree ? free_key : t;
+    vals[i] = static_cast<int32_t>(i);
+  }
+}
+
+__global__ void k_queue_from_sorted(CacheView c, const int32_t *sorted, int32_t *q, int64_t scap) {
+  const long long e = c.sc->entries;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < scap; i += (int64_t)gridDim.x * blockDim.x)
+    q[i] = i < e ? sorted[i] : -1;
+}
+
+int ensure_queue(fx_step *s, cudaStream_t st) {
+  fx_cache *c = s->cache;
+  const int64_t scap = c->v.scap;
+  if (scap != s->scap) {
+    set_error("fx_step: the cache's slot capacity changed; recreate the step");
+    return FX_E_CONFIG;
+  }
+  if (c->q_cap < scap) {
+    if (c->q) cudaFree(c->q);
+    c->q = nullptr;
+    int rc = cuda_check(cudaMalloc(&c->q, scap * sizeof(int32_t)), "fx_step: queue");
+    if (rc) return rc;
+    c->q_cap = scap;
+    c->queue_valid = 0;
+  }
+  s->v.q = c->q;
+  if (c->queue_valid) return FX_OK;
+  // rebuild: occupied slots by ascending tick (free slots sort last)
+  long long *k0 = reinterpret_cast<long long *>(s->v.E);  // scratch: scap doubles
+  long long *k1 = reinterpret_cast<long long *>(s->v.tk_vinv);
+  int32_t *v0 = s->v.hardf, *v1 = s->v.hard;
+  k_lru_sortkeys<<<grid_for(scap, 256), 256, 0, st>>>(c->v, k0, v0, LLONG_MAX);
+  size_t need = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, need, k0, k1, v0, v1, static_cast<int>(scap), 0, 64, st);
+  void *tmp = nullptr;
+  int rc = cuda_check(cudaMallocAsync(&tmp, need, st), "fx_step: sort tmp");
+  if (rc) return rc;
+  cub::DeviceRadixSort::SortPairs(tmp, need, k0, k1, v0, v1, static_cast<int>(scap), 0, 64, st);
+  k_queue_from_sorted<<<grid_for(scap, 256), 256, 0, st>>>(c->v, v1, c->q, scap);
+  cudaFreeAsync(tmp, st);
+  FX_LAUNCH_CHECK("fx_step: queue rebuild");
+  c->queue_valid = 1;
+  return FX_OK;
+}
+
+int select_slot(fx_step *s, int32_t slot, StepView *v) {
+  if (slot < 0 || slot >= s->slots) {
+    set_error("fx_step: slot out of range");
+    return FX_E_CONFIG;
+  }
+  *v = s->v;
+  v->ss = s->ss_base + slot;
+  v->gs = s->ss_base + s->slots;
+  v->ckey = s->ckey_base + static_cast<int64_t>(slot) * s->max_nnz;
+  v->q = s->cache->q;
+  return FX_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int fx_step_create(fx_step **out, fx_cache *cache, int64_t max_nnz, int64_t max_bags, const float *const *table_base,
+                   const int64_t *table_ld, const int64_t *table_rows, int32_t n_tables, int32_t dim,
+                   int64_t stage_limit_cap, int32_t slots) {
+  if (!out || !cache || max_nnz < 0 || max_bags < 0 || n_tables < 1 || dim < 1 || dim > cache->v.row_ld ||
+      slots < 1 || slots > 64) {
+    set_error("fx_step_create: bad arguments");
+    return FX_E_CONFIG;
+  }
+  if (max_nnz >= (1ll << 31) - 1) {
+    set_error("fx_step_create: max_nnz must be < 2^31 (int32 ordinals)");
+    return FX_E_CONFIG;
+  }
+  fx_step *s = new fx_step();
+  s->cache = cache;
+  s->slots = slots;
+  s->max_nnz = max_nnz > 0 ? max_nnz : 1;
+  s->max_bags = max_bags > 0 ? max_bags : 1;
+  s->scap = cache->v.scap;
+  StepView &v = s->v;
+  const int64_t N = s->max_nnz, SC = s->scap;
+  v.max_nnz = N;
+  v.dcap = pow2_ge(2 * N);
+  v.n_tables = n_tables;
+  v.dim = dim;
+  v.S = dim * 4;
+  v.tk_cap = cache->v.kcap > SC ? cache->v.kcap : SC;
+  int rc = FX_OK;
+  rc = rc ? rc : salloc(s, &s->ss_base, slots + 1);
+  rc = rc ? rc : salloc(s, &s->ckey_base, static_cast<size_t>(slots) * N);
+  rc = rc ? rc : salloc(s, &v.dkey, v.dcap);
+  rc = rc ? rc : salloc(s, &v.dent, v.dcap);
+  rc = rc ? rc : salloc(s, &v.dfraw, v.dcap);
+  rc = rc ? rc : salloc(s, &v.uniq, N);
+  rc = rc ? rc : salloc(s, &v.inv, N);
+  rc = rc ? rc : salloc(s, &v.cand_by_first, N);
+  rc = rc ? rc : salloc(s, &v.hit_by_last, N);
+  rc = rc ? rc : salloc(s, &v.cand, N);
+  rc = rc ? rc : salloc(s, &v.hits_ord, N);
+  rc = rc ? rc : salloc(s, &v.estv, N);
+  rc = rc ? rc : salloc(s, &v.pres, N);
+  rc = rc ? rc : salloc(s, &v.cidx, N);
+  rc = rc ? rc : salloc(s, &v.okey, N);
+  rc = rc ? rc : salloc(s, &v.cC, N);
+  rc = rc ? rc : salloc(s, &v.bmax, (N + kFine - 1) / kFine + 1);
+  rc = rc ? rc : salloc(s, &v.qnew, SC);
+  rc = rc ? rc : salloc(s, &v.sflag, SC);
+  rc = rc ? rc : salloc(s, &v.E, SC);
+  rc = rc ? rc : salloc(s, &v.hardf, SC);
+  rc = rc ? rc : salloc(s, &v.hard, SC);
+  rc = rc ? rc : salloc(s, &v.rj_beg, SC + 1);
+  rc = rc ? rc : salloc(s, &v.rj_end, SC + 1);
+  rc = rc ? rc : salloc(s, &v.acc, N);
+  rc = rc ? rc : salloc(s, &v.rank, N);
+  rc = rc ? rc : salloc(s, &v.accslot, N);
+  rc = rc ? rc : salloc(s, &v.accj, N);
+  rc = rc ? rc : salloc(s, &v.tk_key, v.tk_cap);
+  rc = rc ? rc : salloc(s, &v.tk_vinv, v.tk_cap);
+  rc = rc ? rc : salloc(s, &v.tk_val, v.tk_cap);
+  rc = rc ? rc : salloc(s, &v.tk_flag, v.tk_cap);
+  rc = rc ? rc : salloc(s, &v.tk_hist, kTopkBins);
+  rc = rc ? rc : salloc(s, &v.tk_sel, v.tk_cap);
+  float **tb = nullptr;
+  int64_t *tl = nullptr, *tr = nullptr;
+  rc = rc ? rc : salloc(s, &tb, n_tables);
+  rc = rc ? rc : salloc(s, &tl, n_tables);
+  rc = rc ? rc : salloc(s, &tr, n_tables);
+  if (rc) {
+    fx_step_destroy(s);
+    return rc;
+  }
+  cudaMemcpy(tb, table_base, n_tables * sizeof(float *), cudaMemcpyHostToDevice);
+  cudaMemcpy(tl, table_ld, n_tables * sizeof(int64_t), cudaMemcpyHostToDevice);
+  cudaMemcpy(tr, table_rows, n_tables * sizeof(int64_t), cudaMemcpyHostToDevice);
+  v.tbase = tb;
+  v.tld = tl;
+  v.trows = tr;
+  const int big = static_cast<int>(N > SC ? N : SC);
+  size_t b1 = 0, b2 = 0, b3 = 0, b4 = 0;
+  cub::DeviceSelect::If(nullptr, b1, (const int32_t *)nullptr, (int32_t *)nullptr, (int64_t *)nullptr, big, NonNeg());
+  cub::DeviceSelect::Flagged(nullptr, b2, cub::CountingInputIterator<int32_t>(0), (const int32_t *)nullptr,
+                             (int32_t *)nullptr, (int64_t *)nullptr, big);
+  cub::DeviceScan::ExclusiveSum(nullptr, b3, (const int32_t *)nullptr, (int32_t *)nullptr, static_cast<int>(N));
+  QueueKeep qk{nullptr, nullptr};
+  cub::DeviceSelect::If(nullptr, b4, (const int32_t *)nullptr, (int32_t *)nullptr, (int64_t *)nullptr,
+                        static_cast<int>(SC), qk);
+  s->cub_bytes = b1 > b2 ? b1 : b2;
+  if (b3 > s->cub_bytes) s->cub_bytes = b3;
+  if (b4 > s->cub_bytes) s->cub_bytes = b4;
+  rc = cuda_check(cudaMalloc(&s->cub_tmp, s->cub_bytes + 256), "fx_step: cub tmp");
+  if (rc) {
+    fx_step_destroy(s);
+    return rc;
+  }
+  s->allocs.push_back(s->cub_tmp);
+  cudaMemset(s->ss_base, 0, (slots + 1) * sizeof(StepScalars));
+  k_init_dedup<<<grid_for(v.dcap, 256), 256>>>(v);
+  cudaMemset(v.sflag, 0xff, SC * 4);  // no slot carries epoch -1
+  cudaMemset(v.tk_hist, 0, kTopkBins * 4);
+  const int64_t nblk = (N + kFine - 1) / kFine;
+  s->chain_smem = static_cast<int>(nblk * sizeof(double));
+  if (s->chain_smem > 227 * 1024) {
+    set_error("fx_step_create: max_nnz too large for the chain's shared-memory block maxima");
+    fx_step_destroy(s);
+    return FX_E_CONFIG;
+  }
+  cudaFuncSetAttribute(ks_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, s->chain_smem > 0 ? s->chain_smem : 8);
+  s->stage_limit_cap = stage_limit_cap > 0 ? stage_limit_cap : 64;
+  s->stage_smem = static_cast<int>(s->stage_limit_cap * (8 + 8 + 4));
+  cudaFuncSetAttribute(ks_stage_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, s->stage_smem);
+  rc = cuda_check(cudaDeviceSynchronize(), "fx_step_create");
+  if (rc) {
+    fx_step_destroy(s);
+    return rc;
+  }
+  *out = s;
+  return FX_OK;
+}
+
+int fx_step_destroy(fx_step *s) {
+  if (!s) return FX_OK;
+  for (void *p : s->allocs) cudaFree(p);
+  delete s;
+  return FX_OK;
+}
+
+int fx_step_prepare(fx_step *s, void *stream) { return ensure_queue(s, as_stream(stream)); }
+
+int fx_step_start(fx_step *s, int32_t slot, const int32_t *bag_table, const void *indices, int32_t idx_type,
+                  const int64_t *offsets, const int64_t *sm_start, int64_t n_bags, int64_t nnz, int32_t threshold,
+                  int32_t *hits_bag, int32_t *pd_groups, int32_t *pd_rows, int32_t *raw_rows, void *stream) {
+  cudaStream_t st = as_stream(stream);
+  if (nnz > s->max_nnz || n_bags > s->max_bags || nnz < 0 || n_bags < 0) {
+    set_error("fx_step_start: batch larger than the step's capacity");
+    return FX_E_CAPACITY;
+  }
+  int rc = ensure_queue(s, st);
+  if (rc) return rc;
+  StepView v;
+  rc = select_slot(s, slot, &v);
+  if (rc) return rc;
+  fx_cache *cc = s->cache;
+  CacheView &c = cc->v;
+  const int64_t SC = s->scap;
+  if (c.kcap > v.tk_cap) {
+    set_error("fx_step_start: sketch grew beyond the step's temporaries; recreate the step");
+    return FX_E_CONFIG;
+  }
+  ks_begin<<<1, 1, 0, st>>>(c, v, nnz);
+  ks_sketch_collect<<<grid_for(c.kcap, 256), 256, 0, st>>>(c, v);
+  ks_sketch_clear<<<grid_for(c.kcap, 256), 256, 0, st>>>(c, v);
+  ks_sketch_reinsert<<<grid_for(c.kcap, 256), 256, 0, st>>>(c, v);
+  // validation + dedup first: a bad index aborts the batch before any state change
+  if (n_bags > 0) {
+    const int g = grid_for((n_bags + 31) / 32 * 32, 256);
+    if (idx_type == FX_IDX_I32)
+      ks_dedup<int32_t><<<g, 256, 0, st>>>(v, bag_table, static_cast<const int32_t *>(indices), offsets, sm_start,
+                                          n_bags);
+    else
+      ks_dedup<int64_t><<<g, 256, 0, st>>>(v, bag_table, static_cast<const int64_t *>(indices), offsets, sm_start,
+                                          n_bags);
+  }
+  // ranker.py:218-222 order: validate, apply_pending, (admission check: host), probes
+  ks_apply_pending<<<1, 32, 0, st>>>(c, v);
+  const int nn = static_cast<int>(nnz > 0 ? nnz : 1);
+  cudaMemsetAsync(v.cand_by_first, 0xff, static_cast<size_t>(nn) * 4, st);
+  cudaMemsetAsync(v.hit_by_last, 0xff, static_cast<size_t>(nn) * 4, st);
+  ks_probe<<<grid_for(nn, 256), 256, 0, st>>>(c, v, threshold > 0 ? 1 : 0);
+  ks_after_probe<<<1, 1, 0, st>>>(c, v, nnz);
+  ks_bag_plan<<<grid_for(n_bags > 0 ? n_bags * 32 : 32, 256), 256, 0, st>>>(v, offsets, sm_start, n_bags, threshold,
+                                                                            hits_bag, pd_groups, pd_rows, raw_rows);
+  if (threshold > 0) ks_cand_scatter_raw<<<grid_for(nn, 256), 256, 0, st>>>(v);
+  size_t cb = s->cub_bytes;
+  // candidates in first raw-occurrence order; hit slots in last-ordinal order
+  cub::DeviceSelect::If(s->cub_tmp, cb, v.cand_by_first, v.cand, reinterpret_cast<int64_t *>(&v.ss->n_cand), nn,
+                        NonNeg(), st);
+  ks_cand_keys<<<grid_for(nn, 256), 256, 0, st>>>(v);
+  cub::DeviceSelect::If(s->cub_tmp, cb, v.hit_by_last, v.hits_ord, reinterpret_cast<int64_t *>(&v.ss->n_hitu), nn,
+                        NonNeg(), st);
+  // LRU order after the probes: [entries not hit, old order] ++ [hit entries by last ordinal]
+  cudaMemsetAsync(v.qnew, 0xff, SC * 4, st);
+  QueueKeep qk{v.sflag, &v.ss->epoch};
+  cub::DeviceSelect::If(s->cub_tmp, cb, cc->q, v.qnew, reinterpret_cast<int64_t *>(&v.ss->n_nonhit),
+                        static_cast<int>(SC), qk, st);
+  ks_queue_append_hits<<<grid_for(nn, 256), 256, 0, st>>>(v);
+  cudaMemcpyAsync(cc->q, v.qnew, SC * 4, cudaMemcpyDeviceToDevice, st);
+  ks_dedup_reset<<<grid_for(nn, 256), 256, 0, st>>>(v);
+  FX_LAUNCH_CHECK("fx_step_start");
+  return FX_OK;
+}
+
+int fx_step_offer(fx_step *s, int32_t slot, void *stream) {
+  cudaStream_t st = as_stream(stream);
+  int rc = ensure_queue(s, st);
+  if (rc) return rc;
+  StepView v;
+  rc = select_slot(s, slot, &v);
+  if (rc) return rc;
+  fx_cache *cc = s->cache;
+  CacheView &c = cc->v;
+  const int64_t SC = s->scap;
+  const int nn = static_cast<int>(s->max_nnz);
+  size_t cb = s->cub_bytes;
+  ks_offer_prep<<<grid_for(nn, 256), 256, 0, st>>>(c, v, nn);
+  cub::DeviceSelect::Flagged(s->cub_tmp, cb, cub::CountingInputIterator<int32_t>(0), v.pres, v.cidx,
+                             reinterpret_cast<int64_t *>(&v.ss->n_off), nn, st);
+  ks_cand_est<<<grid_for(nn, kFine), kFine, 0, st>>>(v);
+  ks_offer_plan<<<1, 1, 0, st>>>(c, v);
+  ks_victim_est<<<grid_for(SC, 256), 256, 0, st>>>(c, v, SC);
+  cub::DeviceSelect::Flagged(s->cub_tmp, cb, cub::CountingInputIterator<int32_t>(0), v.hardf, v.hard,
+                             reinterpret_cast<int64_t *>(&v.ss->n_hard), static_cast<int>(SC), st);
+  ks_chain<<<1, 1024, s->chain_smem, st>>>(v);
+  ks_accept_flags<<<grid_for(nn, 256), 256, 0, st>>>(v, nn);
+  cub::DeviceScan::ExclusiveSum(s->cub_tmp, cb, v.acc, v.rank, nn, st);
+  cudaMemsetAsync(v.qnew, 0xff, SC * 4, st);
+  ks_apply<<<grid_for(static_cast<int64_t>(nn) * 32, 256), 256, 0, st>>>(c, v);
+  ks_queue_survivors<<<grid_for(SC, 256), 256, 0, st>>>(c, v);
+  ks_seq_offer<<<1, 1, 0, st>>>(c, v);
+  ks_seq_rows<<<grid_for(static_cast<int64_t>(nn) * 32, 256), 256, 0, st>>>(c, v);
+  ks_offer_finish<<<1, 1, 0, st>>>(c, v);
+  ks_queue_commit<<<grid_for(SC, 256), 256, 0, st>>>(v, SC);
+  ks_index_clear<<<grid_for(c.hcap, 256), 256, 0, st>>>(c, v);
+  ks_index_fill<<<grid_for(SC, 256), 256, 0, st>>>(c, v);
+  FX_LAUNCH_CHECK("fx_step_offer");
+  return FX_OK;
+}
+
+int fx_step_maintain(fx_step *s, int32_t slot, int64_t stage_limit, int32_t do_age, void *stream) {
+  cudaStream_t st = as_stream(stream);
+  StepView v;
+  int rc = select_slot(s, slot, &v);
+  if (rc) return rc;
+  CacheView &c = s->cache->v;
+  if (stage_limit > s->stage_limit_cap) {
+    set_error("fx_step_maintain: stage limit above the step's cap");
+    return FX_E_CONFIG;
+  }
+  ks_stage_begin<<<1, 1, 0, st>>>(c, v, stage_limit);
+  if (stage_limit > 0) {
+    ks_topk_collect<<<grid_for(c.kcap, 256), 256, 0, st>>>(c, v);
+    for (int d = 0; d < 8; ++d) {
+      ks_topk_hist<<<grid_for(c.kcap, 256), 256, 0, st>>>(v, d);
+      ks_topk_select<<<1, 1024, 0, st>>>(v, d);
+    }
+    ks_topk_gather<<<grid_for(c.kcap, 256), 256, 0, st>>>(v);
+    ks_stage_finish<<<1, 1024, s->stage_smem, st>>>(c, v, stage_limit);
+  }
+  if (do_age) ks_age<<<grid_for(c.kcap, 256), 256, 0, st>>>(c, v);
+  FX_LAUNCH_CHECK("fx_step_maintain");
+  return FX_OK;
+}
+
+int fx_step_scalars(fx_step *s, int32_t slot, int64_t *out, int64_t n, void *stream) {
+  cudaStream_t st = as_stream(stream);
+  if (slot < 0 || slot > s->slots) {
+    set_error("fx_step_scalars: slot out of range");
+    return FX_E_CONFIG;
+  }
+  const int64_t cnt = static_cast<int64_t>(sizeof(StepScalars) / 8);
+  int rc = cuda_check(cudaMemcpyAsync(out, s->ss_base + slot, (n < cnt ? n : cnt) * 8, cudaMemcpyDeviceToHost, st),
+                      "fx_step_scalars");
+  if (rc) return rc;
+  return cuda_check(cudaStreamSynchronize(st), "fx_step_scalars sync");
+}
+
+const void *fx_step_scalars_device(fx_step *s, int32_t slot) {
+  return (slot >= 0 && slot <= s->slots) ? static_cast<const void *>(s->ss_base + slot) : nullptr;
+}
+
+}  // extern "C"

@@ -32,7 +32,7 @@ import torch
 
 from . import _lib
 from .cache import AdaptiveCache, CachePolicy, LoadTracker, encode_key, target_cache_bytes
-from .dedup import Deduper
+from .dedup import Deduper, sample_major_starts
 from .errors import CapacityError, ConfigError, InvariantError, LookupValidationError
 from .pooling import PoolingOp, op_code, pool_flat
 from .requests import Batch, LookupRequest
@@ -161,7 +161,7 @@ class Ranker:
     def __init__(self, deployment: Deployment, routing: RoutingTable, transport=None,
                  params: RankerParams | None = None, cache: AdaptiveCache | None = None,
                  policy: CachePolicy | None = None, tracker: LoadTracker | None = None, device=None,
-                 hits_from_cache: bool = True):
+                 hits_from_cache: bool = True, fused: bool = True):
         self.deployment = deployment
         self.routing = routing
         self.transport = transport
@@ -204,6 +204,17 @@ class Ranker:
         self.profile = False
         self.stage_ms: dict = {}
         self._marks = []
+        # fused, sync-free batch step (csrc/fx_step.cu) when the deployment is
+        # in its domain: one full shard per table on this GPU, one row size,
+        # row keys only; otherwise the staged pipeline below
+        self._fast = bool(fused) and self._fast_domain()
+        self._step = None
+        self._engine = None
+        self._pool_stream = None
+        self._pending: list = []      # batches whose metrics are still on the device
+        self._inflight: list = []     # started, not yet offered (pipeline_depth > 1)
+        self._epoch_ev = None
+        self._fast_layouts: dict = {}
 
     def _mark(self, name):
         if self.profile:
@@ -219,13 +230,245 @@ class Ranker:
             self.stage_ms[n0] = self.stage_ms.get(n0, 0.0) + e0.elapsed_time(e1)
         self._marks = []
 
+    # -- fused step ---------------------------------------------------------------
+
+    def _fast_domain(self) -> bool:
+        c = self.cache
+        if c is None or c.pooled_results_enabled:
+            return False
+        dims = {m.dim for m in self.deployment.metas.values()}
+        if len(dims) != 1 or max(dims) > c.max_dim:
+            return False
+        for t, m in self.deployment.metas.items():
+            found = False
+            for server in self.deployment.servers.values():
+                for sh in server.shards(t):
+                    if (sh.data is not None and sh.data.device == self.device and sh.start == 0
+                            and sh.end == m.num_rows):
+                        found = True
+            if not found:
+                return False
+        return all(sp.start == 0 and sp.end == self.deployment.meta(sp.table_id).num_rows
+                   for sp in self.routing.shard_list)
+
+    def _admission_needs_resize(self, size: int) -> bool:
+        """ranker.py:195-216 on host scalars: True when the check would raise
+        or resize (those batches take the staged pipeline, which validates
+        first and applies the resize in the reference's order)."""
+        if self.cache is None or self.policy is None:
+            return False
+        model = self.policy.model
+        need = model.nn_bytes(size)
+        return need > model.gpu_capacity_bytes or need + self.cache.budget_bytes > model.gpu_capacity_bytes
+
+    def _get_step(self, nnz: int, n_bags: int):
+        from .step import BatchStep
+        depth = max(1, int(self.params.pipeline_depth))
+        st = self._step
+        if (st is None or nnz > st.max_nnz or n_bags > st.max_bags or st.slots != self.cache._slots
+                or st.n_slots != depth or self.params.admit_per_batch > st.stage_limit_cap):
+            if self._inflight:
+                raise InvariantError("step capacity changed with batches in flight")
+            max_nnz = max(nnz, st.max_nnz if st else 0, 1)
+            max_bags = max(n_bags, st.max_bags if st else 0, 1)
+            # the sketch must take a batch's new keys without rehashing into a
+            # bigger table mid-stream (the step bakes its pointers)
+            self.cache._reserve_sketch(2 * max_nnz)
+            self._step = None
+            self._step = BatchStep(self.cache, self.deployment, max_nnz, max_bags,
+                                   stage_limit_cap=max(64, int(self.params.admit_per_batch)), slots=depth)
+            self._step_slot = 0
+        if self._pool_stream is None:
+            self._pool_stream = torch.cuda.Stream(device=self.device)
+            self._epoch_ev = torch.cuda.Event(enable_timing=True)
+            self._epoch_ev.record()
+        return self._step
+
+    def _fast_start(self, lay: CsrLayout, n_lookups: int, batch_id: int, feature_shape=None, host=None):
+        """Enqueue one batch's start phase and its pooling (K4 on a side
+        stream: the pooled values read only the tables). Returns the in-flight
+        record; its offers/maintenance run in `_fast_finish`."""
+        dev = self.device
+        nnz = int(lay.indices.numel())
+        n_bags = int(lay.offsets.numel()) - 1
+        step = self._get_step(nnz, n_bags)
+        slot = self._step_slot
+        self._step_slot = (slot + 1) % step.n_slots
+        cur = torch.cuda.current_stream(dev)
+        D = next(iter(self.deployment.metas.values())).dim
+        # outputs allocated on the caller's stream (the pooling stream only writes them)
+        if feature_shape is not None:
+            ft, fo, B = feature_shape
+            out = torch.empty((B, len(ft) * D), dtype=torch.float32, device=dev)
+        else:
+            out = torch.zeros((max(n_bags, 1), D), dtype=torch.float32, device=dev)[:n_bags]
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev0.record(cur)
+        side = self._pool_stream
+        side.wait_stream(cur)
+        with torch.cuda.stream(side):
+            if feature_shape is not None:
+                from .engine import CsrBatch, LookupEngine
+                if self._engine is None:
+                    self._engine = LookupEngine(self.deployment, dev)
+                self._engine.pool(CsrBatch(lay.indices, lay.offsets, ft, fo, B), out=out, check=False)
+            elif n_bags:
+                self._pool_fused(lay, n_bags, out=out)
+        cnt = torch.empty((4, max(n_bags, 1)), dtype=torch.int32, device=dev)
+        step.start(slot, lay.bag_table, lay.indices, lay.offsets, lay.sm_start, n_bags, nnz,
+                   self.params.pushdown_threshold, cnt[0], cnt[1], cnt[2], cnt[3])
+        rec = dict(slot=slot, batch_id=batch_id, size=n_lookups, nnz=nnz, out=out, cnt=cnt, ev0=ev0,
+                   lay=lay, host=host, feature_shape=feature_shape)
+        self._inflight.append(rec)
+        return rec
+
+    def _fast_finish(self) -> dict:
+        """Offers + maintenance of the oldest in-flight batch (ranker.py:
+        417-442), then an async snapshot of its metrics."""
+        rec = self._inflight.pop(0)
+        step, c = self._step, self.cache
+        slot = rec["slot"]
+        step.offer(slot)
+        level_before = (list(self.tracker.window), self._last_level) if self.tracker is not None else None
+        rec["tracker_before"] = level_before
+        stage_limit, age = 0, False
+        if self.tracker is not None and self.policy is not None:
+            level = self.tracker.record_batch(rec["size"])
+            self._last_level = level.value
+            if self.params.adaptive_cache:
+                proposed = self.policy.propose(c.budget_bytes, level, self.tracker.windowed_value())
+                if proposed != c.budget_bytes:
+                    # budget change: the staged API (resize -> stage -> age) with host syncs
+                    self._resolve()
+                    sc = step.scalars(slot)
+                    if sc["err"]:
+                        self._fail(rec, sc["err"], sc["err_at"])
+                    rb = lambda t: self.deployment.meta(t).row_bytes
+                    c.resize(proposed, fetcher=lambda t, i: self.deployment.get_row(t, i), row_bytes_of=rb)
+                    if self.params.admit_per_batch > 0:
+                        c.stage_hot_admissions(None, rb, limit=self.params.admit_per_batch)
+                    c.sketch.age()
+                    step.prepare()
+                else:
+                    stage_limit, age = max(0, int(self.params.admit_per_batch)), True
+        if stage_limit or age:
+            step.maintain(slot, stage_limit, age)
+        cur = torch.cuda.current_stream(self.device)
+        cur.wait_stream(self._pool_stream)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev1.record(cur)
+        rec["snap"] = torch.cat([step.scalars_tensor(slot), c.scalars_tensor()])
+        rec["ev1"] = ev1
+        rec["level"] = self._last_level
+        self._pending.append(rec)
+        return rec
+
+    def _fail(self, rec, err: int, err_at: int):
+        from .step import ERR_BAD_INDEX, BatchStep
+        if rec.get("tracker_before") is not None and self.tracker is not None:
+            win, lvl = rec["tracker_before"]
+            self.tracker.window.clear()
+            self.tracker.window.extend(win)
+            self._last_level = lvl
+        if err == ERR_BAD_INDEX:
+            raise self._validation_error(rec, err_at)
+        BatchStep.raise_error(err, f"batch {rec.get('batch_id')}: ")
+
+    def _validation_error(self, rec, err_at: int):
+        """The reference's message for the first bad index in (lookup,
+        feature, position) order (ranker.py:184-193)."""
+        pos = err_at & 0xFFFFFFFF
+        host = rec.get("host")
+        if host is not None:
+            try:
+                host()
+            except LookupValidationError as e:
+                return e
+        lay = rec.get("lay")
+        if lay is None:
+            return LookupValidationError(f"batch {rec.get('batch_id')}: index out of range")
+        offs = lay.offsets.cpu().numpy()
+        b = int(np.searchsorted(offs, pos, side="right") - 1)
+        t = int(lay.bag_table[b].item())
+        index = int(lay.indices[pos].item())
+        n = self.deployment.meta(t).num_rows if t in self.deployment.metas else 0
+        fs = rec.get("feature_shape")
+        li = (b % fs[2]) if fs is not None else int(lay.perm[b] // max(1, len(lay.segs)))
+        return LookupValidationError(f"batch {rec.get('batch_id')}, lookup {li}: index {index} out of "
+                                     f"range [0,{n}) for table {t}")
+
+    def _resolve(self) -> None:
+        """[sync] turn every pending batch's device snapshot into BatchMetrics
+        (and raise the first deferred device error)."""
+        if not self._pending:
+            return
+        from .cache import _SC
+        from .step import IDX, SCALARS
+        pend, self._pending = self._pending, []
+        pend[-1]["ev1"].synchronize()
+        snaps = torch.stack([p["snap"] for p in pend]).cpu().numpy()
+        ns = len(SCALARS)
+        for p, row in zip(pend, snaps):
+            ss, cs = row[:ns], row[ns:]
+            if ss[IDX["err"]]:
+                self._fail(p, int(ss[IDX["err"]]), int(ss[IDX["err_at"]]))
+            entries = int(cs[_SC.index("entries")])
+            m = BatchMetrics(
+                batch_id=p["batch_id"], size=p["size"],
+                started_at=self._epoch_ev.elapsed_time(p["ev0"]) / 1e3,
+                latency=p["ev0"].elapsed_time(p["ev1"]) / 1e3,
+                subrequests=int(ss[IDX["b_groups"]]),
+                cache_hits=int(ss[IDX["b_hits"]]), cache_misses=int(ss[IDX["b_misses"]]),
+                pushdown_groups=int(ss[IDX["b_pd_groups"]]), pushdown_rows=int(ss[IDX["b_pd_rows"]]),
+                raw_rows=int(ss[IDX["b_raw_rows"]]), load_level=p["level"],
+                # ranker.py:397-399: `if self.cache` is False while the cache is empty
+                cache_budget=int(cs[_SC.index("budget")]) if entries else None,
+                cache_used=int(cs[_SC.index("used")]) if entries else None)
+            self.batch_metrics.append(m)
+            cb = p.get("on_resolved")
+            if cb is not None:
+                cb(p, m)
+        # keep the sketch table roomy enough for the next batches' new keys
+        # (the fused step cannot grow it mid-stream)
+        live = int(snaps[-1][ns + _SC.index("sketch_live")])
+        st = self._step
+        if st is not None and not self._inflight and (live + 2 * st.max_nnz) * 10 > self.cache.capacity()["sketch"] * 6:
+            self.cache._reserve_sketch(2 * st.max_nnz + live)
+            if self.cache.capacity()["sketch"] > st.tk_cap:
+                self._step = None
+
+    def sync(self) -> None:
+        """Finish every in-flight batch and resolve deferred metrics / errors."""
+        while self._inflight:
+            self._fast_finish()
+        self._resolve()
+
     # -- driving ----------------------------------------------------------------
 
     def run_trace(self, trace_batches: list) -> None:
-        """Batches run to completion one after another (pipeline_depth > 1 is
-        accepted; the device executes batches in stream order)."""
+        """Closed-loop replay keeping up to `pipeline_depth` batches in flight
+        (ranker.py:161-182): batch k+depth starts (apply_pending + probes)
+        only after batch k finished (offers + maintenance), so with depth d
+        the phases run S0..S(d-1) F0 Sd F1 ... — the reference's order when
+        batches finish in arrival order (one server, FIFO)."""
+        depth = max(1, int(self.params.pipeline_depth))
+        if not getattr(self, "_fast", False) or depth == 1:
+            for b in trace_batches:
+                self._run_batch(b)
+            return
         for b in trace_batches:
-            self._run_batch(b)
+            for lookup in b.lookups:
+                for f in lookup.features:
+                    self.deployment.meta(f.table_id)
+            if self._admission_needs_resize(b.size):
+                raise ConfigError("pipeline_depth > 1 needs an admission check that never resizes the cache "
+                                  "(MemoryModel capacity >= NN bytes + budget)")
+            lay = pack_batch(b, self.device)
+            rec = self._fast_start(lay, b.size, b.batch_id, host=lambda b=b: self._raise_validation(b))
+            rec["on_resolved"] = lambda p, m, b=b: self._emit_fast(b, p)
+            if len(self._inflight) >= depth:
+                self._fast_finish()
+        self.sync()
 
     def execute_batch(self, batch: Batch) -> list:
         self._run_batch(batch)
@@ -267,16 +510,41 @@ class Ranker:
             for f in lookup.features:
                 self.deployment.meta(f.table_id)
         lay = pack_batch(batch, self.device)
+        if getattr(self, "_fast", False) and not self._admission_needs_resize(batch.size):
+            self.sync()
+            rec = self._fast_start(lay, batch.size, batch.batch_id, host=lambda: self._raise_validation(batch))
+            rec["on_resolved"] = lambda p, m: self._emit_fast(batch, p)
+            self.sync()
+            return
+        self.sync()
         res = self._pipeline(lay, batch.size, batch.batch_id, lambda: self._raise_validation(batch))
         self._emit(batch, lay, *res)
 
+    def _emit_fast(self, batch: Batch, rec) -> None:
+        """LookupResults of a fused-step batch (metrics already appended)."""
+        cnt = rec["cnt"].cpu().numpy().astype(np.int64)
+        lay = rec["lay"]
+        n_bags = len(lay.perm)
+        m = self.batch_metrics.pop()
+        self._emit(batch, lay, rec["out"], torch.from_numpy(cnt[0, :n_bags]), torch.from_numpy(cnt[1, :n_bags]),
+                   torch.from_numpy(cnt[2, :n_bags]), torch.from_numpy(cnt[3, :n_bags]), rec["nnz"], m.subrequests,
+                   metrics=m)
+
     def execute_csr(self, indices: torch.Tensor, offsets: torch.Tensor, feature_tables, feature_ops,
-                    batch_size: int, batch_id: int = 0):
+                    batch_size: int, batch_id: int = 0, sync: bool = True):
         """Batched front end (no per-feature Python objects): table-major CSR
         in (bag = f*B + s), pooled [B, F*D] f32 + per-bag counter tensors out.
-        Same pipeline, cache semantics and BatchMetrics as execute_batch."""
+        Same pipeline, cache semantics and BatchMetrics as execute_batch.
+
+        On the fused step (`sync=False`) nothing waits for the device: the
+        batch's BatchMetrics and any deferred error (bad index, capacity) are
+        resolved at the next `sync()` / `sync=True` call."""
         for t in feature_tables:
             self.deployment.meta(t)
+        if getattr(self, "_fast", False) and not self._admission_needs_resize(batch_size):
+            return self._execute_csr_fast(indices, offsets, tuple(feature_tables), tuple(feature_ops), batch_size,
+                                          batch_id, sync)
+        self.sync()
         lay = pack_csr(indices, offsets, feature_tables, feature_ops, batch_size, self.device)
 
         def bad():
@@ -296,6 +564,28 @@ class Ranker:
             cache_used=(c.used_bytes if c else None)))
         return pooled, dict(cache_hits=hits_bag, pushdown_groups=pd_groups, pushdown_rows=pd_rows,
                             raw_rows=raw_rows)
+
+    def _execute_csr_fast(self, indices, offsets, feature_tables, feature_ops, B, batch_id, sync):
+        dev = self.device
+        F = len(feature_tables)
+        key = (feature_tables, B)
+        bt = self._fast_layouts.get(key)
+        if bt is None:
+            bt = torch.tensor(np.repeat(np.asarray(feature_tables, np.int32), B), device=dev)
+            self._fast_layouts[key] = bt
+        idx = indices if indices.dtype in (torch.int32, torch.int64) else indices.long()
+        offs = offsets if offsets.dtype == torch.int64 else offsets.long()
+        if offs.numel() != F * B + 1:
+            raise ConfigError("offsets must describe batch_size * n_features table-major bags")
+        lay = CsrLayout(idx, offs, bt, sample_major_starts(offs, B, F), None, [], None, None, None, B)
+        rec = self._fast_start(lay, B, batch_id, feature_shape=(feature_tables, feature_ops, B))
+        depth = max(1, int(self.params.pipeline_depth))
+        while len(self._inflight) >= depth:
+            self._fast_finish()
+        if sync:
+            self.sync()
+        cnt = rec["cnt"]
+        return rec["out"], dict(cache_hits=cnt[0], pushdown_groups=cnt[1], pushdown_rows=cnt[2], raw_rows=cnt[3])
 
     def _pipeline(self, lay: CsrLayout, n_lookups: int, batch_id: int, raise_validation):
         dev = self.device
@@ -459,12 +749,13 @@ class Ranker:
             return self._pool_fused(lay, n_bags)
         return self._pool_partials(lay, dest, hit_occ, dd, nnz, n_bags)
 
-    def _pool_fused(self, lay: CsrLayout, n_bags) -> torch.Tensor:
+    def _pool_fused(self, lay: CsrLayout, n_bags, out=None) -> torch.Tensor:
         """One K4 launch over the whole batch (f64 accumulate, one rounding)."""
         dev = self.device
         dims = {self.deployment.meta(t).dim for t, *_ in lay.segs}
         D = max(dims) if dims else 1
-        out = torch.zeros((n_bags, D), dtype=torch.float32, device=dev)
+        if out is None:
+            out = torch.zeros((n_bags, D), dtype=torch.float32, device=dev)
         if n_bags == 0:
             return out
         for dim in sorted(dims):
@@ -613,7 +904,7 @@ class Ranker:
             c.stage_hot_admissions(fetcher, rb, limit=self.params.admit_per_batch)
         c.sketch.age()
 
-    def _emit(self, batch, lay, out, hits_bag, pd_groups, pd_rows, raw_rows, nnz, n_groups):
+    def _emit(self, batch, lay, out, hits_bag, pd_groups, pd_rows, raw_rows, nnz, n_groups, metrics=None):
         n_bags = len(lay.perm)
         inv = np.empty(n_bags, dtype=np.int64)
         inv[lay.perm] = np.arange(n_bags)
@@ -645,6 +936,14 @@ class Ranker:
         hits = int(tot[0]) if c is not None else 0
         misses = (nnz - hits) if c is not None else 0
         sub = n_groups  # one subrequest per (lookup, feature, server) group (ranker.py:275-301)
+        if metrics is not None:
+            if (metrics.cache_hits, metrics.pushdown_groups, metrics.pushdown_rows, metrics.raw_rows) != tuple(
+                    int(x) for x in tot):
+                raise InvariantError("fused step counters disagree with the per-bag counters")
+            self.batch_metrics.append(metrics)
+            if self.params.keep_results:
+                self.results[batch.batch_id] = results
+            return
         self.batch_metrics.append(BatchMetrics(
             batch_id=batch.batch_id, size=batch.size, started_at=0.0, latency=0.0, subrequests=sub,
             cache_hits=hits, cache_misses=misses, pushdown_groups=int(tot[1]), pushdown_rows=int(tot[2]),
