@@ -86,12 +86,19 @@ struct StepScalars {
   unsigned long long topk_hi, topk_lo;               // selected prefix of (vinv, key)
   long long topk_digit;
   long long qlen_new;
-  long long pad[8];
+  long long n_levels, codes_on;  // distinct hard-victim estimates (<= 255 -> byte codes)
+  long long chain_cycles;        // clock64 cycles of the decision chain (diagnostics)
+  long long pad[5];
 };
 
-struct DEnt {       // per dedup-hash slot (one 16-byte line for the atomics)
-  int32_t mult, first, last, hit;
+struct DEnt {       // per dedup-hash slot (one 16-byte line for the atomics); all-zero = empty
+  int32_t mult;      // occurrences
+  int32_t first;     // INT_MAX - first sample-major ordinal (atomicMax)
+  int32_t last;      // last ordinal + 1 (atomicMax)
+  int32_t hit;       // cache slot at probe time, -1 = miss
 };
+__device__ __forceinline__ int32_t d_first(const DEnt &e) { return INT_MAX - e.first; }
+__device__ __forceinline__ int32_t d_last(const DEnt &e) { return e.last - 1; }
 
 struct StepView {
   StepScalars *ss;   // this batch's slot
@@ -99,15 +106,17 @@ struct StepView {
   // dedup hash
   uint64_t *dkey;
   DEnt *dent;
-  double *dC;        // sketch estimate after this batch's bump (misses)
   int32_t *dfraw;    // first raw-occurrence ordinal (threshold mode)
   int64_t dcap;
   int32_t *uniq;     // claimed dedup slots
+  int32_t *claim;    // [max_nnz] per occurrence: the dedup slot it claimed, else -1
+  double *dC;        // [dcap] sketch estimate after this batch's bump (misses)
   int32_t *inv;      // per occurrence (CSR position) -> dedup slot
   int32_t *cand_by_first;  // [max_nnz] scatter by ordinal
   int32_t *hit_by_last;    // [max_nnz]
   int32_t *cand;     // compacted candidates (dedup slots) in first raw-occurrence order
   uint64_t *ckey;    // [max_nnz] this slot's candidate keys (kept from start to offer)
+  double *cest;      // [max_nnz] this slot's candidate estimates at probe time
   double *estv;      // [max_nnz] candidate estimates at offer time
   int32_t *pres;     // [max_nnz] 1 = candidate absent at offer time
   int32_t *cidx;     // [max_nnz] absent candidates (positions into ckey)
@@ -122,9 +131,14 @@ struct StepView {
   int32_t *hardf;    // [scap] hard-victim flags
   int32_t *hard;     // [scap] compacted hard positions
   int32_t *rj_beg, *rj_end;  // reject intervals
+  uint8_t *code;     // [max_nnz] per candidate: number of distinct hard levels <= its estimate
+  uint8_t *bsum;     // [max_nnz / 32 + 1] max code per 32 candidates
+  uint8_t *hrank;    // [scap] per hard victim: 1 + index of its level (accept iff code >= hrank)
+  double *levels;    // [256] distinct hard-victim estimates, ascending
   int32_t *acc;      // [max_nnz] accept flags, then ranks
   int32_t *rank;
-  int32_t *accslot;  // [max_nnz] slot taken by accept r (sequential mode)
+  int32_t *aslot;    // [max_nnz] slot taken by accept r
+  uint64_t *akey;    // [max_nnz] key of accept r
   int32_t *accj;     // [max_nnz] candidate index of accept r (sequential mode)
   int64_t max_nnz;
   // per-table row source and validation bounds (dense by table id)
@@ -150,6 +164,45 @@ __device__ __forceinline__ bool aborted(const StepView &v) { return v.ss->err !=
 __device__ __forceinline__ long long warp_sum(long long x) {
   for (int o = 16; o; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
   return x;
+}
+
+// block-aggregated atomicAdd (every thread of the block calls it): one global
+// atomic per block instead of one per warp — same-address atomics serialise
+__device__ __forceinline__ void block_add(unsigned long long *ctr, long long x) {
+  __shared__ long long red[32];
+  x = warp_sum(x);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) red[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    long long y = lane < static_cast<int>(blockDim.x >> 5) ? red[lane] : 0;
+    y = warp_sum(y);
+    if (lane == 0 && y) atomicAdd(ctr, static_cast<unsigned long long>(y));
+  }
+}
+
+// block-aggregated append (every thread calls it): position of this thread's
+// item when `want`, one global atomic per block
+__device__ __forceinline__ long long block_append(unsigned long long *ctr, int want) {
+  __shared__ int wcnt[32];
+  __shared__ unsigned long long base;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned m = __ballot_sync(0xffffffffu, want);
+  __syncthreads();
+  if (lane == 0) wcnt[w] = __popc(m);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int tot = 0;
+    for (int i = 0; i < static_cast<int>(blockDim.x >> 5); ++i) {
+      const int c = wcnt[i];
+      wcnt[i] = tot;
+      tot += c;
+    }
+    base = tot ? atomicAdd(ctr, static_cast<unsigned long long>(tot)) : 0ull;
+  }
+  __syncthreads();
+  return static_cast<long long>(base) + wcnt[w] + __popc(m & ((1u << lane) - 1u));
 }
 
 // warp-aggregated atomicAdd of a per-lane count; returns this lane's base
@@ -223,10 +276,11 @@ __global__ void ks_begin(CacheView c, StepView v, int64_t max_nnz) {
 // in-place sketch rehash (drops tombstones): collect -> clear -> reinsert
 __global__ void ks_sketch_collect(CacheView c, StepView v) {
   if (!v.ss->rehash_sketch) return;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < c.kcap; i += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t k = c.kkeys[i];
+  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x; i0 < c.kcap; i0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = i0 + threadIdx.x;
+    const uint64_t k = i < c.kcap ? c.kkeys[i] : kEmpty;
     const bool live = k != kEmpty && k != kTomb;
-    const long long p = warp_append(reinterpret_cast<unsigned long long *>(&v.ss->rehash_n), live);
+    const long long p = block_append(reinterpret_cast<unsigned long long *>(&v.ss->rehash_n), live);
     if (live) {
       v.tk_key[p] = k;
       v.tk_val[p] = c.kval[i];
@@ -360,7 +414,7 @@ __global__ void __launch_bounds__(256) ks_dedup(StepView v, const int32_t *__res
       const int32_t t = __shfl_sync(0xffffffffu, tab, j);
       const int64_t sm = __shfl_sync(0xffffffffu, sms, j);
       const bool act = p < end;
-      int claimed = 0;
+      bool claimed = false;
       int32_t u = -1;
       int ord = 0;
       if (act) {
@@ -377,20 +431,19 @@ __global__ void __launch_bounds__(256) ks_dedup(StepView v, const int32_t *__res
           while (true) {
             const unsigned long long prev = atomicCAS(reinterpret_cast<unsigned long long *>(&v.dkey[h]),
                                                       (unsigned long long)kEmpty, (unsigned long long)key);
-            if (prev == kEmpty) { claimed = 1; break; }
+            if (prev == kEmpty) { claimed = true; break; }
             if (prev == key) break;
             h = (h + 1) & dm;
           }
           u = static_cast<int32_t>(h);
           DEnt *e = &v.dent[u];
           atomicAdd(&e->mult, 1);
-          atomicMin(&e->first, ord);
-          atomicMax(&e->last, ord);
+          atomicMax(&e->first, INT_MAX - ord);  // zero-initialised encodings (memset reset)
+          atomicMax(&e->last, ord + 1);
           v.inv[p] = u;
         }
+        v.claim[p] = claimed ? u : -1;
       }
-      const long long pos = warp_append(reinterpret_cast<unsigned long long *>(&v.ss->n_uniq), claimed);
-      if (claimed) v.uniq[pos] = u;
     }
   }
 }
@@ -408,30 +461,25 @@ __global__ void __launch_bounds__(256) ks_probe(CacheView c, StepView v, int32_t
     DEnt e = v.dent[u];
     const int32_t s = h_find(c, key);
     if (s >= 0) {
-      c.stick[s] = tick0 + e.last + 1;
+      c.stick[s] = tick0 + d_last(e) + 1;
       c.shits[s] += e.mult;
       v.sflag[s] = static_cast<int32_t>(epoch);
-      v.hit_by_last[e.last] = s;
+      v.hit_by_last[d_last(e)] = s;
       hits += e.mult;
     } else {
       bool b = false;
-      sketch_add_val(c, key, static_cast<double>(e.mult), &b);
+      v.dC[u] = sketch_add_val(c, key, static_cast<double>(e.mult), &b);
       born += b ? 1 : 0;
       misses += e.mult;
-      if (!threshold_on) v.cand_by_first[e.first] = u;
+      if (!threshold_on) v.cand_by_first[d_first(e)] = u;
     }
     v.dent[u].hit = s;
   }
-  hits = warp_sum(hits);
-  misses = warp_sum(misses);
-  born = warp_sum(born);
-  if ((threadIdx.x & 31) == 0) {
-    if (hits) atomicAdd(reinterpret_cast<unsigned long long *>(&c.sc->hits), (unsigned long long)hits);
-    if (misses) atomicAdd(reinterpret_cast<unsigned long long *>(&c.sc->misses), (unsigned long long)misses);
-    if (born) atomicAdd(reinterpret_cast<unsigned long long *>(&c.sc->sketch_live), (unsigned long long)born);
-    if (hits) atomicAdd(reinterpret_cast<unsigned long long *>(&v.ss->b_hits), (unsigned long long)hits);
-    if (misses) atomicAdd(reinterpret_cast<unsigned long long *>(&v.ss->b_misses), (unsigned long long)misses);
-  }
+  block_add(reinterpret_cast<unsigned long long *>(&c.sc->hits), hits);
+  block_add(reinterpret_cast<unsigned long long *>(&c.sc->misses), misses);
+  block_add(reinterpret_cast<unsigned long long *>(&c.sc->sketch_live), born);
+  block_add(reinterpret_cast<unsigned long long *>(&v.ss->b_hits), hits);
+  block_add(reinterpret_cast<unsigned long long *>(&v.ss->b_misses), misses);
 }
 
 __global__ void ks_after_probe(CacheView c, StepView v, int64_t nnz) {
@@ -447,7 +495,7 @@ __global__ void __launch_bounds__(256) ks_bag_plan(StepView v, const int64_t *__
                                                    const int64_t *__restrict__ sm_start, int64_t n_bags,
                                                    int32_t threshold, int32_t *hits_bag, int32_t *pd_groups,
                                                    int32_t *pd_rows, int32_t *raw_rows) {
-  if (aborted(v)) return;
+  if (aborted(v)) return;  // uniform: the whole grid returns
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -473,16 +521,14 @@ __global__ void __launch_bounds__(256) ks_bag_plan(StepView v, const int64_t *__
       const int64_t sm = __ldg(&sm_start[b]);
       for (int64_t p = beg + lane; p < end; p += 32) {
         const int32_t u = v.inv[p];
-        if (v.dent[u].hit < 0) atomicMin(&v.dfraw[u], static_cast<int32_t>(sm + (p - beg)));
+        if (v.dent[u].hit < 0) atomicMax(&v.dfraw[u], INT_MAX - static_cast<int32_t>(sm + (p - beg)));
       }
     }
   }
-  if (lane == 0) {
-    if (groups) atomicAdd(reinterpret_cast<unsigned long long *>(&v.ss->b_groups), (unsigned long long)groups);
-    if (pdg) atomicAdd(reinterpret_cast<unsigned long long *>(&v.ss->b_pd_groups), (unsigned long long)pdg);
-    if (pdr) atomicAdd(reinterpret_cast<unsigned long long *>(&v.ss->b_pd_rows), (unsigned long long)pdr);
-    if (raw) atomicAdd(reinterpret_cast<unsigned long long *>(&v.ss->b_raw_rows), (unsigned long long)raw);
-  }
+  block_add(reinterpret_cast<unsigned long long *>(&v.ss->b_groups), groups);
+  block_add(reinterpret_cast<unsigned long long *>(&v.ss->b_pd_groups), pdg);
+  block_add(reinterpret_cast<unsigned long long *>(&v.ss->b_pd_rows), pdr);
+  block_add(reinterpret_cast<unsigned long long *>(&v.ss->b_raw_rows), raw);
 }
 
 __global__ void ks_cand_scatter_raw(StepView v) {
@@ -491,7 +537,7 @@ __global__ void ks_cand_scatter_raw(StepView v) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int32_t u = v.uniq[i];
     const int32_t f = v.dfraw[u];
-    if (f != INT_MAX) v.cand_by_first[f] = u;
+    if (f != 0) v.cand_by_first[INT_MAX - f] = u;
   }
 }
 
@@ -511,22 +557,33 @@ struct QueueKeep {
 __global__ void ks_cand_keys(StepView v) {
   if (aborted(v)) return;
   const long long n = v.ss->n_cand;
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
-    v.ckey[j] = v.dkey[v.cand[j]];
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t u = v.cand[j];
+    v.ckey[j] = v.dkey[u];
+    v.cest[j] = v.dC[u];  // the sketch value right after this batch's bump
+  }
 }
 
 // offer time: a candidate installed since the probes (apply_pending of a
 // later batch when several are in flight) is present -> offer() returns True
 // with no side effect (cache.py:245-246); the rest keep their order
-__global__ void ks_offer_prep(CacheView c, StepView v, int64_t max_nnz) {
+// `fresh`: no other batch ran between this batch's probes and its offers
+// (pipeline_depth 1), so every candidate is still absent and its estimate is
+// the probe-time value
+__global__ void ks_offer_prep(CacheView c, StepView v, int64_t max_nnz, int32_t fresh) {
   const bool on = !aborted(v);
   const long long n = on ? v.ss->n_cand : 0;
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < max_nnz; j += (int64_t)gridDim.x * blockDim.x) {
     int32_t f = 0;
     if (j < n) {
       const uint64_t key = v.ckey[j];
-      f = h_find(c, key) < 0 ? 1 : 0;
-      if (f) v.estv[j] = k_est(c, key);
+      if (fresh) {
+        f = 1;
+        v.estv[j] = v.cest[j];
+      } else {
+        f = h_find(c, key) < 0 ? 1 : 0;
+        if (f) v.estv[j] = k_est(c, key);
+      }
     }
     v.pres[j] = f;
   }
@@ -650,7 +707,7 @@ __device__ __forceinline__ long long next_ge(const StepView &v, const double *sb
 // first stages the per-block maxima in shared memory).
 __global__ void __launch_bounds__(1024) ks_chain(StepView v) {
   extern __shared__ double sbm[];
-  if (aborted(v) || v.ss->mode != MODE_PAR) return;
+  if (aborted(v) || v.ss->mode != MODE_PAR || v.ss->codes_on) return;
   const long long n = v.ss->n_off, F = v.ss->F, nh = v.ss->n_hard;
   const long long nblk = (n + kFine - 1) / kFine;
   for (long long b = threadIdx.x; b < nblk; b += blockDim.x) sbm[b] = v.bmax[b];
@@ -688,6 +745,310 @@ __global__ void __launch_bounds__(1024) ks_chain(StepView v) {
   if (lane == 0) v.ss->n_rej = nrej;
 }
 
+// Distinct hard-victim estimates (sorted) and each hard victim's rank; one
+// block. More than 255 distinct levels -> codes off (f64 chain instead).
+__global__ void __launch_bounds__(1024) ks_levels(StepView v, int32_t stream_ok) {
+  __shared__ unsigned long long set[4096];
+  __shared__ double lv[256];
+  __shared__ int nset, overflow;
+  if (aborted(v) || v.ss->mode != MODE_PAR) return;
+  const long long nh = v.ss->n_hard;
+  if (threadIdx.x == 0) {
+    nset = 0;
+    overflow = 0;
+    v.ss->codes_on = 0;
+    v.ss->n_levels = 0;
+  }
+  for (int i = threadIdx.x; i < 4096; i += blockDim.x) set[i] = 0ull;
+  __syncthreads();
+  if (nh == 0) return;
+  for (long long k = threadIdx.x; k < nh && !overflow; k += blockDim.x) {
+    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v.E[v.hard[k]]));
+    unsigned h = static_cast<unsigned>(hash_key(b)) & 4095u;
+    for (int probe = 0; probe < 4096; ++probe) {
+      const unsigned long long prev = atomicCAS(&set[h], 0ull, b);
+      if (prev == 0ull) {
+        if (atomicAdd(&nset, 1) >= 255) overflow = 1;
+        break;
+      }
+      if (prev == b) break;
+      h = (h + 1) & 4095u;
+    }
+  }
+  __syncthreads();
+  if (overflow) return;
+  __shared__ int cnt;
+  if (threadIdx.x == 0) cnt = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < 4096; i += blockDim.x)
+    if (set[i]) lv[atomicAdd(&cnt, 1)] = __longlong_as_double(static_cast<long long>(set[i]));
+  __syncthreads();
+  const int K = cnt;
+  if (threadIdx.x < K) {  // rank by counting (distinct values)
+    const double x = lv[threadIdx.x];
+    int r = 0;
+    for (int j = 0; j < K; ++j) r += lv[j] < x ? 1 : 0;
+    v.levels[r] = x;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < K; i += blockDim.x) lv[i] = v.levels[i];
+  __syncthreads();
+  for (long long k = threadIdx.x; k < nh; k += blockDim.x) {
+    const double e = v.E[v.hard[k]];
+    int lo = 0, hi = K;  // first index with lv >= e (== e: e is a level)
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (lv[mid] < e) lo = mid + 1; else hi = mid;
+    }
+    v.hrank[k] = static_cast<uint8_t>(lo + 1);
+  }
+  if (threadIdx.x == 0) {
+    v.ss->n_levels = K;
+    v.ss->codes_on = stream_ok ? 2 : 1;
+  }
+}
+
+// code per candidate (number of levels <= its estimate) and per-32 maxima
+__global__ void __launch_bounds__(256) ks_cand_codes(StepView v) {
+  __shared__ double lv[256];
+  if (aborted(v) || v.ss->mode != MODE_PAR || !v.ss->codes_on) return;
+  const int K = static_cast<int>(v.ss->n_levels);
+  for (int i = threadIdx.x; i < K; i += blockDim.x) lv[i] = v.levels[i];
+  __syncthreads();
+  const long long n = v.ss->n_off;
+  for (int64_t j0 = blockIdx.x * (int64_t)blockDim.x; j0 < n; j0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = j0 + threadIdx.x;
+    int code = 0;
+    if (j < n) {
+      const double x = v.cC[j];
+      int lo = 0, hi = K;  // number of levels <= x
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (lv[mid] <= x) lo = mid + 1; else hi = mid;
+      }
+      code = lo;
+      v.code[j] = static_cast<uint8_t>(code);
+    }
+    int m = code;
+    for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0 && j < n) v.bsum[j >> 5] = static_cast<uint8_t>(m);
+  }
+}
+
+// The decision chain on byte codes: per hard victim one 32-byte probe of the
+// arrival's block and one of the first block (shared-memory per-32 maxima)
+// that can satisfy it, both in flight together.
+__global__ void __launch_bounds__(1024) ks_chain_codes(StepView v) {
+  extern __shared__ uint8_t sb[];
+  if (aborted(v) || v.ss->mode != MODE_PAR || v.ss->codes_on != 1) return;
+  const long long n = v.ss->n_off, F = v.ss->F, nh = v.ss->n_hard;
+  const long long nblk = (n + 31) >> 5;
+  for (long long b = threadIdx.x; b < nblk; b += blockDim.x) sb[b] = v.bsum[b];
+  __syncthreads();
+  if (threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
+  const uint8_t *code = v.code;
+  const long long t_start = clock64();
+  long long x = F, h = 0, nrej = 0;
+  for (long long k0 = 0; k0 < nh; k0 += 32) {
+    const long long kk = k0 + lane;
+    const int32_t hp = kk < nh ? v.hard[kk] : 0;
+    const int hr = kk < nh ? v.hrank[kk] : 0;
+    const int cnt = nh - k0 < 32 ? static_cast<int>(nh - k0) : 32;
+    bool stop = false;
+    for (int t = 0; t < cnt; ++t) {
+      const long long b = __shfl_sync(0xffffffffu, hp, t);
+      const int r = __shfl_sync(0xffffffffu, hr, t);
+      const long long gap = b - h;
+      if (x + gap >= n) { x = n; stop = true; break; }
+      x += gap;
+      h = b;
+      // next candidate j >= x with code[j] >= r
+      const long long base = x & ~31ll;
+      const long long p1 = base + lane;
+      const int c1 = p1 < n ? code[p1] : 0;
+      long long B = nblk;
+      for (long long b0 = (x >> 5) + 1; b0 < nblk; b0 += 32) {
+        const long long bb = b0 + lane;
+        const unsigned m = __ballot_sync(0xffffffffu, bb < nblk && sb[bb] >= r);
+        if (m) { B = b0 + __ffs(m) - 1; break; }
+      }
+      const long long p2 = B * 32 + lane;
+      const int c2 = (B < nblk && p2 < n) ? code[p2] : 0;
+      long long j = n;
+      const unsigned m1 = __ballot_sync(0xffffffffu, p1 >= x && p1 < n && c1 >= r);
+      if (m1) {
+        j = base + __ffs(m1) - 1;
+      } else if (B < nblk) {
+        const unsigned m2 = __ballot_sync(0xffffffffu, p2 < n && c2 >= r);
+        if (m2) j = B * 32 + __ffs(m2) - 1;
+      }
+      if (j > x) {
+        if (lane == 0) {
+          v.rj_beg[nrej] = static_cast<int32_t>(x);
+          v.rj_end[nrej] = static_cast<int32_t>(j);
+        }
+        ++nrej;
+      }
+      if (j >= n) { x = n; stop = true; break; }
+      x = j + 1;
+      h = b + 1;
+    }
+    if (stop) break;
+  }
+  if (lane == 0) {
+    v.ss->n_rej = nrej;
+    v.ss->chain_cycles = clock64() - t_start;
+  }
+}
+
+// The same chain with the codes streamed through a shared-memory ring: the
+// chain's candidate position only moves forward, so producer warps copy the
+// code array ahead of it (16-byte loads, several in flight per thread) while
+// warp 0 walks the hard victims entirely from shared memory — the per-32
+// maxima to skip, the ring to find the exact candidate. Warp 0 publishes the
+// lowest position it can still need; producers restart there when it jumps.
+constexpr int kRing = 1 << 16;        // ring bytes (power of two)
+constexpr int kProdWarps = 16;        // producer warps (1..16)
+constexpr int kProdUnroll = 2;        // 16-byte loads in flight per producer thread
+constexpr int kChunk = kProdWarps * 32 * 16 * kProdUnroll;  // bytes per producer round
+
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
+
+__global__ void __launch_bounds__(1024) ks_chain_stream(StepView v) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ volatile long long filled, consumed, ppos;
+  __shared__ volatile int done;
+  __shared__ long long pstart;
+  if (aborted(v) || v.ss->mode != MODE_PAR || v.ss->codes_on != 2) return;
+  const long long n = v.ss->n_off, F = v.ss->F, nh = v.ss->n_hard;
+  const long long nblk = (n + 31) >> 5;
+  uint8_t *sum = smem;
+  uint8_t *ring = smem + ((nblk + 15) & ~15ll);
+  for (long long b = threadIdx.x; b < nblk; b += blockDim.x) sum[b] = v.bsum[b];
+  if (threadIdx.x == 0) {
+    filled = F & ~15ll;
+    consumed = F & ~15ll;
+    ppos = F & ~15ll;
+    done = 0;
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp >= 1 && warp <= kProdWarps) {
+    // ---- producers
+    const int pt = threadIdx.x - 32;
+    while (true) {
+      if (pt == 0) {
+        long long st;
+        while (true) {
+          const long long c = consumed;
+          st = ppos > (c & ~15ll) ? ppos : (c & ~15ll);
+          if (done || st >= n || st + kChunk <= c + kRing) break;
+        }
+        pstart = (done || st >= n) ? -1 : st;
+      }
+      named_bar(1, kProdWarps * 32);
+      const long long st = pstart;
+      if (st < 0) break;
+      int4 tmp[kProdUnroll];
+#pragma unroll
+      for (int u = 0; u < kProdUnroll; ++u) {
+        const long long p = st + (static_cast<long long>(u) * kProdWarps * 32 + pt) * 16;
+        tmp[u] = p < n ? __ldg(reinterpret_cast<const int4 *>(v.code + p)) : make_int4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < kProdUnroll; ++u) {
+        const long long p = st + (static_cast<long long>(u) * kProdWarps * 32 + pt) * 16;
+        *reinterpret_cast<int4 *>(ring + (p & (kRing - 1))) = tmp[u];
+      }
+      __threadfence_block();
+      named_bar(1, kProdWarps * 32);
+      if (pt == 0) {
+        ppos = st + kChunk;
+        filled = st + kChunk;
+      }
+    }
+    return;
+  }
+  if (warp != 0) return;
+  // ---- the chain
+  const long long t_start = clock64();
+  long long x = F, h = 0, nrej = 0;
+  long long fl = 0, pub = F & ~15ll;  // last seen `filled`, last published `consumed`
+  for (long long k0 = 0; k0 < nh; k0 += 32) {
+    const long long kk = k0 + lane;
+    const int32_t hp = kk < nh ? v.hard[kk] : 0;
+    const int hr = kk < nh ? v.hrank[kk] : 0;
+    const int cnt = nh - k0 < 32 ? static_cast<int>(nh - k0) : 32;
+    bool stop = false;
+    for (int t = 0; t < cnt; ++t) {
+      const long long b = __shfl_sync(0xffffffffu, hp, t);
+      const int r = __shfl_sync(0xffffffffu, hr, t);
+      const long long gap = b - h;
+      if (x + gap >= n) { x = n; stop = true; break; }
+      x += gap;
+      h = b;
+      // next j >= x with code >= r: rest of x's 32-block from the ring, else
+      // the first later block whose maximum reaches r (shared-memory scan)
+      if (x >= pub + 4096) {  // publish progress so producers can reuse ring space
+        pub = x & ~15ll;
+        if (lane == 0) consumed = pub;
+      }
+      const long long blk = x >> 5;
+      long long need = blk * 32 + 32 < n ? blk * 32 + 32 : n;
+      if (need > fl) {
+        if (lane == 0) consumed = x & ~15ll;
+        pub = x & ~15ll;
+        while ((fl = filled) < need) {
+        }
+        __threadfence_block();
+      }
+      long long j = n;
+      const long long p1 = blk * 32 + lane;
+      const int c1 = p1 < n ? ring[p1 & (kRing - 1)] : 0;
+      long long B = nblk;
+      for (long long b0 = blk + 1; b0 < nblk; b0 += 32) {
+        const long long bb = b0 + lane;
+        const unsigned mb = __ballot_sync(0xffffffffu, bb < nblk && sum[bb] >= r);
+        if (mb) { B = b0 + __ffs(mb) - 1; break; }
+      }
+      const unsigned m1 = __ballot_sync(0xffffffffu, p1 >= x && p1 < n && c1 >= r);
+      if (m1) {
+        j = blk * 32 + __ffs(m1) - 1;
+      } else if (B < nblk) {
+        need = B * 32 + 32 < n ? B * 32 + 32 : n;
+        if (need > fl) {
+          if (lane == 0) consumed = (B * 32) & ~15ll;
+          pub = B * 32;
+          while ((fl = filled) < need) {
+          }
+          __threadfence_block();
+        }
+        const long long p2 = B * 32 + lane;
+        const int c2 = p2 < n ? ring[p2 & (kRing - 1)] : 0;
+        const unsigned m2 = __ballot_sync(0xffffffffu, p2 < n && c2 >= r);
+        j = B * 32 + __ffs(m2) - 1;  // m2 != 0: the block's maximum reaches r
+      }
+      if (j > x) {
+        if (lane == 0) {
+          v.rj_beg[nrej] = static_cast<int32_t>(x);
+          v.rj_end[nrej] = static_cast<int32_t>(j);
+        }
+        ++nrej;
+      }
+      if (j >= n) { x = n; stop = true; break; }
+      x = j + 1;
+      h = b + 1;
+    }
+    if (stop) break;
+  }
+  if (lane == 0) {
+    v.ss->n_rej = nrej;
+    v.ss->chain_cycles = clock64() - t_start;
+    done = 1;
+  }
+}
+
 // accept flag per candidate (0 inside a reject interval)
 __global__ void ks_accept_flags(StepView v, int64_t max_nnz) {
   if (aborted(v)) return;
@@ -707,47 +1068,64 @@ __global__ void ks_accept_flags(StepView v, int64_t max_nnz) {
   }
 }
 
-// side effects of the accepts, warp per candidate: accept rank r takes a free
-// slot (r < F) or evicts V[r - F] and takes its slot; tick tick_base + r + 1
+// side effects of the accepts, thread per candidate: accept rank r takes a
+// free slot (r < F) or evicts V[r - F] and takes its slot; tick
+// tick_base + r + 1. Rows are copied by ks_copy_rows.
 __global__ void __launch_bounds__(256) ks_apply(CacheView c, StepView v) {
   if (aborted(v) || v.ss->mode != MODE_PAR) return;
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const long long n = v.ss->n_off, F = v.ss->F, e0 = v.ss->e0, ftop0 = v.ss->ftop0, log0 = v.ss->log0;
   const long long tick_base = v.ss->tick_base;
-  // n_ev = accepts beyond the free units (a prefix of V)
   const long long n_acc = n > 0 ? v.rank[n - 1] + v.acc[n - 1] : 0;
   const long long n_ev = n_acc > F ? n_acc - F : 0;
   long long tombs = 0;
-  for (int64_t j = warp; j < n; j += nw) {
-    if (!v.acc[j]) continue;
-    const long long r = v.rank[j];
-    const uint64_t key = v.okey[j];
-    int32_t slot;
-    if (r < F) {
-      slot = c.free_stack[ftop0 - 1 - r];
-    } else {
-      const long long q = r - F;
-      slot = v.q[q];
-      if (lane == 0) {
+  for (int64_t j0 = blockIdx.x * (int64_t)blockDim.x; j0 < n; j0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = j0 + threadIdx.x;
+    if (j < n && v.acc[j]) {
+      const long long r = v.rank[j];
+      const uint64_t key = v.okey[j];
+      int32_t slot;
+      if (r < F) {
+        slot = c.free_stack[ftop0 - 1 - r];
+        c.ssize[slot] = v.S;
+      } else {
+        const long long q = r - F;
+        slot = v.q[q];
         const uint64_t ok = c.skey[slot];
         if (c.evlog_cap > 0 && log0 + q < c.evlog_cap) c.evlog[log0 + q] = ok;
         tombs += h_erase(c, ok) ? 1 : 0;
       }
-    }
-    if (lane == 0) {
       c.skey[slot] = key;
-      c.skey2[slot] = 0;
       c.stick[slot] = tick_base + r + 1;
-      c.ssize[slot] = v.S;
       c.shits[slot] = 0;
       h_insert(c, key, slot);
       v.qnew[e0 - n_ev + r] = slot;
+      v.aslot[r] = slot;
+      v.akey[r] = key;
     }
-    warp_copy_row(c.rows + static_cast<int64_t>(slot) * c.row_ld, row_src(v, key), v.dim, lane);
   }
-  if (lane == 0 && tombs) atomicAdd(reinterpret_cast<unsigned long long *>(&c.sc->hash_tomb), (unsigned long long)tombs);
+  block_add(reinterpret_cast<unsigned long long *>(&c.sc->hash_tomb), tombs);
+}
+
+// row copies of the accepts (both decision modes): thread per 16 bytes
+__global__ void __launch_bounds__(256) ks_copy_rows(CacheView c, StepView v) {
+  if (aborted(v) || v.ss->mode == MODE_NONE) return;
+  const long long na = v.ss->n_acc;
+  const bool seq = v.ss->mode == MODE_SEQ;
+  const int dim = v.dim;
+  const bool vec = (dim & 3) == 0 && (c.row_ld & 3) == 0;
+  const int per = vec ? dim / 4 : dim;
+  const long long total = na * per;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const long long r = i / per;
+    const int k = static_cast<int>(i - r * per);
+    const int32_t slot = v.aslot[r];
+    const uint64_t key = v.akey[r];
+    if (seq && (c.skey[slot] != key || c.stick[slot] == kFree)) continue;  // evicted again in the same call
+    const float *src = row_src(v, key);
+    float *dst = c.rows + static_cast<int64_t>(slot) * c.row_ld;
+    if (vec) reinterpret_cast<float4 *>(dst)[k] = __ldg(reinterpret_cast<const float4 *>(src) + k);
+    else dst[k] = __ldg(src + k);
+  }
 }
 
 // surviving victims move to the queue front: qnew[i] = q[n_ev + i]
@@ -800,7 +1178,7 @@ __global__ void ks_offer_finish(CacheView c, StepView v) {
 
 // Exact sequential offers for batches outside the parallel domain
 // (cache.py:237-268; V grows by this call's own accepts, or the cache is
-// above budget). Single thread; rows are copied by ks_seq_rows.
+// above budget). Single thread; rows are copied by ks_copy_rows.
 __global__ void ks_seq_offer(CacheView c, StepView v) {
   if (aborted(v) || v.ss->mode != MODE_SEQ || threadIdx.x != 0 || blockIdx.x != 0) return;
   StepScalars *s = v.ss;
@@ -808,7 +1186,7 @@ __global__ void ks_seq_offer(CacheView c, StepView v) {
   const long long n = s->n_off, e0 = s->e0, S = v.S, budget = sc->budget;
   long long e = e0, h = 0, n_acc = 0, ftop = sc->free_top, tick = s->tick_base, nlog = sc->n_evlog, tombs = 0;
   const bool sketch = c.admission == 0;
-  auto vslot = [&](long long q) -> int32_t { return q < e0 ? v.q[q] : v.accslot[q - e0]; };
+  auto vslot = [&](long long q) -> int32_t { return q < e0 ? v.q[q] : v.aslot[q - e0]; };
   for (long long j = 0; j < n; ++j) {
     const double cj = v.cC[j];
     if ((e + 1) * S > budget) {
@@ -840,7 +1218,8 @@ __global__ void ks_seq_offer(CacheView c, StepView v) {
     c.ssize[slot] = static_cast<int32_t>(S);
     c.shits[slot] = 0;
     h_insert(c, key, slot);
-    v.accslot[n_acc] = slot;
+    v.aslot[n_acc] = slot;
+    v.akey[n_acc] = key;
     v.accj[n_acc] = static_cast<int32_t>(j);
     ++n_acc;
     ++e;
@@ -860,20 +1239,6 @@ __global__ void ks_seq_offer(CacheView c, StepView v) {
   s->qlen_new = e;
 }
 
-__global__ void __launch_bounds__(256) ks_seq_rows(CacheView c, StepView v) {
-  if (aborted(v) || v.ss->mode != MODE_SEQ) return;
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const long long na = v.ss->n_acc;
-  for (int64_t a = warp; a < na; a += nw) {
-    const int32_t slot = v.accslot[a];
-    const uint64_t key = v.okey[v.accj[a]];
-    if (c.skey[slot] != key || c.stick[slot] == kFree) continue;  // evicted again in the same call
-    warp_copy_row(c.rows + static_cast<int64_t>(slot) * c.row_ld, row_src(v, key), v.dim, lane);
-  }
-}
-
 __global__ void ks_index_clear(CacheView c, StepView v) {
   if (!v.ss->rebuild_index) return;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < c.hcap; i += (int64_t)gridDim.x * blockDim.x)
@@ -885,17 +1250,6 @@ __global__ void ks_index_fill(CacheView c, StepView v) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < c.scap; i += (int64_t)gridDim.x * blockDim.x)
     if (c.stick[i] != kFree) h_insert(c, c.skey[i], static_cast<int32_t>(i));
   if (blockIdx.x == 0 && threadIdx.x == 0) c.sc->hash_tomb = 0;
-}
-
-// reset the dedup slots this batch claimed (lazy clear: O(unique keys))
-__global__ void ks_dedup_reset(StepView v) {
-  const long long n = v.ss->n_uniq;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t u = v.uniq[i];
-    v.dkey[u] = kEmpty;
-    v.dent[u] = DEnt{0, INT_MAX, -1, -1};
-    v.dfraw[u] = INT_MAX;
-  }
 }
 
 // ---------------------------------------------------------------- 6. stage(limit)
@@ -919,15 +1273,41 @@ __global__ void ks_stage_begin(CacheView c, StepView v, int64_t limit) {
   s->topk_n = 0;
 }
 
-__global__ void ks_topk_collect(CacheView c, StepView v) {
+// pass 0 over the whole sketch: histogram of the top 16 bits of vinv
+__global__ void __launch_bounds__(256) ks_topk_hist0(CacheView c, StepView v) {
   if (!v.ss->stage_on) return;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < c.kcap; i += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t k = c.kkeys[i];
-    const bool live = k != kEmpty && k != kTomb;
-    const long long p = warp_append(reinterpret_cast<unsigned long long *>(&v.ss->topk_live), live);
-    if (live) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); i0 < c.kcap;
+       i0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = i0 + lane;
+    int bin = -1;
+    if (i < c.kcap) {
+      const uint64_t k = c.kkeys[i];
+      if (k != kEmpty && k != kTomb) bin = static_cast<int>(vinv_of(c.kval[i]) >> 48);
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, bin);
+    if (bin >= 0 && lane == __ffs(peers) - 1) atomicAdd(&v.tk_hist[bin], __popc(peers));
+  }
+}
+
+// live entries whose top digit is <= the selected one: every key that can be
+// in the top `limit` (keys below the digit are in for sure)
+__global__ void __launch_bounds__(256) ks_topk_collect(CacheView c, StepView v) {
+  if (!v.ss->stage_on) return;
+  const uint64_t g0 = v.ss->topk_hi >> 48;
+  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x; i0 < c.kcap; i0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = i0 + threadIdx.x;
+    const uint64_t k = i < c.kcap ? c.kkeys[i] : kEmpty;
+    uint64_t vi = 0;
+    bool in = k != kEmpty && k != kTomb;
+    if (in) {
+      vi = vinv_of(c.kval[i]);
+      in = (vi >> 48) <= g0;
+    }
+    const long long p = block_append(reinterpret_cast<unsigned long long *>(&v.ss->topk_live), in);
+    if (in) {
       v.tk_key[p] = k;
-      v.tk_vinv[p] = vinv_of(c.kval[i]);
+      v.tk_vinv[p] = vi;
     }
   }
 }
@@ -950,7 +1330,8 @@ __device__ __forceinline__ bool prefix_match(uint64_t hi, uint64_t lo, uint64_t 
   return sh >= 64 ? true : (lo >> sh) == (plo >> sh);
 }
 
-__global__ void ks_topk_hist(StepView v, int d) {
+// passes d >= 1 over the collected list
+__global__ void __launch_bounds__(256) ks_topk_hist(StepView v, int d) {
   if (!v.ss->stage_on || v.ss->topk_digit == 8) return;
   const long long n = v.ss->topk_live;
   const uint64_t phi = v.ss->topk_hi, plo = v.ss->topk_lo;
@@ -968,74 +1349,118 @@ __global__ void ks_topk_hist(StepView v, int d) {
   }
 }
 
-// one block: the digit holding the k-th remaining key; keys below it are in
+// one block: the digit holding the k-th remaining key (parallel prefix over
+// the 65536 bins); a digit whose bucket is taken whole ends the search
 __global__ void __launch_bounds__(1024) ks_topk_select(StepView v, int d) {
-  if (!v.ss->stage_on || v.ss->topk_digit == 8) return;
   __shared__ long long part[1024];
-  const int per = kTopkBins / 1024;
+  __shared__ long long wsum[32];
+  if (!v.ss->stage_on || v.ss->topk_digit == 8) return;
+  constexpr int per = kTopkBins / 1024;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   long long sum = 0;
-  for (int i = 0; i < per; ++i) sum += v.tk_hist[threadIdx.x * per + i];
-  part[threadIdx.x] = sum;
+  for (int i = 0; i < per; ++i) sum += v.tk_hist[t * per + i];
+  // inclusive block scan of the per-thread sums
+  long long x = sum;
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[w] = x;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    long long k = v.ss->topk_krem;
-    long long cum = 0;
-    int g = kTopkBins - 1;
-    bool found = false;
-    for (int t = 0; t < 1024 && !found; ++t) {
-      if (cum + part[t] < k) { cum += part[t]; continue; }
-      for (int i = 0; i < per; ++i) {
-        const long long hc = v.tk_hist[t * per + i];
-        if (cum + hc >= k) { g = t * per + i; found = true; break; }
-        cum += hc;
-      }
+  if (w == 0) {
+    long long y = wsum[lane];
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long z = __shfl_up_sync(0xffffffffu, y, o);
+      if (lane >= o) y += z;
     }
-    if (!found) {  // fewer than k keys in total: take everything (prefix = max)
-      v.ss->topk_hi = ~0ull;
-      v.ss->topk_lo = ~0ull;
-      v.ss->topk_digit = 8;
-    } else {
-      v.ss->topk_krem = k - cum;
-      if (d < 4) v.ss->topk_hi |= static_cast<uint64_t>(g) << (48 - 16 * d);
-      else v.ss->topk_lo |= static_cast<uint64_t>(g) << (48 - 16 * (d - 4));
+    wsum[lane] = y;
+  }
+  __syncthreads();
+  const long long incl = x + (w ? wsum[w - 1] : 0);
+  part[t] = incl;
+  __syncthreads();
+  const long long k = v.ss->topk_krem;
+  const long long excl = incl - sum;
+  if (t == 1023 && incl < k) {  // fewer than k keys in total: take every candidate
+    v.ss->topk_hi = ~0ull;
+    v.ss->topk_lo = ~0ull;
+    v.ss->topk_digit = 8;
+  }
+  if (excl < k && k <= incl) {
+    long long cum = excl;
+    for (int i = 0; i < per; ++i) {
+      const long long hc = v.tk_hist[t * per + i];
+      if (cum + hc >= k) {
+        const uint64_t g = static_cast<uint64_t>(t * per + i);
+        const long long kr = k - cum;
+        uint64_t hi = v.ss->topk_hi, lo = v.ss->topk_lo;
+        if (d < 4) hi |= g << (48 - 16 * d);
+        else lo |= g << (48 - 16 * (d - 4));
+        if (hc == kr) {  // the whole bucket is in: close every lower digit
+          if (d < 4) {
+            hi |= (48 - 16 * d) ? ((1ull << (48 - 16 * d)) - 1) : 0ull;
+            lo = ~0ull;
+          } else {
+            const int sh = 48 - 16 * (d - 4);
+            lo |= sh ? ((1ull << sh) - 1) : 0ull;
+          }
+          v.ss->topk_digit = 8;
+        }
+        v.ss->topk_hi = hi;
+        v.ss->topk_lo = lo;
+        v.ss->topk_krem = kr;
+        break;
+      }
+      cum += hc;
     }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < kTopkBins; i += blockDim.x) v.tk_hist[i] = 0;
+  for (int i = t; i < kTopkBins; i += blockDim.x) v.tk_hist[i] = 0;
 }
 
 // the (vinv, key) <= threshold entries: exactly min(limit, live) of them
-__global__ void ks_topk_gather(StepView v) {
+__global__ void __launch_bounds__(256) ks_topk_gather(StepView v) {
   if (!v.ss->stage_on) return;
   const long long n = v.ss->topk_live;
   const uint64_t thi = v.ss->topk_hi, tlo = v.ss->topk_lo;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t hi = v.tk_vinv[i], lo = v.tk_key[i];
-    const bool in = hi < thi || (hi == thi && lo <= tlo);
-    const long long p = warp_append(reinterpret_cast<unsigned long long *>(&v.ss->topk_n), in);
+  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x; i0 < n; i0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = i0 + threadIdx.x;
+    bool in = false;
+    if (i < n) {
+      const uint64_t hi = v.tk_vinv[i], lo = v.tk_key[i];
+      in = hi < thi || (hi == thi && lo <= tlo);
+    }
+    const long long p = block_append(reinterpret_cast<unsigned long long *>(&v.ss->topk_n), in);
     if (in) v.tk_sel[p] = static_cast<int32_t>(i);
   }
 }
 
-// rank the <= limit selected keys, then the ordered staging loop (one block)
+// rank the <= limit selected keys; look their pending / cached state up in
+// parallel; then the ordered staging loop over those flags (one block)
 __global__ void __launch_bounds__(1024) ks_stage_finish(CacheView c, StepView v, int64_t limit) {
   if (!v.ss->stage_on) return;
   extern __shared__ unsigned char smem_raw[];
-  const long long m = v.ss->topk_n;
+  const long long m = v.ss->topk_n < limit ? v.ss->topk_n : limit;
   uint64_t *hi = reinterpret_cast<uint64_t *>(smem_raw);
   uint64_t *lo = hi + limit;
   int32_t *ord = reinterpret_cast<int32_t *>(lo + limit);
+  int32_t *kpos = ord + limit;
   for (long long i = threadIdx.x; i < m; i += blockDim.x) {
     const int32_t p = v.tk_sel[i];
     hi[i] = v.tk_vinv[p];
     lo[i] = v.tk_key[p];
   }
   __syncthreads();
-  // rank by counting (keys are distinct)
-  for (long long i = threadIdx.x; i < m; i += blockDim.x) {
+  for (long long i = threadIdx.x; i < m; i += blockDim.x) {  // rank by counting (keys are distinct)
     long long r = 0;
     for (long long j = 0; j < m; ++j) r += (hi[j] < hi[i] || (hi[j] == hi[i] && lo[j] < lo[i])) ? 1 : 0;
     ord[r] = static_cast<int32_t>(i);
+  }
+  __syncthreads();
+  for (long long r = threadIdx.x; r < m; r += blockDim.x) {  // -1: pending or cached (skipped)
+    const uint64_t key = lo[ord[r]];
+    const int64_t kp = k_find(c, key);
+    kpos[r] = (kp < 0 || c.kflag[kp] || h_find(c, key) >= 0) ? -1 : static_cast<int32_t>(kp);
   }
   __syncthreads();
   if (threadIdx.x != 0) return;
@@ -1043,14 +1468,12 @@ __global__ void __launch_bounds__(1024) ks_stage_finish(CacheView c, StepView v,
   long long room = sc->budget - sc->used;
   long long staged = 0, pend = sc->pending;
   for (long long r = 0; r < m; ++r) {
-    const uint64_t key = lo[ord[r]];
-    const int64_t kp = k_find(c, key);
-    if (kp < 0 || c.kflag[kp] || h_find(c, key) >= 0) continue;
+    if (kpos[r] < 0) continue;
     const long long size = v.S;
     if (size > room) continue;
     if (pend >= c.pend_cap) break;
-    c.pend[pend++] = key;
-    c.kflag[kp] = 1;
+    c.pend[pend++] = lo[ord[r]];
+    c.kflag[kpos[r]] = 1;
     room -= size;
     ++staged;
     if (staged >= limit) break;
@@ -1060,7 +1483,7 @@ __global__ void __launch_bounds__(1024) ks_stage_finish(CacheView c, StepView v,
 }
 
 // sketch age (cache.py:128-136): halve, prune below prune_below
-__global__ void ks_age(CacheView c, StepView v) {
+__global__ void __launch_bounds__(256) ks_age(CacheView c, StepView v) {
   if (v.ss->err) return;
   long long dead = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < c.kcap; i += (int64_t)gridDim.x * blockDim.x) {
@@ -1076,11 +1499,8 @@ __global__ void ks_age(CacheView c, StepView v) {
       c.kval[i] = x;
     }
   }
-  dead = warp_sum(dead);
-  if ((threadIdx.x & 31) == 0 && dead) {
-    atomicAdd(reinterpret_cast<unsigned long long *>(&c.sc->sketch_live), (unsigned long long)(-dead));
-    atomicAdd(reinterpret_cast<unsigned long long *>(&c.sc->sketch_tomb), (unsigned long long)dead);
-  }
+  block_add(reinterpret_cast<unsigned long long *>(&c.sc->sketch_live), -dead);
+  block_add(reinterpret_cast<unsigned long long *>(&c.sc->sketch_tomb), dead);
 }
 
 }  // namespace stp
@@ -1094,6 +1514,7 @@ struct fx_step {
   StepView v{};
   StepScalars *ss_base = nullptr;  // [slots + 1]: per in-flight batch, then the global block
   uint64_t *ckey_base = nullptr;   // [slots * max_nnz]
+  double *cest_base = nullptr;     // [slots * max_nnz]
   int32_t slots = 1;
   int64_t max_nnz = 0, max_bags = 0;
   int64_t scap = 0;
@@ -1101,6 +1522,8 @@ struct fx_step {
   size_t cub_bytes = 0;
   std::vector<void *> allocs;
   int chain_smem = 0;
+  int code_smem = 0;
+  int stream_smem = 0;
   int stage_smem = 0;
   int64_t stage_limit_cap = 0;
 };
@@ -1121,14 +1544,6 @@ int64_t pow2_ge(int64_t x) {
   int64_t p = 1024;
   while (p < x) p <<= 1;
   return p;
-}
-
-__global__ void k_init_dedup(StepView v) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < v.dcap; i += (int64_t)gridDim.x * blockDim.x) {
-    v.dkey[i] = kEmpty;
-    v.dent[i] = DEnt{0, INT_MAX, -1, -1};
-    v.dfraw[i] = INT_MAX;
-  }
 }
 
 __global__ void k_lru_sortkeys(CacheView c, long long *keys, int32_t *vals, long long free_key) {
@@ -1189,6 +1604,7 @@ int select_slot(fx_step *s, int32_t slot, StepView *v) {
   v->ss = s->ss_base + slot;
   v->gs = s->ss_base + s->slots;
   v->ckey = s->ckey_base + static_cast<int64_t>(slot) * s->max_nnz;
+  v->cest = s->cest_base + static_cast<int64_t>(slot) * s->max_nnz;
   v->q = s->cache->q;
   return FX_OK;
 }
@@ -1250,7 +1666,15 @@ int fx_step_create(fx_step **out, fx_cache *cache, int64_t max_nnz, int64_t max_
   rc = rc ? rc : salloc(s, &v.rj_end, SC + 1);
   rc = rc ? rc : salloc(s, &v.acc, N);
   rc = rc ? rc : salloc(s, &v.rank, N);
-  rc = rc ? rc : salloc(s, &v.accslot, N);
+  rc = rc ? rc : salloc(s, &v.code, N + kChunk);
+  rc = rc ? rc : salloc(s, &v.bsum, N / 32 + 2);
+  rc = rc ? rc : salloc(s, &v.hrank, SC);
+  rc = rc ? rc : salloc(s, &v.levels, 256);
+  rc = rc ? rc : salloc(s, &v.aslot, N);
+  rc = rc ? rc : salloc(s, &v.akey, N);
+  rc = rc ? rc : salloc(s, &v.claim, N);
+  rc = rc ? rc : salloc(s, &v.dC, v.dcap);
+  rc = rc ? rc : salloc(s, &s->cest_base, static_cast<size_t>(slots) * N);
   rc = rc ? rc : salloc(s, &v.accj, N);
   rc = rc ? rc : salloc(s, &v.tk_key, v.tk_cap);
   rc = rc ? rc : salloc(s, &v.tk_vinv, v.tk_cap);
@@ -1292,7 +1716,6 @@ int fx_step_create(fx_step **out, fx_cache *cache, int64_t max_nnz, int64_t max_
   }
   s->allocs.push_back(s->cub_tmp);
   cudaMemset(s->ss_base, 0, (slots + 1) * sizeof(StepScalars));
-  k_init_dedup<<<grid_for(v.dcap, 256), 256>>>(v);
   cudaMemset(v.sflag, 0xff, SC * 4);  // no slot carries epoch -1
   cudaMemset(v.tk_hist, 0, kTopkBins * 4);
   const int64_t nblk = (N + kFine - 1) / kFine;
@@ -1303,8 +1726,21 @@ int fx_step_create(fx_step **out, fx_cache *cache, int64_t max_nnz, int64_t max_
     return FX_E_CONFIG;
   }
   cudaFuncSetAttribute(ks_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, s->chain_smem > 0 ? s->chain_smem : 8);
+  s->code_smem = static_cast<int>(N / 32 + 2);
+  if (s->code_smem > 227 * 1024) {
+    set_error("fx_step_create: max_nnz too large for the chain's shared-memory block maxima");
+    fx_step_destroy(s);
+    return FX_E_CONFIG;
+  }
+  cudaFuncSetAttribute(ks_chain_codes, cudaFuncAttributeMaxDynamicSharedMemorySize, s->code_smem);
+  {
+    const int64_t need = ((N / 32 + 2 + 15) & ~15ll) + kRing;
+    s->stream_smem = need + 1024 <= 227 * 1024 ? static_cast<int>(need) : 0;  // else the global-memory chain
+    if (s->stream_smem)
+      cudaFuncSetAttribute(ks_chain_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, s->stream_smem);
+  }
   s->stage_limit_cap = stage_limit_cap > 0 ? stage_limit_cap : 64;
-  s->stage_smem = static_cast<int>(s->stage_limit_cap * (8 + 8 + 4));
+  s->stage_smem = static_cast<int>(s->stage_limit_cap * (8 + 8 + 4 + 4));
   cudaFuncSetAttribute(ks_stage_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, s->stage_smem);
   rc = cuda_check(cudaDeviceSynchronize(), "fx_step_create");
   if (rc) {
@@ -1345,6 +1781,10 @@ int fx_step_start(fx_step *s, int32_t slot, const int32_t *bag_table, const void
     return FX_E_CONFIG;
   }
   ks_begin<<<1, 1, 0, st>>>(c, v, nnz);
+  // dedup table reset: a memset beats clearing the claimed slots one by one
+  cudaMemsetAsync(v.dkey, 0xff, v.dcap * sizeof(uint64_t), st);
+  cudaMemsetAsync(v.dent, 0, v.dcap * sizeof(DEnt), st);
+  if (threshold > 0) cudaMemsetAsync(v.dfraw, 0, v.dcap * sizeof(int32_t), st);
   ks_sketch_collect<<<grid_for(c.kcap, 256), 256, 0, st>>>(c, v);
   ks_sketch_clear<<<grid_for(c.kcap, 256), 256, 0, st>>>(c, v);
   ks_sketch_reinsert<<<grid_for(c.kcap, 256), 256, 0, st>>>(c, v);
@@ -1358,9 +1798,12 @@ int fx_step_start(fx_step *s, int32_t slot, const int32_t *bag_table, const void
       ks_dedup<int64_t><<<g, 256, 0, st>>>(v, bag_table, static_cast<const int64_t *>(indices), offsets, sm_start,
                                           n_bags);
   }
+  const int nn = static_cast<int>(nnz > 0 ? nnz : 1);
+  size_t cb = s->cub_bytes;
+  cub::DeviceSelect::If(s->cub_tmp, cb, v.claim, v.uniq, reinterpret_cast<int64_t *>(&v.ss->n_uniq), nn, NonNeg(),
+                        st);
   // ranker.py:218-222 order: validate, apply_pending, (admission check: host), probes
   ks_apply_pending<<<1, 32, 0, st>>>(c, v);
-  const int nn = static_cast<int>(nnz > 0 ? nnz : 1);
   cudaMemsetAsync(v.cand_by_first, 0xff, static_cast<size_t>(nn) * 4, st);
   cudaMemsetAsync(v.hit_by_last, 0xff, static_cast<size_t>(nn) * 4, st);
   ks_probe<<<grid_for(nn, 256), 256, 0, st>>>(c, v, threshold > 0 ? 1 : 0);
@@ -1368,7 +1811,6 @@ int fx_step_start(fx_step *s, int32_t slot, const int32_t *bag_table, const void
   ks_bag_plan<<<grid_for(n_bags > 0 ? n_bags * 32 : 32, 256), 256, 0, st>>>(v, offsets, sm_start, n_bags, threshold,
                                                                             hits_bag, pd_groups, pd_rows, raw_rows);
   if (threshold > 0) ks_cand_scatter_raw<<<grid_for(nn, 256), 256, 0, st>>>(v);
-  size_t cb = s->cub_bytes;
   // candidates in first raw-occurrence order; hit slots in last-ordinal order
   cub::DeviceSelect::If(s->cub_tmp, cb, v.cand_by_first, v.cand, reinterpret_cast<int64_t *>(&v.ss->n_cand), nn,
                         NonNeg(), st);
@@ -1382,7 +1824,6 @@ int fx_step_start(fx_step *s, int32_t slot, const int32_t *bag_table, const void
                         static_cast<int>(SC), qk, st);
   ks_queue_append_hits<<<grid_for(nn, 256), 256, 0, st>>>(v);
   cudaMemcpyAsync(cc->q, v.qnew, SC * 4, cudaMemcpyDeviceToDevice, st);
-  ks_dedup_reset<<<grid_for(nn, 256), 256, 0, st>>>(v);
   FX_LAUNCH_CHECK("fx_step_start");
   return FX_OK;
 }
@@ -1399,7 +1840,7 @@ int fx_step_offer(fx_step *s, int32_t slot, void *stream) {
   const int64_t SC = s->scap;
   const int nn = static_cast<int>(s->max_nnz);
   size_t cb = s->cub_bytes;
-  ks_offer_prep<<<grid_for(nn, 256), 256, 0, st>>>(c, v, nn);
+  ks_offer_prep<<<grid_for(nn, 256), 256, 0, st>>>(c, v, nn, s->slots == 1 ? 1 : 0);
   cub::DeviceSelect::Flagged(s->cub_tmp, cb, cub::CountingInputIterator<int32_t>(0), v.pres, v.cidx,
                              reinterpret_cast<int64_t *>(&v.ss->n_off), nn, st);
   ks_cand_est<<<grid_for(nn, kFine), kFine, 0, st>>>(v);
@@ -1407,15 +1848,19 @@ int fx_step_offer(fx_step *s, int32_t slot, void *stream) {
   ks_victim_est<<<grid_for(SC, 256), 256, 0, st>>>(c, v, SC);
   cub::DeviceSelect::Flagged(s->cub_tmp, cb, cub::CountingInputIterator<int32_t>(0), v.hardf, v.hard,
                              reinterpret_cast<int64_t *>(&v.ss->n_hard), static_cast<int>(SC), st);
+  ks_levels<<<1, 1024, 0, st>>>(v, s->stream_smem > 0 ? 1 : 0);
+  ks_cand_codes<<<grid_for(nn, 256), 256, 0, st>>>(v);
+  if (s->stream_smem > 0) ks_chain_stream<<<1, 1024, s->stream_smem, st>>>(v);
+  ks_chain_codes<<<1, 1024, s->code_smem, st>>>(v);
   ks_chain<<<1, 1024, s->chain_smem, st>>>(v);
   ks_accept_flags<<<grid_for(nn, 256), 256, 0, st>>>(v, nn);
   cub::DeviceScan::ExclusiveSum(s->cub_tmp, cb, v.acc, v.rank, nn, st);
   cudaMemsetAsync(v.qnew, 0xff, SC * 4, st);
-  ks_apply<<<grid_for(static_cast<int64_t>(nn) * 32, 256), 256, 0, st>>>(c, v);
+  ks_apply<<<grid_for(nn, 256), 256, 0, st>>>(c, v);
   ks_queue_survivors<<<grid_for(SC, 256), 256, 0, st>>>(c, v);
   ks_seq_offer<<<1, 1, 0, st>>>(c, v);
-  ks_seq_rows<<<grid_for(static_cast<int64_t>(nn) * 32, 256), 256, 0, st>>>(c, v);
   ks_offer_finish<<<1, 1, 0, st>>>(c, v);
+  ks_copy_rows<<<grid_for(static_cast<int64_t>(nn) * (v.dim / 4 + 1), 256), 256, 0, st>>>(c, v);
   ks_queue_commit<<<grid_for(SC, 256), 256, 0, st>>>(v, SC);
   ks_index_clear<<<grid_for(c.hcap, 256), 256, 0, st>>>(c, v);
   ks_index_fill<<<grid_for(SC, 256), 256, 0, st>>>(c, v);
@@ -1435,9 +1880,11 @@ int fx_step_maintain(fx_step *s, int32_t slot, int64_t stage_limit, int32_t do_a
   }
   ks_stage_begin<<<1, 1, 0, st>>>(c, v, stage_limit);
   if (stage_limit > 0) {
+    ks_topk_hist0<<<grid_for(c.kcap, 256), 256, 0, st>>>(c, v);
+    ks_topk_select<<<1, 1024, 0, st>>>(v, 0);
     ks_topk_collect<<<grid_for(c.kcap, 256), 256, 0, st>>>(c, v);
-    for (int d = 0; d < 8; ++d) {
-      ks_topk_hist<<<grid_for(c.kcap, 256), 256, 0, st>>>(v, d);
+    for (int d = 1; d < 8; ++d) {
+      ks_topk_hist<<<grid_for(4 * 65536, 256), 256, 0, st>>>(v, d);
       ks_topk_select<<<1, 1024, 0, st>>>(v, d);
     }
     ks_topk_gather<<<grid_for(c.kcap, 256), 256, 0, st>>>(v);

@@ -37,6 +37,8 @@ from .errors import CapacityError, ConfigError, InvariantError, LookupValidation
 from .pooling import PoolingOp, op_code, pool_flat
 from .requests import Batch, LookupRequest
 from .store import Deployment, make_segments
+
+_SEG_OUT = 5  # fx_segment.out, in int64 words
 from .routing import RoutingTable
 
 
@@ -215,6 +217,8 @@ class Ranker:
         self._inflight: list = []     # started, not yet offered (pipeline_depth > 1)
         self._epoch_ev = None
         self._fast_layouts: dict = {}
+        self._fast_segs: dict = {}
+        self._views = None
 
     def _mark(self, name):
         if self.profile:
@@ -308,10 +312,7 @@ class Ranker:
         side.wait_stream(cur)
         with torch.cuda.stream(side):
             if feature_shape is not None:
-                from .engine import CsrBatch, LookupEngine
-                if self._engine is None:
-                    self._engine = LookupEngine(self.deployment, dev)
-                self._engine.pool(CsrBatch(lay.indices, lay.offsets, ft, fo, B), out=out, check=False)
+                self._pool_sample_major(lay, out, ft, fo, B)
             elif n_bags:
                 self._pool_fused(lay, n_bags, out=out)
         cnt = torch.empty((4, max(n_bags, 1)), dtype=torch.int32, device=dev)
@@ -321,6 +322,32 @@ class Ranker:
                    lay=lay, host=host, feature_shape=feature_shape)
         self._inflight.append(rec)
         return rec
+
+    def _pool_sample_major(self, lay: CsrLayout, out: torch.Tensor, ft, fo, B: int) -> None:
+        """One K4 launch writing out[B, F*D] sample-major (out[s, f*D:(f+1)*D]
+        = bag (s, f)). The segment descriptors live on the device per batch
+        shape; only their output pointers are patched per call, by a device
+        op (no host->device copy, so the host never waits for the GPU)."""
+        key = (ft, fo, B)
+        ent = self._fast_segs.get(key)
+        F = len(ft)
+        D = out.shape[1] // F
+        if ent is None:
+            segs = []
+            for f, (t, op) in enumerate(zip(ft, fo)):
+                tab, start, end, _, _ = self._table_shard[t]
+                segs.append(_lib.FxSegment(tab.data_ptr(), start, end, f * B, (f + 1) * B, f * D * 4, F * D,
+                                           tab.stride(0), D, op_code(op)))
+            seg = make_segments(segs, self.device)
+            off = seg.view(torch.int64).view(F, _lib.SEGMENT_BYTES // 8)[:, _SEG_OUT].clone()
+            ent = (seg, off)
+            self._fast_segs[key] = ent
+        seg, off = ent
+        seg.view(torch.int64).view(F, _lib.SEGMENT_BYTES // 8)[:, _SEG_OUT] = off + out.data_ptr()
+        _lib.check(_lib.lib.fx_gather_pool(seg.data_ptr(), F, D, lay.indices.data_ptr(), _lib.idx_type_of(lay.indices),
+                                           lay.offsets.data_ptr(), F * B, _lib.FX_OUT_F32, None,
+                                           self._status.err.data_ptr(), _lib.FX_E_LOOKUP_VALIDATION,
+                                           self._status.code.data_ptr(), _lib.stream_ptr()), "gather_pool")
 
     def _fast_finish(self) -> dict:
         """Offers + maintenance of the oldest in-flight batch (ranker.py:
@@ -357,7 +384,9 @@ class Ranker:
         cur.wait_stream(self._pool_stream)
         ev1 = torch.cuda.Event(enable_timing=True)
         ev1.record(cur)
-        rec["snap"] = torch.cat([step.scalars_tensor(slot), c.scalars_tensor()])
+        if self._views is None or self._views[0] is not step:
+            self._views = (step, [step.scalars_tensor(k) for k in range(step.n_slots)], c.scalars_tensor())
+        rec["snap"] = torch.cat([self._views[1][slot], self._views[2]])
         rec["ev1"] = ev1
         rec["level"] = self._last_level
         self._pending.append(rec)
@@ -432,7 +461,7 @@ class Ranker:
         # (the fused step cannot grow it mid-stream)
         live = int(snaps[-1][ns + _SC.index("sketch_live")])
         st = self._step
-        if st is not None and not self._inflight and (live + 2 * st.max_nnz) * 10 > self.cache.capacity()["sketch"] * 6:
+        if st is not None and not self._inflight and (live + 1.5 * st.max_nnz) * 10 > self.cache.capacity()["sketch"] * 7:
             self.cache._reserve_sketch(2 * st.max_nnz + live)
             if self.cache.capacity()["sketch"] > st.tk_cap:
                 self._step = None

@@ -37,6 +37,7 @@ def main():
     ap.add_argument("--warm", type=int, default=3)
     ap.add_argument("--depth", type=int, default=1)
     ap.add_argument("--fused", type=int, default=1)
+    ap.add_argument("--sketch", type=int, default=8_000_000, help="AdaptiveCache sketch_capacity (table = 2x, pow2)")
     a = ap.parse_args()
     torch.cuda.set_device(0)
     thr = None if a.threshold == "none" else int(a.threshold)
@@ -68,7 +69,7 @@ def main():
             rows_c = int(T * N * frac)
             budget = rows_c * D * 4
             cache = C.AdaptiveCache(budget, admission=a.admission, max_dim=D, slot_capacity=rows_c + 1,
-                                    sketch_capacity=8 * B * T * L)
+                                    sketch_capacity=a.sketch)
             rk = Ranker(dep, P.build_routing(metas, placement), None,
                         RankerParams(pushdown_threshold=thr, admit_per_batch=64, pipeline_depth=a.depth),
                         cache=cache, policy=C.CachePolicy(C.MemoryModel(budget + 1_000 + B, 1_000, 1)),
@@ -92,7 +93,9 @@ def main():
                               "bags_per_s": B * T / (ms / 1e3), "hit_rate": sum(hr) / len(hr),
                               "latency_ms": [round(m.latency * 1e3, 3) for m in rk.batch_metrics[a.warm:]],
                               "last_step": {k: sc.get(k) for k in ("n_uniq", "n_cand", "n_off", "n_hard", "n_rej",
-                                                                   "n_acc", "n_ev", "mode", "F")},
+                                                                   "n_acc", "n_ev", "mode", "F", "n_levels",
+                                                                   "chain_cycles")},
+                              "capacity": cache.capacity(),
                               "fused": bool(a.fused), "threshold": thr}), flush=True)
             del rk, cache
             torch.cuda.empty_cache()
