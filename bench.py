@@ -4,12 +4,19 @@ pooled lookups/sec and achieved HBM GB/s vs roofline).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N=1 workload = BASELINE.json configs[1]: Criteo-Kaggle-shaped, 26 tables
-(real cardinalities) x dim 128 fp32, batch 4096, pooling factor U[1,40],
-Zipf alpha 1.05, single B200. A step = one batch through
-the fused gather+pool (validation included). N>1 (torchrun, one rank per
-GPU) runs the cfg2 tables sharded across the GPUs with the fused NVLink
-exchange (see run_sharded), weak scaling, max-over-ranks device time.
+N=1 workload = the largest single-GPU configuration of BASELINE.json,
+configs[2]: 32 tables x 10M rows x dim 128 fp32
+(163.84 GB in HBM), batch 4096, pooling 20, Zipf alpha 1.0, hot-row cache of
+2% of all rows with the reference semantics (threshold None, sketch
+admission, 64 staged admissions per batch, adaptive maintenance with the
+memory model pinned). A step = one batch through the whole Ranker pipeline
+(Ranker.execute_csr): validation, dedup, cache probe, plan, the fused
+gather+pool (K4), ordered offers and maintenance (`run_ranker`).
+`--config cfg2` (configs[1], Criteo-Kaggle-shaped, K4 alone) and the cold
+control are extra lines. N>1 (torchrun, one rank per GPU) defaults to cfg4r
+(100 tables x 1M rows, table-wise) sharded across the GPUs with the fused
+NVLink exchange (see run_sharded), weak scaling, max-over-ranks device
+time.
 
 Prints ONE JSON line on rank 0.
 """
@@ -119,7 +126,7 @@ def committed_traffic(config_name):
 
 
 def build_cfg(cfg_key, rank, n_batches, alpha=None, table_rows=None):
-    from paper_2410_12794_b200.workload import CONFIGS, DlrmBatchGen
+    from flexemb_workload import CONFIGS, DlrmBatchGen
     cfg = dict(CONFIGS[cfg_key])
     if table_rows is not None:
         cfg["table_rows"] = (table_rows,) * len(cfg["table_rows"])
@@ -152,39 +159,70 @@ def cpu_baseline_port(hb, cfg, seconds_target=10.0):
                       "tables row-reduced to 20K rows (per-row cost is table-size independent)"}
 
 
+def ranker_config(cfg, cache_frac, extra=None):
+    """The `config` dict both arms print for the Ranker (cfg3) workload."""
+    d = {"workload": cfg["name"] + f"-cache{cache_frac * 100:g}pct", "global_batch": cfg["batch"],
+         "per_gpu_batch": cfg["batch"], "pooling": cfg["pooling"] if not isinstance(cfg["pooling"], tuple)
+         else list(cfg["pooling"]), "alpha": cfg["alpha"], "dim": cfg["dim"], "tables": len(cfg["table_rows"]),
+         "rows_per_table": cfg["table_rows"][0], "cache_rows_frac": cache_frac, "pushdown_threshold": None,
+         "admission": "sketch", "admit_per_batch": 64, "pipeline": "Ranker.execute_csr (validate, dedup, probe, "
+         "plan, gather+pool, offers, maintenance)"}
+    if extra:
+        d.update(extra)
+    return d
+
+
+REF_ROWS = 20_000  # row-reduced replica for the reference's host tables
+
+
+def ref_baseline(cfg, cache_frac, procs, samples_per_step, steps, warmup):
+    """The unmodified reference (oracle/_ref/embserve) over `procs` forked
+    host processes; returns (bags/s, per-step wall ms, cores, sample text)."""
+    from oracle import ref_arm
+    if not ref_arm.available():
+        return None
+    B, L = cfg["batch"], cfg["pooling"] if not isinstance(cfg["pooling"], tuple) else cfg["pooling"][0]
+    T = len(cfg["table_rows"])
+    t0 = time.perf_counter()
+    res = ref_arm.run_parallel(procs, T, REF_ROWS, cfg["dim"], B, L, cfg["alpha"], cache_frac, samples_per_step,
+                               steps, warmup)
+    wall = time.perf_counter() - t0
+    bags = sum(b for r, _ in res for b, _ in r)
+    busy = max(sum(t for _, t in r) for r, _ in res)
+    step_ms = [1000 * max(r[i][1] for r, _ in res) for i in range(steps)]
+    sample = (f"{procs} forked process(es) x {steps} timed steps (after {warmup} warm-up steps) of a "
+              f"{samples_per_step}-lookup batch ({samples_per_step * T} bags) each, through the unmodified "
+              f"reference (oracle/_ref copy of embserve: Ranker.run_trace with VirtualTransport, "
+              f"AdaptiveCache {cache_frac * 100:g}% of rows, threshold None, sketch admission, admit 64); "
+              f"tables row-reduced to {REF_ROWS} rows per table (indices mod rows; steady-state reference "
+              f"rate measured within 10% at 20K vs 200K rows, profiles/r2_reference_rows.json); "
+              f"{wall:.0f}s wall")
+    return bags / busy, statistics.median(step_ms), procs, sample
+
+
 def run_reference(args, rank, world):
-    """--impl reference: the reference's CPU implementation of the path
-    (oracle port of Ranker.execute_batch) on all host cores, rank 0 only."""
+    """--impl reference: the reference's own CPU implementation of the path
+    (the unmodified embserve Ranker, copied into oracle/_ref by build()) on
+    all host cores, rank 0 only; this process never imports the product
+    package (libflexemb.so stays unloaded)."""
     if rank != 0:
         return
-    from oracle.cpu_pipeline import ParallelPort, RefPipelinePort
-    cfg, batches = build_cfg("cfg2", 0, 1)
-    hb = batches[0]
-    port = RefPipelinePort(0, cfg["table_rows"], cfg["dim"], row_cap=20_000)
-    pp = ParallelPort(port, hb)
-    procs = pp.procs
-    per_proc = 128  # ~3,300 bags per process per step (~50-100 ms of CPU work)
-    for i in range(args.warmup):
-        pp.step(per_proc, offset=i)
-    rates, walls = [], []
-    for i in range(args.steps):
-        r, wall = pp.step(per_proc, offset=7 * i)
-        rates.append(r)
-        walls.append(wall)
-    pp.close()
-    value = statistics.median(rates)
-    F = len(hb.feature_tables)
+    cfg_key = args.config or "cfg3"
+    cfg, _ = build_cfg(cfg_key, 0, 0, args.alpha)
+    procs = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    r = ref_baseline(cfg, args.cache, procs, samples_per_step=32, steps=args.steps, warmup=args.warmup)
+    assert not any(k.startswith("paper_2410_12794_b200") for k in sys.modules), "reference arm loaded the product"
+    if r is None:
+        emit({"impl": "reference", "unavailable": "oracle/_ref/embserve missing (run __graft_entry__.build())"}, args)
+        return
+    value, step_ms, cores, sample = r
     line = {
         "impl": "reference", "metric": "pooled lookups/s (bags/s)", "value": value, "unit": "pooled lookups/s",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1000 * statistics.median(walls), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32 rows, f64 accumulate", "data": "synthetic",
-        "config": {"workload": cfg["name"], "global_batch": cfg["batch"], "pooling": list(cfg["pooling"]),
-                   "alpha": cfg["alpha"], "dim": cfg["dim"], "tables": len(cfg["table_rows"])},
-        "cpu_baseline": {"value": value, "unit": "pooled lookups/s", "cores": procs, "kind": "port",
-                         "sample": f"per step {procs} forked processes x {per_proc} samples x {F} features "
-                                   "of a cfg2 batch (oracle/cpu_pipeline.py restatement of Ranker.execute_batch, "
-                                   "threshold 2, cache off, tables row-reduced to 20K rows)"},
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32 rows, f64 accumulate",
+        "data": "synthetic", "config": ranker_config(cfg, args.cache),
+        "cpu_baseline": {"value": value, "unit": "pooled lookups/s", "cores": cores, "kind": "reference",
+                         "sample": sample},
         "e2e": {"value": value, "unit": "pooled lookups/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     emit(line, args)
@@ -205,7 +243,11 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--config", default=None,
+                    help="workload: cfg3 (N=1 default: full Ranker pipeline with the cache), cfg2 / cfg1 (K4 "
+                         "alone), cfg4r (N>1 default), cfg4, cfg5")
+    ap.add_argument("--cache", type=float, default=0.02, help="cfg3: cache budget as a fraction of all rows")
+    ap.add_argument("--graph-step", type=int, default=0, help="cfg3: replay the Ranker step as a CUDA graph")
     ap.add_argument("--batches", type=int, default=4, help="distinct batches cycled through")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -219,7 +261,7 @@ def main():
                     help="N>1 row-wise partial format (f32 = the reference's PartialResult semantics)")
     ap.add_argument("--graph", type=int, default=0,
                     help="N=1: capture this many batch launches per CUDA graph and time graph replays")
-    ap.add_argument("--replicate-rows", type=int, default=1_000_000,
+    ap.add_argument("--replicate-rows", type=int, default=None,
                     help="N>1 table-wise: replicate tables with <= this many rows on every rank (hybrid "
                          "placement: small tables data-parallel, big tables table-sharded); 0 = pure table-wise")
     ap.add_argument("--threshold", type=int, default=0,
@@ -233,6 +275,10 @@ def main():
     args.warmup = max(args.warmup, 3)
 
     rank, world, local = _env_int("RANK", 0), _env_int("WORLD_SIZE", 1), _env_int("LOCAL_RANK", 0)
+    if args.config is None:
+        args.config = "cfg3" if world == 1 else "cfg4r"
+    if args.replicate_rows is None:
+        args.replicate_rows = 1_000_000 if args.config == "cfg2" else 0
     if args.impl == "reference":
         return run_reference(args, rank, world)
 
@@ -248,6 +294,8 @@ def main():
     from paper_2410_12794_b200.engine import CsrBatch, HostLookup, LookupEngine
     if world > 1:
         return run_sharded(args, rank, world, local)
+    if args.config == "cfg3":
+        return run_ranker(args, rank, world, local)
 
     cfg, host_batches = build_cfg(args.config, rank, args.batches, args.alpha, args.table_rows)
     dim = cfg["dim"]
@@ -403,6 +451,130 @@ def main():
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def run_ranker(args, rank, world, local):
+    """N=1 headline: cfg3 through the whole Ranker pipeline. `value` times K
+    consecutive distinct batches already in HBM through Ranker.execute_csr
+    (sync=False: the fused cache step + K4 on a side stream, no host sync);
+    `e2e` runs Ranker.stream_host (pinned host CSR in, pinned host pooled out,
+    H2D / step / D2H overlapped on three streams)."""
+    import torch
+    import paper_2410_12794_b200 as P
+    from paper_2410_12794_b200 import cache as C
+    from paper_2410_12794_b200.ranker import Ranker, RankerParams
+
+    n_timed = min(args.steps, 40)       # distinct timed batches (cycled beyond 40 steps)
+    n_dev = args.warmup + n_timed
+    cfg, host_batches = build_cfg(args.config, rank, n_dev + max(3, min(args.steps, 40)) + 3, args.alpha,
+                                  args.table_rows)
+    T, D, B = len(cfg["table_rows"]), cfg["dim"], cfg["batch"]
+    N = cfg["table_rows"][0]
+    metas = [P.TableMeta(t, n, D) for t, n in enumerate(cfg["table_rows"])]
+    placement = [P.ShardSpec(t, 0, n, 0) for t, n in enumerate(cfg["table_rows"])]
+    t0 = time.perf_counter()
+    dep = P.init_store(metas, placement, seed=0)
+    torch.cuda.synchronize()
+    init_s = time.perf_counter() - t0
+    rows_c = int(sum(cfg["table_rows"]) * args.cache)
+    budget = rows_c * D * 4
+    cache = C.AdaptiveCache(budget, admission="sketch", max_dim=D, slot_capacity=rows_c + 1,
+                            sketch_capacity=8_000_000)
+    rk = Ranker(dep, P.build_routing(metas, placement), None,
+                RankerParams(pushdown_threshold=None, admit_per_batch=64),
+                cache=cache, policy=C.CachePolicy(C.MemoryModel(budget + 1_000 + B, 1_000, 1)),
+                tracker=C.LoadTracker(16, 10 ** 9, 0))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+    dbs = [(torch.from_numpy(hb.indices).to(dev), torch.from_numpy(hb.offsets).to(dev))
+           for hb in host_batches[:n_dev]]
+    ft, fo = host_batches[0].feature_tables, host_batches[0].feature_ops
+    # warm-up: fills the cache to its steady state (first batches insert everything)
+    for i in range(args.warmup):
+        rk.execute_csr(*dbs[i], ft, fo, B, batch_id=i, sync=False)
+    rk.sync()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    sampler.start()
+    rk.k4_events = []
+    l0 = rk._step.launches()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    for i in range(args.steps):
+        rk.execute_csr(*dbs[args.warmup + i % n_timed], ft, fo, B, batch_id=args.warmup + i, sync=False)
+    ev1.record(stream)
+    ev1.synchronize()
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    launches = rk._step.launches() - l0 + len(rk.k4_events)
+    ms = ev0.elapsed_time(ev1)
+    k4_ms = [a.elapsed_time(b) for a, b in rk.k4_events]
+    rk.k4_events = None
+    rk.sync()
+    mets = rk.batch_metrics[args.warmup:]
+    hit = sum(m.cache_hits for m in mets) / max(1, sum(m.cache_hits + m.cache_misses for m in mets))
+    lat = sorted(m.latency * 1e3 for m in mets)
+    bags = B * T
+    value = bags * args.steps / (ms / 1e3)
+    tot_bytes = sum(algorithmic_bytes(host_batches[args.warmup + i % n_timed], D) for i in range(args.steps))
+    k4_mean = sum(k4_ms) / len(k4_ms)
+    k4_achieved = tot_bytes / args.steps / (k4_mean / 1e3) / 1e9
+    pipe_achieved = tot_bytes / (ms / 1e3) / 1e9
+    peak, peak_src = measured_peak()
+
+    e2e = None
+    if not args.no_e2e:
+        ksteps = max(3, min(args.steps, 40))
+        hbs = host_batches[n_dev:n_dev + ksteps + 3]
+        pinned = [(torch.from_numpy(hb.indices).pin_memory(), torch.from_numpy(hb.offsets).pin_memory())
+                  for hb in hbs]
+        for _ in rk.stream_host(pinned[:3], ft, fo, B, first_batch_id=10_000):
+            pass
+        torch.cuda.synchronize()
+        h2d = sum(ih.numel() * ih.element_size() + oh.numel() * 8 for ih, oh in pinned[3:])
+        d2h = 0
+        t0 = time.perf_counter()
+        for out_h in rk.stream_host(pinned[3:], ft, fo, B, first_batch_id=20_000):
+            d2h += out_h.numel() * 4
+        torch.cuda.synchronize()
+        e2e_s = time.perf_counter() - t0
+        e2e = {"value": bags * ksteps / e2e_s, "unit": "pooled lookups/s", "h2d_bytes_per_step": h2d // ksteps,
+               "d2h_bytes_per_step": d2h // ksteps, "steps": ksteps,
+               "api": "Ranker.stream_host (pinned host CSR -> pinned host pooled [B, F*D]; H2D, fused cache step "
+                      "+ gather/pool and D2H on three streams; wall clock)"}
+
+    cpu = None
+    if not args.no_cpu:
+        r = ref_baseline(cfg, args.cache, 1, samples_per_step=32, steps=8, warmup=8)
+        if r is not None:
+            cpu = {"value": r[0], "unit": "pooled lookups/s", "cores": 1, "kind": "reference", "sample": r[3]}
+
+    prof = os.path.join(ROOT, "profiles", "r2_cfg3_kernels.json")
+    shares = json.load(open(prof)) if os.path.exists(prof) else None
+    line = {
+        "metric": "pooled lookups/s (bags/s)", "value": value, "unit": "pooled lookups/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32 rows, f64 accumulate", "data": "synthetic",
+        "config": ranker_config(cfg, args.cache, {
+            "parallelism": "single", "l2": f"inputs larger than L2: {n_timed} distinct batches "
+            f"({tot_bytes / args.steps / 1e9:.2f} GB algorithmic bytes each) over {N * T * D * 4 / 1e9:.1f} GB of "
+            f"tables + {budget / 1e9:.2f} GB of cached rows", "init_store_s": round(init_s, 2)}),
+        "hit_rate": hit, "latency_ms": {"p50": lat[len(lat) // 2], "max": lat[-1]},
+        "roofline": {"bound": "hbm", "achieved": k4_achieved, "peak": peak, "unit": "GB/s",
+                     "frac": k4_achieved / peak, "traffic": None, "peak_source": peak_src,
+                     "kernel": "fx::k_pool_bulk (fused gather+pool K4, side stream of the Ranker step)",
+                     "bytes_per_launch": tot_bytes / args.steps, "launch_ms": k4_mean,
+                     "pipeline": {"achieved": pipe_achieved, "frac": pipe_achieved / peak,
+                                  "note": "algorithmic bytes of the batch over the whole Ranker step (cache "
+                                          "bookkeeping is latency-bound hash / LRU work, not credited)"},
+                     "kernel_shares": shares},
+        "gpu_launches": launches,
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+        "clocks": clocks,
+    }
+    emit(line, args)
 
 
 def run_sharded(args, rank, world, local):

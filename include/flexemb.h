@@ -370,6 +370,7 @@ int fx_step_offer(fx_step *s, int32_t slot, void *stream);
 int fx_step_maintain(fx_step *s, int32_t slot, int64_t stage_limit, int32_t do_age, void *stream);
 int fx_step_scalars(fx_step *s, int32_t slot, int64_t *out, int64_t n, void *stream);   /* [sync] */
 const void *fx_step_scalars_device(fx_step *s, int32_t slot);
+int64_t fx_step_launches(fx_step *s);  /* kernels launched by this handle so far (CUB sweeps count 2) */
 
 #ifdef __cplusplus
 }

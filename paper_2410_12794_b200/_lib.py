@@ -117,7 +117,7 @@ _SIGS = {
         "fx_cache_pooled_put", "fx_cache_rows", "fx_cache_scalars_device", "fx_cache_capacity",
         # fused batch step, typed in step.py
         "fx_step_create", "fx_step_destroy", "fx_step_prepare", "fx_step_start", "fx_step_offer", "fx_step_maintain",
-        "fx_step_scalars", "fx_step_scalars_device")},
+        "fx_step_scalars", "fx_step_scalars_device", "fx_step_launches")},
     "fx_bag_fingerprint": ([_P, _P, _P, _I32, _P, _I64, _P, _P, _P], ctypes.c_int),
 }
 

@@ -1526,6 +1526,7 @@ struct fx_step {
   int stream_smem = 0;
   int stage_smem = 0;
   int64_t stage_limit_cap = 0;
+  int64_t launches = 0;  // kernels this handle launched (CUB sweeps count 2)
 };
 
 namespace {
@@ -1781,13 +1782,17 @@ int fx_step_start(fx_step *s, int32_t slot, const int32_t *bag_table, const void
     return FX_E_CONFIG;
   }
   ks_begin<<<1, 1, 0, st>>>(c, v, nnz);
+  s->launches += 1;
   // dedup table reset: a memset beats clearing the claimed slots one by one
   cudaMemsetAsync(v.dkey, 0xff, v.dcap * sizeof(uint64_t), st);
   cudaMemsetAsync(v.dent, 0, v.dcap * sizeof(DEnt), st);
   if (threshold > 0) cudaMemsetAsync(v.dfraw, 0, v.dcap * sizeof(int32_t), st);
   ks_sketch_collect<<<grid_for(c.kcap, 256), 256, 0, st>>>(c, v);
+  s->launches += 1;
   ks_sketch_clear<<<grid_for(c.kcap, 256), 256, 0, st>>>(c, v);
+  s->launches += 1;
   ks_sketch_reinsert<<<grid_for(c.kcap, 256), 256, 0, st>>>(c, v);
+  s->launches += 1;
   // validation + dedup first: a bad index aborts the batch before any state change
   if (n_bags > 0) {
     const int g = grid_for((n_bags + 31) / 32 * 32, 256);
@@ -1797,32 +1802,46 @@ int fx_step_start(fx_step *s, int32_t slot, const int32_t *bag_table, const void
     else
       ks_dedup<int64_t><<<g, 256, 0, st>>>(v, bag_table, static_cast<const int64_t *>(indices), offsets, sm_start,
                                           n_bags);
+    s->launches += 1;
   }
   const int nn = static_cast<int>(nnz > 0 ? nnz : 1);
   size_t cb = s->cub_bytes;
   cub::DeviceSelect::If(s->cub_tmp, cb, v.claim, v.uniq, reinterpret_cast<int64_t *>(&v.ss->n_uniq), nn, NonNeg(),
                         st);
+  s->launches += 2;
   // ranker.py:218-222 order: validate, apply_pending, (admission check: host), probes
   ks_apply_pending<<<1, 32, 0, st>>>(c, v);
+  s->launches += 1;
   cudaMemsetAsync(v.cand_by_first, 0xff, static_cast<size_t>(nn) * 4, st);
   cudaMemsetAsync(v.hit_by_last, 0xff, static_cast<size_t>(nn) * 4, st);
   ks_probe<<<grid_for(nn, 256), 256, 0, st>>>(c, v, threshold > 0 ? 1 : 0);
+  s->launches += 1;
   ks_after_probe<<<1, 1, 0, st>>>(c, v, nnz);
+  s->launches += 1;
   ks_bag_plan<<<grid_for(n_bags > 0 ? n_bags * 32 : 32, 256), 256, 0, st>>>(v, offsets, sm_start, n_bags, threshold,
                                                                             hits_bag, pd_groups, pd_rows, raw_rows);
-  if (threshold > 0) ks_cand_scatter_raw<<<grid_for(nn, 256), 256, 0, st>>>(v);
+  s->launches += 1;
+  if (threshold > 0) {
+    ks_cand_scatter_raw<<<grid_for(nn, 256), 256, 0, st>>>(v);
+    s->launches += 1;
+  }
   // candidates in first raw-occurrence order; hit slots in last-ordinal order
   cub::DeviceSelect::If(s->cub_tmp, cb, v.cand_by_first, v.cand, reinterpret_cast<int64_t *>(&v.ss->n_cand), nn,
                         NonNeg(), st);
+  s->launches += 2;
   ks_cand_keys<<<grid_for(nn, 256), 256, 0, st>>>(v);
+  s->launches += 1;
   cub::DeviceSelect::If(s->cub_tmp, cb, v.hit_by_last, v.hits_ord, reinterpret_cast<int64_t *>(&v.ss->n_hitu), nn,
                         NonNeg(), st);
+  s->launches += 2;
   // LRU order after the probes: [entries not hit, old order] ++ [hit entries by last ordinal]
   cudaMemsetAsync(v.qnew, 0xff, SC * 4, st);
   QueueKeep qk{v.sflag, &v.ss->epoch};
   cub::DeviceSelect::If(s->cub_tmp, cb, cc->q, v.qnew, reinterpret_cast<int64_t *>(&v.ss->n_nonhit),
                         static_cast<int>(SC), qk, st);
+  s->launches += 2;
   ks_queue_append_hits<<<grid_for(nn, 256), 256, 0, st>>>(v);
+  s->launches += 1;
   cudaMemcpyAsync(cc->q, v.qnew, SC * 4, cudaMemcpyDeviceToDevice, st);
   FX_LAUNCH_CHECK("fx_step_start");
   return FX_OK;
@@ -1841,29 +1860,50 @@ int fx_step_offer(fx_step *s, int32_t slot, void *stream) {
   const int nn = static_cast<int>(s->max_nnz);
   size_t cb = s->cub_bytes;
   ks_offer_prep<<<grid_for(nn, 256), 256, 0, st>>>(c, v, nn, s->slots == 1 ? 1 : 0);
+  s->launches += 1;
   cub::DeviceSelect::Flagged(s->cub_tmp, cb, cub::CountingInputIterator<int32_t>(0), v.pres, v.cidx,
                              reinterpret_cast<int64_t *>(&v.ss->n_off), nn, st);
+  s->launches += 2;
   ks_cand_est<<<grid_for(nn, kFine), kFine, 0, st>>>(v);
+  s->launches += 1;
   ks_offer_plan<<<1, 1, 0, st>>>(c, v);
+  s->launches += 1;
   ks_victim_est<<<grid_for(SC, 256), 256, 0, st>>>(c, v, SC);
+  s->launches += 1;
   cub::DeviceSelect::Flagged(s->cub_tmp, cb, cub::CountingInputIterator<int32_t>(0), v.hardf, v.hard,
                              reinterpret_cast<int64_t *>(&v.ss->n_hard), static_cast<int>(SC), st);
+  s->launches += 2;
   ks_levels<<<1, 1024, 0, st>>>(v, s->stream_smem > 0 ? 1 : 0);
+  s->launches += 1;
   ks_cand_codes<<<grid_for(nn, 256), 256, 0, st>>>(v);
+  s->launches += 1;
   if (s->stream_smem > 0) ks_chain_stream<<<1, 1024, s->stream_smem, st>>>(v);
+  s->launches += 1;
   ks_chain_codes<<<1, 1024, s->code_smem, st>>>(v);
+  s->launches += 1;
   ks_chain<<<1, 1024, s->chain_smem, st>>>(v);
+  s->launches += 1;
   ks_accept_flags<<<grid_for(nn, 256), 256, 0, st>>>(v, nn);
+  s->launches += 1;
   cub::DeviceScan::ExclusiveSum(s->cub_tmp, cb, v.acc, v.rank, nn, st);
+  s->launches += 2;
   cudaMemsetAsync(v.qnew, 0xff, SC * 4, st);
   ks_apply<<<grid_for(nn, 256), 256, 0, st>>>(c, v);
+  s->launches += 1;
   ks_queue_survivors<<<grid_for(SC, 256), 256, 0, st>>>(c, v);
+  s->launches += 1;
   ks_seq_offer<<<1, 1, 0, st>>>(c, v);
+  s->launches += 1;
   ks_offer_finish<<<1, 1, 0, st>>>(c, v);
+  s->launches += 1;
   ks_copy_rows<<<grid_for(static_cast<int64_t>(nn) * (v.dim / 4 + 1), 256), 256, 0, st>>>(c, v);
+  s->launches += 1;
   ks_queue_commit<<<grid_for(SC, 256), 256, 0, st>>>(v, SC);
+  s->launches += 1;
   ks_index_clear<<<grid_for(c.hcap, 256), 256, 0, st>>>(c, v);
+  s->launches += 1;
   ks_index_fill<<<grid_for(SC, 256), 256, 0, st>>>(c, v);
+  s->launches += 1;
   FX_LAUNCH_CHECK("fx_step_offer");
   return FX_OK;
 }
@@ -1879,18 +1919,29 @@ int fx_step_maintain(fx_step *s, int32_t slot, int64_t stage_limit, int32_t do_a
     return FX_E_CONFIG;
   }
   ks_stage_begin<<<1, 1, 0, st>>>(c, v, stage_limit);
+  s->launches += 1;
   if (stage_limit > 0) {
     ks_topk_hist0<<<grid_for(c.kcap, 256), 256, 0, st>>>(c, v);
+    s->launches += 1;
     ks_topk_select<<<1, 1024, 0, st>>>(v, 0);
+    s->launches += 1;
     ks_topk_collect<<<grid_for(c.kcap, 256), 256, 0, st>>>(c, v);
+    s->launches += 1;
     for (int d = 1; d < 8; ++d) {
       ks_topk_hist<<<grid_for(4 * 65536, 256), 256, 0, st>>>(v, d);
+      s->launches += 1;
       ks_topk_select<<<1, 1024, 0, st>>>(v, d);
+      s->launches += 1;
     }
     ks_topk_gather<<<grid_for(c.kcap, 256), 256, 0, st>>>(v);
+    s->launches += 1;
     ks_stage_finish<<<1, 1024, s->stage_smem, st>>>(c, v, stage_limit);
+    s->launches += 1;
   }
-  if (do_age) ks_age<<<grid_for(c.kcap, 256), 256, 0, st>>>(c, v);
+  if (do_age) {
+    ks_age<<<grid_for(c.kcap, 256), 256, 0, st>>>(c, v);
+    s->launches += 1;
+  }
   FX_LAUNCH_CHECK("fx_step_maintain");
   return FX_OK;
 }
@@ -1907,6 +1958,8 @@ int fx_step_scalars(fx_step *s, int32_t slot, int64_t *out, int64_t n, void *str
   if (rc) return rc;
   return cuda_check(cudaStreamSynchronize(st), "fx_step_scalars sync");
 }
+
+int64_t fx_step_launches(fx_step *s) { return s->launches; }
 
 const void *fx_step_scalars_device(fx_step *s, int32_t slot) {
   return (slot >= 0 && slot <= s->slots) ? static_cast<const void *>(s->ss_base + slot) : nullptr;

@@ -219,6 +219,7 @@ class Ranker:
         self._fast_layouts: dict = {}
         self._fast_segs: dict = {}
         self._views = None
+        self.k4_events = None        # list -> (start, end) events around every K4 launch (bench roofline)
 
     def _mark(self, name):
         if self.profile:
@@ -311,10 +312,17 @@ class Ranker:
         side = self._pool_stream
         side.wait_stream(cur)
         with torch.cuda.stream(side):
+            k4 = None
+            if self.k4_events is not None:
+                k4 = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                k4[0].record(side)
             if feature_shape is not None:
                 self._pool_sample_major(lay, out, ft, fo, B)
             elif n_bags:
                 self._pool_fused(lay, n_bags, out=out)
+            if k4 is not None:
+                k4[1].record(side)
+                self.k4_events.append(k4)
         cnt = torch.empty((4, max(n_bags, 1)), dtype=torch.int32, device=dev)
         step.start(slot, lay.bag_table, lay.indices, lay.offsets, lay.sm_start, n_bags, nnz,
                    self.params.pushdown_threshold, cnt[0], cnt[1], cnt[2], cnt[3])
@@ -465,6 +473,61 @@ class Ranker:
             self.cache._reserve_sketch(2 * st.max_nnz + live)
             if self.cache.capacity()["sketch"] > st.tk_cap:
                 self._step = None
+
+    def stream_host(self, host_batches, feature_tables, feature_ops, batch_size: int, depth: int = 3,
+                    first_batch_id: int = 0):
+        """End-to-end batched API over HOST buffers: pinned host CSR batches
+        (indices, offsets) in -> pinned host pooled [B, F*D] f32 out, in order.
+        Three streams overlap the H2D of batch k+1, the fused step + K4 of
+        batch k and the D2H of batch k-1. A yielded host tensor stays valid
+        until the generator is advanced again (copy it to keep it)."""
+        if not getattr(self, "_fast", False):
+            raise ConfigError("stream_host needs the fused step (one full shard per table, one row size)")
+        dev = self.device
+        ft, fo, B = tuple(feature_tables), tuple(feature_ops), int(batch_size)
+        D = next(iter(self.deployment.metas.values())).dim
+        cur = torch.cuda.current_stream(dev)
+        s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        idx_d = [None] * depth
+        offs_d = [torch.empty(len(ft) * B + 1, dtype=torch.int64, device=dev) for _ in range(depth)]
+        nout = depth + 1
+        outs_h = [torch.empty((B, len(ft) * D), dtype=torch.float32, pin_memory=True) for _ in range(nout)]
+        free = [None] * depth          # compute finished with input slot k
+        done = [None] * nout           # D2H of output slot k finished
+        queue = []
+        for k, (idx_h, offs_h) in enumerate(host_batches):
+            sl = k % depth
+            if idx_d[sl] is None or idx_d[sl].numel() < idx_h.numel():
+                idx_d[sl] = torch.empty(max(idx_h.numel(), 1), dtype=idx_h.dtype, device=dev)
+            if len(queue) >= depth:    # output slot reuse: hand the oldest result out first
+                j, ev = queue.pop(0)
+                ev.synchronize()
+                yield outs_h[j % nout]
+            with torch.cuda.stream(s_in):
+                if free[sl] is not None:
+                    s_in.wait_event(free[sl])
+                idx_dev = idx_d[sl][:idx_h.numel()]
+                idx_dev.copy_(idx_h, non_blocking=True)
+                offs_d[sl].copy_(offs_h, non_blocking=True)
+                ev_in = torch.cuda.Event()
+                ev_in.record(s_in)
+            cur.wait_event(ev_in)
+            out, _ = self.execute_csr(idx_dev, offs_d[sl], ft, fo, B, batch_id=first_batch_id + k, sync=False)
+            free[sl] = torch.cuda.Event()
+            free[sl].record(cur)
+            so = k % nout
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(free[sl])
+                out.record_stream(s_out)
+                outs_h[so].copy_(out, non_blocking=True)
+                done[so] = torch.cuda.Event()
+                done[so].record(s_out)
+            queue.append((k, done[so]))
+        while queue:
+            j, ev = queue.pop(0)
+            ev.synchronize()
+            yield outs_h[j % nout]
+        self.sync()
 
     def sync(self) -> None:
         """Finish every in-flight batch and resolve deferred metrics / errors."""

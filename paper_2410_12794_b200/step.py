@@ -40,6 +40,7 @@ def _sig():
         "fx_step_maintain": ([P, I32, I64, I32, P], ctypes.c_int),
         "fx_step_scalars": ([P, I32, P, I64, P], ctypes.c_int),
         "fx_step_scalars_device": ([P, I32], P),
+        "fx_step_launches": ([P], I64),
     }
     for n, (a, r) in sigs.items():
         f = getattr(L, n)
@@ -128,6 +129,10 @@ class BatchStep:
         _lib.check(self._L.fx_step_scalars(self._h, int(slot), out, len(SCALARS), _lib.stream_ptr(stream)),
                    "step scalars")
         return dict(zip(SCALARS, list(out)))
+
+    def launches(self) -> int:
+        """Kernels this step handle launched so far (CUB sweeps count 2)."""
+        return int(self._L.fx_step_launches(self._h))
 
     def scalars_tensor(self, slot: int) -> torch.Tensor:
         """A zero-copy int64 view of a slot's device scalars (async snapshots)."""
