@@ -492,7 +492,7 @@ def run_ranker(args, rank, world, local):
     # warm-up: fills the cache to its steady state (first batches insert everything)
     for i in range(args.warmup):
         rk.execute_csr(*dbs[i], ft, fo, B, batch_id=i, sync=False)
-    rk.sync()
+    rk.sync()   # resolves metrics; may grow the sketch table / rebuild the step outside the timed region
     torch.cuda.synchronize()
     sampler = ClockSampler(local)
     sampler.start()
@@ -501,8 +501,10 @@ def run_ranker(args, rank, world, local):
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     ev0.record(stream)
+    th0 = time.perf_counter()
     for i in range(args.steps):
         rk.execute_csr(*dbs[args.warmup + i % n_timed], ft, fo, B, batch_id=args.warmup + i, sync=False)
+    host_ms = (time.perf_counter() - th0) * 1e3 / args.steps
     ev1.record(stream)
     ev1.synchronize()
     torch.cuda.synchronize()
@@ -561,6 +563,7 @@ def run_ranker(args, rank, world, local):
             f"({tot_bytes / args.steps / 1e9:.2f} GB algorithmic bytes each) over {N * T * D * 4 / 1e9:.1f} GB of "
             f"tables + {budget / 1e9:.2f} GB of cached rows", "init_store_s": round(init_s, 2)}),
         "hit_rate": hit, "latency_ms": {"p50": lat[len(lat) // 2], "max": lat[-1]},
+        "host_enqueue_ms_per_step": host_ms,
         "roofline": {"bound": "hbm", "achieved": k4_achieved, "peak": peak, "unit": "GB/s",
                      "frac": k4_achieved / peak, "traffic": None, "peak_source": peak_src,
                      "kernel": "fx::k_pool_bulk (fused gather+pool K4, side stream of the Ranker step)",

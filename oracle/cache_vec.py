@@ -156,23 +156,31 @@ class RowCacheVec:
         return uniq, first.astype(np.int64), last, cnt.astype(np.int64), hit, inv
 
     def offer_many(self, cand: np.ndarray) -> np.ndarray:
-        """offer(key) for each candidate in order (cache.py:237-268); the
-        candidates are distinct and absent. Returns the accept mask."""
+        """offer(key) for each distinct candidate in order (cache.py:237-268).
+        A candidate cached when its turn comes returns True with no side
+        effect; one that an earlier offer of the same call evicted is absent
+        again and goes through admission (possible when several batches are
+        in flight). Returns the accept mask."""
         cand = np.asarray(cand, U64)
         n = cand.size
         acc = np.zeros(n, bool)
         if n == 0:
             return acc
         S, budget = self.S, self.budget
-        if S > budget:
-            return acc
         c_est = self.estimate(cand).tolist()
         v_est = self.estimate(self.keys).tolist() if self.admission == "sketch" else []
+        vpos = {k: i for i, k in enumerate(self.keys.tolist())}   # initial entries' LRU positions
         e = self.keys.size           # live entries
         h = 0                        # LRU head position in V = [entries] ++ [accepts]
         acc_idx = []
         sketch = self.admission == "sketch"
-        for j in range(n):
+        for j, k in enumerate(cand.tolist()):
+            p = vpos.get(k)
+            if p is not None and p >= h:   # still cached: offer -> True
+                acc[j] = True
+                continue
+            if S > budget:
+                continue
             if (e + 1) * S > budget:
                 if sketch:
                     ve = v_est[h] if h < len(v_est) else c_est[acc_idx[h - len(v_est)]]
@@ -258,6 +266,11 @@ class RowPipelineVec:
         self.metrics = []
 
     def run(self, keys_sm: np.ndarray, bag_len_sm: np.ndarray, n_lookups: int, batch_id: int = 0):
+        return self.finish(self.start(keys_sm, bag_len_sm, n_lookups, batch_id))
+
+    def start(self, keys_sm: np.ndarray, bag_len_sm: np.ndarray, n_lookups: int, batch_id: int = 0):
+        """_start_batch (ranker.py:218-257): apply_pending -> admission check
+        -> probes -> plan. Returns the in-flight batch state."""
         c = self.cache
         keys_sm = np.asarray(keys_sm, U64)
         c.apply_pending()
@@ -284,12 +297,26 @@ class RowPipelineVec:
         ords = np.nonzero(raw_occ)[0]
         ku, kfirst = np.unique(inv[ords], return_index=True)
         cand_u = ku[np.argsort(ords[kfirst], kind="stable")]
-        cand = uniq[cand_u]
+        hits = int(mult[hit].sum())
+        nnz = int(keys_sm.size)
+        return dict(batch_id=batch_id, size=n_lookups, cand=uniq[cand_u], uniq=uniq, hit=hit, mult=mult,
+                    hit_occ=hit_occ, hits=hits, misses=nnz - hits,
+                    pushdown_groups=int(push_bag[miss_per_bag > 0].sum()),
+                    pushdown_rows=int(miss_per_bag[push_bag].sum()), raw_rows=int(raw_occ.sum()),
+                    subrequests=int((miss_per_bag > 0).sum()))
+
+    def finish(self, st):
+        """_finish_batch (ranker.py:364-442): offers of the raw-fetched rows in
+        first raw-occurrence order — a key installed since the probes (a later
+        batch's apply_pending, pipeline_depth > 1) is present: offer() -> True
+        with no side effect — then maintenance."""
+        c = self.cache
+        cand = st["cand"]
         accepted = c.offer_many(cand)
         level = None
         staged = []
         if self.tracker is not None and self.policy is not None:
-            level = self.tracker.record(n_lookups)
+            level = self.tracker.record(st["size"])
             if self.adaptive:
                 prop = self.policy.propose(c.budget, level, self.tracker.value())
                 if prop != c.budget:
@@ -297,15 +324,24 @@ class RowPipelineVec:
                 if self.admit > 0:
                     staged = c.stage(self.admit)
                 c.age()
-        hits = int(mult[hit].sum())
-        nnz = int(keys_sm.size)
-        pd_groups = int(push_bag[miss_per_bag > 0].sum())
-        pd_rows = int(miss_per_bag[push_bag].sum())
-        self.metrics.append(dict(batch_id=batch_id, size=n_lookups, hits=hits, misses=nnz - hits,
-                                 pushdown_groups=pd_groups, pushdown_rows=pd_rows,
-                                 raw_rows=int(raw_occ.sum()), load_level=level, n_offers=int(cand.size),
-                                 n_accepted=int(accepted.sum()), staged=staged))
-        return dict(uniq=uniq, hit=hit, mult=mult, cand=cand, accepted=accepted, hit_occ=hit_occ)
+        self.metrics.append(dict(batch_id=st["batch_id"], size=st["size"], hits=st["hits"], misses=st["misses"],
+                                 pushdown_groups=st["pushdown_groups"], pushdown_rows=st["pushdown_rows"],
+                                 raw_rows=st["raw_rows"], subrequests=st["subrequests"], load_level=level,
+                                 n_offers=int(cand.size), n_accepted=int(accepted.sum()), staged=staged,
+                                 budget=c.budget if len(c) else None, used=c.used if len(c) else None))
+        return dict(uniq=st["uniq"], hit=st["hit"], mult=st["mult"], cand=cand, accepted=accepted,
+                    hit_occ=st["hit_occ"])
+
+    def run_trace(self, batches, depth: int = 1):
+        """Closed-loop replay with `depth` batches in flight (ranker.py:161-182):
+        S0..S(d-1) F0 Sd F1 ... ; batches = [(keys_sm, bag_len_sm, n_lookups, id)]."""
+        inflight = []
+        for b in batches:
+            inflight.append(self.start(*b))
+            if len(inflight) >= depth:
+                self.finish(inflight.pop(0))
+        while inflight:
+            self.finish(inflight.pop(0))
 
 
 def keys_sample_major(indices: np.ndarray, offsets: np.ndarray, feature_tables, batch_size: int):

@@ -88,7 +88,8 @@ struct StepScalars {
   long long qlen_new;
   long long n_levels, codes_on;  // distinct hard-victim estimates (<= 255 -> byte codes)
   long long chain_cycles;        // clock64 cycles of the decision chain (diagnostics)
-  long long pad[5];
+  long long dyn;                 // a candidate was cached at offer time (several batches in flight)
+  long long pad[4];
 };
 
 struct DEnt {       // per dedup-hash slot (one 16-byte line for the atomics); all-zero = empty
@@ -259,6 +260,7 @@ __global__ void ks_begin(CacheView c, StepView v, int64_t max_nnz) {
   v.gs->epoch += 1;  // global batch counter (slot hit marks)
   s->epoch = v.gs->epoch;
   s->n_uniq = s->n_cand = s->n_hitu = s->n_nonhit = s->n_hard = s->n_rej = s->n_off = 0;
+  s->dyn = 0;
   s->n_acc = s->n_ev = 0;
   s->mode = MODE_NONE;
   s->minc_bits = LLONG_MAX;
@@ -582,11 +584,22 @@ __global__ void ks_offer_prep(CacheView c, StepView v, int64_t max_nnz, int32_t 
         v.estv[j] = v.cest[j];
       } else {
         f = h_find(c, key) < 0 ? 1 : 0;
-        if (f) v.estv[j] = k_est(c, key);
+        v.estv[j] = k_est(c, key);
+        if (!f) v.ss->dyn = 1;
       }
     }
     v.pres[j] = f;
   }
+}
+
+// a candidate cached at offer time can be evicted by an earlier offer of the
+// same call and then be offered for real: such calls keep every candidate
+// and take the sequential path, which checks presence as it goes
+__global__ void ks_offer_flags(StepView v, int64_t max_nnz) {
+  if (aborted(v) || !v.ss->dyn) return;
+  const long long n = v.ss->n_cand;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < max_nnz; j += (int64_t)gridDim.x * blockDim.x)
+    v.pres[j] = j < n ? 1 : 0;
 }
 
 // candidate estimates in offer order, their minimum and per-block maxima
@@ -645,7 +658,7 @@ __global__ void ks_offer_plan(CacheView c, StepView v) {
   const long long cap = budget / S;
   const long long F = cap > e0 ? (cap - e0 < n ? cap - e0 : n) : 0;
   s->F = F;
-  s->mode = (e0 <= cap && n - F <= e0) ? MODE_PAR : MODE_SEQ;
+  s->mode = (e0 <= cap && n - F <= e0 && !s->dyn) ? MODE_PAR : MODE_SEQ;
 }
 
 // victim estimates for V[0, n - F) and hard flags (est > minC)
@@ -1189,6 +1202,7 @@ __global__ void ks_seq_offer(CacheView c, StepView v) {
   auto vslot = [&](long long q) -> int32_t { return q < e0 ? v.q[q] : v.aslot[q - e0]; };
   for (long long j = 0; j < n; ++j) {
     const double cj = v.cC[j];
+    if (s->dyn && h_find(c, v.okey[j]) >= 0) continue;  // still cached: offer -> True, no side effect
     if ((e + 1) * S > budget) {
       if (sketch && e > 0) {
         const int32_t vs = vslot(h);
@@ -1860,6 +1874,8 @@ int fx_step_offer(fx_step *s, int32_t slot, void *stream) {
   const int nn = static_cast<int>(s->max_nnz);
   size_t cb = s->cub_bytes;
   ks_offer_prep<<<grid_for(nn, 256), 256, 0, st>>>(c, v, nn, s->slots == 1 ? 1 : 0);
+  s->launches += 1;
+  ks_offer_flags<<<grid_for(nn, 256), 256, 0, st>>>(v, nn);
   s->launches += 1;
   cub::DeviceSelect::Flagged(s->cub_tmp, cb, cub::CountingInputIterator<int32_t>(0), v.pres, v.cidx,
                              reinterpret_cast<int64_t *>(&v.ss->n_off), nn, st);

@@ -473,6 +473,7 @@ class Ranker:
             self.cache._reserve_sketch(2 * st.max_nnz + live)
             if self.cache.capacity()["sketch"] > st.tk_cap:
                 self._step = None
+                self._get_step(st.max_nnz, st.max_bags)   # rebuilt now, not inside a later batch
 
     def stream_host(self, host_batches, feature_tables, feature_ops, batch_size: int, depth: int = 3,
                     first_batch_id: int = 0):

@@ -216,6 +216,52 @@ def ranker_fixtures():
         json.dump(out, fh)
 
 
+def pipeline_fixtures():
+    """Ranker.run_trace with pipeline_depth 2 and 3 (ranker.py:161-182): up
+    to `depth` batches in flight, so batch k+depth starts (apply_pending +
+    probes) only after batch k finished (offers + maintenance). One server,
+    one connection, one engine: batches finish in arrival order."""
+    out = []
+    rng = np.random.default_rng(21)
+    for depth, thr in ((2, None), (3, None), (2, 2)):
+        metas = [TableMeta(0, 1500, 16), TableMeta(1, 900, 16)]
+        placement = [ShardSpec(0, 0, 1500, 0), ShardSpec(1, 0, 900, 0)]
+        budget = 64 * 150
+        model = MemoryModel(gpu_capacity_bytes=budget + 1000 + 100, nn_fixed_bytes=1000, nn_per_sample_bytes=1)
+        cache = AdaptiveCache(budget_bytes=budget, admission="sketch", record_evictions=True)
+        policy = CachePolicy(model=model, hysteresis_fraction=0.05)
+        tracker = LoadTracker(window=4, high_watermark=512, low_watermark=16)
+        dep = init_store(metas, placement, 0)
+        rt = build_routing(metas, placement)
+        topo = create_connections(1, peers=dep.server_ids, conns_per_peer=1)
+        tr = VirtualTransport(EventLoop(), topo, assign_mapping_aware(topo, 1), TransportParams())
+        rk = Ranker(dep, rt, tr, RankerParams(pushdown_threshold=thr, admit_per_batch=8, pipeline_depth=depth),
+                    cache=cache, policy=policy, tracker=tracker)
+        batches = _zipf_batches(rng, metas, n_batches=7, lookups=(30, 50), L=(1, 6), alpha=1.0)
+        rk.run_trace(batches)
+        out.append(dict(
+            name=f"pipeline_depth{depth}_thr{thr}", depth=depth, threshold=thr,
+            metas=[[m.table_id, m.num_rows, m.dim] for m in metas],
+            placement=[[s.table_id, s.start, s.end, s.server_id] for s in placement],
+            cache=dict(budget=budget, admission="sketch",
+                       model=[model.gpu_capacity_bytes, model.nn_fixed_bytes, model.nn_per_sample_bytes],
+                       hyst=0.05, tracker=[4, 512, 16], admit=8),
+            batches=[[[[f.table_id, f.op.value, f.indices] for f in lk.features] for lk in b.lookups]
+                     for b in batches],
+            metrics=[dict(batch_id=m.batch_id, hits=m.cache_hits, misses=m.cache_misses,
+                          pushdown_groups=m.pushdown_groups, pushdown_rows=m.pushdown_rows, raw_rows=m.raw_rows,
+                          load_level=m.load_level, budget=m.cache_budget, used=m.cache_used,
+                          subrequests=m.subrequests) for m in rk.batch_metrics],
+            results={str(b.batch_id): [[[float(x) for x in v.view(np.uint32).astype(np.float64)] for v in r.vectors]
+                                       for r in rk.results[b.batch_id]] for b in batches},
+            lru=[list(k) for k in cache._entries],
+            ticks=[e.last_tick for e in cache._entries.values()],
+            evictions=[list(k) for k in cache.eviction_log],
+            final_sketch=sorted([[k[0], k[1], v] for k, v in cache.sketch._counts.items()])))
+    with open(os.path.join(HERE, "pipeline.json"), "w") as fh:
+        json.dump(out, fh)
+
+
 def _key_json(k):
     if isinstance(k, tuple) and len(k) == 4 and k[0] == "pooled":
         return ["pooled", k[1], k[2], list(k[3])]
@@ -371,5 +417,6 @@ if __name__ == "__main__":
     ranker_fixtures()
     pooled_fixtures()
     report_fixtures()
+    pipeline_fixtures()
     for f in sorted(os.listdir(HERE)):
         print(f, os.path.getsize(os.path.join(HERE, f)))

@@ -71,3 +71,41 @@ def test_vec_cache_trickle_staging_fills():
     # 64-row stage_hot_admissions trickle and apply_pending (ranker.py:439-441)
     cv = _run_both((1500, 800), 16, 40, (1, 8), 0.9, 300, 2, "sketch", 10, seed=11)
     assert len(cv) == 300
+
+
+def _golden_pipeline(golden_dir):
+    import json
+    import os
+    return json.load(open(os.path.join(golden_dir, "pipeline.json")))
+
+
+def _batch_keys(lookups):
+    keys, lens = [], []
+    for feats in lookups:
+        for t, _op, ix in feats:
+            keys.extend((int(t) << 40) | int(i) for i in ix)
+            lens.append(len(ix))
+    return np.array(keys, np.uint64), np.array(lens, np.int64)
+
+
+def test_vec_pipeline_depth_matches_reference(golden_dir):
+    """pipeline_depth 2/3 (ranker.py:161-182) replayed by the vectorised
+    oracle's start/finish split reproduces the reference Ranker's metrics,
+    final LRU order + ticks, eviction log and sketch (tests/golden/pipeline.json)."""
+    for rec in _golden_pipeline(golden_dir):
+        c = rec["cache"]
+        S = rec["metas"][0][2] * 4
+        cv = RowCacheVec(c["budget"], S, c["admission"], record_evictions=True)
+        pv = RowPipelineVec(cv, rec["threshold"], policy=O.CachePolicyO(O.MemoryModelO(*c["model"]), c["hyst"]),
+                            tracker=O.LoadTrackerO(*c["tracker"]), admit_per_batch=c["admit"])
+        batches = [(*_batch_keys(lk), len(lk), i) for i, lk in enumerate(rec["batches"])]
+        pv.run_trace(batches, depth=rec["depth"])
+        for got, ref in zip(pv.metrics, rec["metrics"]):
+            for k in ("batch_id", "hits", "misses", "pushdown_groups", "pushdown_rows", "raw_rows", "subrequests",
+                      "load_level", "budget", "used"):
+                assert got[k] == ref[k], (rec["name"], k, got[k], ref[k])
+        assert cv.keys.tolist() == [(t << 40) | r for t, r in rec["lru"]], rec["name"]
+        assert cv.ticks.tolist() == rec["ticks"], rec["name"]
+        assert cv.evictions == [(t << 40) | r for t, r in rec["evictions"]], rec["name"]
+        assert cv.sk_keys.tolist() == [(t << 40) | r for t, r, _ in rec["final_sketch"]], rec["name"]
+        assert cv.sk_vals.tolist() == [v for _, _, v in rec["final_sketch"]], rec["name"]
