@@ -273,9 +273,12 @@ class Ranker:
         if (st is None or nnz > st.max_nnz or n_bags > st.max_bags or st.slots != self.cache._slots
                 or st.n_slots != depth or self.params.admit_per_batch > st.stage_limit_cap):
             if self._inflight:
-                raise InvariantError("step capacity changed with batches in flight")
+                raise ConfigError("a batch larger than the fused step's capacity arrived with batches in flight: "
+                                  "call Ranker.reserve(max_nnz, max_bags) first")
             max_nnz = max(nnz, st.max_nnz if st else 0, 1)
             max_bags = max(n_bags, st.max_bags if st else 0, 1)
+            if depth > 1:  # headroom: the step cannot grow while batches are in flight
+                max_nnz, max_bags = max_nnz + max_nnz // 2, max_bags + max_bags // 2
             # the sketch must take a batch's new keys without rehashing into a
             # bigger table mid-stream (the step bakes its pointers)
             self.cache._reserve_sketch(2 * max_nnz)
@@ -288,6 +291,14 @@ class Ranker:
             self._epoch_ev = torch.cuda.Event(enable_timing=True)
             self._epoch_ev.record()
         return self._step
+
+    def reserve(self, max_nnz: int, max_bags: int) -> None:
+        """Size the fused step for batches of up to `max_nnz` indices and
+        `max_bags` bags (needed before streaming batches of growing size with
+        pipeline_depth > 1: the step cannot grow while batches are in flight)."""
+        if getattr(self, "_fast", False):
+            self.sync()
+            self._get_step(int(max_nnz), int(max_bags))
 
     def _fast_start(self, lay: CsrLayout, n_lookups: int, batch_id: int, feature_shape=None, host=None):
         """Enqueue one batch's start phase and its pooling (K4 on a side
@@ -549,6 +560,8 @@ class Ranker:
             for b in trace_batches:
                 self._run_batch(b)
             return
+        self.reserve(max(sum(len(f.indices) for lk in b.lookups for f in lk.features) for b in trace_batches),
+                     max(sum(len(lk.features) for lk in b.lookups) for b in trace_batches))
         for b in trace_batches:
             for lookup in b.lookups:
                 for f in lookup.features:

@@ -223,7 +223,7 @@ def pipeline_fixtures():
     one connection, one engine: batches finish in arrival order."""
     out = []
     rng = np.random.default_rng(21)
-    for depth, thr in ((2, None), (3, None), (2, 2)):
+    for depth, thr in ((2, None), (3, None), (2, 2), (1, None), (1, 2)):
         metas = [TableMeta(0, 1500, 16), TableMeta(1, 900, 16)]
         placement = [ShardSpec(0, 0, 1500, 0), ShardSpec(1, 0, 900, 0)]
         budget = 64 * 150

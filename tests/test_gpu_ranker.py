@@ -25,7 +25,7 @@ def P():
     return P
 
 
-def _build(P, rec):
+def _build(P, rec, fused=True):
     from paper_2410_12794_b200 import cache as C
     from paper_2410_12794_b200.ranker import Ranker, RankerParams
     metas = [P.TableMeta(*m) for m in rec["metas"]]
@@ -42,15 +42,21 @@ def _build(P, rec):
         tracker = C.LoadTracker(window=w, high_watermark=hi, low_watermark=lo)
         admit = cc["admit"]
     rk = Ranker(dep, rt, None, RankerParams(pushdown_threshold=rec["threshold"], admit_per_batch=admit),
-                cache=cache, policy=policy, tracker=tracker)
+                cache=cache, policy=policy, tracker=tracker, fused=fused)
     return dep, rk
 
 
+@pytest.mark.parametrize("fused", [True, False])
 @pytest.mark.parametrize("which", [0, 1, 2])
-def test_ranker_replays_reference(P, golden_dir, which):
+def test_ranker_replays_reference(P, golden_dir, which, fused):
+    """fused=True: the sync-free fused batch step (csrc/fx_step.cu) wherever
+    the deployment is in its domain (the 1-server cache runs); False: the
+    staged pipeline."""
     recs = json.load(open(os.path.join(golden_dir, "ranker.json")))
     rec = recs[which]
-    dep, rk = _build(P, rec)
+    dep, rk = _build(P, rec, fused)
+    # these runs mix row sizes (dims 16 and 8): the staged pipeline serves them
+    # either way; tests/golden/pipeline.json replays the fused step
     for bi, lookups in enumerate(rec["batches"]):
         batch = P.Batch(bi, bi, [P.LookupRequest([P.Feature(t, P.PoolingOp(op), ix) for t, op, ix in lk])
                                  for lk in lookups])
