@@ -53,6 +53,8 @@ extern "C" {
                                      PartialResult.vector semantics, pooling.py:35-47 */
 #define FX_OUT_SYSFENCE 16        /* OR-flag: system-scope fence after the epilogue stores
                                      (outputs written to peer GPUs over NVLink)        */
+#define FX_OUT_SCALAR 32          /* OR-flag: scalar kernel (a segment's table / output pointer, ld or
+                                     out_stride is not 16-byte aligned) */
 /* In both partial modes an EMPTY bag's output row is not written (its count
  * is 0: the partial is absent and K5 never reads it). */
 

@@ -34,6 +34,7 @@ FX_OUT_F32 = 0
 FX_OUT_F64_PARTIAL = 1
 FX_OUT_F32_PARTIAL = 2
 FX_OUT_SYSFENCE = 16
+FX_OUT_SCALAR = 32
 
 INT64_MAX = (1 << 63) - 1
 
@@ -155,6 +156,25 @@ def idx_type_of(t: torch.Tensor) -> int:
     if t.dtype == torch.int64:
         return FX_IDX_I64
     raise errors.ConfigError(f"indices must be int32 or int64, got {t.dtype}")
+
+
+def check_out(out: torch.Tensor, rows: int, cols: int, name: str = "out", dtype=torch.float32) -> None:
+    """A caller-supplied output buffer must be a CUDA tensor of `dtype`, unit
+    column stride and at least [rows, cols] (K4 writes rows*cols elements)."""
+    if not out.is_cuda or out.dtype != dtype:
+        raise errors.ConfigError(f"{name} must be a CUDA {dtype} tensor, got {out.dtype} on {out.device}")
+    if out.dim() != 2 or out.shape[0] < rows or out.shape[1] < cols or (out.shape[1] > 1 and out.stride(1) != 1):
+        raise errors.ConfigError(f"{name} must be a row-major [>= {rows}, >= {cols}] tensor, got shape "
+                                 f"{tuple(out.shape)} strides {tuple(out.stride())}")
+
+
+def vec_ok(*ptrs_and_strides) -> bool:
+    """True when every (pointer, element-stride) pair is 16-byte aligned for
+    4-byte elements (the vector / bulk-copy K4 kernels' requirement)."""
+    for p, st in ptrs_and_strides:
+        if int(p) % 16 or int(st) % 4:
+            return False
+    return True
 
 
 def require_cuda(t: torch.Tensor, name: str) -> None:

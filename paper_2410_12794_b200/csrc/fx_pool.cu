@@ -467,7 +467,7 @@ static int launch_pool(const fx_segment *segs, int n_segs, int dim, const void *
                        int64_t n_bags, int32_t *counts, int64_t *err, int32_t bad_code, int32_t *err_code,
                        cudaStream_t st, bool vec4, bool sf) {
   const IdxT *ix = static_cast<const IdxT *>(indices);
-  const int var = pool_variant();
+  const int var = vec4 ? pool_variant() : 0;
   if (var >= 2 && dim == 128) {
     // 12-row chunks, <= 72 registers: 7 blocks (28 warps) per SM; tuned on B200
     // against 16-row / 6-block and 8..14-row / 7..10-block configurations
@@ -530,17 +530,20 @@ int fx_gather_pool(const fx_segment *segs, int32_t n_segs, int32_t dim, const vo
                    const int64_t *offsets, int64_t n_bags, int32_t out_mode, int32_t *counts, int64_t *err,
                    int32_t bad_code, int32_t *err_code, void *stream) {
   const bool sf = (out_mode & FX_OUT_SYSFENCE) != 0;
-  out_mode &= ~FX_OUT_SYSFENCE;
+  const bool scalar = (out_mode & FX_OUT_SCALAR) != 0;
+  out_mode &= ~(FX_OUT_SYSFENCE | FX_OUT_SCALAR);
   if (n_segs < 1 || dim < 1 || (idx_type != FX_IDX_I32 && idx_type != FX_IDX_I64) ||
       (out_mode != FX_OUT_F32 && out_mode != FX_OUT_F64_PARTIAL && out_mode != FX_OUT_F32_PARTIAL)) {
     set_error("fx_gather_pool: bad arguments");
     return FX_E_CONFIG;
   }
   if (n_bags == 0) return FX_OK;
-  // The caller guarantees 16-B aligned rows/outputs when it requests the
-  // vector path through dim % 4 == 0 (ld and out_stride are multiples of 4 and
-  // base pointers 16-B aligned, checked host-side by the Python binding).
-  const bool vec4 = (dim % 4) == 0;
+  // The vector / bulk-copy kernels move 16-byte pieces: they need every
+  // segment's table base, output pointer (column offset included), ld and
+  // out_stride 16-B aligned. The segments live in device memory, so the caller
+  // states it: FX_OUT_SCALAR selects the scalar kernel (the Python bindings
+  // check the alignment of the descriptors they build and set it otherwise).
+  const bool vec4 = (dim % 4) == 0 && !scalar;
   cudaStream_t st = as_stream(stream);
   if (out_mode == FX_OUT_F32_PARTIAL) {
     return idx_type == FX_IDX_I32

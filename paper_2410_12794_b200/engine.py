@@ -106,28 +106,34 @@ class LookupEngine:
         return sum(self.dim_of(t) for t in batch.feature_tables)
 
     def pool(self, batch: CsrBatch, out: torch.Tensor | None = None, check: bool = True,
-             stream=None) -> torch.Tensor:
+             stream=None, status=None) -> torch.Tensor:
         """Launch K4 for the whole batch; returns out [B, sum(D_f)] f32."""
         B = batch.batch_size
         if batch.n_bags != B * batch.n_features:
             raise ConfigError("offsets must describe batch_size * n_features table-major bags")
         if out is None:
             out = torch.empty((B, self.out_dim(batch)), dtype=torch.float32, device=self.device)
+        _lib.check_out(out, B, self.out_dim(batch))
         dims = {self.dim_of(t) for t in batch.feature_tables}
+        st_ = status or self.status
         if len(dims) != 1:
-            return self._pool_mixed(batch, out, check, stream)
+            return self._pool_mixed(batch, out, check, stream, st_)
         D = dims.pop()
         segs = self._segments(batch, out)
+        aligned = _lib.vec_ok((out.data_ptr(), out.stride(0)), (D * 4, 0),
+                              *[(self.tables[t].data_ptr(), self.tables[t].stride(0)) for t in batch.feature_tables])
         _lib.check(_lib.lib.fx_gather_pool(segs.data_ptr(), batch.n_features, D, batch.indices.data_ptr(),
                                            _lib.idx_type_of(batch.indices), batch.offsets.data_ptr(), batch.n_bags,
-                                           _lib.FX_OUT_F32, None, self.status.err.data_ptr(),
-                                           _lib.FX_E_LOOKUP_VALIDATION, self.status.code.data_ptr(),
+                                           _lib.FX_OUT_F32 | (0 if aligned else _lib.FX_OUT_SCALAR), None,
+                                           st_.err.data_ptr(),
+                                           _lib.FX_E_LOOKUP_VALIDATION, st_.code.data_ptr(),
                                            _lib.stream_ptr(stream)), "gather_pool")
         if check:
             self.raise_if_bad(batch)
         return out
 
-    def _pool_mixed(self, batch, out, check, stream):
+    def _pool_mixed(self, batch, out, check, stream, status=None):
+        status = status or self.status
         # one launch per distinct dim; segments of other dims are skipped by
         # giving the kernel only the bags of the matching features
         segs_all = []
@@ -146,10 +152,13 @@ class LookupEngine:
                                                     out.stride(0), tab.stride(0), D,
                                                     op_code(batch.feature_ops[f]))], self.device)
                 offs = batch.offsets[f * B:(f + 1) * B + 1]
+                # mixed dims: a feature's output column offset need not be 16-B aligned
+                aligned = _lib.vec_ok((out.data_ptr() + c * 4, out.stride(0)), (tab.data_ptr(), tab.stride(0)))
                 _lib.check(_lib.lib.fx_gather_pool(seg.data_ptr(), 1, D, batch.indices.data_ptr(),
                                                    _lib.idx_type_of(batch.indices), offs.data_ptr(), B,
-                                                   _lib.FX_OUT_F32, None, self.status.err.data_ptr(),
-                                                   _lib.FX_E_LOOKUP_VALIDATION, self.status.code.data_ptr(),
+                                                   _lib.FX_OUT_F32 | (0 if aligned else _lib.FX_OUT_SCALAR), None,
+                                                   status.err.data_ptr(),
+                                                   _lib.FX_E_LOOKUP_VALIDATION, status.code.data_ptr(),
                                                    _lib.stream_ptr(stream)), "gather_pool")
         if check:
             self.raise_if_bad(batch)
@@ -331,8 +340,11 @@ class HostLookup:
         outputs, pinned host outputs and events are allocated once per
         (depth, output shape) and reused across calls, so the steady state
         allocates nothing. A yielded tensor is valid until the generator is
-        advanced (its slot is then reused). Validation errors are raised
-        after the last batch."""
+        advanced (its slot is then reused). Each slot carries its own status
+        words, copied back with its output: a batch with a bad index raises
+        the reference's LookupValidationError (first bad index of THAT batch
+        in (lookup, feature, position) order) when its turn to be yielded
+        comes."""
         eng = self.engine
         dev = eng.device
         st = self._stream_state(depth)
@@ -359,35 +371,48 @@ class HostLookup:
                 sl["idx"][:nnz].copy_(bh.indices, non_blocking=True)
                 sl["offs"][:nb].copy_(bh.offsets, non_blocking=True)
                 sl["ev_in"].record(s_in)
+            if "status" not in sl:
+                sl["status"] = _lib.Status(dev)
+                sl["code_h"] = torch.zeros(1, dtype=torch.int32, pin_memory=True)
             with torch.cuda.stream(s_cmp):
                 s_cmp.wait_event(sl["ev_in"])
                 if sl["used"]:
                     s_cmp.wait_event(sl["ev_out"])  # the slot's device output was copied out
                 dbatch = CsrBatch(sl["idx"][:nnz], sl["offs"][:nb], bh.feature_tables, bh.feature_ops, B)
                 sl["batch"] = dbatch
-                eng.pool(dbatch, out=sl["out"], check=False, stream=s_cmp)
+                sl["host_batch"] = bh
+                sl["status"].reset()
+                eng.pool(dbatch, out=sl["out"], check=False, stream=s_cmp, status=sl["status"])
                 sl["ev_cmp"].record(s_cmp)
             with torch.cuda.stream(s_out):
                 s_out.wait_event(sl["ev_cmp"])
                 sl["host"].copy_(sl["out"], non_blocking=True)
+                sl["code_h"].copy_(sl["status"].code, non_blocking=True)
                 sl["ev_out"].record(s_out)
             sl["used"] = True
+
+        def take(kk, idx_batch):
+            sl = slots[kk]
+            sl["ev_out"].synchronize()
+            if int(sl["code_h"][0]):
+                best = eng._first_bad(sl["host_batch"])
+                if best is not None:
+                    s_, _f, index, t, n = best
+                    raise LookupValidationError(f"batch {idx_batch}, lookup {s_}: index {index} out of range "
+                                                f"[0,{n}) for table {t}")
+                raise LookupValidationError(f"batch {idx_batch}: an index was out of range")
+            return sl["host"]
 
         i = 0
         for bh in batches_host:
             k = i % depth
             if len(pending) == depth:
-                kk = pending.pop(0)
-                slots[kk]["ev_out"].synchronize()
-                yield slots[kk]["host"]
+                kk, bi = pending.pop(0)
+                yield take(kk, bi)
             launch(bh, k)
-            pending.append(k)
+            pending.append((k, i))
             i += 1
         while pending:
-            kk = pending.pop(0)
-            slots[kk]["ev_out"].synchronize()
-            yield slots[kk]["host"]
+            kk, bi = pending.pop(0)
+            yield take(kk, bi)
         torch.cuda.synchronize(dev)
-        code, _ = eng.status.read()
-        if code:
-            eng.raise_if_bad(slots[0]["batch"])

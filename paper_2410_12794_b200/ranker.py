@@ -556,6 +556,10 @@ class Ranker:
         the phases run S0..S(d-1) F0 Sd F1 ... — the reference's order when
         batches finish in arrival order (one server, FIFO)."""
         depth = max(1, int(self.params.pipeline_depth))
+        if depth > 1 and self.cache is not None and not getattr(self, "_fast", False):
+            raise ConfigError("pipeline_depth > 1 with a cache needs the fused step (one full shard per table on "
+                              "this GPU, one row size, no pooled-result keyspace); the staged pipeline runs batches "
+                              "one at a time and would not reproduce the reference's interleaving")
         if not getattr(self, "_fast", False) or depth == 1:
             for b in trace_batches:
                 self._run_batch(b)

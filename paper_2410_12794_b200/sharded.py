@@ -201,15 +201,25 @@ class FlexOps:
         self.owner_status.reset()
         if code:
             if batch is not None:
+                # the reference rejects the first bad index in (lookup, feature,
+                # position) order (ranker.py:184-193); the device flag holds the
+                # first in CSR (feature-major) order, so rescan on the host
                 idx, offs = batch
-                offs_h = offs.cpu().numpy()
-                if 0 <= pos < int(offs_h[-1]):
-                    b = int(np.searchsorted(offs_h, pos, side="right") - 1)
-                    f, smp = divmod(b, self.B)
+                offs_h = offs.cpu().numpy().astype(np.int64)
+                idx_h = idx.cpu().numpy().astype(np.int64)
+                nbag = offs_h.size - 1
+                lens = np.diff(offs_h)
+                bag_of = np.repeat(np.arange(nbag), lens)
+                nrows = np.array([int(self.nrows[t].item()) for t in self.ftab], np.int64)
+                f_of = bag_of // self.B
+                bad = np.nonzero((idx_h < 0) | (idx_h >= nrows[f_of]))[0]
+                if bad.size:
+                    smp_of, fp = bag_of[bad] % self.B, f_of[bad]
+                    first = bad[np.lexsort((bad, fp, smp_of))[0]]
+                    f, smp = divmod(int(bag_of[first]), self.B)
                     t = self.ftab[f]
-                    n = int(self.nrows[t].item())
-                    raise LookupValidationError(f"batch {batch_id}, lookup {smp}: index {int(idx[pos].item())} "
-                                                f"out of range [0,{n}) for table {t}")
+                    raise LookupValidationError(f"batch {batch_id}, lookup {smp}: index {int(idx_h[first])} "
+                                                f"out of range [0,{int(nrows[f])}) for table {t}")
             raise LookupValidationError(f"batch {batch_id}: index out of range at CSR position {pos} "
                                         f"(rank {self.rank})")
         raise RoutingViolationError(f"rank {self.rank} was sent a row it does not host")
@@ -455,6 +465,10 @@ class P2PShardedLookup:
         from .store import table_block_device
         self._lib = _lib
         self.replicated = set(replicated_tables)
+        big = [m.table_id for m in (metas.values() if isinstance(metas, dict) else metas) if m.num_rows > 2**31 - 1]
+        if big:
+            # the pushes stage row indices as int32 for the owners' K4
+            raise ConfigError(f"tables {big} have more than 2^31-1 rows: the fused exchange stages int32 row ids")
         if partial_dtype not in ("f64", "f32"):
             raise ConfigError("partial_dtype must be 'f64' or 'f32'")
         # row-wise partials: f64 (bit-exact vs flat) or f32 (PartialResult semantics of the
@@ -836,8 +850,10 @@ class P2PShardedLookup:
         step k's fused gather runs, staging / outputs alternate between two
         buffer sets, and ONE barrier per step certifies both "every rank's push
         of step k landed" and "every rank's gather of step k-1 is done". A
-        yielded tensor is valid until the generator is advanced twice; consume
-        it on the current stream."""
+        yielded tensor is valid until the generator is advanced again (in
+        table-wise mode peer owners store the next-but-one step's rows into the
+        same buffer as soon as the next barrier completes); consume or copy it
+        on the current stream before advancing."""
         main = torch.cuda.current_stream(self.device)
         side = torch.cuda.Stream(self.device)
         # the gather runs on a high-priority stream so its blocks are scheduled

@@ -134,6 +134,9 @@ def pool_csr_device(table: torch.Tensor, row_begin: int, row_end: int, indices: 
         # partial mode leaves empty bags' rows unwritten (count 0 = partial absent)
         out = (torch.zeros if partial else torch.empty)((n_bags, D), dtype=torch.float64 if partial else torch.float32,
                                                         device=dev)
+    _lib.check_out(out, n_bags, D, dtype=torch.float64 if partial else torch.float32)
+    esz = 2 if partial else 1   # f64 outputs: 16 B = 2 elements
+    aligned = _lib.vec_ok((out.data_ptr(), out.stride(0) * esz), (table.data_ptr(), table.stride(0)))
     seg = _lib.FxSegment(table.data_ptr(), row_begin, row_end, 0, n_bags, out.data_ptr(), out.stride(0),
                          table.stride(0), D, op_code(op))
     segs = make_segments([seg], dev)
@@ -141,7 +144,8 @@ def pool_csr_device(table: torch.Tensor, row_begin: int, row_end: int, indices: 
     st = status or _lib.Status(dev)
     _lib.check(_lib.lib.fx_gather_pool(segs.data_ptr(), 1, D, indices.data_ptr(), _lib.idx_type_of(indices),
                                        offsets.data_ptr(), n_bags,
-                                       _lib.FX_OUT_F64_PARTIAL if partial else _lib.FX_OUT_F32,
+                                       (_lib.FX_OUT_F64_PARTIAL if partial else _lib.FX_OUT_F32)
+                                       | (0 if aligned else _lib.FX_OUT_SCALAR),
                                        _lib.ptr(counts), st.err.data_ptr(), bad_code, st.code.data_ptr(),
                                        _lib.stream_ptr()), "gather_pool")
     if own:

@@ -312,3 +312,61 @@ def test_dedup_bit_exact_vs_numpy_unique(P):
     # first-occurrence order: ordinals strictly increasing
     fo = res.first_ord.cpu().numpy()
     assert np.all(np.diff(fo) > 0)
+
+
+def test_pool_mixed_dims_unaligned_columns_and_out_checks(P):
+    """Mixed dims (30, 128): the D=128 feature's output column starts 120 B
+    into a 632-B row; K4 must take the scalar path there (a 16-B vector
+    store would fault) and still match the flat oracle. Bad `out` buffers are
+    rejected before any launch."""
+    from paper_2410_12794_b200.engine import CsrBatch, LookupEngine
+    from paper_2410_12794_b200.workload import DlrmBatchGen
+    rows, dims, B = (5000, 7000), (30, 128), 40
+    metas = [P.TableMeta(t, n, d) for t, (n, d) in enumerate(zip(rows, dims))]
+    dep = P.init_store(metas, [P.ShardSpec(t, 0, n, 0) for t, n in enumerate(rows)], 0)
+    hb = DlrmBatchGen(rows, 1.0, B, (1, 9), seed=8).next()
+    eng = LookupEngine(dep)
+    batch = CsrBatch(torch.from_numpy(hb.indices).cuda(), torch.from_numpy(hb.offsets).cuda(), hb.feature_tables,
+                     hb.feature_ops, B)
+    out = eng.pool(batch).cpu().numpy()
+    col = 0
+    for f, d in enumerate(dims):
+        for s in range(B):
+            b = f * B + s
+            ref = O.pool_flat(O.rows_of(0, f, d, hb.indices[hb.offsets[b]:hb.offsets[b + 1]]), "sum")
+            assert ref.tobytes() == out[s, col:col + d].tobytes()
+        col += d
+    with pytest.raises(P.ConfigError):
+        eng.pool(batch, out=torch.empty((B, 100), dtype=torch.float32, device="cuda"))
+    with pytest.raises(P.ConfigError):
+        eng.pool(batch, out=torch.empty((B, 158), dtype=torch.float64, device="cuda"))
+    # an output view at a 4-byte offset (unaligned): scalar path, same values
+    big = torch.empty((B, 159), dtype=torch.float32, device="cuda")
+    got = eng.pool(batch, out=big[:, 1:]).cpu().numpy()
+    assert np.array_equal(got, out)
+
+
+def test_host_stream_reports_the_failing_batch(P):
+    """HostLookup.stream: a bad index in the 3rd of 5 batches raises the
+    reference's message for THAT batch when it is yielded (per-slot status)."""
+    from paper_2410_12794_b200.engine import CsrBatch, HostLookup, LookupEngine
+    from paper_2410_12794_b200.workload import DlrmBatchGen
+    rows, D, B = (3000, 4000), 32, 16
+    dep = P.init_store([P.TableMeta(t, n, D) for t, n in enumerate(rows)],
+                       [P.ShardSpec(t, 0, n, 0) for t, n in enumerate(rows)], 0)
+    gen = DlrmBatchGen(rows, 1.0, B, (2, 6), seed=4)
+    hbs = [gen.next() for _ in range(5)]
+    bad = hbs[2].indices.copy()
+    b = 1 * B + 5
+    bad[hbs[2].offsets[b]] = 4000 + 3
+    batches = []
+    for i, hb in enumerate(hbs):
+        idx = bad if i == 2 else hb.indices
+        batches.append(CsrBatch(torch.from_numpy(idx).pin_memory(), torch.from_numpy(hb.offsets).pin_memory(),
+                                hb.feature_tables, hb.feature_ops, B))
+    hl = HostLookup(LookupEngine(dep))
+    got = []
+    with pytest.raises(P.LookupValidationError, match="batch 2, lookup 5: index 4003 out of range"):
+        for out in hl.stream(batches, depth=3):
+            got.append(out.clone())
+    assert len(got) == 2
