@@ -42,6 +42,32 @@ def run_compare(tables=32, rows=1_000_000, dim=128, batch=1024, pooling=(20, 20)
                         tracker=O.LoadTrackerO(16, 10 ** 9, 0), admit_per_batch=admit)
     rng = np.random.default_rng(seed)
     report = []
+    if depth > 1:
+        # batches in flight: compare the whole run's metrics and final state
+        # with the oracle's start/finish interleaving (ranker.py:161-182)
+        hbs = [gen.next() for _ in range(n_batches)]
+        rk.reserve(max(int(h.offsets[-1]) for h in hbs), max(h.offsets.size - 1 for h in hbs))
+        for i, hb in enumerate(hbs):
+            rk.execute_csr(torch.from_numpy(hb.indices).cuda(), torch.from_numpy(hb.offsets).cuda(),
+                           hb.feature_tables, hb.feature_ops, B, batch_id=i, sync=False)
+        rk.sync()
+        pv.run_trace([(*keys_sample_major(hb.indices, hb.offsets, hb.feature_tables, B), B, i)
+                      for i, hb in enumerate(hbs)], depth=depth)
+        bad = []
+        for mg, mo in zip(rk.batch_metrics, pv.metrics):
+            if (mg.cache_hits, mg.cache_misses, mg.raw_rows) != (mo["hits"], mo["misses"], mo["raw_rows"]):
+                bad.append(f"batch {mg.batch_id} metrics differ")
+        k, t, h = cache.lru_arrays()
+        if not (np.array_equal(k, cv.keys) and np.array_equal(t, cv.ticks) and np.array_equal(h, cv.hits_e)):
+            bad.append("final LRU differs")
+        if not np.array_equal(cache.eviction_log_array(), np.asarray(cv.evictions, np.uint64)):
+            bad.append("eviction log differs")
+        sk, sv = cache.sketch_arrays()
+        if not (np.array_equal(sk, cv.sk_keys) and np.array_equal(sv, cv.sk_vals)):
+            bad.append("sketch differs")
+        row = dict(batch=n_batches - 1, depth=depth, dyn=rk._step.scalars(0).get("dyn"), bad=bad)
+        log(row)
+        return [row], dict(rk=rk, cache=cache, dep=dep)
     for i in range(n_batches):
         hb = gen.next()
         idx = torch.from_numpy(hb.indices).cuda()

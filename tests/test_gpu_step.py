@@ -89,6 +89,17 @@ def test_small_cache_sequential_path(P, dep_cfg3):
     assert ctx["rk"]._step.scalars(0)["mode"] == 2  # MODE_SEQ
 
 
+@pytest.mark.parametrize("alpha,frac,depth", [(0.8, 0.01, 2), (1.0, 0.02, 3)])
+def test_pipeline_depth_csr_stream(P, dep_cfg3, alpha, frac, depth):
+    """execute_csr(sync=False) with pipeline_depth batches in flight vs the
+    oracle's start/finish interleaving: candidates cached by a later batch's
+    apply_pending take the dynamic-presence path."""
+    from step_harness import run_compare
+    rep, _ = run_compare(tables=32, rows=1_000_000, dim=128, batch=512, pooling=(1, 20), alpha=alpha,
+                         cache_frac=frac, n_batches=7, dep=dep_cfg3, depth=depth, admit=512, log=lambda r: None)
+    _assert_clean(rep)
+
+
 @pytest.mark.parametrize("which", [0, 1, 2, 3, 4])
 def test_pipeline_depth_replays_reference(P, golden_dir, which):
     from paper_2410_12794_b200 import cache as C
