@@ -659,6 +659,10 @@ def run_sharded(args, rank, world, local):
     clocks = sampler.stop()
     ms = ev0.elapsed_time(ev1)
     l1 = getattr(sl, "launches", None)
+    # a peer that stopped participating makes the spin barrier give up after
+    # ~10 s and set a flag: the timed steps are then void — raise
+    if hasattr(sl, "_check"):
+        sl._check()
     # per-phase device times from a separate profiled pass (events on every
     # phase would perturb the timed region)
     prof_steps = min(args.steps, 50)
@@ -710,6 +714,16 @@ def run_sharded(args, rank, world, local):
     achieved = pool_bytes_step / (pool_ms / 1e3) / 1e9 if pool_ms > 0 else None
     peak, peak_src = measured_peak()
     a2a_ms = float(t[2].item()) / args.steps if args.exchange == "nccl" else float(t[1].item()) / args.steps
+    step_ms = ms_max / args.steps
+    # fused compute+collective roofline (B200_PROFILING.md): the step cannot
+    # beat max(HBM bytes / HBM peak, NVLink bytes / measured 770 GB/s peer copy)
+    nvl_peak = 770.0
+    t_hbm = pool_bytes_step / (peak * 1e9) * 1e3
+    t_nvl = a2a_bytes / (nvl_peak * 1e9) * 1e3
+    fused_roof = {"hbm_bytes_per_step": pool_bytes_step, "nvlink_bytes_per_step": a2a_bytes,
+                  "target_ms": max(t_hbm, t_nvl), "bound": "hbm" if t_hbm >= t_nvl else "nvlink",
+                  "frac": max(t_hbm, t_nvl) / step_ms, "nvlink_peak_gbs": nvl_peak,
+                  "nvlink_gbs_over_step": a2a_bytes / (step_ms / 1e3) / 1e9}
     # e2e: pinned host CSR -> device -> sharded lookup -> pinned host out
     e2e = None
     if not args.no_e2e:
@@ -772,6 +786,7 @@ def run_sharded(args, rank, world, local):
                          "peak_source": peak_src, "kernel": "owner gather+pool (K4) launches, rank 0",
                          "bytes_per_step": pool_bytes_step, "pool_ms_per_step": pool_ms,
                          "pool_ms_per_step_all_ranks": pool_ms_ranks},
+            "fused_roofline": fused_roof,
             "a2a": {"bytes_sent_per_step_rank0": a2a_bytes, "ms_per_step_rank0": a2a_ms,
                     "gbs": (a2a_bytes / (a2a_ms / 1e3) / 1e9) if a2a_ms > 0 else None,
                     "peak_gbs": 900.0, "phases_ms_total": {k: round(v, 3) for k, v in phases.items()},
