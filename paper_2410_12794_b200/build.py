@@ -26,6 +26,12 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
          "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include")]
+# A/B builds: FX_EXTRA_NVCC="-DFX_F2D_ALU" FX_BUILD_TAG=f2d python build.py -> libflexemb_f2d.so
+FLAGS += os.environ.get("FX_EXTRA_NVCC", "").split()
+_TAG = os.environ.get("FX_BUILD_TAG", "")
+if _TAG:
+    BUILD = BUILD + "_" + _TAG
+    LIB = os.path.join(PKG, f"libflexemb_{_TAG}.so")
 
 
 def _newest_header() -> float:

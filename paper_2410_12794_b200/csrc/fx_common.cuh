@@ -48,6 +48,23 @@ __device__ __forceinline__ int64_t load_index(const IdxT *p) {
   return static_cast<int64_t>(__ldg(p));
 }
 
+// Exact f32 -> f64 widening. The default (FX_F2D_ALU undefined) is the
+// hardware conversion (F2F.F64.F32, XU pipe, quarter rate); FX_F2D_ALU builds
+// the double with integer ops on the ALU pipe (rebias the exponent, shift
+// the mantissa) and leaves only zero / denormal / inf / nan to F2F — an A/B
+// for K4's XU-pipe pressure (profiles/r2_summary.md).
+__device__ __forceinline__ double f2d(float x) {
+#ifdef FX_F2D_ALU
+  const uint32_t u = __float_as_uint(x);
+  const uint32_t e = (u >> 23) & 0xffu;
+  if (e == 0u || e == 0xffu) return static_cast<double>(x);
+  const uint32_t hi = (u & 0x80000000u) | ((e + 896u) << 20) | ((u >> 3) & 0xfffffu);
+  return __hiloint2double(static_cast<int>(hi), static_cast<int>(u << 29));
+#else
+  return static_cast<double>(x);
+#endif
+}
+
 // 128-bit streaming load of 4 floats; rows are read-only for the kernel's life.
 __device__ __forceinline__ float4 ldg_f4(const float *p) {
   float4 r;

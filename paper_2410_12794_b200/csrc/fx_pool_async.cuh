@@ -192,20 +192,20 @@ __global__ void __launch_bounds__(128, FX_POOL_MINB) k_pool_async(const fx_segme
         for (int u = 0; u < 4; ++u)
 #pragma unroll
           for (int k = 0; k < NCH; ++k) {
-            acc[k][0] += static_cast<double>(v[u][k].x);
-            acc[k][1] += static_cast<double>(v[u][k].y);
-            acc[k][2] += static_cast<double>(v[u][k].z);
-            acc[k][3] += static_cast<double>(v[u][k].w);
+            acc[k][0] += f2d(v[u][k].x);
+            acc[k][1] += f2d(v[u][k].y);
+            acc[k][2] += f2d(v[u][k].z);
+            acc[k][3] += f2d(v[u][k].w);
           }
       }
       for (; r < n; ++r) {
 #pragma unroll
         for (int k = 0; k < NCH; ++k) {
           const float4 v = *reinterpret_cast<const float4 *>(buf + r * ROWB + (k * G + gl) * 16);
-          acc[k][0] += static_cast<double>(v.x);
-          acc[k][1] += static_cast<double>(v.y);
-          acc[k][2] += static_cast<double>(v.z);
-          acc[k][3] += static_cast<double>(v.w);
+          acc[k][0] += f2d(v.x);
+          acc[k][1] += f2d(v.y);
+          acc[k][2] += f2d(v.z);
+          acc[k][3] += f2d(v.w);
         }
       }
       __syncwarp(gmask);
@@ -318,20 +318,20 @@ __global__ void __launch_bounds__(128, MINB) k_pool_bulk(const fx_segment *__res
         for (int u = 0; u < 4; ++u)
 #pragma unroll
           for (int k = 0; k < NCH; ++k) {
-            acc[k][0] += static_cast<double>(v[u][k].x);
-            acc[k][1] += static_cast<double>(v[u][k].y);
-            acc[k][2] += static_cast<double>(v[u][k].z);
-            acc[k][3] += static_cast<double>(v[u][k].w);
+            acc[k][0] += f2d(v[u][k].x);
+            acc[k][1] += f2d(v[u][k].y);
+            acc[k][2] += f2d(v[u][k].z);
+            acc[k][3] += f2d(v[u][k].w);
           }
       }
       for (; r < n; ++r) {
 #pragma unroll
         for (int k = 0; k < NCH; ++k) {
           const float4 v = *reinterpret_cast<const float4 *>(buf + r * ROWB + (k * G + gl) * 16);
-          acc[k][0] += static_cast<double>(v.x);
-          acc[k][1] += static_cast<double>(v.y);
-          acc[k][2] += static_cast<double>(v.z);
-          acc[k][3] += static_cast<double>(v.w);
+          acc[k][0] += f2d(v.x);
+          acc[k][1] += f2d(v.y);
+          acc[k][2] += f2d(v.z);
+          acc[k][3] += f2d(v.w);
         }
       }
       fence_proxy_async_smem();  // generic reads of buf before the next bulk writes into it

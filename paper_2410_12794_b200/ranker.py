@@ -209,7 +209,10 @@ class Ranker:
         # fused, sync-free batch step (csrc/fx_step.cu) when the deployment is
         # in its domain: one full shard per table on this GPU, one row size,
         # row keys only; otherwise the staged pipeline below
-        self._fast = bool(fused) and self._fast_domain()
+        self._init_fast_state(bool(fused) and self._fast_domain())
+
+    def _init_fast_state(self, fast: bool) -> None:
+        self._fast = fast
         self._step = None
         self._engine = None
         self._pool_stream = None

@@ -70,6 +70,7 @@ class ShardedRanker(Ranker):
         self._single_shard, self._table_shard = False, {}
         self.hits_from_cache = True
         self.profile, self.stage_ms, self._marks = False, {}, []
+        self._init_fast_state(False)  # the sharded pooling runs the staged pipeline
         self._occ_slot = None
         self.ftab, self.B = tuple(feature_tables), batch_size
         if cache is not None:
