@@ -693,6 +693,25 @@ class AdaptiveCache:
         if row_bytes_of is not None:
             for t in list(self._row_bytes) or []:
                 self.set_row_bytes(t, int(row_bytes_of(t)))
+        # tables the device does not know a row size for (no deployment bound):
+        # learn it the way the reference does — row_bytes_of(t), else the size
+        # of the fetched vector (cache.py:327-336)
+        keys, _ = self.sketch.ranked_arrays()
+        if keys.size:
+            rows_of_t = {}
+            for k in keys.tolist():
+                if k & POOLED_BIT:
+                    continue
+                rows_of_t.setdefault(k >> ROW_BITS, k & ((1 << ROW_BITS) - 1))
+            for t, r in rows_of_t.items():
+                if t in self._row_bytes:
+                    continue
+                if row_bytes_of is not None:
+                    self.set_row_bytes(t, int(row_bytes_of(t)))
+                elif fetcher is not None:
+                    vv = fetcher(t, r)
+                    if vv is not None:
+                        self.set_row_bytes(t, int(np.asarray(vv).size) * int(np.asarray(vv).itemsize))
         before = self._scalars()["pending"]
         staged = ctypes.c_int64(0)
         _lib.check(self._L.fx_cache_stage(self._h, -1 if limit is None else int(limit), ctypes.byref(staged),

@@ -1287,9 +1287,20 @@ __global__ void ks_stage_begin(CacheView c, StepView v, int64_t limit) {
   s->topk_n = 0;
 }
 
-// pass 0 over the whole sketch: histogram of the top 16 bits of vinv
+// pass 0 over the whole sketch: histogram of the top 16 bits of vinv. Decayed
+// counts take few distinct values, so lanes are merged per warp (match_any)
+// and bins per block in a shared-memory table before one global atomic per
+// (block, bin): plain global atomics on a handful of hot bins serialise.
 __global__ void __launch_bounds__(256) ks_topk_hist0(CacheView c, StepView v) {
+  constexpr int kSlots = 1024;
+  __shared__ int sbin[kSlots];
+  __shared__ int scnt[kSlots];
   if (!v.ss->stage_on) return;
+  for (int i = threadIdx.x; i < kSlots; i += blockDim.x) {
+    sbin[i] = -1;
+    scnt[i] = 0;
+  }
+  __syncthreads();
   const int lane = threadIdx.x & 31;
   for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); i0 < c.kcap;
        i0 += (int64_t)gridDim.x * blockDim.x) {
@@ -1300,8 +1311,20 @@ __global__ void __launch_bounds__(256) ks_topk_hist0(CacheView c, StepView v) {
       if (k != kEmpty && k != kTomb) bin = static_cast<int>(vinv_of(c.kval[i]) >> 48);
     }
     const unsigned peers = __match_any_sync(0xffffffffu, bin);
-    if (bin >= 0 && lane == __ffs(peers) - 1) atomicAdd(&v.tk_hist[bin], __popc(peers));
+    if (bin >= 0 && lane == __ffs(peers) - 1) {
+      int h = (bin * 40503) & (kSlots - 1), probe = 0;
+      for (; probe < kSlots; ++probe) {
+        const int prev = atomicCAS(&sbin[h], -1, bin);
+        if (prev == -1 || prev == bin) break;
+        h = (h + 1) & (kSlots - 1);
+      }
+      if (probe < kSlots) atomicAdd(&scnt[h], __popc(peers));
+      else atomicAdd(&v.tk_hist[bin], __popc(peers));  // table full: straight to global
+    }
   }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kSlots; i += blockDim.x)
+    if (scnt[i]) atomicAdd(&v.tk_hist[sbin[i]], scnt[i]);
 }
 
 // live entries whose top digit is <= the selected one: every key that can be

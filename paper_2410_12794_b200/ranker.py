@@ -338,6 +338,7 @@ class Ranker:
                 k4[1].record(side)
                 self.k4_events.append(k4)
         cnt = torch.empty((4, max(n_bags, 1)), dtype=torch.int32, device=dev)
+        self._mark("start")
         step.start(slot, lay.bag_table, lay.indices, lay.offsets, lay.sm_start, n_bags, nnz,
                    self.params.pushdown_threshold, cnt[0], cnt[1], cnt[2], cnt[3])
         rec = dict(slot=slot, batch_id=batch_id, size=n_lookups, nnz=nnz, out=out, cnt=cnt, ev0=ev0,
@@ -377,7 +378,9 @@ class Ranker:
         rec = self._inflight.pop(0)
         step, c = self._step, self.cache
         slot = rec["slot"]
+        self._mark("offer")
         step.offer(slot)
+        self._mark("maintain")
         level_before = (list(self.tracker.window), self._last_level) if self.tracker is not None else None
         rec["tracker_before"] = level_before
         stage_limit, age = 0, False
@@ -402,6 +405,8 @@ class Ranker:
                     stage_limit, age = max(0, int(self.params.admit_per_batch)), True
         if stage_limit or age:
             step.maintain(slot, stage_limit, age)
+        self._mark("end")
+        self._flush_marks()
         cur = torch.cuda.current_stream(self.device)
         cur.wait_stream(self._pool_stream)
         ev1 = torch.cuda.Event(enable_timing=True)

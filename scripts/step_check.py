@@ -75,7 +75,10 @@ def main():
                         cache=cache, policy=C.CachePolicy(C.MemoryModel(budget + 1_000 + B, 1_000, 1)),
                         tracker=C.LoadTracker(16, 10 ** 9, 0), fused=bool(a.fused))
             times = []
+            rk.profile = True
             for i, (idx, offs) in enumerate(dbs):
+                if i == a.warm:
+                    rk.stage_ms = {}
                 h = hbs[i]
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 torch.cuda.synchronize()
@@ -96,6 +99,8 @@ def main():
                                                                    "n_acc", "n_ev", "mode", "F", "n_levels",
                                                                    "chain_cycles")},
                               "capacity": cache.capacity(),
+                              "phase_ms_per_batch": {k: round(v / max(1, len(times)), 3)
+                                                     for k, v in rk.stage_ms.items()},
                               "fused": bool(a.fused), "threshold": thr}), flush=True)
             del rk, cache
             torch.cuda.empty_cache()
