@@ -374,6 +374,27 @@ int fx_step_scalars(fx_step *s, int32_t slot, int64_t *out, int64_t n, void *str
 const void *fx_step_scalars_device(fx_step *s, int32_t slot);
 int64_t fx_step_launches(fx_step *s);  /* kernels launched by this handle so far (CUB sweeps count 2) */
 
+
+/* ---- store (fx_store_create / fx_store_shard_view) ------------
+ * The shards a placement assigns to `my_rank`, allocated on `device` (row-major
+ * [end-start, dim] f32, ld = dim rounded up to 4) and materialised by K0 with
+ * the reference PRF (store.py:62-89, 228-251); the placement is validated
+ * like validate_placement (store.py:92-119: overlap / gap / end -> FX_E_CONFIG). */
+typedef struct fx_store fx_store;
+typedef struct fx_shard_desc { int32_t table; int32_t owner; int64_t start; int64_t end; } fx_shard_desc;
+int fx_store_create(fx_store **out, int32_t device, int32_t n_tables, const int64_t *rows, const int32_t *dims,
+                    int32_t n_shards, const fx_shard_desc *shards, int32_t my_rank, uint64_t seed, void *stream);
+int fx_store_destroy(fx_store *s);
+/* zero-copy view of the local shard holding (table, row); FX_E_ROUTING_VIOLATION when not hosted here */
+int fx_store_shard_view(fx_store *s, int32_t table, int64_t row, const float **base, int64_t *start, int64_t *end,
+                        int64_t *ld, int32_t *dim);
+/* [sync] read a kernel's device status pair (first bad position, FX_E_* code) */
+int fx_poll_error(const int32_t *err_code, const int64_t *err_pos, int32_t *code, int64_t *pos, void *stream);
+/* Collectives (SURVEY's fx_comm_init / fx_alltoallv) are not wrapped here: the
+ * C1/C2 exchange is torch.distributed (NCCL) in sharded.ShardedLookup, and the
+ * fused path replaces it with peer stores through fx_ipc_* / fx_push_csr /
+ * fx_rw_push*, driven by sharded.P2PShardedLookup. */
+
 #ifdef __cplusplus
 }
 #endif

@@ -1108,6 +1108,18 @@ int read_scalars(fx_cache *c, Scalars *h, cudaStream_t st) {
   return cuda_check(cudaStreamSynchronize(st), "scalars sync");
 }
 
+// rebuild the open-addressing index from the slots after fused steps (which
+// keep a dense index instead)
+int ensure_hash(fx_cache *c, cudaStream_t st) {
+  if (c->hash_valid) return FX_OK;
+  k_fill_u64<<<grid_for(c->v.hcap, 256), 256, 0, st>>>(c->v.hkeys, c->v.hcap, kEmpty);
+  k_index_rebuild<<<grid_for(c->v.scap, 256), 256, 0, st>>>(c->v);
+  cudaMemsetAsync(&c->v.sc->hash_tomb, 0, sizeof(long long), st);
+  FX_LAUNCH_CHECK("fx_cache: hash rebuild");
+  c->hash_valid = 1;
+  return FX_OK;
+}
+
 // LRU order of the live slots into w.lru_slot: the full order, or — when only
 // the `need` oldest entries can be touched (uniform entry size: every accept
 // evicts one entry) and need is small — just a sorted prefix covering them.
@@ -1434,6 +1446,7 @@ int fx_cache_capacity(fx_cache *c, int64_t *out3) {
 }
 
 int fx_cache_set_budget(fx_cache *c, int64_t budget, void *stream) {
+  { int hrc = ensure_hash(c, as_stream(stream)); if (hrc) return hrc; }
   c->queue_valid = 0;
   cudaStream_t st = as_stream(stream);
   cudaMemcpyAsync(&c->v.sc->budget, &budget, 8, cudaMemcpyHostToDevice, st);
@@ -1522,6 +1535,7 @@ int fx_cache_reserve_slots(fx_cache *c, int64_t slots, void *stream) {
   k_fill_u64<<<grid_for(nv.hcap, 256), 256, 0, st>>>(nv.hkeys, nv.hcap, kEmpty);
   k_index_rebuild<<<grid_for(nv.scap, 256), 256, 0, st>>>(nv);
   rc = cuda_check(cudaStreamSynchronize(st), "fx_cache_reserve_slots");
+  c->hash_valid = 1;  // rebuilt from the slots above
   void *old[] = {c->v.skey, c->v.skey2, c->v.stick, c->v.ssize, c->v.shits, c->v.rows, c->v.free_stack, c->v.hkeys,
                  c->v.hslot, c->v.pend};
   for (void *p : old) cudaFree(p);
@@ -1531,6 +1545,7 @@ int fx_cache_reserve_slots(fx_cache *c, int64_t slots, void *stream) {
 
 int fx_cache_probe(fx_cache *c, const uint64_t *uniq, const int32_t *mult, const int64_t *last_ord,
                    const int64_t *n_uniq_dev, int64_t n_uniq_host, int64_t nnz, int32_t *slot_out, void *stream) {
+  { int hrc = ensure_hash(c, as_stream(stream)); if (hrc) return hrc; }
   c->queue_valid = 0;
   cudaStream_t st = as_stream(stream);
   const int64_t work = n_uniq_dev ? nnz : n_uniq_host;
@@ -1543,11 +1558,13 @@ int fx_cache_probe(fx_cache *c, const uint64_t *uniq, const int32_t *mult, const
 
 int fx_cache_offer(fx_cache *c, const uint64_t *keys, int64_t n, const int32_t *sizes, const float *const *src_rows,
                    uint8_t *accepted, void *stream) {
+  { int hrc = ensure_hash(c, as_stream(stream)); if (hrc) return hrc; }
   c->queue_valid = 0;
   return run_offer(c, keys, n, 0, sizes, src_rows, accepted, as_stream(stream));
 }
 
 int fx_cache_apply_pending(fx_cache *c, int64_t *applied, void *stream) {
+  { int hrc = ensure_hash(c, as_stream(stream)); if (hrc) return hrc; }
   c->queue_valid = 0;
   cudaStream_t st = as_stream(stream);
   Scalars h;
@@ -1667,6 +1684,7 @@ static int rank_sketch_topk(fx_cache *c, cudaStream_t st, int64_t k, int64_t *n_
 }
 
 int fx_cache_stage(fx_cache *c, int64_t limit, int64_t *staged, void *stream) {
+  { int hrc = ensure_hash(c, as_stream(stream)); if (hrc) return hrc; }
   cudaStream_t st = as_stream(stream);
   Scalars h;
   int rc = read_scalars(c, &h, st);
@@ -1701,6 +1719,7 @@ int fx_cache_age(fx_cache *c, void *stream) {
 
 int fx_cache_lookup(fx_cache *c, const uint64_t *keys, int64_t n, float *rows_out, int32_t out_ld, int32_t *slot_out,
                     void *stream) {
+  { int hrc = ensure_hash(c, as_stream(stream)); if (hrc) return hrc; }
   if (n <= 0) return FX_OK;
   k_lookup_rows<<<grid_for(n * 32, 256), 256, 0, as_stream(stream)>>>(c->v, keys, n, rows_out, out_ld, slot_out);
   FX_LAUNCH_CHECK("fx_cache_lookup");
@@ -1799,6 +1818,7 @@ int fx_cache_advance_tick(fx_cache *c, int64_t n, void *stream) {
 
 int fx_cache_pooled_find(fx_cache *c, const uint64_t *key_a, const uint64_t *key_b, int64_t n, int32_t *slot_out,
                          void *stream) {
+  { int hrc = ensure_hash(c, as_stream(stream)); if (hrc) return hrc; }
   if (n <= 0) return FX_OK;
   k_pooled_find<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(c->v, key_a, key_b, n, slot_out);
   FX_LAUNCH_CHECK("fx_cache_pooled_find");
@@ -1806,6 +1826,7 @@ int fx_cache_pooled_find(fx_cache *c, const uint64_t *key_a, const uint64_t *key
 }
 
 int fx_cache_pooled_touch(fx_cache *c, const int32_t *slot, const int64_t *pos, int64_t n, void *stream) {
+  { int hrc = ensure_hash(c, as_stream(stream)); if (hrc) return hrc; }
   c->queue_valid = 0;
   if (n <= 0) return FX_OK;
   k_pooled_touch<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(c->v, slot, pos, n);
@@ -1823,6 +1844,7 @@ int fx_cache_read_slots(fx_cache *c, const int32_t *slot, int64_t n, float *out,
 
 int fx_cache_pooled_put(fx_cache *c, const uint64_t *key_a, const uint64_t *key_b, int64_t n, const int32_t *sizes,
                         int32_t uniform_size, const float *const *src_rows, void *stream) {
+  { int hrc = ensure_hash(c, as_stream(stream)); if (hrc) return hrc; }
   c->queue_valid = 0;
   cudaStream_t st = as_stream(stream);
   if (n <= 0) return FX_OK;

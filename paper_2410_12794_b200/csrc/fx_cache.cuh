@@ -177,4 +177,7 @@ struct fx_cache {
   int32_t *q = nullptr;
   int64_t q_cap = 0;
   int32_t queue_valid = 0;
+  // the fused step maintains a dense slot index instead of the hash below;
+  // hash_valid = 0 makes the next staged-pipeline entry point rebuild it
+  int32_t hash_valid = 1;
 };

@@ -89,7 +89,8 @@ struct StepScalars {
   long long n_levels, codes_on;  // distinct hard-victim estimates (<= 255 -> byte codes)
   long long chain_cycles;        // clock64 cycles of the decision chain (diagnostics)
   long long dyn;                 // a candidate was cached at offer time (several batches in flight)
-  long long pad[4];
+  long long claim_tag, claim_clear;  // dense dedup: this batch's tag; clear the claim words first
+  long long pad[2];
 };
 
 struct DEnt {       // per dedup-hash slot (one 16-byte line for the atomics); all-zero = empty
@@ -109,6 +110,8 @@ struct StepView {
   DEnt *dent;
   int32_t *dfraw;    // first raw-occurrence ordinal (threshold mode)
   int64_t dcap;
+  unsigned int *dclaim;  // dense per-row claim words (batch tag | first claimer's CSR position)
+  int32_t rep_bits;  // bits of the claimer position in a claim word
   int32_t *uniq;     // claimed dedup slots
   int32_t *claim;    // [max_nnz] per occurrence: the dedup slot it claimed, else -1
   double *dC;        // [dcap] sketch estimate after this batch's bump (misses)
@@ -126,6 +129,8 @@ struct StepView {
   double *cC;        // candidate estimates in offer order
   double *bmax;      // per kFine-block max of cC
   int32_t *q;        // the cache's LRU queue (fx_cache.q)
+  int32_t *didx;     // dense slot index: one int32 per table row (slot or -1)
+  const int64_t *kbase;  // per table: first dense position
   int32_t *qnew;     // [scap] V = compacted queue
   int32_t *sflag;    // [scap] epoch of the last hit
   double *E;         // [scap] victim estimates
@@ -219,6 +224,17 @@ __device__ __forceinline__ long long warp_append(unsigned long long *ctr, int wa
   return (long long)base + __popc(m & ((1u << lane) - 1u));
 }
 
+// Dense slot index: HBM is plentiful (4 bytes per table row, 1.28 GB for
+// cfg3's 320 M rows, 0.8 % of the tables), so the fast path maps (table, row)
+// to its cache slot directly — one 4-byte access instead of a hash probe
+// chain, and inserts / evictions are plain stores (no tombstones, no
+// rebuilds). The open-addressing hash of fx_cache.cu is rebuilt lazily from
+// the slots when a staged-pipeline entry point needs it.
+__device__ __forceinline__ int64_t dpos(const StepView &v, uint64_t key) {
+  return v.kbase[key >> kRowBitsC] + static_cast<int64_t>(key & kRowMask);
+}
+__device__ __forceinline__ int32_t d_find(const StepView &v, uint64_t key) { return v.didx[dpos(v, key)]; }
+
 __device__ __forceinline__ const float *row_src(const StepView &v, uint64_t key) {
   const int64_t t = static_cast<int64_t>(key >> kRowBitsC);
   const int64_t r = static_cast<int64_t>(key & kRowMask);
@@ -259,6 +275,11 @@ __global__ void ks_begin(CacheView c, StepView v, int64_t max_nnz) {
   s->err_at = ~0ull;
   v.gs->epoch += 1;  // global batch counter (slot hit marks)
   s->epoch = v.gs->epoch;
+  {  // dense-dedup tag in [1, 2^(32-rep_bits) - 1]; a new cycle clears the claim words
+    const long long ntag = (1ll << (32 - v.rep_bits)) - 1;
+    s->claim_tag = ((s->epoch - 1) % ntag) + 1;
+    s->claim_clear = (s->claim_tag == 1 && s->epoch > 1) ? 1 : 0;
+  }
   s->n_uniq = s->n_cand = s->n_hitu = s->n_nonhit = s->n_hard = s->n_rej = s->n_off = 0;
   s->dyn = 0;
   s->n_acc = s->n_ev = 0;
@@ -273,6 +294,12 @@ __global__ void ks_begin(CacheView c, StepView v, int64_t max_nnz) {
   s->rehash_sketch = ((live + tomb + max_nnz) * 10 > c.kcap * 7) ? 1 : 0;
   s->rehash_n = 0;
   if ((live + max_nnz) * 10 > c.kcap * 7) s->err = 2;  // sketch_capacity too small for this batch
+}
+
+__global__ void ks_claim_clear(StepView v, int64_t n_dense) {
+  if (!v.ss->claim_clear) return;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_dense; i += (int64_t)gridDim.x * blockDim.x)
+    v.dclaim[i] = 0u;
 }
 
 // in-place sketch rehash (drops tombstones): collect -> clear -> reinsert
@@ -327,7 +354,7 @@ __global__ void ks_apply_pending(CacheView c, StepView v) {
   const long long n = sc->pending;
   if (n <= 0) return;
   const long long S = v.S;
-  long long e = sc->entries, head = 0, ftop = sc->free_top, tick = sc->tick, nlog = sc->n_evlog, tombs = 0;
+  long long e = sc->entries, head = 0, ftop = sc->free_top, tick = sc->tick, nlog = sc->n_evlog;
   long long applied = 0;
   long long qlen = e;
   for (long long i = 0; i < n; ++i) {
@@ -336,7 +363,7 @@ __global__ void ks_apply_pending(CacheView c, StepView v) {
     if (lane == 0) {
       const int64_t kp = k_find(c, key);
       if (kp >= 0) c.kflag[kp] = 0;
-      const bool present = h_find(c, key) >= 0;
+      const bool present = d_find(v, key) >= 0;
       if (!present && S <= sc->budget) {
         while ((e + 1) * S > sc->budget && e > 0) {  // evict the LRU head
           const int32_t vs = v.q[head];
@@ -345,7 +372,7 @@ __global__ void ks_apply_pending(CacheView c, StepView v) {
           const uint64_t ok = c.skey[vs];
           if (c.evlog_cap > 0 && nlog < c.evlog_cap) c.evlog[nlog] = ok;
           if (c.evlog_cap > 0) ++nlog;
-          tombs += h_erase(c, ok) ? 1 : 0;
+          v.didx[dpos(v, ok)] = -1;
           c.stick[vs] = kFree;
           c.skey[vs] = kEmpty;
           c.free_stack[ftop++] = vs;
@@ -358,7 +385,7 @@ __global__ void ks_apply_pending(CacheView c, StepView v) {
         c.stick[slot] = tick;
         c.ssize[slot] = static_cast<int32_t>(S);
         c.shits[slot] = 0;
-        h_insert(c, key, slot);
+        v.didx[dpos(v, key)] = slot;
         v.q[qlen++] = slot;
         ++e;
         ++applied;
@@ -373,7 +400,6 @@ __global__ void ks_apply_pending(CacheView c, StepView v) {
     sc->free_top = ftop;
     sc->tick = tick;
     sc->n_evlog = nlog;
-    sc->hash_tomb += tombs;
     sc->pending = 0;
     v.ss->b_applied = applied;
   }
@@ -390,7 +416,8 @@ __global__ void __launch_bounds__(256) ks_dedup(StepView v, const int32_t *__res
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const uint64_t dm = static_cast<uint64_t>(v.dcap - 1);
+  const unsigned int tag = static_cast<unsigned int>(v.ss->claim_tag);
+  const unsigned int rmask = (1u << v.rep_bits) - 1u;
   for (int64_t b0 = warp * 32; b0 < n_bags; b0 += nw * 32) {
     const int64_t nb = n_bags - b0 < 32 ? n_bags - b0 : 32;
     const int64_t my = b0 + (lane < nb ? lane : nb - 1);
@@ -429,15 +456,19 @@ __global__ void __launch_bounds__(256) ks_dedup(StepView v, const int32_t *__res
           v.ss->err = 1;
         } else {
           const uint64_t key = (static_cast<uint64_t>(t) << kRowBitsC) | static_cast<uint64_t>(r);
-          uint64_t h = hash_key(key) & dm;
+          // dense claim word of the key: (batch tag << rep_bits) | the CSR
+          // position of this batch's first claimer, which becomes the key's
+          // unique id (per-unique data lives in nnz-sized arrays)
+          unsigned int *cw = &v.dclaim[v.kbase[t] + r];
+          const unsigned int mine = (tag << v.rep_bits) | static_cast<unsigned int>(p);
+          unsigned int w = *cw;
           while (true) {
-            const unsigned long long prev = atomicCAS(reinterpret_cast<unsigned long long *>(&v.dkey[h]),
-                                                      (unsigned long long)kEmpty, (unsigned long long)key);
-            if (prev == kEmpty) { claimed = true; break; }
-            if (prev == key) break;
-            h = (h + 1) & dm;
+            if ((w >> v.rep_bits) == tag) { u = static_cast<int32_t>(w & rmask); break; }
+            const unsigned int prev = atomicCAS(cw, w, mine);
+            if (prev == w) { u = static_cast<int32_t>(p); claimed = true; break; }
+            w = prev;
           }
-          u = static_cast<int32_t>(h);
+          if (claimed) v.dkey[u] = key;
           DEnt *e = &v.dent[u];
           atomicAdd(&e->mult, 1);
           atomicMax(&e->first, INT_MAX - ord);  // zero-initialised encodings (memset reset)
@@ -461,7 +492,7 @@ __global__ void __launch_bounds__(256) ks_probe(CacheView c, StepView v, int32_t
     const int32_t u = v.uniq[i];
     const uint64_t key = v.dkey[u];
     DEnt e = v.dent[u];
-    const int32_t s = h_find(c, key);
+    const int32_t s = d_find(v, key);
     if (s >= 0) {
       c.stick[s] = tick0 + d_last(e) + 1;
       c.shits[s] += e.mult;
@@ -583,7 +614,7 @@ __global__ void ks_offer_prep(CacheView c, StepView v, int64_t max_nnz, int32_t 
         f = 1;
         v.estv[j] = v.cest[j];
       } else {
-        f = h_find(c, key) < 0 ? 1 : 0;
+        f = d_find(v, key) < 0 ? 1 : 0;
         v.estv[j] = k_est(c, key);
         if (!f) v.ss->dyn = 1;
       }
@@ -1090,7 +1121,6 @@ __global__ void __launch_bounds__(256) ks_apply(CacheView c, StepView v) {
   const long long tick_base = v.ss->tick_base;
   const long long n_acc = n > 0 ? v.rank[n - 1] + v.acc[n - 1] : 0;
   const long long n_ev = n_acc > F ? n_acc - F : 0;
-  long long tombs = 0;
   for (int64_t j0 = blockIdx.x * (int64_t)blockDim.x; j0 < n; j0 += (int64_t)gridDim.x * blockDim.x) {
     const int64_t j = j0 + threadIdx.x;
     if (j < n && v.acc[j]) {
@@ -1105,18 +1135,18 @@ __global__ void __launch_bounds__(256) ks_apply(CacheView c, StepView v) {
         slot = v.q[q];
         const uint64_t ok = c.skey[slot];
         if (c.evlog_cap > 0 && log0 + q < c.evlog_cap) c.evlog[log0 + q] = ok;
-        tombs += h_erase(c, ok) ? 1 : 0;
+        v.didx[dpos(v, ok)] = -1;
       }
       c.skey[slot] = key;
       c.stick[slot] = tick_base + r + 1;
       c.shits[slot] = 0;
-      h_insert(c, key, slot);
+      v.didx[dpos(v, key)] = slot;
       v.qnew[e0 - n_ev + r] = slot;
       v.aslot[r] = slot;
       v.akey[r] = key;
     }
   }
-  block_add(reinterpret_cast<unsigned long long *>(&c.sc->hash_tomb), tombs);
+
 }
 
 // row copies of the accepts (both decision modes): thread per 16 bytes
@@ -1185,8 +1215,7 @@ __global__ void ks_offer_finish(CacheView c, StepView v) {
   } else if (s->mode == MODE_NONE) {
     s->qlen_new = s->e0;
   }
-  // keep the cache index below half tombstones (rebuilt by the next two kernels)
-  s->rebuild_index = ((sc->hash_tomb + sc->entries) * 2 > c.hcap) ? 1 : 0;
+  s->rebuild_index = 0;
 }
 
 // Exact sequential offers for batches outside the parallel domain
@@ -1197,12 +1226,12 @@ __global__ void ks_seq_offer(CacheView c, StepView v) {
   StepScalars *s = v.ss;
   Scalars *sc = c.sc;
   const long long n = s->n_off, e0 = s->e0, S = v.S, budget = sc->budget;
-  long long e = e0, h = 0, n_acc = 0, ftop = sc->free_top, tick = s->tick_base, nlog = sc->n_evlog, tombs = 0;
+  long long e = e0, h = 0, n_acc = 0, ftop = sc->free_top, tick = s->tick_base, nlog = sc->n_evlog;
   const bool sketch = c.admission == 0;
   auto vslot = [&](long long q) -> int32_t { return q < e0 ? v.q[q] : v.aslot[q - e0]; };
   for (long long j = 0; j < n; ++j) {
     const double cj = v.cC[j];
-    if (s->dyn && h_find(c, v.okey[j]) >= 0) continue;  // still cached: offer -> True, no side effect
+    if (s->dyn && d_find(v, v.okey[j]) >= 0) continue;  // still cached: offer -> True, no side effect
     if ((e + 1) * S > budget) {
       if (sketch && e > 0) {
         const int32_t vs = vslot(h);
@@ -1215,7 +1244,7 @@ __global__ void ks_seq_offer(CacheView c, StepView v) {
         const uint64_t ok = c.skey[vs];
         if (c.evlog_cap > 0 && nlog < c.evlog_cap) c.evlog[nlog] = ok;
         if (c.evlog_cap > 0) ++nlog;
-        tombs += h_erase(c, ok) ? 1 : 0;
+        v.didx[dpos(v, ok)] = -1;
         c.stick[vs] = kFree;
         c.skey[vs] = kEmpty;
         c.free_stack[ftop++] = vs;
@@ -1231,7 +1260,7 @@ __global__ void ks_seq_offer(CacheView c, StepView v) {
     c.stick[slot] = tick;
     c.ssize[slot] = static_cast<int32_t>(S);
     c.shits[slot] = 0;
-    h_insert(c, key, slot);
+    v.didx[dpos(v, key)] = slot;
     v.aslot[n_acc] = slot;
     v.akey[n_acc] = key;
     v.accj[n_acc] = static_cast<int32_t>(j);
@@ -1246,7 +1275,6 @@ __global__ void ks_seq_offer(CacheView c, StepView v) {
   sc->tick = tick;
   sc->free_top = ftop;
   sc->n_evlog = nlog;
-  sc->hash_tomb += tombs;
   sc->n_acc = n_acc;
   s->n_acc = n_acc;
   s->n_ev = h;
@@ -1497,7 +1525,7 @@ __global__ void __launch_bounds__(1024) ks_stage_finish(CacheView c, StepView v,
   for (long long r = threadIdx.x; r < m; r += blockDim.x) {  // -1: pending or cached (skipped)
     const uint64_t key = lo[ord[r]];
     const int64_t kp = k_find(c, key);
-    kpos[r] = (kp < 0 || c.kflag[kp] || h_find(c, key) >= 0) ? -1 : static_cast<int32_t>(kp);
+    kpos[r] = (kp < 0 || c.kflag[kp] || d_find(v, key) >= 0) ? -1 : static_cast<int32_t>(kp);
   }
   __syncthreads();
   if (threadIdx.x != 0) return;
@@ -1564,6 +1592,7 @@ struct fx_step {
   int stage_smem = 0;
   int64_t stage_limit_cap = 0;
   int64_t launches = 0;  // kernels this handle launched (CUB sweeps count 2)
+  int64_t n_dense = 0;   // dense slot index length (sum of table rows)
 };
 
 namespace {
@@ -1589,6 +1618,16 @@ __global__ void k_lru_sortkeys(CacheView c, long long *keys, int32_t *vals, long
     const long long t = c.stick[i];
     keys[i] = t == kFree ? free_key : t;
     vals[i] = static_cast<int32_t>(i);
+  }
+}
+
+// dense slot index from the slots (after any entry point that moved entries)
+__global__ void k_didx_fill(CacheView c, StepView v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < c.scap; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = c.skey[i];
+    if (c.stick[i] == kFree || (k >> 63)) continue;  // free slot / pooled-result key
+    const int64_t t = static_cast<int64_t>(k >> kRowBitsC);
+    if (t < v.n_tables) v.didx[dpos(v, k)] = static_cast<int32_t>(i);
   }
 }
 
@@ -1628,6 +1667,8 @@ int ensure_queue(fx_step *s, cudaStream_t st) {
   cub::DeviceRadixSort::SortPairs(tmp, need, k0, k1, v0, v1, static_cast<int>(scap), 0, 64, st);
   k_queue_from_sorted<<<grid_for(scap, 256), 256, 0, st>>>(c->v, v1, c->q, scap);
   cudaFreeAsync(tmp, st);
+  cudaMemsetAsync(s->v.didx, 0xff, s->n_dense * sizeof(int32_t), st);
+  k_didx_fill<<<grid_for(scap, 256), 256, 0, st>>>(c->v, s->v);
   FX_LAUNCH_CHECK("fx_step: queue rebuild");
   c->queue_valid = 1;
   return FX_OK;
@@ -1680,9 +1721,9 @@ int fx_step_create(fx_step **out, fx_cache *cache, int64_t max_nnz, int64_t max_
   int rc = FX_OK;
   rc = rc ? rc : salloc(s, &s->ss_base, slots + 1);
   rc = rc ? rc : salloc(s, &s->ckey_base, static_cast<size_t>(slots) * N);
-  rc = rc ? rc : salloc(s, &v.dkey, v.dcap);
-  rc = rc ? rc : salloc(s, &v.dent, v.dcap);
-  rc = rc ? rc : salloc(s, &v.dfraw, v.dcap);
+  rc = rc ? rc : salloc(s, &v.dkey, N);
+  rc = rc ? rc : salloc(s, &v.dent, N);
+  rc = rc ? rc : salloc(s, &v.dfraw, N);
   rc = rc ? rc : salloc(s, &v.uniq, N);
   rc = rc ? rc : salloc(s, &v.inv, N);
   rc = rc ? rc : salloc(s, &v.cand_by_first, N);
@@ -1711,7 +1752,7 @@ int fx_step_create(fx_step **out, fx_cache *cache, int64_t max_nnz, int64_t max_
   rc = rc ? rc : salloc(s, &v.aslot, N);
   rc = rc ? rc : salloc(s, &v.akey, N);
   rc = rc ? rc : salloc(s, &v.claim, N);
-  rc = rc ? rc : salloc(s, &v.dC, v.dcap);
+  rc = rc ? rc : salloc(s, &v.dC, N);
   rc = rc ? rc : salloc(s, &s->cest_base, static_cast<size_t>(slots) * N);
   rc = rc ? rc : salloc(s, &v.accj, N);
   rc = rc ? rc : salloc(s, &v.tk_key, v.tk_cap);
@@ -1735,6 +1776,35 @@ int fx_step_create(fx_step **out, fx_cache *cache, int64_t max_nnz, int64_t max_
   v.tbase = tb;
   v.tld = tl;
   v.trows = tr;
+  {
+    std::vector<int64_t> kb(n_tables);
+    int64_t tot = 0;
+    for (int32_t t = 0; t < n_tables; ++t) {
+      kb[t] = tot;
+      tot += table_rows[t] > 0 ? table_rows[t] : 0;
+    }
+    s->n_dense = tot > 0 ? tot : 1;
+    int64_t *kbd = nullptr;
+    rc = salloc(s, &kbd, n_tables);
+    rc = rc ? rc : salloc(s, &v.didx, static_cast<size_t>(s->n_dense));
+    rc = rc ? rc : salloc(s, &v.dclaim, static_cast<size_t>(s->n_dense));
+    if (rc) {
+      fx_step_destroy(s);
+      return rc;
+    }
+    cudaMemcpy(kbd, kb.data(), n_tables * sizeof(int64_t), cudaMemcpyHostToDevice);
+    v.kbase = kbd;
+    cudaMemset(v.dclaim, 0, static_cast<size_t>(s->n_dense) * sizeof(unsigned int));
+    int rb = 1;
+    while ((1ll << rb) < N) ++rb;
+    if (rb > 26) {
+      set_error("fx_step_create: max_nnz above 2^26 (dense dedup claim words)");
+      fx_step_destroy(s);
+      return FX_E_CONFIG;
+    }
+    v.rep_bits = rb;
+    cache->queue_valid = 0;  // the dense index is built with the queue
+  }
   const int big = static_cast<int>(N > SC ? N : SC);
   size_t b1 = 0, b2 = 0, b3 = 0, b4 = 0;
   cub::DeviceSelect::If(nullptr, b1, (const int32_t *)nullptr, (int32_t *)nullptr, (int64_t *)nullptr, big, NonNeg());
@@ -1821,9 +1891,10 @@ int fx_step_start(fx_step *s, int32_t slot, const int32_t *bag_table, const void
   ks_begin<<<1, 1, 0, st>>>(c, v, nnz);
   s->launches += 1;
   // dedup table reset: a memset beats clearing the claimed slots one by one
-  cudaMemsetAsync(v.dkey, 0xff, v.dcap * sizeof(uint64_t), st);
-  cudaMemsetAsync(v.dent, 0, v.dcap * sizeof(DEnt), st);
-  if (threshold > 0) cudaMemsetAsync(v.dfraw, 0, v.dcap * sizeof(int32_t), st);
+  cudaMemsetAsync(v.dent, 0, static_cast<size_t>(nnz > 0 ? nnz : 1) * sizeof(DEnt), st);
+  if (threshold > 0) cudaMemsetAsync(v.dfraw, 0, static_cast<size_t>(nnz > 0 ? nnz : 1) * sizeof(int32_t), st);
+  ks_claim_clear<<<grid_for(s->n_dense, 256), 256, 0, st>>>(v, s->n_dense);
+  s->launches += 1;
   ks_sketch_collect<<<grid_for(c.kcap, 256), 256, 0, st>>>(c, v);
   s->launches += 1;
   ks_sketch_clear<<<grid_for(c.kcap, 256), 256, 0, st>>>(c, v);
@@ -1880,6 +1951,7 @@ int fx_step_start(fx_step *s, int32_t slot, const int32_t *bag_table, const void
   ks_queue_append_hits<<<grid_for(nn, 256), 256, 0, st>>>(v);
   s->launches += 1;
   cudaMemcpyAsync(cc->q, v.qnew, SC * 4, cudaMemcpyDeviceToDevice, st);
+  cc->hash_valid = 0;  // the fast path keeps the dense index; the hash is rebuilt on demand
   FX_LAUNCH_CHECK("fx_step_start");
   return FX_OK;
 }
@@ -1938,10 +2010,6 @@ int fx_step_offer(fx_step *s, int32_t slot, void *stream) {
   ks_copy_rows<<<grid_for(static_cast<int64_t>(nn) * (v.dim / 4 + 1), 256), 256, 0, st>>>(c, v);
   s->launches += 1;
   ks_queue_commit<<<grid_for(SC, 256), 256, 0, st>>>(v, SC);
-  s->launches += 1;
-  ks_index_clear<<<grid_for(c.hcap, 256), 256, 0, st>>>(c, v);
-  s->launches += 1;
-  ks_index_fill<<<grid_for(SC, 256), 256, 0, st>>>(c, v);
   s->launches += 1;
   FX_LAUNCH_CHECK("fx_step_offer");
   return FX_OK;
