@@ -64,6 +64,9 @@ class ClockSampler:
         self.f = None
 
     def start(self):
+        if os.environ.get("FX_NO_CLOCKS") == "1":  # A/B of the sampler's own cost
+            self.proc = None
+            return
         try:
             self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
@@ -247,7 +250,9 @@ def main():
                     help="workload: cfg3 (N=1 default: full Ranker pipeline with the cache), cfg2 / cfg1 (K4 "
                          "alone), cfg4r (N>1 default), cfg4, cfg5")
     ap.add_argument("--cache", type=float, default=0.02, help="cfg3: cache budget as a fraction of all rows")
-    ap.add_argument("--graph-step", type=int, default=0, help="cfg3: replay the Ranker step as a CUDA graph")
+    ap.add_argument("--graph-step", type=int, default=1,
+                    help="cfg3: replay the whole Ranker batch as one CUDA graph (Ranker.capture_csr); 0 = eager "
+                         "execute_csr(sync=False) per batch")
     ap.add_argument("--batches", type=int, default=4, help="distinct batches cycled through")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -496,23 +501,60 @@ def run_ranker(args, rank, world, local):
     torch.cuda.synchronize()
     sampler = ClockSampler(local)
     sampler.start()
-    rk.k4_events = []
+    graph = None
+    if args.graph_step:
+        # static input buffers: each timed step copies its batch in (D2D, inside
+        # the timed region), then replays the captured batch
+        sidx, soffs = dbs[0][0].clone(), dbs[0][1].clone()
+        lc0 = rk._step.launches()
+        graph = rk.capture_csr(sidx, soffs, ft, fo, B)
+        n_graph_launches = rk._step.launches() - lc0  # step kernels recorded into the graph (+ K4)
+        torch.cuda.synchronize()
+        for i in range(2):  # graph warm-up replays on warm-up batches (cache state keeps evolving)
+            sidx.copy_(dbs[i][0])
+            soffs.copy_(dbs[i][1])
+            graph.replay(batch_id=-1 - i)
+        rk.sync()
+    # K4 alone, timed on its own stream over the timed batches (events inside
+    # a replayed graph are not available): the roofline kernel's launch time
+    k4_ev = []
+    pst = rk._pool_stream
+    for i in range(min(args.steps, n_timed)):
+        idx_, offs_ = dbs[args.warmup + i]
+        from paper_2410_12794_b200.dedup import sample_major_starts  # noqa: F401
+        out_ = torch.empty((B, T * D), dtype=torch.float32, device=dev)
+        e_a, e_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        pst.wait_stream(stream)
+        with torch.cuda.stream(pst):
+            e_a.record(pst)
+            from paper_2410_12794_b200.ranker import CsrLayout
+            rk._pool_sample_major(CsrLayout(idx_, offs_, None, None, None, [], None, None, None, B), out_, ft, fo, B)
+            e_b.record(pst)
+        k4_ev.append((e_a, e_b))
+    torch.cuda.synchronize()
+    k4_ms = [a.elapsed_time(b) for a, b in k4_ev]
     l0 = rk._step.launches()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     ev0.record(stream)
     th0 = time.perf_counter()
-    for i in range(args.steps):
-        rk.execute_csr(*dbs[args.warmup + i % n_timed], ft, fo, B, batch_id=args.warmup + i, sync=False)
+    if graph is not None:
+        for i in range(args.steps):
+            j = args.warmup + i % n_timed
+            sidx.copy_(dbs[j][0])
+            soffs.copy_(dbs[j][1])
+            graph.replay(batch_id=args.warmup + i)
+    else:
+        for i in range(args.steps):
+            rk.execute_csr(*dbs[args.warmup + i % n_timed], ft, fo, B, batch_id=args.warmup + i, sync=False)
     host_ms = (time.perf_counter() - th0) * 1e3 / args.steps
     ev1.record(stream)
     ev1.synchronize()
     torch.cuda.synchronize()
     clocks = sampler.stop()
-    launches = rk._step.launches() - l0 + len(rk.k4_events)
+    launches = ((n_graph_launches + 1) * args.steps if graph is not None
+                else rk._step.launches() - l0 + args.steps)
     ms = ev0.elapsed_time(ev1)
-    k4_ms = [a.elapsed_time(b) for a, b in rk.k4_events]
-    rk.k4_events = None
     rk.sync()
     mets = rk.batch_metrics[args.warmup:]
     hit = sum(m.cache_hits for m in mets) / max(1, sum(m.cache_hits + m.cache_misses for m in mets))
@@ -559,14 +601,16 @@ def run_ranker(args, rank, world, local):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32 rows, f64 accumulate", "data": "synthetic",
         "config": ranker_config(cfg, args.cache, {
-            "parallelism": "single", "l2": f"inputs larger than L2: {n_timed} distinct batches "
+            "parallelism": "single" + (", whole Ranker batch replayed as one CUDA graph" if graph is not None
+                                       else ""), "l2": f"inputs larger than L2: {n_timed} distinct batches "
             f"({tot_bytes / args.steps / 1e9:.2f} GB algorithmic bytes each) over {N * T * D * 4 / 1e9:.1f} GB of "
             f"tables + {budget / 1e9:.2f} GB of cached rows", "init_store_s": round(init_s, 2)}),
         "hit_rate": hit, "latency_ms": {"p50": lat[len(lat) // 2], "max": lat[-1]},
         "host_enqueue_ms_per_step": host_ms,
         "roofline": {"bound": "hbm", "achieved": k4_achieved, "peak": peak, "unit": "GB/s",
                      "frac": k4_achieved / peak, "traffic": None, "peak_source": peak_src,
-                     "kernel": "fx::k_pool_bulk (fused gather+pool K4, side stream of the Ranker step)",
+                     "kernel": "fx::k_pool_bulk (fused gather+pool K4 of the Ranker step, timed alone on its stream "
+                               "over the timed batches)",
                      "bytes_per_launch": tot_bytes / args.steps, "launch_ms": k4_mean,
                      "pipeline": {"achieved": pipe_achieved, "frac": pipe_achieved / peak,
                                   "note": "algorithmic bytes of the batch over the whole Ranker step (cache "

@@ -351,10 +351,20 @@ class Ranker:
         = bag (s, f)). The segment descriptors live on the device per batch
         shape; only their output pointers are patched per call, by a device
         op (no host->device copy, so the host never waits for the GPU)."""
+        F = len(ft)
+        D = out.shape[1] // F
+        seg, off = self._segs_for(ft, fo, B, D)
+        seg.view(torch.int64).view(F, _lib.SEGMENT_BYTES // 8)[:, _SEG_OUT] = off + out.data_ptr()
+        _lib.check(_lib.lib.fx_gather_pool(seg.data_ptr(), F, D, lay.indices.data_ptr(), _lib.idx_type_of(lay.indices),
+                                           lay.offsets.data_ptr(), F * B, _lib.FX_OUT_F32, None,
+                                           self._status.err.data_ptr(), _lib.FX_E_LOOKUP_VALIDATION,
+                                           self._status.code.data_ptr(), _lib.stream_ptr()), "gather_pool")
+
+    def _segs_for(self, ft, fo, B: int, D: int):
+        """Device segment descriptors of a batch shape (output pointers patched per call)."""
         key = (ft, fo, B)
         ent = self._fast_segs.get(key)
         F = len(ft)
-        D = out.shape[1] // F
         if ent is None:
             segs = []
             for f, (t, op) in enumerate(zip(ft, fo)):
@@ -365,12 +375,7 @@ class Ranker:
             off = seg.view(torch.int64).view(F, _lib.SEGMENT_BYTES // 8)[:, _SEG_OUT].clone()
             ent = (seg, off)
             self._fast_segs[key] = ent
-        seg, off = ent
-        seg.view(torch.int64).view(F, _lib.SEGMENT_BYTES // 8)[:, _SEG_OUT] = off + out.data_ptr()
-        _lib.check(_lib.lib.fx_gather_pool(seg.data_ptr(), F, D, lay.indices.data_ptr(), _lib.idx_type_of(lay.indices),
-                                           lay.offsets.data_ptr(), F * B, _lib.FX_OUT_F32, None,
-                                           self._status.err.data_ptr(), _lib.FX_E_LOOKUP_VALIDATION,
-                                           self._status.code.data_ptr(), _lib.stream_ptr()), "gather_pool")
+        return ent
 
     def _fast_finish(self) -> dict:
         """Offers + maintenance of the oldest in-flight batch (ranker.py:
@@ -418,6 +423,61 @@ class Ranker:
         rec["level"] = self._last_level
         self._pending.append(rec)
         return rec
+
+    def capture_csr(self, indices: torch.Tensor, offsets: torch.Tensor, feature_tables, feature_ops,
+                    batch_size: int) -> "RankerGraph":
+        """Record one whole fused Ranker batch — validation, dedup, probes,
+        plan, offers, maintenance (stage + age) and the K4 pooling on its side
+        stream — as ONE CUDA graph over the static device buffers `indices` /
+        `offsets` (table-major CSR of fixed size). `RankerGraph.replay()`
+        re-runs it on whatever the buffers hold, with the host-side policy
+        bookkeeping of a normal batch; a batch whose policy would change the
+        budget (or whose admission check would resize) runs eagerly instead.
+        Needs the fused step and pipeline_depth 1."""
+        if not getattr(self, "_fast", False) or int(self.params.pipeline_depth) != 1:
+            raise ConfigError("capture_csr needs the fused step and pipeline_depth 1")
+        self.sync()
+        dev = self.device
+        ft, fo, B = tuple(feature_tables), tuple(feature_ops), int(batch_size)
+        F = len(ft)
+        nnz, n_bags = int(indices.numel()), F * B
+        step = self._get_step(nnz, n_bags)
+        step.prepare()
+        key = (ft, B)
+        bt = self._fast_layouts.get(key)
+        if bt is None:
+            bt = torch.tensor(np.repeat(np.asarray(ft, np.int32), B), device=dev)
+            self._fast_layouts[key] = bt
+        D = next(iter(self.deployment.metas.values())).dim
+        self._segs_for(ft, fo, B, D)   # host -> device descriptor copy before capture
+        c = self.cache
+        if self._views is None or self._views[0] is not step:
+            self._views = (step, [step.scalars_tensor(k) for k in range(step.n_slots)], c.scalars_tensor())
+        stage_limit = max(0, int(self.params.admit_per_batch)) if self.params.adaptive_cache else 0
+        do_maint = self.tracker is not None and self.policy is not None and self.params.adaptive_cache
+        torch.cuda.synchronize(dev)
+        g = torch.cuda.CUDAGraph()
+        cap = torch.cuda.Stream(dev)
+        cap.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(cap):
+            with torch.cuda.graph(g, stream=cap):
+                sm = sample_major_starts(offsets, B, F)
+                lay = CsrLayout(indices, offsets, bt, sm, None, [], None, None, None, B)
+                out = torch.empty((B, F * D), dtype=torch.float32, device=dev)
+                cnt = torch.empty((4, max(n_bags, 1)), dtype=torch.int32, device=dev)
+                side = self._pool_stream
+                side.wait_stream(cap)
+                with torch.cuda.stream(side):
+                    self._pool_sample_major(lay, out, ft, fo, B)
+                step.start(0, bt, indices, offsets, sm, n_bags, nnz, self.params.pushdown_threshold, cnt[0], cnt[1],
+                           cnt[2], cnt[3])
+                step.offer(0)
+                if do_maint:
+                    step.maintain(0, stage_limit, True)
+                cap.wait_stream(side)
+                snap = torch.cat([self._views[1][0], self._views[2]])
+        torch.cuda.current_stream(dev).wait_stream(cap)
+        return RankerGraph(self, g, out, cnt, snap, (indices, offsets, ft, fo, B), do_maint)
 
     def _fail(self, rec, err: int, err_at: int):
         from .step import ERR_BAD_INDEX, BatchStep
@@ -1069,6 +1129,55 @@ class Ranker:
             cache_budget=(c.budget_bytes if c else None), cache_used=(c.used_bytes if c else None)))
         if self.params.keep_results:
             self.results[batch.batch_id] = results
+
+
+class RankerGraph:
+    """A captured fused Ranker batch (Ranker.capture_csr). `out` / `counters`
+    are static: they hold the last replay's pooled [B, F*D] vectors and per-bag
+    counters until the next replay."""
+
+    def __init__(self, rk, graph, out, cnt, snap, inputs, do_maint):
+        self.rk, self.graph, self.out, self.cnt, self.snap = rk, graph, out, cnt, snap
+        self.inputs = inputs
+        self.do_maint = do_maint
+
+    @property
+    def counters(self) -> dict:
+        c = self.cnt
+        return dict(cache_hits=c[0], pushdown_groups=c[1], pushdown_rows=c[2], raw_rows=c[3])
+
+    def replay(self, batch_id: int = 0) -> torch.Tensor:
+        rk = self.rk
+        idx, offs, ft, fo, B = self.inputs
+        c = rk.cache
+        if rk._admission_needs_resize(B):
+            raise ConfigError("the captured batch's admission check would resize the cache: run execute_csr")
+        rec = dict(batch_id=batch_id, size=B, lay=None, host=None, feature_shape=(ft, fo, B))
+        rec["tracker_before"] = (list(rk.tracker.window), rk._last_level) if rk.tracker is not None else None
+        if rk.tracker is not None and rk.policy is not None:
+            level = rk.tracker.record_batch(B)
+            rk._last_level = level.value
+            if rk.params.adaptive_cache and rk.policy.propose(c.budget_bytes, level,
+                                                              rk.tracker.windowed_value()) != c.budget_bytes:
+                # the graph bakes in "no budget change": undo and run this batch eagerly
+                win, lvl = rec["tracker_before"]
+                rk.tracker.window.clear()
+                rk.tracker.window.extend(win)
+                rk._last_level = lvl
+                out, cnt = rk.execute_csr(idx, offs, ft, fo, B, batch_id=batch_id, sync=False)
+                self.out.copy_(out)
+                return self.out
+        cur = torch.cuda.current_stream(rk.device)
+        if rk._epoch_ev is None:
+            rk._epoch_ev = torch.cuda.Event(enable_timing=True)
+            rk._epoch_ev.record(cur)
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(cur)
+        self.graph.replay()
+        ev1.record(cur)
+        rec.update(ev0=ev0, ev1=ev1, snap=self.snap.clone(), level=rk._last_level)
+        rk._pending.append(rec)
+        return self.out
 
 
 @dataclass

@@ -228,3 +228,43 @@ def test_stream_host_matches_execute_csr(P):
     assert [m.cache_hits for m in ra.batch_metrics] == [m.cache_hits for m in rb.batch_metrics]
     for x, y in zip(ra.cache.lru_arrays(), rb.cache.lru_arrays()):
         assert np.array_equal(x, y)
+
+
+def test_captured_batch_matches_eager(P):
+    """Ranker.capture_csr: one CUDA graph per Ranker batch, replayed over
+    static buffers, leaves exactly the state and metrics of eager batches."""
+    from paper_2410_12794_b200 import cache as C
+    from paper_2410_12794_b200.ranker import Ranker, RankerParams
+    from paper_2410_12794_b200.workload import DlrmBatchGen
+    T, N, D, B = 4, 60_000, 64, 256
+    metas = [P.TableMeta(t, N, D) for t in range(T)]
+    placement = [P.ShardSpec(t, 0, N, 0) for t in range(T)]
+    dep = P.init_store(metas, placement, 0)
+
+    def mk():
+        budget = 3000 * D * 4
+        cache = C.AdaptiveCache(budget, max_dim=D, slot_capacity=3001, sketch_capacity=200_000,
+                                record_evictions=True)
+        return Ranker(dep, P.build_routing(metas, placement), None, RankerParams(pushdown_threshold=None),
+                      cache=cache, policy=C.CachePolicy(C.MemoryModel(budget + 1000 + B, 1000, 1)),
+                      tracker=C.LoadTracker(16, 10 ** 9, 0))
+    ra, rb = mk(), mk()
+    hbs = [b for b in (DlrmBatchGen((N,) * T, 0.9, B, (10, 10), seed=2).next() for _ in range(8))]
+    ft, fo = hbs[0].feature_tables, hbs[0].feature_ops
+    dev = [(torch.from_numpy(h.indices).cuda(), torch.from_numpy(h.offsets).cuda()) for h in hbs]
+    ref = [ra.execute_csr(*dev[i], ft, fo, B, batch_id=i)[0].cpu().numpy() for i in range(8)]
+    rb.execute_csr(*dev[0], ft, fo, B, batch_id=0)
+    sidx, soffs = dev[1][0].clone(), dev[1][1].clone()
+    g = rb.capture_csr(sidx, soffs, ft, fo, B)
+    got = [None]
+    for i in range(1, 8):
+        sidx.copy_(dev[i][0])
+        soffs.copy_(dev[i][1])
+        got.append(g.replay(batch_id=i).cpu().numpy())
+    rb.sync()
+    for i in range(1, 8):
+        assert np.array_equal(ref[i], got[i]), i
+    assert [m.cache_hits for m in ra.batch_metrics] == [m.cache_hits for m in rb.batch_metrics]
+    for x, y in zip(ra.cache.lru_arrays(), rb.cache.lru_arrays()):
+        assert np.array_equal(x, y)
+    assert np.array_equal(ra.cache.eviction_log_array(), rb.cache.eviction_log_array())
