@@ -210,6 +210,7 @@ int fx_cache_set_tables(fx_cache *c, const fx_table_dir *dir, int32_t n_dir, con
 int fx_cache_scalars(fx_cache *c, int64_t *out21, void *stream);               /* [sync] */
 const void *fx_cache_scalars_device(fx_cache *c);  /* the 21 scalars in device memory (async snapshots) */
 int fx_cache_capacity(fx_cache *c, int64_t *out3);  /* slot, index and sketch table capacities */
+int fx_cache_queue_valid(fx_cache *c);  /* 1 while the fused step's LRU queue / dense index are current */
 int fx_cache_reserve_sketch(fx_cache *c, int64_t new_keys, void *stream);      /* [sync] */
 int fx_cache_reserve_slots(fx_cache *c, int64_t slots, void *stream);          /* [sync] */
 /* get() per unique key (cache.py:189-202): hit -> last_tick = tick0 +

@@ -115,7 +115,7 @@ _SIGS = {
         "fx_cache_sketch_bump", "fx_cache_sketch_ranked", "fx_cache_lru", "fx_cache_eviction_log",
         "fx_cache_pending", "fx_cache_last_evicted", "fx_cache_set_pending_rows", "fx_cache_set_parallel",
         "fx_cache_advance_tick", "fx_cache_pooled_find", "fx_cache_pooled_touch", "fx_cache_read_slots",
-        "fx_cache_pooled_put", "fx_cache_rows", "fx_cache_scalars_device", "fx_cache_capacity",
+        "fx_cache_pooled_put", "fx_cache_rows", "fx_cache_scalars_device", "fx_cache_capacity", "fx_cache_queue_valid",
         # fused batch step, typed in step.py
         "fx_step_create", "fx_step_destroy", "fx_step_prepare", "fx_step_start", "fx_step_offer", "fx_step_maintain",
         "fx_step_scalars", "fx_step_scalars_device", "fx_step_launches")},

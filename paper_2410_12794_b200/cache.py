@@ -208,6 +208,7 @@ def _sig():
         "fx_cache_pooled_put": [P, P, P, I64, P, I32, P, P],
         "fx_cache_scalars_device": [P],
         "fx_cache_capacity": [P, P],
+        "fx_cache_queue_valid": [P],
     }
     for n, a in sigs.items():
         f = getattr(L, n)
@@ -335,6 +336,12 @@ class AdaptiveCache:
         out = (ctypes.c_int64 * len(_SC))()
         _lib.check(self._L.fx_cache_scalars(self._h, out, _lib.stream_ptr()), "cache scalars")
         return dict(zip(_SC, list(out)))
+
+    def _queue_valid_host(self) -> bool:
+        """False after a staged-pipeline call moved entries (the fused step
+        then rebuilds its LRU queue on the host before launching — not
+        possible inside a captured graph)."""
+        return bool(self._L.fx_cache_queue_valid(self._h))
 
     def capacity(self) -> dict:
         out = (ctypes.c_int64 * 3)()

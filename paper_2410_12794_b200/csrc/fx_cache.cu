@@ -1438,6 +1438,8 @@ int fx_cache_scalars(fx_cache *c, int64_t *out, void *stream) {
 
 const void *fx_cache_scalars_device(fx_cache *c) { return c->v.sc; }
 
+int fx_cache_queue_valid(fx_cache *c) { return c->queue_valid; }
+
 int fx_cache_capacity(fx_cache *c, int64_t *out3) {
   out3[0] = c->v.scap;
   out3[1] = c->v.hcap;

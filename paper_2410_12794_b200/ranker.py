@@ -477,7 +477,7 @@ class Ranker:
                 cap.wait_stream(side)
                 snap = torch.cat([self._views[1][0], self._views[2]])
         torch.cuda.current_stream(dev).wait_stream(cap)
-        return RankerGraph(self, g, out, cnt, snap, (indices, offsets, ft, fo, B), do_maint)
+        return RankerGraph(self, g, out, cnt, snap, (indices, offsets, ft, fo, B), do_maint, step)
 
     def _fail(self, rec, err: int, err_at: int):
         from .step import ERR_BAD_INDEX, BatchStep
@@ -567,11 +567,19 @@ class Ranker:
         ft, fo, B = tuple(feature_tables), tuple(feature_ops), int(batch_size)
         D = next(iter(self.deployment.metas.values())).dim
         cur = torch.cuda.current_stream(dev)
-        s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
-        idx_d = [None] * depth
-        offs_d = [torch.empty(len(ft) * B + 1, dtype=torch.int64, device=dev) for _ in range(depth)]
         nout = depth + 1
-        outs_h = [torch.empty((B, len(ft) * D), dtype=torch.float32, pin_memory=True) for _ in range(nout)]
+        # streams, device input slots and pinned outputs persist across calls
+        # (pinned allocation is slow): one set per (depth, shape)
+        key = (depth, len(ft), B, D)
+        st = getattr(self, "_host_state", {}).get(key)
+        if st is None:
+            st = dict(streams=(torch.cuda.Stream(dev), torch.cuda.Stream(dev)), idx=[None] * depth,
+                      offs=[torch.empty(len(ft) * B + 1, dtype=torch.int64, device=dev) for _ in range(depth)],
+                      outs=[torch.empty((B, len(ft) * D), dtype=torch.float32, pin_memory=True)
+                            for _ in range(nout)])
+            self._host_state = {key: st}
+        s_in, s_out = st["streams"]
+        idx_d, offs_d, outs_h = st["idx"], st["offs"], st["outs"]
         free = [None] * depth          # compute finished with input slot k
         done = [None] * nout           # D2H of output slot k finished
         queue = []
@@ -1136,10 +1144,11 @@ class RankerGraph:
     are static: they hold the last replay's pooled [B, F*D] vectors and per-bag
     counters until the next replay."""
 
-    def __init__(self, rk, graph, out, cnt, snap, inputs, do_maint):
+    def __init__(self, rk, graph, out, cnt, snap, inputs, do_maint, step):
         self.rk, self.graph, self.out, self.cnt, self.snap = rk, graph, out, cnt, snap
         self.inputs = inputs
         self.do_maint = do_maint
+        self.step = step  # the graph bakes this step's buffers in (kept alive)
 
     @property
     def counters(self) -> dict:
@@ -1150,6 +1159,9 @@ class RankerGraph:
         rk = self.rk
         idx, offs, ft, fo, B = self.inputs
         c = rk.cache
+        if rk._step is not self.step or not c._queue_valid_host():
+            raise ConfigError("the Ranker rebuilt its fused step or another cache call moved entries since "
+                              "capture_csr: capture again")
         if rk._admission_needs_resize(B):
             raise ConfigError("the captured batch's admission check would resize the cache: run execute_csr")
         rec = dict(batch_id=batch_id, size=B, lay=None, host=None, feature_shape=(ft, fo, B))
