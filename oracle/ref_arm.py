@@ -38,11 +38,30 @@ def available() -> bool:
 
 
 def import_reference():
-    """Import embserve from oracle/_ref (never the product package)."""
+    """Import embserve from oracle/_ref (never the product package). If the
+    name is taken by something else (tests/_ref_alias maps `embserve` to the
+    mirror), the reference is loaded anyway and the previous entries are
+    restored afterwards for their users."""
     if not available():
         raise ImportError(f"{REF}/embserve is missing: run __graft_entry__.build() in the build container")
     if REF not in sys.path:
         sys.path.insert(0, REF)
+    cur = sys.modules.get("embserve")
+    if cur is not None and not os.path.abspath(getattr(cur, "__file__", "") or "").startswith(REF):
+        saved = {k: v for k, v in sys.modules.items() if k == "embserve" or k.startswith("embserve.")}
+        for k in saved:
+            del sys.modules[k]
+        try:
+            import embserve  # noqa: F401
+            import embserve.errors  # noqa: F401
+            import embserve.pooling  # noqa: F401
+            ref = {k: v for k, v in sys.modules.items() if k == "embserve" or k.startswith("embserve.")}
+        finally:
+            for k in list(sys.modules):
+                if k == "embserve" or k.startswith("embserve."):
+                    del sys.modules[k]
+            sys.modules.update(saved)
+        return ref["embserve"]
     import embserve  # noqa: F401
     if not os.path.abspath(embserve.__file__).startswith(REF):
         raise ImportError(f"embserve resolved to {embserve.__file__}, not the copy under {REF}")

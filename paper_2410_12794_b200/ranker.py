@@ -555,61 +555,96 @@ class Ranker:
                 self._get_step(st.max_nnz, st.max_bags)   # rebuilt now, not inside a later batch
 
     def stream_host(self, host_batches, feature_tables, feature_ops, batch_size: int, depth: int = 3,
-                    first_batch_id: int = 0):
+                    first_batch_id: int = 0, graphs: bool = True):
         """End-to-end batched API over HOST buffers: pinned host CSR batches
         (indices, offsets) in -> pinned host pooled [B, F*D] f32 out, in order.
-        Three streams overlap the H2D of batch k+1, the fused step + K4 of
-        batch k and the D2H of batch k-1. A yielded host tensor stays valid
-        until the generator is advanced again (copy it to keep it)."""
+        Three streams overlap the H2D of batch k+1, the Ranker batch k and the
+        D2H of batch k-1. With `graphs` (pipeline_depth 1) a batch is a replay
+        of one of two captured graphs (ping-pong over two static input / output
+        buffer sets, Ranker.capture_csr), so the host only enqueues copies and
+        a replay; a batch of another size runs eagerly. A yielded host tensor
+        stays valid until the generator is advanced again (copy it to keep it)."""
         if not getattr(self, "_fast", False):
             raise ConfigError("stream_host needs the fused step (one full shard per table, one row size)")
         dev = self.device
         ft, fo, B = tuple(feature_tables), tuple(feature_ops), int(batch_size)
         D = next(iter(self.deployment.metas.values())).dim
+        use_graphs = graphs and int(self.params.pipeline_depth) == 1
         cur = torch.cuda.current_stream(dev)
         nout = depth + 1
-        # streams, device input slots and pinned outputs persist across calls
-        # (pinned allocation is slow): one set per (depth, shape)
-        key = (depth, len(ft), B, D)
+        # streams, device input slots, graphs and pinned outputs persist
+        # across calls (pinned allocation and capture are slow)
+        key = (depth, ft, fo, B, D)
         st = getattr(self, "_host_state", {}).get(key)
         if st is None:
             st = dict(streams=(torch.cuda.Stream(dev), torch.cuda.Stream(dev)), idx=[None] * depth,
                       offs=[torch.empty(len(ft) * B + 1, dtype=torch.int64, device=dev) for _ in range(depth)],
                       outs=[torch.empty((B, len(ft) * D), dtype=torch.float32, pin_memory=True)
-                            for _ in range(nout)])
+                            for _ in range(nout)], graphs=None, gnnz=None)
             self._host_state = {key: st}
         s_in, s_out = st["streams"]
         idx_d, offs_d, outs_h = st["idx"], st["offs"], st["outs"]
-        free = [None] * depth          # compute finished with input slot k
+        free = [None] * depth          # the batch that read input slot k is done
         done = [None] * nout           # D2H of output slot k finished
+        gout_free = [None, None]       # D2H of a graph's static output finished
         queue = []
         for k, (idx_h, offs_h) in enumerate(host_batches):
-            sl = k % depth
-            if idx_d[sl] is None or idx_d[sl].numel() < idx_h.numel():
-                idx_d[sl] = torch.empty(max(idx_h.numel(), 1), dtype=idx_h.dtype, device=dev)
+            nnz = int(idx_h.numel())
+            graphed = use_graphs and (st["gnnz"] in (None, nnz))
+            sl = (k % 2) if graphed else k % depth
+            if graphed and st["graphs"] is None:
+                self.sync()
+                gi = [torch.empty(max(nnz, 1), dtype=idx_h.dtype, device=dev) for _ in range(2)]
+                go = [torch.empty(len(ft) * B + 1, dtype=torch.int64, device=dev) for _ in range(2)]
+                st["graphs"] = [self.capture_csr(gi[i], go[i], ft, fo, B) for i in range(2)]
+                st["gnnz"] = nnz
+            if graphed and (st["graphs"][0].step is not self._step or not self.cache._queue_valid_host()):
+                self.sync()
+                self.reserve(nnz, len(ft) * B)
+                self._step.prepare()
+                st["graphs"] = [self.capture_csr(g.inputs[0], g.inputs[1], ft, fo, B) for g in st["graphs"]]
+            if not graphed and (idx_d[sl] is None or idx_d[sl].numel() < nnz):
+                idx_d[sl] = torch.empty(max(nnz, 1), dtype=idx_h.dtype, device=dev)
             if len(queue) >= depth:    # output slot reuse: hand the oldest result out first
                 j, ev = queue.pop(0)
                 ev.synchronize()
                 yield outs_h[j % nout]
+            if graphed:
+                g = st["graphs"][sl]
+                idx_dev, offs_dev = g.inputs[0], g.inputs[1]
+            else:
+                idx_dev, offs_dev = idx_d[sl][:nnz], offs_d[sl]
             with torch.cuda.stream(s_in):
-                if free[sl] is not None:
-                    s_in.wait_event(free[sl])
-                idx_dev = idx_d[sl][:idx_h.numel()]
+                fr = (g.__dict__.get("free_ev") if graphed else free[sl])
+                if fr is not None:
+                    s_in.wait_event(fr)
                 idx_dev.copy_(idx_h, non_blocking=True)
-                offs_d[sl].copy_(offs_h, non_blocking=True)
+                offs_dev.copy_(offs_h, non_blocking=True)
                 ev_in = torch.cuda.Event()
                 ev_in.record(s_in)
             cur.wait_event(ev_in)
-            out, _ = self.execute_csr(idx_dev, offs_d[sl], ft, fo, B, batch_id=first_batch_id + k, sync=False)
-            free[sl] = torch.cuda.Event()
-            free[sl].record(cur)
+            if graphed:
+                if gout_free[sl] is not None:
+                    cur.wait_event(gout_free[sl])   # its static output was copied out
+                out = g.replay(batch_id=first_batch_id + k)
+                fe = torch.cuda.Event()
+                fe.record(cur)
+                g.free_ev = fe
+            else:
+                out, _ = self.execute_csr(idx_dev, offs_dev, ft, fo, B, batch_id=first_batch_id + k, sync=False)
+                fe = torch.cuda.Event()
+                fe.record(cur)
+                free[sl] = fe
             so = k % nout
             with torch.cuda.stream(s_out):
-                s_out.wait_event(free[sl])
-                out.record_stream(s_out)
+                s_out.wait_event(fe)
+                if not graphed:
+                    out.record_stream(s_out)
                 outs_h[so].copy_(out, non_blocking=True)
                 done[so] = torch.cuda.Event()
                 done[so].record(s_out)
+            if graphed:
+                gout_free[sl] = done[so]
             queue.append((k, done[so]))
         while queue:
             j, ev = queue.pop(0)

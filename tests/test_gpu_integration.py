@@ -22,9 +22,9 @@ def test_integration_stub_partial_pool(golden_dir):
     from oracle import ref_arm
     if not ref_arm.available():
         pytest.skip("oracle/_ref (the reference copy) is not built")
-    ref_arm.import_reference()
-    from embserve.errors import RoutingViolationError
-    from embserve.pooling import PartialResult
+    emb = ref_arm.import_reference()
+    RoutingViolationError = emb.errors.RoutingViolationError
+    PartialResult = emb.pooling.PartialResult
     text = open(os.path.join(ROOT, "INTEGRATION.md")).read()
     sec = text[text.index("## 2. C-ABI binding"):text.index("## 3.")]
     code = re.search(r"```python\n(.*?)```", sec, re.S).group(1)

@@ -200,9 +200,11 @@ def test_end_to_end_equivalence_check(P):
     assert rep.lookups_checked == 3 * B and rep.passed and rep.max_abs_diff == 0.0
 
 
-def test_stream_host_matches_execute_csr(P):
+@pytest.mark.parametrize("pooling", [(1, 9), (6, 6)])
+def test_stream_host_matches_execute_csr(P, pooling):
     """The end-to-end host API returns the same pooled vectors and leaves the
-    same cache state as device-resident execute_csr calls."""
+    same cache state as device-resident execute_csr calls: fixed-size batches
+    replay the two captured graphs, ragged ones mix graphs and eager batches."""
     from paper_2410_12794_b200 import cache as C
     from paper_2410_12794_b200.ranker import Ranker, RankerParams
     from paper_2410_12794_b200.workload import DlrmBatchGen
@@ -218,7 +220,8 @@ def test_stream_host_matches_execute_csr(P):
                       cache=cache, policy=C.CachePolicy(C.MemoryModel(budget + 1000 + B, 1000, 1)),
                       tracker=C.LoadTracker(16, 10 ** 9, 0))
     ra, rb = mk(), mk()
-    hbs = [b for b in (DlrmBatchGen((N,) * T, 1.0, B, (1, 9), seed=5).next() for _ in range(7))]
+    gen = DlrmBatchGen((N,) * T, 1.0, B, pooling, seed=5)
+    hbs = [gen.next() for _ in range(7)]
     ft, fo = hbs[0].feature_tables, hbs[0].feature_ops
     ref = [ra.execute_csr(torch.from_numpy(h.indices).cuda(), torch.from_numpy(h.offsets).cuda(), ft, fo, B,
                           batch_id=i)[0].cpu().numpy() for i, h in enumerate(hbs)]
