@@ -585,8 +585,8 @@ def run_ranker(args, rank, world, local):
         e2e_s = time.perf_counter() - t0
         e2e = {"value": bags * ksteps / e2e_s, "unit": "pooled lookups/s", "h2d_bytes_per_step": h2d // ksteps,
                "d2h_bytes_per_step": d2h // ksteps, "steps": ksteps,
-               "api": "Ranker.stream_host (pinned host CSR -> pinned host pooled [B, F*D]; H2D, fused cache step "
-                      "+ gather/pool and D2H on three streams; wall clock)"}
+               "api": "Ranker.stream_host (pinned host CSR -> pinned host pooled [B, F*D]; H2D, the whole Ranker "
+                      "batch (two captured graphs, ping-pong buffers) and D2H on three streams; wall clock)"}
 
     cpu = None
     if not args.no_cpu:
