@@ -406,78 +406,157 @@ __global__ void ks_apply_pending(CacheView c, StepView v) {
 }
 
 // ---------------------------------------------------------------- 2. validate + dedup
-// A warp takes 32 consecutive bags; its lanes walk the bags' occurrences 32
-// at a time, each lane locating its bag with a 5-step shuffle search over the
-// 33 bag offsets the warp holds.
+// A block takes 256 consecutive bags (32 per warp; a warp's lanes walk its
+// bags' occurrences 32 at a time, each lane locating its bag with a shuffle
+// search over the warp's 33 bag offsets). Occurrences are first merged per
+// block in a shared-memory table (key -> multiplicity, first / last ordinal,
+// first CSR position), so a hot key costs one global claim and three global
+// atomics per block instead of per occurrence (Zipf: the hottest row of a
+// cfg3 table occurs ~5,000 times per batch). The global step then claims the
+// key's dense claim word — (batch tag << rep_bits) | the CSR position of its
+// first claimer, which becomes the key's unique id (per-unique data lives in
+// nnz-sized arrays) — and folds the block's counts in.
+constexpr int kDBags = 256;     // bags per block chunk (8 warps x 32)
+constexpr int kDHash = 4096;    // shared-memory table entries per block
+constexpr size_t kDSmem = kDHash * (8 + 4 * 5);
+
+__device__ __forceinline__ int32_t dedup_global(const StepView &v, uint64_t key, int t, int64_t r, int rep,
+                                                unsigned int tag, unsigned int rmask, bool *claimed) {
+  unsigned int *cw = &v.dclaim[v.kbase[t] + r];
+  const unsigned int mine = (tag << v.rep_bits) | static_cast<unsigned int>(rep);
+  unsigned int w = *cw;
+  while (true) {
+    if ((w >> v.rep_bits) == tag) { *claimed = false; return static_cast<int32_t>(w & rmask); }
+    const unsigned int prev = atomicCAS(cw, w, mine);
+    if (prev == w) { *claimed = true; return rep; }
+    w = prev;
+  }
+}
+
 template <typename IdxT>
 __global__ void __launch_bounds__(256) ks_dedup(StepView v, const int32_t *__restrict__ bag_table,
                                                 const IdxT *__restrict__ idx, const int64_t *__restrict__ offsets,
                                                 const int64_t *__restrict__ sm_start, int64_t n_bags) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  unsigned long long *hkey = reinterpret_cast<unsigned long long *>(dsm);
+  int *hmult = reinterpret_cast<int *>(hkey + kDHash);
+  int *hfirst = hmult + kDHash;
+  int *hlast = hfirst + kDHash;
+  int *hrep = hlast + kDHash;
+  int *hu = hrep + kDHash;
   const int lane = threadIdx.x & 31;
-  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int wib = threadIdx.x >> 5;
   const unsigned int tag = static_cast<unsigned int>(v.ss->claim_tag);
   const unsigned int rmask = (1u << v.rep_bits) - 1u;
-  for (int64_t b0 = warp * 32; b0 < n_bags; b0 += nw * 32) {
-    const int64_t nb = n_bags - b0 < 32 ? n_bags - b0 : 32;
-    const int64_t my = b0 + (lane < nb ? lane : nb - 1);
-    const int64_t off = lane < nb ? __ldg(&offsets[b0 + lane]) : __ldg(&offsets[b0 + nb]);
-    const int64_t end = __ldg(&offsets[b0 + nb]);
-    const int32_t tab = __ldg(&bag_table[my]);
-    const int64_t sms = __ldg(&sm_start[my]);
-    const int64_t start = __shfl_sync(0xffffffffu, off, 0);
-    for (int64_t p0 = start; p0 < end; p0 += 32) {
-      const int64_t p = p0 + lane;
-      // bag j: last lane with off_j <= p
-      int lo = 0, hi = static_cast<int>(nb);
+  for (int i = threadIdx.x; i < kDHash; i += blockDim.x) {
+    hkey[i] = kEmpty;
+    hmult[i] = 0;
+    hfirst[i] = INT_MAX;
+    hlast[i] = -1;
+    hrep[i] = INT_MAX;
+  }
+  __syncthreads();
+  for (int64_t c0 = blockIdx.x * (int64_t)kDBags; c0 < n_bags; c0 += (int64_t)gridDim.x * kDBags) {
+    // ---- phase 1: occurrences -> block table
+    const int64_t b0 = c0 + wib * 32;
+    if (b0 < n_bags) {
+      const int64_t nb = n_bags - b0 < 32 ? n_bags - b0 : 32;
+      const int64_t my = b0 + (lane < nb ? lane : nb - 1);
+      const int64_t off = lane < nb ? __ldg(&offsets[b0 + lane]) : __ldg(&offsets[b0 + nb]);
+      const int64_t end = __ldg(&offsets[b0 + nb]);
+      const int32_t tab = __ldg(&bag_table[my]);
+      const int64_t sms = __ldg(&sm_start[my]);
+      const int64_t start = __shfl_sync(0xffffffffu, off, 0);
+      for (int64_t p0 = start; p0 < end; p0 += 32) {
+        const int64_t p = p0 + lane;
+        int lo = 0, hi = static_cast<int>(nb);  // bag j: last lane with off_j <= p
 #pragma unroll
-      for (int it = 0; it < 6; ++it) {
-        const int mid = (lo + hi) >> 1;
-        const int64_t om = __shfl_sync(0xffffffffu, off, mid & 31);
-        if (hi - lo > 1) {
-          if (om <= p) lo = mid; else hi = mid;
+        for (int it = 0; it < 6; ++it) {
+          const int mid = (lo + hi) >> 1;
+          const int64_t om = __shfl_sync(0xffffffffu, off, mid & 31);
+          if (hi - lo > 1) {
+            if (om <= p) lo = mid; else hi = mid;
+          }
         }
-      }
-      const int j = lo;
-      const int64_t bo = __shfl_sync(0xffffffffu, off, j);
-      const int32_t t = __shfl_sync(0xffffffffu, tab, j);
-      const int64_t sm = __shfl_sync(0xffffffffu, sms, j);
-      const bool act = p < end;
-      bool claimed = false;
-      int32_t u = -1;
-      int ord = 0;
-      if (act) {
+        const int j = lo;
+        const int64_t bo = __shfl_sync(0xffffffffu, off, j);
+        const int32_t t = __shfl_sync(0xffffffffu, tab, j);
+        const int64_t sm = __shfl_sync(0xffffffffu, sms, j);
+        if (p >= end) continue;
+        v.claim[p] = -1;
         const int64_t r = static_cast<int64_t>(idx[p]);
-        ord = static_cast<int>(sm + (p - bo));
-        const bool okt = t >= 0 && t < v.n_tables;
-        if (!okt || r < 0 || r >= v.trows[t]) {
+        const int ord = static_cast<int>(sm + (p - bo));
+        if (t < 0 || t >= v.n_tables || r < 0 || r >= v.trows[t]) {
           atomicMin(reinterpret_cast<unsigned long long *>(&v.ss->err_at),
                     (static_cast<unsigned long long>(ord) << 32) | static_cast<unsigned long long>(p & 0xffffffff));
           v.ss->err = 1;
-        } else {
-          const uint64_t key = (static_cast<uint64_t>(t) << kRowBitsC) | static_cast<uint64_t>(r);
-          // dense claim word of the key: (batch tag << rep_bits) | the CSR
-          // position of this batch's first claimer, which becomes the key's
-          // unique id (per-unique data lives in nnz-sized arrays)
-          unsigned int *cw = &v.dclaim[v.kbase[t] + r];
-          const unsigned int mine = (tag << v.rep_bits) | static_cast<unsigned int>(p);
-          unsigned int w = *cw;
-          while (true) {
-            if ((w >> v.rep_bits) == tag) { u = static_cast<int32_t>(w & rmask); break; }
-            const unsigned int prev = atomicCAS(cw, w, mine);
-            if (prev == w) { u = static_cast<int32_t>(p); claimed = true; break; }
-            w = prev;
+          v.inv[p] = -1;
+          continue;
+        }
+        const uint64_t key = (static_cast<uint64_t>(t) << kRowBitsC) | static_cast<uint64_t>(r);
+        int h = static_cast<int>(hash_key(key) & (kDHash - 1)), probe = 0;
+        for (; probe < 64; ++probe) {
+          const unsigned long long prev = atomicCAS(&hkey[h], (unsigned long long)kEmpty, (unsigned long long)key);
+          if (prev == kEmpty || prev == key) break;
+          h = (h + 1) & (kDHash - 1);
+        }
+        if (probe < 64) {
+          atomicAdd(&hmult[h], 1);
+          atomicMin(&hfirst[h], ord);
+          atomicMax(&hlast[h], ord);
+          atomicMin(&hrep[h], static_cast<int>(p));
+          v.inv[p] = -2 - h;  // resolved in phase 3
+        } else {              // block table crowded: straight to the global path
+          bool claimed = false;
+          const int32_t u = dedup_global(v, key, t, r, static_cast<int>(p), tag, rmask, &claimed);
+          if (claimed) {
+            v.dkey[u] = key;
+            v.claim[p] = u;
           }
-          if (claimed) v.dkey[u] = key;
           DEnt *e = &v.dent[u];
           atomicAdd(&e->mult, 1);
           atomicMax(&e->first, INT_MAX - ord);  // zero-initialised encodings (memset reset)
           atomicMax(&e->last, ord + 1);
           v.inv[p] = u;
         }
-        v.claim[p] = claimed ? u : -1;
       }
     }
+    __syncthreads();
+    // ---- phase 2: one global claim + fold per distinct key of the chunk
+    for (int i = threadIdx.x; i < kDHash; i += blockDim.x) {
+      const uint64_t key = hkey[i];
+      if (key == kEmpty) continue;
+      const int t = static_cast<int>(key >> kRowBitsC);
+      const int64_t r = static_cast<int64_t>(key & kRowMask);
+      bool claimed = false;
+      const int32_t u = dedup_global(v, key, t, r, hrep[i], tag, rmask, &claimed);
+      if (claimed) {
+        v.dkey[u] = key;
+        v.claim[u] = u;
+      }
+      DEnt *e = &v.dent[u];
+      atomicAdd(&e->mult, hmult[i]);
+      atomicMax(&e->first, INT_MAX - hfirst[i]);
+      atomicMax(&e->last, hlast[i] + 1);
+      hu[i] = u;
+    }
+    __syncthreads();
+    // ---- phase 3: occurrences learn their unique id; the table is reset
+    const int64_t pe = __ldg(&offsets[c0 + kDBags < n_bags ? c0 + kDBags : n_bags]);
+    for (int64_t p = __ldg(&offsets[c0]) + threadIdx.x; p < pe; p += blockDim.x) {
+      const int32_t w = v.inv[p];
+      if (w <= -2) v.inv[p] = hu[-2 - w];
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < kDHash; i += blockDim.x) {
+      if (hkey[i] == kEmpty) continue;
+      hkey[i] = kEmpty;
+      hmult[i] = 0;
+      hfirst[i] = INT_MAX;
+      hlast[i] = -1;
+      hrep[i] = INT_MAX;
+    }
+    __syncthreads();
   }
 }
 
@@ -1551,17 +1630,29 @@ __global__ void __launch_bounds__(1024) ks_stage_finish(CacheView c, StepView v,
 __global__ void __launch_bounds__(256) ks_age(CacheView c, StepView v) {
   if (v.ss->err) return;
   long long dead = 0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < c.kcap; i += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t k = c.kkeys[i];
-    if (k == kEmpty || k == kTomb) continue;
-    const double x = c.kval[i] * c.decay;
-    if (x < c.prune) {
-      c.kkeys[i] = kTomb;
-      c.kval[i] = 0.0;
-      c.kflag[i] = 0;
-      ++dead;
-    } else {
-      c.kval[i] = x;
+  // four table entries per thread and iteration: two 16-byte key loads, the
+  // value loads only for live entries, all issued before any is used
+  const int64_t n4 = c.kcap >> 2;
+  const ulonglong2 *k2 = reinterpret_cast<const ulonglong2 *>(c.kkeys);
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n4; q += (int64_t)gridDim.x * blockDim.x) {
+    const ulonglong2 a = k2[2 * q], b = k2[2 * q + 1];
+    const uint64_t kk[4] = {a.x, a.y, b.x, b.y};
+    double val[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) val[u] = (kk[u] != kEmpty && kk[u] != kTomb) ? c.kval[4 * q + u] : 0.0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (kk[u] == kEmpty || kk[u] == kTomb) continue;
+      const int64_t i = 4 * q + u;
+      const double x = val[u] * c.decay;
+      if (x < c.prune) {
+        c.kkeys[i] = kTomb;
+        c.kval[i] = 0.0;
+        c.kflag[i] = 0;
+        ++dead;
+      } else {
+        c.kval[i] = x;
+      }
     }
   }
   block_add(reinterpret_cast<unsigned long long *>(&c.sc->sketch_live), -dead);
@@ -1841,6 +1932,8 @@ int fx_step_create(fx_step **out, fx_cache *cache, int64_t max_nnz, int64_t max_
     return FX_E_CONFIG;
   }
   cudaFuncSetAttribute(ks_chain_codes, cudaFuncAttributeMaxDynamicSharedMemorySize, s->code_smem);
+  cudaFuncSetAttribute(ks_dedup<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kDSmem));
+  cudaFuncSetAttribute(ks_dedup<int64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kDSmem));
   {
     const int64_t need = ((N / 32 + 2 + 15) & ~15ll) + kRing;
     s->stream_smem = need + 1024 <= 227 * 1024 ? static_cast<int>(need) : 0;  // else the global-memory chain
@@ -1903,13 +1996,15 @@ int fx_step_start(fx_step *s, int32_t slot, const int32_t *bag_table, const void
   s->launches += 1;
   // validation + dedup first: a bad index aborts the batch before any state change
   if (n_bags > 0) {
-    const int g = grid_for((n_bags + 31) / 32 * 32, 256);
+    int g = static_cast<int>((n_bags + kDBags - 1) / kDBags);
+    const int gmax = num_sms() * 2;
+    if (g > gmax) g = gmax;
     if (idx_type == FX_IDX_I32)
-      ks_dedup<int32_t><<<g, 256, 0, st>>>(v, bag_table, static_cast<const int32_t *>(indices), offsets, sm_start,
-                                          n_bags);
+      ks_dedup<int32_t><<<g, 256, kDSmem, st>>>(v, bag_table, static_cast<const int32_t *>(indices), offsets,
+                                                sm_start, n_bags);
     else
-      ks_dedup<int64_t><<<g, 256, 0, st>>>(v, bag_table, static_cast<const int64_t *>(indices), offsets, sm_start,
-                                          n_bags);
+      ks_dedup<int64_t><<<g, 256, kDSmem, st>>>(v, bag_table, static_cast<const int64_t *>(indices), offsets,
+                                                sm_start, n_bags);
     s->launches += 1;
   }
   const int nn = static_cast<int>(nnz > 0 ? nnz : 1);
@@ -2046,7 +2141,7 @@ int fx_step_maintain(fx_step *s, int32_t slot, int64_t stage_limit, int32_t do_a
     s->launches += 1;
   }
   if (do_age) {
-    ks_age<<<grid_for(c.kcap, 256), 256, 0, st>>>(c, v);
+    ks_age<<<grid_for(c.kcap / 4, 256), 256, 0, st>>>(c, v);
     s->launches += 1;
   }
   FX_LAUNCH_CHECK("fx_step_maintain");
