@@ -56,6 +56,7 @@
 
 #include <climits>
 #include <cstring>
+#include <string>
 #include <vector>
 
 #include "fx_cache.cuh"
@@ -557,6 +558,98 @@ __global__ void __launch_bounds__(256) ks_dedup(StepView v, const int32_t *__res
       hrep[i] = INT_MAX;
     }
     __syncthreads();
+  }
+}
+
+// Default dedup (ks_dedup_occ): lanes of a warp holding the same key merge,
+// then one lane per key and warp does the global claim and atomics. The
+// block-merge variant above (FX_DEDUP=blk) measured slower except at
+// alpha 1.2 (ncu, cfg3 2 %: 375 / 223 / 127 us vs 135 / 132 / 208 us per-occurrence
+// at alpha 0.6 / 1.0 / 1.2).
+// A warp takes 32 consecutive bags; its lanes walk the bags' occurrences 32
+// at a time, each lane locating its bag with a 5-step shuffle search over the
+// 33 bag offsets the warp holds.
+template <typename IdxT>
+__global__ void __launch_bounds__(256) ks_dedup_occ(StepView v, const int32_t *__restrict__ bag_table,
+                                                const IdxT *__restrict__ idx, const int64_t *__restrict__ offsets,
+                                                const int64_t *__restrict__ sm_start, int64_t n_bags) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const unsigned int tag = static_cast<unsigned int>(v.ss->claim_tag);
+  const unsigned int rmask = (1u << v.rep_bits) - 1u;
+  for (int64_t b0 = warp * 32; b0 < n_bags; b0 += nw * 32) {
+    const int64_t nb = n_bags - b0 < 32 ? n_bags - b0 : 32;
+    const int64_t my = b0 + (lane < nb ? lane : nb - 1);
+    const int64_t off = lane < nb ? __ldg(&offsets[b0 + lane]) : __ldg(&offsets[b0 + nb]);
+    const int64_t end = __ldg(&offsets[b0 + nb]);
+    const int32_t tab = __ldg(&bag_table[my]);
+    const int64_t sms = __ldg(&sm_start[my]);
+    const int64_t start = __shfl_sync(0xffffffffu, off, 0);
+    for (int64_t p0 = start; p0 < end; p0 += 32) {
+      const int64_t p = p0 + lane;
+      // bag j: last lane with off_j <= p
+      int lo = 0, hi = static_cast<int>(nb);
+#pragma unroll
+      for (int it = 0; it < 6; ++it) {
+        const int mid = (lo + hi) >> 1;
+        const int64_t om = __shfl_sync(0xffffffffu, off, mid & 31);
+        if (hi - lo > 1) {
+          if (om <= p) lo = mid; else hi = mid;
+        }
+      }
+      const int j = lo;
+      const int64_t bo = __shfl_sync(0xffffffffu, off, j);
+      const int32_t t = __shfl_sync(0xffffffffu, tab, j);
+      const int64_t sm = __shfl_sync(0xffffffffu, sms, j);
+      const bool act = p < end;
+      bool claimed = false;
+      int32_t u = -1;
+      int ord = 0;
+      uint64_t key = ~0ull - 2;  // lanes without a valid occurrence get a key no occurrence has
+      int64_t r = 0;
+      if (act) {
+        r = static_cast<int64_t>(idx[p]);
+        ord = static_cast<int>(sm + (p - bo));
+        const bool okt = t >= 0 && t < v.n_tables;
+        if (!okt || r < 0 || r >= v.trows[t]) {
+          atomicMin(reinterpret_cast<unsigned long long *>(&v.ss->err_at),
+                    (static_cast<unsigned long long>(ord) << 32) | static_cast<unsigned long long>(p & 0xffffffff));
+          v.ss->err = 1;
+        } else {
+          key = (static_cast<uint64_t>(t) << kRowBitsC) | static_cast<uint64_t>(r);
+        }
+      }
+      // lanes of the warp holding the same key merge first (Zipf: the hottest
+      // rows repeat within a window of 32 occurrences), then the group's
+      // lowest lane — also its first CSR position — does the global work
+      const unsigned peers = __match_any_sync(0xffffffffu, key);
+      const int leader = __ffs(peers) - 1;
+      const bool valid = key < (~0ull - 2);
+      const int gmin = __reduce_min_sync(peers, static_cast<unsigned>(ord));
+      const int gmax = __reduce_max_sync(peers, static_cast<unsigned>(ord));
+      if (valid && lane == leader) {
+        unsigned int *cw = &v.dclaim[v.kbase[t] + r];
+        const unsigned int mine = (tag << v.rep_bits) | static_cast<unsigned int>(p);
+        unsigned int w = *cw;
+        while (true) {
+          if ((w >> v.rep_bits) == tag) { u = static_cast<int32_t>(w & rmask); break; }
+          const unsigned int prev = atomicCAS(cw, w, mine);
+          if (prev == w) { u = static_cast<int32_t>(p); claimed = true; break; }
+          w = prev;
+        }
+        if (claimed) v.dkey[u] = key;
+        DEnt *e = &v.dent[u];
+        atomicAdd(&e->mult, __popc(peers));
+        atomicMax(&e->first, INT_MAX - gmin);  // zero-initialised encodings (memset reset)
+        atomicMax(&e->last, gmax + 1);
+      }
+      u = __shfl_sync(peers, u, leader);
+      if (act) {
+        if (valid) v.inv[p] = u;
+        v.claim[p] = claimed ? u : -1;
+      }
+    }
   }
 }
 
@@ -1999,12 +2092,22 @@ int fx_step_start(fx_step *s, int32_t slot, const int32_t *bag_table, const void
     int g = static_cast<int>((n_bags + kDBags - 1) / kDBags);
     const int gmax = num_sms() * 2;
     if (g > gmax) g = gmax;
-    if (idx_type == FX_IDX_I32)
+    static const bool occ = !(getenv("FX_DEDUP") && std::string(getenv("FX_DEDUP")) == "blk");
+    if (occ) {
+      const int go = grid_for((n_bags + 31) / 32 * 32, 256);
+      if (idx_type == FX_IDX_I32)
+        ks_dedup_occ<int32_t><<<go, 256, 0, st>>>(v, bag_table, static_cast<const int32_t *>(indices), offsets,
+                                                  sm_start, n_bags);
+      else
+        ks_dedup_occ<int64_t><<<go, 256, 0, st>>>(v, bag_table, static_cast<const int64_t *>(indices), offsets,
+                                                  sm_start, n_bags);
+    } else if (idx_type == FX_IDX_I32) {
       ks_dedup<int32_t><<<g, 256, kDSmem, st>>>(v, bag_table, static_cast<const int32_t *>(indices), offsets,
                                                 sm_start, n_bags);
-    else
+    } else {
       ks_dedup<int64_t><<<g, 256, kDSmem, st>>>(v, bag_table, static_cast<const int64_t *>(indices), offsets,
                                                 sm_start, n_bags);
+    }
     s->launches += 1;
   }
   const int nn = static_cast<int>(nnz > 0 ? nnz : 1);
