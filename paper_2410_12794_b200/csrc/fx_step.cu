@@ -91,7 +91,8 @@ struct StepScalars {
   long long chain_cycles;        // clock64 cycles of the decision chain (diagnostics)
   long long dyn;                 // a candidate was cached at offer time (several batches in flight)
   long long claim_tag, claim_clear;  // dense dedup: this batch's tag; clear the claim words first
-  long long pad[2];
+  long long dedup_merge;   // (global block) merge a warp's equal keys in the next dedup
+  long long pad[1];
 };
 
 struct DEnt {       // per dedup-hash slot (one 16-byte line for the atomics); all-zero = empty
@@ -561,11 +562,12 @@ __global__ void __launch_bounds__(256) ks_dedup(StepView v, const int32_t *__res
   }
 }
 
-// Default dedup (ks_dedup_occ): lanes of a warp holding the same key merge,
-// then one lane per key and warp does the global claim and atomics. The
-// block-merge variant above (FX_DEDUP=blk) measured slower except at
-// alpha 1.2 (ncu, cfg3 2 %: 375 / 223 / 127 us vs 135 / 132 / 208 us per-occurrence
-// at alpha 0.6 / 1.0 / 1.2).
+// Default dedup (ks_dedup_occ): one lane per occurrence does the dense claim
+// and the entry atomics; on skewed batches lanes of a warp holding the same
+// key merge first. ncu, cfg3 2 %, alpha 0.6 / 1.0 / 1.2: per-occurrence
+// 135 / 132 / 208 us, warp-merged 183 / 162 / 125 us, block-merge variant
+// above (FX_DEDUP=blk) 375 / 223 / 127 us — hence the switch on the previous
+// batch's unique fraction (0.97 / 0.48 / 0.17 at those alphas).
 // A warp takes 32 consecutive bags; its lanes walk the bags' occurrences 32
 // at a time, each lane locating its bag with a 5-step shuffle search over the
 // 33 bag offsets the warp holds.
@@ -578,6 +580,7 @@ __global__ void __launch_bounds__(256) ks_dedup_occ(StepView v, const int32_t *_
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const unsigned int tag = static_cast<unsigned int>(v.ss->claim_tag);
   const unsigned int rmask = (1u << v.rep_bits) - 1u;
+  const bool merge = v.gs->dedup_merge != 0;
   for (int64_t b0 = warp * 32; b0 < n_bags; b0 += nw * 32) {
     const int64_t nb = n_bags - b0 < 32 ? n_bags - b0 : 32;
     const int64_t my = b0 + (lane < nb ? lane : nb - 1);
@@ -620,14 +623,19 @@ __global__ void __launch_bounds__(256) ks_dedup_occ(StepView v, const int32_t *_
           key = (static_cast<uint64_t>(t) << kRowBitsC) | static_cast<uint64_t>(r);
         }
       }
-      // lanes of the warp holding the same key merge first (Zipf: the hottest
-      // rows repeat within a window of 32 occurrences), then the group's
-      // lowest lane — also its first CSR position — does the global work
-      const unsigned peers = __match_any_sync(0xffffffffu, key);
+      // skewed batches (unique fraction < 0.35 in the previous batch): lanes
+      // of the warp holding the same key merge first, then the group's lowest
+      // lane — also its first CSR position — does the global work; otherwise
+      // every lane is its own group (the warp match costs more than it saves)
+      unsigned peers = 1u << lane;
+      int gmin = ord, gmax = ord;
+      if (merge) {
+        peers = __match_any_sync(0xffffffffu, key);
+        gmin = __reduce_min_sync(peers, static_cast<unsigned>(ord));
+        gmax = __reduce_max_sync(peers, static_cast<unsigned>(ord));
+      }
       const int leader = __ffs(peers) - 1;
       const bool valid = key < (~0ull - 2);
-      const int gmin = __reduce_min_sync(peers, static_cast<unsigned>(ord));
-      const int gmax = __reduce_max_sync(peers, static_cast<unsigned>(ord));
       if (valid && lane == leader) {
         unsigned int *cw = &v.dclaim[v.kbase[t] + r];
         const unsigned int mine = (tag << v.rep_bits) | static_cast<unsigned int>(p);
@@ -691,6 +699,9 @@ __global__ void ks_after_probe(CacheView c, StepView v, int64_t nnz) {
   if (aborted(v)) return;
   v.ss->tick0 = c.sc->tick;
   c.sc->tick += nnz;  // one tick per probed occurrence (cache.py:193)
+  // few distinct keys -> hot keys repeat inside a warp's 32 occurrences and
+  // their same-address atomics serialise: the next dedup merges them first
+  v.gs->dedup_merge = (v.ss->n_uniq * 20 < nnz * 7) ? 1 : 0;
 }
 
 // ---------------------------------------------------------------- 4. plan + counters
