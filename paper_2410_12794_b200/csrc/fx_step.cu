@@ -1059,7 +1059,8 @@ __global__ void __launch_bounds__(256) ks_cand_codes(StepView v) {
     int m = code;
     for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
     if ((threadIdx.x & 31) == 0 && j < n) v.bsum[j >> 5] = static_cast<uint8_t>(m);
-  }
+  }  // the streamed chain reads whole 16-byte words: codes past n are zero
+  if (blockIdx.x == 0 && threadIdx.x < 32) v.code[n + threadIdx.x] = 0;
 }
 
 // The decision chain on byte codes: per hard victim one 32-byte probe of the
@@ -1139,8 +1140,19 @@ constexpr int kRing = 1 << 16;        // ring bytes (power of two)
 constexpr int kProdWarps = 16;        // producer warps (1..16)
 constexpr int kProdUnroll = 2;        // 16-byte loads in flight per producer thread
 constexpr int kChunk = kProdWarps * 32 * 16 * kProdUnroll;  // bytes per producer round
+constexpr int kSumPad = 64;           // zero per-32 maxima past the last block
 
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
+__device__ __forceinline__ long long ld_acquire_cta(const volatile long long *p) {
+  long long v;
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(const_cast<const long long *>(p)));
+  asm volatile("ld.acquire.cta.shared::cta.b64 %0, [%1];" : "=l"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_cta(volatile long long *p, long long v) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(const_cast<const long long *>(p)));
+  asm volatile("st.release.cta.shared::cta.b64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
+}
 
 __global__ void __launch_bounds__(1024) ks_chain_stream(StepView v) {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -1151,8 +1163,11 @@ __global__ void __launch_bounds__(1024) ks_chain_stream(StepView v) {
   const long long n = v.ss->n_off, F = v.ss->F, nh = v.ss->n_hard;
   const long long nblk = (n + 31) >> 5;
   uint8_t *sum = smem;
-  uint8_t *ring = smem + ((nblk + 15) & ~15ll);
-  for (long long b = threadIdx.x; b < nblk; b += blockDim.x) sum[b] = v.bsum[b];
+  uint8_t *ring = smem + ((nblk + kSumPad + 15) & ~15ll);  // sum[] zero-padded past nblk
+  for (long long b = threadIdx.x; b < nblk / 16; b += blockDim.x)
+    reinterpret_cast<int4 *>(sum)[b] = __ldg(reinterpret_cast<const int4 *>(v.bsum) + b);
+  for (long long b = nblk / 16 * 16 + threadIdx.x; b < nblk + kSumPad; b += blockDim.x)
+    sum[b] = b < nblk ? v.bsum[b] : 0;
   if (threadIdx.x == 0) {
     filled = F & ~15ll;
     consumed = F & ~15ll;
@@ -1170,9 +1185,9 @@ __global__ void __launch_bounds__(1024) ks_chain_stream(StepView v) {
         while (true) {
           const long long c = consumed;
           st = ppos > (c & ~15ll) ? ppos : (c & ~15ll);
-          if (done || st >= n || st + kChunk <= c + kRing) break;
+          if (done || st >= n + 256 || st + kChunk <= c + kRing) break;
         }
-        pstart = (done || st >= n) ? -1 : st;
+        pstart = (done || st >= n + 256) ? -1 : st;  // the ring runs 256 zero codes past n
       }
       named_bar(1, kProdWarps * 32);
       const long long st = pstart;
@@ -1188,86 +1203,106 @@ __global__ void __launch_bounds__(1024) ks_chain_stream(StepView v) {
         const long long p = st + (static_cast<long long>(u) * kProdWarps * 32 + pt) * 16;
         *reinterpret_cast<int4 *>(ring + (p & (kRing - 1))) = tmp[u];
       }
-      __threadfence_block();
-      named_bar(1, kProdWarps * 32);
+      named_bar(1, kProdWarps * 32);  // orders every producer's ring stores before pt 0's release
       if (pt == 0) {
         ppos = st + kChunk;
-        filled = st + kChunk;
+        st_release_cta(&filled, st + kChunk);
       }
     }
     return;
   }
   if (warp != 0) return;
-  // ---- the chain
+  // ---- the chain: 32-bit positions (n <= max_nnz < 2^31), every probe from
+  // shared memory. A step reads a 256-candidate window at x (8 codes per
+  // lane, byte-wise compares) and, in the same round, the per-32 maxima of
+  // the 32 blocks after it; only a longer reject run scans further. The next
+  // hard victim's (position, rank) is fetched a step ahead; codes past n are
+  // zero (and ranks >= 1), so no probe needs an upper bound check.
   const long long t_start = clock64();
-  long long x = F, h = 0, nrej = 0;
-  long long fl = 0, pub = F & ~15ll;  // last seen `filled`, last published `consumed`
-  for (long long k0 = 0; k0 < nh; k0 += 32) {
-    const long long kk = k0 + lane;
-    const int32_t hp = kk < nh ? v.hard[kk] : 0;
-    const int hr = kk < nh ? v.hrank[kk] : 0;
-    const int cnt = nh - k0 < 32 ? static_cast<int>(nh - k0) : 32;
-    bool stop = false;
-    for (int t = 0; t < cnt; ++t) {
-      const long long b = __shfl_sync(0xffffffffu, hp, t);
-      const int r = __shfl_sync(0xffffffffu, hr, t);
-      const long long gap = b - h;
-      if (x + gap >= n) { x = n; stop = true; break; }
-      x += gap;
-      h = b;
-      // next j >= x with code >= r: rest of x's 32-block from the ring, else
-      // the first later block whose maximum reaches r (shared-memory scan)
-      if (x >= pub + 4096) {  // publish progress so producers can reuse ring space
-        pub = x & ~15ll;
-        if (lane == 0) consumed = pub;
+  const int n32 = static_cast<int>(n), nb32 = static_cast<int>(nblk);
+  const int nh32 = static_cast<int>(nh);
+  int x = static_cast<int>(F), h = 0, nrej = 0;
+  int pub = x & ~31;  // last published `consumed`
+  int fl = 0;         // last seen `filled`
+  int thr = -1;       // a window at w > thr must refresh `filled` or publish progress
+  const int lane8 = 8 * lane;
+  int hp = lane < nh32 ? v.hard[lane] : 0, hpn = 32 + lane < nh32 ? v.hard[32 + lane] : 0;
+  unsigned hr = lane < nh32 ? v.hrank[lane] * 0x01010101u : 0u;  // rank in every byte
+  unsigned hrn = 32 + lane < nh32 ? v.hrank[32 + lane] * 0x01010101u : 0u;
+  int b_nx = __shfl_sync(0xffffffffu, hp, 0);
+  unsigned rr_nx = __shfl_sync(0xffffffffu, hr, 0);
+  for (int k = 0; k < nh32; ++k) {
+    const int b = b_nx;
+    const unsigned rr = rr_nx;
+    const int r = static_cast<int>(rr & 0xffu);
+    const int t = (k + 1) & 31;
+    if (t == 0) {
+      hp = hpn;
+      hr = hrn;
+      const int kk = k + 33 + lane;
+      hpn = kk < nh32 ? v.hard[kk] : 0;
+      hrn = kk < nh32 ? v.hrank[kk] * 0x01010101u : 0u;
+    }
+    b_nx = __shfl_sync(0xffffffffu, hp, t);
+    rr_nx = __shfl_sync(0xffffffffu, hr, t);
+    x += b - h;  // easy victims between take one candidate each
+    if (x >= n32) break;
+    h = b + 1;
+    const int w = x & ~31;
+    if (w > thr) {  // rare: publish progress / wait for the window's codes
+      pub = w;
+      if (lane == 0) consumed = pub;
+      while ((fl = static_cast<int>(ld_acquire_cta(&filled))) < w + 256) {
       }
-      const long long blk = x >> 5;
-      long long need = blk * 32 + 32 < n ? blk * 32 + 32 : n;
-      if (need > fl) {
-        if (lane == 0) consumed = x & ~15ll;
-        pub = x & ~15ll;
-        while ((fl = filled) < need) {
+      thr = min(fl - 256, pub + 16384);
+    }
+    const uint2 q = *reinterpret_cast<const uint2 *>(ring + ((w + lane8) & (kRing - 1)));
+    const int sm = sum[(w >> 5) + 8 + lane];
+    unsigned long long M = (static_cast<unsigned long long>(__vcmpgeu4(q.y, rr)) << 32) | __vcmpgeu4(q.x, rr);
+    const int o = x & 31;  // lanes below o/8 hold codes below x; lane o/8 drops o%8
+    M &= ~0ull << (lane == (o >> 3) ? (o & 7) * 8 : 0);
+    const int byte = (__ffsll(static_cast<long long>(M)) - 1) >> 3;
+    const unsigned mw = __ballot_sync(0xffffffffu, M != 0ull) & (0xffffffffu << (o >> 3));
+    int j;
+    if (mw) {
+      const int L = __ffs(mw) - 1;
+      j = w + 8 * L + __shfl_sync(0xffffffffu, byte, L);
+    } else {
+      int B = nb32;
+      const unsigned mb = __ballot_sync(0xffffffffu, sm >= r);
+      if (mb) {
+        B = (w >> 5) + 8 + __ffs(mb) - 1;
+      } else {
+        for (int b0 = (w >> 5) + 40; b0 < nb32; b0 += 32) {
+          const int bb = b0 + lane;
+          const unsigned m3 = __ballot_sync(0xffffffffu, sum[bb] >= r);  // zero-padded past nblk
+          if (m3) { B = b0 + __ffs(m3) - 1; break; }
         }
-        __threadfence_block();
       }
-      long long j = n;
-      const long long p1 = blk * 32 + lane;
-      const int c1 = p1 < n ? ring[p1 & (kRing - 1)] : 0;
-      long long B = nblk;
-      for (long long b0 = blk + 1; b0 < nblk; b0 += 32) {
-        const long long bb = b0 + lane;
-        const unsigned mb = __ballot_sync(0xffffffffu, bb < nblk && sum[bb] >= r);
-        if (mb) { B = b0 + __ffs(mb) - 1; break; }
-      }
-      const unsigned m1 = __ballot_sync(0xffffffffu, p1 >= x && p1 < n && c1 >= r);
-      if (m1) {
-        j = blk * 32 + __ffs(m1) - 1;
-      } else if (B < nblk) {
-        need = B * 32 + 32 < n ? B * 32 + 32 : n;
-        if (need > fl) {
-          if (lane == 0) consumed = (B * 32) & ~15ll;
+      if (B >= nb32) {
+        j = n32;
+      } else {
+        if (B * 32 + 32 > fl) {
           pub = B * 32;
-          while ((fl = filled) < need) {
+          if (lane == 0) consumed = pub;
+          while ((fl = static_cast<int>(ld_acquire_cta(&filled))) < B * 32 + 32) {
           }
-          __threadfence_block();
+          thr = min(fl - 256, pub + 16384);
         }
-        const long long p2 = B * 32 + lane;
-        const int c2 = p2 < n ? ring[p2 & (kRing - 1)] : 0;
-        const unsigned m2 = __ballot_sync(0xffffffffu, p2 < n && c2 >= r);
+        const int c2 = ring[(B * 32 + lane) & (kRing - 1)];
+        const unsigned m2 = __ballot_sync(0xffffffffu, c2 >= r);
         j = B * 32 + __ffs(m2) - 1;  // m2 != 0: the block's maximum reaches r
       }
-      if (j > x) {
-        if (lane == 0) {
-          v.rj_beg[nrej] = static_cast<int32_t>(x);
-          v.rj_end[nrej] = static_cast<int32_t>(j);
-        }
-        ++nrej;
-      }
-      if (j >= n) { x = n; stop = true; break; }
-      x = j + 1;
-      h = b + 1;
     }
-    if (stop) break;
+    if (j > x) {
+      if (lane == 0) {
+        v.rj_beg[nrej] = x;
+        v.rj_end[nrej] = j;
+      }
+      ++nrej;
+    }
+    if (j >= n32) break;
+    x = j + 1;
   }
   if (lane == 0) {
     v.ss->n_rej = nrej;
@@ -2039,7 +2074,7 @@ int fx_step_create(fx_step **out, fx_cache *cache, int64_t max_nnz, int64_t max_
   cudaFuncSetAttribute(ks_dedup<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kDSmem));
   cudaFuncSetAttribute(ks_dedup<int64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kDSmem));
   {
-    const int64_t need = ((N / 32 + 2 + 15) & ~15ll) + kRing;
+    const int64_t need = ((N / 32 + 2 + kSumPad + 15) & ~15ll) + kRing;
     s->stream_smem = need + 1024 <= 227 * 1024 ? static_cast<int>(need) : 0;  // else the global-memory chain
     if (s->stream_smem)
       cudaFuncSetAttribute(ks_chain_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, s->stream_smem);
