@@ -516,7 +516,8 @@ def run_ranker(args, rank, world, local):
             graph.replay(batch_id=-1 - i)
         rk.sync()
     # K4 alone, timed on its own stream over the timed batches (events inside
-    # a replayed graph are not available): the roofline kernel's launch time
+    # a replayed graph are not available): the roofline kernel's launch time,
+    # at full occupancy (inside the step it shares the SMs: FX_OUT_SHARE)
     k4_ev = []
     pst = rk._pool_stream
     for i in range(min(args.steps, n_timed)):
@@ -528,7 +529,8 @@ def run_ranker(args, rank, world, local):
         with torch.cuda.stream(pst):
             e_a.record(pst)
             from paper_2410_12794_b200.ranker import CsrLayout
-            rk._pool_sample_major(CsrLayout(idx_, offs_, None, None, None, [], None, None, None, B), out_, ft, fo, B)
+            rk._pool_sample_major(CsrLayout(idx_, offs_, None, None, None, [], None, None, None, B), out_, ft, fo, B,
+                                  share=False)
             e_b.record(pst)
         k4_ev.append((e_a, e_b))
     torch.cuda.synchronize()

@@ -55,6 +55,8 @@ extern "C" {
                                      (outputs written to peer GPUs over NVLink)        */
 #define FX_OUT_SCALAR 32          /* OR-flag: scalar kernel (a segment's table / output pointer, ld or
                                      out_stride is not 16-byte aligned) */
+#define FX_OUT_SHARE 64           /* OR-flag: the launch shares the GPU with a concurrent stream (the
+                                     one-wave gather kernels keep at most 2 resident blocks per SM) */
 /* In both partial modes an EMPTY bag's output row is not written (its count
  * is 0: the partial is absent and K5 never reads it). */
 

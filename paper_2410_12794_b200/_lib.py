@@ -35,6 +35,7 @@ FX_OUT_F64_PARTIAL = 1
 FX_OUT_F32_PARTIAL = 2
 FX_OUT_SYSFENCE = 16
 FX_OUT_SCALAR = 32
+FX_OUT_SHARE = 64
 
 INT64_MAX = (1 << 63) - 1
 

@@ -92,7 +92,8 @@ struct StepScalars {
   long long dyn;                 // a candidate was cached at offer time (several batches in flight)
   long long claim_tag, claim_clear;  // dense dedup: this batch's tag; clear the claim words first
   long long dedup_merge;   // (global block) merge a warp's equal keys in the next dedup
-  long long pad[1];
+  long long stage_thr;     // (global block) bits of a lower bound on the limit-th hottest count, 0 = none
+  long long topk_fast;     // this stage selects from the entries at or above stage_thr
 };
 
 struct DEnt {       // per dedup-hash slot (one 16-byte line for the atomics); all-zero = empty
@@ -1525,12 +1526,69 @@ __device__ __forceinline__ uint64_t vinv_of(double x) {
 __global__ void ks_stage_begin(CacheView c, StepView v, int64_t limit) {
   StepScalars *s = v.ss;
   const Scalars *sc = c.sc;
-  s->stage_on = (s->err == 0 && limit > 0 && sc->budget - sc->used > 0 && sc->sketch_live > 0) ? 1 : 0;
+  // every row here is S bytes: with room < S each of the hottest keys is
+  // skipped as too big (cache.py:329-330), so the selection is skipped too
+  s->stage_on = (s->err == 0 && limit > 0 && sc->budget - sc->used >= v.S && sc->sketch_live > 0) ? 1 : 0;
   s->topk_live = 0;
   s->topk_krem = limit;
   s->topk_hi = s->topk_lo = 0;
   s->topk_digit = 0;
   s->topk_n = 0;
+  s->topk_fast = (s->stage_on && v.gs->stage_thr != 0) ? 1 : 0;
+}
+
+// Fast stage: the last selection's limit-th count, decayed by every age since
+// (ks_age), bounds this batch's limit-th count from below unless those keys
+// were pruned — counts only grow between ages. One pass collects the entries
+// at or above it; if at least `limit` of them exist they hold the whole top
+// `limit` and the radix select runs on that list alone (else: full path).
+__global__ void __launch_bounds__(256) ks_topk_fast_collect(CacheView c, StepView v) {
+  if (!v.ss->stage_on || !v.ss->topk_fast) return;
+  const uint64_t thr = vinv_of(__longlong_as_double(v.gs->stage_thr));
+  // four entries per thread (32-byte key and value loads); few entries pass,
+  // so a warp appends with one atomic per ballot that has any
+  const int64_t n4 = c.kcap >> 2;
+  const ulonglong2 *k2 = reinterpret_cast<const ulonglong2 *>(c.kkeys);
+  const double2 *v2 = reinterpret_cast<const double2 *>(c.kval);
+  const int lane = threadIdx.x & 31;
+  for (int64_t q0 = blockIdx.x * (int64_t)blockDim.x; q0 < n4; q0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t q = q0 + threadIdx.x;
+    uint64_t kk[4] = {kEmpty, kEmpty, kEmpty, kEmpty};
+    double vv[4] = {0.0, 0.0, 0.0, 0.0};
+    if (q < n4) {
+      const ulonglong2 a = k2[2 * q], b = k2[2 * q + 1];
+      const double2 x = v2[2 * q], y = v2[2 * q + 1];
+      kk[0] = a.x; kk[1] = a.y; kk[2] = b.x; kk[3] = b.y;
+      vv[0] = x.x; vv[1] = x.y; vv[2] = y.x; vv[3] = y.y;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint64_t vi = vinv_of(vv[u]);
+      const bool in = kk[u] != kEmpty && kk[u] != kTomb && vi <= thr;
+      const unsigned m = __ballot_sync(0xffffffffu, in);
+      if (m) {
+        const int leader = __ffs(m) - 1;
+        unsigned long long base = 0;
+        if (lane == leader)
+          base = atomicAdd(reinterpret_cast<unsigned long long *>(&v.ss->topk_live),
+                           static_cast<unsigned long long>(__popc(m)));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (in) {
+          const long long p = static_cast<long long>(base) + __popc(m & ((1u << lane) - 1u));
+          v.tk_key[p] = kk[u];
+          v.tk_vinv[p] = vi;
+        }
+      }
+    }
+  }
+}
+
+__global__ void ks_topk_fast_check(StepView v) {
+  StepScalars *s = v.ss;
+  if (s->stage_on && s->topk_fast && s->topk_live < s->topk_krem) {
+    s->topk_fast = 0;  // the bound missed (pruned keys): full path
+    s->topk_live = 0;
+  }
 }
 
 // pass 0 over the whole sketch: histogram of the top 16 bits of vinv. Decayed
@@ -1541,7 +1599,7 @@ __global__ void __launch_bounds__(256) ks_topk_hist0(CacheView c, StepView v) {
   constexpr int kSlots = 1024;
   __shared__ int sbin[kSlots];
   __shared__ int scnt[kSlots];
-  if (!v.ss->stage_on) return;
+  if (!v.ss->stage_on || v.ss->topk_fast) return;
   for (int i = threadIdx.x; i < kSlots; i += blockDim.x) {
     sbin[i] = -1;
     scnt[i] = 0;
@@ -1576,7 +1634,7 @@ __global__ void __launch_bounds__(256) ks_topk_hist0(CacheView c, StepView v) {
 // live entries whose top digit is <= the selected one: every key that can be
 // in the top `limit` (keys below the digit are in for sure)
 __global__ void __launch_bounds__(256) ks_topk_collect(CacheView c, StepView v) {
-  if (!v.ss->stage_on) return;
+  if (!v.ss->stage_on || v.ss->topk_fast) return;
   const uint64_t g0 = v.ss->topk_hi >> 48;
   for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x; i0 < c.kcap; i0 += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = i0 + threadIdx.x;
@@ -1592,6 +1650,36 @@ __global__ void __launch_bounds__(256) ks_topk_collect(CacheView c, StepView v) 
       v.tk_key[p] = k;
       v.tk_vinv[p] = vi;
     }
+  }
+}
+
+// A short list (the usual fast stage: about `limit` entries) is ranked in one
+// block by counting — keys are distinct — instead of eight radix passes.
+constexpr int kTopkSmall = 1024;
+__global__ void __launch_bounds__(1024) ks_topk_small(StepView v) {
+  __shared__ uint64_t sh[kTopkSmall], sl[kTopkSmall];
+  __shared__ int cnt;
+  StepScalars *s = v.ss;
+  if (!s->stage_on || !s->topk_fast || s->topk_live > kTopkSmall) return;
+  const int n = static_cast<int>(s->topk_live);
+  const long long k = s->topk_krem;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    sh[i] = v.tk_vinv[i];
+    sl[i] = v.tk_key[i];
+  }
+  if (threadIdx.x == 0) cnt = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const uint64_t hi = sh[i], lo = sl[i];
+    int r = 0;
+    for (int j = 0; j < n; ++j) r += (sh[j] < hi || (sh[j] == hi && sl[j] < lo)) ? 1 : 0;
+    if (r < k) v.tk_sel[atomicAdd(&cnt, 1)] = i;  // ks_stage_finish orders them
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    s->topk_n = cnt;
+    s->topk_digit = 8;  // the radix passes and the gather stand down
+    s->topk_fast = 2;
   }
 }
 
@@ -1615,7 +1703,7 @@ __device__ __forceinline__ bool prefix_match(uint64_t hi, uint64_t lo, uint64_t 
 
 // passes d >= 1 over the collected list
 __global__ void __launch_bounds__(256) ks_topk_hist(StepView v, int d) {
-  if (!v.ss->stage_on || v.ss->topk_digit == 8) return;
+  if (!v.ss->stage_on || v.ss->topk_digit == 8 || (d == 0 && !v.ss->topk_fast)) return;
   const long long n = v.ss->topk_live;
   const uint64_t phi = v.ss->topk_hi, plo = v.ss->topk_lo;
   const int lane = threadIdx.x & 31;
@@ -1635,7 +1723,6 @@ __global__ void __launch_bounds__(256) ks_topk_hist(StepView v, int d) {
 // one block: the digit holding the k-th remaining key (parallel prefix over
 // the 65536 bins); a digit whose bucket is taken whole ends the search
 __global__ void __launch_bounds__(1024) ks_topk_select(StepView v, int d) {
-  __shared__ long long part[1024];
   __shared__ long long wsum[32];
   if (!v.ss->stage_on || v.ss->topk_digit == 8) return;
   constexpr int per = kTopkBins / 1024;
@@ -1660,8 +1747,6 @@ __global__ void __launch_bounds__(1024) ks_topk_select(StepView v, int d) {
   }
   __syncthreads();
   const long long incl = x + (w ? wsum[w - 1] : 0);
-  part[t] = incl;
-  __syncthreads();
   const long long k = v.ss->topk_krem;
   const long long excl = incl - sum;
   if (t == 1023 && incl < k) {  // fewer than k keys in total: take every candidate
@@ -1703,7 +1788,7 @@ __global__ void __launch_bounds__(1024) ks_topk_select(StepView v, int d) {
 
 // the (vinv, key) <= threshold entries: exactly min(limit, live) of them
 __global__ void __launch_bounds__(256) ks_topk_gather(StepView v) {
-  if (!v.ss->stage_on) return;
+  if (!v.ss->stage_on || v.ss->topk_fast == 2) return;
   const long long n = v.ss->topk_live;
   const uint64_t thi = v.ss->topk_hi, tlo = v.ss->topk_lo;
   for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x; i0 < n; i0 += (int64_t)gridDim.x * blockDim.x) {
@@ -1747,6 +1832,10 @@ __global__ void __launch_bounds__(1024) ks_stage_finish(CacheView c, StepView v,
   }
   __syncthreads();
   if (threadIdx.x != 0) return;
+  // the next stage's bound: this selection's limit-th count (ks_age decays it)
+  v.gs->stage_thr = m >= limit && m > 0
+                        ? static_cast<long long>(~hi[ord[m - 1]] & static_cast<uint64_t>(LLONG_MAX))
+                        : 0;
   Scalars *sc = c.sc;
   long long room = sc->budget - sc->used;
   long long staged = 0, pend = sc->pending;
@@ -1796,6 +1885,8 @@ __global__ void __launch_bounds__(256) ks_age(CacheView c, StepView v) {
   }
   block_add(reinterpret_cast<unsigned long long *>(&c.sc->sketch_live), -dead);
   block_add(reinterpret_cast<unsigned long long *>(&c.sc->sketch_tomb), dead);
+  if (blockIdx.x == 0 && threadIdx.x == 0 && v.gs->stage_thr != 0)
+    v.gs->stage_thr = __double_as_longlong(__longlong_as_double(v.gs->stage_thr) * c.decay);
 }
 
 }  // namespace stp
@@ -2272,8 +2363,13 @@ int fx_step_maintain(fx_step *s, int32_t slot, int64_t stage_limit, int32_t do_a
   ks_stage_begin<<<1, 1, 0, st>>>(c, v, stage_limit);
   s->launches += 1;
   if (stage_limit > 0) {
-    ks_topk_hist0<<<grid_for(c.kcap, 256), 256, 0, st>>>(c, v);
+    ks_topk_fast_collect<<<grid_for(c.kcap / 4, 256), 256, 0, st>>>(c, v);
+    ks_topk_fast_check<<<1, 1, 0, st>>>(v);
+    ks_topk_small<<<1, 1024, 0, st>>>(v);
     s->launches += 1;
+    ks_topk_hist<<<grid_for(4 * 65536, 256), 256, 0, st>>>(v, 0);  // fast: digit 0 over the list
+    ks_topk_hist0<<<grid_for(c.kcap, 256), 256, 0, st>>>(c, v);     // else: over the whole sketch
+    s->launches += 4;
     ks_topk_select<<<1, 1024, 0, st>>>(v, 0);
     s->launches += 1;
     ks_topk_collect<<<grid_for(c.kcap, 256), 256, 0, st>>>(c, v);

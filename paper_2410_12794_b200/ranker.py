@@ -346,17 +346,19 @@ class Ranker:
         self._inflight.append(rec)
         return rec
 
-    def _pool_sample_major(self, lay: CsrLayout, out: torch.Tensor, ft, fo, B: int) -> None:
+    def _pool_sample_major(self, lay: CsrLayout, out: torch.Tensor, ft, fo, B: int, share: bool = True) -> None:
         """One K4 launch writing out[B, F*D] sample-major (out[s, f*D:(f+1)*D]
         = bag (s, f)). The segment descriptors live on the device per batch
         shape; only their output pointers are patched per call, by a device
-        op (no host->device copy, so the host never waits for the GPU)."""
+        op (no host->device copy, so the host never waits for the GPU).
+        `share`: K4 runs beside the cache step, so it keeps at most two
+        resident blocks per SM (FX_OUT_SHARE) instead of filling every SM."""
         F = len(ft)
         D = out.shape[1] // F
         seg, off = self._segs_for(ft, fo, B, D)
         seg.view(torch.int64).view(F, _lib.SEGMENT_BYTES // 8)[:, _SEG_OUT] = off + out.data_ptr()
         _lib.check(_lib.lib.fx_gather_pool(seg.data_ptr(), F, D, lay.indices.data_ptr(), _lib.idx_type_of(lay.indices),
-                                           lay.offsets.data_ptr(), F * B, _lib.FX_OUT_F32, None,
+                                           lay.offsets.data_ptr(), F * B, _lib.FX_OUT_F32 | (_lib.FX_OUT_SHARE if share else 0), None,
                                            self._status.err.data_ptr(), _lib.FX_E_LOOKUP_VALIDATION,
                                            self._status.code.data_ptr(), _lib.stream_ptr()), "gather_pool")
 

@@ -24,7 +24,7 @@ SCALARS = ("err", "err_at", "epoch", "n_uniq", "n_cand", "n_hitu", "n_nonhit", "
            "F", "mode", "n_acc", "n_ev", "ftop0", "log0", "tick0", "tick_base", "minc_bits", "b_hits", "b_misses",
            "b_groups", "b_applied", "b_pd_groups", "b_pd_rows", "b_raw_rows", "rebuild_index", "rehash_sketch",
            "rehash_n", "stage_on", "topk_live", "topk_krem", "topk_n", "topk_hi", "topk_lo", "topk_digit", "qlen_new", "n_levels", "codes_on", "chain_cycles", "dyn", "claim_tag", "claim_clear",
-           "dedup_merge")
+           "dedup_merge", "stage_thr", "topk_fast")
 IDX = {k: i for i, k in enumerate(SCALARS)}
 ERR_BAD_INDEX, ERR_SKETCH_CAP, ERR_INVARIANT = 1, 2, 3
 

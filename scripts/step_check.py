@@ -97,7 +97,7 @@ def main():
                               "latency_ms": [round(m.latency * 1e3, 3) for m in rk.batch_metrics[a.warm:]],
                               "last_step": {k: sc.get(k) for k in ("n_uniq", "n_cand", "n_off", "n_hard", "n_rej",
                                                                    "n_acc", "n_ev", "mode", "F", "n_levels",
-                                                                   "chain_cycles")},
+                                                                   "chain_cycles", "stage_on", "topk_fast", "topk_live", "topk_n")},
                               "capacity": cache.capacity(),
                               "phase_ms_per_batch": {k: round(v / max(1, len(times)), 3)
                                                      for k, v in rk.stage_ms.items()},
