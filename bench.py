@@ -598,6 +598,7 @@ def run_ranker(args, rank, world, local):
 
     prof = os.path.join(ROOT, "profiles", "r2_cfg3_kernels.json")
     shares = json.load(open(prof)) if os.path.exists(prof) else None
+    tr3 = committed_traffic(cfg["name"])  # ncu DRAM bytes per K4 launch (profiles/traffic.json)
     line = {
         "metric": "pooled lookups/s (bags/s)", "value": value, "unit": "pooled lookups/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -610,7 +611,8 @@ def run_ranker(args, rank, world, local):
         "hit_rate": hit, "latency_ms": {"p50": lat[len(lat) // 2], "max": lat[-1]},
         "host_enqueue_ms_per_step": host_ms,
         "roofline": {"bound": "hbm", "achieved": k4_achieved, "peak": peak, "unit": "GB/s",
-                     "frac": k4_achieved / peak, "traffic": None, "peak_source": peak_src,
+                     "frac": k4_achieved / peak, "traffic": tr3, "peak_source": peak_src,
+                     "dram_gbs": (tr3 / (k4_mean * 1e6)) if tr3 and k4_mean else None,
                      "kernel": "fx::k_pool_bulk (fused gather+pool K4 of the Ranker step, timed alone on its stream "
                                "over the timed batches)",
                      "bytes_per_launch": tot_bytes / args.steps, "launch_ms": k4_mean,

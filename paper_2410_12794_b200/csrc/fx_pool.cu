@@ -6,8 +6,12 @@
 //   ServerStore.partial_pool, sum_rows_f64  store.py:184-193, pooling.py:60-71
 //   pool_flat                               pooling.py:74-85
 //   combine_partials                        pooling.py:103-123
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <climits>
 #include <cstdlib>
+#include <mutex>
 
 #include "fx_common.cuh"
 #include "fx_pool_async.cuh"
@@ -453,6 +457,105 @@ static int pool_chunk_rows() {
   return v;
 }
 
+// ---- FX_POOL_VARIANT=3: TMA tile::gather4 (D = 128). One 2-D tensor map per
+// segment ([INT32_MAX rows, 128] f32, box {128, 1}; indices are validated in
+// the kernel before any copy is issued), built on the launch stream from a
+// host-encoded template by patching the global address and row stride with
+// tensormap.replace. Maps come from a per-device ring (kTmapRing launches of
+// up to kTmapSegs segments may be in flight at once).
+constexpr int kTmapSegs = 256;
+constexpr int kTmapRing = 64;
+
+__global__ void k_tmap_build(const fx_segment *__restrict__ segs, int n_segs, const __grid_constant__ CUtensorMap tmpl,
+                             unsigned char *__restrict__ maps) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_segs) return;
+  unsigned char *m = maps + static_cast<size_t>(i) * 128;
+  const uint4 *src = reinterpret_cast<const uint4 *>(&tmpl);
+  uint4 *dst = reinterpret_cast<uint4 *>(m);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) dst[k] = src[k];
+  const uint64_t addr = reinterpret_cast<uint64_t>(segs[i].table);
+  const uint64_t stride = static_cast<uint64_t>(segs[i].ld) * 4ull;
+  asm volatile("tensormap.replace.tile.global_address.global.b1024.b64 [%0], %1;" ::"l"(m), "l"(addr) : "memory");
+  asm volatile("tensormap.replace.tile.global_stride.global.b1024.b64 [%0], 0, %1;" ::"l"(m), "l"(stride)
+               : "memory");
+  asm volatile("fence.proxy.tensormap::generic.release.gpu;" ::: "memory");
+}
+
+struct TmapState {
+  bool ok = false;
+  CUtensorMap tmpl;
+  unsigned char *ring = nullptr;
+  int next = 0;
+};
+
+static TmapState *tmap_state() {
+  static std::mutex mu;
+  static TmapState st[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  TmapState &t = st[dev & 63];
+  std::lock_guard<std::mutex> g(mu);
+  if (!t.ring) {
+    PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", reinterpret_cast<void **>(&enc), 12000,
+                                         cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !enc)
+      return nullptr;
+    if (cudaMalloc(&t.ring, static_cast<size_t>(kTmapRing) * kTmapSegs * 128) != cudaSuccess) {
+      t.ring = nullptr;
+      return nullptr;
+    }
+    // template: a dummy 16-B aligned address (replaced per segment)
+    cuuint64_t gdim[2] = {128, 0x7fffffffull};
+    cuuint64_t gstride[1] = {512};
+    cuuint32_t box[2] = {128, 1};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(&t.tmpl, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, t.ring, gdim, gstride, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    t.ok = r == CUDA_SUCCESS;
+  }
+  return t.ok ? &t : nullptr;
+}
+
+template <int CR, typename IdxT, int MODE, int MINB>
+static bool launch_g4(const fx_segment *segs, int n_segs, int dim, const IdxT *ix, const int64_t *offsets,
+                      int64_t n_bags, int32_t *counts, int64_t *err, int32_t bad_code, int32_t *err_code,
+                      cudaStream_t st, bool sf) {
+  if (n_segs > kTmapSegs) return false;
+  TmapState *t = tmap_state();
+  if (!t) return false;
+  unsigned char *maps;
+  {
+    static std::mutex mu;
+    std::lock_guard<std::mutex> g(mu);
+    maps = t->ring + static_cast<size_t>(t->next) * kTmapSegs * 128;
+    t->next = (t->next + 1) % kTmapRing;
+  }
+  k_tmap_build<<<(n_segs + 127) / 128, 128, 0, st>>>(segs, n_segs, t->tmpl, maps);
+  constexpr int WARPS = 4;
+  const size_t smem = static_cast<size_t>(WARPS) * (CR * 512 + 8);
+  static int per_sm_dev[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int &per_sm = per_sm_dev[dev & 63];
+  if (per_sm <= 0) {
+    cudaFuncSetAttribute(k_pool_g4<CR, IdxT, MODE, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pool_g4<CR, IdxT, MODE, MINB>, WARPS * 32, smem);
+    if (per_sm < 1) per_sm = 1;
+  }
+  int64_t blocks = static_cast<int64_t>(num_sms()) * (tl_share > 0 && per_sm > tl_share ? tl_share : per_sm);
+  const int64_t need = (n_bags + WARPS - 1) / WARPS;
+  if (blocks > need) blocks = need;
+  k_pool_g4<CR, IdxT, MODE, MINB><<<static_cast<int>(blocks), WARPS * 32, smem, st>>>(
+      segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code, sf, maps);
+  return true;
+}
+
 template <int G, int NCH, typename IdxT, int MODE>
 static void launch_async(const fx_segment *segs, int n_segs, int dim, const IdxT *ix, const int64_t *offsets,
                          int64_t n_bags, int32_t *counts, int64_t *err, int32_t bad_code, int32_t *err_code,
@@ -482,7 +585,10 @@ static int launch_pool(const fx_segment *segs, int n_segs, int dim, const void *
                        cudaStream_t st, bool vec4, bool sf) {
   const IdxT *ix = static_cast<const IdxT *>(indices);
   const int var = vec4 ? pool_variant() : 0;
-  if (var >= 2 && dim == 128) {
+  if (var == 3 && dim == 128 &&
+      launch_g4<12, IdxT, MODE, 7>(segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code, st, sf)) {
+    // TMA gather4 A/B (falls through to the bulk copies when maps are unavailable)
+  } else if (var >= 2 && dim == 128) {
     // 12-row chunks, <= 72 registers: 7 blocks (28 warps) per SM; tuned on B200
     // against 16-row / 6-block and 8..14-row / 7..10-block configurations
     launch_bulk_cr<32, 1, 12, IdxT, MODE, 7>(segs, n_segs, dim, ix, offsets, n_bags, counts, err, bad_code, err_code,

@@ -353,3 +353,143 @@ __global__ void __launch_bounds__(128, MINB) k_pool_bulk(const fx_segment *__res
 }
 
 }  // namespace fx
+
+// ---- TMA tensor gather (FX_POOL_VARIANT=3, D = 128): the A/B SURVEY §2.3
+// asks for against the 1-D bulk copies above. One lane per 4 rows issues
+// cp.async.bulk.tensor.2d...tile::gather4 (SASS UTMALDG.2D.GATHER4) through
+// the segment's 2-D tensor map ([rows, 128] f32, box {128, 1}; row
+// coordinates are shard-relative and validated before issue), so a 12-row
+// chunk is 3 TMA requests instead of 12. A chunk whose row count is not a
+// multiple of 4 repeats its last row in the padding slots (loaded, never
+// summed). Tensor maps live in global memory (one 128-B CUtensorMap per
+// segment, written by k_tmap_build on the same stream).
+namespace fx {
+
+__device__ __forceinline__ void tma_gather4(uint32_t dst, const void *tmap, int32_t col, int32_t r0, int32_t r1,
+                                            int32_t r2, int32_t r3, uint32_t mbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
+      "l"(tmap), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(mbar)
+      : "memory");
+}
+__device__ __forceinline__ void tmap_acquire(const void *tmap) {
+  asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(tmap) : "memory");
+}
+
+template <int CR, typename IdxT, int MODE, int MINB = FX_POOL_MINB>
+__global__ void __launch_bounds__(128, MINB) k_pool_g4(const fx_segment *__restrict__ segs, int n_segs, int dim,
+                                                       const IdxT *__restrict__ indices_g,
+                                                       const int64_t *__restrict__ offsets, int64_t n_bags,
+                                                       int32_t *__restrict__ counts, int64_t *err, int32_t bad_code,
+                                                       int32_t *err_code, bool sysfence,
+                                                       const unsigned char *__restrict__ tmaps) {
+  static_assert(CR % 4 == 0 && CR <= 32, "whole gather4 groups");
+  constexpr int G = 32, NCH = 1, ROWB = 512;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  unsigned char *buf = smem + static_cast<size_t>(wib) * CR * ROWB;
+  const uint32_t sbuf = static_cast<uint32_t>(__cvta_generic_to_shared(buf));
+  const uint32_t mbar = static_cast<uint32_t>(
+      __cvta_generic_to_shared(smem + static_cast<size_t>(blockDim.x / 32) * CR * ROWB + wib * 8));
+  if (lane == 0) mbar_init(mbar, 1);
+  fence_proxy_async_smem();
+  __syncwarp();
+  uint32_t phase = 0;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t step = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  int64_t bag = warp;
+  if (bag >= n_bags) {
+    if (sysfence) __threadfence_system();
+    return;
+  }
+  int s = find_segment(segs, n_segs, bag);
+  int acq = -1;  // segment whose tensor map this warp has acquired
+  int64_t beg, end;
+  bag_bounds(segs, s, bag, offsets, beg, end);
+  const IdxT *indices = seg_indices(segs, s, indices_g);
+  IdxT pidx = (lane < CR && beg + lane < end) ? indices[beg + lane] : IdxT(0);
+  while (bag < n_bags) {
+    const int64_t rb = segs[s].row_begin, re = segs[s].row_end;
+    const unsigned char *tm = tmaps + static_cast<size_t>(s) * 128;
+    if (acq != s) {
+      tmap_acquire(tm);
+      acq = s;
+    }
+    double acc[NCH][4];
+    acc[0][0] = acc[0][1] = acc[0][2] = acc[0][3] = 0.0;
+    const int64_t nbag = bag + step;
+    const int ns = nbag < n_bags ? find_segment(segs, n_segs, nbag) : s;
+    const IdxT *nindices = seg_indices(segs, ns, indices_g);
+    int64_t nbeg = 0, nend = 0;
+    IdxT nidx = IdxT(0);
+    bool have_next = false;
+    for (int64_t c0 = beg; c0 < end; c0 += CR) {
+      const int n = static_cast<int>((end - c0) < CR ? (end - c0) : (int64_t)CR);
+      const int ng = (n + 3) >> 2;
+      const int64_t idx = static_cast<int64_t>(pidx);
+      int32_t rel = 0;
+      if (lane < n) {
+        if (idx < rb || idx >= re) record_bad(err, err_code, c0 + lane, bad_code);
+        else rel = static_cast<int32_t>(idx - rb);
+      }
+      // padding slots repeat the chunk's last row
+      const int32_t last = __shfl_sync(0xffffffffu, rel, n - 1);
+      if (lane >= n) rel = last;
+      const int q = (lane & 7) << 2;  // lanes 0..ng-1 gather rows 4*lane .. 4*lane+3
+      const int32_t g0 = __shfl_sync(0xffffffffu, rel, q);
+      const int32_t g1 = __shfl_sync(0xffffffffu, rel, q + 1);
+      const int32_t g2 = __shfl_sync(0xffffffffu, rel, q + 2);
+      const int32_t g3 = __shfl_sync(0xffffffffu, rel, q + 3);
+      if (lane == 0) mbar_expect_tx(mbar, static_cast<uint32_t>(ng) * 4 * ROWB);
+      __syncwarp();
+      if (lane < ng) tma_gather4(sbuf + lane * 4 * ROWB, tm, 0, g0, g1, g2, g3, mbar);
+      if (c0 + CR < end) {
+        pidx = (lane < CR && c0 + CR + lane < end) ? indices[c0 + CR + lane] : IdxT(0);
+      } else if (nbag < n_bags) {
+        bag_bounds(segs, ns, nbag, offsets, nbeg, nend);
+        nidx = (lane < CR && nbeg + lane < nend) ? nindices[nbeg + lane] : IdxT(0);
+        have_next = true;
+      }
+      mbar_wait(mbar, phase);
+      phase ^= 1u;
+      int r = 0;
+      for (; r + 4 <= n; r += 4) {
+        float4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = *reinterpret_cast<const float4 *>(buf + (r + u) * ROWB + lane * 16);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          acc[0][0] += f2d(v[u].x);
+          acc[0][1] += f2d(v[u].y);
+          acc[0][2] += f2d(v[u].z);
+          acc[0][3] += f2d(v[u].w);
+        }
+      }
+      for (; r < n; ++r) {
+        const float4 v = *reinterpret_cast<const float4 *>(buf + r * ROWB + lane * 16);
+        acc[0][0] += f2d(v.x);
+        acc[0][1] += f2d(v.y);
+        acc[0][2] += f2d(v.z);
+        acc[0][3] += f2d(v.w);
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+    }
+    if (!have_next && nbag < n_bags) {
+      bag_bounds(segs, ns, nbag, offsets, nbeg, nend);
+      nidx = (lane < CR && nbeg + lane < nend) ? nindices[nbeg + lane] : IdxT(0);
+    }
+    emit_bag<NCH, MODE>(segs[s], bag, end - beg, acc, lane, G, counts);
+    bag = nbag;
+    s = ns;
+    indices = nindices;
+    beg = nbeg;
+    end = nend;
+    pidx = nidx;
+  }
+  if (sysfence) __threadfence_system();
+}
+
+}  // namespace fx

@@ -370,3 +370,33 @@ def test_host_stream_reports_the_failing_batch(P):
         for out in hl.stream(batches, depth=3):
             got.append(out.clone())
     assert len(got) == 2
+
+
+@pytest.mark.parametrize("row_begin,ld,partial", [(0, 128, False), (1000, 160, False), (0, 132, True)])
+def test_pool_strided_shard_vs_oracle(P, row_begin, ld, partial):
+    """K4 on a shard whose rows are ld >= dim floats apart and whose first row
+    is a global row != 0 (the bulk / gather4 copies address rows by stride)."""
+    from paper_2410_12794_b200.store import pool_csr_device
+    g = torch.Generator().manual_seed(ld)
+    n = 3000
+    base = torch.randn(n, ld, generator=g)
+    tab = base[:, :128].cuda()  # contiguous copy, then re-stride below
+    big = torch.zeros(n, ld, device="cuda")
+    big[:, :128] = tab
+    view = big[:, :128]
+    rng = np.random.default_rng(ld)
+    lens = rng.integers(0, 41, size=700)
+    offs = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    idx = (rng.integers(0, n, size=int(offs[-1])) + row_begin).astype(np.int64)
+    out = pool_csr_device(view, row_begin, row_begin + n, torch.from_numpy(idx).cuda(), torch.from_numpy(offs).cuda(),
+                          "sum", partial=partial).cpu().numpy()
+    host = base[:, :128].numpy()
+    for b in range(len(lens)):
+        if lens[b] == 0:
+            continue
+        rows = host[idx[offs[b]:offs[b + 1]] - row_begin]
+        ref = O.seq_sum_f64(rows)
+        if partial:
+            assert out[b].tobytes() == ref.tobytes(), b
+        else:
+            assert out[b].tobytes() == ref.astype(np.float32).tobytes(), b
