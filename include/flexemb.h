@@ -63,6 +63,15 @@ extern "C" {
 const char *fx_last_error(void);
 int fx_version(void);
 int fx_num_sms(int device);
+/* Bounds-checked builds (FX_BOUNDS, libflexemb_chk.so; compute-sanitizer
+ * stand-in): out4 = {violations, array base, first bad index, array length}
+ * on the current device; returns 1, 0 for a normal build (out4 untouched),
+ * -1 on a CUDA error. No reference counterpart (test infrastructure). */
+int fx_bounds_report(int64_t *out4);
+/* FX_BOUNDS builds: launch a kernel that reads a checked 4-element array at
+ * index 5 and verify the record caught it (then clear it): 1 = the checks are
+ * live, 0 = normal build, -1 = not caught. */
+int fx_bounds_selftest(void);
 
 /* ---- K0: table materialisation (store.py:62-89 table_block/_table_base) --
  * out[r*ld + c] = f32(((mix64(base_t + (row_start+r)*dim + c) >> 11) * 2^-53)

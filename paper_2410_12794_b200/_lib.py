@@ -87,6 +87,8 @@ _SIGS = {
     "fx_last_error": ([], ctypes.c_char_p),
     "fx_version": ([], ctypes.c_int),
     "fx_num_sms": ([ctypes.c_int], ctypes.c_int),
+    "fx_bounds_report": ([ctypes.POINTER(_I64)], ctypes.c_int),
+    "fx_bounds_selftest": ([], ctypes.c_int),
     "fx_table_base": ([_U64, _I64], _U64),
     "fx_table_init": ([_P, _I64, _U64, _I64, _I32, _I64, _I64, _P], ctypes.c_int),
     "fx_gather_pool": ([_P, _I32, _I32, _P, _I32, _P, _I64, _I32, _P, _P, _I32, _P, _P], ctypes.c_int),
@@ -205,3 +207,16 @@ class Status:
         code = int(self.code.item())
         pos = int(self.err.item())
         return code, pos
+
+
+def bounds_report():
+    """FX_BOUNDS builds (libflexemb_chk.so): {violations, base, index, length}
+    of the first out-of-range device subscript on the current device; None
+    for a normal build."""
+    out = (_I64 * 4)()
+    rc = lib.fx_bounds_report(out)
+    if rc < 0:
+        raise RuntimeError("fx_bounds_report: " + lib.fx_last_error().decode())
+    if rc == 0:
+        return None
+    return {"violations": out[0], "base": out[1], "index": out[2], "length": out[3]}

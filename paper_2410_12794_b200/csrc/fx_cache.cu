@@ -1085,6 +1085,16 @@ int dmalloc(T **p, size_t n) {
   cudaError_t e = cudaMalloc(reinterpret_cast<void **>(p), n * sizeof(T));
   return cuda_check(e, "fx_cache: cudaMalloc");
 }
+#ifdef FX_BOUNDS
+template <typename T>
+int dmalloc(CkPtr<T> *p, size_t n) {
+  T *q = nullptr;
+  const int rc = dmalloc(&q, n);
+  *p = q;
+  ck_size(*p, static_cast<long long>(n));
+  return rc;
+}
+#endif
 
 int ensure_ws(fx_cache *c, size_t need) {
   if (c->ws_bytes >= need) return FX_OK;

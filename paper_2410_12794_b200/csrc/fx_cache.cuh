@@ -6,6 +6,7 @@
 #include <climits>
 #include <vector>
 
+#include "fx_ckptr.cuh"
 #include "fx_common.cuh"
 
 namespace fx {
@@ -29,25 +30,25 @@ struct Scalars {
 
 struct CacheView {
   Scalars *sc;
-  uint64_t *hkeys;
-  int32_t *hslot;
+  CkPtr<uint64_t> hkeys;
+  CkPtr<int32_t> hslot;
   int64_t hcap;
-  uint64_t *skey;
-  uint64_t *skey2;  // second fingerprint of pooled-result keys (0 for row keys)
-  long long *stick;
-  int32_t *ssize;
-  int32_t *shits;
-  float *rows;
+  CkPtr<uint64_t> skey;
+  CkPtr<uint64_t> skey2;  // second fingerprint of pooled-result keys (0 for row keys)
+  CkPtr<long long> stick;
+  CkPtr<int32_t> ssize;
+  CkPtr<int32_t> shits;
+  CkPtr<float> rows;
   int64_t scap;
   int32_t row_ld;
-  int32_t *free_stack;
-  uint64_t *kkeys;
-  double *kval;
-  uint8_t *kflag;
+  CkPtr<int32_t> free_stack;
+  CkPtr<uint64_t> kkeys;
+  CkPtr<double> kval;
+  CkPtr<uint8_t> kflag;
   int64_t kcap;
-  uint64_t *pend;
+  CkPtr<uint64_t> pend;
   int64_t pend_cap;
-  uint64_t *evlog;
+  CkPtr<uint64_t> evlog;
   int64_t evlog_cap;
   const fx_table_dir *dir;
   int32_t n_dir;

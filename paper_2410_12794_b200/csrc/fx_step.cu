@@ -109,46 +109,46 @@ struct StepView {
   StepScalars *ss;   // this batch's slot
   StepScalars *gs;   // global (epoch counter)
   // dedup hash
-  uint64_t *dkey;
-  DEnt *dent;
-  int32_t *dfraw;    // first raw-occurrence ordinal (threshold mode)
+  CkPtr<uint64_t> dkey;
+  CkPtr<DEnt> dent;
+  CkPtr<int32_t> dfraw;    // first raw-occurrence ordinal (threshold mode)
   int64_t dcap;
-  unsigned int *dclaim;  // dense per-row claim words (batch tag | first claimer's CSR position)
+  CkPtr<unsigned int> dclaim;  // dense per-row claim words (batch tag | first claimer's CSR position)
   int32_t rep_bits;  // bits of the claimer position in a claim word
-  int32_t *uniq;     // claimed dedup slots
-  int32_t *claim;    // [max_nnz] per occurrence: the dedup slot it claimed, else -1
-  double *dC;        // [dcap] sketch estimate after this batch's bump (misses)
-  int32_t *inv;      // per occurrence (CSR position) -> dedup slot
-  int32_t *cand_by_first;  // [max_nnz] scatter by ordinal
-  int32_t *hit_by_last;    // [max_nnz]
-  int32_t *cand;     // compacted candidates (dedup slots) in first raw-occurrence order
-  uint64_t *ckey;    // [max_nnz] this slot's candidate keys (kept from start to offer)
-  double *cest;      // [max_nnz] this slot's candidate estimates at probe time
-  double *estv;      // [max_nnz] candidate estimates at offer time
-  int32_t *pres;     // [max_nnz] 1 = candidate absent at offer time
-  int32_t *cidx;     // [max_nnz] absent candidates (positions into ckey)
-  uint64_t *okey;    // [max_nnz] absent candidate keys in offer order
-  int32_t *hits_ord; // compacted hit cache slots in last-ordinal order
-  double *cC;        // candidate estimates in offer order
-  double *bmax;      // per kFine-block max of cC
-  int32_t *q;        // the cache's LRU queue (fx_cache.q)
-  int32_t *didx;     // dense slot index: one int32 per table row (slot or -1)
+  CkPtr<int32_t> uniq;     // claimed dedup slots
+  CkPtr<int32_t> claim;    // [max_nnz] per occurrence: the dedup slot it claimed, else -1
+  CkPtr<double> dC;        // [dcap] sketch estimate after this batch's bump (misses)
+  CkPtr<int32_t> inv;      // per occurrence (CSR position) -> dedup slot
+  CkPtr<int32_t> cand_by_first;  // [max_nnz] scatter by ordinal
+  CkPtr<int32_t> hit_by_last;    // [max_nnz]
+  CkPtr<int32_t> cand;     // compacted candidates (dedup slots) in first raw-occurrence order
+  CkPtr<uint64_t> ckey;    // [max_nnz] this slot's candidate keys (kept from start to offer)
+  CkPtr<double> cest;      // [max_nnz] this slot's candidate estimates at probe time
+  CkPtr<double> estv;      // [max_nnz] candidate estimates at offer time
+  CkPtr<int32_t> pres;     // [max_nnz] 1 = candidate absent at offer time
+  CkPtr<int32_t> cidx;     // [max_nnz] absent candidates (positions into ckey)
+  CkPtr<uint64_t> okey;    // [max_nnz] absent candidate keys in offer order
+  CkPtr<int32_t> hits_ord; // compacted hit cache slots in last-ordinal order
+  CkPtr<double> cC;        // candidate estimates in offer order
+  CkPtr<double> bmax;      // per kFine-block max of cC
+  CkPtr<int32_t> q;        // the cache's LRU queue (fx_cache.q)
+  CkPtr<int32_t> didx;     // dense slot index: one int32 per table row (slot or -1)
   const int64_t *kbase;  // per table: first dense position
-  int32_t *qnew;     // [scap] V = compacted queue
-  int32_t *sflag;    // [scap] epoch of the last hit
-  double *E;         // [scap] victim estimates
-  int32_t *hardf;    // [scap] hard-victim flags
-  int32_t *hard;     // [scap] compacted hard positions
-  int32_t *rj_beg, *rj_end;  // reject intervals
-  uint8_t *code;     // [max_nnz] per candidate: number of distinct hard levels <= its estimate
-  uint8_t *bsum;     // [max_nnz / 32 + 1] max code per 32 candidates
-  uint8_t *hrank;    // [scap] per hard victim: 1 + index of its level (accept iff code >= hrank)
-  double *levels;    // [256] distinct hard-victim estimates, ascending
-  int32_t *acc;      // [max_nnz] accept flags, then ranks
-  int32_t *rank;
-  int32_t *aslot;    // [max_nnz] slot taken by accept r
-  uint64_t *akey;    // [max_nnz] key of accept r
-  int32_t *accj;     // [max_nnz] candidate index of accept r (sequential mode)
+  CkPtr<int32_t> qnew;     // [scap] V = compacted queue
+  CkPtr<int32_t> sflag;    // [scap] epoch of the last hit
+  CkPtr<double> E;         // [scap] victim estimates
+  CkPtr<int32_t> hardf;    // [scap] hard-victim flags
+  CkPtr<int32_t> hard;     // [scap] compacted hard positions
+  CkPtr<int32_t> rj_beg; CkPtr<int32_t> rj_end;  // reject intervals
+  CkPtr<uint8_t> code;     // [max_nnz] per candidate: number of distinct hard levels <= its estimate
+  CkPtr<uint8_t> bsum;     // [max_nnz / 32 + 1] max code per 32 candidates
+  CkPtr<uint8_t> hrank;    // [scap] per hard victim: 1 + index of its level (accept iff code >= hrank)
+  CkPtr<double> levels;    // [256] distinct hard-victim estimates, ascending
+  CkPtr<int32_t> acc;      // [max_nnz] accept flags, then ranks
+  CkPtr<int32_t> rank;
+  CkPtr<int32_t> aslot;    // [max_nnz] slot taken by accept r
+  CkPtr<uint64_t> akey;    // [max_nnz] key of accept r
+  CkPtr<int32_t> accj;     // [max_nnz] candidate index of accept r (sequential mode)
   int64_t max_nnz;
   // per-table row source and validation bounds (dense by table id)
   const float *const *tbase;
@@ -158,13 +158,13 @@ struct StepView {
   int32_t S;         // entry size in bytes
   int32_t dim;       // floats per row
   // rehash / top-k temporaries
-  uint64_t *tk_key;
-  uint64_t *tk_vinv;
-  double *tk_val;
-  uint8_t *tk_flag;
+  CkPtr<uint64_t> tk_key;
+  CkPtr<uint64_t> tk_vinv;
+  CkPtr<double> tk_val;
+  CkPtr<uint8_t> tk_flag;
   int64_t tk_cap;
-  int32_t *tk_hist;
-  int32_t *tk_sel;   // selected top-k list positions
+  CkPtr<int32_t> tk_hist;
+  CkPtr<int32_t> tk_sel;   // selected top-k list positions
 };
 
 // ---------------------------------------------------------------- helpers
@@ -255,17 +255,31 @@ __device__ __forceinline__ void warp_copy_row(float *dst, const float *src, int 
   }
 }
 
+// bump(key, w) for a key probed once per batch (a unique key of the batch):
+// no other thread touches this key's entry in the kernel, so a found entry is
+// updated with a plain load/store; only a new key claims an empty slot by CAS
+// (slots only go empty -> key during the kernel, and an empty slot's value is
+// 0, so the new value is 0.0 + w exactly as in the reference's dict).
 __device__ __forceinline__ double sketch_add_val(const CacheView &c, uint64_t key, double w, bool *born) {
   const uint64_t m = static_cast<uint64_t>(c.kcap - 1);
   uint64_t h = hash_key(key) & m;
   while (true) {
-    const unsigned long long prev =
-        atomicCAS(reinterpret_cast<unsigned long long *>(&c.kkeys[h]), (unsigned long long)kEmpty,
-                  (unsigned long long)key);
-    if (prev == kEmpty || prev == key) {
-      const double old = atomicAdd(&c.kval[h], w);
-      *born = prev == kEmpty;
-      return old + w;
+    uint64_t k = __ldcg(reinterpret_cast<const unsigned long long *>(&c.kkeys[h]));
+    if (k == kEmpty) {
+      k = atomicCAS(reinterpret_cast<unsigned long long *>(&c.kkeys[h]), (unsigned long long)kEmpty,
+                    (unsigned long long)key);
+      if (k == kEmpty) {
+        const double nv = 0.0 + w;
+        c.kval[h] = nv;
+        *born = true;
+        return nv;
+      }
+    }
+    if (k == key) {
+      const double nv = c.kval[h] + w;
+      c.kval[h] = nv;
+      *born = false;
+      return nv;
     }
     h = (h + 1) & m;
   }
@@ -569,21 +583,23 @@ __global__ void __launch_bounds__(256) ks_dedup(StepView v, const int32_t *__res
 // 135 / 132 / 208 us, warp-merged 183 / 162 / 125 us, block-merge variant
 // above (FX_DEDUP=blk) 375 / 223 / 127 us — hence the switch on the previous
 // batch's unique fraction (0.97 / 0.48 / 0.17 at those alphas).
-// A warp takes 32 consecutive bags; its lanes walk the bags' occurrences 32
-// at a time, each lane locating its bag with a 5-step shuffle search over the
-// 33 bag offsets the warp holds.
+// A warp takes `bw` (<= 32) consecutive bags; its lanes walk the bags'
+// occurrences 32 at a time, each lane locating its bag with a shuffle search
+// over the bw + 1 bag offsets the warp holds. Each round of 32 occurrences is
+// a chain of dependent random accesses (claim word in HBM, entry atomics), so
+// fewer bags per warp = more warps in flight.
 template <typename IdxT>
 __global__ void __launch_bounds__(256) ks_dedup_occ(StepView v, const int32_t *__restrict__ bag_table,
                                                 const IdxT *__restrict__ idx, const int64_t *__restrict__ offsets,
-                                                const int64_t *__restrict__ sm_start, int64_t n_bags) {
+                                                const int64_t *__restrict__ sm_start, int64_t n_bags, int bw) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const unsigned int tag = static_cast<unsigned int>(v.ss->claim_tag);
   const unsigned int rmask = (1u << v.rep_bits) - 1u;
   const bool merge = v.gs->dedup_merge != 0;
-  for (int64_t b0 = warp * 32; b0 < n_bags; b0 += nw * 32) {
-    const int64_t nb = n_bags - b0 < 32 ? n_bags - b0 : 32;
+  for (int64_t b0 = warp * bw; b0 < n_bags; b0 += nw * bw) {
+    const int64_t nb = n_bags - b0 < bw ? n_bags - b0 : bw;
     const int64_t my = b0 + (lane < nb ? lane : nb - 1);
     const int64_t off = lane < nb ? __ldg(&offsets[b0 + lane]) : __ldg(&offsets[b0 + nb]);
     const int64_t end = __ldg(&offsets[b0 + nb]);
@@ -663,37 +679,59 @@ __global__ void __launch_bounds__(256) ks_dedup_occ(StepView v, const int32_t *_
 }
 
 // ---------------------------------------------------------------- 3. probe
-__global__ void __launch_bounds__(256) ks_probe(CacheView c, StepView v, int32_t threshold_on) {
+// One thread per CSR position: the claimer of a key (claim[p] == p, the
+// key's unique id) probes it, so no compaction of the claim words is needed;
+// the unique count is block-aggregated here. Two positions per thread and
+// iteration, their loads issued together (the probe is a chain of dependent
+// random accesses: claim word -> entry -> dense slot index -> sketch).
+__global__ void __launch_bounds__(256) ks_probe(CacheView c, StepView v, int32_t threshold_on, int64_t nnz) {
   if (aborted(v)) return;
-  const long long n = v.ss->n_uniq;
   const long long tick0 = c.sc->tick;
   const long long epoch = v.ss->epoch;
-  long long hits = 0, misses = 0, born = 0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t u = v.uniq[i];
-    const uint64_t key = v.dkey[u];
-    DEnt e = v.dent[u];
-    const int32_t s = d_find(v, key);
-    if (s >= 0) {
-      c.stick[s] = tick0 + d_last(e) + 1;
-      c.shits[s] += e.mult;
-      v.sflag[s] = static_cast<int32_t>(epoch);
-      v.hit_by_last[d_last(e)] = s;
-      hits += e.mult;
-    } else {
-      bool b = false;
-      v.dC[u] = sketch_add_val(c, key, static_cast<double>(e.mult), &b);
-      born += b ? 1 : 0;
-      misses += e.mult;
-      if (!threshold_on) v.cand_by_first[d_first(e)] = u;
+  long long hits = 0, misses = 0, born = 0, nu = 0;
+  const int64_t T = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < nnz; i0 += 2 * T) {
+    int32_t u[2];
+    u[0] = v.claim[i0];
+    u[1] = i0 + T < nnz ? v.claim[i0 + T] : -1;
+    uint64_t key[2];
+    DEnt e[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+      if (u[k] >= 0) {
+        key[k] = v.dkey[u[k]];
+        e[k] = v.dent[u[k]];
+      }
+    int32_t sl[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) sl[k] = u[k] >= 0 ? d_find(v, key[k]) : -1;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      if (u[k] < 0) continue;
+      ++nu;
+      const int32_t s = sl[k];
+      if (s >= 0) {
+        c.stick[s] = tick0 + d_last(e[k]) + 1;
+        c.shits[s] += e[k].mult;
+        v.sflag[s] = static_cast<int32_t>(epoch);
+        v.hit_by_last[d_last(e[k])] = s;
+        hits += e[k].mult;
+      } else {
+        bool b = false;
+        v.dC[u[k]] = sketch_add_val(c, key[k], static_cast<double>(e[k].mult), &b);
+        born += b ? 1 : 0;
+        misses += e[k].mult;
+        if (!threshold_on) v.cand_by_first[d_first(e[k])] = u[k];
+      }
+      v.dent[u[k]].hit = s;
     }
-    v.dent[u].hit = s;
   }
   block_add(reinterpret_cast<unsigned long long *>(&c.sc->hits), hits);
   block_add(reinterpret_cast<unsigned long long *>(&c.sc->misses), misses);
   block_add(reinterpret_cast<unsigned long long *>(&c.sc->sketch_live), born);
   block_add(reinterpret_cast<unsigned long long *>(&v.ss->b_hits), hits);
   block_add(reinterpret_cast<unsigned long long *>(&v.ss->b_misses), misses);
+  block_add(reinterpret_cast<unsigned long long *>(&v.ss->n_uniq), nu);
 }
 
 __global__ void ks_after_probe(CacheView c, StepView v, int64_t nnz) {
@@ -748,11 +786,11 @@ __global__ void __launch_bounds__(256) ks_bag_plan(StepView v, const int64_t *__
   block_add(reinterpret_cast<unsigned long long *>(&v.ss->b_raw_rows), raw);
 }
 
-__global__ void ks_cand_scatter_raw(StepView v) {
+__global__ void ks_cand_scatter_raw(StepView v, int64_t nnz) {
   if (aborted(v)) return;
-  const long long n = v.ss->n_uniq;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t u = v.uniq[i];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nnz; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t u = v.claim[i];
+    if (u < 0) continue;
     const int32_t f = v.dfraw[u];
     if (f != 0) v.cand_by_first[INT_MAX - f] = u;
   }
@@ -1166,7 +1204,7 @@ __global__ void __launch_bounds__(1024) ks_chain_stream(StepView v) {
   uint8_t *sum = smem;
   uint8_t *ring = smem + ((nblk + kSumPad + 15) & ~15ll);  // sum[] zero-padded past nblk
   for (long long b = threadIdx.x; b < nblk / 16; b += blockDim.x)
-    reinterpret_cast<int4 *>(sum)[b] = __ldg(reinterpret_cast<const int4 *>(v.bsum) + b);
+    reinterpret_cast<int4 *>(sum)[b] = __ldg(reinterpret_cast<const int4 *>(raw(v.bsum)) + b);
   for (long long b = nblk / 16 * 16 + threadIdx.x; b < nblk + kSumPad; b += blockDim.x)
     sum[b] = b < nblk ? v.bsum[b] : 0;
   if (threadIdx.x == 0) {
@@ -1548,8 +1586,8 @@ __global__ void __launch_bounds__(256) ks_topk_fast_collect(CacheView c, StepVie
   // four entries per thread (32-byte key and value loads); few entries pass,
   // so a warp appends with one atomic per ballot that has any
   const int64_t n4 = c.kcap >> 2;
-  const ulonglong2 *k2 = reinterpret_cast<const ulonglong2 *>(c.kkeys);
-  const double2 *v2 = reinterpret_cast<const double2 *>(c.kval);
+  const ulonglong2 *k2 = reinterpret_cast<const ulonglong2 *>(raw(c.kkeys));
+  const double2 *v2 = reinterpret_cast<const double2 *>(raw(c.kval));
   const int lane = threadIdx.x & 31;
   for (int64_t q0 = blockIdx.x * (int64_t)blockDim.x; q0 < n4; q0 += (int64_t)gridDim.x * blockDim.x) {
     const int64_t q = q0 + threadIdx.x;
@@ -1861,7 +1899,7 @@ __global__ void __launch_bounds__(256) ks_age(CacheView c, StepView v) {
   // four table entries per thread and iteration: two 16-byte key loads, the
   // value loads only for live entries, all issued before any is used
   const int64_t n4 = c.kcap >> 2;
-  const ulonglong2 *k2 = reinterpret_cast<const ulonglong2 *>(c.kkeys);
+  const ulonglong2 *k2 = reinterpret_cast<const ulonglong2 *>(raw(c.kkeys));
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n4; q += (int64_t)gridDim.x * blockDim.x) {
     const ulonglong2 a = k2[2 * q], b = k2[2 * q + 1];
     const uint64_t kk[4] = {a.x, a.y, b.x, b.y};
@@ -1927,6 +1965,16 @@ int salloc(fx_step *s, T **p, size_t n) {
   s->allocs.push_back(*p);
   return FX_OK;
 }
+#ifdef FX_BOUNDS
+template <typename T>
+int salloc(fx_step *s, CkPtr<T> *p, size_t n) {
+  T *q = nullptr;
+  const int rc = salloc(s, &q, n);
+  *p = q;
+  ck_size(*p, static_cast<long long>(n));
+  return rc;
+}
+#endif
 
 int64_t pow2_ge(int64_t x) {
   int64_t p = 1024;
@@ -1974,10 +2022,11 @@ int ensure_queue(fx_step *s, cudaStream_t st) {
     c->queue_valid = 0;
   }
   s->v.q = c->q;
+  ck_size(s->v.q, scap);
   if (c->queue_valid) return FX_OK;
   // rebuild: occupied slots by ascending tick (free slots sort last)
-  long long *k0 = reinterpret_cast<long long *>(s->v.E);  // scratch: scap doubles
-  long long *k1 = reinterpret_cast<long long *>(s->v.tk_vinv);
+  long long *k0 = reinterpret_cast<long long *>(raw(s->v.E));  // scratch: scap doubles
+  long long *k1 = reinterpret_cast<long long *>(raw(s->v.tk_vinv));
   int32_t *v0 = s->v.hardf, *v1 = s->v.hard;
   k_lru_sortkeys<<<grid_for(scap, 256), 256, 0, st>>>(c->v, k0, v0, LLONG_MAX);
   size_t need = 0;
@@ -2005,7 +2054,10 @@ int select_slot(fx_step *s, int32_t slot, StepView *v) {
   v->gs = s->ss_base + s->slots;
   v->ckey = s->ckey_base + static_cast<int64_t>(slot) * s->max_nnz;
   v->cest = s->cest_base + static_cast<int64_t>(slot) * s->max_nnz;
+  ck_size(v->ckey, s->max_nnz);
+  ck_size(v->cest, s->max_nnz);
   v->q = s->cache->q;
+  ck_size(v->q, s->cache->q_cap);
   return FX_OK;
 }
 
@@ -2231,13 +2283,19 @@ int fx_step_start(fx_step *s, int32_t slot, const int32_t *bag_table, const void
     if (g > gmax) g = gmax;
     static const bool occ = !(getenv("FX_DEDUP") && std::string(getenv("FX_DEDUP")) == "blk");
     if (occ) {
-      const int go = grid_for((n_bags + 31) / 32 * 32, 256);
+      // bags per warp (FX_DEDUP_BW, default 32). cfg3 2 % / 1 % cache, ms per
+      // batch at 32 / 16 / 8 / 4 bags per warp: alpha 1.0 1.238 / 1.258 /
+      // 1.284 / 1.301, alpha 1.2 0.790 / 0.798 / 0.810 / 0.837, alpha 0.6
+      // 2.865 / 2.866 / 2.854 / 2.846 (profiles/r2_summary.md)
+      static const int bw = (getenv("FX_DEDUP_BW") && atoi(getenv("FX_DEDUP_BW")) >= 1 &&
+                             atoi(getenv("FX_DEDUP_BW")) <= 32) ? atoi(getenv("FX_DEDUP_BW")) : 32;
+      const int go = grid_for((n_bags + bw - 1) / bw * 32, 256);
       if (idx_type == FX_IDX_I32)
         ks_dedup_occ<int32_t><<<go, 256, 0, st>>>(v, bag_table, static_cast<const int32_t *>(indices), offsets,
-                                                  sm_start, n_bags);
+                                                  sm_start, n_bags, bw);
       else
         ks_dedup_occ<int64_t><<<go, 256, 0, st>>>(v, bag_table, static_cast<const int64_t *>(indices), offsets,
-                                                  sm_start, n_bags);
+                                                  sm_start, n_bags, bw);
     } else if (idx_type == FX_IDX_I32) {
       ks_dedup<int32_t><<<g, 256, kDSmem, st>>>(v, bag_table, static_cast<const int32_t *>(indices), offsets,
                                                 sm_start, n_bags);
@@ -2249,15 +2307,12 @@ int fx_step_start(fx_step *s, int32_t slot, const int32_t *bag_table, const void
   }
   const int nn = static_cast<int>(nnz > 0 ? nnz : 1);
   size_t cb = s->cub_bytes;
-  cub::DeviceSelect::If(s->cub_tmp, cb, v.claim, v.uniq, reinterpret_cast<int64_t *>(&v.ss->n_uniq), nn, NonNeg(),
-                        st);
-  s->launches += 2;
   // ranker.py:218-222 order: validate, apply_pending, (admission check: host), probes
   ks_apply_pending<<<1, 32, 0, st>>>(c, v);
   s->launches += 1;
   cudaMemsetAsync(v.cand_by_first, 0xff, static_cast<size_t>(nn) * 4, st);
   cudaMemsetAsync(v.hit_by_last, 0xff, static_cast<size_t>(nn) * 4, st);
-  ks_probe<<<grid_for(nn, 256), 256, 0, st>>>(c, v, threshold > 0 ? 1 : 0);
+  ks_probe<<<grid_for(nn, 256), 256, 0, st>>>(c, v, threshold > 0 ? 1 : 0, nnz);
   s->launches += 1;
   ks_after_probe<<<1, 1, 0, st>>>(c, v, nnz);
   s->launches += 1;
@@ -2265,22 +2320,22 @@ int fx_step_start(fx_step *s, int32_t slot, const int32_t *bag_table, const void
                                                                             hits_bag, pd_groups, pd_rows, raw_rows);
   s->launches += 1;
   if (threshold > 0) {
-    ks_cand_scatter_raw<<<grid_for(nn, 256), 256, 0, st>>>(v);
+    ks_cand_scatter_raw<<<grid_for(nn, 256), 256, 0, st>>>(v, nnz);
     s->launches += 1;
   }
   // candidates in first raw-occurrence order; hit slots in last-ordinal order
-  cub::DeviceSelect::If(s->cub_tmp, cb, v.cand_by_first, v.cand, reinterpret_cast<int64_t *>(&v.ss->n_cand), nn,
+  cub::DeviceSelect::If(s->cub_tmp, cb, raw(v.cand_by_first), raw(v.cand), reinterpret_cast<int64_t *>(&v.ss->n_cand), nn,
                         NonNeg(), st);
   s->launches += 2;
   ks_cand_keys<<<grid_for(nn, 256), 256, 0, st>>>(v);
   s->launches += 1;
-  cub::DeviceSelect::If(s->cub_tmp, cb, v.hit_by_last, v.hits_ord, reinterpret_cast<int64_t *>(&v.ss->n_hitu), nn,
+  cub::DeviceSelect::If(s->cub_tmp, cb, raw(v.hit_by_last), raw(v.hits_ord), reinterpret_cast<int64_t *>(&v.ss->n_hitu), nn,
                         NonNeg(), st);
   s->launches += 2;
   // LRU order after the probes: [entries not hit, old order] ++ [hit entries by last ordinal]
   cudaMemsetAsync(v.qnew, 0xff, SC * 4, st);
   QueueKeep qk{v.sflag, &v.ss->epoch};
-  cub::DeviceSelect::If(s->cub_tmp, cb, cc->q, v.qnew, reinterpret_cast<int64_t *>(&v.ss->n_nonhit),
+  cub::DeviceSelect::If(s->cub_tmp, cb, cc->q, raw(v.qnew), reinterpret_cast<int64_t *>(&v.ss->n_nonhit),
                         static_cast<int>(SC), qk, st);
   s->launches += 2;
   ks_queue_append_hits<<<grid_for(nn, 256), 256, 0, st>>>(v);
@@ -2307,7 +2362,7 @@ int fx_step_offer(fx_step *s, int32_t slot, void *stream) {
   s->launches += 1;
   ks_offer_flags<<<grid_for(nn, 256), 256, 0, st>>>(v, nn);
   s->launches += 1;
-  cub::DeviceSelect::Flagged(s->cub_tmp, cb, cub::CountingInputIterator<int32_t>(0), v.pres, v.cidx,
+  cub::DeviceSelect::Flagged(s->cub_tmp, cb, cub::CountingInputIterator<int32_t>(0), raw(v.pres), raw(v.cidx),
                              reinterpret_cast<int64_t *>(&v.ss->n_off), nn, st);
   s->launches += 2;
   ks_cand_est<<<grid_for(nn, kFine), kFine, 0, st>>>(v);
@@ -2316,7 +2371,7 @@ int fx_step_offer(fx_step *s, int32_t slot, void *stream) {
   s->launches += 1;
   ks_victim_est<<<grid_for(SC, 256), 256, 0, st>>>(c, v, SC);
   s->launches += 1;
-  cub::DeviceSelect::Flagged(s->cub_tmp, cb, cub::CountingInputIterator<int32_t>(0), v.hardf, v.hard,
+  cub::DeviceSelect::Flagged(s->cub_tmp, cb, cub::CountingInputIterator<int32_t>(0), raw(v.hardf), raw(v.hard),
                              reinterpret_cast<int64_t *>(&v.ss->n_hard), static_cast<int>(SC), st);
   s->launches += 2;
   ks_levels<<<1, 1024, 0, st>>>(v, s->stream_smem > 0 ? 1 : 0);
@@ -2331,7 +2386,7 @@ int fx_step_offer(fx_step *s, int32_t slot, void *stream) {
   s->launches += 1;
   ks_accept_flags<<<grid_for(nn, 256), 256, 0, st>>>(v, nn);
   s->launches += 1;
-  cub::DeviceScan::ExclusiveSum(s->cub_tmp, cb, v.acc, v.rank, nn, st);
+  cub::DeviceScan::ExclusiveSum(s->cub_tmp, cb, raw(v.acc), raw(v.rank), nn, st);
   s->launches += 2;
   cudaMemsetAsync(v.qnew, 0xff, SC * 4, st);
   ks_apply<<<grid_for(nn, 256), 256, 0, st>>>(c, v);

@@ -1,5 +1,8 @@
 """Small fused-step workload for compute-sanitizer (memcheck / racecheck /
-synccheck): every decision mode of csrc/fx_step.cu on tiny shapes —
+synccheck) or, where compute-sanitizer is unavailable (it is closed on the
+GPU pool), for the bounds-checked build (FX_LIB_PATH=.../libflexemb_chk.so:
+every cache / step array subscript checked on the device, report printed at
+the end): every decision mode of csrc/fx_step.cu on tiny shapes —
 parallel chain with rejections, the sequential path, pushdown threshold,
 "always" admission, pipeline_depth 2 (dynamic presence), staging while the
 cache fills, a rejected batch — each checked against the vectorised oracle.
@@ -35,6 +38,12 @@ def main():
         bad += nb
         print(c, "mismatches", nb, flush=True)
     print("sanitize_step done, mismatches", bad)
+    from paper_2410_12794_b200 import _lib
+    rep = _lib.bounds_report()
+    if rep is not None:
+        st = _lib.lib.fx_bounds_selftest()
+        print("FX_BOUNDS report:", rep, "selftest (1 = an injected out-of-range read is caught):", st, flush=True)
+        bad += rep["violations"] + (st != 1)
     sys.exit(1 if bad else 0)
 
 
