@@ -1952,6 +1952,13 @@ struct fx_step {
   int64_t stage_limit_cap = 0;
   int64_t launches = 0;  // kernels this handle launched (CUB sweeps count 2)
   int64_t n_dense = 0;   // dense slot index length (sum of table rows)
+  // The accepts' row copies (bandwidth-bound, nothing else in the batch reads
+  // the cache rows) run on a side stream, forked after the decisions and
+  // joined at the end of fx_step_maintain (or the next start / offer), so
+  // they overlap the queue commit and the maintenance (FX_COPY_SIDE=0: inline)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  bool copy_pending = false;
 };
 
 namespace {
@@ -1975,6 +1982,14 @@ int salloc(fx_step *s, CkPtr<T> *p, size_t n) {
   return rc;
 }
 #endif
+
+// rejoin the side-stream row copies of the last offer call
+void join_copies(fx_step *s, cudaStream_t st) {
+  if (s->copy_pending) {
+    cudaStreamWaitEvent(st, s->ev_join, 0);
+    s->copy_pending = false;
+  }
+}
 
 int64_t pow2_ge(int64_t x) {
   int64_t p = 1024;
@@ -2236,6 +2251,9 @@ int fx_step_create(fx_step **out, fx_cache *cache, int64_t max_nnz, int64_t max_
 
 int fx_step_destroy(fx_step *s) {
   if (!s) return FX_OK;
+  if (s->side) cudaStreamDestroy(s->side);
+  if (s->ev_fork) cudaEventDestroy(s->ev_fork);
+  if (s->ev_join) cudaEventDestroy(s->ev_join);
   for (void *p : s->allocs) cudaFree(p);
   delete s;
   return FX_OK;
@@ -2251,6 +2269,7 @@ int fx_step_start(fx_step *s, int32_t slot, const int32_t *bag_table, const void
     set_error("fx_step_start: batch larger than the step's capacity");
     return FX_E_CAPACITY;
   }
+  join_copies(s, st);
   int rc = ensure_queue(s, st);
   if (rc) return rc;
   StepView v;
@@ -2348,6 +2367,7 @@ int fx_step_start(fx_step *s, int32_t slot, const int32_t *bag_table, const void
 
 int fx_step_offer(fx_step *s, int32_t slot, void *stream) {
   cudaStream_t st = as_stream(stream);
+  join_copies(s, st);
   int rc = ensure_queue(s, st);
   if (rc) return rc;
   StepView v;
@@ -2397,7 +2417,22 @@ int fx_step_offer(fx_step *s, int32_t slot, void *stream) {
   s->launches += 1;
   ks_offer_finish<<<1, 1, 0, st>>>(c, v);
   s->launches += 1;
-  ks_copy_rows<<<grid_for(static_cast<int64_t>(nn) * (v.dim / 4 + 1), 256), 256, 0, st>>>(c, v);
+  static const bool side = !(getenv("FX_COPY_SIDE") && atoi(getenv("FX_COPY_SIDE")) == 0);
+  if (side && !s->side) {
+    if (cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming) != cudaSuccess)
+      return cuda_check(cudaGetLastError(), "fx_step_offer: side stream");
+  }
+  if (side) {
+    cudaEventRecord(s->ev_fork, st);
+    cudaStreamWaitEvent(s->side, s->ev_fork, 0);
+    ks_copy_rows<<<grid_for(static_cast<int64_t>(nn) * (v.dim / 4 + 1), 256), 256, 0, s->side>>>(c, v);
+    cudaEventRecord(s->ev_join, s->side);
+    s->copy_pending = true;
+  } else {
+    ks_copy_rows<<<grid_for(static_cast<int64_t>(nn) * (v.dim / 4 + 1), 256), 256, 0, st>>>(c, v);
+  }
   s->launches += 1;
   ks_queue_commit<<<grid_for(SC, 256), 256, 0, st>>>(v, SC);
   s->launches += 1;
@@ -2444,6 +2479,7 @@ int fx_step_maintain(fx_step *s, int32_t slot, int64_t stage_limit, int32_t do_a
     ks_age<<<grid_for(c.kcap / 4, 256), 256, 0, st>>>(c, v);
     s->launches += 1;
   }
+  join_copies(s, st);
   FX_LAUNCH_CHECK("fx_step_maintain");
   return FX_OK;
 }
