@@ -385,6 +385,12 @@ int fx_step_maintain(fx_step *s, int32_t slot, int64_t stage_limit, int32_t do_a
 int fx_step_scalars(fx_step *s, int32_t slot, int64_t *out, int64_t n, void *stream);   /* [sync] */
 const void *fx_step_scalars_device(fx_step *s, int32_t slot);
 int64_t fx_step_launches(fx_step *s);  /* kernels launched by this handle so far (CUB sweeps count 2) */
+/* Make `stream` wait for the step's side-stream work (the accepts' row
+ * copies, forked by fx_step_offer and otherwise joined at the end of
+ * fx_step_maintain / the next start or offer). Call it before touching the
+ * cache through any other entry point, or at the end of a captured batch
+ * that has no maintenance. No reference counterpart (stream plumbing). */
+int fx_step_join(fx_step *s, void *stream);
 
 
 /* ---- store (fx_store_create / fx_store_shard_view) ------------
@@ -402,10 +408,30 @@ int fx_store_shard_view(fx_store *s, int32_t table, int64_t row, const float **b
                         int64_t *ld, int32_t *dim);
 /* [sync] read a kernel's device status pair (first bad position, FX_E_* code) */
 int fx_poll_error(const int32_t *err_code, const int64_t *err_pos, int32_t *code, int64_t *pos, void *stream);
-/* Collectives (SURVEY's fx_comm_init / fx_alltoallv) are not wrapped here: the
- * C1/C2 exchange is torch.distributed (NCCL) in sharded.ShardedLookup, and the
- * fused path replaces it with peer stores through fx_ipc_* / fx_push_csr /
- * fx_rw_push*, driven by sharded.P2PShardedLookup. */
+/* ---- communicator (fx_comm_init / fx_alltoallv) -------------
+ * The fan-out / response seam (ranker.py:263-347: post_subrequest ->
+ * _server_handler -> _on_response) as a byte all-to-allv over CUDA-IPC-mapped
+ * peer memory of one node, no NCCL: every rank owns a double-buffered window of
+ * `world` slots of `slot_bytes`; fx_alltoallv stores rank r's slice for d
+ * (send + send_displs[d], send_counts[d] bytes; device arrays) into slot r of
+ * d's window and its count next to it, then the ranks meet in a
+ * release/acquire peer barrier. Setup: fx_comm_init on every rank,
+ * fx_comm_handle -> exchange the 64-byte handles out of band (e.g. a
+ * torch.distributed all_gather) -> fx_comm_connect(world x 64 bytes). After
+ * an exchange, fx_comm_recv_buffer / fx_comm_recv_counts give this rank's
+ * received slots (valid until the next-but-one exchange; consume them on the
+ * same stream). The exchange epoch is host-side: not for CUDA-graph capture.
+ * sharded.P2PShardedLookup fuses the same one-sided stores into the push and
+ * gather kernels instead (fx_push_csr / fx_rw_push* / K4 epilogue). */
+typedef struct fx_comm fx_comm;
+int fx_comm_init(fx_comm **out, int32_t rank, int32_t world, int64_t slot_bytes);
+int fx_comm_handle(fx_comm *c, unsigned char handle_out[64]);
+int fx_comm_connect(fx_comm *c, const unsigned char *handles);
+int fx_alltoallv(fx_comm *c, const void *send, const int64_t *send_counts, const int64_t *send_displs, void *stream);
+void *fx_comm_recv_buffer(fx_comm *c);
+const int64_t *fx_comm_recv_counts(fx_comm *c);
+int fx_comm_status(fx_comm *c, int32_t *overflow, int32_t *timed_out);  /* [sync] slot overflow / barrier timeout */
+int fx_comm_destroy(fx_comm *c);
 
 #ifdef __cplusplus
 }

@@ -121,13 +121,21 @@ _SIGS = {
         "fx_cache_pooled_put", "fx_cache_rows", "fx_cache_scalars_device", "fx_cache_capacity", "fx_cache_queue_valid",
         # fused batch step, typed in step.py
         "fx_step_create", "fx_step_destroy", "fx_step_prepare", "fx_step_start", "fx_step_offer", "fx_step_maintain",
-        "fx_step_scalars", "fx_step_scalars_device", "fx_step_launches")},
+        "fx_step_scalars", "fx_step_scalars_device", "fx_step_launches", "fx_step_join")},
     "fx_bag_fingerprint": ([_P, _P, _P, _I32, _P, _I64, _P, _P, _P], ctypes.c_int),
     "fx_store_create": ([ctypes.POINTER(_P), _I32, _I32, _P, _P, _I32, _P, _I32, _U64, _P], ctypes.c_int),
     "fx_store_destroy": ([_P], ctypes.c_int),
     "fx_store_shard_view": ([_P, _I32, _I64, ctypes.POINTER(_P), ctypes.POINTER(_I64), ctypes.POINTER(_I64),
                              ctypes.POINTER(_I64), ctypes.POINTER(_I32)], ctypes.c_int),
     "fx_poll_error": ([_P, _P, ctypes.POINTER(_I32), ctypes.POINTER(_I64), _P], ctypes.c_int),
+    "fx_comm_init": ([ctypes.POINTER(_P), _I32, _I32, _I64], ctypes.c_int),
+    "fx_comm_handle": ([_P, ctypes.c_char_p], ctypes.c_int),
+    "fx_comm_connect": ([_P, ctypes.c_char_p], ctypes.c_int),
+    "fx_alltoallv": ([_P, _P, _P, _P, _P], ctypes.c_int),
+    "fx_comm_recv_buffer": ([_P], _P),
+    "fx_comm_recv_counts": ([_P], _P),
+    "fx_comm_status": ([_P, ctypes.POINTER(_I32), ctypes.POINTER(_I32)], ctypes.c_int),
+    "fx_comm_destroy": ([_P], ctypes.c_int),
 }
 
 EXPORTED = []

@@ -105,6 +105,14 @@ struct DEnt {       // per dedup-hash slot (one 16-byte line for the atomics); a
 __device__ __forceinline__ int32_t d_first(const DEnt &e) { return INT_MAX - e.first; }
 __device__ __forceinline__ int32_t d_last(const DEnt &e) { return e.last - 1; }
 
+// Per table row (dense): this batch's dedup claim word and the row's cache
+// slot, in one 8-byte record so the dedup claimer reads the slot from the
+// sector it just claimed (the probe then needs no slot-index access).
+struct __align__(8) DRow {
+  unsigned int claim;  // batch tag << rep_bits | first claimer's CSR position
+  int32_t slot;        // cache slot or -1
+};
+
 struct StepView {
   StepScalars *ss;   // this batch's slot
   StepScalars *gs;   // global (epoch counter)
@@ -113,7 +121,7 @@ struct StepView {
   CkPtr<DEnt> dent;
   CkPtr<int32_t> dfraw;    // first raw-occurrence ordinal (threshold mode)
   int64_t dcap;
-  CkPtr<unsigned int> dclaim;  // dense per-row claim words (batch tag | first claimer's CSR position)
+  CkPtr<DRow> drow;        // dense per-row claim word + cache slot (one record per table row)
   int32_t rep_bits;  // bits of the claimer position in a claim word
   CkPtr<int32_t> uniq;     // claimed dedup slots
   CkPtr<int32_t> claim;    // [max_nnz] per occurrence: the dedup slot it claimed, else -1
@@ -132,7 +140,6 @@ struct StepView {
   CkPtr<double> cC;        // candidate estimates in offer order
   CkPtr<double> bmax;      // per kFine-block max of cC
   CkPtr<int32_t> q;        // the cache's LRU queue (fx_cache.q)
-  CkPtr<int32_t> didx;     // dense slot index: one int32 per table row (slot or -1)
   const int64_t *kbase;  // per table: first dense position
   CkPtr<int32_t> qnew;     // [scap] V = compacted queue
   CkPtr<int32_t> sflag;    // [scap] epoch of the last hit
@@ -236,7 +243,7 @@ __device__ __forceinline__ long long warp_append(unsigned long long *ctr, int wa
 __device__ __forceinline__ int64_t dpos(const StepView &v, uint64_t key) {
   return v.kbase[key >> kRowBitsC] + static_cast<int64_t>(key & kRowMask);
 }
-__device__ __forceinline__ int32_t d_find(const StepView &v, uint64_t key) { return v.didx[dpos(v, key)]; }
+__device__ __forceinline__ int32_t d_find(const StepView &v, uint64_t key) { return v.drow[dpos(v, key)].slot; }
 
 __device__ __forceinline__ const float *row_src(const StepView &v, uint64_t key) {
   const int64_t t = static_cast<int64_t>(key >> kRowBitsC);
@@ -316,7 +323,7 @@ __global__ void ks_begin(CacheView c, StepView v, int64_t max_nnz) {
 __global__ void ks_claim_clear(StepView v, int64_t n_dense) {
   if (!v.ss->claim_clear) return;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_dense; i += (int64_t)gridDim.x * blockDim.x)
-    v.dclaim[i] = 0u;
+    v.drow[i].claim = 0u;
 }
 
 // in-place sketch rehash (drops tombstones): collect -> clear -> reinsert
@@ -360,6 +367,14 @@ __global__ void ks_sketch_reinsert(CacheView c, StepView v) {
   if (blockIdx.x == 0 && threadIdx.x == 0) c.sc->sketch_tomb = 0;
 }
 
+// a key claimed by this batch's dedup has its probe-time slot in its entry:
+// apply_pending (which runs between dedup and probe) keeps it current
+__device__ __forceinline__ void patch_hit(const StepView &v, uint64_t key, int32_t slot) {
+  const unsigned int w = v.drow[dpos(v, key)].claim;
+  if ((w >> v.rep_bits) == static_cast<unsigned int>(v.ss->claim_tag))
+    v.dent[w & ((1u << v.rep_bits) - 1u)].hit = slot;
+}
+
 // ---------------------------------------------------------------- 1. apply pending
 // cache.py:344-352: install the keys staged by the last maintenance, in
 // order, always-admit (_insert evicts the LRU head until the entry fits).
@@ -389,7 +404,8 @@ __global__ void ks_apply_pending(CacheView c, StepView v) {
           const uint64_t ok = c.skey[vs];
           if (c.evlog_cap > 0 && nlog < c.evlog_cap) c.evlog[nlog] = ok;
           if (c.evlog_cap > 0) ++nlog;
-          v.didx[dpos(v, ok)] = -1;
+          v.drow[dpos(v, ok)].slot = -1;
+          patch_hit(v, ok, -1);
           c.stick[vs] = kFree;
           c.skey[vs] = kEmpty;
           c.free_stack[ftop++] = vs;
@@ -402,7 +418,8 @@ __global__ void ks_apply_pending(CacheView c, StepView v) {
         c.stick[slot] = tick;
         c.ssize[slot] = static_cast<int32_t>(S);
         c.shits[slot] = 0;
-        v.didx[dpos(v, key)] = slot;
+        v.drow[dpos(v, key)].slot = slot;
+        patch_hit(v, key, slot);
         v.q[qlen++] = slot;
         ++e;
         ++applied;
@@ -437,17 +454,37 @@ constexpr int kDBags = 256;     // bags per block chunk (8 warps x 32)
 constexpr int kDHash = 4096;    // shared-memory table entries per block
 constexpr size_t kDSmem = kDHash * (8 + 4 * 5);
 
-__device__ __forceinline__ int32_t dedup_global(const StepView &v, uint64_t key, int t, int64_t r, int rep,
-                                                unsigned int tag, unsigned int rmask, bool *claimed) {
-  unsigned int *cw = &v.dclaim[v.kbase[t] + r];
-  const unsigned int mine = (tag << v.rep_bits) | static_cast<unsigned int>(rep);
-  unsigned int w = *cw;
+// Claim a row's record for this batch with one 64-bit CAS over (claim, slot):
+// the claimer learns the row's cache slot from the same access. Returns the
+// key's unique id (the first claimer's CSR position); *slot_out is set when
+// this call claimed.
+__device__ __forceinline__ int32_t claim_row(const StepView &v, int64_t pos, unsigned int tag, unsigned int rmask,
+                                             int32_t rep, bool *claimed, int32_t *slot_out) {
+  unsigned long long *cw = reinterpret_cast<unsigned long long *>(&v.drow[pos]);
+  const unsigned long long mine = (tag << v.rep_bits) | static_cast<unsigned int>(rep);
+  unsigned long long w = *cw;
   while (true) {
-    if ((w >> v.rep_bits) == tag) { *claimed = false; return static_cast<int32_t>(w & rmask); }
-    const unsigned int prev = atomicCAS(cw, w, mine);
-    if (prev == w) { *claimed = true; return rep; }
+    const unsigned int cl = static_cast<unsigned int>(w);
+    if ((cl >> v.rep_bits) == tag) {
+      *claimed = false;
+      return static_cast<int32_t>(cl & rmask);
+    }
+    const unsigned long long prev = atomicCAS(cw, w, (w & 0xffffffff00000000ull) | mine);
+    if (prev == w) {
+      *claimed = true;
+      *slot_out = static_cast<int32_t>(w >> 32);
+      return rep;
+    }
     w = prev;
   }
+}
+
+__device__ __forceinline__ int32_t dedup_global(const StepView &v, uint64_t key, int t, int64_t r, int rep,
+                                                unsigned int tag, unsigned int rmask, bool *claimed) {
+  int32_t slot = -1;
+  const int32_t u = claim_row(v, v.kbase[t] + r, tag, rmask, rep, claimed, &slot);
+  if (*claimed) v.dent[rep].hit = slot;  // the key's cache slot at dedup time
+  return u;
 }
 
 template <typename IdxT>
@@ -654,16 +691,12 @@ __global__ void __launch_bounds__(256) ks_dedup_occ(StepView v, const int32_t *_
       const int leader = __ffs(peers) - 1;
       const bool valid = key < (~0ull - 2);
       if (valid && lane == leader) {
-        unsigned int *cw = &v.dclaim[v.kbase[t] + r];
-        const unsigned int mine = (tag << v.rep_bits) | static_cast<unsigned int>(p);
-        unsigned int w = *cw;
-        while (true) {
-          if ((w >> v.rep_bits) == tag) { u = static_cast<int32_t>(w & rmask); break; }
-          const unsigned int prev = atomicCAS(cw, w, mine);
-          if (prev == w) { u = static_cast<int32_t>(p); claimed = true; break; }
-          w = prev;
+        int32_t slot = -1;
+        u = claim_row(v, v.kbase[t] + r, tag, rmask, static_cast<int32_t>(p), &claimed, &slot);
+        if (claimed) {
+          v.dkey[u] = key;
+          v.dent[u].hit = slot;  // the key's cache slot at dedup time
         }
-        if (claimed) v.dkey[u] = key;
         DEnt *e = &v.dent[u];
         atomicAdd(&e->mult, __popc(peers));
         atomicMax(&e->first, INT_MAX - gmin);  // zero-initialised encodings (memset reset)
@@ -702,9 +735,9 @@ __global__ void __launch_bounds__(256) ks_probe(CacheView c, StepView v, int32_t
         key[k] = v.dkey[u[k]];
         e[k] = v.dent[u[k]];
       }
-    int32_t sl[2];
+    int32_t sl[2];  // the slot dedup recorded (kept current by apply_pending)
 #pragma unroll
-    for (int k = 0; k < 2; ++k) sl[k] = u[k] >= 0 ? d_find(v, key[k]) : -1;
+    for (int k = 0; k < 2; ++k) sl[k] = u[k] >= 0 ? e[k].hit : -1;
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
       if (u[k] < 0) continue;
@@ -723,7 +756,6 @@ __global__ void __launch_bounds__(256) ks_probe(CacheView c, StepView v, int32_t
         misses += e[k].mult;
         if (!threshold_on) v.cand_by_first[d_first(e[k])] = u[k];
       }
-      v.dent[u[k]].hit = s;
     }
   }
   block_add(reinterpret_cast<unsigned long long *>(&c.sc->hits), hits);
@@ -1392,12 +1424,12 @@ __global__ void __launch_bounds__(256) ks_apply(CacheView c, StepView v) {
         slot = v.q[q];
         const uint64_t ok = c.skey[slot];
         if (c.evlog_cap > 0 && log0 + q < c.evlog_cap) c.evlog[log0 + q] = ok;
-        v.didx[dpos(v, ok)] = -1;
+        v.drow[dpos(v, ok)].slot = -1;
       }
       c.skey[slot] = key;
       c.stick[slot] = tick_base + r + 1;
       c.shits[slot] = 0;
-      v.didx[dpos(v, key)] = slot;
+      v.drow[dpos(v, key)].slot = slot;
       v.qnew[e0 - n_ev + r] = slot;
       v.aslot[r] = slot;
       v.akey[r] = key;
@@ -1415,16 +1447,34 @@ __global__ void __launch_bounds__(256) ks_copy_rows(CacheView c, StepView v) {
   const bool vec = (dim & 3) == 0 && (c.row_ld & 3) == 0;
   const int per = vec ? dim / 4 : dim;
   const long long total = na * per;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const long long r = i / per;
-    const int k = static_cast<int>(i - r * per);
-    const int32_t slot = v.aslot[r];
-    const uint64_t key = v.akey[r];
-    if (seq && (c.skey[slot] != key || c.stick[slot] == kFree)) continue;  // evicted again in the same call
-    const float *src = row_src(v, key);
-    float *dst = c.rows + static_cast<int64_t>(slot) * c.row_ld;
-    if (vec) reinterpret_cast<float4 *>(dst)[k] = __ldg(reinterpret_cast<const float4 *>(src) + k);
-    else dst[k] = __ldg(src + k);
+  // four independent pieces per thread and iteration (loads first): a small
+  // grid keeps enough bytes in flight and leaves SMs to the concurrent stream
+  const int64_t T = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < total; i0 += 4 * T) {
+    float4 val[4];
+    float *dst[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      dst[u] = nullptr;
+      const int64_t i = i0 + u * T;
+      if (i >= total) continue;
+      const long long r = i / per;
+      const int k = static_cast<int>(i - r * per);
+      const int32_t slot = v.aslot[r];
+      const uint64_t key = v.akey[r];
+      if (seq && (c.skey[slot] != key || c.stick[slot] == kFree)) continue;  // evicted again in the same call
+      const float *src = row_src(v, key);
+      float *d = c.rows + static_cast<int64_t>(slot) * c.row_ld;
+      if (vec) {
+        val[u] = __ldg(reinterpret_cast<const float4 *>(src) + k);
+        dst[u] = d + 4 * k;
+      } else {
+        d[k] = __ldg(src + k);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (dst[u]) *reinterpret_cast<float4 *>(dst[u]) = val[u];
   }
 }
 
@@ -1501,7 +1551,7 @@ __global__ void ks_seq_offer(CacheView c, StepView v) {
         const uint64_t ok = c.skey[vs];
         if (c.evlog_cap > 0 && nlog < c.evlog_cap) c.evlog[nlog] = ok;
         if (c.evlog_cap > 0) ++nlog;
-        v.didx[dpos(v, ok)] = -1;
+        v.drow[dpos(v, ok)].slot = -1;
         c.stick[vs] = kFree;
         c.skey[vs] = kEmpty;
         c.free_stack[ftop++] = vs;
@@ -1517,7 +1567,7 @@ __global__ void ks_seq_offer(CacheView c, StepView v) {
     c.stick[slot] = tick;
     c.ssize[slot] = static_cast<int32_t>(S);
     c.shits[slot] = 0;
-    v.didx[dpos(v, key)] = slot;
+    v.drow[dpos(v, key)].slot = slot;
     v.aslot[n_acc] = slot;
     v.akey[n_acc] = key;
     v.accj[n_acc] = static_cast<int32_t>(j);
@@ -1983,7 +2033,42 @@ int salloc(fx_step *s, CkPtr<T> *p, size_t n) {
 }
 #endif
 
-// rejoin the side-stream row copies of the last offer call
+// side-stream work of the step (FX_COPY_SIDE=0: everything inline)
+bool side_on() {
+  static const bool on = !(getenv("FX_COPY_SIDE") && atoi(getenv("FX_COPY_SIDE")) == 0);
+  return on;
+}
+
+// resident 256-thread blocks per SM for the side-stream row copies
+// (FX_SIDE_BLOCKS; default 0 = a full grid). cfg3 ms per batch, alpha 1.0 /
+// 1.2 / 0.6: full grid 1.224 / 0.772 / 2.84, 4 blocks 1.233 / 0.760 / 2.91,
+// 2 blocks 1.360 / 0.798 / 3.23, inline 1.262 / 0.784 / 2.94
+// (profiles/r2_summary.md)
+int side_blocks() {
+  static const int b = (getenv("FX_SIDE_BLOCKS") && atoi(getenv("FX_SIDE_BLOCKS")) > 0) ? atoi(getenv("FX_SIDE_BLOCKS"))
+                                                                                         : 0;
+  return b;
+}
+
+int side_fork(fx_step *s, cudaStream_t st) {
+  if (!s->side) {
+    if (cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming) != cudaSuccess)
+      return cuda_check(cudaGetLastError(), "fx_step: side stream");
+  }
+  cudaEventRecord(s->ev_fork, st);
+  cudaStreamWaitEvent(s->side, s->ev_fork, 0);
+  return FX_OK;
+}
+
+// after launching on s->side: the next join waits for everything on it so far
+void side_close(fx_step *s) {
+  cudaEventRecord(s->ev_join, s->side);
+  s->copy_pending = true;
+}
+
+// rejoin the side-stream work (plan counters of a start, row copies of an offer)
 void join_copies(fx_step *s, cudaStream_t st) {
   if (s->copy_pending) {
     cudaStreamWaitEvent(st, s->ev_join, 0);
@@ -2006,12 +2091,17 @@ __global__ void k_lru_sortkeys(CacheView c, long long *keys, int32_t *vals, long
 }
 
 // dense slot index from the slots (after any entry point that moved entries)
+__global__ void k_didx_clear(StepView v, int64_t n_dense) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_dense; i += (int64_t)gridDim.x * blockDim.x)
+    v.drow[i].slot = -1;
+}
+
 __global__ void k_didx_fill(CacheView c, StepView v) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < c.scap; i += (int64_t)gridDim.x * blockDim.x) {
     const uint64_t k = c.skey[i];
     if (c.stick[i] == kFree || (k >> 63)) continue;  // free slot / pooled-result key
     const int64_t t = static_cast<int64_t>(k >> kRowBitsC);
-    if (t < v.n_tables) v.didx[dpos(v, k)] = static_cast<int32_t>(i);
+    if (t < v.n_tables) v.drow[dpos(v, k)].slot = static_cast<int32_t>(i);
   }
 }
 
@@ -2052,7 +2142,7 @@ int ensure_queue(fx_step *s, cudaStream_t st) {
   cub::DeviceRadixSort::SortPairs(tmp, need, k0, k1, v0, v1, static_cast<int>(scap), 0, 64, st);
   k_queue_from_sorted<<<grid_for(scap, 256), 256, 0, st>>>(c->v, v1, c->q, scap);
   cudaFreeAsync(tmp, st);
-  cudaMemsetAsync(s->v.didx, 0xff, s->n_dense * sizeof(int32_t), st);
+  k_didx_clear<<<grid_for(s->n_dense, 256), 256, 0, st>>>(s->v, s->n_dense);
   k_didx_fill<<<grid_for(scap, 256), 256, 0, st>>>(c->v, s->v);
   FX_LAUNCH_CHECK("fx_step: queue rebuild");
   c->queue_valid = 1;
@@ -2174,15 +2264,14 @@ int fx_step_create(fx_step **out, fx_cache *cache, int64_t max_nnz, int64_t max_
     s->n_dense = tot > 0 ? tot : 1;
     int64_t *kbd = nullptr;
     rc = salloc(s, &kbd, n_tables);
-    rc = rc ? rc : salloc(s, &v.didx, static_cast<size_t>(s->n_dense));
-    rc = rc ? rc : salloc(s, &v.dclaim, static_cast<size_t>(s->n_dense));
+    rc = rc ? rc : salloc(s, &v.drow, static_cast<size_t>(s->n_dense));
     if (rc) {
       fx_step_destroy(s);
       return rc;
     }
     cudaMemcpy(kbd, kb.data(), n_tables * sizeof(int64_t), cudaMemcpyHostToDevice);
     v.kbase = kbd;
-    cudaMemset(v.dclaim, 0, static_cast<size_t>(s->n_dense) * sizeof(unsigned int));
+    cudaMemset(raw(v.drow), 0, static_cast<size_t>(s->n_dense) * sizeof(DRow));
     int rb = 1;
     while ((1ll << rb) < N) ++rb;
     if (rb > 26) {
@@ -2335,6 +2424,8 @@ int fx_step_start(fx_step *s, int32_t slot, const int32_t *bag_table, const void
   s->launches += 1;
   ks_after_probe<<<1, 1, 0, st>>>(c, v, nnz);
   s->launches += 1;
+  // (on a side stream beside the compactions the plan measured slower: the
+  // compactions and the plan both want every SM)
   ks_bag_plan<<<grid_for(n_bags > 0 ? n_bags * 32 : 32, 256), 256, 0, st>>>(v, offsets, sm_start, n_bags, threshold,
                                                                             hits_bag, pd_groups, pd_rows, raw_rows);
   s->launches += 1;
@@ -2417,19 +2508,13 @@ int fx_step_offer(fx_step *s, int32_t slot, void *stream) {
   s->launches += 1;
   ks_offer_finish<<<1, 1, 0, st>>>(c, v);
   s->launches += 1;
-  static const bool side = !(getenv("FX_COPY_SIDE") && atoi(getenv("FX_COPY_SIDE")) == 0);
-  if (side && !s->side) {
-    if (cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming) != cudaSuccess)
-      return cuda_check(cudaGetLastError(), "fx_step_offer: side stream");
-  }
-  if (side) {
-    cudaEventRecord(s->ev_fork, st);
-    cudaStreamWaitEvent(s->side, s->ev_fork, 0);
-    ks_copy_rows<<<grid_for(static_cast<int64_t>(nn) * (v.dim / 4 + 1), 256), 256, 0, s->side>>>(c, v);
-    cudaEventRecord(s->ev_join, s->side);
-    s->copy_pending = true;
+  if (side_on()) {
+    rc = side_fork(s, st);
+    if (rc) return rc;
+    ks_copy_rows<<<side_blocks() > 0 ? num_sms() * side_blocks()
+                                      : grid_for(static_cast<int64_t>(nn) * (v.dim / 4 + 1) / 4 + 1, 256),
+                   256, 0, s->side>>>(c, v);
+    side_close(s);
   } else {
     ks_copy_rows<<<grid_for(static_cast<int64_t>(nn) * (v.dim / 4 + 1), 256), 256, 0, st>>>(c, v);
   }
@@ -2482,6 +2567,12 @@ int fx_step_maintain(fx_step *s, int32_t slot, int64_t stage_limit, int32_t do_a
   join_copies(s, st);
   FX_LAUNCH_CHECK("fx_step_maintain");
   return FX_OK;
+}
+
+int fx_step_join(fx_step *s, void *stream) {
+  if (!s) return FX_OK;
+  join_copies(s, as_stream(stream));
+  return cuda_check(cudaGetLastError(), "fx_step_join");
 }
 
 int fx_step_scalars(fx_step *s, int32_t slot, int64_t *out, int64_t n, void *stream) {

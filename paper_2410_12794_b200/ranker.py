@@ -27,6 +27,8 @@ from __future__ import annotations
 import ctypes
 from dataclasses import dataclass, field
 
+import os
+
 import numpy as np
 import torch
 
@@ -398,6 +400,7 @@ class Ranker:
                 proposed = self.policy.propose(c.budget_bytes, level, self.tracker.windowed_value())
                 if proposed != c.budget_bytes:
                     # budget change: the staged API (resize -> stage -> age) with host syncs
+                    step.join()
                     self._resolve()
                     sc = step.scalars(slot)
                     if sc["err"]:
@@ -412,6 +415,7 @@ class Ranker:
                     stage_limit, age = max(0, int(self.params.admit_per_batch)), True
         if stage_limit or age:
             step.maintain(slot, stage_limit, age)
+        step.join()
         self._mark("end")
         self._flush_marks()
         cur = torch.cuda.current_stream(self.device)
@@ -467,16 +471,24 @@ class Ranker:
                 lay = CsrLayout(indices, offsets, bt, sm, None, [], None, None, None, B)
                 out = torch.empty((B, F * D), dtype=torch.float32, device=dev)
                 cnt = torch.empty((4, max(n_bags, 1)), dtype=torch.int32, device=dev)
+                # K4 beside the step on a side stream (default), or after it on
+                # the capture stream at full occupancy (FX_K4_SERIAL=1, A/B)
+                serial = os.environ.get("FX_K4_SERIAL") == "1"
                 side = self._pool_stream
-                side.wait_stream(cap)
-                with torch.cuda.stream(side):
-                    self._pool_sample_major(lay, out, ft, fo, B)
+                if not serial:
+                    side.wait_stream(cap)
+                    with torch.cuda.stream(side):
+                        self._pool_sample_major(lay, out, ft, fo, B)
                 step.start(0, bt, indices, offsets, sm, n_bags, nnz, self.params.pushdown_threshold, cnt[0], cnt[1],
                            cnt[2], cnt[3])
                 step.offer(0)
                 if do_maint:
                     step.maintain(0, stage_limit, True)
-                cap.wait_stream(side)
+                step.join()
+                if serial:
+                    self._pool_sample_major(lay, out, ft, fo, B, share=False)
+                else:
+                    cap.wait_stream(side)
                 snap = torch.cat([self._views[1][0], self._views[2]])
         torch.cuda.current_stream(dev).wait_stream(cap)
         return RankerGraph(self, g, out, cnt, snap, (indices, offsets, ft, fo, B), do_maint, step)
@@ -740,8 +752,22 @@ class Ranker:
             self.sync()
             return
         self.sync()
-        res = self._pipeline(lay, batch.size, batch.batch_id, lambda: self._raise_validation(batch))
-        self._emit(batch, lay, *res)
+        res, t = self._timed_pipeline(lay, batch.size, batch.batch_id, lambda: self._raise_validation(batch))
+        self._emit(batch, lay, *res, times=t)
+
+    def _timed_pipeline(self, lay, size, batch_id, bad):
+        """The staged pipeline between two device events on the current
+        stream: (results, (started_at, latency)) in seconds, started_at from
+        the Ranker's first batch (BatchMetrics, ranker.py:60-72)."""
+        if self._epoch_ev is None:
+            self._epoch_ev = torch.cuda.Event(enable_timing=True)
+            self._epoch_ev.record()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        res = self._pipeline(lay, size, batch_id, bad)
+        ev1.record()
+        ev1.synchronize()
+        return res, (self._epoch_ev.elapsed_time(ev0) / 1e3, ev0.elapsed_time(ev1) / 1e3)
 
     def _emit_fast(self, batch: Batch, rec) -> None:
         """LookupResults of a fused-step batch (metrics already appended)."""
@@ -772,7 +798,8 @@ class Ranker:
 
         def bad():
             raise LookupValidationError(f"batch {batch_id}: index out of range (CSR batch)")
-        out, hits_bag, pd_groups, pd_rows, raw_rows, nnz, n_groups = self._pipeline(lay, batch_size, batch_id, bad)
+        (out, hits_bag, pd_groups, pd_rows, raw_rows, nnz, n_groups), (t0, lat) = self._timed_pipeline(
+            lay, batch_size, batch_id, bad)
         F, B = len(feature_tables), batch_size
         dims = {self.deployment.meta(t).dim for t in feature_tables}
         D = out.shape[1]
@@ -780,7 +807,7 @@ class Ranker:
         c = self.cache
         hits = int(hits_bag.sum()) if c is not None else 0
         self.batch_metrics.append(BatchMetrics(
-            batch_id=batch_id, size=batch_size, started_at=0.0, latency=0.0, subrequests=n_groups,
+            batch_id=batch_id, size=batch_size, started_at=t0, latency=lat, subrequests=n_groups,
             cache_hits=hits, cache_misses=(nnz - hits) if c is not None else 0,
             pushdown_groups=int(pd_groups.sum()), pushdown_rows=int(pd_rows.sum()), raw_rows=int(raw_rows.sum()),
             load_level=self._last_level, cache_budget=(c.budget_bytes if c else None),
@@ -1127,7 +1154,8 @@ class Ranker:
             c.stage_hot_admissions(fetcher, rb, limit=self.params.admit_per_batch)
         c.sketch.age()
 
-    def _emit(self, batch, lay, out, hits_bag, pd_groups, pd_rows, raw_rows, nnz, n_groups, metrics=None):
+    def _emit(self, batch, lay, out, hits_bag, pd_groups, pd_rows, raw_rows, nnz, n_groups, metrics=None,
+              times=(0.0, 0.0)):
         n_bags = len(lay.perm)
         inv = np.empty(n_bags, dtype=np.int64)
         inv[lay.perm] = np.arange(n_bags)
@@ -1168,7 +1196,7 @@ class Ranker:
                 self.results[batch.batch_id] = results
             return
         self.batch_metrics.append(BatchMetrics(
-            batch_id=batch.batch_id, size=batch.size, started_at=0.0, latency=0.0, subrequests=sub,
+            batch_id=batch.batch_id, size=batch.size, started_at=times[0], latency=times[1], subrequests=sub,
             cache_hits=hits, cache_misses=misses, pushdown_groups=int(tot[1]), pushdown_rows=int(tot[2]),
             raw_rows=int(tot[3]), load_level=self._last_level,
             cache_budget=(c.budget_bytes if c else None), cache_used=(c.used_bytes if c else None)))

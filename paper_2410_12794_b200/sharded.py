@@ -424,6 +424,54 @@ def _ipc_open(handle: bytes) -> int:
     return int(p.value)
 
 
+class PeerComm:
+    """fx_comm (include/flexemb.h, SURVEY §8(b) fx_comm_init / fx_alltoallv):
+    a byte all-to-allv over CUDA-IPC-mapped peer memory of one node, no NCCL.
+    Collective constructor (handles are exchanged with torch.distributed)."""
+
+    def __init__(self, slot_bytes: int, group=None):
+        import torch.distributed as dist
+        from . import _lib
+        self._lib = _lib
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        self.slot_bytes = (int(slot_bytes) + 15) // 16 * 16
+        h = ctypes.c_void_p()
+        _lib.check(_lib.lib.fx_comm_init(ctypes.byref(h), self.rank, self.world, self.slot_bytes), "comm init")
+        self._h = h.value
+        buf = ctypes.create_string_buffer(64)
+        _lib.check(_lib.lib.fx_comm_handle(self._h, buf), "comm handle")
+        handles = [None] * self.world
+        dist.all_gather_object(handles, buf.raw, group=group)
+        _lib.check(_lib.lib.fx_comm_connect(self._h, b"".join(handles)), "comm connect")
+
+    def alltoallv(self, send: torch.Tensor, counts: torch.Tensor, displs: torch.Tensor, stream=None):
+        """send: uint8 CUDA tensor; counts / displs: int64 CUDA [world] (bytes
+        for each destination). Returns (recv [world, slot_bytes] uint8 copy,
+        recv_counts int64 [world]): row s holds recv_counts[s] bytes from rank s."""
+        L = self._lib
+        L.check(L.lib.fx_alltoallv(self._h, send.data_ptr(), counts.data_ptr(), displs.data_ptr(),
+                                   L.stream_ptr(stream)), "alltoallv")
+        recv = torch.empty((self.world, self.slot_bytes), dtype=torch.uint8, device=send.device)
+        rc = torch.empty(self.world, dtype=torch.int64, device=send.device)
+        L.check(L.lib.fx_memcpy_async(recv.data_ptr(), L.lib.fx_comm_recv_buffer(self._h), recv.numel(),
+                                      L.stream_ptr(stream)), "alltoallv recv")
+        L.check(L.lib.fx_memcpy_async(rc.data_ptr(), L.lib.fx_comm_recv_counts(self._h), 8 * self.world,
+                                      L.stream_ptr(stream)), "alltoallv counts")
+        return recv, rc
+
+    def status(self) -> tuple:
+        """[sync] (slot overflow, barrier timeout) flags."""
+        a, b = ctypes.c_int32(), ctypes.c_int32()
+        self._lib.check(self._lib.lib.fx_comm_status(self._h, ctypes.byref(a), ctypes.byref(b)), "comm status")
+        return a.value, b.value
+
+    def __del__(self):
+        try:
+            self._lib.lib.fx_comm_destroy(self._h)
+        except Exception:
+            pass
+
+
 class P2PShardedLookup:
     """Sharded lookup whose exchange rides on the gather+pool kernel itself.
 

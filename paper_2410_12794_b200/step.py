@@ -39,6 +39,7 @@ def _sig():
         "fx_step_start": ([P, I32, P, P, I32, P, P, I64, I64, I32, P, P, P, P, P], ctypes.c_int),
         "fx_step_offer": ([P, I32, P], ctypes.c_int),
         "fx_step_maintain": ([P, I32, I64, I32, P], ctypes.c_int),
+        "fx_step_join": ([P, P], ctypes.c_int),
         "fx_step_scalars": ([P, I32, P, I64, P], ctypes.c_int),
         "fx_step_scalars_device": ([P, I32], P),
         "fx_step_launches": ([P], I64),
@@ -123,6 +124,10 @@ class BatchStep:
         """stage_hot_admissions(stage_limit) then sketch age."""
         _lib.check(self._L.fx_step_maintain(self._h, int(slot), int(stage_limit), 1 if age else 0,
                                             _lib.stream_ptr(stream)), "step maintain")
+
+    def join(self, stream=None) -> None:
+        """Order `stream` after the step's side-stream row copies."""
+        _lib.check(self._L.fx_step_join(self._h, _lib.stream_ptr(stream)), "step join")
 
     def scalars(self, slot: int = 0, stream=None) -> dict:
         """[sync] a slot's device scalars."""

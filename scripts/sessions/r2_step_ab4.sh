@@ -1,0 +1,18 @@
+#!/bin/bash
+# plan counters beside the compactions, side kernels on 2 (4) blocks/SM, fx_step_join, K4 serial A/B
+O=gpurun_out/s9
+mkdir -p $O
+timeout 900 python -m pytest tests/test_gpu_step.py tests/test_gpu_ranker.py tests/test_gpu_cache.py tests/test_gpu_pooled.py tests/test_gpu_integration.py -q -x -p no:cacheprovider > $O/pytest_step.log 2>&1; echo "rc=$?" >> $O/pytest_step.log
+FX_LIB_PATH=$PWD/paper_2410_12794_b200/libflexemb_chk.so timeout 900 python scripts/sanitize_step.py > $O/sanitize_chk.log 2>&1; echo "rc=$?" >> $O/sanitize_chk.log
+for rep in 1 2; do
+  for mode in side side4 inline serial; do
+    for a in 1.0 1.2 0.6; do
+      c=0.02; [ $a != 1.0 ] && c=0.01
+      env_="FX_COPY_SIDE=1"; [ $mode = inline ] && env_="FX_COPY_SIDE=0"; [ $mode = serial ] && env_="FX_K4_SERIAL=1"
+      [ $mode = side4 ] && env_="FX_SIDE_BLOCKS=4"
+      env $env_ timeout 300 python bench.py --alpha $a --cache $c --steps 40 --warmup 6 --no-cpu --no-e2e > $O/b_${mode}_a${a}_r$rep.json 2>> $O/bench.err
+    done
+  done
+done
+timeout 400 python scripts/timeline.py --alpha 1.0 --cache 0.02 --steps 4 > $O/tl_1.0_0.02.json 2> $O/tl_1.0_0.02.err
+echo done

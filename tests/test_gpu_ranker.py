@@ -147,6 +147,8 @@ def test_execute_csr_and_fused_path_match_execute_batch(P):
         for m in (mb, mc):
             assert (m.cache_hits, m.cache_misses, m.raw_rows, m.subrequests) == \
                 (ma.cache_hits, ma.cache_misses, ma.raw_rows, ma.subrequests)
+        # device-event latency / start time on every path (BatchMetrics, ranker.py:60-72)
+        assert all(m.latency > 0 and m.started_at >= 0 for m in (ma, mb, mc))
         hits_sm = np.array([r.cache_hits for r in res])
         assert np.array_equal(cb["cache_hits"].view(len(rows), B).sum(0).cpu().numpy(), hits_sm)
         assert ra.cache.lru_entries() == rb.cache.lru_entries() == rc.cache.lru_entries()

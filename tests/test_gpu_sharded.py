@@ -88,3 +88,16 @@ def test_sharded_ranker_with_per_gpu_caches(args):
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "SHARDED_RANKER" in r.stdout and "lru_mismatch_batches=0" in r.stdout
+
+
+def test_peer_alltoallv_matches_nccl():
+    """fx_comm / fx_alltoallv vs NCCL all_to_all_single."""
+    n = torch.cuda.device_count() if torch.cuda.is_available() else 0
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    w = min(n, 4)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={w}",
+           "--master-addr", "127.0.0.1", "--master-port", "29573", os.path.join(ROOT, "scripts", "comm_check.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert f"COMM OK world={w}" in r.stdout
