@@ -59,7 +59,15 @@ __global__ void __launch_bounds__(256) k_alltoallv(const unsigned char *__restri
     const int64_t n16 = n >> 4;
     const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
     uint4 *d4 = reinterpret_cast<uint4 *>(dst);
-    for (int64_t i = tid; i < n16; i += T) d4[i] = __ldg(s4 + i);
+    int64_t i = tid;
+    for (; i + 3 * T < n16; i += 4 * T) {  // four 16-byte stores in flight per thread
+      const uint4 a = __ldg(s4 + i), b = __ldg(s4 + i + T), c = __ldg(s4 + i + 2 * T), e = __ldg(s4 + i + 3 * T);
+      d4[i] = a;
+      d4[i + T] = b;
+      d4[i + 2 * T] = c;
+      d4[i + 3 * T] = e;
+    }
+    for (; i < n16; i += T) d4[i] = __ldg(s4 + i);
     for (int64_t i = (n16 << 4) + tid; i < n; i += T) dst[i] = src[i];
   } else {
     for (int64_t i = tid; i < n; i += T) dst[i] = src[i];
@@ -189,7 +197,7 @@ int fx_alltoallv(fx_comm *c, const void *send, const int64_t *send_counts, const
     peers.counts[r] = count_half(c, c->pbase[r], c->epoch);
     peers.flags[r] = flag_area(c, c->pbase[r]);
   }
-  const int C = num_sms() / c->world > 1 ? num_sms() / c->world : 1;
+  const int C = 4 * num_sms() / c->world > 1 ? 4 * num_sms() / c->world : 1;
   k_alltoallv<<<dim3(C, c->world), 256, 0, st>>>(static_cast<const unsigned char *>(send), send_counts, send_displs,
                                                  peers, c->rank, c->slot_bytes, c->status);
   k_comm_barrier<<<1, 32, 0, st>>>(peers, flag_area(c, c->base), c->rank, c->world, c->epoch, c->status + 1);
