@@ -1480,6 +1480,14 @@ __global__ void ks_queue_survivors(CacheView c, StepView v) {
     v.qnew[i] = v.q[n_ev + i];
 }
 
+// the destination queue of the offers starts as all -1 (no-op for a rejected
+// batch, whose queue stays where it is)
+__global__ void ks_queue_clear(StepView v, int64_t scap) {
+  if (aborted(v)) return;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < scap; i += (int64_t)gridDim.x * blockDim.x)
+    v.qnew[i] = -1;
+}
+
 __global__ void ks_queue_commit(StepView v, int64_t scap) {
   if (aborted(v)) return;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < scap; i += (int64_t)gridDim.x * blockDim.x)
@@ -1995,6 +2003,11 @@ struct fx_step {
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool copy_pending = false;
+  // one batch in flight (slots == 1): the post-probe LRU queue stays in qnew
+  // after fx_step_start and fx_step_offer writes the final queue back into
+  // fx_cache.q (the roles of the two buffers swap), so neither phase copies
+  // the whole queue; true between such a start and its offer
+  bool queue_in_qnew = false;
 };
 
 namespace {
@@ -2346,6 +2359,10 @@ int fx_step_start(fx_step *s, int32_t slot, const int32_t *bag_table, const void
     return FX_E_CAPACITY;
   }
   join_copies(s, st);
+  if (s->queue_in_qnew) {  // the previous start's offers never ran: bring its queue back
+    cudaMemcpyAsync(s->cache->q, raw(s->v.qnew), s->scap * 4, cudaMemcpyDeviceToDevice, st);
+    s->queue_in_qnew = false;
+  }
   int rc = ensure_queue(s, st);
   if (rc) return rc;
   StepView v;
@@ -2437,7 +2454,11 @@ int fx_step_start(fx_step *s, int32_t slot, const int32_t *bag_table, const void
   s->launches += 2;
   ks_queue_append_hits<<<grid_for(nn, 256), 256, 0, st>>>(v);
   s->launches += 1;
-  cudaMemcpyAsync(cc->q, v.qnew, SC * 4, cudaMemcpyDeviceToDevice, st);
+  if (s->slots == 1) {
+    s->queue_in_qnew = true;  // the offers read it from qnew (no copy back)
+  } else {
+    cudaMemcpyAsync(cc->q, raw(v.qnew), SC * 4, cudaMemcpyDeviceToDevice, st);
+  }
   cc->hash_valid = 0;  // the fast path keeps the dense index; the hash is rebuilt on demand
   FX_LAUNCH_CHECK("fx_step_start");
   return FX_OK;
@@ -2446,11 +2467,18 @@ int fx_step_start(fx_step *s, int32_t slot, const int32_t *bag_table, const void
 int fx_step_offer(fx_step *s, int32_t slot, void *stream) {
   cudaStream_t st = as_stream(stream);
   join_copies(s, st);
+  const bool swapped = s->queue_in_qnew && s->cache->queue_valid;
+  s->queue_in_qnew = false;  // either consumed below, or invalidated meanwhile and rebuilt from the ticks
   int rc = ensure_queue(s, st);
   if (rc) return rc;
   StepView v;
   rc = select_slot(s, slot, &v);
   if (rc) return rc;
+  if (swapped) {  // current queue = qnew; the offers write the final queue into fx_cache.q
+    CkPtr<int32_t> t = v.q;
+    v.q = v.qnew;
+    v.qnew = t;
+  }
   fx_cache *cc = s->cache;
   CacheView &c = cc->v;
   const int64_t SC = s->scap;
@@ -2486,7 +2514,8 @@ int fx_step_offer(fx_step *s, int32_t slot, void *stream) {
   s->launches += 1;
   cub::DeviceScan::ExclusiveSum(s->cub_tmp, cb, raw(v.acc), raw(v.rank), nn, st);
   s->launches += 2;
-  cudaMemsetAsync(v.qnew, 0xff, SC * 4, st);
+  ks_queue_clear<<<grid_for(SC, 256), 256, 0, st>>>(v, SC);
+  s->launches += 1;
   ks_apply<<<grid_for(nn, 256), 256, 0, st>>>(c, v);
   s->launches += 1;
   ks_queue_survivors<<<grid_for(SC, 256), 256, 0, st>>>(c, v);
@@ -2506,8 +2535,10 @@ int fx_step_offer(fx_step *s, int32_t slot, void *stream) {
     ks_copy_rows<<<grid_for(static_cast<int64_t>(nn) * (v.dim / 4 + 1), 256), 256, 0, st>>>(c, v);
   }
   s->launches += 1;
-  ks_queue_commit<<<grid_for(SC, 256), 256, 0, st>>>(v, SC);
-  s->launches += 1;
+  if (!swapped) {
+    ks_queue_commit<<<grid_for(SC, 256), 256, 0, st>>>(v, SC);
+    s->launches += 1;
+  }
   FX_LAUNCH_CHECK("fx_step_offer");
   return FX_OK;
 }
