@@ -54,9 +54,15 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--batch", type=int, default=None)
     a = ap.parse_args()
-    local = int(os.environ["LOCAL_RANK"])
+    # FX_FOLD_DEVICES=1: ranks folded onto the visible GPUs (one-GPU box: every
+    # rank on cuda:0, exchange through same-device IPC mappings, gloo control)
+    fold = os.environ.get("FX_FOLD_DEVICES") == "1"
+    local = int(os.environ["LOCAL_RANK"]) % (torch.cuda.device_count() if fold else 1 << 30)
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if fold:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     rank, world = dist.get_rank(), dist.get_world_size()
     cfg = dict(CONFIGS["cfg4r" if a.which == "cfg4r" else "cfg5"])
     rows, D = cfg["table_rows"], cfg["dim"]
@@ -104,7 +110,7 @@ def main():
             if thr is not None:
                 want = plan_counters(ix, starts[f], srvs[f], thr)
                 cnt_bad += tuple(int(x) for x in cnts[it][:, b]) != want
-    t = torch.tensor([worst, float(checked - exact), float(cnt_bad)], device="cuda", dtype=torch.float64)
+    t = torch.tensor([worst, float(checked - exact), float(cnt_bad)], device="cpu" if fold else "cuda", dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     if rank == 0:
         print(json.dumps({"check": a.which, "world": world, "mode": mode, "partials": pdt, "threshold": thr,

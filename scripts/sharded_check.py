@@ -1,5 +1,10 @@
-"""torchrun --nproc-per-node N scripts/sharded_check.py [tablewise|rowwise]
-Sharded lookup on N GPUs vs the CPU oracle (flat f64 pool) for every rank's batch."""
+"""torchrun --nproc-per-node N scripts/sharded_check.py [tablewise|rowwise] [exchange]
+Sharded lookup on N GPUs vs the CPU oracle (flat f64 pool) for every rank's batch.
+
+FX_FOLD_DEVICES=1 folds the ranks onto the visible GPUs (rank r on device
+r % count; a one-GPU box runs every rank on cuda:0): the fused exchange then
+goes through same-device CUDA-IPC mappings of the other ranks' buffers, the
+control plane uses gloo, and the NCCL exchange is not available."""
 import os
 import sys
 
@@ -21,9 +26,15 @@ def main():
     hosted = exchange.endswith("-host")  # pinned host in/out through stream_host
     pipelined = exchange.endswith("-pipe") or hosted
     exchange = exchange[:-5] if pipelined else exchange
-    local = int(os.environ["LOCAL_RANK"])
+    fold = os.environ.get("FX_FOLD_DEVICES") == "1"
+    local = int(os.environ["LOCAL_RANK"]) % (torch.cuda.device_count() if fold else 1 << 30)
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if fold:
+        if exchange == "nccl":
+            raise SystemExit("the NCCL exchange needs one GPU per rank (FX_FOLD_DEVICES folds ranks onto one GPU)")
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     rank, world = dist.get_rank(), dist.get_world_size()
     rows = (50_000, 123, 20_000, 7, 9_999, 100_000, 31, 4_096, 64, 2)
     ops = ("sum", "mean") * 5
@@ -142,7 +153,7 @@ def main():
         ref = O.pool_flat(O.rows_of(0, 0, D, hb.indices[hb.offsets[0]:hb.offsets[1]]), ops[0])
         val_bad += 0.0 if O.within_tolerance(ref, out[0, :D]) else 1.0
     t = torch.tensor([worst, float(n - exact), float(cnt_bad), float(hier_exact), val_bad, empty_bad],
-                     device="cuda", dtype=torch.float64)
+                     device="cpu" if fold else "cuda", dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     if rank == 0:
         print(f"SHARDED {mode} {exchange}{('-host' if hosted else '-pipe') if pipelined else ''} world={world} worst_tolerance_ratio={t[0].item():.4f} "

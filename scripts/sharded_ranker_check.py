@@ -24,9 +24,15 @@ from paper_2410_12794_b200.workload import DlrmBatchGen  # noqa: E402
 def main():
     thr = None if (len(sys.argv) < 2 or sys.argv[1] == "none") else int(sys.argv[1])
     pooled = len(sys.argv) > 2 and sys.argv[2] == "pooled"
-    local = int(os.environ["LOCAL_RANK"])
+    # FX_FOLD_DEVICES=1: ranks folded onto the visible GPUs (one-GPU box: every
+    # rank on cuda:0, exchange through same-device IPC mappings, gloo control)
+    fold = os.environ.get("FX_FOLD_DEVICES") == "1"
+    local = int(os.environ["LOCAL_RANK"]) % (torch.cuda.device_count() if fold else 1 << 30)
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if fold:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     rank, world = dist.get_rank(), dist.get_world_size()
     rows = (3000, 120, 2500, 40, 900, 7)
     ops = ("sum", "mean", "sum", "sum", "mean", "sum")
@@ -83,7 +89,7 @@ def main():
         bad["lru"] += lru_gpu != lru_ref
     ev_ok = [k for k in rk.cache.eviction_log if k[0] != "pooled"] == [k for k in oc.evictions if k[0] != "pooled"]
     t = torch.tensor([bad["metrics"], bad["counters"], bad["lru"], bad["tol"], bad["flat"], 0 if ev_ok else 1, hits, raw],
-                     device="cuda", dtype=torch.int64)
+                     device="cpu" if fold else "cuda", dtype=torch.int64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     if rank == 0:
         print(f"SHARDED_RANKER thr={thr} pooled={pooled} world={world} metric_mismatch_batches={t[0].item()} "

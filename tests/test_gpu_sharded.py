@@ -101,3 +101,51 @@ def test_peer_alltoallv_matches_nccl():
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert f"COMM OK world={w}" in r.stdout
+
+
+@pytest.mark.parametrize("mode,exchange", [("tablewise", "p2p"), ("rowwise", "p2p"), ("rowwise", "p2pthr"),
+                                           ("tablewise", "p2p-pipe")])
+def test_sharded_two_ranks_folded_on_one_gpu(mode, exchange):
+    """The fused exchange with 2 ranks on ONE GPU (FX_FOLD_DEVICES=1): every
+    owner / requester store goes through a same-device CUDA-IPC mapping of the
+    other process's buffers, the peer barrier through IPC-mapped flags; the
+    protocol and the reference plan (threshold 2: raw fetch of the other
+    rank's rows) checked against the oracle on a single-GPU box."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29574", os.path.join(ROOT, "scripts", "sharded_check.py"),
+           mode, exchange]
+    env = dict(os.environ, FX_FOLD_DEVICES="1")
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert f"SHARDED {mode} {exchange}" in r.stdout and "world=2" in r.stdout
+
+
+@pytest.mark.parametrize("args", [["2"], ["none"]])
+def test_sharded_ranker_folded_on_one_gpu(args):
+    """ShardedRanker (per-rank GPU caches over a sharded store) with 2 ranks
+    folded onto one GPU: per-batch metrics, counters, LRU order, eviction log
+    vs the canonical-order oracle of the same topology."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29576",
+           os.path.join(ROOT, "scripts", "sharded_ranker_check.py"), *args]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=dict(os.environ, FX_FOLD_DEVICES="1"))
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "SHARDED_RANKER" in r.stdout and "lru_mismatch_batches=0" in r.stdout
+
+
+def test_sharded_bigcheck_cfg4r_folded_on_one_gpu():
+    """cfg4r-sized table-wise exchange (100 tables x 1M rows x 128, B=4096,
+    L=20) with 2 ranks folded onto one GPU: sampled bags bit-exact vs the
+    flat f64 oracle."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29577",
+           os.path.join(ROOT, "scripts", "sharded_bigcheck.py"), "cfg4r", "--bags", "500", "--steps", "2"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=dict(os.environ, FX_FOLD_DEVICES="1"))
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert '"max_non_bit_exact": 0' in r.stdout and '"counter_mismatches": 0' in r.stdout
