@@ -265,45 +265,31 @@ __device__ __forceinline__ void warp_copy_row(float *dst, const float *src, int 
 
 // bump(key, w) for a key probed once per batch (a unique key of the batch):
 // no other thread touches this key's entry in the kernel, so a found entry is
-// updated with a plain load/store. An absent key (the scan reached an empty
-// slot) is inserted into the first tombstone of its probe chain — pruned
-// entries are recycled, so the table needs rehashing far less often — or else
-// into that empty slot, claimed by CAS; a lost race rescans. A claimed slot's
-// value is 0 (empty and pruned slots hold 0.0), so the new value is 0.0 + w
-// exactly as in the reference's dict.
-__device__ __forceinline__ double sketch_add_val(const CacheView &c, uint64_t key, double w, bool *born,
-                                                 bool *reused) {
+// updated with a plain load/store; only a new key claims an empty slot by CAS
+// (slots only go empty -> key during the kernel, and an empty slot's value is
+// 0, so the new value is 0.0 + w exactly as in the reference's dict).
+__device__ __forceinline__ double sketch_add_val(const CacheView &c, uint64_t key, double w, bool *born) {
   const uint64_t m = static_cast<uint64_t>(c.kcap - 1);
-  const uint64_t h0 = hash_key(key) & m;
+  uint64_t h = hash_key(key) & m;
   while (true) {
-    int64_t tomb_at = -1;
-    uint64_t h = h0;
-    while (true) {
-      const uint64_t k = __ldcg(reinterpret_cast<const unsigned long long *>(&c.kkeys[h]));
-      if (k == key) {
-        const double nv = c.kval[h] + w;
+    uint64_t k = __ldcg(reinterpret_cast<const unsigned long long *>(&c.kkeys[h]));
+    if (k == kEmpty) {
+      k = atomicCAS(reinterpret_cast<unsigned long long *>(&c.kkeys[h]), (unsigned long long)kEmpty,
+                    (unsigned long long)key);
+      if (k == kEmpty) {
+        const double nv = 0.0 + w;
         c.kval[h] = nv;
-        *born = false;
-        *reused = false;
+        *born = true;
         return nv;
       }
-      if (k == kTomb) {
-        if (tomb_at < 0) tomb_at = static_cast<int64_t>(h);
-      } else if (k == kEmpty) {
-        const uint64_t at = tomb_at >= 0 ? static_cast<uint64_t>(tomb_at) : h;
-        const unsigned long long expect = tomb_at >= 0 ? (unsigned long long)kTomb : (unsigned long long)kEmpty;
-        if (atomicCAS(reinterpret_cast<unsigned long long *>(&c.kkeys[at]), expect, (unsigned long long)key) ==
-            expect) {
-          const double nv = 0.0 + w;
-          c.kval[at] = nv;
-          *born = true;
-          *reused = tomb_at >= 0;
-          return nv;
-        }
-        break;  // another key took the slot: rescan
-      }
-      h = (h + 1) & m;
     }
+    if (k == key) {
+      const double nv = c.kval[h] + w;
+      c.kval[h] = nv;
+      *born = false;
+      return nv;
+    }
+    h = (h + 1) & m;
   }
 }
 
@@ -736,7 +722,7 @@ __global__ void __launch_bounds__(256) ks_probe(CacheView c, StepView v, int32_t
   if (aborted(v)) return;
   const long long tick0 = c.sc->tick;
   const long long epoch = v.ss->epoch;
-  long long hits = 0, misses = 0, born = 0, nu = 0, reused = 0;
+  long long hits = 0, misses = 0, born = 0, nu = 0;
   const int64_t T = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < nnz; i0 += 2 * T) {
     int32_t u[2];
@@ -766,10 +752,9 @@ __global__ void __launch_bounds__(256) ks_probe(CacheView c, StepView v, int32_t
         v.hit_by_last[d_last(e[k])] = s;
         hits += e[k].mult;
       } else {
-        bool b = false, ru = false;
-        v.dC[u[k]] = sketch_add_val(c, key[k], static_cast<double>(e[k].mult), &b, &ru);
+        bool b = false;
+        v.dC[u[k]] = sketch_add_val(c, key[k], static_cast<double>(e[k].mult), &b);
         born += b ? 1 : 0;
-        reused += ru ? 1 : 0;
         misses += e[k].mult;
         if (!threshold_on) v.cand_by_first[d_first(e[k])] = u[k];
       }
@@ -778,7 +763,6 @@ __global__ void __launch_bounds__(256) ks_probe(CacheView c, StepView v, int32_t
   block_add(reinterpret_cast<unsigned long long *>(&c.sc->hits), hits);
   block_add(reinterpret_cast<unsigned long long *>(&c.sc->misses), misses);
   block_add(reinterpret_cast<unsigned long long *>(&c.sc->sketch_live), born);
-  block_add(reinterpret_cast<unsigned long long *>(&c.sc->sketch_tomb), -reused);
   block_add(reinterpret_cast<unsigned long long *>(&v.ss->b_hits), hits);
   block_add(reinterpret_cast<unsigned long long *>(&v.ss->b_misses), misses);
   block_add(reinterpret_cast<unsigned long long *>(&v.ss->n_uniq), nu);
