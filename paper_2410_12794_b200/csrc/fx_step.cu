@@ -718,29 +718,30 @@ __global__ void __launch_bounds__(256) ks_dedup_occ(StepView v, const int32_t *_
 // the unique count is block-aggregated here. Two positions per thread and
 // iteration, their loads issued together (the probe is a chain of dependent
 // random accesses: claim word -> entry -> dense slot index -> sketch).
+template <int KP>
 __global__ void __launch_bounds__(256) ks_probe(CacheView c, StepView v, int32_t threshold_on, int64_t nnz) {
   if (aborted(v)) return;
   const long long tick0 = c.sc->tick;
   const long long epoch = v.ss->epoch;
   long long hits = 0, misses = 0, born = 0, nu = 0;
   const int64_t T = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < nnz; i0 += 2 * T) {
-    int32_t u[2];
-    u[0] = v.claim[i0];
-    u[1] = i0 + T < nnz ? v.claim[i0 + T] : -1;
-    uint64_t key[2];
-    DEnt e[2];
+  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < nnz; i0 += KP * T) {
+    int32_t u[KP];
 #pragma unroll
-    for (int k = 0; k < 2; ++k)
+    for (int k = 0; k < KP; ++k) u[k] = i0 + k * T < nnz ? v.claim[i0 + k * T] : -1;
+    uint64_t key[KP];
+    DEnt e[KP];
+#pragma unroll
+    for (int k = 0; k < KP; ++k)
       if (u[k] >= 0) {
         key[k] = v.dkey[u[k]];
         e[k] = v.dent[u[k]];
       }
-    int32_t sl[2];  // the slot dedup recorded (kept current by apply_pending)
+    int32_t sl[KP];  // the slot dedup recorded (kept current by apply_pending)
 #pragma unroll
-    for (int k = 0; k < 2; ++k) sl[k] = u[k] >= 0 ? e[k].hit : -1;
+    for (int k = 0; k < KP; ++k) sl[k] = u[k] >= 0 ? e[k].hit : -1;
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
+    for (int k = 0; k < KP; ++k) {
       if (u[k] < 0) continue;
       ++nu;
       const int32_t s = sl[k];
@@ -2424,7 +2425,13 @@ int fx_step_start(fx_step *s, int32_t slot, const int32_t *bag_table, const void
   s->launches += 1;
   cudaMemsetAsync(v.cand_by_first, 0xff, static_cast<size_t>(nn) * 4, st);
   cudaMemsetAsync(v.hit_by_last, 0xff, static_cast<size_t>(nn) * 4, st);
-  ks_probe<<<grid_for(nn, 256), 256, 0, st>>>(c, v, threshold > 0 ? 1 : 0, nnz);
+  {  // keys in flight per thread (FX_PROBE_ILP: 2 default, 4 measured 2.5 % slower)
+    static const int ilp = (getenv("FX_PROBE_ILP") && atoi(getenv("FX_PROBE_ILP")) == 4) ? 4 : 2;
+    if (ilp == 4)
+      ks_probe<4><<<grid_for(nn, 256), 256, 0, st>>>(c, v, threshold > 0 ? 1 : 0, nnz);
+    else
+      ks_probe<2><<<grid_for(nn, 256), 256, 0, st>>>(c, v, threshold > 0 ? 1 : 0, nnz);
+  }
   s->launches += 1;
   ks_after_probe<<<1, 1, 0, st>>>(c, v, nnz);
   s->launches += 1;
