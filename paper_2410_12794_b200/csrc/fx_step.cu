@@ -146,7 +146,8 @@ struct StepView {
   CkPtr<uint32_t> hitbits; // [scap / 32] slots hit by this batch's probes (cleared per batch;
                            // 0.8 MB for 6.4 M slots: stays in L2 for the queue compaction)
   CkPtr<double> E;         // [scap] victim estimates
-  CkPtr<int32_t> hardf;    // [scap] hard-victim flags
+  CkPtr<int32_t> hardf;    // [scap] scratch (queue rebuild sort values)
+  CkPtr<uint32_t> hardbits;  // [scap / 32] hard-victim flags, one bit per victim position
   CkPtr<int32_t> hard;     // [scap] compacted hard positions
   CkPtr<int32_t> rj_beg; CkPtr<int32_t> rj_end;  // reject intervals
   CkPtr<uint8_t> code;     // [max_nnz] per candidate: number of distinct hard levels <= its estimate
@@ -875,8 +876,17 @@ __global__ void ks_offer_prep(CacheView c, StepView v, int64_t max_nnz, int32_t 
         if (!f) v.ss->dyn = 1;
       }
     }
-    v.pres[j] = f;
+    if (!fresh) v.pres[j] = f;
   }
+}
+
+// `fresh` offers (one batch in flight): every candidate is still absent, so
+// the offer list is the candidate list itself (no flag compaction)
+__global__ void ks_cidx_identity(StepView v) {
+  const long long n = aborted(v) ? 0 : v.ss->n_cand;
+  if (blockIdx.x == 0 && threadIdx.x == 0) v.ss->n_off = n;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+    v.cidx[j] = static_cast<int32_t>(j);
 }
 
 // a candidate cached at offer time can be evicted by an earlier offer of the
@@ -955,16 +965,29 @@ __global__ void ks_victim_est(CacheView c, StepView v, int64_t scap) {
   const bool on = s->mode == MODE_PAR && c.admission == 0;
   const long long need = on ? s->n_off - s->F : 0;
   const double minc = __longlong_as_double(s->minc_bits);
-  for (int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; h < scap; h += (int64_t)gridDim.x * blockDim.x) {
-    int32_t f = 0;
+  // a warp covers 32 consecutive positions (the grid is a multiple of 32
+  // threads): one ballot word per warp and iteration
+  const int lane = threadIdx.x & 31;
+  for (int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; h - lane < scap;
+       h += (int64_t)gridDim.x * blockDim.x) {
+    bool f = false;
     if (h < need) {
       const double e = k_est(c, c.skey[v.q[h]]);
       v.E[h] = e;
-      f = e > minc ? 1 : 0;
+      f = e > minc;
     }
-    v.hardf[h] = f;
+    const unsigned b = __ballot_sync(0xffffffffu, f);
+    if (lane == 0) v.hardbits[(h - lane) >> 5] = b;
   }
 }
+
+// selection predicate over victim positions: the hard-victim bit
+struct HardBit {
+  const uint32_t *bits;
+  __device__ __forceinline__ bool operator()(const int32_t &h) const {
+    return ((__ldg(&bits[h >> 5]) >> (h & 31)) & 1u) != 0;
+  }
+};
 
 // first j in [x, n) with cC[j] >= e (n if none); whole warp, uniform result
 __device__ __forceinline__ long long next_ge(const StepView &v, const double *sbm, long long nblk, long long n,
@@ -2218,6 +2241,7 @@ int fx_step_create(fx_step **out, fx_cache *cache, int64_t max_nnz, int64_t max_
   rc = rc ? rc : salloc(s, &v.hitbits, (SC + 31) / 32);
   rc = rc ? rc : salloc(s, &v.E, SC);
   rc = rc ? rc : salloc(s, &v.hardf, SC);
+  rc = rc ? rc : salloc(s, &v.hardbits, (SC + 31) / 32);
   rc = rc ? rc : salloc(s, &v.hard, SC);
   rc = rc ? rc : salloc(s, &v.rj_beg, SC + 1);
   rc = rc ? rc : salloc(s, &v.rj_end, SC + 1);
@@ -2291,9 +2315,13 @@ int fx_step_create(fx_step **out, fx_cache *cache, int64_t max_nnz, int64_t max_
   QueueKeep qk{nullptr};
   cub::DeviceSelect::If(nullptr, b4, (const int32_t *)nullptr, (int32_t *)nullptr, (int64_t *)nullptr,
                         static_cast<int>(SC), qk);
+  size_t b5 = 0;
+  cub::DeviceSelect::If(nullptr, b5, cub::CountingInputIterator<int32_t>(0), (int32_t *)nullptr, (int64_t *)nullptr,
+                        static_cast<int>(SC), HardBit{nullptr});
   s->cub_bytes = b1 > b2 ? b1 : b2;
   if (b3 > s->cub_bytes) s->cub_bytes = b3;
   if (b4 > s->cub_bytes) s->cub_bytes = b4;
+  if (b5 > s->cub_bytes) s->cub_bytes = b5;
   rc = cuda_check(cudaMalloc(&s->cub_tmp, s->cub_bytes + 256), "fx_step: cub tmp");
   if (rc) {
     fx_step_destroy(s);
@@ -2359,8 +2387,8 @@ int fx_step_start(fx_step *s, int32_t slot, const int32_t *bag_table, const void
     return FX_E_CAPACITY;
   }
   join_copies(s, st);
-  if (s->queue_in_qnew) {  // the previous start's offers never ran: bring its queue back
-    cudaMemcpyAsync(s->cache->q, raw(s->v.qnew), s->scap * 4, cudaMemcpyDeviceToDevice, st);
+  if (s->queue_in_qnew) {  // the previous start's offers never ran: rebuild the queue from the ticks
+    s->cache->queue_valid = 0;
     s->queue_in_qnew = false;
   }
   int rc = ensure_queue(s, st);
@@ -2454,7 +2482,9 @@ int fx_step_start(fx_step *s, int32_t slot, const int32_t *bag_table, const void
                         NonNeg(), st);
   s->launches += 2;
   // LRU order after the probes: [entries not hit, old order] ++ [hit entries by last ordinal]
-  cudaMemsetAsync(v.qnew, 0xff, SC * 4, st);
+  // with one batch in flight only qnew[0, entries) is read before the offers
+  // rewrite fx_cache.q; otherwise qnew is copied back whole (-1 beyond)
+  if (s->slots > 1) cudaMemsetAsync(v.qnew, 0xff, SC * 4, st);
   QueueKeep qk{raw(v.hitbits)};
   cub::DeviceSelect::If(s->cub_tmp, cb, cc->q, raw(v.qnew), reinterpret_cast<int64_t *>(&v.ss->n_nonhit),
                         static_cast<int>(SC), qk, st);
@@ -2493,19 +2523,24 @@ int fx_step_offer(fx_step *s, int32_t slot, void *stream) {
   size_t cb = s->cub_bytes;
   ks_offer_prep<<<grid_for(nn, 256), 256, 0, st>>>(c, v, nn, s->slots == 1 ? 1 : 0);
   s->launches += 1;
-  ks_offer_flags<<<grid_for(nn, 256), 256, 0, st>>>(v, nn);
-  s->launches += 1;
-  cub::DeviceSelect::Flagged(s->cub_tmp, cb, cub::CountingInputIterator<int32_t>(0), raw(v.pres), raw(v.cidx),
-                             reinterpret_cast<int64_t *>(&v.ss->n_off), nn, st);
-  s->launches += 2;
+  if (s->slots == 1) {
+    ks_cidx_identity<<<grid_for(nn, 256), 256, 0, st>>>(v);
+    s->launches += 1;
+  } else {
+    ks_offer_flags<<<grid_for(nn, 256), 256, 0, st>>>(v, nn);
+    s->launches += 1;
+    cub::DeviceSelect::Flagged(s->cub_tmp, cb, cub::CountingInputIterator<int32_t>(0), raw(v.pres), raw(v.cidx),
+                               reinterpret_cast<int64_t *>(&v.ss->n_off), nn, st);
+    s->launches += 2;
+  }
   ks_cand_est<<<grid_for(nn, kFine), kFine, 0, st>>>(v);
   s->launches += 1;
   ks_offer_plan<<<1, 1, 0, st>>>(c, v);
   s->launches += 1;
   ks_victim_est<<<grid_for(SC, 256), 256, 0, st>>>(c, v, SC);
   s->launches += 1;
-  cub::DeviceSelect::Flagged(s->cub_tmp, cb, cub::CountingInputIterator<int32_t>(0), raw(v.hardf), raw(v.hard),
-                             reinterpret_cast<int64_t *>(&v.ss->n_hard), static_cast<int>(SC), st);
+  cub::DeviceSelect::If(s->cub_tmp, cb, cub::CountingInputIterator<int32_t>(0), raw(v.hard),
+                        reinterpret_cast<int64_t *>(&v.ss->n_hard), static_cast<int>(SC), HardBit{raw(v.hardbits)}, st);
   s->launches += 2;
   ks_levels<<<1, 1024, 0, st>>>(v, s->stream_smem > 0 ? 1 : 0);
   s->launches += 1;
