@@ -1,7 +1,7 @@
 #!/bin/bash
 # multi-GPU evidence for this round's code: sharded parity tests (2 or 4 GPUs),
 # the N-GPU bench (cfg4r table-wise default, cfg5 row-wise), reference arm at N
-O=gpurun_out/m$1
+O=gpurun_out/m$1${2:-}
 mkdir -p $O
 N=$(python -c "import torch; print(torch.cuda.device_count())")
 nvidia-smi topo -m > $O/topo.txt 2>&1
