@@ -262,8 +262,10 @@ def main():
     ap.add_argument("--sync", action="store_true",
                     help="N>1 fused exchange: synchronous steps (2 barriers each) instead of the pipelined stream "
                          "(push of step k+1 overlapping the gather of step k, one barrier per step)")
-    ap.add_argument("--partial", default="f64", choices=["f64", "f32"],
-                    help="N>1 row-wise partial format (f32 = the reference's PartialResult semantics)")
+    ap.add_argument("--partial", default="f32", choices=["f64", "f32"],
+                    help="N>1 row-wise partial format: f32 (default) = the reference's PartialResult / "
+                         "combine_partials semantics, bit-identical to its hierarchical result and half the "
+                         "NVLink bytes; f64 = bit-identical to the flat f64 pool instead")
     ap.add_argument("--graph", type=int, default=0,
                     help="N=1: capture this many batch launches per CUDA graph and time graph replays")
     ap.add_argument("--replicate-rows", type=int, default=None,
@@ -705,6 +707,8 @@ def run_sharded(args, rank, world, local):
     torch.cuda.synchronize()
     dist.barrier()
     clocks = sampler.stop()
+    clocks_ranks = [None] * world  # every rank's own GPU clocks during the timed region
+    dist.all_gather_object(clocks_ranks, clocks)
     ms = ev0.elapsed_time(ev1)
     l1 = getattr(sl, "launches", None)
     # a peer that stopped participating makes the spin barrier give up after
@@ -841,7 +845,7 @@ def run_sharded(args, rank, world, local):
                     "note": ("NCCL all_to_all_single; includes the self-slice" if args.exchange == "nccl" else
                              "fused: pooled rows stored to peers inside K4; ms = the fused kernel's time")},
             "gpu_launches": (l1 - l0) if l0 is not None else None,
-            "e2e": e2e, "cpu_baseline": None, "clocks": clocks,
+            "e2e": e2e, "cpu_baseline": None, "clocks": clocks, "clocks_ranks": clocks_ranks,
         }
         emit(line, args)
     dist.barrier()
