@@ -653,7 +653,12 @@ class P2PShardedLookup:
             # owner segments over every requester's bags (virtual bag space), set p
             segs = []
             vb = 0
-            for q in range(W):
+            # requesters in the order rank+1, rank+2, ..., rank: the persistent
+            # K4 warps walk the virtual bags in order, so at any moment each
+            # owner stores into a different requester (a shifted all-to-all:
+            # no GPU's NVLink ingress takes every owner's stores at once)
+            for qi in range(W):
+                q = (rank + 1 + qi) % W
                 qout = ptrs[q][2] + p * out_set
                 lidx = self.b_idx.ptr + p * self.idx_set + q * self.max_nnz * 4
                 loffs = self.b_offs.ptr + p * self.offs_set[rank] + q * offs_slot(rank)
