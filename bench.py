@@ -175,6 +175,39 @@ def ranker_config(cfg, cache_frac, extra=None):
     return d
 
 
+def sharded_config(cfg, args, world):
+    """The `config` dict both arms print for the N>1 sharded workload (derived
+    from the configuration and the flags only, so the reference arm prints the
+    identical dict)."""
+    rows, B, F, mode = cfg["table_rows"], cfg["batch"], len(cfg["table_rows"]), args.mode
+    repl = ([t for t, n in enumerate(rows) if n <= args.replicate_rows]
+            if mode == "tablewise" and args.exchange == "p2p" else [])
+    if len(repl) == F:
+        repl = repl[:-1]
+    return {"workload": cfg["name"] + f"-{mode}", "global_batch": B * world, "per_gpu_batch": B,
+            "pooling": list(cfg["pooling"]) if isinstance(cfg["pooling"], tuple) else cfg["pooling"],
+            "alpha": cfg["alpha"], "dim": cfg["dim"], "tables": F, "rows_per_table": rows[0],
+            "cache_rows_frac": 0.0,
+            "parallelism": f"{mode}-sharded x{world} ({args.exchange} exchange)"
+                           + (f", {len(repl)} small tables replicated" if repl else "")
+                           + (f", {args.partial} partials" if mode == "rowwise" else "")
+                           + (f", pushdown threshold {args.threshold} (raw fetch over NVLink below)"
+                              if mode == "rowwise" and args.threshold else "")
+                           + (", pipelined (depth 2)" if args.exchange == "p2p" and not args.sync else ""),
+            "l2": f"inputs larger than L2: a distinct batch per rank and step over "
+                  f"{sum(rows) * cfg['dim'] * 4 / 1e9:.1f} GB of tables"}
+
+
+def cfg3_config(cfg, args):
+    """The `config` dict both arms print for the N=1 cfg3 Ranker workload."""
+    N, T, D = cfg["table_rows"][0], len(cfg["table_rows"]), cfg["dim"]
+    budget = int(T * N * args.cache) * D * 4
+    return ranker_config(cfg, args.cache, {
+        "parallelism": "single" + (", whole Ranker batch replayed as one CUDA graph" if args.graph_step else ""),
+        "l2": f"inputs larger than L2: distinct batches (up to 40, cycled) over {N * T * D * 4 / 1e9:.1f} GB of "
+              f"tables + {budget / 1e9:.2f} GB of cached rows"})
+
+
 REF_ROWS = 20_000  # row-reduced replica for the reference's host tables
 
 
@@ -213,7 +246,9 @@ def run_reference(args, rank, world):
     cfg_key = args.config or "cfg3"
     cfg, _ = build_cfg(cfg_key, 0, 0, args.alpha)
     procs = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
-    r = ref_baseline(cfg, args.cache, procs, samples_per_step=32, steps=args.steps, warmup=args.warmup)
+    # N>1: the GPU arm's sharded lookup has no cache, so neither has the reference's Ranker here
+    cache_frac = 0.0 if world > 1 else args.cache
+    r = ref_baseline(cfg, cache_frac, procs, samples_per_step=32, steps=args.steps, warmup=args.warmup)
     assert not any(k.startswith("paper_2410_12794_b200") for k in sys.modules), "reference arm loaded the product"
     if r is None:
         emit({"impl": "reference", "unavailable": "oracle/_ref/embserve missing (run __graft_entry__.build())"}, args)
@@ -223,7 +258,9 @@ def run_reference(args, rank, world):
         "impl": "reference", "metric": "pooled lookups/s (bags/s)", "value": value, "unit": "pooled lookups/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32 rows, f64 accumulate",
-        "data": "synthetic", "config": ranker_config(cfg, args.cache),
+        "data": "synthetic",
+        "config": sharded_config(cfg, args, world) if world > 1 else (cfg3_config(cfg, args) if cfg_key == "cfg3"
+                                                                     else ranker_config(cfg, args.cache)),
         "cpu_baseline": {"value": value, "unit": "pooled lookups/s", "cores": cores, "kind": "reference",
                          "sample": sample},
         "e2e": {"value": value, "unit": "pooled lookups/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -605,11 +642,7 @@ def run_ranker(args, rank, world, local):
         "metric": "pooled lookups/s (bags/s)", "value": value, "unit": "pooled lookups/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32 rows, f64 accumulate", "data": "synthetic",
-        "config": ranker_config(cfg, args.cache, {
-            "parallelism": "single" + (", whole Ranker batch replayed as one CUDA graph" if graph is not None
-                                       else ""), "l2": f"inputs larger than L2: {n_timed} distinct batches "
-            f"({tot_bytes / args.steps / 1e9:.2f} GB algorithmic bytes each) over {N * T * D * 4 / 1e9:.1f} GB of "
-            f"tables + {budget / 1e9:.2f} GB of cached rows", "init_store_s": round(init_s, 2)}),
+        "config": cfg3_config(cfg, args), "init_store_s": round(init_s, 2),
         "hit_rate": hit, "latency_ms": {"p50": lat[len(lat) // 2], "max": lat[-1]},
         "host_enqueue_ms_per_step": host_ms,
         "roofline": {"bound": "hbm", "achieved": k4_achieved, "peak": peak, "unit": "GB/s",
@@ -822,17 +855,7 @@ def run_sharded(args, rank, world, local):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32 rows, f64 accumulate", "data": "synthetic",
-            "config": {"workload": cfg["name"] + f"-{mode}", "global_batch": B * world, "per_gpu_batch": B,
-                       "pooling": list(cfg["pooling"]) if isinstance(cfg["pooling"], tuple) else cfg["pooling"],
-                       "alpha": cfg["alpha"], "dim": dim, "tables": F,
-                       "parallelism": f"{mode}-sharded x{world} ({args.exchange} exchange)"
-                                      + (f", {len(repl)} small tables replicated" if repl else "")
-                                      + (f", {args.partial} partials" if mode == "rowwise" else "")
-                                      + (f", pushdown threshold {args.threshold} (raw fetch over NVLink below)"
-                                         if mode == "rowwise" and args.threshold else "")
-                                      + (", pipelined (depth 2)" if args.exchange == "p2p" and not args.sync else ""),
-                       "l2": "inputs larger than L2 (1.18 GB algorithmic bytes per rank-batch)",
-                       "init_store_s": round(init_s, 2)},
+            "config": sharded_config(cfg, args, world), "init_store_s": round(init_s, 2),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": None,
                          "peak_source": peak_src, "kernel": "owner gather+pool (K4) launches, rank 0",
